@@ -1,0 +1,41 @@
+# Builds every native artefact in-tree (the .so files travel to the GPU box with
+# the gpurun snapshot; they are git-ignored).
+#   gen/libqrgen_host.so   host generators (gcc, OpenMP)          — harness, shared by both sides
+#   gen/libqrgen_dev.so    device generators (nvcc, sm_100a)      — harness
+#   oracle/liboracle.so    CPU oracle (plain C, gcc)              — test infrastructure only
+#   paper_2602_04103_b200/lib/libqrank.so   the product C-ABI library (nvcc, sm_100a)
+NVCC    ?= /usr/local/cuda/bin/nvcc
+HOSTCC  := gcc
+ARCH    := -gencode arch=compute_100a,code=sm_100a
+NVFLAGS := -O3 -lineinfo $(ARCH) -std=c++17 -Xcompiler -fPIC -Xcompiler -fvisibility=hidden \
+           -Xptxas -v --expt-relaxed-constexpr -Iinclude
+CFLAGS  := -O2 -fPIC -fopenmp -std=c11 -Wall -Wno-unused-function
+
+PKG     := paper_2602_04103_b200
+QR_SRC  := $(wildcard $(PKG)/csrc/*.cu)
+QR_HDR  := $(wildcard $(PKG)/csrc/*.cuh) include/qrank.h
+QR_OBJ  := $(patsubst $(PKG)/csrc/%.cu,build/qr_%.o,$(QR_SRC))
+
+all: gen/libqrgen_host.so gen/libqrgen_dev.so oracle/liboracle.so $(if $(QR_SRC),$(PKG)/lib/libqrank.so)
+
+gen/libqrgen_host.so: gen/qrgen_host.c gen/qrgen.h
+	$(HOSTCC) $(CFLAGS) -shared -o $@ gen/qrgen_host.c
+
+gen/libqrgen_dev.so: gen/qrgen_dev.cu gen/qrgen.h
+	$(NVCC) -O3 $(ARCH) -std=c++17 -Xcompiler -fPIC -shared -o $@ gen/qrgen_dev.cu
+
+oracle/liboracle.so: oracle/oracle.c
+	$(HOSTCC) $(CFLAGS) -shared -o $@ oracle/oracle.c
+
+build/qr_%.o: $(PKG)/csrc/%.cu $(QR_HDR)
+	@mkdir -p build
+	$(NVCC) $(NVFLAGS) -c -o $@ $< 2> build/qr_$*.ptxas.txt || (cat build/qr_$*.ptxas.txt; false)
+
+$(PKG)/lib/libqrank.so: $(QR_OBJ)
+	@mkdir -p $(PKG)/lib
+	$(NVCC) $(ARCH) -shared -o $@ $(QR_OBJ)
+
+clean:
+	rm -rf build gen/*.so oracle/*.so $(PKG)/lib/*.so
+
+.PHONY: all clean
