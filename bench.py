@@ -1,0 +1,442 @@
+#!/usr/bin/env python
+"""Benchmark of the hot path on B200 (BASELINE.json metric).
+
+python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--rows all|headline]
+
+Headline (`value`): BiRank16 rank queries/s on configs[1] (n = 2^34 bits, p = 0.5, 10^9 queries
+per GPU, u64 out), whole job over N GPUs (weak scaling: each GPU keeps its 10^9 queries),
+CUDA-event time on the launching stream, max over ranks.  `rows` adds every other §8(a) row
+measured in the same run (gather ceiling, p = 0.01, QuadRank rank / rank_all4 on configs[2],
+QuadFm count on configs[3] and configs[4], the small configs[0]).  Inputs are created on the
+device from the seeded generators before the timed region; every timed input (the line array
+2.2 GB, the query array 8 GB) is far larger than the 126 MB L2, so no flush is needed.
+
+--impl reference: the CPU oracle (oracle/, plain C, OpenMP over queries) timed on the host
+cores on a bounded sample of the same workload each step; rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "rank Gqueries/s & HBM gather GB/s vs roofline; QuadFm patterns/s @1/2/4/8"
+N2, M2 = 1 << 34, 10**9                 # configs[1]
+N3, M3 = 1 << 32, 10**9                 # configs[2]
+N4, M4, L4 = 1 << 26, 10**7, 32         # configs[3]
+N5, M5, L5 = 1 << 30, 10**8, 100        # configs[4] (patterns; rank queries: 10^9 per GPU shard)
+N1, M1 = 1 << 20, 10**6                 # configs[0]
+SEED = {1: 1, 2: 2, 3: 3, 4: 4, 5: 5}
+# expected bytes of one BiRank query: sector 0 always, sector 1 when the
+# query lies right of the anchor (data bits [240,496): 256/496 of uniform q) + 8 B q + 8 B out
+BI_LINE_BYTES = 32 + 32 * 256 / 496
+QD_LINE_BYTES = 32 + 32 * 128 / 224     # data chars [96,224) of 224 need sector 1
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class Clocks:
+    """nvidia-smi clocks / throttle reasons sampled DURING the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                                          "-lms", "100", "-i", str(self.idx)], stdout=open(self.path, "w"),
+                                         stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        self.proc.wait()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            p = [x.strip() for x in line.split(",")]
+            if len(p) < 9:
+                continue
+            try:
+                sm.append(float(p[1]))
+                mx = float(p[2])
+            except ValueError:
+                continue
+            for k, name in enumerate(names):
+                if p[5 + k].lower().startswith("active"):
+                    reasons.add(name)
+        os.unlink(self.path)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+class Ctx:
+    def __init__(self, args):
+        import torch
+
+        self.torch = torch
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        self.args = args
+        self.dist = None
+        if self.world > 1:
+            import torch.distributed as dist
+
+            torch.cuda.set_device(self.local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
+            self.dist = dist
+        else:
+            torch.cuda.set_device(0)
+        self.dev = torch.device("cuda", self.local)
+        self.stream = torch.cuda.current_stream()
+
+    def barrier(self):
+        if self.dist:
+            self.dist.barrier()
+
+    def max_over_ranks(self, x: float) -> float:
+        if not self.dist:
+            return x
+        t = self.torch.tensor([x], dtype=self.torch.float64, device=self.dev)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum_over_ranks(self, x: int) -> int:
+        if not self.dist:
+            return x
+        t = self.torch.tensor([x], dtype=self.torch.int64, device=self.dev)
+        self.dist.all_reduce(t)
+        return int(t.item())
+
+    def timed(self, fn, steps: int, warmup: int, clocks: Clocks | None = None) -> float:
+        """ms per step: W warm-up calls, then EXACTLY K calls bracketed by barrier + synchronize,
+        CUDA events on the launching stream, max over ranks."""
+        torch = self.torch
+        for _ in range(warmup):
+            fn()
+        torch.cuda.synchronize()
+        self.barrier()
+        torch.cuda.synchronize()
+        if clocks:
+            clocks.start()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(self.stream)
+        for _ in range(steps):
+            fn()
+        e1.record(self.stream)
+        torch.cuda.synchronize()
+        self.barrier()
+        ms = e0.elapsed_time(e1) / steps
+        return self.max_over_ranks(ms)
+
+
+def shard(total: int, world: int, rank: int):
+    lo = total * rank // world
+    hi = total * (rank + 1) // world
+    return lo, hi - lo
+
+
+# ------------------------------------------------------------------ rows
+def bench_birank(ctx, p: float, steps, warmup, with_ceiling: bool, clocks=None, e2e=False):
+    import gen
+    import paper_2602_04103_b200 as qr
+
+    torch = ctx.torch
+    bits = torch.empty((N2 + 63) // 64, dtype=torch.uint64, device=ctx.dev)
+    gen.bits_dev(SEED[2] if p == 0.5 else 22, N2, p, bits)
+    h = qr.qr_birank_build(bits, N2, device=ctx.local)
+    del bits
+    m = M2                                         # per GPU (weak scaling)
+    i0 = ctx.rank * m
+    q = torch.empty(m, dtype=torch.uint64, device=ctx.dev)
+    gen.queries_dev(SEED[2], N2, m, q, i0=i0)
+    out = torch.empty_like(q)
+    torch.cuda.synchronize()
+    ms = ctx.timed(lambda: qr.qr_rank(h, q, None, out, m, ctx.stream), steps, warmup, clocks)
+    clk = clocks.stop() if clocks else None
+    res = {"ms": ms, "m_per_gpu": m, "gq_s": ctx.world * m / ms / 1e6, "launches": steps, "clocks": clk}
+    if with_ceiling:
+        for mode in (0, 1):
+            cms = ctx.timed(lambda: qr.qr_gather_ceiling(h, q, out, mode, m, ctx.stream), steps, warmup)
+            res[f"ceiling_mode{mode}"] = {"ms": cms, "gq_s": ctx.world * m / cms / 1e6}
+    if e2e:
+        me = 2 * 10**8
+        qh = torch.empty(me, dtype=torch.uint64).pin_memory()
+        gen_q = q[:me].cpu()
+        qh.copy_(gen_q)
+        oh = torch.empty(me, dtype=torch.uint64).pin_memory()
+
+        def call():
+            qr.qr_rank(h, qh, None, oh, me, ctx.stream)
+            ctx.stream.synchronize()
+            _ = int(oh[-1])                        # the D2H result is read by the host
+        for _ in range(2):
+            call()
+        torch.cuda.synchronize()
+        ctx.barrier()
+        t0 = time.perf_counter()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(ctx.stream)
+        k = max(2, steps // 2)
+        for _ in range(k):
+            call()
+        e1.record(ctx.stream)
+        torch.cuda.synchronize()
+        wall = (time.perf_counter() - t0) * 1e3 / k
+        ems = ctx.max_over_ranks(max(e0.elapsed_time(e1) / k, wall))
+        res["e2e"] = {"value": round(ctx.world * me / ems / 1e6, 4), "unit": "Gqueries/s",
+                      "h2d_bytes_per_step": 8 * me, "d2h_bytes_per_step": 8 * me, "queries_per_step": me,
+                      "ms_per_step": round(ems, 3)}
+        del qh, oh
+    del q, out
+    h.free()
+    torch.cuda.empty_cache()
+    return res
+
+
+def bench_quadrank(ctx, steps, warmup):
+    import gen
+    import paper_2602_04103_b200 as qr
+
+    torch = ctx.torch
+    text = torch.empty((N3 + 31) // 32, dtype=torch.uint64, device=ctx.dev)
+    gen.dna_dev(SEED[3], N3, 0, text)
+    h = qr.qr_quadrank_build(text, N3, device=ctx.local)
+    del text
+    m = M3
+    q = torch.empty(m, dtype=torch.uint64, device=ctx.dev)
+    c = torch.empty(m, dtype=torch.uint8, device=ctx.dev)
+    gen.queries_dev(SEED[3], N3, m, q, c, i0=ctx.rank * m)
+    out = torch.empty_like(q)
+    ms = ctx.timed(lambda: qr.qr_rank(h, q, c, out, m, ctx.stream), steps, warmup)
+    cms = ctx.timed(lambda: qr.qr_gather_ceiling(h, q, out, 0, m, ctx.stream), steps, warmup)
+    del out
+    out4 = torch.empty((m, 4), dtype=torch.uint64, device=ctx.dev)
+    ms4 = ctx.timed(lambda: qr.qr_rank_all4(h, q, out4, m, ctx.stream), steps, warmup)
+    del q, c, out4
+    h.free()
+    torch.cuda.empty_cache()
+    return {"rank": {"ms": ms, "gq_s": ctx.world * m / ms / 1e6},
+            "ceiling_mode0": {"ms": cms, "gq_s": ctx.world * m / cms / 1e6},
+            "rank_all4": {"ms": ms4, "gq_s": ctx.world * m / ms4 / 1e6}}
+
+
+def bench_fm(ctx, n, kind, m_total, length, seed, steps, warmup, rank_queries=0):
+    import gen
+    import paper_2602_04103_b200 as qr
+
+    torch = ctx.torch
+    text = torch.empty((n + 31) // 32 + 1, dtype=torch.uint64, device=ctx.dev)
+    gen.dna_dev(seed, n, kind, text)
+    t0 = time.perf_counter()
+    fm = qr.qr_fm_build(text, n, device=ctx.local)
+    build_s = time.perf_counter() - t0
+    i0, m = shard(m_total, ctx.world, ctx.rank)
+    pats = torch.empty(m * length, dtype=torch.uint8, device=ctx.dev)
+    gen.patterns_dev(seed, 0 if kind == 0 else 1, m, length, text, n, pats, i0=i0)
+    out = torch.empty(m, dtype=torch.int32, device=ctx.dev)
+    work = torch.zeros(2, dtype=torch.uint64, device=ctx.dev)
+    qr.qr_fm_count_work(fm, pats, None, length, out, m, work, ctx.stream)
+    torch.cuda.synchronize()
+    steps_done, lines = (int(x) for x in work.cpu())
+    ms = ctx.timed(lambda: qr.qr_fm_count(fm, pats, None, length, out, m, ctx.stream), steps, warmup)
+    lines_all = ctx.sum_over_ranks(lines)
+    res = {"ms": ms, "patterns_per_s": m_total / ms * 1e3, "build_s": round(build_s, 3),
+           "steps_per_pattern": steps_done / max(m, 1), "lines_per_pattern": lines / max(m, 1),
+           "lines_per_s": lines_all / ms * 1e3,
+           "alg_gbs": (lines_all * 64 + m_total * (length + 4)) / ms / 1e6}
+    del pats, out
+    if rank_queries:
+        q = torch.empty(rank_queries, dtype=torch.uint64, device=ctx.dev)
+        c = torch.empty(rank_queries, dtype=torch.uint8, device=ctx.dev)
+        gen.queries_dev(seed, n + 1, rank_queries, q, c, i0=ctx.rank * rank_queries)
+        o = torch.empty_like(q)
+        rms = ctx.timed(lambda: qr.qr_rank(fm.bwt, q, c, o, rank_queries, ctx.stream), steps, warmup)
+        res["rank"] = {"ms": rms, "gq_s": ctx.world * rank_queries / rms / 1e6, "m_per_gpu": rank_queries}
+        del q, c, o
+    fm.free()
+    del text
+    torch.cuda.empty_cache()
+    return res
+
+
+def bench_small(ctx, steps, warmup):
+    import gen
+    import paper_2602_04103_b200 as qr
+
+    torch = ctx.torch
+    bits = torch.empty((N1 + 63) // 64, dtype=torch.uint64, device=ctx.dev)
+    gen.bits_dev(SEED[1], N1, 0.5, bits)
+    h = qr.qr_birank_build(bits, N1, device=ctx.local)
+    q = torch.empty(M1, dtype=torch.uint64, device=ctx.dev)
+    gen.queries_dev(SEED[1], N1, M1, q, i0=ctx.rank * M1)
+    out = torch.empty_like(q)
+    ms = ctx.timed(lambda: qr.qr_rank(h, q, None, out, M1, ctx.stream), steps * 10, warmup)
+    h.free()
+    return {"ms": ms, "gq_s": ctx.world * M1 / ms / 1e6}
+
+
+# ------------------------------------------------------------------ CPU oracle
+def cpu_oracle_rank(target_s: float = 10.0, per_step_q: int | None = None):
+    """The oracle (as it stands) on the host cores: BiRank config 2 text regenerated on the
+    host, plain prefix array, rank on a bounded sample of the same query stream."""
+    import numpy as np
+
+    import gen
+    import oracle
+
+    t0 = time.perf_counter()
+    words = gen.bits(SEED[2], N2, 0.5)
+    ora = oracle.BitsOracle(words, N2)
+    prep = time.perf_counter() - t0
+    m = 1 << 21
+    q = gen.queries(SEED[2], N2, m)
+    t0 = time.perf_counter()
+    ora.rank(q)
+    dt = time.perf_counter() - t0
+    if per_step_q is None:
+        per_step_q = int(min(2e8, max(m, m * target_s / max(dt, 1e-6))))
+    q = gen.queries(SEED[2], N2, per_step_q)
+    return ora, q, prep
+
+
+def run_reference(args):
+    """--impl reference: the oracle timed on the host, same metric / config / unit."""
+    import oracle
+
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    ora, q, prep = cpu_oracle_rank(per_step_q=1 << 24)
+    for _ in range(args.warmup):
+        ora.rank(q)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        ora.rank(q)
+    ms = (time.perf_counter() - t0) * 1e3 / args.steps
+    v = q.size / ms / 1e6
+    line = {"impl": "reference", "metric": METRIC, "value": round(v, 6), "unit": "Gqueries/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+            "config": workload_config(args.gpus),
+            "cpu_baseline": {"value": round(v, 6), "unit": "Gqueries/s", "cores": oracle.threads(), "kind": "oracle",
+                             "sample": f"{q.size} of the configs[1] queries per step (host-regenerated), text 2^34 bits; "
+                                       f"prefix-array precompute {prep:.1f}s untimed"},
+            "e2e": {"value": round(v, 6), "unit": "Gqueries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(n_gpus):
+    return {"workload": "configs[1]: BiRank16 rank, n=2^34 bits iid Bernoulli(0.5), 10^9 uniform q in [0,n] per GPU, "
+                        "u64 out", "n_bits": N2, "queries_per_gpu": M2, "global_queries": M2 * n_gpus,
+            "parallelism": f"replicate structure, shard queries x{n_gpus}",
+            "l2": "no flush: timed inputs (2.2 GB lines, 8 GB queries) >> 126 MB L2"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--rows", default="all", choices=["all", "headline"])
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import paper_2602_04103_b200 as qr
+
+    ctx = Ctx(args)
+    K, W = args.steps, max(3, args.warmup)
+    peak, peak_src = peaks()
+    clocks = Clocks(ctx.local)
+    wall0 = time.perf_counter()
+    c2 = bench_birank(ctx, 0.5, K, W, with_ceiling=True, clocks=clocks, e2e=True)
+    rows = {}
+    if args.rows == "all":
+        rows["c2_p0.01"] = bench_birank(ctx, 0.01, K, W, with_ceiling=False)
+        rows["c3_quadrank"] = bench_quadrank(ctx, K, W)
+        rows["c4_quadfm"] = bench_fm(ctx, N4, 0, M4, L4, SEED[4], K, W)
+        rows["c5_quadfm"] = bench_fm(ctx, N5, 1, M5, L5, SEED[5], K, W, rank_queries=10**9)
+        rows["c1_small"] = bench_small(ctx, K, W)
+    ms = c2["ms"]
+    value = c2["gq_s"]
+    alg_bytes_q = BI_LINE_BYTES + 16
+    achieved = alg_bytes_q * M2 / (ms * 1e-3) / 1e9          # per GPU, GB/s
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            tj = json.load(f)
+        traffic = tj.get("k_bi_rank_bytes_per_launch")
+    except Exception:
+        pass
+    cpu = None
+    if ctx.rank == 0 and ctx.world == 1 and not args.no_cpu:
+        import oracle
+
+        ora, q, prep = cpu_oracle_rank()
+        t0 = time.perf_counter()
+        ora.rank(q)
+        dt = time.perf_counter() - t0
+        cpu = {"value": round(q.size / dt / 1e9, 6), "unit": "Gqueries/s", "cores": oracle.threads(), "kind": "oracle",
+               "sample": f"{q.size} queries of the configs[1] stream (host-regenerated text 2^34 bits, plain prefix "
+                         f"array precompute {prep:.1f}s untimed), {dt:.1f}s of CPU work"}
+    ceil0 = c2["ceiling_mode0"]["gq_s"]
+    line = {
+        "metric": METRIC, "value": round(value, 4), "unit": "Gqueries/s", "n_gpus": ctx.world, "steps": K,
+        "warmup": W, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "u64", "data": "synthetic (seeded counter-based generators, gen/qrgen.h)",
+        "config": workload_config(ctx.world),
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                     "frac": round(achieved / peak, 4), "traffic": traffic,
+                     "kernel": "k_bi_rank (BiRank16 rank, Eq. 1)",
+                     "alg_bytes_per_query": round(alg_bytes_q, 3), "peak_source": peak_src,
+                     "gather_ceiling_gq_s": round(ceil0, 4), "frac_of_gather_ceiling": round(value / ceil0, 4)},
+        "cpu_baseline": cpu,
+        "e2e": c2.get("e2e"),
+        "gpu_launches": c2["launches"],
+        "clocks": c2["clocks"],
+        "gather_ceiling": {k: {kk: round(vv, 4) for kk, vv in v.items()} for k, v in c2.items() if k.startswith("ceiling")},
+        "rows": rows,
+        "wall_s": round(time.perf_counter() - wall0, 1),
+        "lib": qr.qr_version(),
+    }
+    if ctx.rank == 0:
+        print(json.dumps(line, default=lambda x: round(x, 4) if isinstance(x, float) else str(x)), flush=True)
+    if ctx.dist:
+        ctx.dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,159 @@
+/*
+ * qrank.h — C ABI of the B200-native rank / QuadFm library
+ * (libqrank.so; arXiv 2602.04103 "BiRank / QuadRank / QuadFm").
+ *
+ * Citations: PAPER.md line numbers with their section; SPEC.md lines as S:n.
+ *
+ * Definitions the calls compute (§1, lines 55-66):
+ *     rank(q, c) := #{ i in [0, q) : t_i = c },   0 <= q <= n;   rank(q) := rank(q, 1) for sigma = 2.
+ *
+ * Text encodings (reading R1):
+ *   bits   : n bits in u64 words, little-endian: t_i = bit (i % 64) of word i / 64.
+ *   DNA    : n symbols, 2 bits each, little-endian: t_i = bits 2(i%32)..2(i%32)+1 of word i/32;
+ *            A = 0, C = 1, G = 2, T = 3.
+ * Bits/symbols at positions >= n in the last word are ignored (the builder masks them).
+ *
+ * Ownership and memory spaces:
+ *   - A handle owns the device memory of its layout and frees it in qr_free / qr_fm_free.
+ *     Handles are immutable after build and may be used concurrently from any number of
+ *     host threads and CUDA streams.
+ *   - Build inputs may be host or device pointers (detected with cudaPointerGetAttributes);
+ *     the library copies what it needs and never retains the caller's pointer.
+ *   - Query arrays (q, c, out, patterns, lengths) are either ALL device pointers on the
+ *     handle's device (fast path: one kernel launch, fully asynchronous on `stream`), or ALL
+ *     host pointers (staged path: chunked host->device copy, kernel, device->host copy,
+ *     double-buffered over two internal streams; `stream` is made to wait for the whole
+ *     pipeline; pinned host memory gives overlap, pageable memory works but serialises).
+ *     Mixed spaces are QR_EINVAL.
+ *   - `stream` is a cudaStream_t passed as void* (NULL = the legacy default stream).
+ *
+ * Errors: every call returns a qr_status; no exception crosses the ABI.  On failure,
+ * qr_last_error() returns a thread-local message.  Asynchronous kernel faults surface
+ * on the next call or on qr_sync().
+ */
+#ifndef QRANK_H
+#define QRANK_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef int32_t qr_status;
+#define QR_OK        0
+#define QR_EINVAL    1  /* null pointer, wrong sigma, bad enum, mixed host/device pointers    */
+#define QR_ECAPACITY 2  /* n >= 2^43 (sigma=2), n >= 2^45 (sigma=4,          */
+                        /* PAPER.md:514-515), or n+1 >= 2^32 for QuadFm (u32 counts)          */
+#define QR_ENOMEM    3  /* device or host allocation failed                                   */
+#define QR_ECUDA     4  /* a CUDA runtime call or kernel launch failed                        */
+
+typedef struct qr_index qr_index;   /* BiRank16 (sigma=2) or QuadRank16 (sigma=4) layout      */
+typedef struct qr_fm qr_fm;         /* QuadFm: QuadRank over the BWT + C + spos + 8-mer table */
+
+/* ------------------------------------------------------------------ build */
+
+/* BiRank16 (§3): 64-B lines j = [u16 b_j | 496 text bits], B = 496,
+ * superblocks of S = 128 B bits with u32 s_i = floor(rank(iS) / 2^11) (line 407) and
+ * b_j = rank(jB + 240) - 2^11 s_{j/128} (line 439).  Lines = floor(n/B)+1 (reading R4).
+ * bits: packed text (host or device), ceil(n/64) words.  n < 2^43.  The build runs on
+ * `device` (per-line popcount kernel, device-wide exclusive scan, inlining kernel). */
+qr_status qr_birank_build(const uint64_t* bits, uint64_t n, int device, void* stream, qr_index** out);
+
+/* QuadRank16 (§4; Listing 1): 64-B lines of four
+ * u16 deltas b_{j,c} (u16 slots c + (c&2)) and B4 = 224 characters in transposed, negated
+ * low/high bit planes; superblocks of 256 lines with u32 s_{i,c} = floor(rank(i S4, c)/2^13),
+ * b_{j,c} = rank(j B4 + 96, c) - 2^13 s_{j/256, c}.  text2b: ceil(n/32) words.  n < 2^45. */
+qr_status qr_quadrank_build(const uint64_t* text2b, uint64_t n, int device, void* stream, qr_index** out);
+
+/* ------------------------------------------------------------------ queries */
+
+/* out[k] = rank(q[k], c[k]) as u64, k < m.  Requires q[k] <= n; a larger q is a
+ * contract violation: memory-safe (the line index is clamped), value unspecified.
+ *   sigma = 4: c is required, c[k] in 0..3 (values are taken mod 4).
+ *   sigma = 2: c may be NULL -> rank(q) (= rank(q,1)); else c[k] = 0 -> q - rank(q).
+ * Per query: one 64-B line (one 32-B sector if q lies left of the block's anchor, else two)
+ * plus one L2-resident superblock word (Eq. 1; Listing 1). */
+qr_status qr_rank(const qr_index* h, const uint64_t* q, const uint8_t* c, uint64_t* out, uint64_t m, void* stream);
+
+/* out4[4k + c] = rank(q[k], c) for c = 0..3 (rank_4).  sigma = 4
+ * only (QR_EINVAL on a BiRank handle).  Output is 32 B per query, array-of-structs. */
+qr_status qr_rank_all4(const qr_index* h, const uint64_t* q, uint64_t* out4, uint64_t m, void* stream);
+
+/* ------------------------------------------------------------------ QuadFm */
+
+/* Count-only FM index over a DNA text (App. D).  Builds the suffix
+ * array of T$ on the GPU (prefix doubling over device radix sorts) unless sa_or_null gives
+ * it (n+1 u32 entries, host or device), the BWT with '$' stored as A and its row spos kept
+ * (lines 919-920), C[c] = 1 + #{t_i < c}, QuadRank16 over the n+1 BWT symbols, and the
+ * 8-mer interval table (line 918; key = 2 bits per char, last pattern char in the low bits).
+ * text2b: ceil(n/32) words (host or device).  Requires 1 <= n and n + 1 < 2^32. */
+qr_status qr_fm_build(const uint64_t* text2b, uint64_t n, const uint32_t* sa_or_null, int device, void* stream,
+                      qr_fm** out);
+
+/* out[k] = number of (overlapping) occurrences of pattern k in T, as u32 (backward search:
+ * lo = C[c] + Occ(c, lo), hi = C[c] + Occ(c, hi), Occ(c,x) = rank(x,c) - [c = A and x > spos];
+ * seeded by the 8-mer table when the pattern has >= 8 symbols).  patterns: concatenated, one
+ * byte per symbol (0..3, taken mod 4).  lengths: u32[m], pattern k starts at the exclusive
+ * prefix sum of lengths (computed on the device); or lengths = NULL and every pattern has
+ * fixed_len symbols.  An empty pattern counts n + 1.  Patterns are counted as given (no
+ * reverse complement: that is a second call). */
+qr_status qr_fm_count(const qr_fm* fm, const uint8_t* patterns, const uint32_t* lengths, uint32_t fixed_len,
+                      uint32_t* out, uint64_t m, void* stream);
+
+/* As qr_fm_count (device pointers only), additionally accumulating into work[0] the number of
+ * backward steps executed after seeding and into work[1] the number of distinct 64-B lines
+ * those steps touch (1 or 2 per step) — the algorithmic-bytes denominator of SURVEY §8(d).
+ * work: 2 u64 on the device, accumulated (not reset). */
+qr_status qr_fm_count_work(const qr_fm* fm, const uint8_t* patterns, const uint32_t* lengths, uint32_t fixed_len,
+                           uint32_t* out, uint64_t m, uint64_t* work, void* stream);
+
+/* ------------------------------------------------------------------ measurement */
+
+/* Gather ceiling ("null rank"): the same q stream, the same line-index
+ * arithmetic and the same loads as qr_rank, no popcount and no superblock read;
+ * out[k] = XOR of the loaded words.  mode 0: exactly the sectors qr_rank reads (32 B or
+ * 64 B); mode 1: the full 64-B line always.  Device pointers only. */
+qr_status qr_gather_ceiling(const qr_index* h, const uint64_t* q, uint64_t* out, uint64_t m, int mode, void* stream);
+
+/* ------------------------------------------------------------------ handles */
+
+/* sigma (2 or 4), n, and the layout's device bytes (lines + superblock array). */
+qr_status qr_info(const qr_index* h, uint64_t* n, int* sigma, uint64_t* line_bytes, uint64_t* super_bytes);
+
+/* Copy the layout to host buffers of qr_info's sizes (either may be NULL). Synchronous. */
+qr_status qr_export_layout(const qr_index* h, void* host_lines, void* host_super);
+
+/* n, N = n+1 BWT rows, spos, C[0..4] (C[4] = n+1), and the QuadRank handle over the BWT
+ * (owned by fm; valid until qr_fm_free). */
+qr_status qr_fm_info(const qr_fm* fm, uint64_t* n, uint64_t* spos, uint64_t C[5], const qr_index** bwt_rank);
+
+/* Copy the 8-mer interval table (65536 pairs of u32 [lo, hi)) to a host buffer. Synchronous. */
+qr_status qr_fm_export_kmer(const qr_fm* fm, uint32_t* host_pairs);
+
+/* Replicate a handle onto another device (peer copy over NVLink when available). */
+qr_status qr_clone_to_device(const qr_index* h, int device, void* stream, qr_index** out);
+qr_status qr_fm_clone_to_device(const qr_fm* fm, int device, void* stream, qr_fm** out);
+
+/* Synchronise `stream` and surface any asynchronous error. */
+qr_status qr_sync(void* stream);
+
+void qr_free(qr_index* h);
+void qr_fm_free(qr_fm* fm);
+
+/* Thread-local message of the last failure on this thread ("" if none). */
+const char* qr_last_error(void);
+
+/* Process-wide launch-configuration knobs for measurement sweeps (results never depend on
+ * them): "rank_k" (1, 2, 4 or 8 independent queries per thread per iteration),
+ * "rank_blocks_per_sm" and "fm_blocks_per_sm" (256-thread CTAs per SM of the grid-stride
+ * rank / FM kernels, 1..64), "stage_chunk" (queries per chunk of the staged host path).
+ * QR_EINVAL for an unknown key or out-of-range value. */
+qr_status qr_set_tuning(const char* key, int64_t value);
+
+/* Library version string. */
+const char* qr_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* QRANK_H */

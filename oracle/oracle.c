@@ -216,9 +216,10 @@ EXPORT void or_fm_work(const uint8_t* bwt, const uint64_t* cp, const uint64_t* C
     const uint8_t* P = pat + off[k];
     uint64_t lo = 0, hi = N;
     uint32_t st = 0;
+    uint32_t sk = len[k] >= skip ? skip : 0;   /* a k-mer table seeds only patterns of >= skip symbols */
     for (int64_t j = (int64_t)len[k] - 1; j >= 0 && lo < hi; --j) {
       uint32_t c = P[j];
-      if (st >= skip) { ts += 1; tl += (lo / block != hi / block) ? 2 : 1; }
+      if (st >= sk) { ts += 1; tl += (lo / block != hi / block) ? 2 : 1; }
       lo = C[c] + occ(bwt, cp, lo, c);
       hi = C[c] + occ(bwt, cp, hi, c);
       ++st;

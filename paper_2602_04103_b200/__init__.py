@@ -1,0 +1,251 @@
+"""B200-native BiRank / QuadRank / QuadFm (arXiv 2602.04103) — Python binding.
+
+Thin ctypes marshalling over the C-ABI library ``lib/libqrank.so`` (declared in
+``include/qrank.h``).  Every function here has the C name and only turns
+arguments into pointers/sizes: every step of the method runs in the library's
+CUDA kernels.  There is no fallback — if the library is missing, importing the
+binding raises.
+
+Arrays may be torch tensors (device tensors on the handle's device, or CPU
+tensors) or numpy arrays (host).  All query arrays of one call must live in the
+same space (all device = one asynchronous kernel launch on ``stream``; all host =
+the library's staged, pipelined host<->device path).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "libqrank.so")
+
+QR_OK, QR_EINVAL, QR_ECAPACITY, QR_ENOMEM, QR_ECUDA = 0, 1, 2, 3, 4
+_STATUS = {1: "QR_EINVAL", 2: "QR_ECAPACITY", 3: "QR_ENOMEM", 4: "QR_ECUDA"}
+
+# every symbol include/qrank.h declares (tests check the .so exports all of them)
+EXPORTS = (
+    "qr_birank_build", "qr_quadrank_build", "qr_rank", "qr_rank_all4", "qr_fm_build", "qr_fm_count",
+    "qr_fm_count_work", "qr_gather_ceiling", "qr_info", "qr_export_layout", "qr_fm_info", "qr_fm_export_kmer",
+    "qr_clone_to_device", "qr_fm_clone_to_device", "qr_sync", "qr_free", "qr_fm_free", "qr_last_error",
+    "qr_version", "qr_set_tuning",
+)
+
+
+class QrError(RuntimeError):
+    def __init__(self, status: int, where: str, msg: str):
+        super().__init__(f"{where}: {_STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+_lib = None
+
+
+def lib():
+    """Load libqrank.so (raises if it was not built — no CPU fallback exists)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"libqrank.so not built: {LIB_PATH} (run `make` at the repo root)")
+        L = C.CDLL(LIB_PATH)
+        V, U64, I32, U32 = C.c_void_p, C.c_uint64, C.c_int, C.c_uint32
+        PP = C.POINTER(C.c_void_p)
+        sig = {
+            "qr_birank_build": ([V, U64, I32, V, PP], I32),
+            "qr_quadrank_build": ([V, U64, I32, V, PP], I32),
+            "qr_rank": ([V, V, V, V, U64, V], I32),
+            "qr_rank_all4": ([V, V, V, U64, V], I32),
+            "qr_fm_build": ([V, U64, V, I32, V, PP], I32),
+            "qr_fm_count": ([V, V, V, U32, V, U64, V], I32),
+            "qr_fm_count_work": ([V, V, V, U32, V, U64, V, V], I32),
+            "qr_gather_ceiling": ([V, V, V, U64, I32, V], I32),
+            "qr_info": ([V, C.POINTER(U64), C.POINTER(C.c_int), C.POINTER(U64), C.POINTER(U64)], I32),
+            "qr_export_layout": ([V, V, V], I32),
+            "qr_fm_info": ([V, C.POINTER(U64), C.POINTER(U64), C.POINTER(U64), PP], I32),
+            "qr_fm_export_kmer": ([V, V], I32),
+            "qr_clone_to_device": ([V, I32, V, PP], I32),
+            "qr_fm_clone_to_device": ([V, I32, V, PP], I32),
+            "qr_sync": ([V], I32),
+            "qr_free": ([V], None),
+            "qr_fm_free": ([V], None),
+            "qr_last_error": ([], C.c_char_p),
+            "qr_version": ([], C.c_char_p),
+            "qr_set_tuning": ([C.c_char_p, C.c_int64], I32),
+        }
+        for name, (args, res) in sig.items():
+            f = getattr(L, name)
+            f.argtypes = args
+            f.restype = res
+        _lib = L
+    return _lib
+
+
+def _check(st: int, where: str):
+    if st != QR_OK:
+        raise QrError(st, where, lib().qr_last_error().decode())
+
+
+def _ptr(a):
+    """data pointer of a torch tensor / numpy array / int / None."""
+    if a is None:
+        return None
+    if isinstance(a, int):
+        return C.c_void_p(a)
+    if hasattr(a, "data_ptr"):
+        return C.c_void_p(a.data_ptr())
+    if hasattr(a, "ctypes"):
+        return C.c_void_p(a.ctypes.data)
+    raise TypeError(f"cannot take a pointer of {type(a)}")
+
+
+def _stream(s):
+    if s is None:
+        try:
+            import torch
+
+            if torch.cuda.is_available():
+                return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+        except Exception:
+            pass
+        return None
+    if isinstance(s, int):
+        return C.c_void_p(s)
+    return C.c_void_p(s.cuda_stream)
+
+
+class Index:
+    """Owning wrapper of a qr_index* (BiRank16 or QuadRank16)."""
+
+    def __init__(self, ptr: int, owned: bool = True):
+        self.ptr = C.c_void_p(ptr)
+        self.owned = owned
+        n, sig, lb, sb = C.c_uint64(), C.c_int(), C.c_uint64(), C.c_uint64()
+        _check(lib().qr_info(self.ptr, C.byref(n), C.byref(sig), C.byref(lb), C.byref(sb)), "qr_info")
+        self.n, self.sigma, self.line_bytes, self.super_bytes = n.value, sig.value, lb.value, sb.value
+
+    def free(self):
+        if self.owned and self.ptr:
+            lib().qr_free(self.ptr)
+        self.ptr = C.c_void_p(0)
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+class Fm:
+    """Owning wrapper of a qr_fm*."""
+
+    def __init__(self, ptr: int):
+        self.ptr = C.c_void_p(ptr)
+        n, sp = C.c_uint64(), C.c_uint64()
+        Cs = (C.c_uint64 * 5)()
+        bw = C.c_void_p()
+        _check(lib().qr_fm_info(self.ptr, C.byref(n), C.byref(sp), Cs, C.byref(bw)), "qr_fm_info")
+        self.n, self.spos, self.C = n.value, sp.value, list(Cs)
+        self.bwt = Index(bw.value, owned=False)
+
+    def free(self):
+        if self.ptr:
+            lib().qr_fm_free(self.ptr)
+        self.ptr = C.c_void_p(0)
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+# ----------------------------------------------------------------- C-ABI mirror (same names)
+def qr_birank_build(bits, n: int, device: int = 0, stream=None) -> Index:
+    out = C.c_void_p()
+    _check(lib().qr_birank_build(_ptr(bits), n, device, _stream(stream), C.byref(out)), "qr_birank_build")
+    return Index(out.value)
+
+
+def qr_quadrank_build(text2b, n: int, device: int = 0, stream=None) -> Index:
+    out = C.c_void_p()
+    _check(lib().qr_quadrank_build(_ptr(text2b), n, device, _stream(stream), C.byref(out)), "qr_quadrank_build")
+    return Index(out.value)
+
+
+def qr_rank(h: Index, q, c, out, m: int | None = None, stream=None):
+    m = (q.numel() if hasattr(q, "numel") else q.size) if m is None else m
+    _check(lib().qr_rank(h.ptr, _ptr(q), _ptr(c), _ptr(out), m, _stream(stream)), "qr_rank")
+    return out
+
+
+def qr_rank_all4(h: Index, q, out4, m: int | None = None, stream=None):
+    m = (q.numel() if hasattr(q, "numel") else q.size) if m is None else m
+    _check(lib().qr_rank_all4(h.ptr, _ptr(q), _ptr(out4), m, _stream(stream)), "qr_rank_all4")
+    return out4
+
+
+def qr_fm_build(text2b, n: int, sa=None, device: int = 0, stream=None) -> Fm:
+    out = C.c_void_p()
+    _check(lib().qr_fm_build(_ptr(text2b), n, _ptr(sa), device, _stream(stream), C.byref(out)), "qr_fm_build")
+    return Fm(out.value)
+
+
+def qr_fm_count(fm: Fm, patterns, lengths, fixed_len: int, out, m: int, stream=None):
+    _check(lib().qr_fm_count(fm.ptr, _ptr(patterns), _ptr(lengths), fixed_len, _ptr(out), m, _stream(stream)),
+           "qr_fm_count")
+    return out
+
+
+def qr_fm_count_work(fm: Fm, patterns, lengths, fixed_len: int, out, m: int, work, stream=None):
+    _check(lib().qr_fm_count_work(fm.ptr, _ptr(patterns), _ptr(lengths), fixed_len, _ptr(out), m, _ptr(work),
+                                  _stream(stream)), "qr_fm_count_work")
+    return out
+
+
+def qr_gather_ceiling(h: Index, q, out, mode: int = 0, m: int | None = None, stream=None):
+    m = (q.numel() if hasattr(q, "numel") else q.size) if m is None else m
+    _check(lib().qr_gather_ceiling(h.ptr, _ptr(q), _ptr(out), m, mode, _stream(stream)), "qr_gather_ceiling")
+    return out
+
+
+def qr_export_layout(h: Index):
+    import numpy as np
+
+    lines = np.empty(h.line_bytes, dtype=np.uint8)
+    sup = np.empty(h.super_bytes, dtype=np.uint8)
+    _check(lib().qr_export_layout(h.ptr, _ptr(lines), _ptr(sup)), "qr_export_layout")
+    return lines, sup.view(np.uint32)
+
+
+def qr_fm_export_kmer(fm: Fm):
+    import numpy as np
+
+    t = np.empty(2 * 65536, dtype=np.uint32)
+    _check(lib().qr_fm_export_kmer(fm.ptr, _ptr(t)), "qr_fm_export_kmer")
+    return t.reshape(65536, 2)
+
+
+def qr_clone_to_device(h: Index, device: int, stream=None) -> Index:
+    out = C.c_void_p()
+    _check(lib().qr_clone_to_device(h.ptr, device, _stream(stream), C.byref(out)), "qr_clone_to_device")
+    return Index(out.value)
+
+
+def qr_fm_clone_to_device(fm: Fm, device: int, stream=None) -> Fm:
+    out = C.c_void_p()
+    _check(lib().qr_fm_clone_to_device(fm.ptr, device, _stream(stream), C.byref(out)), "qr_fm_clone_to_device")
+    return Fm(out.value)
+
+
+def qr_sync(stream=None):
+    _check(lib().qr_sync(_stream(stream)), "qr_sync")
+
+
+def qr_set_tuning(key: str, value: int):
+    _check(lib().qr_set_tuning(key.encode(), int(value)), "qr_set_tuning")
+
+
+def qr_version() -> str:
+    return lib().qr_version().decode()
+
+
+lib()  # fail loudly at import when the native library is missing

@@ -1,0 +1,534 @@
+// api.cu — the extern "C" boundary of libqrank.so (include/qrank.h).
+//
+// Validation, handle lifetime, pointer-space detection and the staged host-pointer path
+// live here; every step of the method runs in the kernels of birank.cu, quadrank.cu and
+// fm.cu.  No exception crosses the ABI; errors are status codes plus a thread-local message.
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <mutex>
+#include <new>
+#include <vector>
+
+#include "qr_common.cuh"
+
+#define QR_EXPORT extern "C" __attribute__((visibility("default")))
+
+namespace qr {
+
+// ---- tuning knobs (set through qr_set_tuning; defaults chosen from B200 measurements) ----
+int g_rank_k = 4;               // independent queries per thread per iteration
+int g_rank_blocks_per_sm = 8;   // 256-thread CTAs per SM for the rank/gather kernels
+int g_fm_blocks_per_sm = 8;     // 256-thread CTAs per SM for the FM count kernel
+uint64_t g_stage_chunk = 1ull << 24;   // queries per chunk on the staged host path
+
+static thread_local char t_err[512] = "";
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(t_err, sizeof(t_err), fmt, ap);
+  va_end(ap);
+}
+qr_status fail(qr_status st, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(t_err, sizeof(t_err), fmt, ap);
+  va_end(ap);
+  return st;
+}
+qr_status cuda_fail(cudaError_t e, const char* what) {
+  set_error("%s: %s (%s)", what, cudaGetErrorName(e), cudaGetErrorString(e));
+  return e == cudaErrorMemoryAllocation ? QR_ENOMEM : QR_ECUDA;
+}
+
+int pointer_space(const void* p, int device) {
+  cudaPointerAttributes a;
+  cudaError_t e = cudaPointerGetAttributes(&a, p);
+  if (e != cudaSuccess) {
+    cudaGetLastError();  // clear: unregistered host memory on older runtimes
+    return 0;
+  }
+  if (a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged) return a.device == device ? 1 : -1;
+  return 0;
+}
+
+int sm_count(int device) {
+  static std::mutex mu;
+  static std::vector<int> cache;
+  std::lock_guard<std::mutex> g(mu);
+  if ((int)cache.size() <= device) cache.resize(device + 1, 0);
+  if (!cache[device]) {
+    int v = 0;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device) != cudaSuccess || v <= 0) v = NUM_SMS_B200;
+    cache[device] = v;
+  }
+  return cache[device];
+}
+
+qr_status alloc_index(int sigma, uint64_t n, int device, qr_index** out) {
+  qr_index* h = new (std::nothrow) qr_index();
+  if (!h) return fail(QR_ENOMEM, "host allocation");
+  h->sigma = sigma;
+  h->device = device;
+  h->n = n;
+  const uint64_t B = sigma == 2 ? BI_B : QD_B;
+  const uint32_t sb = sigma == 2 ? BI_SB_LOG : QD_SB_LOG;
+  h->n_lines = n / B + 1;                               // reading R4: q = n stays in range
+  h->n_super = ((h->n_lines - 1) >> sb) + 1;
+  h->sm_count = sm_count(device);
+  cudaError_t e;
+  if ((e = cudaMalloc((void**)&h->lines, h->n_lines * 64))) { delete h; return cuda_fail(e, "alloc lines"); }
+  const uint64_t sbytes = h->n_super * (sigma == 2 ? 4 : 16);
+  if ((e = cudaMalloc((void**)&h->super, sbytes))) { cudaFree(h->lines); delete h; return cuda_fail(e, "alloc super"); }
+  *out = h;
+  return QR_OK;
+}
+
+qr_status fm_build_device(const uint64_t* d_text, uint64_t n, const uint32_t* d_sa_given, int device, cudaStream_t st,
+                          qr_fm** out);
+cudaError_t launch_bi_gather(const qr_index* h, const uint64_t* q, uint64_t* out, uint64_t m, int mode, cudaStream_t st);
+cudaError_t launch_qd_gather(const qr_index* h, const uint64_t* q, uint64_t* out, uint64_t m, int mode, cudaStream_t st);
+
+cudaError_t launch_gather(const qr_index* h, const uint64_t* q, uint64_t* out, uint64_t m, int mode, cudaStream_t st) {
+  return h->sigma == 2 ? launch_bi_gather(h, q, out, m, mode, st) : launch_qd_gather(h, q, out, m, mode, st);
+}
+
+// RAII device guard
+struct DeviceGuard {
+  int prev = -1;
+  bool ok = false;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) == cudaSuccess && cudaSetDevice(dev) == cudaSuccess) ok = true;
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+// Copy `words` u64 of a host-or-device input into a fresh zero-padded device buffer of
+// `padded_words` u64 (stream-ordered).  Caller frees with cudaFreeAsync.
+static qr_status stage_input(const uint64_t* src, uint64_t words, uint64_t padded_words, cudaStream_t st,
+                             uint64_t** dst) {
+  cudaError_t e;
+  uint64_t* d = nullptr;
+  if ((e = cudaMallocAsync((void**)&d, padded_words * 8, st))) return cuda_fail(e, "alloc staged input");
+  if (padded_words > words) cudaMemsetAsync(d + words, 0, (padded_words - words) * 8, st);
+  if (words && (e = cudaMemcpyAsync(d, src, words * 8, cudaMemcpyDefault, st))) {
+    cudaFreeAsync(d, st);
+    return cuda_fail(e, "copy input");
+  }
+  *dst = d;
+  return QR_OK;
+}
+
+// ---- staged host-pointer pipeline ----------------------------------------------------------
+// Two slots, one internal stream each: chunk k uses slot k%2 on stream k%2, so the H2D copy
+// and kernel of one chunk overlap the kernel and D2H copy of the other (separate copy
+// engines).  In-order streams make slot reuse safe across chunks and across calls.
+struct Stager {
+  std::mutex mu;
+  cudaStream_t s[2] = {nullptr, nullptr};
+  cudaEvent_t ev_start = nullptr, ev_done[2] = {nullptr, nullptr};
+  void* buf[2] = {nullptr, nullptr};
+  size_t cap = 0;
+};
+static std::mutex g_stagers_mu;
+static std::vector<Stager*> g_stagers;
+
+static Stager* stager_for(int device) {
+  std::lock_guard<std::mutex> g(g_stagers_mu);
+  if ((int)g_stagers.size() <= device) g_stagers.resize(device + 1, nullptr);
+  if (!g_stagers[device]) {
+    Stager* S = new Stager();
+    for (int i = 0; i < 2; ++i) {
+      cudaStreamCreateWithFlags(&S->s[i], cudaStreamNonBlocking);
+      cudaEventCreateWithFlags(&S->ev_done[i], cudaEventDisableTiming);
+    }
+    cudaEventCreateWithFlags(&S->ev_start, cudaEventDisableTiming);
+    g_stagers[device] = S;
+  }
+  return g_stagers[device];
+}
+
+struct StageArray {
+  const void* host_in;   // input (host) or nullptr
+  void* host_out;        // output (host) or nullptr
+  size_t item_bytes;
+};
+
+template <typename Launch>
+static qr_status run_staged(int device, cudaStream_t user, uint64_t m, const std::vector<StageArray>& arrays,
+                            Launch launch) {
+  Stager* S = stager_for(device);
+  std::lock_guard<std::mutex> g(S->mu);
+  size_t per_item = 0;
+  for (auto& a : arrays) per_item += (a.item_bytes + 15) & ~size_t(15);
+  const uint64_t chunk = g_stage_chunk;
+  const size_t need = per_item * (size_t)(m < chunk ? m : chunk) + 256 * arrays.size();
+  cudaError_t e;
+  if (S->cap < need) {
+    for (int i = 0; i < 2; ++i) {
+      if (S->buf[i]) { cudaStreamSynchronize(S->s[i]); cudaFree(S->buf[i]); S->buf[i] = nullptr; }
+    }
+    S->cap = 0;
+    for (int i = 0; i < 2; ++i)
+      if ((e = cudaMalloc(&S->buf[i], need))) return cuda_fail(e, "alloc staging buffers");
+    S->cap = need;
+  }
+  cudaEventRecord(S->ev_start, user);                   // respect work already queued on `user`
+  cudaStreamWaitEvent(S->s[0], S->ev_start, 0);
+  cudaStreamWaitEvent(S->s[1], S->ev_start, 0);
+  uint64_t k = 0;
+  for (uint64_t lo = 0; lo < m; lo += chunk, ++k) {
+    const uint64_t cnt = (m - lo < chunk) ? m - lo : chunk;
+    const int slot = (int)(k & 1);
+    cudaStream_t st = S->s[slot];
+    char* base = static_cast<char*>(S->buf[slot]);
+    std::vector<void*> dptr(arrays.size());
+    size_t off = 0;
+    for (size_t a = 0; a < arrays.size(); ++a) {
+      dptr[a] = base + off;
+      off += (((arrays[a].item_bytes + 15) & ~size_t(15)) * (size_t)cnt + 255) & ~size_t(255);
+      if (arrays[a].host_in &&
+          (e = cudaMemcpyAsync(dptr[a], static_cast<const char*>(arrays[a].host_in) + lo * arrays[a].item_bytes,
+                               cnt * arrays[a].item_bytes, cudaMemcpyHostToDevice, st)))
+        return cuda_fail(e, "staged H2D");
+    }
+    qr_status rs = launch(dptr, cnt, st);
+    if (rs != QR_OK) return rs;
+    for (size_t a = 0; a < arrays.size(); ++a)
+      if (arrays[a].host_out &&
+          (e = cudaMemcpyAsync(static_cast<char*>(arrays[a].host_out) + lo * arrays[a].item_bytes, dptr[a],
+                               cnt * arrays[a].item_bytes, cudaMemcpyDeviceToHost, st)))
+        return cuda_fail(e, "staged D2H");
+  }
+  for (int i = 0; i < 2; ++i) {
+    cudaEventRecord(S->ev_done[i], S->s[i]);
+    cudaStreamWaitEvent(user, S->ev_done[i], 0);
+  }
+  if ((e = cudaGetLastError())) return cuda_fail(e, "staged pipeline");
+  return QR_OK;
+}
+
+// classify a set of query pointers: 1 = all device (on `device`), 0 = all host, -1 = mixed/foreign
+static int classify(std::initializer_list<const void*> ptrs, int device) {
+  int kind = -2;
+  for (const void* p : ptrs) {
+    if (!p) continue;
+    int s = pointer_space(p, device);
+    if (s < 0) return -1;
+    if (kind == -2) kind = s;
+    else if (kind != s) return -1;
+  }
+  return kind == -2 ? 1 : kind;
+}
+
+}  // namespace qr
+
+using namespace qr;
+
+// =============================================================================== exports
+
+QR_EXPORT const char* qr_last_error(void) { return t_err; }
+QR_EXPORT const char* qr_version(void) { return "qrank-b200 0.1 (sm_100a)"; }
+
+QR_EXPORT qr_status qr_set_tuning(const char* key, int64_t value) {
+  if (!key) return fail(QR_EINVAL, "qr_set_tuning: null key");
+  if (!strcmp(key, "rank_k")) {
+    if (value != 1 && value != 2 && value != 4 && value != 8) return fail(QR_EINVAL, "rank_k must be 1, 2, 4 or 8");
+    g_rank_k = (int)value;
+  } else if (!strcmp(key, "rank_blocks_per_sm")) {
+    if (value < 1 || value > 64) return fail(QR_EINVAL, "rank_blocks_per_sm out of range");
+    g_rank_blocks_per_sm = (int)value;
+  } else if (!strcmp(key, "fm_blocks_per_sm")) {
+    if (value < 1 || value > 64) return fail(QR_EINVAL, "fm_blocks_per_sm out of range");
+    g_fm_blocks_per_sm = (int)value;
+  } else if (!strcmp(key, "stage_chunk")) {
+    if (value < 1024) return fail(QR_EINVAL, "stage_chunk too small");
+    g_stage_chunk = (uint64_t)value;
+  } else {
+    return fail(QR_EINVAL, "unknown tuning key '%s'", key);
+  }
+  return QR_OK;
+}
+
+QR_EXPORT qr_status qr_birank_build(const uint64_t* bits, uint64_t n, int device, void* stream, qr_index** out) {
+  if (!out || (!bits && n)) return fail(QR_EINVAL, "qr_birank_build: null pointer");
+  *out = nullptr;
+  if (n >= BI_MAX_N) return fail(QR_ECAPACITY, "qr_birank_build: n >= 2^43 (PAPER.md:411-412)");
+  DeviceGuard dg(device);
+  if (!dg.ok) return fail(QR_EINVAL, "qr_birank_build: bad device %d", device);
+  cudaStream_t st = (cudaStream_t)stream;
+  const uint64_t L = n / BI_B + 1;
+  const uint64_t words = (n + 63) >> 6;
+  uint64_t padded = (L * 62 + 7) / 8 + 2;
+  if (padded < words + 1) padded = words + 1;
+  uint64_t* d = nullptr;
+  qr_status s = stage_input(bits, words, padded, st, &d);
+  if (s != QR_OK) return s;
+  s = birank_build_device(d, n, device, st, out);
+  cudaFreeAsync(d, st);
+  if (s == QR_OK) {
+    cudaError_t e = cudaStreamSynchronize(st);
+    if (e) { qr_free(*out); *out = nullptr; return cuda_fail(e, "qr_birank_build"); }
+  }
+  return s;
+}
+
+QR_EXPORT qr_status qr_quadrank_build(const uint64_t* text2b, uint64_t n, int device, void* stream, qr_index** out) {
+  if (!out || (!text2b && n)) return fail(QR_EINVAL, "qr_quadrank_build: null pointer");
+  *out = nullptr;
+  if (n >= QD_MAX_N) return fail(QR_ECAPACITY, "qr_quadrank_build: n >= 2^45 (PAPER.md:514-515)");
+  DeviceGuard dg(device);
+  if (!dg.ok) return fail(QR_EINVAL, "qr_quadrank_build: bad device %d", device);
+  cudaStream_t st = (cudaStream_t)stream;
+  const uint64_t L = n / QD_B + 1;
+  const uint64_t words = (n + 31) >> 5;
+  uint64_t padded = 7 * L;
+  if (padded < words) padded = words;
+  uint64_t* d = nullptr;
+  qr_status s = stage_input(text2b, words, padded, st, &d);
+  if (s != QR_OK) return s;
+  s = quadrank_build_device(d, n, device, st, out);
+  cudaFreeAsync(d, st);
+  if (s == QR_OK) {
+    cudaError_t e = cudaStreamSynchronize(st);
+    if (e) { qr_free(*out); *out = nullptr; return cuda_fail(e, "qr_quadrank_build"); }
+  }
+  return s;
+}
+
+QR_EXPORT qr_status qr_rank(const qr_index* h, const uint64_t* q, const uint8_t* c, uint64_t* out, uint64_t m,
+                            void* stream) {
+  if (!h) return fail(QR_EINVAL, "qr_rank: null handle");
+  if (m == 0) return QR_OK;
+  if (!q || !out) return fail(QR_EINVAL, "qr_rank: null q/out");
+  if (h->sigma == 4 && !c) return fail(QR_EINVAL, "qr_rank: sigma=4 requires c");
+  DeviceGuard dg(h->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  auto launch = [&](const uint64_t* dq, const uint8_t* dc, uint64_t* dout, uint64_t cnt, cudaStream_t s) -> cudaError_t {
+    return h->sigma == 2 ? launch_birank_rank(h, dq, dc, dout, cnt, s) : launch_quadrank_rank(h, dq, dc, dout, cnt, s);
+  };
+  int sp = classify({q, c, out}, h->device);
+  if (sp < 0) return fail(QR_EINVAL, "qr_rank: q, c, out must all be device pointers on device %d or all host", h->device);
+  if (sp == 1) {
+    cudaError_t e = launch(q, c, out, m, st);
+    return e ? cuda_fail(e, "qr_rank launch") : QR_OK;
+  }
+  std::vector<StageArray> arr = {{q, nullptr, 8}, {nullptr, out, 8}};
+  if (c) arr.push_back({c, nullptr, 1});
+  return run_staged(h->device, st, m, arr, [&](const std::vector<void*>& d, uint64_t cnt, cudaStream_t s) -> qr_status {
+    cudaError_t e = launch((const uint64_t*)d[0], c ? (const uint8_t*)d[2] : nullptr, (uint64_t*)d[1], cnt, s);
+    return e ? cuda_fail(e, "qr_rank launch") : QR_OK;
+  });
+}
+
+QR_EXPORT qr_status qr_rank_all4(const qr_index* h, const uint64_t* q, uint64_t* out4, uint64_t m, void* stream) {
+  if (!h) return fail(QR_EINVAL, "qr_rank_all4: null handle");
+  if (h->sigma != 4) return fail(QR_EINVAL, "qr_rank_all4: needs a QuadRank (sigma=4) handle");
+  if (m == 0) return QR_OK;
+  if (!q || !out4) return fail(QR_EINVAL, "qr_rank_all4: null q/out4");
+  DeviceGuard dg(h->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  int sp = classify({q, out4}, h->device);
+  if (sp < 0) return fail(QR_EINVAL, "qr_rank_all4: q and out4 must both be device (device %d) or both host", h->device);
+  if (sp == 1) {
+    cudaError_t e = launch_quadrank_all4(h, q, out4, m, st);
+    return e ? cuda_fail(e, "qr_rank_all4 launch") : QR_OK;
+  }
+  std::vector<StageArray> arr = {{q, nullptr, 8}, {nullptr, out4, 32}};
+  return run_staged(h->device, st, m, arr, [&](const std::vector<void*>& d, uint64_t cnt, cudaStream_t s) -> qr_status {
+    cudaError_t e = launch_quadrank_all4(h, (const uint64_t*)d[0], (uint64_t*)d[1], cnt, s);
+    return e ? cuda_fail(e, "qr_rank_all4 launch") : QR_OK;
+  });
+}
+
+QR_EXPORT qr_status qr_gather_ceiling(const qr_index* h, const uint64_t* q, uint64_t* out, uint64_t m, int mode,
+                                      void* stream) {
+  if (!h || (m && (!q || !out))) return fail(QR_EINVAL, "qr_gather_ceiling: null pointer");
+  if (mode != 0 && mode != 1) return fail(QR_EINVAL, "qr_gather_ceiling: mode must be 0 or 1");
+  DeviceGuard dg(h->device);
+  if (m && classify({q, out}, h->device) != 1) return fail(QR_EINVAL, "qr_gather_ceiling: device pointers only");
+  cudaError_t e = launch_gather(h, q, out, m, mode, (cudaStream_t)stream);
+  return e ? cuda_fail(e, "qr_gather_ceiling launch") : QR_OK;
+}
+
+QR_EXPORT qr_status qr_fm_build(const uint64_t* text2b, uint64_t n, const uint32_t* sa_or_null, int device,
+                                void* stream, qr_fm** out) {
+  if (!out || !text2b) return fail(QR_EINVAL, "qr_fm_build: null pointer");
+  *out = nullptr;
+  if (n == 0) return fail(QR_EINVAL, "qr_fm_build: empty text");
+  if (n + 1 >= (1ull << 32)) return fail(QR_ECAPACITY, "qr_fm_build: n+1 >= 2^32 (u32 counts)");
+  DeviceGuard dg(device);
+  if (!dg.ok) return fail(QR_EINVAL, "qr_fm_build: bad device %d", device);
+  cudaStream_t st = (cudaStream_t)stream;
+  const uint64_t words = (n + 31) >> 5;
+  uint64_t* d = nullptr;
+  qr_status s = stage_input(text2b, words, words + 1, st, &d);
+  if (s != QR_OK) return s;
+  // chars >= n are never read by the FM builder (SA keys, BWT and C stop at n)
+  uint32_t* dsa = nullptr;
+  if (sa_or_null) {
+    cudaError_t e;
+    if ((e = cudaMallocAsync((void**)&dsa, (n + 1) * 4, st))) { cudaFreeAsync(d, st); return cuda_fail(e, "alloc sa"); }
+    if ((e = cudaMemcpyAsync(dsa, sa_or_null, (n + 1) * 4, cudaMemcpyDefault, st))) {
+      cudaFreeAsync(d, st); cudaFreeAsync(dsa, st); return cuda_fail(e, "copy sa");
+    }
+  }
+  s = fm_build_device(d, n, dsa, device, st, out);
+  cudaFreeAsync(d, st);
+  if (dsa) cudaFreeAsync(dsa, st);
+  cudaStreamSynchronize(st);
+  return s;
+}
+
+static qr_status fm_count_impl(const qr_fm* fm, const uint8_t* patterns, const uint32_t* lengths, uint32_t fixed_len,
+                               uint32_t* out, uint64_t m, uint64_t* work, void* stream) {
+  if (!fm) return fail(QR_EINVAL, "qr_fm_count: null handle");
+  if (m == 0) return QR_OK;
+  if (!out || (!patterns && (lengths || fixed_len))) return fail(QR_EINVAL, "qr_fm_count: null pointer");
+  DeviceGuard dg(fm->bwt->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  const uint8_t* pat = patterns;
+  static const uint8_t dummy = 0;
+  int sp = classify({patterns, lengths, out, work}, fm->bwt->device);
+  if (sp < 0) return fail(QR_EINVAL, "qr_fm_count: pointers must all be device (device %d) or all host", fm->bwt->device);
+  if (sp == 1) return fm_count_device(fm, pat ? pat : &dummy, lengths, fixed_len, out, m, work, st);
+  if (work) return fail(QR_EINVAL, "qr_fm_count_work: device pointers only");
+  if (!lengths) {
+    std::vector<StageArray> arr = {{patterns, nullptr, (size_t)fixed_len}, {nullptr, out, 4}};
+    if (fixed_len == 0) arr[0].host_in = nullptr, arr[0].item_bytes = 1;
+    return run_staged(fm->bwt->device, st, m, arr, [&](const std::vector<void*>& d, uint64_t cnt, cudaStream_t s) {
+      return fm_count_device(fm, (const uint8_t*)d[0], nullptr, fixed_len, (uint32_t*)d[1], cnt, nullptr, s);
+    });
+  }
+  // variable lengths from host: one whole copy (offsets depend on every earlier length)
+  uint64_t total = 0;
+  for (uint64_t i = 0; i < m; ++i) total += lengths[i];
+  uint8_t* dp = nullptr;
+  uint32_t *dl = nullptr, *dout = nullptr;
+  cudaError_t e;
+  if ((e = cudaMallocAsync((void**)&dp, total + 1, st)) || (e = cudaMallocAsync((void**)&dl, m * 4, st)) ||
+      (e = cudaMallocAsync((void**)&dout, m * 4, st))) {
+    cudaFreeAsync(dp, st); cudaFreeAsync(dl, st); cudaFreeAsync(dout, st);
+    return cuda_fail(e, "qr_fm_count: staging alloc");
+  }
+  if (total) cudaMemcpyAsync(dp, patterns, total, cudaMemcpyHostToDevice, st);
+  cudaMemcpyAsync(dl, lengths, m * 4, cudaMemcpyHostToDevice, st);
+  qr_status s = fm_count_device(fm, dp, dl, 0, dout, m, nullptr, st);
+  if (s == QR_OK) cudaMemcpyAsync(out, dout, m * 4, cudaMemcpyDeviceToHost, st);
+  cudaFreeAsync(dp, st); cudaFreeAsync(dl, st); cudaFreeAsync(dout, st);
+  return s;
+}
+
+QR_EXPORT qr_status qr_fm_count(const qr_fm* fm, const uint8_t* patterns, const uint32_t* lengths, uint32_t fixed_len,
+                                uint32_t* out, uint64_t m, void* stream) {
+  return fm_count_impl(fm, patterns, lengths, fixed_len, out, m, nullptr, stream);
+}
+
+QR_EXPORT qr_status qr_fm_count_work(const qr_fm* fm, const uint8_t* patterns, const uint32_t* lengths,
+                                     uint32_t fixed_len, uint32_t* out, uint64_t m, uint64_t* work, void* stream) {
+  if (!work) return fail(QR_EINVAL, "qr_fm_count_work: null work");
+  return fm_count_impl(fm, patterns, lengths, fixed_len, out, m, work, stream);
+}
+
+QR_EXPORT qr_status qr_info(const qr_index* h, uint64_t* n, int* sigma, uint64_t* line_bytes, uint64_t* super_bytes) {
+  if (!h) return fail(QR_EINVAL, "qr_info: null handle");
+  if (n) *n = h->n;
+  if (sigma) *sigma = h->sigma;
+  if (line_bytes) *line_bytes = h->n_lines * 64;
+  if (super_bytes) *super_bytes = h->n_super * (h->sigma == 2 ? 4 : 16);
+  return QR_OK;
+}
+
+QR_EXPORT qr_status qr_export_layout(const qr_index* h, void* host_lines, void* host_super) {
+  if (!h) return fail(QR_EINVAL, "qr_export_layout: null handle");
+  DeviceGuard dg(h->device);
+  cudaError_t e;
+  if (host_lines && (e = cudaMemcpy(host_lines, h->lines, h->n_lines * 64, cudaMemcpyDeviceToHost)))
+    return cuda_fail(e, "qr_export_layout lines");
+  if (host_super &&
+      (e = cudaMemcpy(host_super, h->super, h->n_super * (h->sigma == 2 ? 4 : 16), cudaMemcpyDeviceToHost)))
+    return cuda_fail(e, "qr_export_layout super");
+  return QR_OK;
+}
+
+QR_EXPORT qr_status qr_fm_info(const qr_fm* fm, uint64_t* n, uint64_t* spos, uint64_t C[5], const qr_index** bwt_rank) {
+  if (!fm) return fail(QR_EINVAL, "qr_fm_info: null handle");
+  if (n) *n = fm->n;
+  if (spos) *spos = fm->spos;
+  if (C) for (int c = 0; c < 5; ++c) C[c] = fm->C[c];
+  if (bwt_rank) *bwt_rank = fm->bwt;
+  return QR_OK;
+}
+
+QR_EXPORT qr_status qr_fm_export_kmer(const qr_fm* fm, uint32_t* host_pairs) {
+  if (!fm || !host_pairs) return fail(QR_EINVAL, "qr_fm_export_kmer: null pointer");
+  DeviceGuard dg(fm->bwt->device);
+  cudaError_t e = cudaMemcpy(host_pairs, fm->kmer, 65536 * sizeof(uint2), cudaMemcpyDeviceToHost);
+  return e ? cuda_fail(e, "qr_fm_export_kmer") : QR_OK;
+}
+
+QR_EXPORT qr_status qr_clone_to_device(const qr_index* h, int device, void* stream, qr_index** out) {
+  if (!h || !out) return fail(QR_EINVAL, "qr_clone_to_device: null pointer");
+  *out = nullptr;
+  DeviceGuard dg(device);
+  if (!dg.ok) return fail(QR_EINVAL, "qr_clone_to_device: bad device %d", device);
+  qr_index* c = nullptr;
+  qr_status s = alloc_index(h->sigma, h->n, device, &c);
+  if (s != QR_OK) return s;
+  cudaStream_t st = (cudaStream_t)stream;
+  int can = 0;
+  if (device != h->device) cudaDeviceCanAccessPeer(&can, device, h->device);
+  if (can) cudaDeviceEnablePeerAccess(h->device, 0), cudaGetLastError();
+  cudaError_t e = cudaMemcpyPeerAsync(c->lines, device, h->lines, h->device, h->n_lines * 64, st);
+  if (!e) e = cudaMemcpyPeerAsync(c->super, device, h->super, h->device, h->n_super * (h->sigma == 2 ? 4 : 16), st);
+  if (!e) e = cudaStreamSynchronize(st);
+  if (e) { qr_free(c); return cuda_fail(e, "qr_clone_to_device"); }
+  *out = c;
+  return QR_OK;
+}
+
+QR_EXPORT qr_status qr_fm_clone_to_device(const qr_fm* fm, int device, void* stream, qr_fm** out) {
+  if (!fm || !out) return fail(QR_EINVAL, "qr_fm_clone_to_device: null pointer");
+  *out = nullptr;
+  qr_fm* c = new (std::nothrow) qr_fm(*fm);
+  if (!c) return fail(QR_ENOMEM, "host allocation");
+  c->bwt = nullptr;
+  c->kmer = nullptr;
+  qr_status s = qr_clone_to_device(fm->bwt, device, stream, &c->bwt);
+  if (s != QR_OK) { delete c; return s; }
+  DeviceGuard dg(device);
+  cudaError_t e = cudaMalloc((void**)&c->kmer, 65536 * sizeof(uint2));
+  if (!e) e = cudaMemcpyPeerAsync(c->kmer, device, fm->kmer, fm->bwt->device, 65536 * sizeof(uint2), (cudaStream_t)stream);
+  if (!e) e = cudaStreamSynchronize((cudaStream_t)stream);
+  if (e) { qr_fm_free(c); return cuda_fail(e, "qr_fm_clone_to_device"); }
+  *out = c;
+  return QR_OK;
+}
+
+QR_EXPORT qr_status qr_sync(void* stream) {
+  cudaError_t e = cudaStreamSynchronize((cudaStream_t)stream);
+  if (!e) e = cudaGetLastError();
+  return e ? cuda_fail(e, "qr_sync") : QR_OK;
+}
+
+QR_EXPORT void qr_free(qr_index* h) {
+  if (!h) return;
+  DeviceGuard dg(h->device);
+  if (h->lines) cudaFree(h->lines);
+  if (h->super) cudaFree(h->super);
+  delete h;
+}
+
+QR_EXPORT void qr_fm_free(qr_fm* fm) {
+  if (!fm) return;
+  if (fm->bwt) {
+    DeviceGuard dg(fm->bwt->device);
+    if (fm->kmer) cudaFree(fm->kmer);
+    qr_free(fm->bwt);
+  }
+  delete fm;
+}

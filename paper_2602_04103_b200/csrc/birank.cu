@@ -1,0 +1,251 @@
+// birank.cu — BiRank16 (sigma = 2) on sm_100a: layout builder and the rank(q) kernel.
+//
+// Layout (§3; R2, R4): line j is 64 B = 32 u16:
+//   u16[0] = b_j = rank(jB + 240) - 2^11 s_{j>>7}
+//   u16[1..31] = text u16 words [31j, 31j+31)            (496 = 31*16 data bits)
+// so line bit 16+k is data bit k, and the anchor (data bit 240) is line bit 256: the
+// first 32-B sector holds b_j and data bits [0,240), the second holds data bits [240,496).
+// Superblocks: s_i = floor(rank(128 i B) / 2^11) as u32.
+//
+// Query (Eq. 1): j = q / 496, p = 16 + q - 496 j in [16, 512);
+//   p <  256: rank = 2^11 s + b_j - popc(line bits [p, 256))     (sector 0 only)
+//   p >= 256: rank = 2^11 s + b_j + popc(line bits [256, p))     (sectors 0 and 1)
+#include <cub/device/device_scan.cuh>
+
+#include "qr_common.cuh"
+
+namespace qr {
+
+// ------------------------------------------------------------------ build
+
+// Per line: c1 = popc(data bits [0,240)) = 15 text u16 words, tot = popc(all 496 data bits).
+__global__ void k_bi_count(const uint16_t* __restrict__ t16, uint64_t L, uint32_t* __restrict__ c1,
+                           uint64_t* __restrict__ tot) {
+  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < L; j += (uint64_t)gridDim.x * blockDim.x) {
+    const uint16_t* p = t16 + 31 * j;
+    uint32_t lo = 0, hi = 0;
+#pragma unroll
+    for (int k = 0; k < 15; ++k) lo += __popc((uint32_t)p[k]);
+#pragma unroll
+    for (int k = 15; k < 31; ++k) hi += __popc((uint32_t)p[k]);
+    c1[j] = lo;
+    tot[j] = lo + hi;
+  }
+}
+
+// R = exclusive prefix of tot (R_j = rank(jB)); writes s_i and the lines.
+__global__ void k_bi_write(const uint16_t* __restrict__ t16, uint64_t L, const uint32_t* __restrict__ c1,
+                           const uint64_t* __restrict__ R, uint4* __restrict__ lines, uint32_t* __restrict__ super) {
+  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < L; j += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t sb = R[(j >> BI_SB_LOG) << BI_SB_LOG] >> BI_SHIFT;        // s_{j>>7}
+    if ((j & ((1u << BI_SB_LOG) - 1)) == 0) super[j >> BI_SB_LOG] = (uint32_t)sb;
+    uint32_t b = (uint32_t)(R[j] + c1[j] - (sb << BI_SHIFT));         // rank(jB+240) - 2^11 s
+    const uint16_t* p = t16 + 31 * j;
+    uint32_t u[16];
+    u[0] = b | ((uint32_t)p[0] << 16);
+#pragma unroll
+    for (int k = 1; k < 16; ++k) u[k] = (uint32_t)p[2 * k - 1] | ((uint32_t)p[2 * k] << 16);
+    uint4* dst = lines + 4 * j;
+#pragma unroll
+    for (int v = 0; v < 4; ++v) dst[v] = make_uint4(u[4 * v], u[4 * v + 1], u[4 * v + 2], u[4 * v + 3]);
+  }
+}
+
+__global__ void k_mask_tail_bits(uint64_t* words, uint64_t n) {
+  uint64_t r = n & 63;
+  if (r) words[n >> 6] &= (1ull << r) - 1ull;
+}
+
+qr_status birank_build_device(const uint64_t* d_bits, uint64_t n, int device, cudaStream_t st, qr_index** out) {
+  // d_bits: device copy owned by the caller (api.cu), >= max(62 L, 8 ceil(n/64)) bytes, zero padded.
+  qr_index* h = nullptr;
+  qr_status rs = alloc_index(2, n, device, &h);
+  if (rs != QR_OK) return rs;
+  const uint64_t L = h->n_lines;
+  uint32_t* c1 = nullptr;
+  uint64_t *tot = nullptr, *R = nullptr;
+  void* tmp = nullptr;
+  size_t tmp_bytes = 0;
+  cudaError_t e = cudaSuccess;
+  auto bail = [&](cudaError_t err, const char* what) {
+    cudaFreeAsync(c1, st); cudaFreeAsync(tot, st); cudaFreeAsync(R, st); cudaFreeAsync(tmp, st);
+    qr_free(h);
+    return cuda_fail(err, what);
+  };
+  k_mask_tail_bits<<<1, 1, 0, st>>>(const_cast<uint64_t*>(d_bits), n);
+  if ((e = cudaMallocAsync((void**)&c1, L * sizeof(uint32_t), st))) return bail(e, "alloc c1");
+  if ((e = cudaMallocAsync((void**)&tot, L * sizeof(uint64_t), st))) return bail(e, "alloc tot");
+  if ((e = cudaMallocAsync((void**)&R, L * sizeof(uint64_t), st))) return bail(e, "alloc R");
+  const int sms = h->sm_count;
+  unsigned g = grid_stride_blocks(L, 256, sms, 16);
+  k_bi_count<<<g, 256, 0, st>>>(reinterpret_cast<const uint16_t*>(d_bits), L, c1, tot);
+  if ((e = cudaGetLastError())) return bail(e, "k_bi_count");
+  if ((e = cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, tot, R, (int64_t)L, st))) return bail(e, "scan size");
+  if ((e = cudaMallocAsync(&tmp, tmp_bytes, st))) return bail(e, "alloc scan tmp");
+  if ((e = cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, tot, R, (int64_t)L, st))) return bail(e, "scan");
+  k_bi_write<<<g, 256, 0, st>>>(reinterpret_cast<const uint16_t*>(d_bits), L, c1, R, h->lines, h->super);
+  if ((e = cudaGetLastError())) return bail(e, "k_bi_write");
+  cudaFreeAsync(c1, st); cudaFreeAsync(tot, st); cudaFreeAsync(R, st); cudaFreeAsync(tmp, st);
+  *out = h;
+  return QR_OK;
+}
+
+// ------------------------------------------------------------------ rank
+
+template <bool SMALLQ>
+__device__ __forceinline__ uint64_t bi_line_of(uint64_t q) {
+  if (SMALLQ) return (uint64_t)((uint32_t)(q >> 4) / 31u);   // floor(floor(q/16)/31) = floor(q/496), q < 2^36
+  return q / BI_B;
+}
+
+// K independent queries per thread per iteration: all K line gathers are issued before any
+// popcount, so each thread keeps K (or 2K) sectors in flight; the grid is a multiple of the
+// SM count and grid-strides over the query array (coalesced q loads and out stores).
+template <int K, bool SMALLQ, bool HAS_C>
+__global__ void __launch_bounds__(256) k_bi_rank(const uint4* __restrict__ lines, const uint32_t* __restrict__ super,
+                                                 const uint64_t* __restrict__ q, const uint8_t* __restrict__ cs,
+                                                 uint64_t* __restrict__ out, uint64_t m, uint64_t last_line) {
+  const uint64_t nthr = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i0 = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i0 < m; i0 += nthr * K) {
+    uint64_t qq[K], jj[K];
+    uint32_t pp[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      uint64_t idx = i0 + (uint64_t)k * nthr;
+      qq[k] = idx < m ? ld_stream_u64(q + idx) : 0;
+    }
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      uint64_t j = bi_line_of<SMALLQ>(qq[k]);
+      j = j > last_line ? last_line : j;                 // q > n: memory-safe clamp
+      uint64_t p = 16 + qq[k] - j * BI_B;
+      pp[k] = p > 511 ? 511u : (uint32_t)p;
+      jj[k] = j;
+    }
+    uint64_t a[K][4], b[K][4];
+    uint32_t s[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const uint4* ln = lines + 4 * jj[k];
+      ld_sector_na(ln, a[k][0], a[k][1], a[k][2], a[k][3]);
+      b[k][0] = b[k][1] = b[k][2] = b[k][3] = 0;
+      if (pp[k] >= 256) ld_sector_na(ln + 2, b[k][0], b[k][1], b[k][2], b[k][3]);
+      s[k] = __ldg(super + (jj[k] >> BI_SB_LOG));
+    }
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      uint64_t idx = i0 + (uint64_t)k * nthr;
+      const bool right = pp[k] >= 256;
+      const int x = (int)(pp[k] & 255u);                  // p (left) or p - 256 (right)
+      const uint64_t inv = right ? 0ull : ~0ull;          // left: suffix [p,256) = ~prefix(p)
+      uint32_t cnt = 0;
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        uint64_t w = right ? b[k][t] : a[k][t];
+        cnt += __popcll(w & (prefix_mask(x, t) ^ inv));
+      }
+      // left queries have p >= 16, so the inverted prefix never covers line bits [0,16) = b_j.
+      uint64_t base = ((uint64_t)s[k] << BI_SHIFT) + (a[k][0] & 0xffffull);
+      uint64_t r = right ? base + cnt : base - cnt;
+      if (HAS_C) {
+        if (idx < m && cs[idx] == 0) r = qq[k] - r;
+      }
+      if (idx < m) st_stream_u64(out + idx, r);
+    }
+  }
+}
+
+// Gather ceiling (G9): identical q stream, line arithmetic and sector loads; no popcount,
+// no superblock read.  MODE 0: the sectors rank reads; MODE 1: always the full line.
+template <int K, bool SMALLQ, int MODE>
+__global__ void __launch_bounds__(256) k_bi_gather(const uint4* __restrict__ lines, const uint64_t* __restrict__ q,
+                                                   uint64_t* __restrict__ out, uint64_t m, uint64_t last_line) {
+  const uint64_t nthr = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i0 = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i0 < m; i0 += nthr * K) {
+    uint64_t jj[K];
+    uint32_t pp[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      uint64_t idx = i0 + (uint64_t)k * nthr;
+      uint64_t qv = idx < m ? ld_stream_u64(q + idx) : 0;
+      uint64_t j = bi_line_of<SMALLQ>(qv);
+      j = j > last_line ? last_line : j;
+      uint64_t p = 16 + qv - j * BI_B;
+      pp[k] = p > 511 ? 511u : (uint32_t)p;
+      jj[k] = j;
+    }
+    uint64_t a[K][4], b[K][4];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const uint4* ln = lines + 4 * jj[k];
+      ld_sector_na(ln, a[k][0], a[k][1], a[k][2], a[k][3]);
+      b[k][0] = b[k][1] = b[k][2] = b[k][3] = 0;
+      if (MODE == 1 || pp[k] >= 256) ld_sector_na(ln + 2, b[k][0], b[k][1], b[k][2], b[k][3]);
+    }
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      uint64_t idx = i0 + (uint64_t)k * nthr;
+      uint64_t r = a[k][0] ^ a[k][1] ^ a[k][2] ^ a[k][3] ^ b[k][0] ^ b[k][1] ^ b[k][2] ^ b[k][3];
+      if (idx < m) st_stream_u64(out + idx, r);
+    }
+  }
+}
+
+extern int g_rank_k;              // tuning knobs (api.cu)
+extern int g_rank_blocks_per_sm;
+
+template <int K>
+static cudaError_t bi_rank_k(const qr_index* h, const uint64_t* q, const uint8_t* c, uint64_t* out, uint64_t m,
+                             cudaStream_t st) {
+  const bool small = h->n < (1ull << 36);
+  unsigned g = grid_stride_blocks((m + K - 1) / K, 256, h->sm_count, g_rank_blocks_per_sm);
+  const uint64_t last = h->n_lines - 1;
+  if (small) {
+    if (c) k_bi_rank<K, true, true><<<g, 256, 0, st>>>(h->lines, h->super, q, c, out, m, last);
+    else   k_bi_rank<K, true, false><<<g, 256, 0, st>>>(h->lines, h->super, q, c, out, m, last);
+  } else {
+    if (c) k_bi_rank<K, false, true><<<g, 256, 0, st>>>(h->lines, h->super, q, c, out, m, last);
+    else   k_bi_rank<K, false, false><<<g, 256, 0, st>>>(h->lines, h->super, q, c, out, m, last);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_birank_rank(const qr_index* h, const uint64_t* q, const uint8_t* c, uint64_t* out, uint64_t m,
+                               cudaStream_t st) {
+  if (m == 0) return cudaSuccess;
+  switch (g_rank_k) {
+    case 1: return bi_rank_k<1>(h, q, c, out, m, st);
+    case 2: return bi_rank_k<2>(h, q, c, out, m, st);
+    case 8: return bi_rank_k<8>(h, q, c, out, m, st);
+    default: return bi_rank_k<4>(h, q, c, out, m, st);
+  }
+}
+
+template <int K>
+static cudaError_t bi_gather_k(const qr_index* h, const uint64_t* q, uint64_t* out, uint64_t m, int mode,
+                               cudaStream_t st) {
+  const bool small = h->n < (1ull << 36);
+  unsigned g = grid_stride_blocks((m + K - 1) / K, 256, h->sm_count, g_rank_blocks_per_sm);
+  const uint64_t last = h->n_lines - 1;
+  if (small) {
+    if (mode) k_bi_gather<K, true, 1><<<g, 256, 0, st>>>(h->lines, q, out, m, last);
+    else      k_bi_gather<K, true, 0><<<g, 256, 0, st>>>(h->lines, q, out, m, last);
+  } else {
+    if (mode) k_bi_gather<K, false, 1><<<g, 256, 0, st>>>(h->lines, q, out, m, last);
+    else      k_bi_gather<K, false, 0><<<g, 256, 0, st>>>(h->lines, q, out, m, last);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_bi_gather(const qr_index* h, const uint64_t* q, uint64_t* out, uint64_t m, int mode,
+                             cudaStream_t st) {
+  if (m == 0) return cudaSuccess;
+  switch (g_rank_k) {
+    case 1: return bi_gather_k<1>(h, q, out, m, mode, st);
+    case 2: return bi_gather_k<2>(h, q, out, m, mode, st);
+    case 8: return bi_gather_k<8>(h, q, out, m, mode, st);
+    default: return bi_gather_k<4>(h, q, out, m, mode, st);
+  }
+}
+
+}  // namespace qr

@@ -1,0 +1,400 @@
+// fm.cu — QuadFm (App. D) on sm_100a.
+//
+// Build: suffix array of T$ on the GPU by prefix doubling over device radix sorts (the
+// paper leaves SA construction implicit), the BWT with '$' stored as A
+// and its row spos kept, C[c] = 1 + #{t_i < c}, QuadRank16 over the
+// N = n+1 BWT symbols (quadrank.cu), and the 8-mer interval table.
+//
+// Count: backward search: [lo,hi) from the 8-mer table (or [0,N)), then
+// for each remaining pattern char c right to left: lo = C[c] + Occ(c,lo), hi = C[c] + Occ(c,hi)
+// with Occ(c,x) = rank(x,c) - [c = A and x > spos]; stop when lo >= hi.  One pattern per lane;
+// a lane refills itself from its grid-stride pattern sequence as soon as its pattern finishes,
+// so lanes never wait for the slowest pattern of a static batch (the GPU analogue of the
+// paper's swap-pop active list).
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+
+#include "qr_common.cuh"
+
+namespace qr {
+
+struct FmParams {
+  const uint4* lines;
+  const uint32_t* super;
+  const uint2* kmer;
+  uint64_t spos;
+  uint64_t N;
+  uint64_t last_line;
+  uint32_t C[4];
+};
+
+__device__ __forceinline__ uint32_t text_char(const uint64_t* t, uint64_t i) {
+  return (uint32_t)(t[i >> 5] >> (2 * (i & 31))) & 3u;
+}
+
+// ------------------------------------------------------------------ SA by prefix doubling
+
+// initial key: the first 21 characters, 3 bits each ($ and beyond = 0, A..T = 1..4), MSB first
+__global__ void k_sa_init(const uint64_t* __restrict__ text, uint64_t n, uint64_t* __restrict__ keys,
+                          uint32_t* __restrict__ vals) {
+  const uint64_t N = n + 1;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < N; i += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t key = 0;
+#pragma unroll
+    for (int t = 0; t < 21; ++t) {
+      uint64_t x = i + t;
+      uint64_t code = x < n ? (uint64_t)text_char(text, x) + 1 : 0;
+      key = (key << 3) | code;
+    }
+    keys[i] = key;
+    vals[i] = (uint32_t)i;
+  }
+}
+
+// head[j] = j if sorted key j starts a new group, else 0; counts group starts
+__global__ void k_sa_heads(const uint64_t* __restrict__ keys, uint64_t N, uint32_t* __restrict__ head,
+                           unsigned long long* __restrict__ groups) {
+  uint32_t local = 0;
+  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < N; j += (uint64_t)gridDim.x * blockDim.x) {
+    bool h = (j == 0) || keys[j] != keys[j - 1];
+    head[j] = h ? (uint32_t)j : 0u;
+    local += h;
+  }
+  for (int o = 16; o; o >>= 1) local += __shfl_xor_sync(~0u, local, o);
+  if ((threadIdx.x & 31) == 0 && local) atomicAdd(groups, (unsigned long long)local);
+}
+
+struct MaxU32 {
+  __device__ __forceinline__ uint32_t operator()(uint32_t a, uint32_t b) const { return a > b ? a : b; }
+};
+
+__global__ void k_sa_scatter_rank(const uint32_t* __restrict__ sa, const uint32_t* __restrict__ grp, uint64_t N,
+                                  uint32_t* __restrict__ rank) {
+  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < N; j += (uint64_t)gridDim.x * blockDim.x)
+    rank[sa[j]] = grp[j];
+}
+
+// doubling key: (rank[i], rank[i+h]+1 or 0 past the end), packed in 2*b bits
+__global__ void k_sa_keys(const uint32_t* __restrict__ rank, uint64_t N, uint64_t h, int b, uint64_t* __restrict__ keys,
+                          uint32_t* __restrict__ vals) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < N; i += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t r2 = (i + h < N) ? (uint64_t)rank[i + h] + 1 : 0;
+    keys[i] = ((uint64_t)rank[i] << b) | r2;
+    vals[i] = (uint32_t)i;
+  }
+}
+
+static int bits_for(uint64_t x) {  // bits needed to represent values 0..x
+  int b = 0;
+  while (b < 64 && (x >> b)) ++b;
+  return b ? b : 1;
+}
+
+// d_sa: N u32 outputs.  Temporaries are stream-ordered allocations.
+static qr_status build_sa(const uint64_t* d_text, uint64_t n, int sms, cudaStream_t st, uint32_t* d_sa) {
+  const uint64_t N = n + 1;
+  uint64_t *ka = nullptr, *kb = nullptr;
+  uint32_t *va = nullptr, *vb = nullptr, *rank = nullptr, *head = nullptr;
+  unsigned long long* groups = nullptr;
+  unsigned long long* h_groups = nullptr;
+  void* tmp = nullptr;
+  size_t tmp_bytes = 0, need = 0;
+  cudaError_t e;
+  auto cleanup = [&]() {
+    cudaFreeAsync(ka, st); cudaFreeAsync(kb, st); cudaFreeAsync(va, st); cudaFreeAsync(vb, st);
+    cudaFreeAsync(rank, st); cudaFreeAsync(head, st); cudaFreeAsync(groups, st); cudaFreeAsync(tmp, st);
+    if (h_groups) cudaFreeHost(h_groups);
+  };
+  auto bail = [&](cudaError_t err, const char* what) { cleanup(); return cuda_fail(err, what); };
+  if ((e = cudaMallocAsync((void**)&ka, N * 8, st))) return bail(e, "sa keys");
+  if ((e = cudaMallocAsync((void**)&kb, N * 8, st))) return bail(e, "sa keys");
+  if ((e = cudaMallocAsync((void**)&va, N * 4, st))) return bail(e, "sa vals");
+  if ((e = cudaMallocAsync((void**)&vb, N * 4, st))) return bail(e, "sa vals");
+  if ((e = cudaMallocAsync((void**)&rank, N * 4, st))) return bail(e, "sa rank");
+  if ((e = cudaMallocAsync((void**)&head, N * 4, st))) return bail(e, "sa head");
+  if ((e = cudaMallocAsync((void**)&groups, 8, st))) return bail(e, "sa groups");
+  if ((e = cudaMallocHost((void**)&h_groups, 8))) return bail(e, "sa host groups");
+  {
+    cub::DoubleBuffer<uint64_t> K(ka, kb);
+    cub::DoubleBuffer<uint32_t> V(va, vb);
+    if ((e = cub::DeviceRadixSort::SortPairs(nullptr, need, K, V, (int)N, 0, 64, st))) return bail(e, "sort size");
+    size_t need2 = 0;
+    if ((e = cub::DeviceScan::InclusiveScan(nullptr, need2, head, head, MaxU32(), (int)N, st))) return bail(e, "scan size");
+    tmp_bytes = need > need2 ? need : need2;
+  }
+  if ((e = cudaMallocAsync(&tmp, tmp_bytes, st))) return bail(e, "sa tmp");
+  const unsigned g = grid_stride_blocks(N, 256, sms, 16);
+  const int b = bits_for(N);
+  k_sa_init<<<g, 256, 0, st>>>(d_text, n, ka, va);
+  cub::DoubleBuffer<uint64_t> K(ka, kb);
+  cub::DoubleBuffer<uint32_t> V(va, vb);
+  size_t tb = tmp_bytes;
+  if ((e = cub::DeviceRadixSort::SortPairs(tmp, tb, K, V, (int)N, 0, 63, st))) return bail(e, "sort");
+  uint64_t h = 21;
+  for (int round = 0; round < 64; ++round) {
+    cudaMemsetAsync(groups, 0, 8, st);
+    k_sa_heads<<<g, 256, 0, st>>>(K.Current(), N, head, groups);
+    tb = tmp_bytes;
+    if ((e = cub::DeviceScan::InclusiveScan(tmp, tb, head, head, MaxU32(), (int)N, st))) return bail(e, "scan");
+    k_sa_scatter_rank<<<g, 256, 0, st>>>(V.Current(), head, N, rank);
+    cudaMemcpyAsync(h_groups, groups, 8, cudaMemcpyDeviceToHost, st);
+    if ((e = cudaStreamSynchronize(st))) return bail(e, "sa round sync");
+    if (*h_groups == N) break;                      // every suffix has a distinct rank
+    k_sa_keys<<<g, 256, 0, st>>>(rank, N, h, b, K.Current(), V.Current());
+    tb = tmp_bytes;
+    if ((e = cub::DeviceRadixSort::SortPairs(tmp, tb, K, V, (int)N, 0, 2 * b, st))) return bail(e, "sort");
+    h *= 2;
+  }
+  if ((e = cudaMemcpyAsync(d_sa, V.Current(), N * 4, cudaMemcpyDeviceToDevice, st))) return bail(e, "sa copy");
+  if ((e = cudaGetLastError())) return bail(e, "sa kernels");
+  cleanup();
+  return QR_OK;
+}
+
+// ------------------------------------------------------------------ BWT
+
+// one output word (32 BWT symbols) per thread; '$' stored as A (0); spos recorded
+__global__ void k_bwt(const uint64_t* __restrict__ text, const uint32_t* __restrict__ sa, uint64_t N,
+                      uint64_t* __restrict__ bwt, unsigned long long* __restrict__ spos) {
+  const uint64_t nw = (N + 31) >> 5;
+  for (uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w < nw; w += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t x = 0;
+    for (uint64_t k = 0; k < 32 && 32 * w + k < N; ++k) {
+      uint64_t s = sa[32 * w + k];
+      if (s == 0) *spos = 32 * w + k;
+      else x |= (uint64_t)text_char(text, s - 1) << (2 * k);
+    }
+    bwt[w] = x;
+  }
+}
+
+// symbol counts of the text (first n chars): cnt[c]
+__global__ void k_sym_counts(const uint64_t* __restrict__ text, uint64_t n, unsigned long long* __restrict__ cnt) {
+  uint32_t a[4] = {0, 0, 0, 0};
+  const uint64_t nw = (n + 31) >> 5;
+  const uint64_t M = 0x5555555555555555ull;
+  for (uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w < nw; w += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t x = text[w];
+    uint64_t valid = (32 * w + 32 <= n) ? 32 : n - 32 * w;
+    uint64_t vm = valid == 32 ? M : (((1ull << (2 * valid)) - 1) & M);
+    uint64_t lo = x & vm, hi = (x >> 1) & vm;
+    uint32_t c3 = __popcll(lo & hi), l1 = __popcll(lo), h1 = __popcll(hi);
+    a[3] += c3; a[1] += l1 - c3; a[2] += h1 - c3; a[0] += (uint32_t)valid - l1 - h1 + c3;
+  }
+  for (int c = 0; c < 4; ++c) {
+    uint32_t v = a[c];
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(~0u, v, o);
+    if ((threadIdx.x & 31) == 0 && v) atomicAdd(cnt + c, (unsigned long long)v);
+  }
+}
+
+// ------------------------------------------------------------------ rank inside the FM loop
+
+// Occ for lo and hi of one backward step, both gathers issued before either is used.
+// Lines are read with L1 allocation: lo and hi often share a line.
+__device__ __forceinline__ void fm_step(const FmParams& F, uint32_t c, uint64_t& lo, uint64_t& hi, uint32_t& lines) {
+  uint64_t jl = (uint64_t)((uint32_t)(lo >> 5) / 7u);       // N < 2^32: floor(lo/224)
+  uint64_t jh = (uint64_t)((uint32_t)(hi >> 5) / 7u);
+  jl = jl > F.last_line ? F.last_line : jl;
+  jh = jh > F.last_line ? F.last_line : jh;
+  const uint32_t pl = (uint32_t)(32 + lo - jl * QD_B), ph = (uint32_t)(32 + hi - jh * QD_B);
+  uint64_t al[4], bl[4] = {0, 0, 0, 0}, ah[4], bh[4] = {0, 0, 0, 0};
+  const uint4* Ll = F.lines + 4 * jl;
+  const uint4* Lh = F.lines + 4 * jh;
+  ld_sector(Ll, al[0], al[1], al[2], al[3]);
+  if (pl >= 128) ld_sector(Ll + 2, bl[0], bl[1], bl[2], bl[3]);
+  ld_sector(Lh, ah[0], ah[1], ah[2], ah[3]);
+  if (ph >= 128) ld_sector(Lh + 2, bh[0], bh[1], bh[2], bh[3]);
+  const uint32_t sl = __ldg(F.super + 4 * (jl >> QD_SB_LOG) + c);
+  const uint32_t sh = __ldg(F.super + 4 * (jh >> QD_SB_LOG) + c);
+  lines = (jl != jh) ? 2u : 1u;
+  const uint64_t cl = 0ull - (uint64_t)(c & 1u), ch = 0ull - (uint64_t)(c >> 1);
+  auto rank1 = [&](const uint64_t* a, const uint64_t* b, uint32_t p, uint32_t s) -> uint64_t {
+    const bool right = p >= 128;
+    const int x = (int)(p & 127u);
+    const uint64_t inv = right ? 0ull : ~0ull;
+    const uint64_t* w = right ? b : a;
+    uint32_t cnt = __popcll((w[0] ^ cl) & (w[1] ^ ch) & (prefix_mask(x, 0) ^ inv)) +
+                   __popcll((w[2] ^ cl) & (w[3] ^ ch) & (prefix_mask(x, 1) ^ inv));
+    uint64_t dw = (c & 2u) ? a[1] : a[0];
+    uint64_t base = ((uint64_t)s << QD_SHIFT) + ((dw >> (16 * (c & 1u))) & 0xffffull);
+    return right ? base + cnt : base - cnt;
+  };
+  uint64_t rl = rank1(al, bl, pl, sl), rh = rank1(ah, bh, ph, sh);
+  // '$' is stored as A at row spos: Occ(A, x) = rank(x, A) - [x > spos]
+  if (c == 0) { rl -= (lo > F.spos); rh -= (hi > F.spos); }
+  lo = F.C[c] + rl;
+  hi = F.C[c] + rh;
+}
+
+__global__ void k_kmer_table(FmParams F, uint2* __restrict__ table) {
+  uint32_t key = blockIdx.x * blockDim.x + threadIdx.x;
+  if (key >= 65536u) return;
+  uint64_t lo = 0, hi = F.N;
+  uint32_t dummy;
+  for (int t = 0; t < 8 && lo < hi; ++t) fm_step(F, (key >> (2 * t)) & 3u, lo, hi, dummy);   // last char first
+  if (lo >= hi) lo = hi = 0;
+  table[key] = make_uint2((uint32_t)lo, (uint32_t)hi);
+}
+
+template <bool FIXED, bool WORK>
+__global__ void __launch_bounds__(256) k_fm_count(FmParams F, const uint8_t* __restrict__ pat,
+                                                  const uint64_t* __restrict__ offs, const uint32_t* __restrict__ lens,
+                                                  uint32_t fixed_len, uint32_t* __restrict__ out, uint64_t m,
+                                                  unsigned long long* __restrict__ work) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  uint64_t pi = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  uint64_t lo = 0, hi = 0;
+  int64_t k = -1;
+  const uint8_t* P = nullptr;
+  bool have = false;
+  uint64_t n_steps = 0, n_lines = 0;
+  for (;;) {
+    if (!have) {
+      if (pi >= m) break;
+      const uint32_t len = FIXED ? fixed_len : lens[pi];
+      P = pat + (FIXED ? pi * (uint64_t)fixed_len : offs[pi]);
+      if (len >= 8) {                                    // seed from the 8-mer table
+        uint32_t key = 0;
+#pragma unroll
+        for (int t = 0; t < 8; ++t) key |= ((uint32_t)__ldg(P + len - 1 - t) & 3u) << (2 * t);
+        uint2 iv = __ldg(F.kmer + key);
+        lo = iv.x; hi = iv.y;
+        k = (int64_t)len - 9;
+      } else {
+        lo = 0; hi = F.N;
+        k = (int64_t)len - 1;
+      }
+      have = true;
+    }
+    if (k < 0 || lo >= hi) {
+      out[pi] = lo < hi ? (uint32_t)(hi - lo) : 0u;
+      pi += stride;
+      have = false;
+      continue;
+    }
+    const uint32_t c = (uint32_t)__ldg(P + k) & 3u;
+    uint32_t nl;
+    fm_step(F, c, lo, hi, nl);
+    --k;
+    if (WORK) { n_steps += 1; n_lines += nl; }
+  }
+  if (WORK) {
+    for (int o = 16; o; o >>= 1) {
+      n_steps += __shfl_xor_sync(~0u, n_steps, o);
+      n_lines += __shfl_xor_sync(~0u, n_lines, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+      atomicAdd(work, (unsigned long long)n_steps);
+      atomicAdd(work + 1, (unsigned long long)n_lines);
+    }
+  }
+}
+
+__global__ void k_u32_to_u64(const uint32_t* __restrict__ a, uint64_t* __restrict__ b, uint64_t m) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m; i += (uint64_t)gridDim.x * blockDim.x)
+    b[i] = a[i];
+}
+
+static FmParams params_of(const qr_fm* fm) {
+  FmParams F;
+  F.lines = fm->bwt->lines;
+  F.super = fm->bwt->super;
+  F.kmer = fm->kmer;
+  F.spos = fm->spos;
+  F.N = fm->N;
+  F.last_line = fm->bwt->n_lines - 1;
+  for (int c = 0; c < 4; ++c) F.C[c] = (uint32_t)fm->C[c];
+  return F;
+}
+
+extern int g_fm_blocks_per_sm;
+
+qr_status fm_count_device(const qr_fm* fm, const uint8_t* pat, const uint32_t* lengths, uint32_t fixed_len,
+                          uint32_t* out, uint64_t m, uint64_t* work, cudaStream_t st) {
+  if (m == 0) return QR_OK;
+  FmParams F = params_of(fm);
+  const int sms = fm->bwt->sm_count;
+  unsigned g = grid_stride_blocks(m, 256, sms, g_fm_blocks_per_sm);
+  unsigned long long* w = reinterpret_cast<unsigned long long*>(work);
+  cudaError_t e;
+  if (!lengths) {
+    if (work) k_fm_count<true, true><<<g, 256, 0, st>>>(F, pat, nullptr, nullptr, fixed_len, out, m, w);
+    else      k_fm_count<true, false><<<g, 256, 0, st>>>(F, pat, nullptr, nullptr, fixed_len, out, m, w);
+    if ((e = cudaGetLastError())) return cuda_fail(e, "k_fm_count");
+    return QR_OK;
+  }
+  uint64_t* offs = nullptr;
+  void* tmp = nullptr;
+  size_t tb = 0;
+  if ((e = cudaMallocAsync((void**)&offs, m * 8, st))) return cuda_fail(e, "alloc offsets");
+  k_u32_to_u64<<<grid_stride_blocks(m, 256, sms, 8), 256, 0, st>>>(lengths, offs, m);
+  if ((e = cub::DeviceScan::ExclusiveSum(nullptr, tb, offs, offs, (int64_t)m, st))) { cudaFreeAsync(offs, st); return cuda_fail(e, "scan"); }
+  if ((e = cudaMallocAsync(&tmp, tb, st))) { cudaFreeAsync(offs, st); return cuda_fail(e, "alloc scan tmp"); }
+  if ((e = cub::DeviceScan::ExclusiveSum(tmp, tb, offs, offs, (int64_t)m, st))) {
+    cudaFreeAsync(offs, st); cudaFreeAsync(tmp, st); return cuda_fail(e, "scan");
+  }
+  if (work) k_fm_count<false, true><<<g, 256, 0, st>>>(F, pat, offs, lengths, 0, out, m, w);
+  else      k_fm_count<false, false><<<g, 256, 0, st>>>(F, pat, offs, lengths, 0, out, m, w);
+  e = cudaGetLastError();
+  cudaFreeAsync(offs, st);
+  cudaFreeAsync(tmp, st);
+  if (e) return cuda_fail(e, "k_fm_count");
+  return QR_OK;
+}
+
+// d_text: device copy, >= ceil(n/32) words, zero padded.  d_sa: optional device SA (N u32).
+qr_status fm_build_device(const uint64_t* d_text, uint64_t n, const uint32_t* d_sa_given, int device, cudaStream_t st,
+                          qr_fm** out) {
+  const uint64_t N = n + 1;
+  const int sms = sm_count(device);
+  cudaError_t e;
+  uint32_t* d_sa = nullptr;
+  uint64_t* d_bwt = nullptr;
+  unsigned long long* d_aux = nullptr;   // [0] spos, [1..4] symbol counts
+  unsigned long long h_aux[5];
+  qr_fm* fm = new (std::nothrow) qr_fm();
+  if (!fm) return fail(QR_ENOMEM, "qr_fm_build: host allocation");
+  auto bail = [&](qr_status s) {
+    cudaFreeAsync(d_sa, st); cudaFreeAsync(d_bwt, st); cudaFreeAsync(d_aux, st);
+    qr_fm_free(fm);
+    return s;
+  };
+  const uint64_t L = N / QD_B + 1;
+  const uint64_t bwt_words = 7 * L;            // the QuadRank builder reads 7 words per line
+  if ((e = cudaMallocAsync((void**)&d_aux, 5 * 8, st))) return bail(cuda_fail(e, "alloc aux"));
+  cudaMemsetAsync(d_aux, 0, 5 * 8, st);
+  if (!d_sa_given) {
+    if ((e = cudaMallocAsync((void**)&d_sa, N * 4, st))) return bail(cuda_fail(e, "alloc sa"));
+    qr_status s = build_sa(d_text, n, sms, st, d_sa);
+    if (s != QR_OK) return bail(s);
+  }
+  if ((e = cudaMallocAsync((void**)&d_bwt, bwt_words * 8, st))) return bail(cuda_fail(e, "alloc bwt"));
+  cudaMemsetAsync(d_bwt, 0, bwt_words * 8, st);
+  k_bwt<<<grid_stride_blocks((N + 31) / 32, 256, sms, 16), 256, 0, st>>>(d_text, d_sa_given ? d_sa_given : d_sa, N,
+                                                                          d_bwt, d_aux);
+  k_sym_counts<<<grid_stride_blocks((n + 31) / 32, 256, sms, 8), 256, 0, st>>>(d_text, n, d_aux + 1);
+  if ((e = cudaGetLastError())) return bail(cuda_fail(e, "k_bwt"));
+  qr_status s = quadrank_build_device(d_bwt, N, device, st, &fm->bwt);
+  if (s != QR_OK) return bail(s);
+  cudaMemcpyAsync(h_aux, d_aux, 5 * 8, cudaMemcpyDeviceToHost, st);
+  if ((e = cudaStreamSynchronize(st))) return bail(cuda_fail(e, "fm build sync"));
+  fm->n = n;
+  fm->N = N;
+  fm->spos = h_aux[0];
+  fm->C[0] = 1;
+  for (int c = 1; c < 4; ++c) fm->C[c] = fm->C[c - 1] + h_aux[c];   // C[c] = 1 + #{t_i < c}
+  fm->C[4] = N;
+  if ((e = cudaMalloc((void**)&fm->kmer, 65536 * sizeof(uint2)))) return bail(cuda_fail(e, "alloc kmer"));
+  FmParams F = params_of(fm);
+  k_kmer_table<<<65536 / 256, 256, 0, st>>>(F, fm->kmer);
+  if ((e = cudaGetLastError())) return bail(cuda_fail(e, "k_kmer_table"));
+  cudaFreeAsync(d_sa, st);
+  cudaFreeAsync(d_bwt, st);
+  cudaFreeAsync(d_aux, st);
+  if ((e = cudaStreamSynchronize(st))) { qr_fm_free(fm); return cuda_fail(e, "fm build"); }
+  *out = fm;
+  return QR_OK;
+}
+
+}  // namespace qr

@@ -1,0 +1,119 @@
+// qr_common.cuh — shared internals of libqrank.so (product path only).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "qrank.h"
+
+namespace qr {
+
+// ---- BiRank16 geometry (§3) ----
+constexpr uint64_t BI_B = 496;          // data bits per 64-B line
+constexpr uint32_t BI_SB_LOG = 7;       // 128 lines per superblock
+constexpr uint32_t BI_SHIFT = 11;       // s_i = floor(rank(iS)/2^11)
+constexpr uint32_t BI_ANCHOR = 240;     // b_j to data bit 240 = line bit 256
+constexpr uint64_t BI_MAX_N = 1ull << 43;
+
+// ---- QuadRank16 geometry (§4, Listing 1) ----
+constexpr uint64_t QD_B = 224;          // data chars per line
+constexpr uint32_t QD_SB_LOG = 8;       // 256 lines per superblock, PAPER.md:511 (reading R5)
+constexpr uint32_t QD_SHIFT = 13;
+constexpr uint32_t QD_ANCHOR = 96;      // data char 96 = line char 128
+constexpr uint64_t QD_MAX_N = 1ull << 45;
+
+// ---- launch geometry ----
+constexpr int NUM_SMS_B200 = 148;
+
+}  // namespace qr
+
+// Handle layouts (opaque to callers).
+struct qr_index {
+  int sigma;            // 2 or 4
+  int device;
+  uint64_t n;           // text length (bits or symbols)
+  uint64_t n_lines;     // floor(n/B)+1
+  uint64_t n_super;     // ((n_lines-1) >> SB_LOG) + 1
+  uint4* lines;         // n_lines * 64 B, 256-B aligned (cudaMalloc)
+  uint32_t* super;      // sigma=2: u32[n_super]; sigma=4: u32[4*n_super] (s_{i,c} at 4i+c)
+  int sm_count;
+};
+
+struct qr_fm {
+  qr_index* bwt;        // QuadRank16 over the N = n+1 BWT symbols ('$' stored as A)
+  uint64_t n;           // text length
+  uint64_t N;           // n + 1
+  uint64_t spos;        // BWT row of '$'
+  uint64_t C[5];        // C[c] = 1 + #{t_i < c}; C[4] = N
+  uint2* kmer;          // 65536 [lo, hi) intervals after 8 backward steps
+};
+
+namespace qr {
+// thread-local error channel
+void set_error(const char* fmt, ...);
+qr_status fail(qr_status st, const char* fmt, ...);
+qr_status cuda_fail(cudaError_t e, const char* what);
+
+// pointer space: 0 = host (pinned or pageable), 1 = device on `device`, -1 = device elsewhere
+int pointer_space(const void* p, int device);
+
+// SM count of a device (cached)
+int sm_count(int device);
+
+// internal builders used by fm.cu
+qr_status quadrank_build_device(const uint64_t* d_text2b, uint64_t n, int device, cudaStream_t st, qr_index** out);
+qr_status alloc_index(int sigma, uint64_t n, int device, qr_index** out);
+
+// kernel launchers (device pointers; validated by api.cu)
+cudaError_t launch_birank_rank(const qr_index* h, const uint64_t* q, const uint8_t* c, uint64_t* out, uint64_t m,
+                               cudaStream_t st);
+cudaError_t launch_quadrank_rank(const qr_index* h, const uint64_t* q, const uint8_t* c, uint64_t* out, uint64_t m,
+                                 cudaStream_t st);
+cudaError_t launch_quadrank_all4(const qr_index* h, const uint64_t* q, uint64_t* out4, uint64_t m, cudaStream_t st);
+cudaError_t launch_gather(const qr_index* h, const uint64_t* q, uint64_t* out, uint64_t m, int mode, cudaStream_t st);
+qr_status fm_count_device(const qr_fm* fm, const uint8_t* pat, const uint32_t* lengths, uint32_t fixed_len,
+                          uint32_t* out, uint64_t m, uint64_t* work, cudaStream_t st);
+qr_status birank_build_device(const uint64_t* d_bits, uint64_t n, int device, cudaStream_t st, qr_index** out);
+
+// grid for a grid-stride kernel: a multiple of the SM count
+inline unsigned grid_stride_blocks(uint64_t work_items, unsigned threads, int sms, int blocks_per_sm) {
+  uint64_t need = (work_items + threads - 1) / threads;
+  uint64_t cap = (uint64_t)sms * (uint64_t)blocks_per_sm;
+  if (need > cap) need = cap;
+  return need ? (unsigned)need : 1u;
+}
+
+// ---- device helpers ----
+// 256-bit gather of one 32-B sector (LDG.E.256 on sm_100a), not allocated in L1.  Deliberately
+// not .nc: ptxas may sink .nc loads below later uses (it did, serialising the K queries of a
+// thread); a coherent load cannot move past the stores that follow the gathers.
+__device__ __forceinline__ void ld_sector_na(const void* p, uint64_t& w0, uint64_t& w1, uint64_t& w2, uint64_t& w3) {
+  asm volatile("ld.global.L1::no_allocate.v4.u64 {%0,%1,%2,%3}, [%4];"
+               : "=l"(w0), "=l"(w1), "=l"(w2), "=l"(w3)
+               : "l"(p));
+}
+// 256-bit read-only load that may allocate in L1 (FM: lo and hi often share a line).
+__device__ __forceinline__ void ld_sector(const void* p, uint64_t& w0, uint64_t& w1, uint64_t& w2, uint64_t& w3) {
+  asm volatile("ld.global.v4.u64 {%0,%1,%2,%3}, [%4];" : "=l"(w0), "=l"(w1), "=l"(w2), "=l"(w3) : "l"(p));
+}
+// streaming loads/stores of the query stream / outputs (read once, write once)
+__device__ __forceinline__ uint64_t ld_stream_u64(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.global.nc.L1::no_allocate.u64 %0, [%1];" : "=l"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ void st_stream_u64(uint64_t* p, uint64_t v) {
+  asm volatile("st.global.L1::no_allocate.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void st_stream_v4u64(uint64_t* p, uint64_t a, uint64_t b, uint64_t c, uint64_t d) {
+  asm volatile("st.global.L1::no_allocate.v4.u64 [%0], {%1,%2,%3,%4};" ::"l"(p), "l"(a), "l"(b), "l"(c), "l"(d)
+               : "memory");
+}
+
+// prefix mask of the first x bits of word t of a multi-word field (x may exceed the word).
+__device__ __forceinline__ uint64_t prefix_mask(int x, int t) {
+  int d = x - 64 * t;
+  d = d < 0 ? 0 : d;
+  return d >= 64 ? ~0ull : ((1ull << d) - 1ull);
+}
+
+}  // namespace qr

@@ -1,0 +1,175 @@
+"""GPU parity of QuadFm (App. D) against the CPU oracle: GPU-built suffix array /
+BWT / C / spos, the BWT QuadRank, the 8-mer table, and fm_count on exact, random, short,
+empty, seeded-length and longer-than-text patterns.  Bit-exact (u32 counts)."""
+import itertools
+
+import numpy as np
+import pytest
+
+import gen
+import oracle
+import paper_2602_04103_b200 as qr
+from tests._util import to_dev, to_host
+
+pytestmark = pytest.mark.gpu
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+def pack2(sym: np.ndarray) -> np.ndarray:
+    n = sym.size
+    w = np.zeros((n + 31) // 32 + 1, np.uint64)
+    s = np.zeros(((n + 31) // 32) * 32, np.uint64)
+    s[:n] = sym
+    s = s.reshape(-1, 32)
+    w[: s.shape[0]] = (s << (2 * np.arange(32, dtype=np.uint64))).sum(axis=1, dtype=np.uint64)
+    return w
+
+
+def mixed_patterns(rng, sym, count):
+    n = sym.size
+    pats = []
+    for i in range(count):
+        kind = i % 5
+        if kind == 0:                                   # exact substring, any length
+            L = int(rng.integers(1, 60)); a = int(rng.integers(0, max(1, n - L + 1)))
+            pats.append(sym[a:a + L].copy())
+        elif kind == 1:                                 # random, short (< 8: no seeding)
+            pats.append(rng.integers(0, 4, int(rng.integers(0, 8))).astype(np.uint8))
+        elif kind == 2:                                 # exactly 8 (seed only), 9
+            pats.append(rng.integers(0, 4, 8 + int(rng.integers(0, 2))).astype(np.uint8))
+        elif kind == 3:                                 # random long
+            pats.append(rng.integers(0, 4, int(rng.integers(8, 40))).astype(np.uint8))
+        else:                                           # exact with one substitution
+            L = int(rng.integers(10, 50)); a = int(rng.integers(0, max(1, n - L + 1)))
+            p = sym[a:a + L].copy()
+            if p.size:
+                k = int(rng.integers(0, p.size)); p[k] = (p[k] + 1 + rng.integers(0, 3)) % 4
+            pats.append(p)
+    pats.append(sym.copy())                             # whole text
+    pats.append(np.concatenate([sym, sym[:3]]))          # longer than the text
+    pats.append(np.zeros(0, np.uint8))                   # empty -> n+1
+    return pats
+
+
+@pytest.mark.parametrize("n,kind", [(1, 0), (2, 0), (7, 0), (31, 0), (100, 0), (224, 0), (1000, 0), (50000, 0),
+                                    (131072 + 123, 0), (25000, 1), (200000, 1)])
+def test_fm_build_and_count_parity(cuda, n, kind):
+    torch = _torch()
+    w = gen.dna(300 + n, n, kind)
+    sym = gen.unpack_dna(w, n)
+    ora = oracle.FmOracle(sym)
+    fm = qr.qr_fm_build(w, n)
+    # SA-derived quantities (GPU prefix doubling vs oracle doubling + qsort)
+    assert fm.spos == ora.spos
+    assert fm.C == [int(x) for x in ora.C]
+    # the BWT rank structure ('$' stored as A) vs the oracle BWT with '$' -> A
+    bw = ora.bwt.copy(); bw[bw == 4] = 0
+    bora = oracle.DnaOracle(pack2(bw), n + 1)
+    if n < 20000:                                               # every q in [0, N], every c
+        q = np.repeat(np.arange(n + 2, dtype=np.uint64), 4)
+        c = np.tile(np.arange(4, dtype=np.uint8), n + 2)
+    else:
+        q, c = gen.queries(1, n + 1, 100000, with_c=True)
+    out = torch.empty(q.size, dtype=torch.uint64, device=cuda)
+    qr.qr_rank(fm.bwt, to_dev(q, cuda), to_dev(c, cuda), out)
+    torch.cuda.synchronize()
+    assert np.array_equal(to_host(out), bora.rank(q, c))
+    # counts
+    rng = np.random.default_rng(n)
+    pats = mixed_patterns(rng, sym, 600)
+    cat, off, lens = oracle.pack_patterns(pats)
+    ref = ora.count(cat, off, lens)
+    if n <= 1000:
+        brute = np.array([sum(1 for i in range(n - len(p) + 1) if np.array_equal(sym[i:i + len(p)], p)) if len(p) else n + 1
+                          for p in pats], np.uint32)
+        assert np.array_equal(ref, brute)
+    dout = torch.empty(lens.size, dtype=torch.int32, device=cuda)
+    qr.qr_fm_count(fm, to_dev(cat, cuda), to_dev(lens, cuda), 0, dout, lens.size)
+    torch.cuda.synchronize()
+    got = to_host(dout).view(np.uint32)
+    bad = np.nonzero(got != ref)[0]
+    assert bad.size == 0, f"n={n}: {bad.size} mismatches: idx={bad[:5]} got={got[bad[:5]]} ref={ref[bad[:5]]}"
+    # host-pointer path with variable lengths
+    hout = np.zeros(lens.size, np.uint32)
+    qr.qr_fm_count(fm, cat, lens, 0, hout, lens.size)
+    qr.qr_sync()
+    assert np.array_equal(hout, ref)
+
+
+def test_fm_kmer_table_matches_oracle(cuda):
+    n = 300000
+    w = gen.dna(42, n)
+    sym = gen.unpack_dna(w, n)
+    ora = oracle.FmOracle(sym)
+    fm = qr.qr_fm_build(w, n)
+    t = qr.qr_fm_export_kmer(fm)
+    # key: 2 bits per char, last pattern char in the low bits
+    keys = np.arange(65536, dtype=np.uint32)
+    pats = np.stack([(keys >> (2 * (7 - i))) & 3 for i in range(8)], axis=1).astype(np.uint8)
+    cat = np.ascontiguousarray(pats.reshape(-1))
+    off = np.arange(65536, dtype=np.uint64) * 8
+    lens = np.full(65536, 8, np.uint32)
+    ref = ora.count(cat, off, lens)
+    size = (t[:, 1].astype(np.int64) - t[:, 0].astype(np.int64))
+    assert np.array_equal(size, ref.astype(np.int64))
+    assert int(ref.sum()) == n - 7                               # partition identity
+    # lo of a non-empty interval = C[c_last] + ... : check monotone order of the 4^8 intervals
+    nz = size > 0
+    order = np.argsort(t[nz, 0])
+    assert np.all(np.diff(t[nz, 0][order].astype(np.int64)) > 0)
+
+
+def test_fm_given_sa_and_fixed_length_and_work(cuda):
+    torch = _torch()
+    n = 120000
+    w = gen.dna(77, n)
+    sym = gen.unpack_dna(w, n)
+    ora = oracle.FmOracle(sym)
+    fm_gpu_sa = qr.qr_fm_build(w, n)
+    fm_given = qr.qr_fm_build(to_dev(w, cuda), n, sa=ora.sa)      # caller-provided SA (host)
+    L, m = 32, 20000
+    pats = gen.patterns(5, 0, m, L, w, n)
+    off = np.arange(m, dtype=np.uint64) * L
+    lens = np.full(m, L, np.uint32)
+    ref = ora.count(pats, off, lens)
+    assert np.all(ref[0::2] >= 1)                               # exact substrings occur
+    for fm in (fm_gpu_sa, fm_given):
+        d = torch.empty(m, dtype=torch.int32, device=cuda)
+        qr.qr_fm_count(fm, to_dev(pats, cuda), None, L, d, m)
+        torch.cuda.synchronize()
+        assert np.array_equal(to_host(d).view(np.uint32), ref)
+    work = torch.zeros(2, dtype=torch.uint64, device=cuda)
+    d = torch.empty(m, dtype=torch.int32, device=cuda)
+    qr.qr_fm_count_work(fm_gpu_sa, to_dev(pats, cuda), None, L, d, m, work)
+    torch.cuda.synchronize()
+    ts, tl = ora.work(pats, off, lens, skip=8, block=224)
+    assert [int(x) for x in to_host(work)] == [ts, tl]
+    # host staged fixed-length path
+    h = np.zeros(m, np.uint32)
+    qr.qr_set_tuning("stage_chunk", 4096)
+    try:
+        qr.qr_fm_count(fm_gpu_sa, pats, None, L, h, m)
+        qr.qr_sync()
+    finally:
+        qr.qr_set_tuning("stage_chunk", 1 << 24)
+    assert np.array_equal(h, ref)
+
+
+def test_fm_all_kmers_partition(cuda):
+    torch = _torch()
+    n = 40000
+    w = gen.dna(8, n, 1 if n >= 2 * gen.BLOCK else 0)
+    fm = qr.qr_fm_build(w, n)
+    for k in (1, 2, 3, 9):
+        pats = np.array(list(itertools.product(range(4), repeat=k)) if k < 9 else
+                        np.random.default_rng(1).integers(0, 4, (5000, 9)), np.uint8)
+        d = torch.empty(pats.shape[0], dtype=torch.int32, device=cuda)
+        qr.qr_fm_count(fm, to_dev(pats.reshape(-1), cuda), None, k, d, pats.shape[0])
+        torch.cuda.synchronize()
+        if k < 9:
+            assert int(to_host(d).astype(np.int64).sum()) == n - k + 1

@@ -1,0 +1,256 @@
+"""GPU parity of BiRank16 / QuadRank16 (rank, rank_all4, layout) against the CPU oracle.
+
+Every comparison is element-by-element and bit-exact (integer outputs), on seeded
+inputs from gen/, at sizes that span several lines and superblocks with ragged
+tails, plus the degenerate cases (n = 0, 1, B-1, B, B+1, all-zero, all-one, all-G).
+"""
+import numpy as np
+import pytest
+
+import gen
+import oracle
+import paper_2602_04103_b200 as qr
+from tests._util import B, B4, S, S4, boundary_queries, to_dev, to_host
+
+pytestmark = pytest.mark.gpu
+
+BI_SIZES = [0, 1, 2, 63, 64, 240, 241, 495, 496, 497, 991, 992, 993, S - 1, S, S + 1, 2 * S + 7, 5 * S + 4321,
+            (1 << 20)]
+QD_SIZES = [0, 1, 31, 32, 95, 96, 97, 223, 224, 225, 447, 448, S4 - 1, S4, S4 + 1, 3 * S4 + 12345, (1 << 20) + 17]
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+def bits_for(n, p, seed):
+    if p == "zeros":
+        return np.zeros(max(1, (n + 63) // 64), np.uint64)
+    return gen.bits(seed, n, p)
+
+
+# ------------------------------------------------------------------ BiRank
+@pytest.mark.parametrize("n", BI_SIZES)
+@pytest.mark.parametrize("p", [0.5, 0.01, 1.0, "zeros"])
+def test_birank_rank_parity(cuda, n, p):
+    torch = _torch()
+    w = bits_for(n, p, 1000 + n)
+    ora = oracle.BitsOracle(w, n)
+    h = qr.qr_birank_build(w, n, device=0)                       # host input pointer
+    if n <= 200000:
+        q = np.arange(n + 1, dtype=np.uint64)
+    else:
+        q = np.concatenate([gen.queries(7, n, 300000), boundary_queries(n, B, S, 240)])
+    dq = to_dev(q, cuda)
+    out = torch.empty_like(dq)
+    qr.qr_rank(h, dq, None, out)
+    torch.cuda.synchronize()
+    got = to_host(out)
+    ref = ora.rank(q)
+    bad = np.nonzero(got != ref)[0]
+    assert bad.size == 0, f"n={n} p={p}: {bad.size} mismatches, first q={q[bad[:5]]} got={got[bad[:5]]} ref={ref[bad[:5]]}"
+    # sigma = 2 with a symbol array: c = 0 -> q - rank(q)
+    c = (gen.queries(3, 1, q.size, with_c=True)[1] & 1).astype(np.uint8)
+    out2 = torch.empty_like(dq)
+    qr.qr_rank(h, dq, to_dev(c, cuda), out2)
+    assert np.array_equal(to_host(out2), ora.rank(q, c))
+
+
+def test_birank_layout_closed_forms(cuda):
+    """Decode every line: b_j = rank(jB+240) - 2^11 s_{j>>7}, s_i = rank(iS)>>11 (:407),
+    data bits = text; all-ones b_0 = 240 (golden); byte accounting = 3.2762%."""
+    for n, p in [(5 * S + 4321, 0.5), (3 * S + 17, 1.0), (1000, 0.01)]:
+        w = gen.bits(55, n, p)
+        h = qr.qr_birank_build(w, n)
+        lines, sup = qr.qr_export_layout(h)
+        L = n // B + 1
+        assert lines.size == 64 * L and sup.size == (L - 1) // 128 + 1
+        u16 = lines.view(np.uint16).reshape(L, 32)
+        ora = oracle.BitsOracle(w, n)
+        anchors = np.minimum(np.arange(L, dtype=np.uint64) * B + 240, n)
+        b = u16[:, 0].astype(np.uint64) + (sup[np.arange(L) // 128].astype(np.uint64) << 11)
+        assert np.array_equal(b, ora.rank(anchors))
+        sb = np.minimum(np.arange(sup.size, dtype=np.uint64) * S, n)
+        assert np.array_equal(sup.astype(np.uint64), ora.rank(sb) >> 11)
+        text16 = np.zeros(31 * L, np.uint16)
+        t = w.view(np.uint16)[: min(w.size * 4, 31 * L)]
+        text16[: t.size] = t
+        assert np.array_equal(u16[:, 1:].reshape(-1), text16)
+        if p == 1.0:
+            assert u16[0, 0] == 240
+    n = 1 << 24
+    h = qr.qr_birank_build(gen.bits(1, n), n)
+    overhead = (h.line_bytes + h.super_bytes) / (n / 8) - 1
+    assert abs(overhead - (16 / 496 + 32 / S)) < 2e-4
+    assert abs(round(overhead * 100, 2) - 3.28) < 0.011
+
+
+def test_birank_device_input_and_host_query_path(cuda):
+    torch = _torch()
+    n = 3 * S + 999
+    w = gen.bits(9, n)
+    h = qr.qr_birank_build(to_dev(w, cuda), n)                   # device input pointer
+    q = gen.queries(4, n, 100000)
+    ref = oracle.BitsOracle(w, n).rank(q)
+    out_h = np.zeros(q.size, np.uint64)
+    qr.qr_set_tuning("stage_chunk", 4096)                        # many chunks through both slots
+    try:
+        qr.qr_rank(h, q, None, out_h)                            # host pointers: staged path
+        qr.qr_sync()
+    finally:
+        qr.qr_set_tuning("stage_chunk", 1 << 24)
+    assert np.array_equal(out_h, ref)
+    qp = torch.from_numpy(q).pin_memory()
+    op = torch.zeros_like(qp).pin_memory()
+    qr.qr_rank(h, qp, None, op)
+    torch.cuda.synchronize()
+    assert np.array_equal(op.numpy(), ref)
+
+
+@pytest.mark.parametrize("k", [1, 2, 4, 8])
+def test_birank_tuning_does_not_change_results(cuda, k):
+    torch = _torch()
+    n = 7 * S + 5
+    w = gen.bits(17, n)
+    h = qr.qr_birank_build(w, n)
+    q = np.concatenate([gen.queries(5, n, 200001), boundary_queries(n, B, S, 240)])
+    dq = to_dev(q, cuda)
+    out = torch.empty_like(dq)
+    qr.qr_set_tuning("rank_k", k)
+    qr.qr_set_tuning("rank_blocks_per_sm", 1 + k)
+    try:
+        qr.qr_rank(h, dq, None, out)
+        torch.cuda.synchronize()
+    finally:
+        qr.qr_set_tuning("rank_k", 4)
+        qr.qr_set_tuning("rank_blocks_per_sm", 8)
+    assert np.array_equal(to_host(out), oracle.BitsOracle(w, n).rank(q))
+
+
+def test_gather_ceiling_loads_the_same_sectors(cuda):
+    torch = _torch()
+    n = 4 * S + 77
+    w = gen.bits(3, n)
+    h = qr.qr_birank_build(w, n)
+    lines, _ = qr.qr_export_layout(h)
+    u64 = lines.view(np.uint64).reshape(-1, 8)
+    q = gen.queries(8, n, 50000)
+    dq = to_dev(q, cuda)
+    for mode in (0, 1):
+        out = torch.empty_like(dq)
+        qr.qr_gather_ceiling(h, dq, out, mode)
+        torch.cuda.synchronize()
+        j = (q // B).astype(np.int64)
+        p = 16 + q - j.astype(np.uint64) * B
+        a = np.bitwise_xor.reduce(u64[j, :4], axis=1)
+        b = np.bitwise_xor.reduce(u64[j, 4:], axis=1)
+        exp = a ^ np.where((p >= 256) | (mode == 1), b, 0).astype(np.uint64)
+        assert np.array_equal(to_host(out), exp)
+
+
+# ------------------------------------------------------------------ QuadRank
+@pytest.mark.parametrize("n", QD_SIZES)
+def test_quadrank_rank_and_all4_parity(cuda, n):
+    torch = _torch()
+    w = gen.dna(2000 + n, n)
+    ora = oracle.DnaOracle(w, n)
+    h = qr.qr_quadrank_build(w, n)
+    if n <= 60000:
+        q = np.repeat(np.arange(n + 1, dtype=np.uint64), 4)
+        c = np.tile(np.arange(4, dtype=np.uint8), n + 1)
+    else:
+        q = np.concatenate([gen.queries(7, n, 300000), boundary_queries(n, B4, S4, 96)])
+        c = (gen.queries(9, n, q.size, with_c=True)[1]).astype(np.uint8)
+    dq = to_dev(q, cuda)
+    out = torch.empty_like(dq)
+    qr.qr_rank(h, dq, to_dev(c, cuda), out)
+    torch.cuda.synchronize()
+    got, ref = to_host(out), ora.rank(q, c)
+    bad = np.nonzero(got != ref)[0]
+    assert bad.size == 0, f"n={n}: {bad.size} mismatches, q={q[bad[:5]]} c={c[bad[:5]]} got={got[bad[:5]]} ref={ref[bad[:5]]}"
+    qu = np.unique(q)
+    out4 = torch.empty((qu.size, 4), dtype=torch.uint64, device=cuda)
+    qr.qr_rank_all4(h, to_dev(qu, cuda), out4)
+    torch.cuda.synchronize()
+    a4 = to_host(out4)
+    assert np.array_equal(a4, ora.rank_all4(qu))
+    assert np.array_equal(a4.sum(axis=1), qu)                    # sum_c rank(q,c) = q
+
+
+def test_quadrank_all_G_and_layout(cuda):
+    """all-G deltas (0,0,96,0) (golden); b_{j,c}, s_{i,c} closed forms;
+    plane soundness: (w_low ^ cl) & (w_high ^ ch) marks exactly the chars equal to c; 14.40%."""
+    n = 3 * S4 + 1000
+    w = np.full((n + 31) // 32, 0xAAAAAAAAAAAAAAAA, np.uint64)
+    h = qr.qr_quadrank_build(w, n)
+    lines, sup = qr.qr_export_layout(h)
+    u16 = lines.view(np.uint16).reshape(-1, 32)
+    assert list(u16[0, [0, 1, 4, 5]]) == [0, 0, 96, 0]
+    for n, seed in [(3 * S4 + 12345, 4), (5000, 5)]:
+        w = gen.dna(seed, n)
+        h = qr.qr_quadrank_build(w, n)
+        lines, sup = qr.qr_export_layout(h)
+        L = n // B4 + 1
+        u16 = lines.view(np.uint16).reshape(L, 32)
+        u64 = lines.view(np.uint64).reshape(L, 8)
+        sup = sup.reshape(-1, 4).astype(np.uint64)
+        ora = oracle.DnaOracle(w, n)
+        anchors = np.minimum(np.arange(L, dtype=np.uint64) * B4 + 96, n)
+        for c, slot in enumerate([0, 1, 4, 5]):
+            b = u16[:, slot].astype(np.uint64) + (sup[np.arange(L) // 256, c] << 13)
+            # beyond n the padding is A: rank(x, A) grows past n, other symbols stay
+            extra = np.zeros(L, np.uint64)
+            if c == 0:
+                extra = (np.arange(L, dtype=np.uint64) * B4 + 96) - anchors
+            assert np.array_equal(b, ora.rank(anchors, np.full(L, c, np.uint8)) + extra), c
+        sym = gen.unpack_dna(w, n)
+        pad = np.zeros(L * B4, np.uint8)
+        pad[:n] = sym
+        pad = pad.reshape(L, B4)
+        for c in range(4):
+            cl = np.uint64(0xFFFFFFFFFFFFFFFF if c & 1 else 0)
+            ch = np.uint64(0xFFFFFFFFFFFFFFFF if c >> 1 else 0)
+            match = [(u64[:, 4 * hh + 2 * t] ^ cl) & (u64[:, 4 * hh + 2 * t + 1] ^ ch) for hh in (0, 1) for t in (0, 1)]
+            bits = np.unpackbits(np.stack(match, axis=1).view(np.uint8), bitorder="little").reshape(L, 256)
+            assert np.array_equal(bits[:, 32:].astype(bool), pad == c), c
+    n = 1 << 24
+    h = qr.qr_quadrank_build(gen.dna(1, n), n)
+    overhead = (h.line_bytes + h.super_bytes) / (n / 4) - 1
+    assert abs(round(overhead * 100, 2) - 14.40) < 0.011
+
+
+def test_quadrank_host_path_and_c_mod4(cuda):
+    n = 2 * S4 + 3
+    w = gen.dna(12, n)
+    h = qr.qr_quadrank_build(to_dev(w, cuda), n)
+    q, c = gen.queries(6, n, 70000, with_c=True)
+    ora = oracle.DnaOracle(w, n)
+    out = np.zeros(q.size, np.uint64)
+    qr.qr_set_tuning("stage_chunk", 8192)
+    try:
+        qr.qr_rank(h, q, (c | 4).astype(np.uint8), out)          # symbols are taken mod 4
+        out4 = np.zeros((q.size, 4), np.uint64)
+        qr.qr_rank_all4(h, q, out4)
+        qr.qr_sync()
+    finally:
+        qr.qr_set_tuning("stage_chunk", 1 << 24)
+    assert np.array_equal(out, ora.rank(q, c))
+    assert np.array_equal(out4, ora.rank_all4(q))
+
+
+def test_errors_surface(cuda):
+    torch = _torch()
+    n = 1000
+    hb = qr.qr_birank_build(gen.bits(1, n), n)
+    q = torch.zeros(10, dtype=torch.uint64, device=cuda)
+    o4 = torch.zeros(40, dtype=torch.uint64, device=cuda)
+    with pytest.raises(qr.QrError) as e:
+        qr.qr_rank_all4(hb, q, o4)
+    assert e.value.status == qr.QR_EINVAL
+    hq = qr.qr_quadrank_build(gen.dna(1, n), n)
+    with pytest.raises(qr.QrError):
+        qr.qr_rank(hq, q, None, o4[:10])                        # sigma=4 needs c
+    with pytest.raises(qr.QrError):
+        qr.qr_rank(hq, q, np.zeros(10, np.uint8), o4[:10])      # mixed host/device pointers
