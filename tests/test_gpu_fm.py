@@ -9,7 +9,7 @@ import pytest
 import gen
 import oracle
 import paper_2602_04103_b200 as qr
-from tests._util import to_dev, to_host
+from _util import to_dev, to_host
 
 pytestmark = pytest.mark.gpu
 
