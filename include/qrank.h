@@ -112,7 +112,8 @@ qr_status qr_fm_count_work(const qr_fm* fm, const uint8_t* patterns, const uint3
 /* Gather ceiling ("null rank"): the same q stream, the same line-index
  * arithmetic and the same loads as qr_rank, no popcount and no superblock read;
  * out[k] = XOR of the loaded words.  mode 0: exactly the sectors qr_rank reads (32 B or
- * 64 B); mode 1: the full 64-B line always.  Device pointers only. */
+ * 64 B); mode 1: the full 64-B line always; mode 2: mode 0 plus qr_rank's superblock-word
+ * read (BiRank; on QuadRank mode 2 = mode 0).  Device pointers only. */
 qr_status qr_gather_ceiling(const qr_index* h, const uint64_t* q, uint64_t* out, uint64_t m, int mode, void* stream);
 
 /* ------------------------------------------------------------------ handles */
@@ -146,7 +147,8 @@ const char* qr_last_error(void);
 /* Process-wide launch-configuration knobs for measurement sweeps (results never depend on
  * them): "rank_k" (1, 2, 4 or 8 independent queries per thread per iteration),
  * "rank_blocks_per_sm" and "fm_blocks_per_sm" (256-thread CTAs per SM of the grid-stride
- * rank / FM kernels, 1..64), "stage_chunk" (queries per chunk of the staged host path).
+ * rank / FM kernels, 1..64), "stage_chunk" (queries per chunk of the staged host path),
+ * "l2_fetch_granularity" (cudaLimitMaxL2FetchGranularity of the current device, bytes).
  * QR_EINVAL for an unknown key or out-of-range value. */
 qr_status qr_set_tuning(const char* key, int64_t value);
 

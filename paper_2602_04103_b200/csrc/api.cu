@@ -21,6 +21,8 @@ namespace qr {
 int g_rank_k = 4;               // independent queries per thread per iteration
 int g_rank_blocks_per_sm = 8;   // 256-thread CTAs per SM for the rank/gather kernels
 int g_fm_blocks_per_sm = 8;     // 256-thread CTAs per SM for the FM count kernel
+int g_rank_s_lane = 0;          // lane of a pair that loads the superblock word (measurement)
+int g_rank_pair = 1;            // 1: lane-pair kernels (one L2 request per query); 0: one lane per query
 uint64_t g_stage_chunk = 1ull << 24;   // queries per chunk on the staged host path
 
 static thread_local char t_err[512] = "";
@@ -242,9 +244,19 @@ QR_EXPORT qr_status qr_set_tuning(const char* key, int64_t value) {
   } else if (!strcmp(key, "rank_blocks_per_sm")) {
     if (value < 1 || value > 64) return fail(QR_EINVAL, "rank_blocks_per_sm out of range");
     g_rank_blocks_per_sm = (int)value;
+  } else if (!strcmp(key, "rank_pair")) {
+    if (value != 0 && value != 1) return fail(QR_EINVAL, "rank_pair must be 0 or 1");
+    g_rank_pair = (int)value;
+  } else if (!strcmp(key, "rank_s_lane")) {
+    if (value != 0 && value != 1) return fail(QR_EINVAL, "rank_s_lane must be 0 or 1");
+    g_rank_s_lane = (int)value;
   } else if (!strcmp(key, "fm_blocks_per_sm")) {
     if (value < 1 || value > 64) return fail(QR_EINVAL, "fm_blocks_per_sm out of range");
     g_fm_blocks_per_sm = (int)value;
+  } else if (!strcmp(key, "l2_fetch_granularity")) {
+    // cudaLimitMaxL2FetchGranularity of the current device (0..128 B; a hint to the L2)
+    cudaError_t e = cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)value);
+    if (e) return cuda_fail(e, "qr_set_tuning l2_fetch_granularity");
   } else if (!strcmp(key, "stage_chunk")) {
     if (value < 1024) return fail(QR_EINVAL, "stage_chunk too small");
     g_stage_chunk = (uint64_t)value;
@@ -348,7 +360,7 @@ QR_EXPORT qr_status qr_rank_all4(const qr_index* h, const uint64_t* q, uint64_t*
 QR_EXPORT qr_status qr_gather_ceiling(const qr_index* h, const uint64_t* q, uint64_t* out, uint64_t m, int mode,
                                       void* stream) {
   if (!h || (m && (!q || !out))) return fail(QR_EINVAL, "qr_gather_ceiling: null pointer");
-  if (mode != 0 && mode != 1) return fail(QR_EINVAL, "qr_gather_ceiling: mode must be 0 or 1");
+  if (mode < 0 || mode > 2) return fail(QR_EINVAL, "qr_gather_ceiling: mode must be 0, 1 or 2");
   DeviceGuard dg(h->device);
   if (m && classify({q, out}, h->device) != 1) return fail(QR_EINVAL, "qr_gather_ceiling: device pointers only");
   cudaError_t e = launch_gather(h, q, out, m, mode, (cudaStream_t)stream);

@@ -98,30 +98,48 @@ __device__ __forceinline__ uint64_t bi_line_of(uint64_t q) {
   return q / BI_B;
 }
 
-// K independent queries per thread per iteration: all K line gathers are issued before any
-// popcount, so each thread keeps K (or 2K) sectors in flight; the grid is a multiple of the
-// SM count and grid-strides over the query array (coalesced q loads and out stores).
+// K independent queries per thread per group: all K line gathers are issued before any
+// popcount, and the next group's K query positions are loaded while those gathers are in
+// flight (software pipelining of the dependent q -> line chain), so a thread keeps K line
+// misses outstanding nearly all the time.  Grid = SM count x CTAs/SM, grid-stride over the
+// query array (coalesced q loads and out stores).
+template <int K, bool SMALLQ>
+__device__ __forceinline__ void bi_locate(const uint64_t (&qq)[K], uint64_t last_line, uint64_t (&jj)[K],
+                                          uint32_t (&pp)[K]) {
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    uint64_t j = bi_line_of<SMALLQ>(qq[k]);
+    j = j > last_line ? last_line : j;                   // q > n: memory-safe clamp
+    uint64_t p = 16 + qq[k] - j * BI_B;
+    pp[k] = p > 511 ? 511u : (uint32_t)p;
+    jj[k] = j;
+  }
+}
+
+template <int K>
+__device__ __forceinline__ void load_q_group(const uint64_t* __restrict__ q, uint64_t i0, uint64_t nthr, uint64_t m,
+                                             uint64_t (&qn)[K]) {
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    uint64_t idx = i0 + (uint64_t)k * nthr;
+    qn[k] = idx < m ? ld_stream_u64(q + idx) : 0;
+  }
+}
+
 template <int K, bool SMALLQ, bool HAS_C>
 __global__ void __launch_bounds__(256) k_bi_rank(const uint4* __restrict__ lines, const uint32_t* __restrict__ super,
                                                  const uint64_t* __restrict__ q, const uint8_t* __restrict__ cs,
                                                  uint64_t* __restrict__ out, uint64_t m, uint64_t last_line) {
   const uint64_t nthr = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t i0 = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i0 < m; i0 += nthr * K) {
+  uint64_t i0 = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  uint64_t qn[K];
+  load_q_group<K>(q, i0, nthr, m, qn);
+  for (; i0 < m; i0 += nthr * K) {
     uint64_t qq[K], jj[K];
     uint32_t pp[K];
 #pragma unroll
-    for (int k = 0; k < K; ++k) {
-      uint64_t idx = i0 + (uint64_t)k * nthr;
-      qq[k] = idx < m ? ld_stream_u64(q + idx) : 0;
-    }
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-      uint64_t j = bi_line_of<SMALLQ>(qq[k]);
-      j = j > last_line ? last_line : j;                 // q > n: memory-safe clamp
-      uint64_t p = 16 + qq[k] - j * BI_B;
-      pp[k] = p > 511 ? 511u : (uint32_t)p;
-      jj[k] = j;
-    }
+    for (int k = 0; k < K; ++k) qq[k] = qn[k];
+    bi_locate<K, SMALLQ>(qq, last_line, jj, pp);
     uint64_t a[K][4], b[K][4];
     uint32_t s[K];
 #pragma unroll
@@ -132,6 +150,7 @@ __global__ void __launch_bounds__(256) k_bi_rank(const uint4* __restrict__ lines
       if (pp[k] >= 256) ld_sector_na(ln + 2, b[k][0], b[k][1], b[k][2], b[k][3]);
       s[k] = __ldg(super + (jj[k] >> BI_SB_LOG));
     }
+    load_q_group<K>(q, i0 + nthr * K, nthr, m, qn);      // next group, overlapping the gathers
 #pragma unroll
     for (int k = 0; k < K; ++k) {
       uint64_t idx = i0 + (uint64_t)k * nthr;
@@ -155,25 +174,21 @@ __global__ void __launch_bounds__(256) k_bi_rank(const uint4* __restrict__ lines
   }
 }
 
-// Gather ceiling (G9): identical q stream, line arithmetic and sector loads; no popcount,
-// no superblock read.  MODE 0: the sectors rank reads; MODE 1: always the full line.
+// Gather ceiling (G9): identical q stream (same pipelining), line arithmetic and sector
+// loads; no popcount, no superblock read.  MODE 0: the sectors rank reads; MODE 1: the full line.
 template <int K, bool SMALLQ, int MODE>
 __global__ void __launch_bounds__(256) k_bi_gather(const uint4* __restrict__ lines, const uint64_t* __restrict__ q,
                                                    uint64_t* __restrict__ out, uint64_t m, uint64_t last_line) {
   const uint64_t nthr = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t i0 = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i0 < m; i0 += nthr * K) {
-    uint64_t jj[K];
+  uint64_t i0 = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  uint64_t qn[K];
+  load_q_group<K>(q, i0, nthr, m, qn);
+  for (; i0 < m; i0 += nthr * K) {
+    uint64_t qq[K], jj[K];
     uint32_t pp[K];
 #pragma unroll
-    for (int k = 0; k < K; ++k) {
-      uint64_t idx = i0 + (uint64_t)k * nthr;
-      uint64_t qv = idx < m ? ld_stream_u64(q + idx) : 0;
-      uint64_t j = bi_line_of<SMALLQ>(qv);
-      j = j > last_line ? last_line : j;
-      uint64_t p = 16 + qv - j * BI_B;
-      pp[k] = p > 511 ? 511u : (uint32_t)p;
-      jj[k] = j;
-    }
+    for (int k = 0; k < K; ++k) qq[k] = qn[k];
+    bi_locate<K, SMALLQ>(qq, last_line, jj, pp);
     uint64_t a[K][4], b[K][4];
 #pragma unroll
     for (int k = 0; k < K; ++k) {
@@ -182,6 +197,7 @@ __global__ void __launch_bounds__(256) k_bi_gather(const uint4* __restrict__ lin
       b[k][0] = b[k][1] = b[k][2] = b[k][3] = 0;
       if (MODE == 1 || pp[k] >= 256) ld_sector_na(ln + 2, b[k][0], b[k][1], b[k][2], b[k][3]);
     }
+    load_q_group<K>(q, i0 + nthr * K, nthr, m, qn);
 #pragma unroll
     for (int k = 0; k < K; ++k) {
       uint64_t idx = i0 + (uint64_t)k * nthr;
@@ -191,15 +207,125 @@ __global__ void __launch_bounds__(256) k_bi_gather(const uint4* __restrict__ lin
   }
 }
 
+// ---- lane-pair variants: one L2 request per query ---------------------------------------
+// Every random sector load is one L2 request, and on B200 the random-miss path saturates at
+// ~45 G requests/s whatever the request size (tools/gather_probe: 4 B to 32 B loads all run
+// at the same rate).  So the two sectors of a query are loaded by two lanes of the SAME warp
+// instruction (lane 2i: sector 0 with b_j and data bits [0,240); lane 2i+1: sector 1, only
+// when q lies right of the anchor): the L1 merges them into ONE request for the 64-B line
+// with a two-sector mask, i.e. 1 request per query instead of 1.52.  Each lane counts its own
+// half (Eq. 1's two cases are exactly the two sectors) and one shuffle adds the halves.
+// Loop bounds are warp-uniform so that the shuffle sees every lane.
+template <int K, bool SMALLQ, bool HAS_C, uint32_t S_LANE = 0>
+__global__ void __launch_bounds__(256) k_bi_rank2(const uint4* __restrict__ lines, const uint32_t* __restrict__ super,
+                                                  const uint64_t* __restrict__ q, const uint8_t* __restrict__ cs,
+                                                  uint64_t* __restrict__ out, uint64_t m, uint64_t last_line) {
+  const uint64_t npair = ((uint64_t)gridDim.x * blockDim.x) >> 1;
+  const uint32_t half = threadIdx.x & 1u;
+  const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  uint64_t i0 = tid >> 1;
+  uint64_t iw = (tid & ~31ull) >> 1;                      // first pair of this warp (uniform)
+  uint64_t qn[K];
+  load_q_group<K>(q, i0, npair, m, qn);
+  for (; iw < m; iw += npair * K, i0 += npair * K) {
+    uint64_t qq[K], jj[K];
+    uint32_t pp[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) qq[k] = qn[k];
+    bi_locate<K, SMALLQ>(qq, last_line, jj, pp);
+    uint64_t w[K][4];
+    uint32_t s[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      w[k][0] = w[k][1] = w[k][2] = w[k][3] = 0;
+      if (half == 0 || pp[k] >= 256) ld_sector_na(lines + 4 * jj[k] + 2 * half, w[k][0], w[k][1], w[k][2], w[k][3]);
+      s[k] = half == S_LANE ? __ldg(super + (jj[k] >> BI_SB_LOG)) : 0u;
+    }
+    load_q_group<K>(q, i0 + npair * K, npair, m, qn);
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const uint64_t idx = i0 + (uint64_t)k * npair;
+      const bool right = pp[k] >= 256;
+      const int x = (int)(pp[k] & 255u);
+      const bool mine = half ? right : !right;            // which case of Eq. 1 this lane counts
+      const uint64_t inv = half ? 0ull : ~0ull;           // lane 0: suffix [p,256); lane 1: prefix [256,p)
+      uint32_t cnt = 0;
+#pragma unroll
+      for (int t = 0; t < 4; ++t) cnt += __popcll(w[k][t] & (prefix_mask(x, t) ^ inv));
+      cnt = mine ? cnt : 0u;
+      // lane 0: b_j - (left count); lane 1: + (right count); 2^11 s from the lane that loaded it
+      uint64_t v = (half ? (uint64_t)cnt : (w[k][0] & 0xffffull) - cnt) + ((uint64_t)s[k] << BI_SHIFT);
+      v += __shfl_xor_sync(0xffffffffu, v, 1);
+      if (HAS_C) {
+        if (half == 0 && idx < m && cs[idx] == 0) v = qq[k] - v;
+      }
+      if (half == 0 && idx < m) st_stream_u64(out + idx, v);
+    }
+  }
+}
+
+// Gather ceiling with the same lane-pair loads (MODE 0: the sectors rank2 reads; MODE 1: both
+// sectors always; MODE 2: the sectors rank2 reads plus its superblock-word load).
+template <int K, bool SMALLQ, int MODE>
+__global__ void __launch_bounds__(256) k_bi_gather2(const uint4* __restrict__ lines, const uint32_t* __restrict__ super,
+                                                    const uint64_t* __restrict__ q, uint64_t* __restrict__ out, uint64_t m,
+                                                    uint64_t last_line) {
+  const uint64_t npair = ((uint64_t)gridDim.x * blockDim.x) >> 1;
+  const uint32_t half = threadIdx.x & 1u;
+  const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  uint64_t i0 = tid >> 1;
+  uint64_t iw = (tid & ~31ull) >> 1;
+  uint64_t qn[K];
+  load_q_group<K>(q, i0, npair, m, qn);
+  for (; iw < m; iw += npair * K, i0 += npair * K) {
+    uint64_t qq[K], jj[K];
+    uint32_t pp[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) qq[k] = qn[k];
+    bi_locate<K, SMALLQ>(qq, last_line, jj, pp);
+    uint64_t w[K][4];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      w[k][0] = w[k][1] = w[k][2] = w[k][3] = 0;
+      if (MODE == 1 || half == 0 || pp[k] >= 256)
+        ld_sector_na(lines + 4 * jj[k] + 2 * half, w[k][0], w[k][1], w[k][2], w[k][3]);
+      if (MODE == 2 && half == 0) w[k][0] ^= __ldg(super + (jj[k] >> BI_SB_LOG));
+    }
+    load_q_group<K>(q, i0 + npair * K, npair, m, qn);
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const uint64_t idx = i0 + (uint64_t)k * npair;
+      uint64_t v = w[k][0] ^ w[k][1] ^ w[k][2] ^ w[k][3];
+      v ^= __shfl_xor_sync(0xffffffffu, v, 1);
+      if (half == 0 && idx < m) st_stream_u64(out + idx, v);
+    }
+  }
+}
+
 extern int g_rank_k;              // tuning knobs (api.cu)
 extern int g_rank_blocks_per_sm;
+extern int g_rank_pair;
+extern int g_rank_s_lane;
 
 template <int K>
 static cudaError_t bi_rank_k(const qr_index* h, const uint64_t* q, const uint8_t* c, uint64_t* out, uint64_t m,
                              cudaStream_t st) {
   const bool small = h->n < (1ull << 36);
-  unsigned g = grid_stride_blocks((m + K - 1) / K, 256, h->sm_count, g_rank_blocks_per_sm);
+  const uint64_t per_thread = g_rank_pair ? K : 2 * K;   // pair kernels: 2 threads per query
+  unsigned g = grid_stride_blocks((2 * m + per_thread - 1) / per_thread, 256, h->sm_count, g_rank_blocks_per_sm);
   const uint64_t last = h->n_lines - 1;
+  if (g_rank_pair) {
+    const bool s1 = g_rank_s_lane == 1;
+    if (small) {
+      if (c) k_bi_rank2<K, true, true><<<g, 256, 0, st>>>(h->lines, h->super, q, c, out, m, last);
+      else if (s1) k_bi_rank2<K, true, false, 1><<<g, 256, 0, st>>>(h->lines, h->super, q, c, out, m, last);
+      else   k_bi_rank2<K, true, false><<<g, 256, 0, st>>>(h->lines, h->super, q, c, out, m, last);
+    } else {
+      if (c) k_bi_rank2<K, false, true><<<g, 256, 0, st>>>(h->lines, h->super, q, c, out, m, last);
+      else   k_bi_rank2<K, false, false><<<g, 256, 0, st>>>(h->lines, h->super, q, c, out, m, last);
+    }
+    return cudaGetLastError();
+  }
   if (small) {
     if (c) k_bi_rank<K, true, true><<<g, 256, 0, st>>>(h->lines, h->super, q, c, out, m, last);
     else   k_bi_rank<K, true, false><<<g, 256, 0, st>>>(h->lines, h->super, q, c, out, m, last);
@@ -225,8 +351,22 @@ template <int K>
 static cudaError_t bi_gather_k(const qr_index* h, const uint64_t* q, uint64_t* out, uint64_t m, int mode,
                                cudaStream_t st) {
   const bool small = h->n < (1ull << 36);
-  unsigned g = grid_stride_blocks((m + K - 1) / K, 256, h->sm_count, g_rank_blocks_per_sm);
+  const uint64_t per_thread = g_rank_pair ? K : 2 * K;
+  unsigned g = grid_stride_blocks((2 * m + per_thread - 1) / per_thread, 256, h->sm_count, g_rank_blocks_per_sm);
   const uint64_t last = h->n_lines - 1;
+  if (g_rank_pair) {
+    if (small) {
+      if (mode == 2)      k_bi_gather2<K, true, 2><<<g, 256, 0, st>>>(h->lines, h->super, q, out, m, last);
+      else if (mode == 1) k_bi_gather2<K, true, 1><<<g, 256, 0, st>>>(h->lines, h->super, q, out, m, last);
+      else                k_bi_gather2<K, true, 0><<<g, 256, 0, st>>>(h->lines, h->super, q, out, m, last);
+    } else {
+      if (mode == 2)      k_bi_gather2<K, false, 2><<<g, 256, 0, st>>>(h->lines, h->super, q, out, m, last);
+      else if (mode == 1) k_bi_gather2<K, false, 1><<<g, 256, 0, st>>>(h->lines, h->super, q, out, m, last);
+      else                k_bi_gather2<K, false, 0><<<g, 256, 0, st>>>(h->lines, h->super, q, out, m, last);
+    }
+    return cudaGetLastError();
+  }
+  if (mode == 2) mode = 0;
   if (small) {
     if (mode) k_bi_gather<K, true, 1><<<g, 256, 0, st>>>(h->lines, q, out, m, last);
     else      k_bi_gather<K, true, 0><<<g, 256, 0, st>>>(h->lines, q, out, m, last);

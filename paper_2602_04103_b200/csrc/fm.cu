@@ -190,26 +190,39 @@ __global__ void k_sym_counts(const uint64_t* __restrict__ text, uint64_t n, unsi
 
 // ------------------------------------------------------------------ rank inside the FM loop
 
-// Occ for lo and hi of one backward step, both gathers issued before either is used.
-// Lines are read with L1 allocation: lo and hi often share a line.
-__device__ __forceinline__ void fm_step(const FmParams& F, uint32_t c, uint64_t& lo, uint64_t& hi, uint32_t& lines) {
-  uint64_t jl = (uint64_t)((uint32_t)(lo >> 5) / 7u);       // N < 2^32: floor(lo/224)
-  uint64_t jh = (uint64_t)((uint32_t)(hi >> 5) / 7u);
-  jl = jl > F.last_line ? F.last_line : jl;
-  jh = jh > F.last_line ? F.last_line : jh;
-  const uint32_t pl = (uint32_t)(32 + lo - jl * QD_B), ph = (uint32_t)(32 + hi - jh * QD_B);
-  uint64_t al[4], bl[4] = {0, 0, 0, 0}, ah[4], bh[4] = {0, 0, 0, 0};
-  const uint4* Ll = F.lines + 4 * jl;
-  const uint4* Lh = F.lines + 4 * jh;
+// Occ for lo and hi of one backward step, all gathers issued before any is used.  lo and hi
+// often share a line ("cache lines are automatically reused"); then the line's
+// sectors and the superblock word are loaded once and reused from registers, which halves the
+// L1 wavefronts of a step when the structure is L2-resident.  N < 2^32: u32 arithmetic.
+__device__ __forceinline__ void fm_step(const FmParams& F, uint32_t c, uint32_t& lo, uint32_t& hi, uint32_t& lines) {
+  uint32_t jl = (lo >> 5) / 7u;                                  // floor(lo/224)
+  uint32_t jh = (hi >> 5) / 7u;
+  jl = jl > (uint32_t)F.last_line ? (uint32_t)F.last_line : jl;
+  jh = jh > (uint32_t)F.last_line ? (uint32_t)F.last_line : jh;
+  const uint32_t pl = 32u + lo - jl * (uint32_t)QD_B, ph = 32u + hi - jh * (uint32_t)QD_B;
+  const bool same = jl == jh;
+  const bool rl_ = pl >= 128, rh_ = ph >= 128;
+  uint64_t al[4], bl[4] = {0, 0, 0, 0}, ah[4] = {0, 0, 0, 0}, bh[4] = {0, 0, 0, 0};
+  const uint4* Ll = F.lines + 4 * (uint64_t)jl;
+  const uint4* Lh = F.lines + 4 * (uint64_t)jh;
   ld_sector(Ll, al[0], al[1], al[2], al[3]);
-  if (pl >= 128) ld_sector(Ll + 2, bl[0], bl[1], bl[2], bl[3]);
-  ld_sector(Lh, ah[0], ah[1], ah[2], ah[3]);
-  if (ph >= 128) ld_sector(Lh + 2, bh[0], bh[1], bh[2], bh[3]);
+  if (rl_) ld_sector(Ll + 2, bl[0], bl[1], bl[2], bl[3]);
+  if (!same) ld_sector(Lh, ah[0], ah[1], ah[2], ah[3]);
+  if (rh_ && !(same && rl_)) ld_sector(Lh + 2, bh[0], bh[1], bh[2], bh[3]);
   const uint32_t sl = __ldg(F.super + 4 * (jl >> QD_SB_LOG) + c);
-  const uint32_t sh = __ldg(F.super + 4 * (jh >> QD_SB_LOG) + c);
-  lines = (jl != jh) ? 2u : 1u;
+  const bool same_sb = (jl >> QD_SB_LOG) == (jh >> QD_SB_LOG);
+  uint32_t sh = same_sb ? sl : __ldg(F.super + 4 * (jh >> QD_SB_LOG) + c);
+  if (same) {
+#pragma unroll
+    for (int t = 0; t < 4; ++t) ah[t] = al[t];
+    if (rl_) {
+#pragma unroll
+      for (int t = 0; t < 4; ++t) bh[t] = bl[t];
+    }
+  }
+  lines = same ? 1u : 2u;
   const uint64_t cl = 0ull - (uint64_t)(c & 1u), ch = 0ull - (uint64_t)(c >> 1);
-  auto rank1 = [&](const uint64_t* a, const uint64_t* b, uint32_t p, uint32_t s) -> uint64_t {
+  auto rank1 = [&](const uint64_t* a, const uint64_t* b, uint32_t p, uint32_t s) -> uint32_t {
     const bool right = p >= 128;
     const int x = (int)(p & 127u);
     const uint64_t inv = right ? 0ull : ~0ull;
@@ -217,12 +230,12 @@ __device__ __forceinline__ void fm_step(const FmParams& F, uint32_t c, uint64_t&
     uint32_t cnt = __popcll((w[0] ^ cl) & (w[1] ^ ch) & (prefix_mask(x, 0) ^ inv)) +
                    __popcll((w[2] ^ cl) & (w[3] ^ ch) & (prefix_mask(x, 1) ^ inv));
     uint64_t dw = (c & 2u) ? a[1] : a[0];
-    uint64_t base = ((uint64_t)s << QD_SHIFT) + ((dw >> (16 * (c & 1u))) & 0xffffull);
+    uint32_t base = (s << QD_SHIFT) + (uint32_t)((dw >> (16 * (c & 1u))) & 0xffffull);
     return right ? base + cnt : base - cnt;
   };
-  uint64_t rl = rank1(al, bl, pl, sl), rh = rank1(ah, bh, ph, sh);
+  uint32_t rl = rank1(al, bl, pl, sl), rh = rank1(ah, bh, ph, sh);
   // '$' is stored as A at row spos: Occ(A, x) = rank(x, A) - [x > spos]
-  if (c == 0) { rl -= (lo > F.spos); rh -= (hi > F.spos); }
+  if (c == 0) { rl -= (lo > (uint32_t)F.spos); rh -= (hi > (uint32_t)F.spos); }
   lo = F.C[c] + rl;
   hi = F.C[c] + rh;
 }
@@ -230,50 +243,71 @@ __device__ __forceinline__ void fm_step(const FmParams& F, uint32_t c, uint64_t&
 __global__ void k_kmer_table(FmParams F, uint2* __restrict__ table) {
   uint32_t key = blockIdx.x * blockDim.x + threadIdx.x;
   if (key >= 65536u) return;
-  uint64_t lo = 0, hi = F.N;
+  uint32_t lo = 0, hi = (uint32_t)F.N;
   uint32_t dummy;
   for (int t = 0; t < 8 && lo < hi; ++t) fm_step(F, (key >> (2 * t)) & 3u, lo, hi, dummy);   // last char first
   if (lo >= hi) lo = hi = 0;
-  table[key] = make_uint2((uint32_t)lo, (uint32_t)hi);
+  table[key] = make_uint2(lo, hi);
 }
 
+// Pattern symbols are read through an 8-byte window held in a register (one aligned u64
+// load per 8 steps instead of one byte load per step: a warp's 32 lanes read 32 different
+// patterns, so every load instruction costs 32 L1 wavefronts).
+struct PatWindow {
+  const uint8_t* base;
+  uint64_t word;
+  int64_t wk;        // index (relative to base's aligned start) of the cached word, -1 if none
+  uint32_t mis;      // base misalignment in bytes
+  __device__ __forceinline__ void reset(const uint8_t* P) {
+    mis = (uint32_t)((uintptr_t)P & 7u);
+    base = P - mis;
+    wk = -1;
+  }
+  __device__ __forceinline__ uint32_t at(int64_t k) {
+    const int64_t a = k + mis;
+    const int64_t w = a >> 3;
+    if (w != wk) { word = __ldg(reinterpret_cast<const unsigned long long*>(base) + w); wk = w; }
+    return (uint32_t)(word >> (8 * (a & 7))) & 3u;
+  }
+};
+
 template <bool FIXED, bool WORK>
-__global__ void __launch_bounds__(256) k_fm_count(FmParams F, const uint8_t* __restrict__ pat,
+__global__ void __launch_bounds__(256, 4) k_fm_count(FmParams F, const uint8_t* __restrict__ pat,
                                                   const uint64_t* __restrict__ offs, const uint32_t* __restrict__ lens,
                                                   uint32_t fixed_len, uint32_t* __restrict__ out, uint64_t m,
                                                   unsigned long long* __restrict__ work) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   uint64_t pi = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-  uint64_t lo = 0, hi = 0;
+  uint32_t lo = 0, hi = 0;
   int64_t k = -1;
-  const uint8_t* P = nullptr;
+  PatWindow P;
   bool have = false;
   uint64_t n_steps = 0, n_lines = 0;
   for (;;) {
     if (!have) {
       if (pi >= m) break;
       const uint32_t len = FIXED ? fixed_len : lens[pi];
-      P = pat + (FIXED ? pi * (uint64_t)fixed_len : offs[pi]);
+      P.reset(pat + (FIXED ? pi * (uint64_t)fixed_len : offs[pi]));
       if (len >= 8) {                                    // seed from the 8-mer table
         uint32_t key = 0;
 #pragma unroll
-        for (int t = 0; t < 8; ++t) key |= ((uint32_t)__ldg(P + len - 1 - t) & 3u) << (2 * t);
+        for (int t = 0; t < 8; ++t) key |= P.at((int64_t)len - 8 + t) << (2 * (7 - t));
         uint2 iv = __ldg(F.kmer + key);
         lo = iv.x; hi = iv.y;
         k = (int64_t)len - 9;
       } else {
-        lo = 0; hi = F.N;
+        lo = 0; hi = (uint32_t)F.N;
         k = (int64_t)len - 1;
       }
       have = true;
     }
     if (k < 0 || lo >= hi) {
-      out[pi] = lo < hi ? (uint32_t)(hi - lo) : 0u;
+      out[pi] = lo < hi ? hi - lo : 0u;
       pi += stride;
       have = false;
       continue;
     }
-    const uint32_t c = (uint32_t)__ldg(P + k) & 3u;
+    const uint32_t c = P.at(k);
     uint32_t nl;
     fm_step(F, c, lo, hi, nl);
     --k;

@@ -83,22 +83,31 @@ inline unsigned grid_stride_blocks(uint64_t work_items, unsigned threads, int sm
 }
 
 // ---- device helpers ----
-// 256-bit gather of one 32-B sector (LDG.E.256 on sm_100a), not allocated in L1.  Deliberately
-// not .nc: ptxas may sink .nc loads below later uses (it did, serialising the K queries of a
-// thread); a coherent load cannot move past the stores that follow the gathers.
+// 256-bit gather of one 32-B sector (LDG.E.256 on sm_100a), not allocated in L1, with the
+// L2 fill limited to the 64-B line that holds it (.L2::64B: without it every random miss
+// fills a whole 128-B L2 line — 123 B of DRAM per load measured by ncu, tools/gather_probe).
+// Deliberately not .nc: ptxas may sink .nc loads below later uses (it did, serialising the K
+// queries of a thread); a coherent load cannot move past the stores that follow the gathers.
 __device__ __forceinline__ void ld_sector_na(const void* p, uint64_t& w0, uint64_t& w1, uint64_t& w2, uint64_t& w3) {
-  asm volatile("ld.global.L1::no_allocate.v4.u64 {%0,%1,%2,%3}, [%4];"
+  asm volatile("ld.global.L1::no_allocate.L2::64B.v4.u64 {%0,%1,%2,%3}, [%4];"
                : "=l"(w0), "=l"(w1), "=l"(w2), "=l"(w3)
                : "l"(p));
 }
-// 256-bit read-only load that may allocate in L1 (FM: lo and hi often share a line).
+// Same, allocating in L1 (FM: lo and hi of a step, and consecutive steps, often share a line).
 __device__ __forceinline__ void ld_sector(const void* p, uint64_t& w0, uint64_t& w1, uint64_t& w2, uint64_t& w3) {
-  asm volatile("ld.global.v4.u64 {%0,%1,%2,%3}, [%4];" : "=l"(w0), "=l"(w1), "=l"(w2), "=l"(w3) : "l"(p));
+  asm volatile("ld.global.L2::64B.v4.u64 {%0,%1,%2,%3}, [%4];" : "=l"(w0), "=l"(w1), "=l"(w2), "=l"(w3) : "l"(p));
 }
-// streaming loads/stores of the query stream / outputs (read once, write once)
+// Query-stream loads (coalesced, read once).  Coherent + volatile so that the software
+// prefetch of the next group's queries stays where it is written (issued while the current
+// group's gathers are in flight) instead of being sunk to its use.
 __device__ __forceinline__ uint64_t ld_stream_u64(const uint64_t* p) {
   uint64_t v;
-  asm volatile("ld.global.nc.L1::no_allocate.u64 %0, [%1];" : "=l"(v) : "l"(p));
+  asm volatile("ld.global.L1::no_allocate.u64 %0, [%1];" : "=l"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ uint32_t ld_stream_u8(const uint8_t* p) {
+  uint16_t v;
+  asm volatile("ld.global.L1::no_allocate.u8 %0, [%1];" : "=h"(v) : "l"(p));
   return v;
 }
 __device__ __forceinline__ void st_stream_u64(uint64_t* p, uint64_t v) {

@@ -152,27 +152,47 @@ __device__ __forceinline__ uint32_t qd_count(const uint64_t w[4], uint32_t c, in
 }
 
 template <int K, bool SMALLQ>
+__device__ __forceinline__ void qd_locate(const uint64_t (&qq)[K], uint64_t last_line, uint64_t (&jj)[K],
+                                          uint32_t (&pp)[K]) {
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    uint64_t j = qd_line_of<SMALLQ>(qq[k]);
+    j = j > last_line ? last_line : j;                   // q > n: memory-safe clamp
+    uint64_t p = 32 + qq[k] - j * QD_B;
+    pp[k] = p > 255 ? 255u : (uint32_t)p;
+    jj[k] = j;
+  }
+}
+
+// next group's query positions (and symbols), loaded while the current gathers are in flight
+template <int K, bool WITH_C>
+__device__ __forceinline__ void qd_load_group(const uint64_t* __restrict__ q, const uint8_t* __restrict__ cs,
+                                              uint64_t i0, uint64_t nthr, uint64_t m, uint64_t (&qn)[K],
+                                              uint32_t (&cn)[K]) {
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    uint64_t idx = i0 + (uint64_t)k * nthr;
+    qn[k] = idx < m ? ld_stream_u64(q + idx) : 0;
+    if (WITH_C) cn[k] = idx < m ? ld_stream_u8(cs + idx) & 3u : 0u;
+  }
+}
+
+// Same structure as k_bi_rank (K gathers in flight per thread, next group's (q, c) prefetched).
+template <int K, bool SMALLQ>
 __global__ void __launch_bounds__(256) k_qd_rank(const uint4* __restrict__ lines, const uint32_t* __restrict__ super,
                                                  const uint64_t* __restrict__ q, const uint8_t* __restrict__ cs,
                                                  uint64_t* __restrict__ out, uint64_t m, uint64_t last_line) {
   const uint64_t nthr = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t i0 = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i0 < m; i0 += nthr * K) {
+  uint64_t i0 = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  uint64_t qn[K];
+  uint32_t cn[K];
+  qd_load_group<K, true>(q, cs, i0, nthr, m, qn, cn);
+  for (; i0 < m; i0 += nthr * K) {
     uint64_t qq[K], jj[K];
     uint32_t pp[K], cc[K];
 #pragma unroll
-    for (int k = 0; k < K; ++k) {
-      uint64_t idx = i0 + (uint64_t)k * nthr;
-      qq[k] = idx < m ? ld_stream_u64(q + idx) : 0;
-      cc[k] = idx < m ? (uint32_t)__ldg(cs + idx) & 3u : 0u;
-    }
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-      uint64_t j = qd_line_of<SMALLQ>(qq[k]);
-      j = j > last_line ? last_line : j;
-      uint64_t p = 32 + qq[k] - j * QD_B;
-      pp[k] = p > 255 ? 255u : (uint32_t)p;
-      jj[k] = j;
-    }
+    for (int k = 0; k < K; ++k) { qq[k] = qn[k]; cc[k] = cn[k]; }
+    qd_locate<K, SMALLQ>(qq, last_line, jj, pp);
     uint64_t a[K][4], b[K][4];
     uint32_t s[K];
 #pragma unroll
@@ -183,6 +203,7 @@ __global__ void __launch_bounds__(256) k_qd_rank(const uint4* __restrict__ lines
       if (pp[k] >= 128) ld_sector_na(ln + 2, b[k][0], b[k][1], b[k][2], b[k][3]);
       s[k] = __ldg(super + 4 * (jj[k] >> QD_SB_LOG) + cc[k]);
     }
+    qd_load_group<K, true>(q, cs, i0 + nthr * K, nthr, m, qn, cn);
 #pragma unroll
     for (int k = 0; k < K; ++k) {
       uint64_t idx = i0 + (uint64_t)k * nthr;
@@ -206,19 +227,16 @@ __global__ void __launch_bounds__(256) k_qd_all4(const uint4* __restrict__ lines
                                                  const uint64_t* __restrict__ q, uint64_t* __restrict__ out4,
                                                  uint64_t m, uint64_t last_line) {
   const uint64_t nthr = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t i0 = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i0 < m; i0 += nthr * K) {
+  uint64_t i0 = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  uint64_t qn[K];
+  uint32_t cn[K];
+  qd_load_group<K, false>(q, nullptr, i0, nthr, m, qn, cn);
+  for (; i0 < m; i0 += nthr * K) {
     uint64_t qq[K], jj[K];
     uint32_t pp[K];
 #pragma unroll
-    for (int k = 0; k < K; ++k) {
-      uint64_t idx = i0 + (uint64_t)k * nthr;
-      qq[k] = idx < m ? ld_stream_u64(q + idx) : 0;
-      uint64_t j = qd_line_of<SMALLQ>(qq[k]);
-      j = j > last_line ? last_line : j;
-      uint64_t p = 32 + qq[k] - j * QD_B;
-      pp[k] = p > 255 ? 255u : (uint32_t)p;
-      jj[k] = j;
-    }
+    for (int k = 0; k < K; ++k) qq[k] = qn[k];
+    qd_locate<K, SMALLQ>(qq, last_line, jj, pp);
     uint64_t a[K][4], b[K][4];
     uint4 s[K];
 #pragma unroll
@@ -229,6 +247,7 @@ __global__ void __launch_bounds__(256) k_qd_all4(const uint4* __restrict__ lines
       if (pp[k] >= 128) ld_sector_na(ln + 2, b[k][0], b[k][1], b[k][2], b[k][3]);
       s[k] = __ldg(reinterpret_cast<const uint4*>(super) + (jj[k] >> QD_SB_LOG));
     }
+    qd_load_group<K, false>(q, nullptr, i0 + nthr * K, nthr, m, qn, cn);
 #pragma unroll
     for (int k = 0; k < K; ++k) {
       uint64_t idx = i0 + (uint64_t)k * nthr;
@@ -265,19 +284,16 @@ template <int K, bool SMALLQ, int MODE>
 __global__ void __launch_bounds__(256) k_qd_gather(const uint4* __restrict__ lines, const uint64_t* __restrict__ q,
                                                    uint64_t* __restrict__ out, uint64_t m, uint64_t last_line) {
   const uint64_t nthr = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t i0 = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i0 < m; i0 += nthr * K) {
-    uint64_t jj[K];
+  uint64_t i0 = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  uint64_t qn[K];
+  uint32_t cn[K];
+  qd_load_group<K, false>(q, nullptr, i0, nthr, m, qn, cn);
+  for (; i0 < m; i0 += nthr * K) {
+    uint64_t qq[K], jj[K];
     uint32_t pp[K];
 #pragma unroll
-    for (int k = 0; k < K; ++k) {
-      uint64_t idx = i0 + (uint64_t)k * nthr;
-      uint64_t qv = idx < m ? ld_stream_u64(q + idx) : 0;
-      uint64_t j = qd_line_of<SMALLQ>(qv);
-      j = j > last_line ? last_line : j;
-      uint64_t p = 32 + qv - j * QD_B;
-      pp[k] = p > 255 ? 255u : (uint32_t)p;
-      jj[k] = j;
-    }
+    for (int k = 0; k < K; ++k) qq[k] = qn[k];
+    qd_locate<K, SMALLQ>(qq, last_line, jj, pp);
     uint64_t a[K][4], b[K][4];
 #pragma unroll
     for (int k = 0; k < K; ++k) {
@@ -286,6 +302,7 @@ __global__ void __launch_bounds__(256) k_qd_gather(const uint4* __restrict__ lin
       b[k][0] = b[k][1] = b[k][2] = b[k][3] = 0;
       if (MODE == 1 || pp[k] >= 128) ld_sector_na(ln + 2, b[k][0], b[k][1], b[k][2], b[k][3]);
     }
+    qd_load_group<K, false>(q, nullptr, i0 + nthr * K, nthr, m, qn, cn);
 #pragma unroll
     for (int k = 0; k < K; ++k) {
       uint64_t idx = i0 + (uint64_t)k * nthr;
@@ -295,32 +312,207 @@ __global__ void __launch_bounds__(256) k_qd_gather(const uint4* __restrict__ lin
   }
 }
 
+// ---- lane-pair variants: one L2 request per query (see k_bi_rank2 in birank.cu) ------------
+// lane 2i loads sector 0 (deltas + data chars [0,96)), lane 2i+1 loads sector 1 (data chars
+// [96,224)) only for queries right of the anchor; both loads are in the same warp instruction,
+// so the L1 sends one request per 64-B line.  Each lane counts its own case of Listing 1.
+template <int K, bool SMALLQ>
+__global__ void __launch_bounds__(256) k_qd_rank2(const uint4* __restrict__ lines, const uint32_t* __restrict__ super,
+                                                  const uint64_t* __restrict__ q, const uint8_t* __restrict__ cs,
+                                                  uint64_t* __restrict__ out, uint64_t m, uint64_t last_line) {
+  const uint64_t npair = ((uint64_t)gridDim.x * blockDim.x) >> 1;
+  const uint32_t half = threadIdx.x & 1u;
+  const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  uint64_t i0 = tid >> 1;
+  uint64_t iw = (tid & ~31ull) >> 1;
+  uint64_t qn[K];
+  uint32_t cn[K];
+  qd_load_group<K, true>(q, cs, i0, npair, m, qn, cn);
+  for (; iw < m; iw += npair * K, i0 += npair * K) {
+    uint64_t qq[K], jj[K];
+    uint32_t pp[K], cc[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) { qq[k] = qn[k]; cc[k] = cn[k]; }
+    qd_locate<K, SMALLQ>(qq, last_line, jj, pp);
+    uint64_t w[K][4];
+    uint32_t s[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      w[k][0] = w[k][1] = w[k][2] = w[k][3] = 0;
+      if (half == 0 || pp[k] >= 128) ld_sector_na(lines + 4 * jj[k] + 2 * half, w[k][0], w[k][1], w[k][2], w[k][3]);
+      s[k] = half == 0 ? __ldg(super + 4 * (jj[k] >> QD_SB_LOG) + cc[k]) : 0u;
+    }
+    qd_load_group<K, true>(q, cs, i0 + npair * K, npair, m, qn, cn);
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const uint64_t idx = i0 + (uint64_t)k * npair;
+      const bool right = pp[k] >= 128;
+      const bool mine = half ? right : !right;
+      uint32_t cnt = qd_count(w[k], cc[k], (int)(pp[k] & 127u), half ? 0ull : ~0ull);
+      cnt = mine ? cnt : 0u;
+      uint64_t dw = (cc[k] & 2u) ? w[k][1] : w[k][0];
+      uint64_t delta = (dw >> (16 * (cc[k] & 1u))) & 0xffffull;        // u16 slot c + (c & 2)
+      uint64_t v = half ? (uint64_t)cnt : ((uint64_t)s[k] << QD_SHIFT) + delta - cnt;
+      v += __shfl_xor_sync(0xffffffffu, v, 1);
+      if (half == 0 && idx < m) st_stream_u64(out + idx, v);
+    }
+  }
+}
+
+template <int K, bool SMALLQ>
+__global__ void __launch_bounds__(256) k_qd_all4_2(const uint4* __restrict__ lines, const uint32_t* __restrict__ super,
+                                                   const uint64_t* __restrict__ q, uint64_t* __restrict__ out4,
+                                                   uint64_t m, uint64_t last_line) {
+  const uint64_t npair = ((uint64_t)gridDim.x * blockDim.x) >> 1;
+  const uint32_t half = threadIdx.x & 1u;
+  const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  uint64_t i0 = tid >> 1;
+  uint64_t iw = (tid & ~31ull) >> 1;
+  uint64_t qn[K];
+  uint32_t cn[K];
+  qd_load_group<K, false>(q, nullptr, i0, npair, m, qn, cn);
+  for (; iw < m; iw += npair * K, i0 += npair * K) {
+    uint64_t qq[K], jj[K];
+    uint32_t pp[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) qq[k] = qn[k];
+    qd_locate<K, SMALLQ>(qq, last_line, jj, pp);
+    uint64_t w[K][4];
+    uint4 s[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      w[k][0] = w[k][1] = w[k][2] = w[k][3] = 0;
+      if (half == 0 || pp[k] >= 128) ld_sector_na(lines + 4 * jj[k] + 2 * half, w[k][0], w[k][1], w[k][2], w[k][3]);
+      s[k] = half == 0 ? __ldg(reinterpret_cast<const uint4*>(super) + (jj[k] >> QD_SB_LOG)) : make_uint4(0, 0, 0, 0);
+    }
+    qd_load_group<K, false>(q, nullptr, i0 + npair * K, npair, m, qn, cn);
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const uint64_t idx = i0 + (uint64_t)k * npair;
+      const bool right = pp[k] >= 128;
+      const int x = (int)(pp[k] & 127u);
+      const uint64_t inv = half ? 0ull : ~0ull;
+      uint32_t nl = 0, nh = 0, nt = 0;
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {
+        uint64_t msk = prefix_mask(x, t) ^ inv;
+        uint64_t l = ~w[k][2 * t] & msk, hh = ~w[k][2 * t + 1] & msk;   // planes store the negation
+        nl += __popcll(l);
+        nh += __popcll(hh);
+        nt += __popcll(l & hh);
+      }
+      const uint32_t len = half ? (uint32_t)x : 128u - (uint32_t)x;
+      // four counts <= 128 packed in 8-bit fields: A | C << 8 | G << 16 | T << 24
+      uint32_t packed = (len - nl - nh + nt) | ((nl - nt) << 8) | ((nh - nt) << 16) | (nt << 24);
+      uint32_t other = __shfl_xor_sync(0xffffffffu, packed, 1);
+      if (half == 0 && idx < m) {
+        const uint32_t cnt = right ? other : packed;
+        uint32_t sv[4] = {s[k].x, s[k].y, s[k].z, s[k].w};
+        uint64_t r[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          uint64_t dw = (c & 2) ? w[k][1] : w[k][0];
+          uint64_t delta = (dw >> (16 * (c & 1))) & 0xffffull;
+          uint64_t base = ((uint64_t)sv[c] << QD_SHIFT) + delta;
+          uint32_t cc = (cnt >> (8 * c)) & 0xffu;
+          r[c] = right ? base + cc : base - cc;
+        }
+        st_stream_v4u64(out4 + 4 * idx, r[0], r[1], r[2], r[3]);
+      }
+    }
+  }
+}
+
+template <int K, bool SMALLQ, int MODE>
+__global__ void __launch_bounds__(256) k_qd_gather2(const uint4* __restrict__ lines, const uint64_t* __restrict__ q,
+                                                    uint64_t* __restrict__ out, uint64_t m, uint64_t last_line) {
+  const uint64_t npair = ((uint64_t)gridDim.x * blockDim.x) >> 1;
+  const uint32_t half = threadIdx.x & 1u;
+  const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  uint64_t i0 = tid >> 1;
+  uint64_t iw = (tid & ~31ull) >> 1;
+  uint64_t qn[K];
+  uint32_t cn[K];
+  qd_load_group<K, false>(q, nullptr, i0, npair, m, qn, cn);
+  for (; iw < m; iw += npair * K, i0 += npair * K) {
+    uint64_t qq[K], jj[K];
+    uint32_t pp[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) qq[k] = qn[k];
+    qd_locate<K, SMALLQ>(qq, last_line, jj, pp);
+    uint64_t w[K][4];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      w[k][0] = w[k][1] = w[k][2] = w[k][3] = 0;
+      if (MODE == 1 || half == 0 || pp[k] >= 128)
+        ld_sector_na(lines + 4 * jj[k] + 2 * half, w[k][0], w[k][1], w[k][2], w[k][3]);
+    }
+    qd_load_group<K, false>(q, nullptr, i0 + npair * K, npair, m, qn, cn);
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const uint64_t idx = i0 + (uint64_t)k * npair;
+      uint64_t v = w[k][0] ^ w[k][1] ^ w[k][2] ^ w[k][3];
+      v ^= __shfl_xor_sync(0xffffffffu, v, 1);
+      if (half == 0 && idx < m) st_stream_u64(out + idx, v);
+    }
+  }
+}
+
 extern int g_rank_k;
 extern int g_rank_blocks_per_sm;
+extern int g_rank_pair;
 
+template <int K>
+static unsigned qd_grid(const qr_index* h, uint64_t m) {
+  const uint64_t per_thread = g_rank_pair ? K : 2 * K;
+  return grid_stride_blocks((2 * m + per_thread - 1) / per_thread, 256, h->sm_count, g_rank_blocks_per_sm);
+}
 template <int K>
 static cudaError_t qd_rank_k(const qr_index* h, const uint64_t* q, const uint8_t* c, uint64_t* out, uint64_t m,
                              cudaStream_t st) {
-  unsigned g = grid_stride_blocks((m + K - 1) / K, 256, h->sm_count, g_rank_blocks_per_sm);
+  unsigned g = qd_grid<K>(h, m);
   const uint64_t last = h->n_lines - 1;
-  if (h->n < (1ull << 37)) k_qd_rank<K, true><<<g, 256, 0, st>>>(h->lines, h->super, q, c, out, m, last);
-  else                      k_qd_rank<K, false><<<g, 256, 0, st>>>(h->lines, h->super, q, c, out, m, last);
+  const bool small = h->n < (1ull << 37);
+  if (g_rank_pair) {
+    if (small) k_qd_rank2<K, true><<<g, 256, 0, st>>>(h->lines, h->super, q, c, out, m, last);
+    else       k_qd_rank2<K, false><<<g, 256, 0, st>>>(h->lines, h->super, q, c, out, m, last);
+  } else {
+    if (small) k_qd_rank<K, true><<<g, 256, 0, st>>>(h->lines, h->super, q, c, out, m, last);
+    else       k_qd_rank<K, false><<<g, 256, 0, st>>>(h->lines, h->super, q, c, out, m, last);
+  }
   return cudaGetLastError();
 }
 template <int K>
 static cudaError_t qd_all4_k(const qr_index* h, const uint64_t* q, uint64_t* out4, uint64_t m, cudaStream_t st) {
-  unsigned g = grid_stride_blocks((m + K - 1) / K, 256, h->sm_count, g_rank_blocks_per_sm);
+  unsigned g = qd_grid<K>(h, m);
   const uint64_t last = h->n_lines - 1;
-  if (h->n < (1ull << 37)) k_qd_all4<K, true><<<g, 256, 0, st>>>(h->lines, h->super, q, out4, m, last);
-  else                      k_qd_all4<K, false><<<g, 256, 0, st>>>(h->lines, h->super, q, out4, m, last);
+  const bool small = h->n < (1ull << 37);
+  if (g_rank_pair) {
+    if (small) k_qd_all4_2<K, true><<<g, 256, 0, st>>>(h->lines, h->super, q, out4, m, last);
+    else       k_qd_all4_2<K, false><<<g, 256, 0, st>>>(h->lines, h->super, q, out4, m, last);
+  } else {
+    if (small) k_qd_all4<K, true><<<g, 256, 0, st>>>(h->lines, h->super, q, out4, m, last);
+    else       k_qd_all4<K, false><<<g, 256, 0, st>>>(h->lines, h->super, q, out4, m, last);
+  }
   return cudaGetLastError();
 }
 template <int K>
 static cudaError_t qd_gather_k(const qr_index* h, const uint64_t* q, uint64_t* out, uint64_t m, int mode,
                                cudaStream_t st) {
-  unsigned g = grid_stride_blocks((m + K - 1) / K, 256, h->sm_count, g_rank_blocks_per_sm);
+  unsigned g = qd_grid<K>(h, m);
   const uint64_t last = h->n_lines - 1;
   const bool small = h->n < (1ull << 37);
+  if (mode == 2) mode = 0;   // (superblock-inclusive ceiling: BiRank only)
+  if (g_rank_pair) {
+    if (small) {
+      if (mode) k_qd_gather2<K, true, 1><<<g, 256, 0, st>>>(h->lines, q, out, m, last);
+      else      k_qd_gather2<K, true, 0><<<g, 256, 0, st>>>(h->lines, q, out, m, last);
+    } else {
+      if (mode) k_qd_gather2<K, false, 1><<<g, 256, 0, st>>>(h->lines, q, out, m, last);
+      else      k_qd_gather2<K, false, 0><<<g, 256, 0, st>>>(h->lines, q, out, m, last);
+    }
+    return cudaGetLastError();
+  }
   if (small) {
     if (mode) k_qd_gather<K, true, 1><<<g, 256, 0, st>>>(h->lines, q, out, m, last);
     else      k_qd_gather<K, true, 0><<<g, 256, 0, st>>>(h->lines, q, out, m, last);

@@ -1,0 +1,56 @@
+"""Single-box multi-GPU driver pieces: replicate the structure, shard the
+queries/patterns, no data-path collective.
+
+Every query and pattern is independent, so rank r of W takes the
+contiguous global index range [r*M/W, (r+1)*M/W) and generates it locally from
+(seed, global index); the only collectives are the max of the per-rank kernel times and
+the sum of per-rank counters at the end (torch.distributed: NCCL on GPUs, gloo in tests).
+"""
+from __future__ import annotations
+
+
+def shard(total: int, world: int, rank: int) -> tuple[int, int]:
+    """(first global index, count) of rank's contiguous share of `total` items."""
+    if world < 1 or not (0 <= rank < world):
+        raise ValueError("bad world/rank")
+    lo = total * rank // world
+    hi = total * (rank + 1) // world
+    return lo, hi - lo
+
+
+def weak_shard(per_rank: int, rank: int) -> tuple[int, int]:
+    """Weak scaling: every rank keeps `per_rank` items; rank r owns [r*per_rank, (r+1)*per_rank)."""
+    return rank * per_rank, per_rank
+
+
+def reduce_max(x: float, dist=None, device=None) -> float:
+    """max over ranks of a per-rank time (the job time of a data-parallel step)."""
+    if dist is None or not dist.is_initialized() or dist.get_world_size() == 1:
+        return float(x)
+    import torch
+
+    t = torch.tensor([float(x)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def reduce_sum(x: int, dist=None, device=None) -> int:
+    if dist is None or not dist.is_initialized() or dist.get_world_size() == 1:
+        return int(x)
+    import torch
+
+    t = torch.tensor([int(x)], dtype=torch.int64, device=device)
+    dist.all_reduce(t)
+    return int(t.item())
+
+
+def throughput(units_all_ranks: int, max_ms: float) -> float:
+    """whole-job units per second: all ranks' units over the slowest rank's time."""
+    return units_all_ranks / (max_ms * 1e-3)
+
+
+def replicate(handle, device: int, stream=None):
+    """Copy a built BiRank/QuadRank handle to another GPU (peer copy over NVLink/NVSwitch)."""
+    from . import qr_clone_to_device
+
+    return qr_clone_to_device(handle, device, stream)

@@ -109,8 +109,9 @@ def test_birank_device_input_and_host_query_path(cuda):
     assert np.array_equal(op.numpy(), ref)
 
 
+@pytest.mark.parametrize("pair", [0, 1])
 @pytest.mark.parametrize("k", [1, 2, 4, 8])
-def test_birank_tuning_does_not_change_results(cuda, k):
+def test_birank_tuning_does_not_change_results(cuda, k, pair):
     torch = _torch()
     n = 7 * S + 5
     w = gen.bits(17, n)
@@ -118,19 +119,62 @@ def test_birank_tuning_does_not_change_results(cuda, k):
     q = np.concatenate([gen.queries(5, n, 200001), boundary_queries(n, B, S, 240)])
     dq = to_dev(q, cuda)
     out = torch.empty_like(dq)
+    c = (gen.queries(3, 1, q.size, with_c=True)[1] & 1).astype(np.uint8)
+    out2 = torch.empty_like(dq)
     qr.qr_set_tuning("rank_k", k)
     qr.qr_set_tuning("rank_blocks_per_sm", 1 + k)
+    qr.qr_set_tuning("rank_pair", pair)
     try:
         qr.qr_rank(h, dq, None, out)
+        qr.qr_rank(h, dq, to_dev(c, cuda), out2)
         torch.cuda.synchronize()
     finally:
         qr.qr_set_tuning("rank_k", 4)
         qr.qr_set_tuning("rank_blocks_per_sm", 8)
-    assert np.array_equal(to_host(out), oracle.BitsOracle(w, n).rank(q))
+        qr.qr_set_tuning("rank_pair", 1)
+    ora = oracle.BitsOracle(w, n)
+    assert np.array_equal(to_host(out), ora.rank(q))
+    assert np.array_equal(to_host(out2), ora.rank(q, c))
 
 
-def test_gather_ceiling_loads_the_same_sectors(cuda):
+@pytest.mark.parametrize("pair", [0, 1])
+@pytest.mark.parametrize("k", [1, 2, 8])
+def test_quadrank_tuning_does_not_change_results(cuda, k, pair):
     torch = _torch()
+    n = 3 * S4 + 777
+    w = gen.dna(19, n)
+    h = qr.qr_quadrank_build(w, n)
+    q, c = gen.queries(5, n, 100001, with_c=True)
+    q = np.concatenate([q, boundary_queries(n, B4, S4, 96)])
+    c = np.concatenate([c, (np.arange(q.size - c.size) % 4).astype(np.uint8)])
+    dq = to_dev(q, cuda)
+    out = torch.empty_like(dq)
+    o4 = torch.empty((q.size, 4), dtype=torch.uint64, device=cuda)
+    g = torch.empty_like(dq)
+    qr.qr_set_tuning("rank_k", k)
+    qr.qr_set_tuning("rank_blocks_per_sm", 2 + k)
+    qr.qr_set_tuning("rank_pair", pair)
+    try:
+        qr.qr_rank(h, dq, to_dev(c, cuda), out)
+        qr.qr_rank_all4(h, dq, o4)
+        qr.qr_gather_ceiling(h, dq, g, 1)
+        torch.cuda.synchronize()
+    finally:
+        qr.qr_set_tuning("rank_k", 4)
+        qr.qr_set_tuning("rank_blocks_per_sm", 8)
+        qr.qr_set_tuning("rank_pair", 1)
+    ora = oracle.DnaOracle(w, n)
+    assert np.array_equal(to_host(out), ora.rank(q, c))
+    assert np.array_equal(to_host(o4), ora.rank_all4(q))
+    lines, _ = qr.qr_export_layout(h)
+    u64 = lines.view(np.uint64).reshape(-1, 8)
+    assert np.array_equal(to_host(g), np.bitwise_xor.reduce(u64[(q // B4).astype(np.int64)], axis=1))
+
+
+@pytest.mark.parametrize("pair", [0, 1])
+def test_gather_ceiling_loads_the_same_sectors(cuda, pair):
+    torch = _torch()
+    qr.qr_set_tuning("rank_pair", pair)
     n = 4 * S + 77
     w = gen.bits(3, n)
     h = qr.qr_birank_build(w, n)
@@ -148,6 +192,7 @@ def test_gather_ceiling_loads_the_same_sectors(cuda):
         b = np.bitwise_xor.reduce(u64[j, 4:], axis=1)
         exp = a ^ np.where((p >= 256) | (mode == 1), b, 0).astype(np.uint64)
         assert np.array_equal(to_host(out), exp)
+    qr.qr_set_tuning("rank_pair", 1)
 
 
 # ------------------------------------------------------------------ QuadRank

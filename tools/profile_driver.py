@@ -1,0 +1,52 @@
+"""One launch of each hot kernel at the bench's configs, for ncu (--set full) captures."""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import torch  # noqa: E402
+
+import gen  # noqa: E402
+import paper_2602_04103_b200 as qr  # noqa: E402
+
+dev = torch.device("cuda:0")
+st = torch.cuda.current_stream()
+M = 10**9
+n = 1 << 34
+bits = torch.empty((n + 63) // 64, dtype=torch.uint64, device=dev)
+gen.bits_dev(2, n, 0.5, bits)
+h = qr.qr_birank_build(bits, n)
+del bits
+q = torch.empty(M, dtype=torch.uint64, device=dev)
+gen.queries_dev(2, n, M, q)
+out = torch.empty_like(q)
+qr.qr_rank(h, q, None, out, M, st)
+qr.qr_gather_ceiling(h, q, out, 0, M, st)
+qr.qr_gather_ceiling(h, q, out, 1, M, st)
+torch.cuda.synchronize()
+h.free()
+n = 1 << 32
+t = torch.empty((n + 31) // 32, dtype=torch.uint64, device=dev)
+gen.dna_dev(3, n, 0, t)
+h = qr.qr_quadrank_build(t, n)
+del t
+c = torch.empty(M, dtype=torch.uint8, device=dev)
+gen.queries_dev(3, n, M, q, c)
+qr.qr_rank(h, q, c, out, M, st)
+del out
+o4 = torch.empty((M, 4), dtype=torch.uint64, device=dev)
+qr.qr_rank_all4(h, q, o4, M, st)
+torch.cuda.synchronize()
+del o4, q, c
+h.free()
+n = 1 << 26
+t = torch.empty((n + 31) // 32 + 1, dtype=torch.uint64, device=dev)
+gen.dna_dev(4, n, 0, t)
+fm = qr.qr_fm_build(t, n)
+m = 10**7
+pats = torch.empty(m * 32, dtype=torch.uint8, device=dev)
+gen.patterns_dev(4, 0, m, 32, t, n, pats)
+o = torch.empty(m, dtype=torch.int32, device=dev)
+qr.qr_fm_count(fm, pats, None, 32, o, m, st)
+torch.cuda.synchronize()
+print("profile driver done")
