@@ -18,10 +18,10 @@
 namespace qr {
 
 // ---- tuning knobs (set through qr_set_tuning; defaults chosen from B200 measurements) ----
-int g_rank_k = 4;               // independent queries per thread per iteration
-int g_rank_blocks_per_sm = 8;   // 256-thread CTAs per SM for the rank/gather kernels
+int g_rank_k = 2;               // independent queries per lane (pair) per iteration
+int g_rank_blocks_per_sm = 64;  // 256-thread CTAs per SM of the grid (several waves)
 int g_fm_blocks_per_sm = 8;     // 256-thread CTAs per SM for the FM count kernel
-int g_rank_s_lane = 0;          // lane of a pair that loads the superblock word (measurement)
+int g_rank_s_lane = 1;          // lane of a pair that loads the superblock word
 int g_rank_pair = 1;            // 1: lane-pair kernels (one L2 request per query); 0: one lane per query
 uint64_t g_stage_chunk = 1ull << 24;   // queries per chunk on the staged host path
 

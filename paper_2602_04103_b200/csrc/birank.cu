@@ -216,7 +216,7 @@ __global__ void __launch_bounds__(256) k_bi_gather(const uint4* __restrict__ lin
 // with a two-sector mask, i.e. 1 request per query instead of 1.52.  Each lane counts its own
 // half (Eq. 1's two cases are exactly the two sectors) and one shuffle adds the halves.
 // Loop bounds are warp-uniform so that the shuffle sees every lane.
-template <int K, bool SMALLQ, bool HAS_C, uint32_t S_LANE = 0>
+template <int K, bool SMALLQ, bool HAS_C, uint32_t S_LANE = 1>
 __global__ void __launch_bounds__(256) k_bi_rank2(const uint4* __restrict__ lines, const uint32_t* __restrict__ super,
                                                   const uint64_t* __restrict__ q, const uint8_t* __restrict__ cs,
                                                   uint64_t* __restrict__ out, uint64_t m, uint64_t last_line) {
@@ -264,6 +264,8 @@ __global__ void __launch_bounds__(256) k_bi_rank2(const uint4* __restrict__ line
   }
 }
 
+// (S_LANE: the pair lane that loads the superblock word; lane 1 — idle for the 48% of queries
+// left of the anchor — measured 36.9 vs 35.6 Gq/s for lane 0 on configs[1], profiles/r01_s_probe.)
 // Gather ceiling with the same lane-pair loads (MODE 0: the sectors rank2 reads; MODE 1: both
 // sectors always; MODE 2: the sectors rank2 reads plus its superblock-word load).
 template <int K, bool SMALLQ, int MODE>
@@ -315,10 +317,10 @@ static cudaError_t bi_rank_k(const qr_index* h, const uint64_t* q, const uint8_t
   unsigned g = grid_stride_blocks((2 * m + per_thread - 1) / per_thread, 256, h->sm_count, g_rank_blocks_per_sm);
   const uint64_t last = h->n_lines - 1;
   if (g_rank_pair) {
-    const bool s1 = g_rank_s_lane == 1;
+    const bool s0 = g_rank_s_lane == 0;
     if (small) {
       if (c) k_bi_rank2<K, true, true><<<g, 256, 0, st>>>(h->lines, h->super, q, c, out, m, last);
-      else if (s1) k_bi_rank2<K, true, false, 1><<<g, 256, 0, st>>>(h->lines, h->super, q, c, out, m, last);
+      else if (s0) k_bi_rank2<K, true, false, 0><<<g, 256, 0, st>>>(h->lines, h->super, q, c, out, m, last);
       else   k_bi_rank2<K, true, false><<<g, 256, 0, st>>>(h->lines, h->super, q, c, out, m, last);
     } else {
       if (c) k_bi_rank2<K, false, true><<<g, 256, 0, st>>>(h->lines, h->super, q, c, out, m, last);

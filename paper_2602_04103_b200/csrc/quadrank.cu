@@ -316,7 +316,7 @@ __global__ void __launch_bounds__(256) k_qd_gather(const uint4* __restrict__ lin
 // lane 2i loads sector 0 (deltas + data chars [0,96)), lane 2i+1 loads sector 1 (data chars
 // [96,224)) only for queries right of the anchor; both loads are in the same warp instruction,
 // so the L1 sends one request per 64-B line.  Each lane counts its own case of Listing 1.
-template <int K, bool SMALLQ>
+template <int K, bool SMALLQ, uint32_t S_LANE = 1>
 __global__ void __launch_bounds__(256) k_qd_rank2(const uint4* __restrict__ lines, const uint32_t* __restrict__ super,
                                                   const uint64_t* __restrict__ q, const uint8_t* __restrict__ cs,
                                                   uint64_t* __restrict__ out, uint64_t m, uint64_t last_line) {
@@ -340,7 +340,7 @@ __global__ void __launch_bounds__(256) k_qd_rank2(const uint4* __restrict__ line
     for (int k = 0; k < K; ++k) {
       w[k][0] = w[k][1] = w[k][2] = w[k][3] = 0;
       if (half == 0 || pp[k] >= 128) ld_sector_na(lines + 4 * jj[k] + 2 * half, w[k][0], w[k][1], w[k][2], w[k][3]);
-      s[k] = half == 0 ? __ldg(super + 4 * (jj[k] >> QD_SB_LOG) + cc[k]) : 0u;
+      s[k] = half == S_LANE ? __ldg(super + 4 * (jj[k] >> QD_SB_LOG) + cc[k]) : 0u;
     }
     qd_load_group<K, true>(q, cs, i0 + npair * K, npair, m, qn, cn);
 #pragma unroll
@@ -352,7 +352,8 @@ __global__ void __launch_bounds__(256) k_qd_rank2(const uint4* __restrict__ line
       cnt = mine ? cnt : 0u;
       uint64_t dw = (cc[k] & 2u) ? w[k][1] : w[k][0];
       uint64_t delta = (dw >> (16 * (cc[k] & 1u))) & 0xffffull;        // u16 slot c + (c & 2)
-      uint64_t v = half ? (uint64_t)cnt : ((uint64_t)s[k] << QD_SHIFT) + delta - cnt;
+      // lane 0: delta - (left count); lane 1: + (right count); 2^13 s from the lane that loaded it
+      uint64_t v = (half ? (uint64_t)cnt : delta - cnt) + ((uint64_t)s[k] << QD_SHIFT);
       v += __shfl_xor_sync(0xffffffffu, v, 1);
       if (half == 0 && idx < m) st_stream_u64(out + idx, v);
     }

@@ -129,8 +129,8 @@ def test_birank_tuning_does_not_change_results(cuda, k, pair):
         qr.qr_rank(h, dq, to_dev(c, cuda), out2)
         torch.cuda.synchronize()
     finally:
-        qr.qr_set_tuning("rank_k", 4)
-        qr.qr_set_tuning("rank_blocks_per_sm", 8)
+        qr.qr_set_tuning("rank_k", 2)
+        qr.qr_set_tuning("rank_blocks_per_sm", 64)
         qr.qr_set_tuning("rank_pair", 1)
     ora = oracle.BitsOracle(w, n)
     assert np.array_equal(to_host(out), ora.rank(q))
@@ -160,8 +160,8 @@ def test_quadrank_tuning_does_not_change_results(cuda, k, pair):
         qr.qr_gather_ceiling(h, dq, g, 1)
         torch.cuda.synchronize()
     finally:
-        qr.qr_set_tuning("rank_k", 4)
-        qr.qr_set_tuning("rank_blocks_per_sm", 8)
+        qr.qr_set_tuning("rank_k", 2)
+        qr.qr_set_tuning("rank_blocks_per_sm", 64)
         qr.qr_set_tuning("rank_pair", 1)
     ora = oracle.DnaOracle(w, n)
     assert np.array_equal(to_host(out), ora.rank(q, c))

@@ -1,0 +1,12 @@
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out
+make -s all > gpurun_out/make.log 2>&1
+timeout 1200 python -m pytest tests -m gpu -q --timeout 900 -x -rf > gpurun_out/pytest_gpu.log 2>&1
+echo "pytest exit $?" >> gpurun_out/pytest_gpu.log
+timeout 900 python bench.py --steps 5 --warmup 3 > gpurun_out/bench.log 2>&1
+echo "bench exit $?" >> gpurun_out/bench.log
+timeout 300 python tools/profile_driver.py > gpurun_out/prof_plain.log 2>&1 && \
+timeout 1500 ncu --set full --clock-control none --import-source on \
+  -k 'regex:k_(bi_rank|bi_gather|qd_rank|qd_all4|fm_count)' -c 7 -o gpurun_out/prof_r01b -f \
+  python tools/profile_driver.py > gpurun_out/ncu_full.log 2>&1
+echo "ncu full exit $?" >> gpurun_out/ncu_full.log

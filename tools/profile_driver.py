@@ -50,3 +50,15 @@ o = torch.empty(m, dtype=torch.int32, device=dev)
 qr.qr_fm_count(fm, pats, None, 32, o, m, st)
 torch.cuda.synchronize()
 print("profile driver done")
+fm.free()
+n = 1 << 30
+t = torch.empty((n + 31) // 32 + 1, dtype=torch.uint64, device=dev)
+gen.dna_dev(5, n, 1, t)
+fm = qr.qr_fm_build(t, n)
+m = 10**8
+pats = torch.empty(m * 100, dtype=torch.uint8, device=dev)
+gen.patterns_dev(5, 1, m, 100, t, n, pats)
+o = torch.empty(m, dtype=torch.int32, device=dev)
+qr.qr_fm_count(fm, pats, None, 100, o, m, st)
+torch.cuda.synchronize()
+print("profile driver done (c5)")
