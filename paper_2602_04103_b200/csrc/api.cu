@@ -21,6 +21,7 @@ namespace qr {
 int g_rank_k = 2;               // independent queries per lane (pair) per iteration
 int g_rank_blocks_per_sm = 64;  // 256-thread CTAs per SM of the grid (several waves)
 int g_fm_blocks_per_sm = 8;     // 256-thread CTAs per SM for the FM count kernel
+int g_fm_pair = 0;              // 1: lane-pair FM kernel (one request per distinct line of a step)
 int g_rank_s_lane = 1;          // lane of a pair that loads the superblock word
 int g_rank_pair = 1;            // 1: lane-pair kernels (one L2 request per query); 0: one lane per query
 uint64_t g_stage_chunk = 1ull << 24;   // queries per chunk on the staged host path
@@ -250,6 +251,9 @@ QR_EXPORT qr_status qr_set_tuning(const char* key, int64_t value) {
   } else if (!strcmp(key, "rank_s_lane")) {
     if (value != 0 && value != 1) return fail(QR_EINVAL, "rank_s_lane must be 0 or 1");
     g_rank_s_lane = (int)value;
+  } else if (!strcmp(key, "fm_pair")) {
+    if (value != 0 && value != 1) return fail(QR_EINVAL, "fm_pair must be 0 or 1");
+    g_fm_pair = (int)value;
   } else if (!strcmp(key, "fm_blocks_per_sm")) {
     if (value < 1 || value > 64) return fail(QR_EINVAL, "fm_blocks_per_sm out of range");
     g_fm_blocks_per_sm = (int)value;

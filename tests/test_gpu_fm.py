@@ -173,3 +173,35 @@ def test_fm_all_kmers_partition(cuda):
         torch.cuda.synchronize()
         if k < 9:
             assert int(to_host(d).astype(np.int64).sum()) == n - k + 1
+
+
+@pytest.mark.parametrize("pair,bps", [(0, 2), (1, 4), (1, 16), (0, 32)])
+def test_fm_tuning_does_not_change_results(cuda, pair, bps):
+    torch = _torch()
+    n = 90000
+    w = gen.dna(31, n, 1)
+    sym = gen.unpack_dna(w, n)
+    ora = oracle.FmOracle(sym)
+    fm = qr.qr_fm_build(w, n)
+    pats = mixed_patterns(np.random.default_rng(5), sym, 3000)
+    cat, off, lens = oracle.pack_patterns(pats)
+    ref = ora.count(cat, off, lens)
+    L, m = 40, 5000
+    fixed = gen.patterns(9, 1, m, L, w, n)
+    ref_fixed = ora.count(fixed, np.arange(m, dtype=np.uint64) * L, np.full(m, L, np.uint32))
+    qr.qr_set_tuning("fm_pair", pair)
+    qr.qr_set_tuning("fm_blocks_per_sm", bps)
+    try:
+        d = torch.empty(lens.size, dtype=torch.int32, device=cuda)
+        qr.qr_fm_count(fm, to_dev(cat, cuda), to_dev(lens, cuda), 0, d, lens.size)
+        d2 = torch.empty(m, dtype=torch.int32, device=cuda)
+        work = torch.zeros(2, dtype=torch.uint64, device=cuda)
+        qr.qr_fm_count_work(fm, to_dev(fixed, cuda), None, L, d2, m, work)
+        torch.cuda.synchronize()
+    finally:
+        qr.qr_set_tuning("fm_pair", 0)
+        qr.qr_set_tuning("fm_blocks_per_sm", 8)
+    assert np.array_equal(to_host(d).view(np.uint32), ref)
+    assert np.array_equal(to_host(d2).view(np.uint32), ref_fixed)
+    ts, tl = ora.work(fixed, np.arange(m, dtype=np.uint64) * L, np.full(m, L, np.uint32), skip=8, block=224)
+    assert [int(x) for x in to_host(work)] == [ts, tl]
