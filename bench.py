@@ -287,6 +287,31 @@ def bench_fm(ctx, n, kind, m_total, length, seed, steps, warmup, rank_queries=0)
     return res
 
 
+def bench_reads(ctx, n, m_total, length, seed, steps, warmup):
+    """The paper's FM workload shape: 150-bp reads with 1% substitutions from
+    either strand, each counted in both directions in one launch (qr_fm_count_both), over the
+    configs[4] block-repeat text (stand-in for CHM13v2)."""
+    import gen
+    import paper_2602_04103_b200 as qr
+
+    torch = ctx.torch
+    text = torch.empty((n + 31) // 32 + 1, dtype=torch.uint64, device=ctx.dev)
+    gen.dna_dev(seed, n, 1, text)
+    fm = qr.qr_fm_build(text, n, device=ctx.local)
+    i0, m = shard(m_total, ctx.world, ctx.rank)
+    pats = torch.empty(m * length, dtype=torch.uint8, device=ctx.dev)
+    gen.patterns_dev(seed, 2, m, length, text, n, pats, i0=i0)
+    of = torch.empty(m, dtype=torch.int32, device=ctx.dev)
+    orc = torch.empty(m, dtype=torch.int32, device=ctx.dev)
+    ms = ctx.timed(lambda: qr.qr_fm_count_both(fm, pats, None, length, of, orc, m, ctx.stream), steps, warmup)
+    hit = int(((of > 0) | (orc > 0)).sum())
+    fm.free()
+    del text, pats, of, orc
+    torch.cuda.empty_cache()
+    return {"ms": ms, "reads_per_s": m_total / ms * 1e3, "searches_per_s": 2 * m_total / ms * 1e3,
+            "read_len": length, "reads": m_total, "frac_reads_matching": hit / max(m, 1)}
+
+
 def bench_small(ctx, steps, warmup):
     import gen
     import paper_2602_04103_b200 as qr
@@ -386,6 +411,7 @@ def main():
         rows["c3_quadrank"] = bench_quadrank(ctx, K, W)
         rows["c4_quadfm"] = bench_fm(ctx, N4, 0, M4, L4, SEED[4], K, W)
         rows["c5_quadfm"] = bench_fm(ctx, N5, 1, M5, L5, SEED[5], K, W, rank_queries=10**9)
+        rows["c5_reads_150bp_both_strands"] = bench_reads(ctx, N5, 10**7, 150, 55, K, W)
         rows["c1_small"] = bench_small(ctx, K, W)
     ms = c2["ms"]
     value = c2["gq_s"]

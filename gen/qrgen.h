@@ -46,6 +46,9 @@
 #define QRG_TAG_PCHR  10u
 #define QRG_TAG_PKIND 11u
 #define QRG_TAG_PSUB  12u
+#define QRG_TAG_RMUT  13u
+#define QRG_TAG_RSYM  14u
+#define QRG_TAG_RSTR  15u
 
 #define QRG_BLOCK 10000ull          /* config 5 block length (BASELINE.json configs[4]) */
 #define QRG_P_COPY  0x4CCCCCCCCCCCCCCDull   /* ceil(0.3 * 2^64)  */
@@ -124,6 +127,10 @@ QRG_HD uint32_t qrg_text_char(const uint64_t* text2b, uint64_t k) {
  * kind 1 ("config 5"): substring at mulhi(h(PPOS,i), n-len+1) with s = mulhi(h(PKIND,i),3)
  *   substitutions at distinct positions (rejection on the PSUB stream), each
  *   replaced by one of the 3 other symbols uniformly.
+ * kind 2 ("reads", the paper's FM workload shape): substring at
+ *   mulhi(h(PPOS,i), n-len+1), each position independently substituted with probability 0.01
+ *   (RMUT stream) by one of the 3 other symbols (RSYM), then reverse-complemented when
+ *   h(RSTR,i) is odd (reads come from either strand).
  * Writes len symbols (0..3, one byte each) to out.
  */
 QRG_HD void qrg_pattern(uint64_t seed, int kind, uint64_t i, uint32_t len,
@@ -137,6 +144,19 @@ QRG_HD void qrg_pattern(uint64_t seed, int kind, uint64_t i, uint32_t len,
   uint64_t pos = qrg_below(seed, QRG_TAG_PPOS, i, span);
   for (uint32_t k = 0; k < len; ++k)
     out[k] = (pos + k < n) ? (uint8_t)qrg_text_char(text2b, pos + k) : (uint8_t)0;
+  if (kind == 2) {
+    for (uint32_t k = 0; k < len; ++k)
+      if (qrg_hash(seed, QRG_TAG_RMUT, i * (uint64_t)len + k) < QRG_P_MUT)
+        out[k] = (uint8_t)((out[k] + 1u + (uint32_t)qrg_below(seed, QRG_TAG_RSYM, i * (uint64_t)len + k, 3)) & 3u);
+    if (qrg_hash(seed, QRG_TAG_RSTR, i) & 1u)
+      for (uint32_t a = 0, b = len - 1; a <= b && b < len; ++a, --b) {
+        uint8_t x = (uint8_t)(3u - out[a]), y = (uint8_t)(3u - out[b]);
+        out[a] = y;
+        out[b] = x;
+        if (b == 0) break;
+      }
+    return;
+  }
   if (kind == 1 && len > 0) {
     uint32_t s = (uint32_t)qrg_below(seed, QRG_TAG_PKIND, i, 3);
     uint32_t used[2] = {0xffffffffu, 0xffffffffu};

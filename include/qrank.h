@@ -100,6 +100,14 @@ qr_status qr_fm_build(const uint64_t* text2b, uint64_t n, const uint32_t* sa_or_
 qr_status qr_fm_count(const qr_fm* fm, const uint8_t* patterns, const uint32_t* lengths, uint32_t fixed_len,
                       uint32_t* out, uint64_t m, void* stream);
 
+/* Both strands in one launch (reads are counted "in both forward and
+ * reverse-complement direction"; NEXT §8(f)1): out_fwd[k] = count of pattern k,
+ * out_rc[k] = count of its reverse complement RC(P)[j] = 3 - P[len-1-j] (A<->T, C<->G,
+ * reversed).  The reverse complement is read from the same bytes inside the kernel (no copy).
+ * Arguments and memory spaces as qr_fm_count. */
+qr_status qr_fm_count_both(const qr_fm* fm, const uint8_t* patterns, const uint32_t* lengths, uint32_t fixed_len,
+                           uint32_t* out_fwd, uint32_t* out_rc, uint64_t m, void* stream);
+
 /* As qr_fm_count (device pointers only), additionally accumulating into work[0] the number of
  * backward steps executed after seeding and into work[1] the number of distinct 64-B lines
  * those steps touch (1 or 2 per step) — the algorithmic-bytes denominator of SURVEY §8(d).

@@ -20,8 +20,7 @@ namespace qr {
 // ---- tuning knobs (set through qr_set_tuning; defaults chosen from B200 measurements) ----
 int g_rank_k = 2;               // independent queries per lane (pair) per iteration
 int g_rank_blocks_per_sm = 64;  // 256-thread CTAs per SM of the grid (several waves)
-int g_fm_blocks_per_sm = 8;     // 256-thread CTAs per SM for the FM count kernel
-int g_fm_pair = 0;              // 1: lane-pair FM kernel (one request per distinct line of a step)
+int g_fm_blocks_per_sm = 64;    // 256-thread CTAs per SM of the FM grid (several waves)
 int g_rank_s_lane = 1;          // lane of a pair that loads the superblock word
 int g_rank_pair = 1;            // 1: lane-pair kernels (one L2 request per query); 0: one lane per query
 uint64_t g_stage_chunk = 1ull << 24;   // queries per chunk on the staged host path
@@ -251,9 +250,6 @@ QR_EXPORT qr_status qr_set_tuning(const char* key, int64_t value) {
   } else if (!strcmp(key, "rank_s_lane")) {
     if (value != 0 && value != 1) return fail(QR_EINVAL, "rank_s_lane must be 0 or 1");
     g_rank_s_lane = (int)value;
-  } else if (!strcmp(key, "fm_pair")) {
-    if (value != 0 && value != 1) return fail(QR_EINVAL, "fm_pair must be 0 or 1");
-    g_fm_pair = (int)value;
   } else if (!strcmp(key, "fm_blocks_per_sm")) {
     if (value < 1 || value > 64) return fail(QR_EINVAL, "fm_blocks_per_sm out of range");
     g_fm_blocks_per_sm = (int)value;
@@ -401,7 +397,7 @@ QR_EXPORT qr_status qr_fm_build(const uint64_t* text2b, uint64_t n, const uint32
 }
 
 static qr_status fm_count_impl(const qr_fm* fm, const uint8_t* patterns, const uint32_t* lengths, uint32_t fixed_len,
-                               uint32_t* out, uint64_t m, uint64_t* work, void* stream) {
+                               uint32_t* out, uint32_t* out_rc, uint64_t m, uint64_t* work, void* stream) {
   if (!fm) return fail(QR_EINVAL, "qr_fm_count: null handle");
   if (m == 0) return QR_OK;
   if (!out || (!patterns && (lengths || fixed_len))) return fail(QR_EINVAL, "qr_fm_count: null pointer");
@@ -409,15 +405,17 @@ static qr_status fm_count_impl(const qr_fm* fm, const uint8_t* patterns, const u
   cudaStream_t st = (cudaStream_t)stream;
   const uint8_t* pat = patterns;
   static const uint8_t dummy = 0;
-  int sp = classify({patterns, lengths, out, work}, fm->bwt->device);
+  int sp = classify({patterns, lengths, out, out_rc, work}, fm->bwt->device);
   if (sp < 0) return fail(QR_EINVAL, "qr_fm_count: pointers must all be device (device %d) or all host", fm->bwt->device);
-  if (sp == 1) return fm_count_device(fm, pat ? pat : &dummy, lengths, fixed_len, out, m, work, st);
+  if (sp == 1) return fm_count_device(fm, pat ? pat : &dummy, lengths, fixed_len, out, out_rc, m, work, st);
   if (work) return fail(QR_EINVAL, "qr_fm_count_work: device pointers only");
   if (!lengths) {
     std::vector<StageArray> arr = {{patterns, nullptr, (size_t)fixed_len}, {nullptr, out, 4}};
     if (fixed_len == 0) arr[0].host_in = nullptr, arr[0].item_bytes = 1;
+    if (out_rc) arr.push_back({nullptr, out_rc, 4});
     return run_staged(fm->bwt->device, st, m, arr, [&](const std::vector<void*>& d, uint64_t cnt, cudaStream_t s) {
-      return fm_count_device(fm, (const uint8_t*)d[0], nullptr, fixed_len, (uint32_t*)d[1], cnt, nullptr, s);
+      return fm_count_device(fm, (const uint8_t*)d[0], nullptr, fixed_len, (uint32_t*)d[1],
+                             out_rc ? (uint32_t*)d[2] : nullptr, cnt, nullptr, s);
     });
   }
   // variable lengths from host: one whole copy (offsets depend on every earlier length)
@@ -426,28 +424,37 @@ static qr_status fm_count_impl(const qr_fm* fm, const uint8_t* patterns, const u
   uint8_t* dp = nullptr;
   uint32_t *dl = nullptr, *dout = nullptr;
   cudaError_t e;
-  if ((e = cudaMallocAsync((void**)&dp, total + 1, st)) || (e = cudaMallocAsync((void**)&dl, m * 4, st)) ||
-      (e = cudaMallocAsync((void**)&dout, m * 4, st))) {
+  if ((e = cudaMallocAsync((void**)&dp, total + 8, st)) || (e = cudaMallocAsync((void**)&dl, m * 4, st)) ||
+      (e = cudaMallocAsync((void**)&dout, m * 8, st))) {
     cudaFreeAsync(dp, st); cudaFreeAsync(dl, st); cudaFreeAsync(dout, st);
     return cuda_fail(e, "qr_fm_count: staging alloc");
   }
   if (total) cudaMemcpyAsync(dp, patterns, total, cudaMemcpyHostToDevice, st);
   cudaMemcpyAsync(dl, lengths, m * 4, cudaMemcpyHostToDevice, st);
-  qr_status s = fm_count_device(fm, dp, dl, 0, dout, m, nullptr, st);
-  if (s == QR_OK) cudaMemcpyAsync(out, dout, m * 4, cudaMemcpyDeviceToHost, st);
+  qr_status s = fm_count_device(fm, dp, dl, 0, dout, out_rc ? dout + m : nullptr, m, nullptr, st);
+  if (s == QR_OK) {
+    cudaMemcpyAsync(out, dout, m * 4, cudaMemcpyDeviceToHost, st);
+    if (out_rc) cudaMemcpyAsync(out_rc, dout + m, m * 4, cudaMemcpyDeviceToHost, st);
+  }
   cudaFreeAsync(dp, st); cudaFreeAsync(dl, st); cudaFreeAsync(dout, st);
   return s;
 }
 
 QR_EXPORT qr_status qr_fm_count(const qr_fm* fm, const uint8_t* patterns, const uint32_t* lengths, uint32_t fixed_len,
                                 uint32_t* out, uint64_t m, void* stream) {
-  return fm_count_impl(fm, patterns, lengths, fixed_len, out, m, nullptr, stream);
+  return fm_count_impl(fm, patterns, lengths, fixed_len, out, nullptr, m, nullptr, stream);
+}
+
+QR_EXPORT qr_status qr_fm_count_both(const qr_fm* fm, const uint8_t* patterns, const uint32_t* lengths,
+                                     uint32_t fixed_len, uint32_t* out_fwd, uint32_t* out_rc, uint64_t m, void* stream) {
+  if (!out_rc) return fail(QR_EINVAL, "qr_fm_count_both: null out_rc");
+  return fm_count_impl(fm, patterns, lengths, fixed_len, out_fwd, out_rc, m, nullptr, stream);
 }
 
 QR_EXPORT qr_status qr_fm_count_work(const qr_fm* fm, const uint8_t* patterns, const uint32_t* lengths,
                                      uint32_t fixed_len, uint32_t* out, uint64_t m, uint64_t* work, void* stream) {
   if (!work) return fail(QR_EINVAL, "qr_fm_count_work: null work");
-  return fm_count_impl(fm, patterns, lengths, fixed_len, out, m, work, stream);
+  return fm_count_impl(fm, patterns, lengths, fixed_len, out, nullptr, m, work, stream);
 }
 
 QR_EXPORT qr_status qr_info(const qr_index* h, uint64_t* n, int* sigma, uint64_t* line_bytes, uint64_t* super_bytes) {
@@ -517,8 +524,9 @@ QR_EXPORT qr_status qr_fm_clone_to_device(const qr_fm* fm, int device, void* str
   qr_status s = qr_clone_to_device(fm->bwt, device, stream, &c->bwt);
   if (s != QR_OK) { delete c; return s; }
   DeviceGuard dg(device);
-  cudaError_t e = cudaMalloc((void**)&c->kmer, 65536 * sizeof(uint2));
-  if (!e) e = cudaMemcpyPeerAsync(c->kmer, device, fm->kmer, fm->bwt->device, 65536 * sizeof(uint2), (cudaStream_t)stream);
+  cudaError_t e = cudaMalloc((void**)&c->kmer, (65536 + 2) * sizeof(uint2));   // table + C[0..3] tail
+  if (!e) e = cudaMemcpyPeerAsync(c->kmer, device, fm->kmer, fm->bwt->device, (65536 + 2) * sizeof(uint2),
+                                  (cudaStream_t)stream);
   if (!e) e = cudaStreamSynchronize((cudaStream_t)stream);
   if (e) { qr_fm_free(c); return cuda_fail(e, "qr_fm_clone_to_device"); }
   *out = c;

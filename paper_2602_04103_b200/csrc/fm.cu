@@ -25,7 +25,8 @@ struct FmParams {
   uint64_t spos;
   uint64_t N;
   uint64_t last_line;
-  uint32_t C[4];
+  uint32_t C[4];        // host copy; the kernels read C from the table tail (Ct) with one load
+  const uint32_t* Ct;   // = (const uint32_t*)(kmer + 65536): C[0..3] stored after the 8-mer table
 };
 
 __device__ __forceinline__ uint32_t text_char(const uint64_t* t, uint64_t i) {
@@ -236,8 +237,9 @@ __device__ __forceinline__ void fm_step(const FmParams& F, uint32_t c, uint32_t&
   uint32_t rl = rank1(al, bl, pl, sl), rh = rank1(ah, bh, ph, sh);
   // '$' is stored as A at row spos: Occ(A, x) = rank(x, A) - [x > spos]
   if (c == 0) { rl -= (lo > (uint32_t)F.spos); rh -= (hi > (uint32_t)F.spos); }
-  lo = F.C[c] + rl;
-  hi = F.C[c] + rh;
+  const uint32_t Cc = __ldg(F.Ct + c);   // L1-resident; a register-indexed param array costs ~26 SASS
+  lo = Cc + rl;
+  hi = Cc + rh;
 }
 
 __global__ void k_kmer_table(FmParams F, uint2* __restrict__ table) {
@@ -274,38 +276,55 @@ struct PatWindow {
 // 8-mer table key of the pattern's last 8 symbols (P[len-8..len), 2 bits each, the last symbol
 // in the low bits — PAPER.md:918, reading R14) from one unaligned 8-byte read: reverse the byte
 // order, keep 2 bits per byte and compact the eight 2-bit fields into 16 bits.
-__device__ __forceinline__ uint32_t kmer_key8(const uint8_t* last8) {
-  const uintptr_t a = (uintptr_t)last8;
+__device__ __forceinline__ uint64_t load8_unaligned(const uint8_t* p) {
+  const uintptr_t a = (uintptr_t)p;
   const unsigned long long* base = reinterpret_cast<const unsigned long long*>(a & ~(uintptr_t)7);
   const uint32_t sh = (uint32_t)(a & 7u) * 8u;
   uint64_t x = __ldg(base);
   if (sh) x = (x >> sh) | ((uint64_t)__ldg(base + 1) << (64u - sh));
-  x &= 0x0303030303030303ull;
-  uint64_t r = ((uint64_t)__byte_perm((uint32_t)x, 0, 0x0123) << 32) | __byte_perm((uint32_t)(x >> 32), 0, 0x0123);
+  return x & 0x0303030303030303ull;
+}
+// compact the 2-bit fields at bits 8t (t = 0..7) to bits 2t
+__device__ __forceinline__ uint32_t compact8(uint64_t r) {
   r = (r | (r >> 6)) & 0x000F000F000F000Full;
   r = (r | (r >> 12)) & 0x000000FF000000FFull;
   r = (r | (r >> 24)) & 0xFFFFull;
   return (uint32_t)r;
 }
+__device__ __forceinline__ uint32_t kmer_key8(const uint8_t* last8) {
+  uint64_t x = load8_unaligned(last8);
+  return compact8(((uint64_t)__byte_perm((uint32_t)x, 0, 0x0123) << 32) | __byte_perm((uint32_t)(x >> 32), 0, 0x0123));
+}
+// Key of the reverse complement's last 8 symbols: RC(P)[len-1-t] = 3 - P[t], so the key is
+// sum_t (3 - P[t]) << 2t = 0xFFFF ^ (P[0..8) compacted without byte reversal).
+__device__ __forceinline__ uint32_t kmer_key8_rc(const uint8_t* first8) { return 0xFFFFu ^ compact8(load8_unaligned(first8)); }
 
-template <bool FIXED, bool WORK>
+// STRANDS = 1: count each pattern as given.  STRANDS = 2: task 2i counts pattern i and task
+// 2i+1 its reverse complement RC(P)[j] = 3 - P[len-1-j] ("both forward and
+// reverse-complement direction"; NEXT §8(f)1), read from the same bytes in the opposite
+// direction, so no reverse-complemented copy is ever materialised.
+template <bool FIXED, bool WORK, int STRANDS>
 __global__ void __launch_bounds__(256, 4) k_fm_count(FmParams F, const uint8_t* __restrict__ pat,
                                                      const uint64_t* __restrict__ offs, const uint32_t* __restrict__ lens,
-                                                     uint32_t fixed_len, uint32_t* __restrict__ out, uint64_t m,
+                                                     uint32_t fixed_len, uint32_t* __restrict__ out,
+                                                     uint32_t* __restrict__ out_rc, uint64_t m,
                                                      unsigned long long* __restrict__ work) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  uint64_t pi = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-  uint32_t lo = 0, hi = 0;
+  const uint64_t ntask = m * STRANDS;
+  uint64_t ti = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  uint32_t lo = 0, hi = 0, len = 0, rc = 0;
   int64_t k = -1;
   PatWindow P;
   uint64_t n_steps = 0, n_lines = 0;
-  // seed pattern pi: the 8-mer table interval of its last 8 symbols, or the full interval
+  // seed task ti: the 8-mer table interval of the (virtual) pattern's last 8 symbols, or [0, N)
   auto seed = [&]() {
-    const uint32_t len = FIXED ? fixed_len : lens[pi];
+    const uint64_t pi = STRANDS == 2 ? ti >> 1 : ti;
+    rc = STRANDS == 2 ? (uint32_t)(ti & 1) : 0u;
+    len = FIXED ? fixed_len : lens[pi];
     const uint8_t* p = pat + (FIXED ? pi * (uint64_t)fixed_len : offs[pi]);
     P.reset(p);
     if (len >= 8) {
-      uint2 iv = __ldg(F.kmer + kmer_key8(p + len - 8));
+      uint2 iv = __ldg(F.kmer + (rc ? kmer_key8_rc(p) : kmer_key8(p + len - 8)));
       lo = iv.x; hi = iv.y;
       k = (int64_t)len - 9;
     } else {
@@ -313,119 +332,24 @@ __global__ void __launch_bounds__(256, 4) k_fm_count(FmParams F, const uint8_t* 
       k = (int64_t)len - 1;
     }
   };
-  if (pi < m) seed();
-  while (pi < m) {
+  if (ti < ntask) seed();
+  while (ti < ntask) {
     if (k >= 0 && lo < hi) {                             // one backward step (LF mapping)
+      const uint32_t c = rc ? 3u - P.at((int64_t)len - 1 - k) : P.at(k);
       uint32_t nl;
-      fm_step(F, P.at(k), lo, hi, nl);
+      fm_step(F, c, lo, hi, nl);
       --k;
       if (WORK) { n_steps += 1; n_lines += nl; }
     }
-    if (k < 0 || lo >= hi) {                             // finished: write, claim the next pattern
-      out[pi] = lo < hi ? hi - lo : 0u;
-      pi += stride;
-      if (pi < m) seed();
+    if (k < 0 || lo >= hi) {                             // finished: write, claim the next task
+      const uint32_t cnt = lo < hi ? hi - lo : 0u;
+      if (STRANDS == 2 && rc) out_rc[ti >> 1] = cnt;
+      else out[STRANDS == 2 ? ti >> 1 : ti] = cnt;
+      ti += stride;
+      if (ti < ntask) seed();
     }
   }
   if (WORK && n_steps) {
-    atomicAdd(work, (unsigned long long)n_steps);
-    atomicAdd(work + 1, (unsigned long long)n_lines);
-  }
-}
-
-// ---- lane-pair FM: one L2 request per distinct line of a step ------------------------------
-// Two lanes share a pattern.  In the first load instruction lane 0 reads sector 0 (deltas +
-// data chars [0,96)) of lo's line and lane 1 its sector 1 when a rank needs it; in the second
-// (only when hi lies in another line) the same for hi's line.  Both sectors of a line are then
-// one L2 request, so a step costs as many requests as it touches lines (1 or 2) instead of up
-// to 4 sector loads.  Lane 0 contributes delta - (left count), lane 1 the right count and
-// 2^13 s (it also loads the superblock word); a 2-lane shuffle adds the halves.  Both lanes
-// keep identical pattern state, so the pair stays converged.
-__device__ __forceinline__ uint32_t fm_half_count(const uint64_t w[4], uint32_t c, uint32_t p) {
-  const uint64_t cl = 0ull - (uint64_t)(c & 1u), ch = 0ull - (uint64_t)(c >> 1);
-  const int x = (int)(p & 127u);
-  const uint64_t inv = p >= 128 ? 0ull : ~0ull;
-  return __popcll((w[0] ^ cl) & (w[1] ^ ch) & (prefix_mask(x, 0) ^ inv)) +
-         __popcll((w[2] ^ cl) & (w[3] ^ ch) & (prefix_mask(x, 1) ^ inv));
-}
-
-__device__ __forceinline__ void fm_step2(const FmParams& F, uint32_t c, uint32_t& lo, uint32_t& hi, uint32_t half,
-                                         uint32_t pmask, uint32_t& lines) {
-  uint32_t jl = (lo >> 5) / 7u, jh = (hi >> 5) / 7u;
-  jl = jl > (uint32_t)F.last_line ? (uint32_t)F.last_line : jl;
-  jh = jh > (uint32_t)F.last_line ? (uint32_t)F.last_line : jh;
-  const uint32_t pl = 32u + lo - jl * (uint32_t)QD_B, ph = 32u + hi - jh * (uint32_t)QD_B;
-  const bool same = jl == jh;
-  uint64_t w1[4] = {0, 0, 0, 0}, w2[4] = {0, 0, 0, 0};
-  if (half == 0 || pl >= 128 || (same && ph >= 128)) ld_sector(F.lines + 4 * (uint64_t)jl + 2 * half, w1[0], w1[1], w1[2], w1[3]);
-  if (!same && (half == 0 || ph >= 128)) ld_sector(F.lines + 4 * (uint64_t)jh + 2 * half, w2[0], w2[1], w2[2], w2[3]);
-  uint32_t sl = 0, sh = 0;
-  if (half == 1) {
-    sl = __ldg(F.super + 4 * (jl >> QD_SB_LOG) + c);
-    sh = (jl >> QD_SB_LOG) == (jh >> QD_SB_LOG) ? sl : __ldg(F.super + 4 * (jh >> QD_SB_LOG) + c);
-  }
-  lines = same ? 1u : 2u;
-  const uint64_t* wl = w1;
-  const uint64_t* wh = same ? w1 : w2;
-  uint32_t vl, vh;
-  if (half == 0) {            // sector 0: delta - count of [p,128) when p < 128
-    const uint64_t dl = (c & 2u) ? wl[1] : wl[0], dh = (c & 2u) ? wh[1] : wh[0];
-    vl = (uint32_t)((dl >> (16 * (c & 1u))) & 0xffffull) - (pl < 128 ? fm_half_count(wl, c, pl) : 0u);
-    vh = (uint32_t)((dh >> (16 * (c & 1u))) & 0xffffull) - (ph < 128 ? fm_half_count(wh, c, ph) : 0u);
-  } else {                    // sector 1: count of [128,p) when p >= 128, plus 2^13 s
-    vl = (sl << QD_SHIFT) + (pl >= 128 ? fm_half_count(wl, c, pl) : 0u);
-    vh = (sh << QD_SHIFT) + (ph >= 128 ? fm_half_count(wh, c, ph) : 0u);
-  }
-  uint64_t both = ((uint64_t)vh << 32) | vl;
-  uint64_t oth = __shfl_xor_sync(pmask, both, 1);
-  uint32_t rl = vl + (uint32_t)oth, rh = vh + (uint32_t)(oth >> 32);
-  if (c == 0) { rl -= (lo > (uint32_t)F.spos); rh -= (hi > (uint32_t)F.spos); }
-  lo = F.C[c] + rl;
-  hi = F.C[c] + rh;
-}
-
-template <bool FIXED, bool WORK>
-__global__ void __launch_bounds__(256, 4) k_fm_count2(FmParams F, const uint8_t* __restrict__ pat,
-                                                      const uint64_t* __restrict__ offs, const uint32_t* __restrict__ lens,
-                                                      uint32_t fixed_len, uint32_t* __restrict__ out, uint64_t m,
-                                                      unsigned long long* __restrict__ work) {
-  const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-  const uint64_t stride = ((uint64_t)gridDim.x * blockDim.x) >> 1;
-  const uint32_t half = (uint32_t)(tid & 1u);
-  const uint32_t pmask = 3u << (threadIdx.x & 30u);
-  uint64_t pi = tid >> 1;
-  uint32_t lo = 0, hi = 0;
-  int64_t k = -1;
-  PatWindow P;
-  uint64_t n_steps = 0, n_lines = 0;
-  auto seed = [&]() {
-    const uint32_t len = FIXED ? fixed_len : lens[pi];
-    const uint8_t* p = pat + (FIXED ? pi * (uint64_t)fixed_len : offs[pi]);
-    P.reset(p);
-    if (len >= 8) {
-      uint2 iv = __ldg(F.kmer + kmer_key8(p + len - 8));
-      lo = iv.x; hi = iv.y;
-      k = (int64_t)len - 9;
-    } else {
-      lo = 0; hi = (uint32_t)F.N;
-      k = (int64_t)len - 1;
-    }
-  };
-  if (pi < m) seed();
-  while (pi < m) {
-    if (k >= 0 && lo < hi) {
-      uint32_t nl;
-      fm_step2(F, P.at(k), lo, hi, half, pmask, nl);
-      --k;
-      if (WORK && half == 0) { n_steps += 1; n_lines += nl; }
-    }
-    if (k < 0 || lo >= hi) {
-      if (half == 0) out[pi] = lo < hi ? hi - lo : 0u;
-      pi += stride;
-      if (pi < m) seed();
-    }
-  }
-  if (WORK && n_steps) {       // pairs finish at different times: no full-warp reduction here
     atomicAdd(work, (unsigned long long)n_steps);
     atomicAdd(work + 1, (unsigned long long)n_lines);
   }
@@ -445,29 +369,32 @@ static FmParams params_of(const qr_fm* fm) {
   F.N = fm->N;
   F.last_line = fm->bwt->n_lines - 1;
   for (int c = 0; c < 4; ++c) F.C[c] = (uint32_t)fm->C[c];
+  F.Ct = reinterpret_cast<const uint32_t*>(fm->kmer + 65536);
   return F;
 }
 
 extern int g_fm_blocks_per_sm;
-extern int g_fm_pair;
+
+template <bool FIXED, bool WORK>
+static void launch_fm(unsigned g, cudaStream_t st, const FmParams& F, const uint8_t* pat, const uint64_t* offs,
+                      const uint32_t* lens, uint32_t fixed_len, uint32_t* out, uint32_t* out_rc, uint64_t m,
+                      unsigned long long* w) {
+  if (out_rc) k_fm_count<FIXED, WORK, 2><<<g, 256, 0, st>>>(F, pat, offs, lens, fixed_len, out, out_rc, m, w);
+  else        k_fm_count<FIXED, WORK, 1><<<g, 256, 0, st>>>(F, pat, offs, lens, fixed_len, out, out_rc, m, w);
+}
 
 qr_status fm_count_device(const qr_fm* fm, const uint8_t* pat, const uint32_t* lengths, uint32_t fixed_len,
-                          uint32_t* out, uint64_t m, uint64_t* work, cudaStream_t st) {
+                          uint32_t* out, uint32_t* out_rc, uint64_t m, uint64_t* work, cudaStream_t st) {
   if (m == 0) return QR_OK;
   FmParams F = params_of(fm);
   const int sms = fm->bwt->sm_count;
-  unsigned g = grid_stride_blocks(m, 256, sms, g_fm_blocks_per_sm);
+  const uint64_t tasks = out_rc ? 2 * m : m;
+  unsigned g = grid_stride_blocks(tasks, 256, sms, g_fm_blocks_per_sm);
   unsigned long long* w = reinterpret_cast<unsigned long long*>(work);
   cudaError_t e;
-  if (g_fm_pair) g = grid_stride_blocks(2 * m, 256, sms, g_fm_blocks_per_sm);
   if (!lengths) {
-    if (g_fm_pair) {
-      if (work) k_fm_count2<true, true><<<g, 256, 0, st>>>(F, pat, nullptr, nullptr, fixed_len, out, m, w);
-      else      k_fm_count2<true, false><<<g, 256, 0, st>>>(F, pat, nullptr, nullptr, fixed_len, out, m, w);
-    } else {
-      if (work) k_fm_count<true, true><<<g, 256, 0, st>>>(F, pat, nullptr, nullptr, fixed_len, out, m, w);
-      else      k_fm_count<true, false><<<g, 256, 0, st>>>(F, pat, nullptr, nullptr, fixed_len, out, m, w);
-    }
+    if (work) launch_fm<true, true>(g, st, F, pat, nullptr, nullptr, fixed_len, out, out_rc, m, w);
+    else      launch_fm<true, false>(g, st, F, pat, nullptr, nullptr, fixed_len, out, out_rc, m, w);
     if ((e = cudaGetLastError())) return cuda_fail(e, "k_fm_count");
     return QR_OK;
   }
@@ -481,13 +408,8 @@ qr_status fm_count_device(const qr_fm* fm, const uint8_t* pat, const uint32_t* l
   if ((e = cub::DeviceScan::ExclusiveSum(tmp, tb, offs, offs, (int64_t)m, st))) {
     cudaFreeAsync(offs, st); cudaFreeAsync(tmp, st); return cuda_fail(e, "scan");
   }
-  if (g_fm_pair) {
-    if (work) k_fm_count2<false, true><<<g, 256, 0, st>>>(F, pat, offs, lengths, 0, out, m, w);
-    else      k_fm_count2<false, false><<<g, 256, 0, st>>>(F, pat, offs, lengths, 0, out, m, w);
-  } else {
-    if (work) k_fm_count<false, true><<<g, 256, 0, st>>>(F, pat, offs, lengths, 0, out, m, w);
-    else      k_fm_count<false, false><<<g, 256, 0, st>>>(F, pat, offs, lengths, 0, out, m, w);
-  }
+  if (work) launch_fm<false, true>(g, st, F, pat, offs, lengths, 0, out, out_rc, m, w);
+  else      launch_fm<false, false>(g, st, F, pat, offs, lengths, 0, out, out_rc, m, w);
   e = cudaGetLastError();
   cudaFreeAsync(offs, st);
   cudaFreeAsync(tmp, st);
@@ -537,7 +459,13 @@ qr_status fm_build_device(const uint64_t* d_text, uint64_t n, const uint32_t* d_
   fm->C[0] = 1;
   for (int c = 1; c < 4; ++c) fm->C[c] = fm->C[c - 1] + h_aux[c];   // C[c] = 1 + #{t_i < c}
   fm->C[4] = N;
-  if ((e = cudaMalloc((void**)&fm->kmer, 65536 * sizeof(uint2)))) return bail(cuda_fail(e, "alloc kmer"));
+  if ((e = cudaMalloc((void**)&fm->kmer, (65536 + 2) * sizeof(uint2)))) return bail(cuda_fail(e, "alloc kmer"));
+  {
+    uint32_t Ch[4] = {(uint32_t)fm->C[0], (uint32_t)fm->C[1], (uint32_t)fm->C[2], (uint32_t)fm->C[3]};
+    if ((e = cudaMemcpyAsync(fm->kmer + 65536, Ch, sizeof(Ch), cudaMemcpyHostToDevice, st)))
+      return bail(cuda_fail(e, "copy C"));
+    if ((e = cudaStreamSynchronize(st))) return bail(cuda_fail(e, "copy C"));
+  }
   FmParams F = params_of(fm);
   k_kmer_table<<<65536 / 256, 256, 0, st>>>(F, fm->kmer);
   if ((e = cudaGetLastError())) return bail(cuda_fail(e, "k_kmer_table"));

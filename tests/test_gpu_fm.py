@@ -175,8 +175,8 @@ def test_fm_all_kmers_partition(cuda):
             assert int(to_host(d).astype(np.int64).sum()) == n - k + 1
 
 
-@pytest.mark.parametrize("pair,bps", [(0, 2), (1, 4), (1, 16), (0, 32)])
-def test_fm_tuning_does_not_change_results(cuda, pair, bps):
+@pytest.mark.parametrize("bps", [2, 4, 16, 64])
+def test_fm_tuning_does_not_change_results(cuda, bps):
     torch = _torch()
     n = 90000
     w = gen.dna(31, n, 1)
@@ -189,7 +189,6 @@ def test_fm_tuning_does_not_change_results(cuda, pair, bps):
     L, m = 40, 5000
     fixed = gen.patterns(9, 1, m, L, w, n)
     ref_fixed = ora.count(fixed, np.arange(m, dtype=np.uint64) * L, np.full(m, L, np.uint32))
-    qr.qr_set_tuning("fm_pair", pair)
     qr.qr_set_tuning("fm_blocks_per_sm", bps)
     try:
         d = torch.empty(lens.size, dtype=torch.int32, device=cuda)
@@ -199,9 +198,49 @@ def test_fm_tuning_does_not_change_results(cuda, pair, bps):
         qr.qr_fm_count_work(fm, to_dev(fixed, cuda), None, L, d2, m, work)
         torch.cuda.synchronize()
     finally:
-        qr.qr_set_tuning("fm_pair", 0)
-        qr.qr_set_tuning("fm_blocks_per_sm", 8)
+        qr.qr_set_tuning("fm_blocks_per_sm", 64)
     assert np.array_equal(to_host(d).view(np.uint32), ref)
     assert np.array_equal(to_host(d2).view(np.uint32), ref_fixed)
     ts, tl = ora.work(fixed, np.arange(m, dtype=np.uint64) * L, np.full(m, L, np.uint32), skip=8, block=224)
     assert [int(x) for x in to_host(work)] == [ts, tl]
+
+
+def revcomp(p):
+    return (3 - np.asarray(p, np.uint8)[::-1]).astype(np.uint8)
+
+
+def test_fm_count_both_strands(cuda):
+    """qr_fm_count_both = counts of P and of RC(P), checked against the oracle
+    counting explicitly reverse-complemented copies (RC([0,1]) = [2,3])."""
+    torch = _torch()
+    assert list(revcomp([0, 1])) == [2, 3]
+    n = 150000
+    w = gen.dna(61, n, 1)
+    sym = gen.unpack_dna(w, n)
+    ora = oracle.FmOracle(sym)
+    fm = qr.qr_fm_build(w, n)
+    rng = np.random.default_rng(6)
+    pats = mixed_patterns(rng, sym, 2000)
+    pats += [revcomp(sym[a:a + 40]) for a in rng.integers(0, n - 40, 200)]
+    cat, off, lens = oracle.pack_patterns(pats)
+    rcat, roff, rlens = oracle.pack_patterns([revcomp(p) for p in pats])
+    ref_f, ref_r = ora.count(cat, off, lens), ora.count(rcat, roff, rlens)
+    assert ref_r[-200:].min() >= 1
+    df = torch.empty(lens.size, dtype=torch.int32, device=cuda)
+    dr = torch.empty(lens.size, dtype=torch.int32, device=cuda)
+    qr.qr_fm_count_both(fm, to_dev(cat, cuda), to_dev(lens, cuda), 0, df, dr, lens.size)
+    torch.cuda.synchronize()
+    assert np.array_equal(to_host(df).view(np.uint32), ref_f)
+    assert np.array_equal(to_host(dr).view(np.uint32), ref_r)
+    # fixed-length reads of the paper's shape (150 bp, 1% substitutions, either strand), host path
+    L, m = 150, 3000
+    reads = gen.patterns(7, 2, m, L, w, n)
+    offs = np.arange(m, dtype=np.uint64) * L
+    rr = np.concatenate([revcomp(reads[i * L:(i + 1) * L]) for i in range(m)])
+    ref_f = ora.count(reads, offs, np.full(m, L, np.uint32))
+    ref_r = ora.count(rr, offs, np.full(m, L, np.uint32))
+    hf, hr = np.zeros(m, np.uint32), np.zeros(m, np.uint32)
+    qr.qr_fm_count_both(fm, reads, None, L, hf, hr, m)
+    qr.qr_sync()
+    assert np.array_equal(hf, ref_f) and np.array_equal(hr, ref_r)
+    assert (np.maximum(ref_f, ref_r) >= 1).mean() > 0.1          # error-free reads match one strand

@@ -105,6 +105,17 @@ def test_gen_patterns_recipe():
     for i in range(0, 10, 2):
         pos = (_py_hash(4, 9, i) * (n - 32 + 1)) >> 64
         assert np.array_equal(pats[i], sym[pos:pos + 32])
+    rd = gen.patterns(4, 2, 40, 150, text, n).reshape(40, 150)
+    pm = 0x028F5C28F5C28F5C                                      # QRG_P_MUT = floor(0.01 * 2^64)
+    for i in range(40):
+        pos = (_py_hash(4, 9, i) * (n - 150 + 1)) >> 64
+        exp = sym[pos:pos + 150].copy()
+        for k in range(150):
+            if _py_hash(4, 13, i * 150 + k) < pm:
+                exp[k] = (exp[k] + 1 + ((_py_hash(4, 14, i * 150 + k) * 3) >> 64)) & 3
+        if _py_hash(4, 15, i) & 1:
+            exp = (3 - exp[::-1]).astype(np.uint8)
+        assert np.array_equal(rd[i], exp)
     p5 = gen.patterns(4, 1, 30, 100, text, n).reshape(30, 100)
     for i in range(30):
         pos = (_py_hash(4, 9, i) * (n - 100 + 1)) >> 64
