@@ -107,15 +107,20 @@ class Ctx:
         self.local = int(os.environ.get("LOCAL_RANK", "0"))
         self.args = args
         self.dist = None
+        ndev = max(1, torch.cuda.device_count())
+        self.gpu = self.local % ndev        # one process per GPU; modulo only for the 1-GPU gloo smoke
         if self.world > 1:
             import torch.distributed as dist
 
-            torch.cuda.set_device(self.local)
-            dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
+            torch.cuda.set_device(self.gpu)
+            if args.dist_backend == "nccl":
+                dist.init_process_group("nccl", device_id=torch.device("cuda", self.gpu))
+            else:
+                dist.init_process_group(args.dist_backend)
             self.dist = dist
         else:
             torch.cuda.set_device(0)
-        self.dev = torch.device("cuda", self.local)
+        self.dev = torch.device("cuda", self.gpu)
         self.stream = torch.cuda.current_stream()
 
     def barrier(self):
@@ -170,7 +175,7 @@ def bench_birank(ctx, p: float, steps, warmup, with_ceiling: bool, clocks=None, 
     torch = ctx.torch
     bits = torch.empty((N2 + 63) // 64, dtype=torch.uint64, device=ctx.dev)
     gen.bits_dev(SEED[2] if p == 0.5 else 22, N2, p, bits)
-    h = qr.qr_birank_build(bits, N2, device=ctx.local)
+    h = qr.qr_birank_build(bits, N2, device=ctx.gpu)
     del bits
     m = M2                                         # per GPU (weak scaling)
     i0 = ctx.rank * m
@@ -228,7 +233,7 @@ def bench_quadrank(ctx, steps, warmup):
     torch = ctx.torch
     text = torch.empty((N3 + 31) // 32, dtype=torch.uint64, device=ctx.dev)
     gen.dna_dev(SEED[3], N3, 0, text)
-    h = qr.qr_quadrank_build(text, N3, device=ctx.local)
+    h = qr.qr_quadrank_build(text, N3, device=ctx.gpu)
     del text
     m = M3
     q = torch.empty(m, dtype=torch.uint64, device=ctx.dev)
@@ -256,7 +261,7 @@ def bench_fm(ctx, n, kind, m_total, length, seed, steps, warmup, rank_queries=0)
     text = torch.empty((n + 31) // 32 + 1, dtype=torch.uint64, device=ctx.dev)
     gen.dna_dev(seed, n, kind, text)
     t0 = time.perf_counter()
-    fm = qr.qr_fm_build(text, n, device=ctx.local)
+    fm = qr.qr_fm_build(text, n, device=ctx.gpu)
     build_s = time.perf_counter() - t0
     i0, m = shard(m_total, ctx.world, ctx.rank)
     pats = torch.empty(m * length, dtype=torch.uint8, device=ctx.dev)
@@ -297,7 +302,7 @@ def bench_reads(ctx, n, m_total, length, seed, steps, warmup):
     torch = ctx.torch
     text = torch.empty((n + 31) // 32 + 1, dtype=torch.uint64, device=ctx.dev)
     gen.dna_dev(seed, n, 1, text)
-    fm = qr.qr_fm_build(text, n, device=ctx.local)
+    fm = qr.qr_fm_build(text, n, device=ctx.gpu)
     i0, m = shard(m_total, ctx.world, ctx.rank)
     pats = torch.empty(m * length, dtype=torch.uint8, device=ctx.dev)
     gen.patterns_dev(seed, 2, m, length, text, n, pats, i0=i0)
@@ -319,7 +324,7 @@ def bench_small(ctx, steps, warmup):
     torch = ctx.torch
     bits = torch.empty((N1 + 63) // 64, dtype=torch.uint64, device=ctx.dev)
     gen.bits_dev(SEED[1], N1, 0.5, bits)
-    h = qr.qr_birank_build(bits, N1, device=ctx.local)
+    h = qr.qr_birank_build(bits, N1, device=ctx.gpu)
     q = torch.empty(M1, dtype=torch.uint64, device=ctx.dev)
     gen.queries_dev(SEED[1], N1, M1, q, i0=ctx.rank * M1)
     out = torch.empty_like(q)
@@ -393,6 +398,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--rows", default="all", choices=["all", "headline"])
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="process-group backend (gloo only to smoke-test the multi-rank path on one GPU)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
@@ -402,7 +409,7 @@ def main():
     ctx = Ctx(args)
     K, W = args.steps, max(3, args.warmup)
     peak, peak_src = peaks()
-    clocks = Clocks(ctx.local)
+    clocks = Clocks(ctx.gpu)
     wall0 = time.perf_counter()
     c2 = bench_birank(ctx, 0.5, K, W, with_ceiling=True, clocks=clocks, e2e=True)
     rows = {}

@@ -108,6 +108,15 @@ qr_status qr_fm_count(const qr_fm* fm, const uint8_t* patterns, const uint32_t* 
 qr_status qr_fm_count_both(const qr_fm* fm, const uint8_t* patterns, const uint32_t* lengths, uint32_t fixed_len,
                            uint32_t* out_fwd, uint32_t* out_rc, uint64_t m, void* stream);
 
+/* Approximate counting (NEXT §8(f)3; rank_4's motivation): out[k] = number of
+ * text positions where pattern k matches with at most max_mismatches substitutions (Hamming
+ * distance; 0 or 1 — QR_EINVAL otherwise).  max_mismatches = 1 branches on every pattern
+ * position with one rank_4 at lo and one at hi (the four extensions of the exact interval) and
+ * reads the 24 single-substitution variants of the last 8 symbols from the 8-mer table.
+ * Arguments and memory spaces as qr_fm_count. */
+qr_status qr_fm_count_approx(const qr_fm* fm, const uint8_t* patterns, const uint32_t* lengths, uint32_t fixed_len,
+                             uint32_t max_mismatches, uint32_t* out, uint64_t m, void* stream);
+
 /* As qr_fm_count (device pointers only), additionally accumulating into work[0] the number of
  * backward steps executed after seeding and into work[1] the number of distinct 64-B lines
  * those steps touch (1 or 2 per step) — the algorithmic-bytes denominator of SURVEY §8(d).

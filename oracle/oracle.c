@@ -272,4 +272,25 @@ EXPORT void or_scan_count(const uint8_t* s, uint64_t n, const uint8_t* pat, cons
   }
 }
 
+/* Approximate occurrences (NEXT §8(f)3; the paper's motivation for rank_4):
+ * the number of text positions i in [0, n-L] where s[i..i+L) differs from P in at most one
+ * symbol (Hamming distance <= 1).  Direct scan of every position.  L = 0 counts n+1. */
+EXPORT void or_scan_count_hd1(const uint8_t* s, uint64_t n, const uint8_t* pat, const uint64_t* off,
+                              const uint32_t* len, uint64_t m, uint32_t* out) {
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int64_t k = 0; k < (int64_t)m; ++k) {
+    const uint8_t* P = pat + off[k];
+    uint32_t L = len[k];
+    uint64_t cnt = 0;
+    if (L == 0) cnt = n + 1;
+    else if (L <= n)
+      for (uint64_t i = 0; i + L <= n; ++i) {
+        uint32_t mism = 0;
+        for (uint32_t j = 0; j < L && mism <= 1; ++j) mism += (s[i + j] != P[j]);
+        cnt += (mism <= 1);
+      }
+    out[k] = (uint32_t)cnt;
+  }
+}
+
 EXPORT int or_threads(void) { return omp_get_max_threads(); }

@@ -24,7 +24,7 @@ _STATUS = {1: "QR_EINVAL", 2: "QR_ECAPACITY", 3: "QR_ENOMEM", 4: "QR_ECUDA"}
 
 # every symbol include/qrank.h declares (tests check the .so exports all of them)
 EXPORTS = (
-    "qr_birank_build", "qr_quadrank_build", "qr_rank", "qr_rank_all4", "qr_fm_build", "qr_fm_count", "qr_fm_count_both",
+    "qr_birank_build", "qr_quadrank_build", "qr_rank", "qr_rank_all4", "qr_fm_build", "qr_fm_count", "qr_fm_count_both", "qr_fm_count_approx",
     "qr_fm_count_work", "qr_gather_ceiling", "qr_info", "qr_export_layout", "qr_fm_info", "qr_fm_export_kmer",
     "qr_clone_to_device", "qr_fm_clone_to_device", "qr_sync", "qr_free", "qr_fm_free", "qr_last_error",
     "qr_version", "qr_set_tuning",
@@ -58,6 +58,7 @@ def lib():
             "qr_fm_count": ([V, V, V, U32, V, U64, V], I32),
             "qr_fm_count_work": ([V, V, V, U32, V, U64, V, V], I32),
             "qr_fm_count_both": ([V, V, V, U32, V, V, U64, V], I32),
+            "qr_fm_count_approx": ([V, V, V, U32, U32, V, U64, V], I32),
             "qr_gather_ceiling": ([V, V, V, U64, I32, V], I32),
             "qr_info": ([V, C.POINTER(U64), C.POINTER(C.c_int), C.POINTER(U64), C.POINTER(U64)], I32),
             "qr_export_layout": ([V, V, V], I32),
@@ -200,6 +201,12 @@ def qr_fm_count_both(fm: Fm, patterns, lengths, fixed_len: int, out_fwd, out_rc,
     _check(lib().qr_fm_count_both(fm.ptr, _ptr(patterns), _ptr(lengths), fixed_len, _ptr(out_fwd), _ptr(out_rc), m,
                                   _stream(stream)), "qr_fm_count_both")
     return out_fwd, out_rc
+
+
+def qr_fm_count_approx(fm: Fm, patterns, lengths, fixed_len: int, max_mismatches: int, out, m: int, stream=None):
+    _check(lib().qr_fm_count_approx(fm.ptr, _ptr(patterns), _ptr(lengths), fixed_len, max_mismatches, _ptr(out), m,
+                                    _stream(stream)), "qr_fm_count_approx")
+    return out
 
 
 def qr_fm_count_work(fm: Fm, patterns, lengths, fixed_len: int, out, m: int, work, stream=None):

@@ -397,7 +397,8 @@ QR_EXPORT qr_status qr_fm_build(const uint64_t* text2b, uint64_t n, const uint32
 }
 
 static qr_status fm_count_impl(const qr_fm* fm, const uint8_t* patterns, const uint32_t* lengths, uint32_t fixed_len,
-                               uint32_t* out, uint32_t* out_rc, uint64_t m, uint64_t* work, void* stream) {
+                               uint32_t* out, uint32_t* out_rc, uint64_t m, uint64_t* work, void* stream,
+                               int approx = 0) {
   if (!fm) return fail(QR_EINVAL, "qr_fm_count: null handle");
   if (m == 0) return QR_OK;
   if (!out || (!patterns && (lengths || fixed_len))) return fail(QR_EINVAL, "qr_fm_count: null pointer");
@@ -407,7 +408,7 @@ static qr_status fm_count_impl(const qr_fm* fm, const uint8_t* patterns, const u
   static const uint8_t dummy = 0;
   int sp = classify({patterns, lengths, out, out_rc, work}, fm->bwt->device);
   if (sp < 0) return fail(QR_EINVAL, "qr_fm_count: pointers must all be device (device %d) or all host", fm->bwt->device);
-  if (sp == 1) return fm_count_device(fm, pat ? pat : &dummy, lengths, fixed_len, out, out_rc, m, work, st);
+  if (sp == 1) return fm_count_device(fm, pat ? pat : &dummy, lengths, fixed_len, out, out_rc, m, work, st, approx);
   if (work) return fail(QR_EINVAL, "qr_fm_count_work: device pointers only");
   if (!lengths) {
     std::vector<StageArray> arr = {{patterns, nullptr, (size_t)fixed_len}, {nullptr, out, 4}};
@@ -415,7 +416,7 @@ static qr_status fm_count_impl(const qr_fm* fm, const uint8_t* patterns, const u
     if (out_rc) arr.push_back({nullptr, out_rc, 4});
     return run_staged(fm->bwt->device, st, m, arr, [&](const std::vector<void*>& d, uint64_t cnt, cudaStream_t s) {
       return fm_count_device(fm, (const uint8_t*)d[0], nullptr, fixed_len, (uint32_t*)d[1],
-                             out_rc ? (uint32_t*)d[2] : nullptr, cnt, nullptr, s);
+                             out_rc ? (uint32_t*)d[2] : nullptr, cnt, nullptr, s, approx);
     });
   }
   // variable lengths from host: one whole copy (offsets depend on every earlier length)
@@ -431,7 +432,7 @@ static qr_status fm_count_impl(const qr_fm* fm, const uint8_t* patterns, const u
   }
   if (total) cudaMemcpyAsync(dp, patterns, total, cudaMemcpyHostToDevice, st);
   cudaMemcpyAsync(dl, lengths, m * 4, cudaMemcpyHostToDevice, st);
-  qr_status s = fm_count_device(fm, dp, dl, 0, dout, out_rc ? dout + m : nullptr, m, nullptr, st);
+  qr_status s = fm_count_device(fm, dp, dl, 0, dout, out_rc ? dout + m : nullptr, m, nullptr, st, approx);
   if (s == QR_OK) {
     cudaMemcpyAsync(out, dout, m * 4, cudaMemcpyDeviceToHost, st);
     if (out_rc) cudaMemcpyAsync(out_rc, dout + m, m * 4, cudaMemcpyDeviceToHost, st);
@@ -443,6 +444,13 @@ static qr_status fm_count_impl(const qr_fm* fm, const uint8_t* patterns, const u
 QR_EXPORT qr_status qr_fm_count(const qr_fm* fm, const uint8_t* patterns, const uint32_t* lengths, uint32_t fixed_len,
                                 uint32_t* out, uint64_t m, void* stream) {
   return fm_count_impl(fm, patterns, lengths, fixed_len, out, nullptr, m, nullptr, stream);
+}
+
+QR_EXPORT qr_status qr_fm_count_approx(const qr_fm* fm, const uint8_t* patterns, const uint32_t* lengths,
+                                       uint32_t fixed_len, uint32_t max_mismatches, uint32_t* out, uint64_t m,
+                                       void* stream) {
+  if (max_mismatches > 1) return fail(QR_EINVAL, "qr_fm_count_approx: max_mismatches must be 0 or 1");
+  return fm_count_impl(fm, patterns, lengths, fixed_len, out, nullptr, m, nullptr, stream, (int)max_mismatches);
 }
 
 QR_EXPORT qr_status qr_fm_count_both(const qr_fm* fm, const uint8_t* patterns, const uint32_t* lengths,

@@ -355,6 +355,110 @@ __global__ void __launch_bounds__(256, 4) k_fm_count(FmParams F, const uint8_t* 
   }
 }
 
+// ---- approximate counting with <= 1 substitution (NEXT §8(f)3) ---------------------------
+// The paper motivates rank_4 by approximate matching in an FM index: one
+// rank_4 at lo and one at hi give the four extensions of an interval at once.  A text position
+// matches P with at most one substitution in exactly one way (exactly, or with the single
+// mismatch at a unique position j and text symbol c), so
+//   count_{<=1}(P) = |exact interval| + sum_j sum_{c != P[j]} |backward search of P[0..j) from
+//                    extend(I_{j+1}, c)|,
+// where I_{j+1} is the exact interval of P[j+1..).  Mismatches inside the pattern's last 8
+// symbols read their extended interval straight from the 8-mer table (24 substituted keys);
+// the others branch from the exact path with rank_4.  Each branch continues as an exact
+// backward search and usually dies within a few steps.
+
+// rank_4 over the BWT at row x (Occ of all four symbols, '$' correction on A).
+__device__ __forceinline__ void fm_occ4(const FmParams& F, uint32_t x, uint32_t occ[4]) {
+  uint32_t j = (x >> 5) / 7u;
+  j = j > (uint32_t)F.last_line ? (uint32_t)F.last_line : j;
+  const uint32_t p = 32u + x - j * (uint32_t)QD_B;
+  const uint4* L = F.lines + 4 * (uint64_t)j;
+  uint64_t a[4], b[4] = {0, 0, 0, 0};
+  ld_sector(L, a[0], a[1], a[2], a[3]);
+  if (p >= 128) ld_sector(L + 2, b[0], b[1], b[2], b[3]);
+  const uint4 sv = __ldg(reinterpret_cast<const uint4*>(F.super) + (j >> QD_SB_LOG));
+  const bool right = p >= 128;
+  const int xx = (int)(p & 127u);
+  const uint64_t inv = right ? 0ull : ~0ull;
+  const uint64_t* w = right ? b : a;
+  uint32_t nl = 0, nh = 0, nt = 0;
+#pragma unroll
+  for (int t = 0; t < 2; ++t) {
+    uint64_t msk = prefix_mask(xx, t) ^ inv;
+    uint64_t l = ~w[2 * t] & msk, hh = ~w[2 * t + 1] & msk;
+    nl += __popcll(l);
+    nh += __popcll(hh);
+    nt += __popcll(l & hh);
+  }
+  const uint32_t len = right ? (uint32_t)xx : 128u - (uint32_t)xx;
+  const uint32_t cnt[4] = {len - nl - nh + nt, nl - nt, nh - nt, nt};
+  const uint32_t s4[4] = {sv.x, sv.y, sv.z, sv.w};
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const uint64_t dw = (c & 2) ? a[1] : a[0];
+    const uint32_t base = (s4[c] << QD_SHIFT) + (uint32_t)((dw >> (16 * (c & 1))) & 0xffffull);
+    occ[c] = right ? base + cnt[c] : base - cnt[c];
+  }
+  occ[0] -= (x > (uint32_t)F.spos);
+}
+
+// exact backward search of P[0..k] from [lo, hi); returns the final interval size
+__device__ __forceinline__ uint32_t fm_continue(const FmParams& F, PatWindow& P, int64_t k, uint32_t lo, uint32_t hi) {
+  uint32_t nl;
+  for (; k >= 0 && lo < hi; --k) fm_step(F, P.at(k), lo, hi, nl);
+  return lo < hi ? hi - lo : 0u;
+}
+
+template <bool FIXED>
+__global__ void __launch_bounds__(256) k_fm_approx1(FmParams F, const uint8_t* __restrict__ pat,
+                                                    const uint64_t* __restrict__ offs,
+                                                    const uint32_t* __restrict__ lens, uint32_t fixed_len,
+                                                    uint32_t* __restrict__ out, uint64_t m) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  const uint4 C4 = __ldg(reinterpret_cast<const uint4*>(F.Ct));
+  const uint32_t Cs[4] = {C4.x, C4.y, C4.z, C4.w};
+  for (uint64_t pi = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; pi < m; pi += stride) {
+    const uint32_t len = FIXED ? fixed_len : lens[pi];
+    const uint8_t* p = pat + (FIXED ? pi * (uint64_t)fixed_len : offs[pi]);
+    PatWindow P;
+    P.reset(p);
+    uint64_t total = 0;
+    uint32_t lo, hi;
+    int64_t j;
+    if (len >= 8) {
+      const uint32_t key0 = kmer_key8(p + len - 8);
+      for (int t = 0; t < 8; ++t) {                       // one substitution among the last 8 symbols
+        const uint32_t f = (key0 >> (2 * t)) & 3u;
+        for (uint32_t r = 1; r < 4; ++r) {
+          const uint2 iv = __ldg(F.kmer + (key0 ^ ((f ^ ((f + r) & 3u)) << (2 * t))));
+          if (iv.x < iv.y) total += fm_continue(F, P, (int64_t)len - 9, iv.x, iv.y);
+        }
+      }
+      const uint2 iv0 = __ldg(F.kmer + key0);
+      lo = iv0.x; hi = iv0.y;
+      j = (int64_t)len - 9;
+    } else {
+      lo = 0; hi = (uint32_t)F.N;
+      j = (int64_t)len - 1;
+    }
+    for (; j >= 0 && lo < hi; --j) {                     // exact path; branch on the mismatch at j
+      uint32_t ol[4], oh[4];
+      fm_occ4(F, lo, ol);
+      fm_occ4(F, hi, oh);
+      const uint32_t cj = P.at(j);
+#pragma unroll
+      for (uint32_t c = 0; c < 4; ++c) {
+        const uint32_t a = Cs[c] + ol[c], b = Cs[c] + oh[c];
+        if (c != cj && a < b) total += fm_continue(F, P, j - 1, a, b);
+      }
+      lo = Cs[cj] + ol[cj];
+      hi = Cs[cj] + oh[cj];
+    }
+    if (lo < hi) total += hi - lo;
+    out[pi] = (uint32_t)total;
+  }
+}
+
 __global__ void k_u32_to_u64(const uint32_t* __restrict__ a, uint64_t* __restrict__ b, uint64_t m) {
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m; i += (uint64_t)gridDim.x * blockDim.x)
     b[i] = a[i];
@@ -384,7 +488,7 @@ static void launch_fm(unsigned g, cudaStream_t st, const FmParams& F, const uint
 }
 
 qr_status fm_count_device(const qr_fm* fm, const uint8_t* pat, const uint32_t* lengths, uint32_t fixed_len,
-                          uint32_t* out, uint32_t* out_rc, uint64_t m, uint64_t* work, cudaStream_t st) {
+                          uint32_t* out, uint32_t* out_rc, uint64_t m, uint64_t* work, cudaStream_t st, int approx) {
   if (m == 0) return QR_OK;
   FmParams F = params_of(fm);
   const int sms = fm->bwt->sm_count;
@@ -393,7 +497,8 @@ qr_status fm_count_device(const qr_fm* fm, const uint8_t* pat, const uint32_t* l
   unsigned long long* w = reinterpret_cast<unsigned long long*>(work);
   cudaError_t e;
   if (!lengths) {
-    if (work) launch_fm<true, true>(g, st, F, pat, nullptr, nullptr, fixed_len, out, out_rc, m, w);
+    if (approx) k_fm_approx1<true><<<g, 256, 0, st>>>(F, pat, nullptr, nullptr, fixed_len, out, m);
+    else if (work) launch_fm<true, true>(g, st, F, pat, nullptr, nullptr, fixed_len, out, out_rc, m, w);
     else      launch_fm<true, false>(g, st, F, pat, nullptr, nullptr, fixed_len, out, out_rc, m, w);
     if ((e = cudaGetLastError())) return cuda_fail(e, "k_fm_count");
     return QR_OK;
@@ -408,7 +513,8 @@ qr_status fm_count_device(const qr_fm* fm, const uint8_t* pat, const uint32_t* l
   if ((e = cub::DeviceScan::ExclusiveSum(tmp, tb, offs, offs, (int64_t)m, st))) {
     cudaFreeAsync(offs, st); cudaFreeAsync(tmp, st); return cuda_fail(e, "scan");
   }
-  if (work) launch_fm<false, true>(g, st, F, pat, offs, lengths, 0, out, out_rc, m, w);
+  if (approx) k_fm_approx1<false><<<g, 256, 0, st>>>(F, pat, offs, lengths, 0, out, m);
+  else if (work) launch_fm<false, true>(g, st, F, pat, offs, lengths, 0, out, out_rc, m, w);
   else      launch_fm<false, false>(g, st, F, pat, offs, lengths, 0, out, out_rc, m, w);
   e = cudaGetLastError();
   cudaFreeAsync(offs, st);

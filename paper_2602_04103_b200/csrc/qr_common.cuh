@@ -71,7 +71,8 @@ cudaError_t launch_quadrank_rank(const qr_index* h, const uint64_t* q, const uin
 cudaError_t launch_quadrank_all4(const qr_index* h, const uint64_t* q, uint64_t* out4, uint64_t m, cudaStream_t st);
 cudaError_t launch_gather(const qr_index* h, const uint64_t* q, uint64_t* out, uint64_t m, int mode, cudaStream_t st);
 qr_status fm_count_device(const qr_fm* fm, const uint8_t* pat, const uint32_t* lengths, uint32_t fixed_len,
-                          uint32_t* out, uint32_t* out_rc, uint64_t m, uint64_t* work, cudaStream_t st);
+                          uint32_t* out, uint32_t* out_rc, uint64_t m, uint64_t* work, cudaStream_t st,
+                          int approx = 0);
 qr_status birank_build_device(const uint64_t* d_bits, uint64_t n, int device, cudaStream_t st, qr_index** out);
 
 // grid for a grid-stride kernel: a multiple of the SM count

@@ -244,3 +244,44 @@ def test_fm_count_both_strands(cuda):
     qr.qr_sync()
     assert np.array_equal(hf, ref_f) and np.array_equal(hr, ref_r)
     assert (np.maximum(ref_f, ref_r) >= 1).mean() > 0.1          # error-free reads match one strand
+
+
+@pytest.mark.parametrize("n,kind", [(1, 0), (30, 0), (1000, 0), (60000, 1), (131072 + 5, 0)])
+def test_fm_count_approx_one_mismatch(cuda, n, kind):
+    """<=1-substitution counts (rank_4-driven branching + 8-mer table variants) vs the oracle's
+    direct Hamming-distance scan; max_mismatches=0 equals exact counting."""
+    torch = _torch()
+    w = gen.dna(71 + n, n, kind)
+    sym = gen.unpack_dna(w, n)
+    fm = qr.qr_fm_build(w, n)
+    rng = np.random.default_rng(n)
+    pats = mixed_patterns(rng, sym, 1200)
+    for _ in range(200):                                   # exact and 1-/2-substitution variants
+        L = int(rng.integers(1, 40)); a = int(rng.integers(0, max(1, n - L + 1)))
+        p = sym[a:a + L].copy()
+        for _s in range(int(rng.integers(0, 3))):
+            if p.size:
+                k = int(rng.integers(0, p.size)); p[k] = (p[k] + 1 + rng.integers(0, 3)) % 4
+        pats.append(p)
+    cat, off, lens = oracle.pack_patterns(pats)
+    ref1 = oracle.scan_count_hd1(sym, cat, off, lens)
+    ref0 = oracle.scan_count(sym, cat, off, lens)
+    d1 = torch.empty(lens.size, dtype=torch.int32, device=cuda)
+    d0 = torch.empty(lens.size, dtype=torch.int32, device=cuda)
+    qr.qr_fm_count_approx(fm, to_dev(cat, cuda), to_dev(lens, cuda), 0, 1, d1, lens.size)
+    qr.qr_fm_count_approx(fm, to_dev(cat, cuda), to_dev(lens, cuda), 0, 0, d0, lens.size)
+    torch.cuda.synchronize()
+    got1 = to_host(d1).view(np.uint32)
+    bad = np.nonzero(got1 != ref1)[0]
+    assert bad.size == 0, f"{bad.size} mismatches: {[(len(pats[i]), got1[i], ref1[i]) for i in bad[:5]]}"
+    assert np.array_equal(to_host(d0).view(np.uint32), ref0)
+    assert np.all(ref1 >= ref0)
+    # fixed-length host path
+    L, m = 24, 2000
+    fx = gen.patterns(3, 1, m, L, w, n)
+    h = np.zeros(m, np.uint32)
+    qr.qr_fm_count_approx(fm, fx, None, L, 1, h, m)
+    qr.qr_sync()
+    assert np.array_equal(h, oracle.scan_count_hd1(sym, fx, np.arange(m, dtype=np.uint64) * L, np.full(m, L, np.uint32)))
+    with pytest.raises(qr.QrError):
+        qr.qr_fm_count_approx(fm, fx, None, L, 2, h, m)

@@ -268,3 +268,28 @@ def test_fm_work_instrumentation_consistent():
     assert ts == int(steps.sum())
     assert ts <= tl <= 2 * ts
     assert np.array_equal(cnt[0::2] >= 1, np.ones(100, bool))    # exact substrings occur
+
+
+def test_hd1_scan_vs_bruteforce_and_variant_sum():
+    """<=1-substitution counts: Python brute force on tiny texts, and the identity
+    count_hd1(P) = sum over P and its 3L single-substitution variants of the exact count."""
+    rng = np.random.default_rng(12)
+    for t in range(12):
+        n = int(rng.integers(1, 300))
+        sym = rng.integers(0, 4, n).astype(np.uint8) if t % 2 else np.tile(rng.integers(0, 4, 2), 200)[:n].astype(np.uint8)
+        f = oracle.FmOracle(sym)
+        pats = [rng.integers(0, 4, int(rng.integers(0, 10))).astype(np.uint8) for _ in range(25)]
+        pats += [sym[a:a + 6].copy() for a in rng.integers(0, n, 10)]
+        cat, off, lens = oracle.pack_patterns(pats)
+        got = oracle.scan_count_hd1(sym, cat, off, lens)
+        for p, g in zip(pats, got):
+            L = len(p)
+            if L == 0:
+                assert g == n + 1
+                continue
+            brute = sum(1 for i in range(n - L + 1) if int((sym[i:i + L] != p).sum()) <= 1)
+            assert g == brute
+            variants = [p] + [np.concatenate([p[:j], [(p[j] + d) % 4], p[j + 1:]]).astype(np.uint8)
+                              for j in range(L) for d in (1, 2, 3)]
+            vc, vo, vl = oracle.pack_patterns(variants)
+            assert int(f.count(vc, vo, vl).astype(np.int64).sum()) == g
