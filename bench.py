@@ -317,6 +317,27 @@ def bench_reads(ctx, n, m_total, length, seed, steps, warmup):
             "read_len": length, "reads": m_total, "frac_reads_matching": hit / max(m, 1)}
 
 
+def bench_approx(ctx, n, m_total, length, seed, steps, warmup):
+    """<=1-substitution counting (rank_4-driven, NEXT §8(f)3) on the configs[3] text/patterns."""
+    import gen
+    import paper_2602_04103_b200 as qr
+
+    torch = ctx.torch
+    text = torch.empty((n + 31) // 32 + 1, dtype=torch.uint64, device=ctx.dev)
+    gen.dna_dev(seed, n, 0, text)
+    fm = qr.qr_fm_build(text, n, device=ctx.gpu)
+    i0, m = shard(m_total, ctx.world, ctx.rank)
+    pats = torch.empty(m * length, dtype=torch.uint8, device=ctx.dev)
+    gen.patterns_dev(seed, 0, m, length, text, n, pats, i0=i0)
+    out = torch.empty(m, dtype=torch.int32, device=ctx.dev)
+    ms = ctx.timed(lambda: qr.qr_fm_count_approx(fm, pats, None, length, 1, out, m, ctx.stream), steps, warmup)
+    fm.free()
+    del text, pats, out
+    torch.cuda.empty_cache()
+    return {"ms": ms, "patterns_per_s": m_total / ms * 1e3, "max_mismatches": 1, "patterns": m_total,
+            "pattern_len": length}
+
+
 def bench_small(ctx, steps, warmup):
     import gen
     import paper_2602_04103_b200 as qr
@@ -419,6 +440,7 @@ def main():
         rows["c4_quadfm"] = bench_fm(ctx, N4, 0, M4, L4, SEED[4], K, W)
         rows["c5_quadfm"] = bench_fm(ctx, N5, 1, M5, L5, SEED[5], K, W, rank_queries=10**9)
         rows["c5_reads_150bp_both_strands"] = bench_reads(ctx, N5, 10**7, 150, 55, K, W)
+        rows["c4_quadfm_approx1"] = bench_approx(ctx, N4, 10**6, L4, SEED[4], K, W)
         rows["c1_small"] = bench_small(ctx, K, W)
     ms = c2["ms"]
     value = c2["gq_s"]
