@@ -165,6 +165,7 @@ const char* qr_last_error(void);
  * them): "rank_k" (1, 2, 4 or 8 independent queries per thread per iteration),
  * "rank_blocks_per_sm" and "fm_blocks_per_sm" (256-thread CTAs per SM of the grid-stride
  * rank / FM kernels, 1..64), "stage_chunk" (queries per chunk of the staged host path),
+ * "stage_slots" (2..4 device buffers / internal streams of the staged host path),
  * "l2_fetch_granularity" (cudaLimitMaxL2FetchGranularity of the current device, bytes).
  * QR_EINVAL for an unknown key or out-of-range value. */
 qr_status qr_set_tuning(const char* key, int64_t value);

@@ -23,7 +23,8 @@ int g_rank_blocks_per_sm = 64;  // 256-thread CTAs per SM of the grid (several w
 int g_fm_blocks_per_sm = 64;    // 256-thread CTAs per SM of the FM grid (several waves)
 int g_rank_s_lane = 1;          // lane of a pair that loads the superblock word
 int g_rank_pair = 1;            // 1: lane-pair kernels (one L2 request per query); 0: one lane per query
-uint64_t g_stage_chunk = 1ull << 24;   // queries per chunk on the staged host path
+uint64_t g_stage_chunk = 1ull << 23;   // queries per chunk on the staged host path (sweep: profiles/r01_e2e_sweep)
+int g_stage_slots = 3;                 // device buffers / internal streams of the staged path
 
 static thread_local char t_err[512] = "";
 
@@ -126,14 +127,15 @@ static qr_status stage_input(const uint64_t* src, uint64_t words, uint64_t padde
 }
 
 // ---- staged host-pointer pipeline ----------------------------------------------------------
-// Two slots, one internal stream each: chunk k uses slot k%2 on stream k%2, so the H2D copy
-// and kernel of one chunk overlap the kernel and D2H copy of the other (separate copy
+// S slots (default 2), one internal stream each: chunk k uses slot k%S on stream k%S, so the H2D
+// copy and kernel of one chunk overlap the kernel and D2H copy of the others (separate copy
 // engines).  In-order streams make slot reuse safe across chunks and across calls.
+constexpr int MAX_SLOTS = 4;
 struct Stager {
   std::mutex mu;
-  cudaStream_t s[2] = {nullptr, nullptr};
-  cudaEvent_t ev_start = nullptr, ev_done[2] = {nullptr, nullptr};
-  void* buf[2] = {nullptr, nullptr};
+  cudaStream_t s[MAX_SLOTS] = {};
+  cudaEvent_t ev_start = nullptr, ev_done[MAX_SLOTS] = {};
+  void* buf[MAX_SLOTS] = {};
   size_t cap = 0;
 };
 static std::mutex g_stagers_mu;
@@ -144,7 +146,7 @@ static Stager* stager_for(int device) {
   if ((int)g_stagers.size() <= device) g_stagers.resize(device + 1, nullptr);
   if (!g_stagers[device]) {
     Stager* S = new Stager();
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < MAX_SLOTS; ++i) {
       cudaStreamCreateWithFlags(&S->s[i], cudaStreamNonBlocking);
       cudaEventCreateWithFlags(&S->ev_done[i], cudaEventDisableTiming);
     }
@@ -168,24 +170,24 @@ static qr_status run_staged(int device, cudaStream_t user, uint64_t m, const std
   size_t per_item = 0;
   for (auto& a : arrays) per_item += (a.item_bytes + 15) & ~size_t(15);
   const uint64_t chunk = g_stage_chunk;
+  const int nslot = g_stage_slots;
   const size_t need = per_item * (size_t)(m < chunk ? m : chunk) + 256 * arrays.size();
   cudaError_t e;
-  if (S->cap < need) {
-    for (int i = 0; i < 2; ++i) {
+  if (S->cap < need || !S->buf[nslot - 1]) {
+    for (int i = 0; i < MAX_SLOTS; ++i) {
       if (S->buf[i]) { cudaStreamSynchronize(S->s[i]); cudaFree(S->buf[i]); S->buf[i] = nullptr; }
     }
     S->cap = 0;
-    for (int i = 0; i < 2; ++i)
+    for (int i = 0; i < nslot; ++i)
       if ((e = cudaMalloc(&S->buf[i], need))) return cuda_fail(e, "alloc staging buffers");
     S->cap = need;
   }
   cudaEventRecord(S->ev_start, user);                   // respect work already queued on `user`
-  cudaStreamWaitEvent(S->s[0], S->ev_start, 0);
-  cudaStreamWaitEvent(S->s[1], S->ev_start, 0);
+  for (int i = 0; i < nslot; ++i) cudaStreamWaitEvent(S->s[i], S->ev_start, 0);
   uint64_t k = 0;
   for (uint64_t lo = 0; lo < m; lo += chunk, ++k) {
     const uint64_t cnt = (m - lo < chunk) ? m - lo : chunk;
-    const int slot = (int)(k & 1);
+    const int slot = (int)(k % (uint64_t)nslot);
     cudaStream_t st = S->s[slot];
     char* base = static_cast<char*>(S->buf[slot]);
     std::vector<void*> dptr(arrays.size());
@@ -206,7 +208,7 @@ static qr_status run_staged(int device, cudaStream_t user, uint64_t m, const std
                                cnt * arrays[a].item_bytes, cudaMemcpyDeviceToHost, st)))
         return cuda_fail(e, "staged D2H");
   }
-  for (int i = 0; i < 2; ++i) {
+  for (int i = 0; i < nslot; ++i) {
     cudaEventRecord(S->ev_done[i], S->s[i]);
     cudaStreamWaitEvent(user, S->ev_done[i], 0);
   }
@@ -257,6 +259,9 @@ QR_EXPORT qr_status qr_set_tuning(const char* key, int64_t value) {
     // cudaLimitMaxL2FetchGranularity of the current device (0..128 B; a hint to the L2)
     cudaError_t e = cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)value);
     if (e) return cuda_fail(e, "qr_set_tuning l2_fetch_granularity");
+  } else if (!strcmp(key, "stage_slots")) {
+    if (value < 2 || value > MAX_SLOTS) return fail(QR_EINVAL, "stage_slots must be 2..4");
+    g_stage_slots = (int)value;
   } else if (!strcmp(key, "stage_chunk")) {
     if (value < 1024) return fail(QR_EINVAL, "stage_chunk too small");
     g_stage_chunk = (uint64_t)value;

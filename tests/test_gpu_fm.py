@@ -156,7 +156,7 @@ def test_fm_given_sa_and_fixed_length_and_work(cuda):
         qr.qr_fm_count(fm_gpu_sa, pats, None, L, h, m)
         qr.qr_sync()
     finally:
-        qr.qr_set_tuning("stage_chunk", 1 << 24)
+        qr.qr_set_tuning("stage_chunk", 1 << 23)
     assert np.array_equal(h, ref)
 
 

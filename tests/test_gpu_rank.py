@@ -100,7 +100,7 @@ def test_birank_device_input_and_host_query_path(cuda):
         qr.qr_rank(h, q, None, out_h)                            # host pointers: staged path
         qr.qr_sync()
     finally:
-        qr.qr_set_tuning("stage_chunk", 1 << 24)
+        qr.qr_set_tuning("stage_chunk", 1 << 23)
     assert np.array_equal(out_h, ref)
     qp = torch.from_numpy(q).pin_memory()
     op = torch.zeros_like(qp).pin_memory()
@@ -280,7 +280,7 @@ def test_quadrank_host_path_and_c_mod4(cuda):
         qr.qr_rank_all4(h, q, out4)
         qr.qr_sync()
     finally:
-        qr.qr_set_tuning("stage_chunk", 1 << 24)
+        qr.qr_set_tuning("stage_chunk", 1 << 23)
     assert np.array_equal(out, ora.rank(q, c))
     assert np.array_equal(out4, ora.rank_all4(q))
 
@@ -299,3 +299,43 @@ def test_errors_surface(cuda):
         qr.qr_rank(hq, q, None, o4[:10])                        # sigma=4 needs c
     with pytest.raises(qr.QrError):
         qr.qr_rank(hq, q, np.zeros(10, np.uint8), o4[:10])      # mixed host/device pointers
+
+
+def test_edge_cases_and_contract(cuda):
+    """m = 0 is a no-op; q > n is memory-safe (clamped line); a cloned handle answers identically."""
+    torch = _torch()
+    n = 2 * S + 3
+    w = gen.bits(5, n)
+    h = qr.qr_birank_build(w, n)
+    empty = torch.empty(0, dtype=torch.uint64, device=cuda)
+    qr.qr_rank(h, empty, None, empty)                              # m = 0
+    big = to_dev(np.array([n + 1, n + 496, 2 * n, (1 << 40)], np.uint64), cuda)
+    ob = torch.empty_like(big)
+    qr.qr_rank(h, big, None, ob)                                   # contract violation: must not fault
+    qr.qr_sync()
+    h2 = qr.qr_clone_to_device(h, 0)
+    q = gen.queries(9, n, 50000)
+    o1 = torch.empty(q.size, dtype=torch.uint64, device=cuda)
+    o2 = torch.empty_like(o1)
+    qr.qr_rank(h, to_dev(q, cuda), None, o1)
+    qr.qr_rank(h2, to_dev(q, cuda), None, o2)
+    torch.cuda.synchronize()
+    assert np.array_equal(to_host(o1), to_host(o2))
+    assert np.array_equal(to_host(o1), oracle.BitsOracle(w, n).rank(q))
+    n4 = 3 * S4 + 9
+    t = gen.dna(6, n4)
+    h4 = qr.qr_quadrank_build(t, n4)
+    qb = to_dev(np.array([n4 + 1, 10 * n4], np.uint64), cuda)
+    qr.qr_rank(h4, qb, to_dev(np.array([1, 3], np.uint8), cuda), torch.empty_like(qb))
+    qr.qr_rank_all4(h4, qb, torch.empty((2, 4), dtype=torch.uint64, device=cuda))
+    qr.qr_sync()
+    fm = qr.qr_fm_build(t, n4)
+    fm2 = qr.qr_fm_clone_to_device(fm, 0)
+    pats = gen.patterns(2, 0, 3000, 20, t, n4)
+    d1 = torch.empty(3000, dtype=torch.int32, device=cuda)
+    d2 = torch.empty_like(d1)
+    qr.qr_fm_count(fm, to_dev(pats, cuda), None, 20, d1, 3000)
+    qr.qr_fm_count(fm2, to_dev(pats, cuda), None, 20, d2, 3000)
+    torch.cuda.synchronize()
+    assert np.array_equal(to_host(d1), to_host(d2))
+    assert fm2.C == fm.C and fm2.spos == fm.spos
