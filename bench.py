@@ -338,6 +338,43 @@ def bench_approx(ctx, n, m_total, length, seed, steps, warmup):
             "pattern_len": length}
 
 
+def bench_variants(ctx, steps, warmup):
+    """The no-L1-array layouts (NEXT §8(f)4) on the configs[1] / configs[2] workloads."""
+    import gen
+    import paper_2602_04103_b200 as qr
+
+    torch = ctx.torch
+    res = {}
+    bits = torch.empty((N2 + 63) // 64, dtype=torch.uint64, device=ctx.dev)
+    gen.bits_dev(SEED[2], N2, 0.5, bits)
+    h = qr.qr_build(bits, N2, qr.QR_LAYOUT_BIRANK64X2, device=ctx.gpu)
+    del bits
+    q = torch.empty(M2, dtype=torch.uint64, device=ctx.dev)
+    gen.queries_dev(SEED[2], N2, M2, q, i0=ctx.rank * M2)
+    out = torch.empty_like(q)
+    ms = ctx.timed(lambda: qr.qr_rank(h, q, None, out, M2, ctx.stream), steps, warmup)
+    res["c2_birank64x2"] = {"ms": ms, "gq_s": ctx.world * M2 / ms / 1e6, "bytes": h.line_bytes,
+                            "overhead": h.line_bytes / (N2 / 8) - 1}
+    h.free()
+    text = torch.empty((N3 + 31) // 32, dtype=torch.uint64, device=ctx.dev)
+    gen.dna_dev(SEED[3], N3, 0, text)
+    h = qr.qr_build(text, N3, qr.QR_LAYOUT_QUADRANK64, device=ctx.gpu)
+    del text
+    c = torch.empty(M3, dtype=torch.uint8, device=ctx.dev)
+    gen.queries_dev(SEED[3], N3, M3, q, c, i0=ctx.rank * M3)
+    ms = ctx.timed(lambda: qr.qr_rank(h, q, c, out, M3, ctx.stream), steps, warmup)
+    del out
+    o4 = torch.empty((M3, 4), dtype=torch.uint64, device=ctx.dev)
+    ms4 = ctx.timed(lambda: qr.qr_rank_all4(h, q, o4, M3, ctx.stream), steps, warmup)
+    res["c3_quadrank64"] = {"rank": {"ms": ms, "gq_s": ctx.world * M3 / ms / 1e6},
+                            "rank_all4": {"ms": ms4, "gq_s": ctx.world * M3 / ms4 / 1e6},
+                            "bytes": h.line_bytes, "overhead": h.line_bytes / (N3 / 4) - 1}
+    h.free()
+    del q, c, o4
+    torch.cuda.empty_cache()
+    return res
+
+
 def bench_small(ctx, steps, warmup):
     import gen
     import paper_2602_04103_b200 as qr
@@ -441,6 +478,7 @@ def main():
         rows["c5_quadfm"] = bench_fm(ctx, N5, 1, M5, L5, SEED[5], K, W, rank_queries=10**9)
         rows["c5_reads_150bp_both_strands"] = bench_reads(ctx, N5, 10**7, 150, 55, K, W)
         rows["c4_quadfm_approx1"] = bench_approx(ctx, N4, 10**6, L4, SEED[4], K, W)
+        rows["layout_variants"] = bench_variants(ctx, K, W)
         rows["c1_small"] = bench_small(ctx, K, W)
     ms = c2["ms"]
     value = c2["gq_s"]

@@ -47,7 +47,18 @@ typedef int32_t qr_status;
 #define QR_ENOMEM    3  /* device or host allocation failed                                   */
 #define QR_ECUDA     4  /* a CUDA runtime call or kernel launch failed                        */
 
-typedef struct qr_index qr_index;   /* BiRank16 (sigma=2) or QuadRank16 (sigma=4) layout      */
+typedef struct qr_index qr_index;   /* a rank layout (QR_LAYOUT_*)                             */
+
+/* Rank layouts.  BIRANK16 / QUADRANK16 are the paper's headline structures (§3, §4); the two
+ * others are its no-L1-array variants (NEXT §8(f)4): BiRank64x2 (33.3%: each
+ * 32-B sector = u64 rank to the sector's middle + 192 data bits, so a query reads one sector
+ * and no superblock word) and QuadRank64 (100%: four u64 ranks to the middle
+ * of 128 characters in sector 0, the characters as two transposed negated plane pairs in
+ * sector 1).  All layouts answer every query identically. */
+#define QR_LAYOUT_BIRANK16    1
+#define QR_LAYOUT_BIRANK64X2  2
+#define QR_LAYOUT_QUADRANK16  3
+#define QR_LAYOUT_QUADRANK64  4
 typedef struct qr_fm qr_fm;         /* QuadFm: QuadRank over the BWT + C + spos + 8-mer table */
 
 /* ------------------------------------------------------------------ build */
@@ -64,6 +75,15 @@ qr_status qr_birank_build(const uint64_t* bits, uint64_t n, int device, void* st
  * low/high bit planes; superblocks of 256 lines with u32 s_{i,c} = floor(rank(i S4, c)/2^13),
  * b_{j,c} = rank(j B4 + 96, c) - 2^13 s_{j/256, c}.  text2b: ceil(n/32) words.  n < 2^45. */
 qr_status qr_quadrank_build(const uint64_t* text2b, uint64_t n, int device, void* stream, qr_index** out);
+
+/* Build any layout: text is bits (BIRANK*) or 2-bit DNA (QUADRANK*), host or device, with the
+ * conventions of qr_birank_build / qr_quadrank_build (which equal qr_build with layout
+ * BIRANK16 / QUADRANK16).  n < 2^43 (BIRANK16), < 2^45 (QUADRANK16), < 2^48 (the 64-bit
+ * variants).  QR_EINVAL for an unknown layout. */
+qr_status qr_build(const uint64_t* text, uint64_t n, int layout, int device, void* stream, qr_index** out);
+
+/* The layout of a handle (QR_LAYOUT_*). */
+qr_status qr_layout(const qr_index* h, int* layout);
 
 /* ------------------------------------------------------------------ queries */
 

@@ -20,6 +20,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "lib", "libqrank.so")
 
 QR_OK, QR_EINVAL, QR_ECAPACITY, QR_ENOMEM, QR_ECUDA = 0, 1, 2, 3, 4
+QR_LAYOUT_BIRANK16, QR_LAYOUT_BIRANK64X2, QR_LAYOUT_QUADRANK16, QR_LAYOUT_QUADRANK64 = 1, 2, 3, 4
 _STATUS = {1: "QR_EINVAL", 2: "QR_ECAPACITY", 3: "QR_ENOMEM", 4: "QR_ECUDA"}
 
 # every symbol include/qrank.h declares (tests check the .so exports all of them)
@@ -27,7 +28,7 @@ EXPORTS = (
     "qr_birank_build", "qr_quadrank_build", "qr_rank", "qr_rank_all4", "qr_fm_build", "qr_fm_count", "qr_fm_count_both", "qr_fm_count_approx",
     "qr_fm_count_work", "qr_gather_ceiling", "qr_info", "qr_export_layout", "qr_fm_info", "qr_fm_export_kmer",
     "qr_clone_to_device", "qr_fm_clone_to_device", "qr_sync", "qr_free", "qr_fm_free", "qr_last_error",
-    "qr_version", "qr_set_tuning",
+    "qr_version", "qr_set_tuning", "qr_build", "qr_layout",
 )
 
 
@@ -72,6 +73,8 @@ def lib():
             "qr_last_error": ([], C.c_char_p),
             "qr_version": ([], C.c_char_p),
             "qr_set_tuning": ([C.c_char_p, C.c_int64], I32),
+            "qr_build": ([V, U64, I32, I32, V, PP], I32),
+            "qr_layout": ([V, C.POINTER(C.c_int)], I32),
         }
         for name, (args, res) in sig.items():
             f = getattr(L, name)
@@ -123,6 +126,9 @@ class Index:
         n, sig, lb, sb = C.c_uint64(), C.c_int(), C.c_uint64(), C.c_uint64()
         _check(lib().qr_info(self.ptr, C.byref(n), C.byref(sig), C.byref(lb), C.byref(sb)), "qr_info")
         self.n, self.sigma, self.line_bytes, self.super_bytes = n.value, sig.value, lb.value, sb.value
+        lay = C.c_int()
+        _check(lib().qr_layout(self.ptr, C.byref(lay)), "qr_layout")
+        self.layout = lay.value
 
     def free(self):
         if self.owned and self.ptr:
@@ -164,6 +170,12 @@ class Fm:
 def qr_birank_build(bits, n: int, device: int = 0, stream=None) -> Index:
     out = C.c_void_p()
     _check(lib().qr_birank_build(_ptr(bits), n, device, _stream(stream), C.byref(out)), "qr_birank_build")
+    return Index(out.value)
+
+
+def qr_build(text, n: int, layout: int, device: int = 0, stream=None) -> Index:
+    out = C.c_void_p()
+    _check(lib().qr_build(_ptr(text), n, layout, device, _stream(stream), C.byref(out)), "qr_build")
     return Index(out.value)
 
 

@@ -70,32 +70,51 @@ int sm_count(int device) {
   return cache[device];
 }
 
-qr_status alloc_index(int sigma, uint64_t n, int device, qr_index** out) {
+qr_status alloc_index(int sigma, uint64_t n, int device, qr_index** out, int layout) {
   qr_index* h = new (std::nothrow) qr_index();
   if (!h) return fail(QR_ENOMEM, "host allocation");
+  if (!layout) layout = sigma == 2 ? QR_LAYOUT_BIRANK16 : QR_LAYOUT_QUADRANK16;
   h->sigma = sigma;
+  h->layout = layout;
   h->device = device;
   h->n = n;
-  const uint64_t B = sigma == 2 ? BI_B : QD_B;
-  const uint32_t sb = sigma == 2 ? BI_SB_LOG : QD_SB_LOG;
+  uint64_t B = 0;
+  uint32_t sb = 0;
+  switch (layout) {
+    case QR_LAYOUT_BIRANK16: B = BI_B; sb = BI_SB_LOG; break;
+    case QR_LAYOUT_QUADRANK16: B = QD_B; sb = QD_SB_LOG; break;
+    case QR_LAYOUT_BIRANK64X2: B = 384; break;      // 2 x 192 data bits per line
+    default: B = 128; break;                        // QuadRank64: 128 chars per line
+  }
   h->n_lines = n / B + 1;                               // reading R4: q = n stays in range
-  h->n_super = ((h->n_lines - 1) >> sb) + 1;
+  h->n_super = sb ? ((h->n_lines - 1) >> sb) + 1 : 0;   // the 64-bit variants have no L1 array
   h->sm_count = sm_count(device);
   cudaError_t e;
   if ((e = cudaMalloc((void**)&h->lines, h->n_lines * 64))) { delete h; return cuda_fail(e, "alloc lines"); }
-  const uint64_t sbytes = h->n_super * (sigma == 2 ? 4 : 16);
-  if ((e = cudaMalloc((void**)&h->super, sbytes))) { cudaFree(h->lines); delete h; return cuda_fail(e, "alloc super"); }
+  const uint64_t sbytes = super_bytes_of(h);
+  if (sbytes && (e = cudaMalloc((void**)&h->super, sbytes))) {
+    cudaFree(h->lines); delete h; return cuda_fail(e, "alloc super");
+  }
   *out = h;
   return QR_OK;
 }
 
+uint64_t super_bytes_of(const qr_index* h) { return h->n_super * (h->sigma == 2 ? 4 : 16); }
+
 qr_status fm_build_device(const uint64_t* d_text, uint64_t n, const uint32_t* d_sa_given, int device, cudaStream_t st,
                           qr_fm** out);
+__global__ void k_mask_tail_bits(uint64_t* words, uint64_t n);
+__global__ void k_mask_tail_chars(uint64_t* words, uint64_t n);
 cudaError_t launch_bi_gather(const qr_index* h, const uint64_t* q, uint64_t* out, uint64_t m, int mode, cudaStream_t st);
 cudaError_t launch_qd_gather(const qr_index* h, const uint64_t* q, uint64_t* out, uint64_t m, int mode, cudaStream_t st);
 
 cudaError_t launch_gather(const qr_index* h, const uint64_t* q, uint64_t* out, uint64_t m, int mode, cudaStream_t st) {
+  if (h->layout == QR_LAYOUT_BIRANK64X2 || h->layout == QR_LAYOUT_QUADRANK64)
+    return launch_variant(h, q, nullptr, out, m, 2, st);   // the variants' loads (modes coincide)
   return h->sigma == 2 ? launch_bi_gather(h, q, out, m, mode, st) : launch_qd_gather(h, q, out, m, mode, st);
+}
+static bool is_variant(const qr_index* h) {
+  return h->layout == QR_LAYOUT_BIRANK64X2 || h->layout == QR_LAYOUT_QUADRANK64;
 }
 
 // RAII device guard
@@ -317,6 +336,41 @@ QR_EXPORT qr_status qr_quadrank_build(const uint64_t* text2b, uint64_t n, int de
   return s;
 }
 
+QR_EXPORT qr_status qr_build(const uint64_t* text, uint64_t n, int layout, int device, void* stream, qr_index** out) {
+  if (layout == QR_LAYOUT_BIRANK16) return qr_birank_build(text, n, device, stream, out);
+  if (layout == QR_LAYOUT_QUADRANK16) return qr_quadrank_build(text, n, device, stream, out);
+  if (layout != QR_LAYOUT_BIRANK64X2 && layout != QR_LAYOUT_QUADRANK64) return fail(QR_EINVAL, "qr_build: bad layout %d", layout);
+  if (!out || (!text && n)) return fail(QR_EINVAL, "qr_build: null pointer");
+  *out = nullptr;
+  if (n >= (1ull << 48)) return fail(QR_ECAPACITY, "qr_build: n >= 2^48");
+  DeviceGuard dg(device);
+  if (!dg.ok) return fail(QR_EINVAL, "qr_build: bad device %d", device);
+  cudaStream_t st = (cudaStream_t)stream;
+  const bool bits = layout == QR_LAYOUT_BIRANK64X2;
+  const uint64_t L = bits ? n / 384 + 1 : n / 128 + 1;
+  const uint64_t words = bits ? (n + 63) >> 6 : (n + 31) >> 5;
+  uint64_t padded = bits ? 6 * L : 4 * L;
+  if (padded < words) padded = words;
+  uint64_t* d = nullptr;
+  qr_status s = stage_input(text, words, padded, st, &d);
+  if (s != QR_OK) return s;
+  if (bits) k_mask_tail_bits<<<1, 1, 0, st>>>(d, n);
+  else      k_mask_tail_chars<<<1, 1, 0, st>>>(d, n);
+  s = bits ? birank64x2_build_device(d, n, device, st, out) : quadrank64_build_device(d, n, device, st, out);
+  cudaFreeAsync(d, st);
+  if (s == QR_OK) {
+    cudaError_t e = cudaStreamSynchronize(st);
+    if (e) { qr_free(*out); *out = nullptr; return cuda_fail(e, "qr_build"); }
+  }
+  return s;
+}
+
+QR_EXPORT qr_status qr_layout(const qr_index* h, int* layout) {
+  if (!h || !layout) return fail(QR_EINVAL, "qr_layout: null pointer");
+  *layout = h->layout;
+  return QR_OK;
+}
+
 QR_EXPORT qr_status qr_rank(const qr_index* h, const uint64_t* q, const uint8_t* c, uint64_t* out, uint64_t m,
                             void* stream) {
   if (!h) return fail(QR_EINVAL, "qr_rank: null handle");
@@ -326,6 +380,7 @@ QR_EXPORT qr_status qr_rank(const qr_index* h, const uint64_t* q, const uint8_t*
   DeviceGuard dg(h->device);
   cudaStream_t st = (cudaStream_t)stream;
   auto launch = [&](const uint64_t* dq, const uint8_t* dc, uint64_t* dout, uint64_t cnt, cudaStream_t s) -> cudaError_t {
+    if (is_variant(h)) return launch_variant(h, dq, dc, dout, cnt, 0, s);
     return h->sigma == 2 ? launch_birank_rank(h, dq, dc, dout, cnt, s) : launch_quadrank_rank(h, dq, dc, dout, cnt, s);
   };
   int sp = classify({q, c, out}, h->device);
@@ -351,13 +406,16 @@ QR_EXPORT qr_status qr_rank_all4(const qr_index* h, const uint64_t* q, uint64_t*
   cudaStream_t st = (cudaStream_t)stream;
   int sp = classify({q, out4}, h->device);
   if (sp < 0) return fail(QR_EINVAL, "qr_rank_all4: q and out4 must both be device (device %d) or both host", h->device);
+  auto launch4 = [&](const uint64_t* dq, uint64_t* d4, uint64_t cnt, cudaStream_t s) -> cudaError_t {
+    return is_variant(h) ? launch_variant(h, dq, nullptr, d4, cnt, 1, s) : launch_quadrank_all4(h, dq, d4, cnt, s);
+  };
   if (sp == 1) {
-    cudaError_t e = launch_quadrank_all4(h, q, out4, m, st);
+    cudaError_t e = launch4(q, out4, m, st);
     return e ? cuda_fail(e, "qr_rank_all4 launch") : QR_OK;
   }
   std::vector<StageArray> arr = {{q, nullptr, 8}, {nullptr, out4, 32}};
   return run_staged(h->device, st, m, arr, [&](const std::vector<void*>& d, uint64_t cnt, cudaStream_t s) -> qr_status {
-    cudaError_t e = launch_quadrank_all4(h, (const uint64_t*)d[0], (uint64_t*)d[1], cnt, s);
+    cudaError_t e = launch4((const uint64_t*)d[0], (uint64_t*)d[1], cnt, s);
     return e ? cuda_fail(e, "qr_rank_all4 launch") : QR_OK;
   });
 }
@@ -475,7 +533,7 @@ QR_EXPORT qr_status qr_info(const qr_index* h, uint64_t* n, int* sigma, uint64_t
   if (n) *n = h->n;
   if (sigma) *sigma = h->sigma;
   if (line_bytes) *line_bytes = h->n_lines * 64;
-  if (super_bytes) *super_bytes = h->n_super * (h->sigma == 2 ? 4 : 16);
+  if (super_bytes) *super_bytes = super_bytes_of(h);
   return QR_OK;
 }
 
@@ -485,8 +543,8 @@ QR_EXPORT qr_status qr_export_layout(const qr_index* h, void* host_lines, void* 
   cudaError_t e;
   if (host_lines && (e = cudaMemcpy(host_lines, h->lines, h->n_lines * 64, cudaMemcpyDeviceToHost)))
     return cuda_fail(e, "qr_export_layout lines");
-  if (host_super &&
-      (e = cudaMemcpy(host_super, h->super, h->n_super * (h->sigma == 2 ? 4 : 16), cudaMemcpyDeviceToHost)))
+  if (host_super && super_bytes_of(h) &&
+      (e = cudaMemcpy(host_super, h->super, super_bytes_of(h), cudaMemcpyDeviceToHost)))
     return cuda_fail(e, "qr_export_layout super");
   return QR_OK;
 }
@@ -513,14 +571,14 @@ QR_EXPORT qr_status qr_clone_to_device(const qr_index* h, int device, void* stre
   DeviceGuard dg(device);
   if (!dg.ok) return fail(QR_EINVAL, "qr_clone_to_device: bad device %d", device);
   qr_index* c = nullptr;
-  qr_status s = alloc_index(h->sigma, h->n, device, &c);
+  qr_status s = alloc_index(h->sigma, h->n, device, &c, h->layout);
   if (s != QR_OK) return s;
   cudaStream_t st = (cudaStream_t)stream;
   int can = 0;
   if (device != h->device) cudaDeviceCanAccessPeer(&can, device, h->device);
   if (can) cudaDeviceEnablePeerAccess(h->device, 0), cudaGetLastError();
   cudaError_t e = cudaMemcpyPeerAsync(c->lines, device, h->lines, h->device, h->n_lines * 64, st);
-  if (!e) e = cudaMemcpyPeerAsync(c->super, device, h->super, h->device, h->n_super * (h->sigma == 2 ? 4 : 16), st);
+  if (!e && super_bytes_of(h)) e = cudaMemcpyPeerAsync(c->super, device, h->super, h->device, super_bytes_of(h), st);
   if (!e) e = cudaStreamSynchronize(st);
   if (e) { qr_free(c); return cuda_fail(e, "qr_clone_to_device"); }
   *out = c;

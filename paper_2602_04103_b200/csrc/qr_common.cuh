@@ -29,6 +29,7 @@ constexpr int NUM_SMS_B200 = 148;
 // Handle layouts (opaque to callers).
 struct qr_index {
   int sigma;            // 2 or 4
+  int layout;           // QR_LAYOUT_* (include/qrank.h)
   int device;
   uint64_t n;           // text length (bits or symbols)
   uint64_t n_lines;     // floor(n/B)+1
@@ -61,7 +62,12 @@ int sm_count(int device);
 
 // internal builders used by fm.cu
 qr_status quadrank_build_device(const uint64_t* d_text2b, uint64_t n, int device, cudaStream_t st, qr_index** out);
-qr_status alloc_index(int sigma, uint64_t n, int device, qr_index** out);
+qr_status alloc_index(int sigma, uint64_t n, int device, qr_index** out, int layout = 0);
+uint64_t super_bytes_of(const qr_index* h);
+qr_status birank64x2_build_device(const uint64_t* d_bits, uint64_t n, int device, cudaStream_t st, qr_index** out);
+qr_status quadrank64_build_device(const uint64_t* d_text, uint64_t n, int device, cudaStream_t st, qr_index** out);
+cudaError_t launch_variant(const qr_index* h, const uint64_t* q, const uint8_t* c, uint64_t* out, uint64_t m, int what,
+                           cudaStream_t st);
 
 // kernel launchers (device pointers; validated by api.cu)
 cudaError_t launch_birank_rank(const qr_index* h, const uint64_t* q, const uint8_t* c, uint64_t* out, uint64_t m,

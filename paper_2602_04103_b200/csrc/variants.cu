@@ -1,0 +1,323 @@
+// variants.cu — the paper's no-L1-array layout variants on sm_100a (NEXT §8(f)4).
+//
+// On B200 a random query costs L2 requests, not bytes: BiRank16/QuadRank16
+// need a second request per query for the L2-resident superblock word.  The paper's larger
+// variants that "completely remove the L1 level" trade space for exactly that request:
+//
+// BiRank64x2 (33.3%): every 32-B sector is self-contained —
+//   sector h of line j = [u64 v_{j,h} | 192 data bits],  v_{j,h} = rank(384 j + 192 h + 96),
+//   i.e. two 64-bit values "to 1/4th and 3/4th" of the 384-bit block (the x2 family anchors,
+//   PAPER.md:484-492).  Line j's data bits are text words [6j, 6j+6) (384 = 6 * 64).  A query
+//   reads ONE 32-B sector: one L2 request, no superblock word, popcount over <= 96 bits.
+//
+// QuadRank64 (100%, "stores 4 64-bit values, as does BWA-MEM, removing the
+//   L1 array ... each half is now only 64 of them"): sector 0 = v_{j,c} = rank(128 j + 64, c)
+//   for c = A, C, G, T; sector 1 = 128 chars as two transposed negated plane pairs (word 4+2t =
+//   NOT low bits, 5+2t = NOT high bits of chars 64t..64t+63).  Line j's chars are text words
+//   [4j, 4j+4).  A query needs both sectors: the lane pair loads them in one instruction (one
+//   L2 request), no superblock word.
+#include <cub/device/device_scan.cuh>
+
+#include "qr_common.cuh"
+
+namespace qr {
+
+extern int g_rank_k;
+extern int g_rank_blocks_per_sm;
+
+__device__ __forceinline__ uint64_t even_bits64(uint64_t x) {
+  x &= 0x5555555555555555ull;
+  x = (x | (x >> 1)) & 0x3333333333333333ull;
+  x = (x | (x >> 2)) & 0x0F0F0F0F0F0F0F0Full;
+  x = (x | (x >> 4)) & 0x00FF00FF00FF00FFull;
+  x = (x | (x >> 8)) & 0x0000FFFF0000FFFFull;
+  x = (x | (x >> 16)) & 0x00000000FFFFFFFFull;
+  return x;
+}
+
+// ------------------------------------------------------------------ BiRank64x2 build
+
+// per sector: total and count of its first 96 data bits
+__global__ void k_b64_count(const uint64_t* __restrict__ t, uint64_t L, uint64_t* __restrict__ tot,
+                            uint32_t* __restrict__ half) {
+  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < L; j += (uint64_t)gridDim.x * blockDim.x) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const uint64_t* w = t + 6 * j + 3 * h;
+      const uint32_t a = __popcll(w[0]), b = __popcll(w[1] & 0xffffffffull);
+      half[2 * j + h] = a + b;
+      tot[2 * j + h] = a + __popcll(w[1]) + __popcll(w[2]);
+    }
+  }
+}
+
+__global__ void k_b64_write(const uint64_t* __restrict__ t, uint64_t L, const uint64_t* __restrict__ R,
+                            const uint32_t* __restrict__ half, uint4* __restrict__ lines) {
+  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < L; j += (uint64_t)gridDim.x * blockDim.x) {
+    ulonglong2* dst = reinterpret_cast<ulonglong2*>(lines + 4 * j);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const uint64_t* w = t + 6 * j + 3 * h;
+      const uint64_t v = R[2 * j + h] + half[2 * j + h];      // rank(384 j + 192 h + 96)
+      dst[2 * h] = make_ulonglong2(v, w[0]);
+      dst[2 * h + 1] = make_ulonglong2(w[1], w[2]);
+    }
+  }
+}
+
+qr_status birank64x2_build_device(const uint64_t* d_bits, uint64_t n, int device, cudaStream_t st, qr_index** out) {
+  qr_index* h = nullptr;
+  qr_status rs = alloc_index(2, n, device, &h, QR_LAYOUT_BIRANK64X2);
+  if (rs != QR_OK) return rs;
+  const uint64_t L = h->n_lines;
+  uint64_t *tot = nullptr, *R = nullptr;
+  uint32_t* half = nullptr;
+  void* tmp = nullptr;
+  size_t tb = 0;
+  cudaError_t e;
+  auto bail = [&](cudaError_t err, const char* what) {
+    cudaFreeAsync(tot, st); cudaFreeAsync(R, st); cudaFreeAsync(half, st); cudaFreeAsync(tmp, st);
+    qr_free(h);
+    return cuda_fail(err, what);
+  };
+  if ((e = cudaMallocAsync((void**)&tot, 2 * L * 8, st))) return bail(e, "alloc tot");
+  if ((e = cudaMallocAsync((void**)&R, 2 * L * 8, st))) return bail(e, "alloc R");
+  if ((e = cudaMallocAsync((void**)&half, 2 * L * 4, st))) return bail(e, "alloc half");
+  const unsigned g = grid_stride_blocks(L, 256, h->sm_count, 16);
+  k_b64_count<<<g, 256, 0, st>>>(d_bits, L, tot, half);
+  if ((e = cub::DeviceScan::ExclusiveSum(nullptr, tb, tot, R, (int64_t)(2 * L), st))) return bail(e, "scan size");
+  if ((e = cudaMallocAsync(&tmp, tb, st))) return bail(e, "alloc scan tmp");
+  if ((e = cub::DeviceScan::ExclusiveSum(tmp, tb, tot, R, (int64_t)(2 * L), st))) return bail(e, "scan");
+  k_b64_write<<<g, 256, 0, st>>>(d_bits, L, R, half, h->lines);
+  if ((e = cudaGetLastError())) return bail(e, "k_b64_write");
+  cudaFreeAsync(tot, st); cudaFreeAsync(R, st); cudaFreeAsync(half, st); cudaFreeAsync(tmp, st);
+  *out = h;
+  return QR_OK;
+}
+
+// ------------------------------------------------------------------ QuadRank64 build
+
+__global__ void k_q64_count(const uint64_t* __restrict__ t, uint64_t L, uint64_t* __restrict__ tot,
+                            uint32_t* __restrict__ c64) {
+  const uint64_t M = 0x5555555555555555ull;
+  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < L; j += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t a[4] = {0, 0, 0, 0};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if (k == 2) c64[j] = a[0] | (a[1] << 8) | (a[2] << 16) | (a[3] << 24);   // chars [0,64)
+      const uint64_t w = t[4 * j + k];
+      const uint64_t lo = w & M, hi = (w >> 1) & M;
+      const uint32_t c3 = __popcll(lo & hi), l1 = __popcll(lo), h1 = __popcll(hi);
+      a[3] += c3; a[1] += l1 - c3; a[2] += h1 - c3; a[0] += 32 - l1 - h1 + c3;
+    }
+#pragma unroll
+    for (int c = 0; c < 4; ++c) tot[(uint64_t)c * L + j] = a[c];
+  }
+}
+
+__global__ void k_q64_write(const uint64_t* __restrict__ t, uint64_t L, const uint64_t* __restrict__ R,
+                            const uint32_t* __restrict__ c64, uint4* __restrict__ lines) {
+  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < L; j += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t cp = c64[j];
+    uint64_t v[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) v[c] = R[(uint64_t)c * L + j] + ((cp >> (8 * c)) & 0xffu);   // rank(128j+64, c)
+    const uint64_t* w = t + 4 * j;
+    const uint64_t l0 = even_bits64(w[0]) | (even_bits64(w[1]) << 32), h0 = even_bits64(w[0] >> 1) | (even_bits64(w[1] >> 1) << 32);
+    const uint64_t l1 = even_bits64(w[2]) | (even_bits64(w[3]) << 32), h1 = even_bits64(w[2] >> 1) | (even_bits64(w[3] >> 1) << 32);
+    ulonglong2* dst = reinterpret_cast<ulonglong2*>(lines + 4 * j);
+    dst[0] = make_ulonglong2(v[0], v[1]);
+    dst[1] = make_ulonglong2(v[2], v[3]);
+    dst[2] = make_ulonglong2(~l0, ~h0);
+    dst[3] = make_ulonglong2(~l1, ~h1);
+  }
+}
+
+qr_status quadrank64_build_device(const uint64_t* d_text, uint64_t n, int device, cudaStream_t st, qr_index** out) {
+  qr_index* h = nullptr;
+  qr_status rs = alloc_index(4, n, device, &h, QR_LAYOUT_QUADRANK64);
+  if (rs != QR_OK) return rs;
+  const uint64_t L = h->n_lines;
+  uint64_t *tot = nullptr, *R = nullptr;
+  uint32_t* c64 = nullptr;
+  void* tmp = nullptr;
+  size_t tb = 0;
+  cudaError_t e;
+  auto bail = [&](cudaError_t err, const char* what) {
+    cudaFreeAsync(tot, st); cudaFreeAsync(R, st); cudaFreeAsync(c64, st); cudaFreeAsync(tmp, st);
+    qr_free(h);
+    return cuda_fail(err, what);
+  };
+  if ((e = cudaMallocAsync((void**)&tot, 4 * L * 8, st))) return bail(e, "alloc tot");
+  if ((e = cudaMallocAsync((void**)&R, 4 * L * 8, st))) return bail(e, "alloc R");
+  if ((e = cudaMallocAsync((void**)&c64, L * 4, st))) return bail(e, "alloc c64");
+  const unsigned g = grid_stride_blocks(L, 256, h->sm_count, 16);
+  k_q64_count<<<g, 256, 0, st>>>(d_text, L, tot, c64);
+  if ((e = cub::DeviceScan::ExclusiveSum(nullptr, tb, tot, R, (int64_t)L, st))) return bail(e, "scan size");
+  if ((e = cudaMallocAsync(&tmp, tb, st))) return bail(e, "alloc scan tmp");
+  for (int c = 0; c < 4; ++c)
+    if ((e = cub::DeviceScan::ExclusiveSum(tmp, tb, tot + (uint64_t)c * L, R + (uint64_t)c * L, (int64_t)L, st)))
+      return bail(e, "scan");
+  k_q64_write<<<g, 256, 0, st>>>(d_text, L, R, c64, h->lines);
+  if ((e = cudaGetLastError())) return bail(e, "k_q64_write");
+  cudaFreeAsync(tot, st); cudaFreeAsync(R, st); cudaFreeAsync(c64, st); cudaFreeAsync(tmp, st);
+  *out = h;
+  return QR_OK;
+}
+
+// ------------------------------------------------------------------ queries
+
+template <int K>
+__device__ __forceinline__ void v_load_q(const uint64_t* __restrict__ q, const uint8_t* __restrict__ cs, uint64_t i0,
+                                         uint64_t stride, uint64_t m, uint64_t (&qn)[K], uint32_t (&cn)[K]) {
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    const uint64_t idx = i0 + (uint64_t)k * stride;
+    qn[k] = idx < m ? ld_stream_u64(q + idx) : 0;
+    if (cs) cn[k] = idx < m ? ld_stream_u8(cs + idx) & 3u : 0u;
+  }
+}
+
+// BiRank64x2: one lane per query, one 32-B sector.  Count over the sector's 192 data bits
+// (3 words) of [x, 96) or [96, x): mask = prefix(x) XOR prefix(96), the symmetric difference.
+template <int K, int MODE>   // MODE 0: rank; 1: gather ceiling (same load, no popcount)
+__global__ void __launch_bounds__(256) k_b64_rank(const uint4* __restrict__ lines, const uint64_t* __restrict__ q,
+                                                  const uint8_t* __restrict__ cs, uint64_t* __restrict__ out,
+                                                  uint64_t m, uint64_t last_line) {
+  const uint64_t nthr = (uint64_t)gridDim.x * blockDim.x;
+  uint64_t i0 = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  uint64_t qn[K];
+  uint32_t cn[K];
+  v_load_q<K>(q, cs, i0, nthr, m, qn, cn);
+  for (; i0 < m; i0 += nthr * K) {
+    uint64_t qq[K], w[K][4];
+    uint32_t xx[K], cc[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      qq[k] = qn[k];
+      cc[k] = cn[k];
+      uint64_t j = qq[k] < (1ull << 39) ? (uint64_t)((uint32_t)(qq[k] >> 7) / 3u) : qq[k] / 384;   // floor(q/384)
+      j = j > last_line ? last_line : j;
+      uint64_t r = qq[k] - j * 384;
+      r = r > 383 ? 383 : r;
+      const uint32_t h = r >= 192 ? 1u : 0u;
+      xx[k] = (uint32_t)r - 192u * h;
+      ld_sector_na(lines + 4 * j + 2 * h, w[k][0], w[k][1], w[k][2], w[k][3]);
+    }
+    v_load_q<K>(q, cs, i0 + nthr * K, nthr, m, qn, cn);
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const uint64_t idx = i0 + (uint64_t)k * nthr;
+      uint64_t r;
+      if (MODE == 1) {
+        r = w[k][0] ^ w[k][1] ^ w[k][2] ^ w[k][3];
+      } else {
+        const int x = (int)xx[k];
+        uint32_t cnt = __popcll(w[k][1] & (prefix_mask(x, 0) ^ ~0ull)) +
+                       __popcll(w[k][2] & (prefix_mask(x, 1) ^ 0xffffffffull)) +
+                       __popcll(w[k][3] & prefix_mask(x, 2));
+        r = x >= 96 ? w[k][0] + cnt : w[k][0] - cnt;
+        if (cs && cc[k] == 0) r = qq[k] - r;                   // sigma = 2 with c = 0
+      }
+      if (idx < m) st_stream_u64(out + idx, r);
+    }
+  }
+}
+
+// QuadRank64: lane pairs (lane 0: sector 0 with the four counts, lane 1: sector 1 with the
+// 128 chars) -> one request per query.  ALL4 = 1 returns the four ranks.
+template <int K, int MODE>   // MODE 0: rank(q,c); 1: rank_4(q); 2: gather ceiling
+__global__ void __launch_bounds__(256) k_q64_rank(const uint4* __restrict__ lines, const uint64_t* __restrict__ q,
+                                                  const uint8_t* __restrict__ cs, uint64_t* __restrict__ out,
+                                                  uint64_t m, uint64_t last_line) {
+  const uint64_t npair = ((uint64_t)gridDim.x * blockDim.x) >> 1;
+  const uint32_t half = threadIdx.x & 1u;
+  const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  uint64_t i0 = tid >> 1;
+  uint64_t iw = (tid & ~31ull) >> 1;
+  uint64_t qn[K];
+  uint32_t cn[K];
+  v_load_q<K>(q, MODE == 0 ? cs : nullptr, i0, npair, m, qn, cn);
+  for (; iw < m; iw += npair * K, i0 += npair * K) {
+    uint64_t qq[K], w[K][4];
+    uint32_t cc[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      qq[k] = qn[k];
+      cc[k] = MODE == 0 ? cn[k] : 0u;
+      uint64_t j = qq[k] >> 7;
+      j = j > last_line ? last_line : j;
+      ld_sector_na(lines + 4 * j + 2 * half, w[k][0], w[k][1], w[k][2], w[k][3]);
+      if (j << 7 != (qq[k] & ~127ull)) qq[k] = (j << 7) | 127;   // q > n: clamp inside the last line
+    }
+    v_load_q<K>(q, MODE == 0 ? cs : nullptr, i0 + npair * K, npair, m, qn, cn);
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const uint64_t idx = i0 + (uint64_t)k * npair;
+      const uint32_t x = (uint32_t)(qq[k] & 127u);
+      const bool right = x >= 64;
+      const int y = (int)(x & 63u);
+      const uint64_t msk = prefix_mask(y, 0) ^ (right ? 0ull : ~0ull);     // [y,64) of pair 0 or [0,y) of pair 1
+      const uint64_t wl = right ? w[k][2] : w[k][0], wh = right ? w[k][3] : w[k][1];   // lane 1's plane pair
+      if (MODE == 2) {
+        uint64_t v = w[k][0] ^ w[k][1] ^ w[k][2] ^ w[k][3];
+        v ^= __shfl_xor_sync(0xffffffffu, v, 1);
+        if (half == 0 && idx < m) st_stream_u64(out + idx, v);
+      } else if (MODE == 0) {
+        const uint32_t c = cc[k];
+        const uint64_t cl = 0ull - (uint64_t)(c & 1u), ch = 0ull - (uint64_t)(c >> 1);
+        const uint32_t cnt = __popcll((wl ^ cl) & (wh ^ ch) & msk);
+        const uint64_t vc = (c & 2u) ? ((c & 1u) ? w[k][3] : w[k][2]) : ((c & 1u) ? w[k][1] : w[k][0]);
+        uint64_t v = half ? (right ? (uint64_t)cnt : 0ull - (uint64_t)cnt) : vc;
+        v += __shfl_xor_sync(0xffffffffu, v, 1);
+        if (half == 0 && idx < m) st_stream_u64(out + idx, v);
+      } else {
+        const uint64_t l = ~wl & msk, hh = ~wh & msk;
+        const uint32_t nl = __popcll(l), nh = __popcll(hh), nt = __popcll(l & hh);
+        const uint32_t len = right ? (uint32_t)y : 64u - (uint32_t)y;
+        const uint32_t packed = (len - nl - nh + nt) | ((nl - nt) << 8) | ((nh - nt) << 16) | (nt << 24);
+        const uint32_t other = __shfl_xor_sync(0xffffffffu, packed, 1);
+        if (half == 0 && idx < m) {
+          uint64_t r[4];
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            const uint32_t cn4 = (other >> (8 * c)) & 0xffu;
+            r[c] = right ? w[k][c] + cn4 : w[k][c] - cn4;
+          }
+          st_stream_v4u64(out + 4 * idx, r[0], r[1], r[2], r[3]);
+        }
+      }
+    }
+  }
+}
+
+template <int K>
+static cudaError_t v_launch(const qr_index* h, const uint64_t* q, const uint8_t* c, uint64_t* out, uint64_t m,
+                            int what, cudaStream_t st) {
+  const uint64_t last = h->n_lines - 1;
+  if (h->layout == QR_LAYOUT_BIRANK64X2) {
+    unsigned g = grid_stride_blocks((m + K - 1) / K, 256, h->sm_count, g_rank_blocks_per_sm);
+    if (what == 2) k_b64_rank<K, 1><<<g, 256, 0, st>>>(h->lines, q, nullptr, out, m, last);
+    else           k_b64_rank<K, 0><<<g, 256, 0, st>>>(h->lines, q, c, out, m, last);
+  } else {
+    unsigned g = grid_stride_blocks((2 * m + K - 1) / K, 256, h->sm_count, g_rank_blocks_per_sm);
+    if (what == 0)      k_q64_rank<K, 0><<<g, 256, 0, st>>>(h->lines, q, c, out, m, last);
+    else if (what == 1) k_q64_rank<K, 1><<<g, 256, 0, st>>>(h->lines, q, nullptr, out, m, last);
+    else                k_q64_rank<K, 2><<<g, 256, 0, st>>>(h->lines, q, nullptr, out, m, last);
+  }
+  return cudaGetLastError();
+}
+
+// what: 0 = rank, 1 = rank_4 (QuadRank64), 2 = gather ceiling
+cudaError_t launch_variant(const qr_index* h, const uint64_t* q, const uint8_t* c, uint64_t* out, uint64_t m, int what,
+                           cudaStream_t st) {
+  if (m == 0) return cudaSuccess;
+  switch (g_rank_k) {
+    case 1: return v_launch<1>(h, q, c, out, m, what, st);
+    case 4: return v_launch<4>(h, q, c, out, m, what, st);
+    case 8: return v_launch<8>(h, q, c, out, m, what, st);
+    default: return v_launch<2>(h, q, c, out, m, what, st);
+  }
+}
+
+}  // namespace qr

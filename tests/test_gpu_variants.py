@@ -1,0 +1,103 @@
+"""GPU parity of the no-L1-array layout variants (NEXT §8(f)4): BiRank64x2 and
+QuadRank64 against the same oracle, bit-exact, incl. the sector / line
+boundaries (192, 384 bits; 64, 128 chars), ragged tails and the host-pointer path."""
+import numpy as np
+import pytest
+
+import gen
+import oracle
+import paper_2602_04103_b200 as qr
+from _util import boundary_queries, to_dev, to_host
+
+pytestmark = pytest.mark.gpu
+
+B64_SIZES = [0, 1, 95, 96, 97, 191, 192, 193, 383, 384, 385, 5000, 3 * 384 * 1000 + 77, (1 << 22) + 3]
+Q64_SIZES = [0, 1, 63, 64, 65, 127, 128, 129, 3000, 128 * 5000 + 31, (1 << 21) + 5]
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+@pytest.mark.parametrize("n", B64_SIZES)
+@pytest.mark.parametrize("p", [0.5, 1.0])
+def test_birank64x2_parity(cuda, n, p):
+    torch = _torch()
+    w = gen.bits(3000 + n, n, p)
+    h = qr.qr_build(w, n, qr.QR_LAYOUT_BIRANK64X2)
+    assert h.layout == qr.QR_LAYOUT_BIRANK64X2 and h.super_bytes == 0
+    assert h.line_bytes == 64 * (n // 384 + 1)
+    ora = oracle.BitsOracle(w, n)
+    q = np.arange(n + 1, dtype=np.uint64) if n <= 100000 else \
+        np.concatenate([gen.queries(1, n, 200000), boundary_queries(n, 192, 384, 96)])
+    dq = to_dev(q, cuda)
+    out = torch.empty_like(dq)
+    qr.qr_rank(h, dq, None, out)
+    c = (gen.queries(2, 1, q.size, with_c=True)[1] & 1).astype(np.uint8)
+    out2 = torch.empty_like(dq)
+    qr.qr_rank(h, dq, to_dev(c, cuda), out2)
+    torch.cuda.synchronize()
+    assert np.array_equal(to_host(out), ora.rank(q))
+    assert np.array_equal(to_host(out2), ora.rank(q, c))
+
+
+@pytest.mark.parametrize("n", Q64_SIZES)
+def test_quadrank64_parity(cuda, n):
+    torch = _torch()
+    w = gen.dna(4000 + n, n)
+    h = qr.qr_build(w, n, qr.QR_LAYOUT_QUADRANK64)
+    assert h.layout == qr.QR_LAYOUT_QUADRANK64 and h.super_bytes == 0
+    ora = oracle.DnaOracle(w, n)
+    if n <= 40000:
+        q = np.repeat(np.arange(n + 1, dtype=np.uint64), 4)
+        c = np.tile(np.arange(4, dtype=np.uint8), n + 1)
+    else:
+        q, c = gen.queries(5, n, 200000, with_c=True)
+        q = np.concatenate([q, boundary_queries(n, 64, 128, 0)])
+        c = np.concatenate([c, (np.arange(q.size - c.size) % 4).astype(np.uint8)])
+    dq = to_dev(q, cuda)
+    out = torch.empty_like(dq)
+    qr.qr_rank(h, dq, to_dev(c, cuda), out)
+    qu = np.unique(q)
+    o4 = torch.empty((qu.size, 4), dtype=torch.uint64, device=cuda)
+    qr.qr_rank_all4(h, to_dev(qu, cuda), o4)
+    torch.cuda.synchronize()
+    assert np.array_equal(to_host(out), ora.rank(q, c))
+    assert np.array_equal(to_host(o4), ora.rank_all4(qu))
+
+
+@pytest.mark.parametrize("k", [1, 2, 4, 8])
+def test_variants_tuning_and_host_path(cuda, k):
+    torch = _torch()
+    n = 777777
+    wb, wd = gen.bits(8, n), gen.dna(9, n)
+    hb = qr.qr_build(to_dev(wb, cuda), n, qr.QR_LAYOUT_BIRANK64X2)
+    hq = qr.qr_build(to_dev(wd, cuda), n, qr.QR_LAYOUT_QUADRANK64)
+    q, c = gen.queries(10, n, 123457, with_c=True)
+    qr.qr_set_tuning("rank_k", k)
+    try:
+        ob, oq = np.zeros(q.size, np.uint64), np.zeros(q.size, np.uint64)
+        o4 = np.zeros((q.size, 4), np.uint64)
+        qr.qr_rank(hb, q, None, ob)
+        qr.qr_rank(hq, q, c, oq)
+        qr.qr_rank_all4(hq, q, o4)
+        qr.qr_sync()
+        big = to_dev(np.array([n + 1, 5 * n, 1 << 40], np.uint64), cuda)      # q > n: memory-safe
+        qr.qr_rank(hb, big, None, torch.empty_like(big))
+        qr.qr_rank(hq, big, to_dev(np.zeros(3, np.uint8), cuda), torch.empty_like(big))
+        g = torch.empty(q.size, dtype=torch.uint64, device=cuda)
+        qr.qr_gather_ceiling(hq, to_dev(q, cuda), g, 0)
+        qr.qr_sync()
+    finally:
+        qr.qr_set_tuning("rank_k", 2)
+    assert np.array_equal(ob, oracle.BitsOracle(wb, n).rank(q))
+    oraq = oracle.DnaOracle(wd, n)
+    assert np.array_equal(oq, oraq.rank(q, c))
+    assert np.array_equal(o4, oraq.rank_all4(q))
+    lines, _ = qr.qr_export_layout(hq)
+    u64 = lines.view(np.uint64).reshape(-1, 8)
+    assert np.array_equal(to_host(g), np.bitwise_xor.reduce(u64[(q >> np.uint64(7)).astype(np.int64)], axis=1))
+    with pytest.raises(qr.QrError):
+        qr.qr_build(wb, n, 99)
