@@ -375,6 +375,39 @@ def bench_variants(ctx, steps, warmup):
     return res
 
 
+def bench_latency(ctx, steps, warmup):
+    """Dependent-chain ("latency") mode vs the independent-query ("loop") mode on configs[1]
+    (the paper reports ~80 ns per dependent query on DDR4)."""
+    import gen
+    import paper_2602_04103_b200 as qr
+
+    torch = ctx.torch
+    bits = torch.empty((N2 + 63) // 64, dtype=torch.uint64, device=ctx.dev)
+    gen.bits_dev(SEED[2], N2, 0.5, bits)
+    res = {}
+    for name, layout in (("birank16", qr.QR_LAYOUT_BIRANK16), ("birank64x2", qr.QR_LAYOUT_BIRANK64X2)):
+        h = qr.qr_build(bits, N2, layout, device=ctx.gpu)
+        L, chains = 2000, 148                          # one chain per SM: pure latency
+        m = L * chains
+        q = torch.empty(m, dtype=torch.uint64, device=ctx.dev)
+        gen.queries_dev(SEED[2], N2, m, q)
+        out = torch.empty_like(q)
+        ms = ctx.timed(lambda: qr.qr_rank_chain(h, q, None, out, L, m, ctx.stream), max(2, steps // 2), warmup)
+        L2, chains2 = 200, 148 * 2048                  # many chains: latency-bound throughput
+        m2 = L2 * chains2
+        q2 = torch.empty(m2, dtype=torch.uint64, device=ctx.dev)
+        gen.queries_dev(SEED[2] + 1, N2, m2, q2)
+        out2 = torch.empty_like(q2)
+        ms2 = ctx.timed(lambda: qr.qr_rank_chain(h, q2, None, out2, L2, m2, ctx.stream), max(2, steps // 2), warmup)
+        res[name] = {"ns_per_dependent_query": ms * 1e6 / L, "chains": chains, "chain_len": L,
+                     "many_chains_gq_s": m2 / ms2 / 1e6, "many_chains": chains2}
+        h.free()
+        del q, out, q2, out2
+    del bits
+    torch.cuda.empty_cache()
+    return res
+
+
 def bench_small(ctx, steps, warmup):
     import gen
     import paper_2602_04103_b200 as qr
@@ -479,6 +512,7 @@ def main():
         rows["c5_reads_150bp_both_strands"] = bench_reads(ctx, N5, 10**7, 150, 55, K, W)
         rows["c4_quadfm_approx1"] = bench_approx(ctx, N4, 10**6, L4, SEED[4], K, W)
         rows["layout_variants"] = bench_variants(ctx, K, W)
+        rows["latency_mode"] = bench_latency(ctx, K, W)
         rows["c1_small"] = bench_small(ctx, K, W)
     ms = c2["ms"]
     value = c2["gq_s"]

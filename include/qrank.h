@@ -99,6 +99,14 @@ qr_status qr_rank(const qr_index* h, const uint64_t* q, const uint8_t* c, uint64
  * only (QR_EINVAL on a BiRank handle).  Output is 32 B per query, array-of-structs. */
 qr_status qr_rank_all4(const qr_index* h, const uint64_t* q, uint64_t* out4, uint64_t m, void* stream);
 
+/* Dependent-chain ("latency") mode (SPEC S:413 chaining rule; NEXT §8(f)4):
+ * the m queries form chains of chain_len consecutive entries; inside a chain the i-th query
+ * is q_eff = (q[i] + r_{i-1}) mod (n+1) with r_{-1} = 0, and out[i] = r_i = rank(q_eff, c[i])
+ * (c as in qr_rank; NULL on sigma = 2 means rank(q)).  One thread walks each chain, so the time
+ * per step is the latency of one dependent random gather.  Any layout; device pointers only. */
+qr_status qr_rank_chain(const qr_index* h, const uint64_t* q, const uint8_t* c, uint64_t* out, uint64_t m,
+                        uint64_t chain_len, void* stream);
+
 /* ------------------------------------------------------------------ QuadFm */
 
 /* Count-only FM index over a DNA text (App. D).  Builds the suffix

@@ -28,7 +28,7 @@ EXPORTS = (
     "qr_birank_build", "qr_quadrank_build", "qr_rank", "qr_rank_all4", "qr_fm_build", "qr_fm_count", "qr_fm_count_both", "qr_fm_count_approx",
     "qr_fm_count_work", "qr_gather_ceiling", "qr_info", "qr_export_layout", "qr_fm_info", "qr_fm_export_kmer",
     "qr_clone_to_device", "qr_fm_clone_to_device", "qr_sync", "qr_free", "qr_fm_free", "qr_last_error",
-    "qr_version", "qr_set_tuning", "qr_build", "qr_layout",
+    "qr_version", "qr_set_tuning", "qr_build", "qr_layout", "qr_rank_chain",
 )
 
 
@@ -75,6 +75,7 @@ def lib():
             "qr_set_tuning": ([C.c_char_p, C.c_int64], I32),
             "qr_build": ([V, U64, I32, I32, V, PP], I32),
             "qr_layout": ([V, C.POINTER(C.c_int)], I32),
+            "qr_rank_chain": ([V, V, V, V, U64, U64, V], I32),
         }
         for name, (args, res) in sig.items():
             f = getattr(L, name)
@@ -188,6 +189,12 @@ def qr_quadrank_build(text2b, n: int, device: int = 0, stream=None) -> Index:
 def qr_rank(h: Index, q, c, out, m: int | None = None, stream=None):
     m = (q.numel() if hasattr(q, "numel") else q.size) if m is None else m
     _check(lib().qr_rank(h.ptr, _ptr(q), _ptr(c), _ptr(out), m, _stream(stream)), "qr_rank")
+    return out
+
+
+def qr_rank_chain(h: Index, q, c, out, chain_len: int, m: int | None = None, stream=None):
+    m = (q.numel() if hasattr(q, "numel") else q.size) if m is None else m
+    _check(lib().qr_rank_chain(h.ptr, _ptr(q), _ptr(c), _ptr(out), m, chain_len, _stream(stream)), "qr_rank_chain")
     return out
 
 

@@ -397,6 +397,18 @@ QR_EXPORT qr_status qr_rank(const qr_index* h, const uint64_t* q, const uint8_t*
   });
 }
 
+QR_EXPORT qr_status qr_rank_chain(const qr_index* h, const uint64_t* q, const uint8_t* c, uint64_t* out, uint64_t m,
+                                  uint64_t chain_len, void* stream) {
+  if (!h) return fail(QR_EINVAL, "qr_rank_chain: null handle");
+  if (m == 0) return QR_OK;
+  if (!q || !out || chain_len == 0) return fail(QR_EINVAL, "qr_rank_chain: null q/out or chain_len = 0");
+  if (h->sigma == 4 && !c) return fail(QR_EINVAL, "qr_rank_chain: sigma=4 requires c");
+  DeviceGuard dg(h->device);
+  if (classify({q, c, out}, h->device) != 1) return fail(QR_EINVAL, "qr_rank_chain: device pointers only");
+  cudaError_t e = launch_rank_chain(h, q, c, out, m, chain_len, (cudaStream_t)stream);
+  return e ? cuda_fail(e, "qr_rank_chain launch") : QR_OK;
+}
+
 QR_EXPORT qr_status qr_rank_all4(const qr_index* h, const uint64_t* q, uint64_t* out4, uint64_t m, void* stream) {
   if (!h) return fail(QR_EINVAL, "qr_rank_all4: null handle");
   if (h->sigma != 4) return fail(QR_EINVAL, "qr_rank_all4: needs a QuadRank (sigma=4) handle");

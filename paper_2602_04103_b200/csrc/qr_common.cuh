@@ -66,6 +66,8 @@ qr_status alloc_index(int sigma, uint64_t n, int device, qr_index** out, int lay
 uint64_t super_bytes_of(const qr_index* h);
 qr_status birank64x2_build_device(const uint64_t* d_bits, uint64_t n, int device, cudaStream_t st, qr_index** out);
 qr_status quadrank64_build_device(const uint64_t* d_text, uint64_t n, int device, cudaStream_t st, qr_index** out);
+cudaError_t launch_rank_chain(const qr_index* h, const uint64_t* q, const uint8_t* c, uint64_t* out, uint64_t m,
+                              uint64_t chain_len, cudaStream_t st);
 cudaError_t launch_variant(const qr_index* h, const uint64_t* q, const uint8_t* c, uint64_t* out, uint64_t m, int what,
                            cudaStream_t st);
 

@@ -320,4 +320,114 @@ cudaError_t launch_variant(const qr_index* h, const uint64_t* q, const uint8_t* 
   }
 }
 
+
+// ------------------------------------------------------------------ latency (dependent-chain) mode
+// The paper's "latency" benchmark mode (each query "dependent on the result of
+// the previous one"; NEXT §8(f)4) with SPEC's chaining rule: within a chain of length L,
+// the i-th query is q_eff = (q[i] + r_{i-1}) mod (n+1), r_{-1} = 0, and out[i] = rank(q_eff, c[i]).
+// One thread per chain, one rank at a time: the time per step is the loaded latency of one
+// random line gather (+ the superblock word), the GPU analogue of the paper's ~80 ns DRAM bound.
+namespace {
+struct RankOne {
+  const qr_index h;
+  __device__ __forceinline__ uint64_t operator()(uint64_t q, uint32_t c) const {
+    const uint64_t last = h.n_lines - 1;
+    uint64_t a[4], b[4] = {0, 0, 0, 0};
+    if (h.layout == QR_LAYOUT_BIRANK16) {
+      uint64_t j = q / BI_B;
+      j = j > last ? last : j;
+      uint64_t p = 16 + q - j * BI_B;
+      p = p > 511 ? 511 : p;
+      const uint4* ln = h.lines + 4 * j;
+      ld_sector_na(ln, a[0], a[1], a[2], a[3]);
+      if (p >= 256) ld_sector_na(ln + 2, b[0], b[1], b[2], b[3]);
+      const uint32_t s = __ldg(h.super + (j >> BI_SB_LOG));
+      const bool right = p >= 256;
+      const int x = (int)(p & 255u);
+      uint32_t cnt = 0;
+#pragma unroll
+      for (int t = 0; t < 4; ++t) cnt += __popcll((right ? b[t] : a[t]) & (prefix_mask(x, t) ^ (right ? 0ull : ~0ull)));
+      const uint64_t base = ((uint64_t)s << BI_SHIFT) + (a[0] & 0xffffull);
+      const uint64_t r = right ? base + cnt : base - cnt;
+      return c == 0 ? q - r : r;
+    }
+    if (h.layout == QR_LAYOUT_BIRANK64X2) {
+      uint64_t j = q / 384;
+      j = j > last ? last : j;
+      uint64_t rr = q - j * 384;
+      rr = rr > 383 ? 383 : rr;
+      const uint32_t hh = rr >= 192 ? 1u : 0u;
+      const int x = (int)(rr - 192 * hh);
+      ld_sector_na(h.lines + 4 * j + 2 * hh, a[0], a[1], a[2], a[3]);
+      const uint32_t cnt = __popcll(a[1] & (prefix_mask(x, 0) ^ ~0ull)) +
+                           __popcll(a[2] & (prefix_mask(x, 1) ^ 0xffffffffull)) + __popcll(a[3] & prefix_mask(x, 2));
+      const uint64_t r = x >= 96 ? a[0] + cnt : a[0] - cnt;
+      return c == 0 ? q - r : r;
+    }
+    const uint64_t cl = 0ull - (uint64_t)(c & 1u), ch = 0ull - (uint64_t)((c >> 1) & 1u);
+    if (h.layout == QR_LAYOUT_QUADRANK16) {
+      uint64_t j = q / QD_B;
+      j = j > last ? last : j;
+      uint64_t p = 32 + q - j * QD_B;
+      p = p > 255 ? 255 : p;
+      const uint4* ln = h.lines + 4 * j;
+      ld_sector_na(ln, a[0], a[1], a[2], a[3]);
+      if (p >= 128) ld_sector_na(ln + 2, b[0], b[1], b[2], b[3]);
+      const uint32_t s = __ldg(h.super + 4 * (j >> QD_SB_LOG) + (c & 3u));
+      const bool right = p >= 128;
+      const int x = (int)(p & 127u);
+      const uint64_t* w = right ? b : a;
+      const uint64_t inv = right ? 0ull : ~0ull;
+      const uint32_t cnt = __popcll((w[0] ^ cl) & (w[1] ^ ch) & (prefix_mask(x, 0) ^ inv)) +
+                           __popcll((w[2] ^ cl) & (w[3] ^ ch) & (prefix_mask(x, 1) ^ inv));
+      const uint64_t dw = (c & 2u) ? a[1] : a[0];
+      const uint64_t base = ((uint64_t)s << QD_SHIFT) + ((dw >> (16 * (c & 1u))) & 0xffffull);
+      return right ? base + cnt : base - cnt;
+    }
+    // QuadRank64
+    uint64_t j = q >> 7;
+    j = j > last ? last : j;
+    const uint64_t x = (j << 7 == (q & ~127ull)) ? (q & 127u) : 127u;
+    const uint4* ln = h.lines + 4 * j;
+    ld_sector_na(ln, a[0], a[1], a[2], a[3]);
+    ld_sector_na(ln + 2, b[0], b[1], b[2], b[3]);
+    const bool right = x >= 64;
+    const int y = (int)(x & 63u);
+    const uint64_t wl = right ? b[2] : b[0], wh = right ? b[3] : b[1];
+    const uint32_t cnt = __popcll((wl ^ cl) & (wh ^ ch) & (prefix_mask(y, 0) ^ (right ? 0ull : ~0ull)));
+    const uint64_t v = (c & 2u) ? ((c & 1u) ? a[3] : a[2]) : ((c & 1u) ? a[1] : a[0]);
+    return right ? v + cnt : v - cnt;
+  }
+};
+}  // namespace
+
+__global__ void k_rank_chain(const qr_index h, const uint64_t* __restrict__ q, const uint8_t* __restrict__ cs,
+                             uint64_t* __restrict__ out, uint64_t m, uint64_t chain_len) {
+  const RankOne rank{h};
+  const uint64_t chains = (m + chain_len - 1) / chain_len;
+  const uint64_t np1 = h.n + 1;
+  for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < chains; k += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t r = 0;
+    const uint64_t end = (k + 1) * chain_len < m ? (k + 1) * chain_len : m;
+    for (uint64_t i = k * chain_len; i < end; ++i) {
+      uint64_t qe = q[i] + r;                     // q[i] <= n and r <= n: one subtraction is the mod
+      qe = qe >= np1 ? qe - np1 : qe;
+      const uint32_t c = cs ? (uint32_t)cs[i] : 1u;
+      r = rank(qe, c);
+      out[i] = r;
+    }
+  }
+}
+
+cudaError_t launch_rank_chain(const qr_index* h, const uint64_t* q, const uint8_t* c, uint64_t* out, uint64_t m,
+                              uint64_t chain_len, cudaStream_t st) {
+  if (m == 0) return cudaSuccess;
+  const uint64_t chains = (m + chain_len - 1) / chain_len;
+  const unsigned threads = chains < 128 ? 32u : 128u;
+  uint64_t g = (chains + threads - 1) / threads;
+  if (g > (uint64_t)h->sm_count * 64) g = (uint64_t)h->sm_count * 64;
+  k_rank_chain<<<(unsigned)g, threads, 0, st>>>(*h, q, c, out, m, chain_len);
+  return cudaGetLastError();
+}
+
 }  // namespace qr

@@ -101,3 +101,53 @@ def test_variants_tuning_and_host_path(cuda, k):
     assert np.array_equal(to_host(g), np.bitwise_xor.reduce(u64[(q >> np.uint64(7)).astype(np.int64)], axis=1))
     with pytest.raises(qr.QrError):
         qr.qr_build(wb, n, 99)
+
+
+def _chain_reference(rank_fn, q, n, L):
+    """Host simulation of the dependent chains with the oracle (SPEC S:413 rule)."""
+    m = q.size
+    out = np.zeros(m, np.uint64)
+    chains = (m + L - 1) // L
+    qq = np.zeros((chains, L), np.uint64)
+    valid = np.zeros((chains, L), bool)
+    flat = np.arange(chains * L)
+    qq.reshape(-1)[: m] = q
+    valid.reshape(-1)[: m] = True
+    r = np.zeros(chains, np.uint64)
+    for i in range(L):
+        qe = qq[:, i] + r
+        qe = np.where(qe >= n + 1, qe - np.uint64(n + 1), qe)
+        ri = rank_fn(qe, i)
+        r = np.where(valid[:, i], ri, r)
+        idx = np.arange(chains) * L + i
+        ok = idx < m
+        out[idx[ok]] = ri[ok]
+    del flat
+    return out
+
+
+@pytest.mark.parametrize("layout", [qr.QR_LAYOUT_BIRANK16, qr.QR_LAYOUT_BIRANK64X2, qr.QR_LAYOUT_QUADRANK16,
+                                    qr.QR_LAYOUT_QUADRANK64])
+def test_rank_chain_latency_mode(cuda, layout):
+    torch = _torch()
+    n = 3 * 63488 + 1001
+    bits = layout in (qr.QR_LAYOUT_BIRANK16, qr.QR_LAYOUT_BIRANK64X2)
+    w = gen.bits(21, n) if bits else gen.dna(22, n)
+    h = qr.qr_build(w, n, layout)
+    m, L = 40003, 37                                  # ragged last chain
+    q, c = gen.queries(23, n, m, with_c=True)
+    if bits:
+        ora = oracle.BitsOracle(w, n)
+        ref = _chain_reference(lambda qe, i: ora.rank(qe), q, n, L)
+        cdev = None
+    else:
+        ora = oracle.DnaOracle(w, n)
+        cc = np.zeros(((m + L - 1) // L) * L, np.uint8)
+        cc[:m] = c
+        cm = cc.reshape(-1, L)
+        ref = _chain_reference(lambda qe, i: ora.rank(qe, cm[:, i]), q, n, L)
+        cdev = to_dev(c, cuda)
+    out = torch.empty(m, dtype=torch.uint64, device=cuda)
+    qr.qr_rank_chain(h, to_dev(q, cuda), cdev, out, L)
+    torch.cuda.synchronize()
+    assert np.array_equal(to_host(out), ref)
