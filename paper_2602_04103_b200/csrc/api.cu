@@ -21,7 +21,9 @@ namespace qr {
 int g_rank_k = 2;               // independent queries per lane (pair) per iteration
 int g_rank_blocks_per_sm = 64;  // 256-thread CTAs per SM of the grid (several waves)
 int g_fm_blocks_per_sm = 64;    // 256-thread CTAs per SM of the FM grid (several waves)
-int g_rank_s_lane = 1;          // lane of a pair that loads the superblock word
+int g_rank_s_lane = 1;
+int g_fm_lean = 0;              // 1: lean FM step (fm_step_lean)
+int g_index64 = 0;              // 1: force the 64-bit line-index path (tests the n >= 2^36/2^37 code on small n)          // lane of a pair that loads the superblock word
 int g_rank_pair = 1;            // 1: lane-pair kernels (one L2 request per query); 0: one lane per query
 uint64_t g_stage_chunk = 1ull << 23;   // queries per chunk on the staged host path (sweep: profiles/r01_e2e_sweep)
 int g_stage_slots = 3;                 // device buffers / internal streams of the staged path
@@ -271,6 +273,12 @@ QR_EXPORT qr_status qr_set_tuning(const char* key, int64_t value) {
   } else if (!strcmp(key, "rank_s_lane")) {
     if (value != 0 && value != 1) return fail(QR_EINVAL, "rank_s_lane must be 0 or 1");
     g_rank_s_lane = (int)value;
+  } else if (!strcmp(key, "fm_step")) {
+    if (value != 0 && value != 1) return fail(QR_EINVAL, "fm_step must be 0 or 1");
+    g_fm_lean = (int)value;
+  } else if (!strcmp(key, "index64")) {
+    if (value != 0 && value != 1) return fail(QR_EINVAL, "index64 must be 0 or 1");
+    g_index64 = (int)value;
   } else if (!strcmp(key, "fm_blocks_per_sm")) {
     if (value < 1 || value > 64) return fail(QR_EINVAL, "fm_blocks_per_sm out of range");
     g_fm_blocks_per_sm = (int)value;

@@ -307,12 +307,13 @@ __global__ void __launch_bounds__(256) k_bi_gather2(const uint4* __restrict__ li
 extern int g_rank_k;              // tuning knobs (api.cu)
 extern int g_rank_blocks_per_sm;
 extern int g_rank_pair;
+extern int g_index64;
 extern int g_rank_s_lane;
 
 template <int K>
 static cudaError_t bi_rank_k(const qr_index* h, const uint64_t* q, const uint8_t* c, uint64_t* out, uint64_t m,
                              cudaStream_t st) {
-  const bool small = h->n < (1ull << 36);
+  const bool small = h->n < (1ull << 36) && !g_index64;
   const uint64_t per_thread = g_rank_pair ? K : 2 * K;   // pair kernels: 2 threads per query
   unsigned g = grid_stride_blocks((2 * m + per_thread - 1) / per_thread, 256, h->sm_count, g_rank_blocks_per_sm);
   const uint64_t last = h->n_lines - 1;
@@ -352,7 +353,7 @@ cudaError_t launch_birank_rank(const qr_index* h, const uint64_t* q, const uint8
 template <int K>
 static cudaError_t bi_gather_k(const qr_index* h, const uint64_t* q, uint64_t* out, uint64_t m, int mode,
                                cudaStream_t st) {
-  const bool small = h->n < (1ull << 36);
+  const bool small = h->n < (1ull << 36) && !g_index64;
   const uint64_t per_thread = g_rank_pair ? K : 2 * K;
   unsigned g = grid_stride_blocks((2 * m + per_thread - 1) / per_thread, 256, h->sm_count, g_rank_blocks_per_sm);
   const uint64_t last = h->n_lines - 1;

@@ -273,6 +273,40 @@ struct PatWindow {
   }
 };
 
+// Lean variant of fm_step (knob "fm_step" = 1): each rank loads its counted half directly
+// (sector 0 left of the anchor, sector 1 right of it) and, only when right, the one u64 word of
+// sector 0 that holds its delta; no de-duplication of shared lines (the L1 merges them), so no
+// register copies or half selects.  Fewer instructions, a few more L1 wavefronts.
+__device__ __forceinline__ uint32_t fm_rank_lean(const FmParams& F, uint32_t x, uint32_t c, uint64_t cl, uint64_t ch) {
+  const uint32_t j = (x >> 5) / 7u;                  // x <= N: j <= last_line, no clamp needed
+  const uint32_t p = 32u + x - j * (uint32_t)QD_B;
+  const bool right = p >= 128;
+  const uint4* L = F.lines + 4 * (uint64_t)j;
+  uint64_t w0, w1, w2, w3;
+  ld_sector(L + 2 * (right ? 1 : 0), w0, w1, w2, w3);
+  uint64_t dr = 0;
+  if (right) dr = __ldg(reinterpret_cast<const unsigned long long*>(L) + (c >> 1));
+  const uint32_t s = __ldg(F.super + 4 * (j >> QD_SB_LOG) + c);
+  const int xx = (int)(p & 127u);
+  const uint64_t inv = right ? 0ull : ~0ull;
+  const uint32_t cnt = __popcll((w0 ^ cl) & (w1 ^ ch) & (prefix_mask(xx, 0) ^ inv)) +
+                       __popcll((w2 ^ cl) & (w3 ^ ch) & (prefix_mask(xx, 1) ^ inv));
+  const uint64_t dw = right ? dr : ((c & 2u) ? w1 : w0);
+  const uint32_t base = (s << QD_SHIFT) + (uint32_t)((dw >> (16 * (c & 1u))) & 0xffffull);
+  return right ? base + cnt : base - cnt;
+}
+
+__device__ __forceinline__ void fm_step_lean(const FmParams& F, uint32_t c, uint32_t& lo, uint32_t& hi, uint32_t& lines) {
+  const uint64_t cl = 0ull - (uint64_t)(c & 1u), ch = 0ull - (uint64_t)(c >> 1);
+  const uint32_t Cc = __ldg(F.Ct + c);
+  uint32_t rl = fm_rank_lean(F, lo, c, cl, ch);
+  uint32_t rh = fm_rank_lean(F, hi, c, cl, ch);
+  lines = ((lo >> 5) / 7u == (hi >> 5) / 7u) ? 1u : 2u;
+  if (c == 0) { rl -= (lo > (uint32_t)F.spos); rh -= (hi > (uint32_t)F.spos); }
+  lo = Cc + rl;
+  hi = Cc + rh;
+}
+
 // 8-mer table key of the pattern's last 8 symbols (P[len-8..len), 2 bits each, the last symbol
 // in the low bits — PAPER.md:918, reading R14) from one unaligned 8-byte read: reverse the byte
 // order, keep 2 bits per byte and compact the eight 2-bit fields into 16 bits.
@@ -303,7 +337,7 @@ __device__ __forceinline__ uint32_t kmer_key8_rc(const uint8_t* first8) { return
 // 2i+1 its reverse complement RC(P)[j] = 3 - P[len-1-j] ("both forward and
 // reverse-complement direction"; NEXT §8(f)1), read from the same bytes in the opposite
 // direction, so no reverse-complemented copy is ever materialised.
-template <bool FIXED, bool WORK, int STRANDS>
+template <bool FIXED, bool WORK, int STRANDS, bool LEAN>
 __global__ void __launch_bounds__(256, 4) k_fm_count(FmParams F, const uint8_t* __restrict__ pat,
                                                      const uint64_t* __restrict__ offs, const uint32_t* __restrict__ lens,
                                                      uint32_t fixed_len, uint32_t* __restrict__ out,
@@ -337,7 +371,8 @@ __global__ void __launch_bounds__(256, 4) k_fm_count(FmParams F, const uint8_t* 
     if (k >= 0 && lo < hi) {                             // one backward step (LF mapping)
       const uint32_t c = rc ? 3u - P.at((int64_t)len - 1 - k) : P.at(k);
       uint32_t nl;
-      fm_step(F, c, lo, hi, nl);
+      if (LEAN) fm_step_lean(F, c, lo, hi, nl);
+      else      fm_step(F, c, lo, hi, nl);
       --k;
       if (WORK) { n_steps += 1; n_lines += nl; }
     }
@@ -478,13 +513,19 @@ static FmParams params_of(const qr_fm* fm) {
 }
 
 extern int g_fm_blocks_per_sm;
+extern int g_fm_lean;
 
 template <bool FIXED, bool WORK>
 static void launch_fm(unsigned g, cudaStream_t st, const FmParams& F, const uint8_t* pat, const uint64_t* offs,
                       const uint32_t* lens, uint32_t fixed_len, uint32_t* out, uint32_t* out_rc, uint64_t m,
                       unsigned long long* w) {
-  if (out_rc) k_fm_count<FIXED, WORK, 2><<<g, 256, 0, st>>>(F, pat, offs, lens, fixed_len, out, out_rc, m, w);
-  else        k_fm_count<FIXED, WORK, 1><<<g, 256, 0, st>>>(F, pat, offs, lens, fixed_len, out, out_rc, m, w);
+  if (g_fm_lean) {
+    if (out_rc) k_fm_count<FIXED, WORK, 2, true><<<g, 256, 0, st>>>(F, pat, offs, lens, fixed_len, out, out_rc, m, w);
+    else        k_fm_count<FIXED, WORK, 1, true><<<g, 256, 0, st>>>(F, pat, offs, lens, fixed_len, out, out_rc, m, w);
+  } else {
+    if (out_rc) k_fm_count<FIXED, WORK, 2, false><<<g, 256, 0, st>>>(F, pat, offs, lens, fixed_len, out, out_rc, m, w);
+    else        k_fm_count<FIXED, WORK, 1, false><<<g, 256, 0, st>>>(F, pat, offs, lens, fixed_len, out, out_rc, m, w);
+  }
 }
 
 qr_status fm_count_device(const qr_fm* fm, const uint8_t* pat, const uint32_t* lengths, uint32_t fixed_len,

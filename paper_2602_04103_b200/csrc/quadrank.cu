@@ -462,6 +462,7 @@ __global__ void __launch_bounds__(256) k_qd_gather2(const uint4* __restrict__ li
 extern int g_rank_k;
 extern int g_rank_blocks_per_sm;
 extern int g_rank_pair;
+extern int g_index64;
 
 template <int K>
 static unsigned qd_grid(const qr_index* h, uint64_t m) {
@@ -473,7 +474,7 @@ static cudaError_t qd_rank_k(const qr_index* h, const uint64_t* q, const uint8_t
                              cudaStream_t st) {
   unsigned g = qd_grid<K>(h, m);
   const uint64_t last = h->n_lines - 1;
-  const bool small = h->n < (1ull << 37);
+  const bool small = h->n < (1ull << 37) && !g_index64;
   if (g_rank_pair) {
     if (small) k_qd_rank2<K, true><<<g, 256, 0, st>>>(h->lines, h->super, q, c, out, m, last);
     else       k_qd_rank2<K, false><<<g, 256, 0, st>>>(h->lines, h->super, q, c, out, m, last);
@@ -487,7 +488,7 @@ template <int K>
 static cudaError_t qd_all4_k(const qr_index* h, const uint64_t* q, uint64_t* out4, uint64_t m, cudaStream_t st) {
   unsigned g = qd_grid<K>(h, m);
   const uint64_t last = h->n_lines - 1;
-  const bool small = h->n < (1ull << 37);
+  const bool small = h->n < (1ull << 37) && !g_index64;
   if (g_rank_pair) {
     if (small) k_qd_all4_2<K, true><<<g, 256, 0, st>>>(h->lines, h->super, q, out4, m, last);
     else       k_qd_all4_2<K, false><<<g, 256, 0, st>>>(h->lines, h->super, q, out4, m, last);
@@ -502,7 +503,7 @@ static cudaError_t qd_gather_k(const qr_index* h, const uint64_t* q, uint64_t* o
                                cudaStream_t st) {
   unsigned g = qd_grid<K>(h, m);
   const uint64_t last = h->n_lines - 1;
-  const bool small = h->n < (1ull << 37);
+  const bool small = h->n < (1ull << 37) && !g_index64;
   if (mode == 2) mode = 0;   // (superblock-inclusive ceiling: BiRank only)
   if (g_rank_pair) {
     if (small) {

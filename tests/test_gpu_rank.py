@@ -339,3 +339,32 @@ def test_edge_cases_and_contract(cuda):
     torch.cuda.synchronize()
     assert np.array_equal(to_host(d1), to_host(d2))
     assert fm2.C == fm.C and fm2.spos == fm.spos
+
+
+@pytest.mark.parametrize("pair", [0, 1])
+def test_index64_path(cuda, pair):
+    """The 64-bit line-index path (selected for n >= 2^36 / 2^37) forced on small n: bit-exact."""
+    torch = _torch()
+    n = 5 * S + 4321
+    w, t = gen.bits(41, n), gen.dna(42, n)
+    hb, hq = qr.qr_birank_build(w, n), qr.qr_quadrank_build(t, n)
+    q, c = gen.queries(43, n, 100000, with_c=True)
+    q = np.concatenate([q, boundary_queries(n, B, S, 240)])
+    c = np.concatenate([c, (np.arange(q.size - c.size) % 4).astype(np.uint8)])
+    dq, dc = to_dev(q, cuda), to_dev(c, cuda)
+    ob, oq = torch.empty_like(dq), torch.empty_like(dq)
+    o4 = torch.empty((q.size, 4), dtype=torch.uint64, device=cuda)
+    qr.qr_set_tuning("index64", 1)
+    qr.qr_set_tuning("rank_pair", pair)
+    try:
+        qr.qr_rank(hb, dq, None, ob)
+        qr.qr_rank(hq, dq, dc, oq)
+        qr.qr_rank_all4(hq, dq, o4)
+        torch.cuda.synchronize()
+    finally:
+        qr.qr_set_tuning("index64", 0)
+        qr.qr_set_tuning("rank_pair", 1)
+    assert np.array_equal(to_host(ob), oracle.BitsOracle(w, n).rank(q))
+    ora = oracle.DnaOracle(t, n)
+    assert np.array_equal(to_host(oq), ora.rank(q, c))
+    assert np.array_equal(to_host(o4), ora.rank_all4(q))
