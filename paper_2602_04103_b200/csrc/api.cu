@@ -22,7 +22,7 @@ int g_rank_k = 2;               // independent queries per lane (pair) per itera
 int g_rank_blocks_per_sm = 64;  // 256-thread CTAs per SM of the grid (several waves)
 int g_fm_blocks_per_sm = 64;    // 256-thread CTAs per SM of the FM grid (several waves)
 int g_rank_s_lane = 1;
-int g_fm_lean = 0;              // 1: lean FM step (fm_step_lean)
+int g_fm_lean = 0;              // FM step flavour: 0 auto (by L2 residency), 1 de-duplicating, 2 lean
 int g_index64 = 0;              // 1: force the 64-bit line-index path (tests the n >= 2^36/2^37 code on small n)          // lane of a pair that loads the superblock word
 int g_rank_pair = 1;            // 1: lane-pair kernels (one L2 request per query); 0: one lane per query
 uint64_t g_stage_chunk = 1ull << 23;   // queries per chunk on the staged host path (sweep: profiles/r01_e2e_sweep)
@@ -67,6 +67,19 @@ int sm_count(int device) {
   if (!cache[device]) {
     int v = 0;
     if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device) != cudaSuccess || v <= 0) v = NUM_SMS_B200;
+    cache[device] = v;
+  }
+  return cache[device];
+}
+
+int l2_bytes(int device) {
+  static std::mutex mu;
+  static std::vector<int> cache;
+  std::lock_guard<std::mutex> g(mu);
+  if ((int)cache.size() <= device) cache.resize(device + 1, 0);
+  if (!cache[device]) {
+    int v = 0;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrL2CacheSize, device) != cudaSuccess || v <= 0) v = 126 << 20;
     cache[device] = v;
   }
   return cache[device];
@@ -274,7 +287,7 @@ QR_EXPORT qr_status qr_set_tuning(const char* key, int64_t value) {
     if (value != 0 && value != 1) return fail(QR_EINVAL, "rank_s_lane must be 0 or 1");
     g_rank_s_lane = (int)value;
   } else if (!strcmp(key, "fm_step")) {
-    if (value != 0 && value != 1) return fail(QR_EINVAL, "fm_step must be 0 or 1");
+    if (value < 0 || value > 2) return fail(QR_EINVAL, "fm_step must be 0 (auto), 1 or 2");
     g_fm_lean = (int)value;
   } else if (!strcmp(key, "index64")) {
     if (value != 0 && value != 1) return fail(QR_EINVAL, "index64 must be 0 or 1");

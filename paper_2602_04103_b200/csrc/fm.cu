@@ -515,11 +515,23 @@ static FmParams params_of(const qr_fm* fm) {
 extern int g_fm_blocks_per_sm;
 extern int g_fm_lean;
 
+int l2_bytes(int device);
+
+// Step flavour: the lean step issues fewer instructions but more L1 wavefronts and L2 requests
+// (no line de-duplication); it wins when the BWT layout is L2-resident (instruction bound,
+// configs[3]: 4.55 -> 5.53 G patterns/s) and loses when it is HBM-resident (request bound,
+// configs[4]: 0.81 -> 0.76).  Auto = lean iff the layout fits in half of the L2.
+static bool use_lean(const qr_fm* fm) {
+  if (g_fm_lean == 1) return false;
+  if (g_fm_lean == 2) return true;
+  return fm->bwt->n_lines * 64 <= (uint64_t)l2_bytes(fm->bwt->device) / 2;
+}
+
 template <bool FIXED, bool WORK>
-static void launch_fm(unsigned g, cudaStream_t st, const FmParams& F, const uint8_t* pat, const uint64_t* offs,
+static void launch_fm(bool lean, unsigned g, cudaStream_t st, const FmParams& F, const uint8_t* pat, const uint64_t* offs,
                       const uint32_t* lens, uint32_t fixed_len, uint32_t* out, uint32_t* out_rc, uint64_t m,
                       unsigned long long* w) {
-  if (g_fm_lean) {
+  if (lean) {
     if (out_rc) k_fm_count<FIXED, WORK, 2, true><<<g, 256, 0, st>>>(F, pat, offs, lens, fixed_len, out, out_rc, m, w);
     else        k_fm_count<FIXED, WORK, 1, true><<<g, 256, 0, st>>>(F, pat, offs, lens, fixed_len, out, out_rc, m, w);
   } else {
@@ -539,8 +551,8 @@ qr_status fm_count_device(const qr_fm* fm, const uint8_t* pat, const uint32_t* l
   cudaError_t e;
   if (!lengths) {
     if (approx) k_fm_approx1<true><<<g, 256, 0, st>>>(F, pat, nullptr, nullptr, fixed_len, out, m);
-    else if (work) launch_fm<true, true>(g, st, F, pat, nullptr, nullptr, fixed_len, out, out_rc, m, w);
-    else      launch_fm<true, false>(g, st, F, pat, nullptr, nullptr, fixed_len, out, out_rc, m, w);
+    else if (work) launch_fm<true, true>(use_lean(fm), g, st, F, pat, nullptr, nullptr, fixed_len, out, out_rc, m, w);
+    else      launch_fm<true, false>(use_lean(fm), g, st, F, pat, nullptr, nullptr, fixed_len, out, out_rc, m, w);
     if ((e = cudaGetLastError())) return cuda_fail(e, "k_fm_count");
     return QR_OK;
   }
@@ -555,8 +567,8 @@ qr_status fm_count_device(const qr_fm* fm, const uint8_t* pat, const uint32_t* l
     cudaFreeAsync(offs, st); cudaFreeAsync(tmp, st); return cuda_fail(e, "scan");
   }
   if (approx) k_fm_approx1<false><<<g, 256, 0, st>>>(F, pat, offs, lengths, 0, out, m);
-  else if (work) launch_fm<false, true>(g, st, F, pat, offs, lengths, 0, out, out_rc, m, w);
-  else      launch_fm<false, false>(g, st, F, pat, offs, lengths, 0, out, out_rc, m, w);
+  else if (work) launch_fm<false, true>(use_lean(fm), g, st, F, pat, offs, lengths, 0, out, out_rc, m, w);
+  else      launch_fm<false, false>(use_lean(fm), g, st, F, pat, offs, lengths, 0, out, out_rc, m, w);
   e = cudaGetLastError();
   cudaFreeAsync(offs, st);
   cudaFreeAsync(tmp, st);

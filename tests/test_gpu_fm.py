@@ -12,6 +12,7 @@ import paper_2602_04103_b200 as qr
 from _util import to_dev, to_host
 
 pytestmark = pytest.mark.gpu
+DEFAULT_FM_STEP = 0
 
 
 def _torch():
@@ -175,8 +176,9 @@ def test_fm_all_kmers_partition(cuda):
             assert int(to_host(d).astype(np.int64).sum()) == n - k + 1
 
 
-@pytest.mark.parametrize("bps", [2, 4, 16, 64])
-def test_fm_tuning_does_not_change_results(cuda, bps):
+@pytest.mark.parametrize("step", [1, 2])
+@pytest.mark.parametrize("bps", [2, 16, 64])
+def test_fm_tuning_does_not_change_results(cuda, bps, step):
     torch = _torch()
     n = 90000
     w = gen.dna(31, n, 1)
@@ -190,6 +192,7 @@ def test_fm_tuning_does_not_change_results(cuda, bps):
     fixed = gen.patterns(9, 1, m, L, w, n)
     ref_fixed = ora.count(fixed, np.arange(m, dtype=np.uint64) * L, np.full(m, L, np.uint32))
     qr.qr_set_tuning("fm_blocks_per_sm", bps)
+    qr.qr_set_tuning("fm_step", step)
     try:
         d = torch.empty(lens.size, dtype=torch.int32, device=cuda)
         qr.qr_fm_count(fm, to_dev(cat, cuda), to_dev(lens, cuda), 0, d, lens.size)
@@ -197,8 +200,17 @@ def test_fm_tuning_does_not_change_results(cuda, bps):
         work = torch.zeros(2, dtype=torch.uint64, device=cuda)
         qr.qr_fm_count_work(fm, to_dev(fixed, cuda), None, L, d2, m, work)
         torch.cuda.synchronize()
+        db = torch.empty(m, dtype=torch.int32, device=cuda)
+        dr = torch.empty(m, dtype=torch.int32, device=cuda)
+        qr.qr_fm_count_both(fm, to_dev(fixed, cuda), None, L, db, dr, m)
+        torch.cuda.synchronize()
     finally:
         qr.qr_set_tuning("fm_blocks_per_sm", 64)
+        qr.qr_set_tuning("fm_step", DEFAULT_FM_STEP)
+    rc = np.concatenate([(3 - fixed[i * L:(i + 1) * L][::-1]).astype(np.uint8) for i in range(m)])
+    assert np.array_equal(to_host(db).view(np.uint32), ref_fixed)
+    assert np.array_equal(to_host(dr).view(np.uint32),
+                          ora.count(rc, np.arange(m, dtype=np.uint64) * L, np.full(m, L, np.uint32)))
     assert np.array_equal(to_host(d).view(np.uint32), ref)
     assert np.array_equal(to_host(d2).view(np.uint32), ref_fixed)
     ts, tl = ora.work(fixed, np.arange(m, dtype=np.uint64) * L, np.full(m, L, np.uint32), skip=8, block=224)
