@@ -169,6 +169,13 @@ qr_status qr_info(const qr_index* h, uint64_t* n, int* sigma, uint64_t* line_byt
 /* Copy the layout to host buffers of qr_info's sizes (either may be NULL). Synchronous. */
 qr_status qr_export_layout(const qr_index* h, void* host_lines, void* host_super);
 
+/* Re-create a handle from a layout saved with qr_export_layout (checkpoint / resume without
+ * rebuilding; builds are deterministic): lines and super are host or device buffers of
+ * the sizes qr_info reports for (n, layout); super may be NULL for layouts without an L1 array.
+ * The contents are trusted (no validation pass). */
+qr_status qr_import_layout(const void* lines, const void* super, uint64_t n, int layout, int device, void* stream,
+                           qr_index** out);
+
 /* n, N = n+1 BWT rows, spos, C[0..4] (C[4] = n+1), and the QuadRank handle over the BWT
  * (owned by fm; valid until qr_fm_free). */
 qr_status qr_fm_info(const qr_fm* fm, uint64_t* n, uint64_t* spos, uint64_t C[5], const qr_index** bwt_rank);

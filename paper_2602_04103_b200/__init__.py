@@ -28,7 +28,7 @@ EXPORTS = (
     "qr_birank_build", "qr_quadrank_build", "qr_rank", "qr_rank_all4", "qr_fm_build", "qr_fm_count", "qr_fm_count_both", "qr_fm_count_approx",
     "qr_fm_count_work", "qr_gather_ceiling", "qr_info", "qr_export_layout", "qr_fm_info", "qr_fm_export_kmer",
     "qr_clone_to_device", "qr_fm_clone_to_device", "qr_sync", "qr_free", "qr_fm_free", "qr_last_error",
-    "qr_version", "qr_set_tuning", "qr_build", "qr_layout", "qr_rank_chain",
+    "qr_version", "qr_set_tuning", "qr_build", "qr_layout", "qr_rank_chain", "qr_import_layout",
 )
 
 
@@ -76,6 +76,7 @@ def lib():
             "qr_build": ([V, U64, I32, I32, V, PP], I32),
             "qr_layout": ([V, C.POINTER(C.c_int)], I32),
             "qr_rank_chain": ([V, V, V, V, U64, U64, V], I32),
+            "qr_import_layout": ([V, V, U64, I32, I32, V, PP], I32),
         }
         for name, (args, res) in sig.items():
             f = getattr(L, name)
@@ -247,6 +248,29 @@ def qr_export_layout(h: Index):
     sup = np.empty(h.super_bytes, dtype=np.uint8)
     _check(lib().qr_export_layout(h.ptr, _ptr(lines), _ptr(sup)), "qr_export_layout")
     return lines, sup.view(np.uint32)
+
+
+def qr_import_layout(lines, sup, n: int, layout: int, device: int = 0, stream=None) -> Index:
+    out = C.c_void_p()
+    sp = _ptr(sup) if sup is not None and getattr(sup, "size", 1) else None
+    _check(lib().qr_import_layout(_ptr(lines), sp, n, layout, device, _stream(stream), C.byref(out)), "qr_import_layout")
+    return Index(out.value)
+
+
+def save_index(h: Index, path: str):
+    """Write a layout to a .npz file (header: n, layout; arrays: lines, super)."""
+    import numpy as np
+
+    lines, sup = qr_export_layout(h)
+    np.savez(path, n=np.uint64(h.n), layout=np.int32(h.layout), lines=lines, super=sup)
+
+
+def load_index(path: str, device: int = 0) -> Index:
+    import numpy as np
+
+    z = np.load(path)
+    return qr_import_layout(np.ascontiguousarray(z["lines"]), np.ascontiguousarray(z["super"]), int(z["n"]),
+                            int(z["layout"]), device)
 
 
 def qr_fm_export_kmer(fm: Fm):

@@ -582,6 +582,27 @@ QR_EXPORT qr_status qr_export_layout(const qr_index* h, void* host_lines, void* 
   return QR_OK;
 }
 
+QR_EXPORT qr_status qr_import_layout(const void* lines, const void* super, uint64_t n, int layout, int device,
+                                     void* stream, qr_index** out) {
+  if (!out || !lines) return fail(QR_EINVAL, "qr_import_layout: null pointer");
+  *out = nullptr;
+  if (layout < QR_LAYOUT_BIRANK16 || layout > QR_LAYOUT_QUADRANK64) return fail(QR_EINVAL, "qr_import_layout: bad layout");
+  DeviceGuard dg(device);
+  if (!dg.ok) return fail(QR_EINVAL, "qr_import_layout: bad device %d", device);
+  const int sigma = (layout == QR_LAYOUT_BIRANK16 || layout == QR_LAYOUT_BIRANK64X2) ? 2 : 4;
+  qr_index* h = nullptr;
+  qr_status s = alloc_index(sigma, n, device, &h, layout);
+  if (s != QR_OK) return s;
+  if (super_bytes_of(h) && !super) { qr_free(h); return fail(QR_EINVAL, "qr_import_layout: layout needs a superblock array"); }
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaError_t e = cudaMemcpyAsync(h->lines, lines, h->n_lines * 64, cudaMemcpyDefault, st);
+  if (!e && super_bytes_of(h)) e = cudaMemcpyAsync(h->super, super, super_bytes_of(h), cudaMemcpyDefault, st);
+  if (!e) e = cudaStreamSynchronize(st);
+  if (e) { qr_free(h); return cuda_fail(e, "qr_import_layout"); }
+  *out = h;
+  return QR_OK;
+}
+
 QR_EXPORT qr_status qr_fm_info(const qr_fm* fm, uint64_t* n, uint64_t* spos, uint64_t C[5], const qr_index** bwt_rank) {
   if (!fm) return fail(QR_EINVAL, "qr_fm_info: null handle");
   if (n) *n = fm->n;

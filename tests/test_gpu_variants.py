@@ -151,3 +151,30 @@ def test_rank_chain_latency_mode(cuda, layout):
     qr.qr_rank_chain(h, to_dev(q, cuda), cdev, out, L)
     torch.cuda.synchronize()
     assert np.array_equal(to_host(out), ref)
+
+
+@pytest.mark.parametrize("layout", [qr.QR_LAYOUT_BIRANK16, qr.QR_LAYOUT_BIRANK64X2, qr.QR_LAYOUT_QUADRANK16,
+                                    qr.QR_LAYOUT_QUADRANK64])
+def test_save_load_roundtrip(cuda, layout, tmp_path):
+    """Checkpoint/resume: export -> .npz -> import gives a handle that answers identically, and the
+    build is deterministic (byte-identical layout on a rebuild)."""
+    torch = _torch()
+    n = 2 * 63488 * 2 + 999
+    bits = layout in (qr.QR_LAYOUT_BIRANK16, qr.QR_LAYOUT_BIRANK64X2)
+    w = gen.bits(31, n) if bits else gen.dna(32, n)
+    h = qr.qr_build(w, n, layout)
+    p = str(tmp_path / "idx.npz")
+    qr.save_index(h, p)
+    h2 = qr.load_index(p)
+    assert (h2.n, h2.layout, h2.line_bytes, h2.super_bytes) == (h.n, h.layout, h.line_bytes, h.super_bytes)
+    l1, s1 = qr.qr_export_layout(h)
+    l3, s3 = qr.qr_export_layout(qr.qr_build(w, n, layout))
+    assert np.array_equal(l1, l3) and np.array_equal(s1, s3)
+    q, c = gen.queries(33, n, 50000, with_c=True)
+    dq = to_dev(q, cuda)
+    dc = None if bits else to_dev(c, cuda)
+    o1, o2 = torch.empty_like(dq), torch.empty_like(dq)
+    qr.qr_rank(h, dq, dc, o1)
+    qr.qr_rank(h2, dq, dc, o2)
+    torch.cuda.synchronize()
+    assert np.array_equal(to_host(o1), to_host(o2))
