@@ -191,10 +191,9 @@ def bench_birank(ctx, p: float, steps, warmup, with_ceiling: bool, clocks=None, 
             cms = ctx.timed(lambda: qr.qr_gather_ceiling(h, q, out, mode, m, ctx.stream), steps, warmup)
             res[f"ceiling_mode{mode}"] = {"ms": cms, "gq_s": ctx.world * m / cms / 1e6}
     if e2e:
-        me = 2 * 10**8
+        me = M2                                    # the full per-GPU batch, host-resident
         qh = torch.empty(me, dtype=torch.uint64).pin_memory()
-        gen_q = q[:me].cpu()
-        qh.copy_(gen_q)
+        qh.copy_(q[:me])
         oh = torch.empty(me, dtype=torch.uint64).pin_memory()
 
         def call():

@@ -337,6 +337,8 @@ __device__ __forceinline__ uint32_t kmer_key8_rc(const uint8_t* first8) { return
 // 2i+1 its reverse complement RC(P)[j] = 3 - P[len-1-j] ("both forward and
 // reverse-complement direction"; NEXT §8(f)1), read from the same bytes in the opposite
 // direction, so no reverse-complemented copy is ever materialised.
+// 4 resident CTAs (64 registers): capping registers for 6 or 8 CTAs/SM spills and runs 2-4x
+// slower on configs[3]/[4] (profiles/r01_fm_occupancy_sweep.jsonl).
 template <bool FIXED, bool WORK, int STRANDS, bool LEAN>
 __global__ void __launch_bounds__(256, 4) k_fm_count(FmParams F, const uint8_t* __restrict__ pat,
                                                      const uint64_t* __restrict__ offs, const uint32_t* __restrict__ lens,
