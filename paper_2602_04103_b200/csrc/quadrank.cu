@@ -379,12 +379,13 @@ __global__ void __launch_bounds__(256) k_qd_all4_2(const uint4* __restrict__ lin
     for (int k = 0; k < K; ++k) qq[k] = qn[k];
     qd_locate<K, SMALLQ>(qq, last_line, jj, pp);
     uint64_t w[K][4];
-    uint4 s[K];
+    uint2 s[K];
 #pragma unroll
     for (int k = 0; k < K; ++k) {
       w[k][0] = w[k][1] = w[k][2] = w[k][3] = 0;
       if (half == 0 || pp[k] >= 128) ld_sector_na(lines + 4 * jj[k] + 2 * half, w[k][0], w[k][1], w[k][2], w[k][3]);
-      s[k] = half == 0 ? __ldg(reinterpret_cast<const uint4*>(super) + (jj[k] >> QD_SB_LOG)) : make_uint4(0, 0, 0, 0);
+      // lane 0 reads s_A, s_C and lane 1 s_G, s_T: one 16-B segment, one request for the pair
+      s[k] = __ldg(reinterpret_cast<const uint2*>(super) + 2 * (jj[k] >> QD_SB_LOG) + half);
     }
     qd_load_group<K, false>(q, nullptr, i0 + npair * K, npair, m, qn, cn);
 #pragma unroll
@@ -404,22 +405,19 @@ __global__ void __launch_bounds__(256) k_qd_all4_2(const uint4* __restrict__ lin
       }
       const uint32_t len = half ? (uint32_t)x : 128u - (uint32_t)x;
       // four counts <= 128 packed in 8-bit fields: A | C << 8 | G << 16 | T << 24
-      uint32_t packed = (len - nl - nh + nt) | ((nl - nt) << 8) | ((nh - nt) << 16) | (nt << 24);
-      uint32_t other = __shfl_xor_sync(0xffffffffu, packed, 1);
-      if (half == 0 && idx < m) {
-        const uint32_t cnt = right ? other : packed;
-        uint32_t sv[4] = {s[k].x, s[k].y, s[k].z, s[k].w};
-        uint64_t r[4];
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          uint64_t dw = (c & 2) ? w[k][1] : w[k][0];
-          uint64_t delta = (dw >> (16 * (c & 1))) & 0xffffull;
-          uint64_t base = ((uint64_t)sv[c] << QD_SHIFT) + delta;
-          uint32_t cc = (cnt >> (8 * c)) & 0xffu;
-          r[c] = right ? base + cc : base - cc;
-        }
-        st_stream_v4u64(out4 + 4 * idx, r[0], r[1], r[2], r[3]);
-      }
+      const uint32_t packed = (len - nl - nh + nt) | ((nl - nt) << 8) | ((nh - nt) << 16) | (nt << 24);
+      const uint32_t other = __shfl_xor_sync(0xffffffffu, packed, 1);
+      // lane 1 needs b_G | b_T << 16 (low half of sector-0 word 1, held by lane 0)
+      const uint32_t dgt = __shfl_xor_sync(0xffffffffu, (uint32_t)w[k][1], 1);
+      // each lane finishes two of the four symbols: lane 0 -> A, C; lane 1 -> G, T
+      const uint32_t cnt = (right == (half == 1)) ? packed : other;     // the counting lane's packed counts
+      const uint32_t dl = half ? dgt : (uint32_t)w[k][0];
+      const uint32_t c0 = (cnt >> (16 * half)) & 0xffu, c1 = (cnt >> (16 * half + 8)) & 0xffu;
+      const uint64_t b0 = ((uint64_t)s[k].x << QD_SHIFT) + (dl & 0xffffu);
+      const uint64_t b1 = ((uint64_t)s[k].y << QD_SHIFT) + (dl >> 16);
+      const uint64_t r0 = right ? b0 + c0 : b0 - c0, r1 = right ? b1 + c1 : b1 - c1;
+      if (idx < m) asm volatile("st.global.L1::no_allocate.v2.u64 [%0], {%1,%2};" ::"l"(out4 + 4 * idx + 2 * half),
+                                "l"(r0), "l"(r1) : "memory");
     }
   }
 }
