@@ -173,10 +173,22 @@ def bench_birank(ctx, p: float, steps, warmup, with_ceiling: bool, clocks=None, 
     import paper_2602_04103_b200 as qr
 
     torch = ctx.torch
-    bits = torch.empty((N2 + 63) // 64, dtype=torch.uint64, device=ctx.dev)
-    gen.bits_dev(SEED[2] if p == 0.5 else 22, N2, p, bits)
-    h = qr.qr_birank_build(bits, N2, device=ctx.gpu)
-    del bits
+    if ctx.dist and ctx.args.replicate == "broadcast":
+        # rank 0 builds; the layout is broadcast to every rank (NCCL over NVLink) and imported
+        from paper_2602_04103_b200.multigpu import broadcast_index
+
+        h0 = None
+        if ctx.rank == 0:
+            bits = torch.empty((N2 + 63) // 64, dtype=torch.uint64, device=ctx.dev)
+            gen.bits_dev(SEED[2] if p == 0.5 else 22, N2, p, bits)
+            h0 = qr.qr_birank_build(bits, N2, device=ctx.gpu)
+            del bits
+        h = broadcast_index(h0, N2, qr.QR_LAYOUT_BIRANK16, ctx.dist, ctx.dev)
+    else:
+        bits = torch.empty((N2 + 63) // 64, dtype=torch.uint64, device=ctx.dev)
+        gen.bits_dev(SEED[2] if p == 0.5 else 22, N2, p, bits)
+        h = qr.qr_birank_build(bits, N2, device=ctx.gpu)
+        del bits
     m = M2                                         # per GPU (weak scaling)
     i0 = ctx.rank * m
     q = torch.empty(m, dtype=torch.uint64, device=ctx.dev)
@@ -488,6 +500,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--rows", default="all", choices=["all", "headline"])
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--replicate", default="build", choices=["build", "broadcast"],
+                    help="multi-GPU: every rank builds from the seeded text, or rank 0 builds and broadcasts")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="process-group backend (gloo only to smoke-test the multi-rank path on one GPU)")
     args = ap.parse_args()

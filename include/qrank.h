@@ -166,7 +166,8 @@ qr_status qr_gather_ceiling(const qr_index* h, const uint64_t* q, uint64_t* out,
 /* sigma (2 or 4), n, and the layout's device bytes (lines + superblock array). */
 qr_status qr_info(const qr_index* h, uint64_t* n, int* sigma, uint64_t* line_bytes, uint64_t* super_bytes);
 
-/* Copy the layout to host buffers of qr_info's sizes (either may be NULL). Synchronous. */
+/* Copy the layout to buffers of qr_info's sizes (host, or device — e.g. to broadcast a built
+ * structure to other GPUs; either may be NULL).  Synchronous. */
 qr_status qr_export_layout(const qr_index* h, void* host_lines, void* host_super);
 
 /* Re-create a handle from a layout saved with qr_export_layout (checkpoint / resume without

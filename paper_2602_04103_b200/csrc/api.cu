@@ -574,10 +574,10 @@ QR_EXPORT qr_status qr_export_layout(const qr_index* h, void* host_lines, void* 
   if (!h) return fail(QR_EINVAL, "qr_export_layout: null handle");
   DeviceGuard dg(h->device);
   cudaError_t e;
-  if (host_lines && (e = cudaMemcpy(host_lines, h->lines, h->n_lines * 64, cudaMemcpyDeviceToHost)))
+  if (host_lines && (e = cudaMemcpy(host_lines, h->lines, h->n_lines * 64, cudaMemcpyDefault)))
     return cuda_fail(e, "qr_export_layout lines");
   if (host_super && super_bytes_of(h) &&
-      (e = cudaMemcpy(host_super, h->super, super_bytes_of(h), cudaMemcpyDeviceToHost)))
+      (e = cudaMemcpy(host_super, h->super, super_bytes_of(h), cudaMemcpyDefault)))
     return cuda_fail(e, "qr_export_layout super");
   return QR_OK;
 }

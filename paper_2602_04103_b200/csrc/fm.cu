@@ -118,9 +118,9 @@ static qr_status build_sa(const uint64_t* d_text, uint64_t n, int sms, cudaStrea
   {
     cub::DoubleBuffer<uint64_t> K(ka, kb);
     cub::DoubleBuffer<uint32_t> V(va, vb);
-    if ((e = cub::DeviceRadixSort::SortPairs(nullptr, need, K, V, (int)N, 0, 64, st))) return bail(e, "sort size");
+    if ((e = cub::DeviceRadixSort::SortPairs(nullptr, need, K, V, (int64_t)N, 0, 64, st))) return bail(e, "sort size");
     size_t need2 = 0;
-    if ((e = cub::DeviceScan::InclusiveScan(nullptr, need2, head, head, MaxU32(), (int)N, st))) return bail(e, "scan size");
+    if ((e = cub::DeviceScan::InclusiveScan(nullptr, need2, head, head, MaxU32(), (int64_t)N, st))) return bail(e, "scan size");
     tmp_bytes = need > need2 ? need : need2;
   }
   if ((e = cudaMallocAsync(&tmp, tmp_bytes, st))) return bail(e, "sa tmp");
@@ -130,20 +130,20 @@ static qr_status build_sa(const uint64_t* d_text, uint64_t n, int sms, cudaStrea
   cub::DoubleBuffer<uint64_t> K(ka, kb);
   cub::DoubleBuffer<uint32_t> V(va, vb);
   size_t tb = tmp_bytes;
-  if ((e = cub::DeviceRadixSort::SortPairs(tmp, tb, K, V, (int)N, 0, 63, st))) return bail(e, "sort");
+  if ((e = cub::DeviceRadixSort::SortPairs(tmp, tb, K, V, (int64_t)N, 0, 63, st))) return bail(e, "sort");
   uint64_t h = 21;
   for (int round = 0; round < 64; ++round) {
     cudaMemsetAsync(groups, 0, 8, st);
     k_sa_heads<<<g, 256, 0, st>>>(K.Current(), N, head, groups);
     tb = tmp_bytes;
-    if ((e = cub::DeviceScan::InclusiveScan(tmp, tb, head, head, MaxU32(), (int)N, st))) return bail(e, "scan");
+    if ((e = cub::DeviceScan::InclusiveScan(tmp, tb, head, head, MaxU32(), (int64_t)N, st))) return bail(e, "scan");
     k_sa_scatter_rank<<<g, 256, 0, st>>>(V.Current(), head, N, rank);
     cudaMemcpyAsync(h_groups, groups, 8, cudaMemcpyDeviceToHost, st);
     if ((e = cudaStreamSynchronize(st))) return bail(e, "sa round sync");
     if (*h_groups == N) break;                      // every suffix has a distinct rank
     k_sa_keys<<<g, 256, 0, st>>>(rank, N, h, b, K.Current(), V.Current());
     tb = tmp_bytes;
-    if ((e = cub::DeviceRadixSort::SortPairs(tmp, tb, K, V, (int)N, 0, 2 * b, st))) return bail(e, "sort");
+    if ((e = cub::DeviceRadixSort::SortPairs(tmp, tb, K, V, (int64_t)N, 0, 2 * b, st))) return bail(e, "sort");
     h *= 2;
   }
   if ((e = cudaMemcpyAsync(d_sa, V.Current(), N * 4, cudaMemcpyDeviceToDevice, st))) return bail(e, "sa copy");

@@ -54,3 +54,31 @@ def replicate(handle, device: int, stream=None):
     from . import qr_clone_to_device
 
     return qr_clone_to_device(handle, device, stream)
+
+
+def broadcast_index(h, n: int, layout: int, dist, device, src: int = 0):
+    """Replicate a rank structure over the process group: rank `src` exports its layout into
+    device buffers, one broadcast per buffer over NCCL (NVLink / NVSwitch on a B200 box), every
+    other rank imports it (`h` is ignored there and may be None).  Returns the local handle."""
+    import torch
+
+    from . import _check, _ptr, lib, qr_import_layout
+
+    rank = dist.get_rank()
+    if rank == src:
+        sizes = torch.tensor([h.line_bytes, h.super_bytes], dtype=torch.int64, device=device)
+    else:
+        sizes = torch.zeros(2, dtype=torch.int64, device=device)
+    dist.broadcast(sizes, src)
+    lb, sb = (int(x) for x in sizes.cpu())
+    lines = torch.empty(lb, dtype=torch.uint8, device=device)
+    sup = torch.empty(max(sb, 1), dtype=torch.uint8, device=device)
+    if rank == src:
+        _check(lib().qr_export_layout(h.ptr, _ptr(lines), _ptr(sup) if sb else None), "qr_export_layout")
+    dist.broadcast(lines, src)
+    if sb:
+        dist.broadcast(sup, src)
+    torch.cuda.synchronize(device)
+    if rank == src:
+        return h
+    return qr_import_layout(lines, sup if sb else None, n, layout, device=device.index if hasattr(device, "index") else 0)

@@ -141,3 +141,12 @@ def test_config5_quadfm_full(cuda):
     s = (_splitmix_np(5, 11, np.arange(m)) >= np.uint64(0x5555555555555556)).astype(np.int8)
     assert counts[s == 0].min() >= 1
     assert (s == 0).mean() == pytest.approx(1 / 3, abs=0.01)
+
+
+def test_fm_beyond_2_31_rows(cuda):
+    """N = n+1 > 2^31 exercises the 64-bit item counts of the GPU suffix sort and the u32
+    interval arithmetic near its top (reading R11: counts are u32, n+1 < 2^32)."""
+    torch = _torch()
+    n = (1 << 31) + 7
+    counts = _fm_full(cuda, n, 0, 10**6, 40, 9, 24)
+    assert counts[0::2].min() >= 1
