@@ -1,4 +1,6 @@
-"""One launch of each hot kernel at the bench's configs, for ncu (--set full) captures."""
+"""One launch of each hot kernel at the bench's configs and default launch configuration, for
+ncu --set full captures (kernel order: bi_rank2, bi_gather2 x3, qd_rank2, qd_all4_2, b64_rank,
+q64_rank, fm_count (c4, lean), fm_count (c5, de-duplicating), fm_count both strands, fm_approx1)."""
 import os
 import sys
 
@@ -16,29 +18,37 @@ n = 1 << 34
 bits = torch.empty((n + 63) // 64, dtype=torch.uint64, device=dev)
 gen.bits_dev(2, n, 0.5, bits)
 h = qr.qr_birank_build(bits, n)
-del bits
 q = torch.empty(M, dtype=torch.uint64, device=dev)
 gen.queries_dev(2, n, M, q)
 out = torch.empty_like(q)
 qr.qr_rank(h, q, None, out, M, st)
-qr.qr_gather_ceiling(h, q, out, 0, M, st)
-qr.qr_gather_ceiling(h, q, out, 1, M, st)
+for mode in (0, 1, 2):
+    qr.qr_gather_ceiling(h, q, out, mode, M, st)
 torch.cuda.synchronize()
 h.free()
-n = 1 << 32
-t = torch.empty((n + 31) // 32, dtype=torch.uint64, device=dev)
-gen.dna_dev(3, n, 0, t)
-h = qr.qr_quadrank_build(t, n)
-del t
+hb = qr.qr_build(bits, n, qr.QR_LAYOUT_BIRANK64X2)
+del bits
+n4 = 1 << 32
+t = torch.empty((n4 + 31) // 32, dtype=torch.uint64, device=dev)
+gen.dna_dev(3, n4, 0, t)
+h = qr.qr_quadrank_build(t, n4)
 c = torch.empty(M, dtype=torch.uint8, device=dev)
-gen.queries_dev(3, n, M, q, c)
+gen.queries_dev(3, n4, M, q, c)
 qr.qr_rank(h, q, c, out, M, st)
-del out
 o4 = torch.empty((M, 4), dtype=torch.uint64, device=dev)
 qr.qr_rank_all4(h, q, o4, M, st)
 torch.cuda.synchronize()
-del o4, q, c
 h.free()
+del o4
+hq = qr.qr_build(t, n4, qr.QR_LAYOUT_QUADRANK64)
+del t
+qb = torch.empty(M, dtype=torch.uint64, device=dev)
+gen.queries_dev(2, n, M, qb)
+qr.qr_rank(hb, qb, None, out, M, st)
+qr.qr_rank(hq, q, c, out, M, st)
+torch.cuda.synchronize()
+hb.free(); hq.free()
+del q, c, qb, out
 n = 1 << 26
 t = torch.empty((n + 31) // 32 + 1, dtype=torch.uint64, device=dev)
 gen.dna_dev(4, n, 0, t)
@@ -49,7 +59,6 @@ gen.patterns_dev(4, 0, m, 32, t, n, pats)
 o = torch.empty(m, dtype=torch.int32, device=dev)
 qr.qr_fm_count(fm, pats, None, 32, o, m, st)
 torch.cuda.synchronize()
-print("profile driver done")
 fm.free()
 n = 1 << 30
 t = torch.empty((n + 31) // 32 + 1, dtype=torch.uint64, device=dev)
@@ -60,5 +69,22 @@ pats = torch.empty(m * 100, dtype=torch.uint8, device=dev)
 gen.patterns_dev(5, 1, m, 100, t, n, pats)
 o = torch.empty(m, dtype=torch.int32, device=dev)
 qr.qr_fm_count(fm, pats, None, 100, o, m, st)
+mr = 10**7
+reads = torch.empty(mr * 150, dtype=torch.uint8, device=dev)
+gen.patterns_dev(55, 2, mr, 150, t, n, reads)
+of = torch.empty(mr, dtype=torch.int32, device=dev)
+orc = torch.empty(mr, dtype=torch.int32, device=dev)
+qr.qr_fm_count_both(fm, reads, None, 150, of, orc, mr, st)
 torch.cuda.synchronize()
-print("profile driver done (c5)")
+fm.free()
+n = 1 << 26
+t = torch.empty((n + 31) // 32 + 1, dtype=torch.uint64, device=dev)
+gen.dna_dev(4, n, 0, t)
+fm = qr.qr_fm_build(t, n)
+m = 10**6
+pats = torch.empty(m * 32, dtype=torch.uint8, device=dev)
+gen.patterns_dev(4, 0, m, 32, t, n, pats)
+o = torch.empty(m, dtype=torch.int32, device=dev)
+qr.qr_fm_count_approx(fm, pats, None, 32, 1, o, m, st)
+torch.cuda.synchronize()
+print("profile driver done")
