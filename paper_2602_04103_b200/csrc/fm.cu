@@ -277,16 +277,14 @@ struct PatWindow {
 // (sector 0 left of the anchor, sector 1 right of it) and, only when right, the one u64 word of
 // sector 0 that holds its delta; no de-duplication of shared lines (the L1 merges them), so no
 // register copies or half selects.  Fewer instructions, a few more L1 wavefronts.
-__device__ __forceinline__ uint32_t fm_rank_lean(const FmParams& F, uint32_t x, uint32_t c, uint64_t cl, uint64_t ch) {
-  const uint32_t j = (x >> 5) / 7u;                  // x <= N: j <= last_line, no clamp needed
-  const uint32_t p = 32u + x - j * (uint32_t)QD_B;
+__device__ __forceinline__ uint32_t fm_rank_lean(const FmParams& F, uint32_t j, uint32_t p, uint32_t c, uint64_t cl,
+                                                 uint64_t ch, uint32_t s) {
   const bool right = p >= 128;
   const uint4* L = F.lines + 4 * (uint64_t)j;
   uint64_t w0, w1, w2, w3;
   ld_sector(L + 2 * (right ? 1 : 0), w0, w1, w2, w3);
   uint64_t dr = 0;
   if (right) dr = __ldg(reinterpret_cast<const unsigned long long*>(L) + (c >> 1));
-  const uint32_t s = __ldg(F.super + 4 * (j >> QD_SB_LOG) + c);
   const int xx = (int)(p & 127u);
   const uint64_t inv = right ? 0ull : ~0ull;
   const uint32_t cnt = __popcll((w0 ^ cl) & (w1 ^ ch) & (prefix_mask(xx, 0) ^ inv)) +
@@ -296,13 +294,25 @@ __device__ __forceinline__ uint32_t fm_rank_lean(const FmParams& F, uint32_t x, 
   return right ? base + cnt : base - cnt;
 }
 
-__device__ __forceinline__ void fm_step_lean(const FmParams& F, uint32_t c, uint32_t& lo, uint32_t& hi, uint32_t& lines) {
+// C[c] from four registers (3 selects) instead of an L1 load: the lean step is L1-bound on an
+// L2-resident BWT (ncu: L1 91% busy), so ALU is the cheaper resource.
+__device__ __forceinline__ uint32_t pick4(uint4 v, uint32_t c) {
+  return (c & 2u) ? ((c & 1u) ? v.w : v.z) : ((c & 1u) ? v.y : v.x);
+}
+
+__device__ __forceinline__ void fm_step_lean(const FmParams& F, uint4 C4, uint32_t c, uint32_t& lo, uint32_t& hi,
+                                             uint32_t& lines) {
   const uint64_t cl = 0ull - (uint64_t)(c & 1u), ch = 0ull - (uint64_t)(c >> 1);
-  const uint32_t Cc = __ldg(F.Ct + c);
-  uint32_t rl = fm_rank_lean(F, lo, c, cl, ch);
-  uint32_t rh = fm_rank_lean(F, hi, c, cl, ch);
-  lines = ((lo >> 5) / 7u == (hi >> 5) / 7u) ? 1u : 2u;
+  const uint32_t jl = (lo >> 5) / 7u, jh = (hi >> 5) / 7u;   // lo, hi <= N: j <= last_line
+  const uint32_t pl = 32u + lo - jl * (uint32_t)QD_B, ph = 32u + hi - jh * (uint32_t)QD_B;
+  // one superblock-word load when both ranks fall in the same superblock (nearly always)
+  const uint32_t sl = __ldg(F.super + 4 * (jl >> QD_SB_LOG) + c);
+  const uint32_t sh = (jl >> QD_SB_LOG) == (jh >> QD_SB_LOG) ? sl : __ldg(F.super + 4 * (jh >> QD_SB_LOG) + c);
+  uint32_t rl = fm_rank_lean(F, jl, pl, c, cl, ch, sl);
+  uint32_t rh = fm_rank_lean(F, jh, ph, c, cl, ch, sh);
+  lines = jl == jh ? 1u : 2u;
   if (c == 0) { rl -= (lo > (uint32_t)F.spos); rh -= (hi > (uint32_t)F.spos); }
+  const uint32_t Cc = pick4(C4, c);
   lo = Cc + rl;
   hi = Cc + rh;
 }
@@ -347,6 +357,7 @@ __global__ void __launch_bounds__(256, 4) k_fm_count(FmParams F, const uint8_t* 
                                                      unsigned long long* __restrict__ work) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   const uint64_t ntask = m * STRANDS;
+  const uint4 C4 = __ldg(reinterpret_cast<const uint4*>(F.Ct));
   uint64_t ti = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
   uint32_t lo = 0, hi = 0, len = 0, rc = 0;
   int64_t k = -1;
@@ -373,7 +384,7 @@ __global__ void __launch_bounds__(256, 4) k_fm_count(FmParams F, const uint8_t* 
     if (k >= 0 && lo < hi) {                             // one backward step (LF mapping)
       const uint32_t c = rc ? 3u - P.at((int64_t)len - 1 - k) : P.at(k);
       uint32_t nl;
-      if (LEAN) fm_step_lean(F, c, lo, hi, nl);
+      if (LEAN) fm_step_lean(F, C4, c, lo, hi, nl);
       else      fm_step(F, c, lo, hi, nl);
       --k;
       if (WORK) { n_steps += 1; n_lines += nl; }

@@ -21,11 +21,11 @@ for name, n, kind, m, L, seed in (("c4", 1 << 26, 0, 10**7, 32, 4), ("c5", 1 << 
     out = torch.empty(m, dtype=torch.int32, device=dev)
     ref = None
     for pair in (1, 2):                     # here: fm_step flavour (1 = de-duplicating, 2 = lean)
-        for bps in (4, 6, 8):                # here: min resident CTAs per SM (register cap)
-            qr.qr_set_tuning("fm_step", pair); qr.qr_set_tuning("fm_minblocks", bps)
+        for bps in (64,):
+            qr.qr_set_tuning("fm_step", pair); qr.qr_set_tuning("fm_blocks_per_sm", bps)
             ms = t(lambda: qr.qr_fm_count(fm, pats, None, L, out, m, st), reps=3 if name == "c5" else 10)
             h = int(out.view(torch.int32).to(torch.int64).sum())
             ref = h if ref is None else ref
             print(json.dumps(dict(cfg=name, pair=pair, bps=bps, ms=ms, gpat_s=m / ms / 1e6, checksum_ok=(h == ref))), flush=True)
     fm.free(); del txt, pats, out; torch.cuda.empty_cache()
-qr.qr_set_tuning("fm_step", 0); qr.qr_set_tuning("fm_minblocks", 4)
+qr.qr_set_tuning("fm_step", 0); qr.qr_set_tuning("fm_blocks_per_sm", 64)
