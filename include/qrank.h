@@ -124,7 +124,9 @@ qr_status qr_fm_build(const uint64_t* text2b, uint64_t n, const uint32_t* sa_or_
  * byte per symbol (0..3, taken mod 4).  lengths: u32[m], pattern k starts at the exclusive
  * prefix sum of lengths (computed on the device); or lengths = NULL and every pattern has
  * fixed_len symbols.  An empty pattern counts n + 1.  Patterns are counted as given (no
- * reverse complement: that is a second call). */
+ * reverse complement: that is a second call).  The kernel reads pattern bytes in
+ * aligned 8-byte words, so it may read up to 7 bytes past the last pattern inside the same
+ * 8-byte-aligned word (never across an allocation: such a word always holds a valid byte). */
 qr_status qr_fm_count(const qr_fm* fm, const uint8_t* patterns, const uint32_t* lengths, uint32_t fixed_len,
                       uint32_t* out, uint64_t m, void* stream);
 
@@ -198,7 +200,7 @@ void qr_fm_free(qr_fm* fm);
 const char* qr_last_error(void);
 
 /* Process-wide launch-configuration knobs for measurement sweeps (results never depend on
- * them): "rank_k" (1, 2, 4 or 8 independent queries per thread per iteration),
+ * them; not synchronised — set them before issuing work from other threads): "rank_k" (1, 2, 4 or 8 independent queries per thread per iteration),
  * "rank_blocks_per_sm" and "fm_blocks_per_sm" (256-thread CTAs per SM of the grid-stride
  * rank / FM kernels, 1..64), "stage_chunk" (queries per chunk of the staged host path),
  * "stage_slots" (2..4 device buffers / internal streams of the staged host path),

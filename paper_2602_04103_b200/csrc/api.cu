@@ -218,6 +218,14 @@ static qr_status run_staged(int device, cudaStream_t user, uint64_t m, const std
   }
   cudaEventRecord(S->ev_start, user);                   // respect work already queued on `user`
   for (int i = 0; i < nslot; ++i) cudaStreamWaitEvent(S->s[i], S->ev_start, 0);
+  // Whatever happens below, `user` is made to wait for everything already enqueued on the
+  // internal streams, so the caller can never free buffers that a copy still reads or writes.
+  auto join = [&]() {
+    for (int i = 0; i < nslot; ++i) {
+      cudaEventRecord(S->ev_done[i], S->s[i]);
+      cudaStreamWaitEvent(user, S->ev_done[i], 0);
+    }
+  };
   uint64_t k = 0;
   for (uint64_t lo = 0; lo < m; lo += chunk, ++k) {
     const uint64_t cnt = (m - lo < chunk) ? m - lo : chunk;
@@ -231,21 +239,22 @@ static qr_status run_staged(int device, cudaStream_t user, uint64_t m, const std
       off += (((arrays[a].item_bytes + 15) & ~size_t(15)) * (size_t)cnt + 255) & ~size_t(255);
       if (arrays[a].host_in &&
           (e = cudaMemcpyAsync(dptr[a], static_cast<const char*>(arrays[a].host_in) + lo * arrays[a].item_bytes,
-                               cnt * arrays[a].item_bytes, cudaMemcpyHostToDevice, st)))
+                               cnt * arrays[a].item_bytes, cudaMemcpyHostToDevice, st))) {
+        join();
         return cuda_fail(e, "staged H2D");
+      }
     }
     qr_status rs = launch(dptr, cnt, st);
-    if (rs != QR_OK) return rs;
+    if (rs != QR_OK) { join(); return rs; }
     for (size_t a = 0; a < arrays.size(); ++a)
       if (arrays[a].host_out &&
           (e = cudaMemcpyAsync(static_cast<char*>(arrays[a].host_out) + lo * arrays[a].item_bytes, dptr[a],
-                               cnt * arrays[a].item_bytes, cudaMemcpyDeviceToHost, st)))
+                               cnt * arrays[a].item_bytes, cudaMemcpyDeviceToHost, st))) {
+        join();
         return cuda_fail(e, "staged D2H");
+      }
   }
-  for (int i = 0; i < nslot; ++i) {
-    cudaEventRecord(S->ev_done[i], S->s[i]);
-    cudaStreamWaitEvent(user, S->ev_done[i], 0);
-  }
+  join();
   if ((e = cudaGetLastError())) return cuda_fail(e, "staged pipeline");
   return QR_OK;
 }
