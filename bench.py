@@ -303,6 +303,15 @@ def bench_fm(ctx, n, kind, m_total, length, seed, steps, warmup, rank_queries=0)
     return res
 
 
+def bench_reads_safe(ctx, n, m_total, length, seed, steps, warmup):
+    try:
+        ctx.torch.cuda.empty_cache()
+        return bench_reads(ctx, n, m_total, length, seed, steps, warmup)
+    except Exception as e:                          # e.g. out of memory on a smaller GPU
+        ctx.torch.cuda.empty_cache()
+        return {"skipped": str(e)[:200]}
+
+
 def bench_reads(ctx, n, m_total, length, seed, steps, warmup):
     """The paper's FM workload shape: 150-bp reads with 1% substitutions from
     either strand, each counted in both directions in one launch (qr_fm_count_both), over the
@@ -313,7 +322,9 @@ def bench_reads(ctx, n, m_total, length, seed, steps, warmup):
     torch = ctx.torch
     text = torch.empty((n + 31) // 32 + 1, dtype=torch.uint64, device=ctx.dev)
     gen.dna_dev(seed, n, 1, text)
+    t0 = time.perf_counter()
     fm = qr.qr_fm_build(text, n, device=ctx.gpu)
+    build_s = time.perf_counter() - t0
     i0, m = shard(m_total, ctx.world, ctx.rank)
     pats = torch.empty(m * length, dtype=torch.uint8, device=ctx.dev)
     gen.patterns_dev(seed, 2, m, length, text, n, pats, i0=i0)
@@ -325,7 +336,8 @@ def bench_reads(ctx, n, m_total, length, seed, steps, warmup):
     del text, pats, of, orc
     torch.cuda.empty_cache()
     return {"ms": ms, "reads_per_s": m_total / ms * 1e3, "searches_per_s": 2 * m_total / ms * 1e3,
-            "read_len": length, "reads": m_total, "frac_reads_matching": hit / max(m, 1)}
+            "read_len": length, "reads": m_total, "frac_reads_matching": hit / max(m, 1), "text_len": n,
+            "fm_build_s": round(build_s, 2)}
 
 
 def bench_approx(ctx, n, m_total, length, seed, steps, warmup):
@@ -523,6 +535,9 @@ def main():
         rows["c4_quadfm"] = bench_fm(ctx, N4, 0, M4, L4, SEED[4], K, W)
         rows["c5_quadfm"] = bench_fm(ctx, N5, 1, M5, L5, SEED[5], K, W, rank_queries=10**9)
         rows["c5_reads_150bp_both_strands"] = bench_reads(ctx, N5, 10**7, 150, 55, K, W)
+        # the paper's FM workload at its own scale: a 3.1 Gbp text (block-repeat
+        # stand-in for CHM13v2; n+1 < 2^32), 150-bp reads at 1% substitutions, both strands
+        rows["genome_scale_reads_3.1Gbp"] = bench_reads_safe(ctx, 3_100_000_000, 10**7, 150, 56, K, W)
         rows["c4_quadfm_approx1"] = bench_approx(ctx, N4, 10**6, L4, SEED[4], K, W)
         rows["layout_variants"] = bench_variants(ctx, K, W)
         rows["latency_mode"] = bench_latency(ctx, K, W)
