@@ -368,3 +368,29 @@ def test_index64_path(cuda, pair):
     ora = oracle.DnaOracle(t, n)
     assert np.array_equal(to_host(oq), ora.rank(q, c))
     assert np.array_equal(to_host(o4), ora.rank_all4(q))
+
+
+def test_concurrent_streams_share_a_handle(cuda):
+    """Handles are immutable: queries on several streams at once (and from the staged path on
+    internal streams) give the same answers as one stream."""
+    torch = _torch()
+    n = 9 * S + 123
+    w = gen.bits(51, n)
+    h = qr.qr_birank_build(w, n)
+    ref = None
+    streams = [torch.cuda.Stream() for _ in range(4)]
+    q = gen.queries(52, n, 400000)
+    dq = to_dev(q, cuda)
+    outs = [torch.empty_like(dq) for _ in streams]
+    torch.cuda.synchronize()
+    for s, o in zip(streams, outs):
+        with torch.cuda.stream(s):
+            qr.qr_rank(h, dq, None, o, stream=s)
+    host_out = np.zeros(q.size, np.uint64)
+    qr.qr_rank(h, q, None, host_out)
+    torch.cuda.synchronize()
+    qr.qr_sync()
+    ref = oracle.BitsOracle(w, n).rank(q)
+    for o in outs:
+        assert np.array_equal(to_host(o), ref)
+    assert np.array_equal(host_out, ref)
