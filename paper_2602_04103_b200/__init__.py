@@ -104,6 +104,28 @@ def _ptr(a):
     raise TypeError(f"cannot take a pointer of {type(a)}")
 
 
+def _nbytes_item(a):
+    """(element size, element count) of a torch tensor / numpy array, or None for raw pointers."""
+    if a is None or isinstance(a, int):
+        return None
+    if hasattr(a, "element_size"):
+        return a.element_size(), a.numel()
+    if hasattr(a, "itemsize"):
+        return a.itemsize, a.size
+    return None
+
+
+def _need(a, itemsize: int, count: int, name: str):
+    """Reject arrays whose element size or length cannot hold `count` items (marshalling check:
+    a wrong dtype would otherwise be read or written out of bounds by the kernels)."""
+    info = _nbytes_item(a)
+    if info is None:
+        return
+    es, n = info
+    if es * n < itemsize * count or (es != itemsize and itemsize in (1, 4, 8) and es not in (itemsize,)):
+        raise QrError(QR_EINVAL, name, f"needs {count} items of {itemsize} B, got {n} of {es} B")
+
+
 def _stream(s):
     if s is None:
         try:
@@ -189,6 +211,10 @@ def qr_quadrank_build(text2b, n: int, device: int = 0, stream=None) -> Index:
 
 def qr_rank(h: Index, q, c, out, m: int | None = None, stream=None):
     m = (q.numel() if hasattr(q, "numel") else q.size) if m is None else m
+    _need(q, 8, m, "qr_rank q")
+    _need(out, 8, m, "qr_rank out")
+    if c is not None:
+        _need(c, 1, m, "qr_rank c")
     _check(lib().qr_rank(h.ptr, _ptr(q), _ptr(c), _ptr(out), m, _stream(stream)), "qr_rank")
     return out
 
@@ -201,6 +227,8 @@ def qr_rank_chain(h: Index, q, c, out, chain_len: int, m: int | None = None, str
 
 def qr_rank_all4(h: Index, q, out4, m: int | None = None, stream=None):
     m = (q.numel() if hasattr(q, "numel") else q.size) if m is None else m
+    _need(q, 8, m, "qr_rank_all4 q")
+    _need(out4, 8, 4 * m, "qr_rank_all4 out4")
     _check(lib().qr_rank_all4(h.ptr, _ptr(q), _ptr(out4), m, _stream(stream)), "qr_rank_all4")
     return out4
 
@@ -212,6 +240,11 @@ def qr_fm_build(text2b, n: int, sa=None, device: int = 0, stream=None) -> Fm:
 
 
 def qr_fm_count(fm: Fm, patterns, lengths, fixed_len: int, out, m: int, stream=None):
+    _need(out, 4, m, "qr_fm_count out")
+    if lengths is not None:
+        _need(lengths, 4, m, "qr_fm_count lengths")
+    else:
+        _need(patterns, 1, m * fixed_len, "qr_fm_count patterns")
     _check(lib().qr_fm_count(fm.ptr, _ptr(patterns), _ptr(lengths), fixed_len, _ptr(out), m, _stream(stream)),
            "qr_fm_count")
     return out

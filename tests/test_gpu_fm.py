@@ -297,3 +297,24 @@ def test_fm_count_approx_one_mismatch(cuda, n, kind):
     assert np.array_equal(h, oracle.scan_count_hd1(sym, fx, np.arange(m, dtype=np.uint64) * L, np.full(m, L, np.uint32)))
     with pytest.raises(qr.QrError):
         qr.qr_fm_count_approx(fm, fx, None, L, 2, h, m)
+
+
+def test_cli_fm_count(cuda, tmp_path):
+    """End-to-end CLI on real-format files: FASTA genome, FASTQ reads, both strands."""
+    from paper_2602_04103_b200 import cli, io
+
+    n = 20000
+    sym = gen.unpack_dna(gen.dna(91, n), n)
+    fa = tmp_path / "g.fa"
+    fa.write_text(">g\n" + "\n".join(io.decode(sym[i:i + 70]) for i in range(0, n, 70)) + "\n")
+    rng = np.random.default_rng(3)
+    reads = [sym[a:a + 30].copy() for a in rng.integers(0, n - 30, 20)] + [rng.integers(0, 4, 25).astype(np.uint8)]
+    fq = tmp_path / "r.fq"
+    fq.write_text("".join(f"@r{i}\n{io.decode(r)}\n+\n{'I' * len(r)}\n" for i, r in enumerate(reads)))
+    out = tmp_path / "c.tsv"
+    assert cli.main(["fm-count", "--fasta", str(fa), "--fastq", str(fq), "--both-strands", "--out", str(out)]) == 0
+    rows = [tuple(int(x) for x in line.split("\t")) for line in out.read_text().splitlines()]
+    cat, off, lens = oracle.pack_patterns(reads)
+    rcat, roff, rlens = oracle.pack_patterns([revcomp(r) for r in reads])
+    assert [r[1] for r in rows] == list(oracle.scan_count(sym, cat, off, lens))
+    assert [r[2] for r in rows] == list(oracle.scan_count(sym, rcat, roff, rlens))

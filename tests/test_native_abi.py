@@ -68,3 +68,16 @@ def test_argument_validation_without_gpu():
     L.qr_fm_free(None)
     with pytest.raises(qr.QrError):
         qr.qr_set_tuning("rank_blocks_per_sm", 0)
+
+
+def test_binding_rejects_wrong_dtypes():
+    """The binding refuses arrays too small for the call (e.g. an int32 query array)."""
+    import numpy as np
+
+    h = object.__new__(qr.Index)          # never reaches the library: the size check fires first
+    with pytest.raises(qr.QrError):
+        qr.qr_rank(h, np.zeros(10, np.int32), None, np.zeros(10, np.uint64))
+    with pytest.raises(qr.QrError):
+        qr.qr_rank(h, np.zeros(10, np.uint64), None, np.zeros(5, np.uint64))
+    with pytest.raises(qr.QrError):
+        qr.qr_rank_all4(h, np.zeros(10, np.uint64), np.zeros(10, np.uint64))
