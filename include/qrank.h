@@ -118,6 +118,16 @@ qr_status qr_rank_chain(const qr_index* h, const uint64_t* q, const uint8_t* c, 
 qr_status qr_fm_build(const uint64_t* text2b, uint64_t n, const uint32_t* sa_or_null, int device, void* stream,
                       qr_fm** out);
 
+/* As qr_fm_build with a k-mer seed table of width kmer_k (0..12; 0 = no table, every search
+ * starts from [0, n+1); qr_fm_build uses the paper's 8).  The table holds 4^kmer_k intervals
+ * (8 B each: 512 KiB at 8, 8 MiB at 10, 128 MiB at 12).  Counts never depend on kmer_k
+ * (S:366); wider tables skip more backward steps.  QR_EINVAL outside 0..12. */
+qr_status qr_fm_build_ex(const uint64_t* text2b, uint64_t n, const uint32_t* sa_or_null, int kmer_k, int device,
+                         void* stream, qr_fm** out);
+
+/* The k-mer table width of an FM handle. */
+qr_status qr_fm_kmer_width(const qr_fm* fm, int* kmer_k);
+
 /* out[k] = number of (overlapping) occurrences of pattern k in T, as u32 (backward search:
  * lo = C[c] + Occ(c, lo), hi = C[c] + Occ(c, hi), Occ(c,x) = rank(x,c) - [c = A and x > spos];
  * seeded by the 8-mer table when the pattern has >= 8 symbols).  patterns: concatenated, one
@@ -183,7 +193,8 @@ qr_status qr_import_layout(const void* lines, const void* super, uint64_t n, int
  * (owned by fm; valid until qr_fm_free). */
 qr_status qr_fm_info(const qr_fm* fm, uint64_t* n, uint64_t* spos, uint64_t C[5], const qr_index** bwt_rank);
 
-/* Copy the 8-mer interval table (65536 pairs of u32 [lo, hi)) to a host buffer. Synchronous. */
+/* Copy the k-mer interval table (4^kmer_k pairs of u32 [lo, hi); 65536 for the default
+ * width 8) to a host buffer. Synchronous. */
 qr_status qr_fm_export_kmer(const qr_fm* fm, uint32_t* host_pairs);
 
 /* Replicate a handle onto another device (peer copy over NVLink when available). */

@@ -28,7 +28,7 @@ EXPORTS = (
     "qr_birank_build", "qr_quadrank_build", "qr_rank", "qr_rank_all4", "qr_fm_build", "qr_fm_count", "qr_fm_count_both", "qr_fm_count_approx",
     "qr_fm_count_work", "qr_gather_ceiling", "qr_info", "qr_export_layout", "qr_fm_info", "qr_fm_export_kmer",
     "qr_clone_to_device", "qr_fm_clone_to_device", "qr_sync", "qr_free", "qr_fm_free", "qr_last_error",
-    "qr_version", "qr_set_tuning", "qr_build", "qr_layout", "qr_rank_chain", "qr_import_layout",
+    "qr_version", "qr_set_tuning", "qr_build", "qr_layout", "qr_rank_chain", "qr_import_layout", "qr_fm_build_ex", "qr_fm_kmer_width",
 )
 
 
@@ -77,6 +77,8 @@ def lib():
             "qr_layout": ([V, C.POINTER(C.c_int)], I32),
             "qr_rank_chain": ([V, V, V, V, U64, U64, V], I32),
             "qr_import_layout": ([V, V, U64, I32, I32, V, PP], I32),
+            "qr_fm_build_ex": ([V, U64, V, I32, I32, V, PP], I32),
+            "qr_fm_kmer_width": ([V, C.POINTER(C.c_int)], I32),
         }
         for name, (args, res) in sig.items():
             f = getattr(L, name)
@@ -177,6 +179,9 @@ class Fm:
         _check(lib().qr_fm_info(self.ptr, C.byref(n), C.byref(sp), Cs, C.byref(bw)), "qr_fm_info")
         self.n, self.spos, self.C = n.value, sp.value, list(Cs)
         self.bwt = Index(bw.value, owned=False)
+        kk = C.c_int()
+        _check(lib().qr_fm_kmer_width(self.ptr, C.byref(kk)), "qr_fm_kmer_width")
+        self.kmer_k = kk.value
 
     def free(self):
         if self.ptr:
@@ -233,9 +238,14 @@ def qr_rank_all4(h: Index, q, out4, m: int | None = None, stream=None):
     return out4
 
 
-def qr_fm_build(text2b, n: int, sa=None, device: int = 0, stream=None) -> Fm:
+def qr_fm_build(text2b, n: int, sa=None, device: int = 0, stream=None, kmer_k: int = 8) -> Fm:
+    """qr_fm_build (kmer_k = 8, the paper's table) or qr_fm_build_ex (other widths)."""
     out = C.c_void_p()
-    _check(lib().qr_fm_build(_ptr(text2b), n, _ptr(sa), device, _stream(stream), C.byref(out)), "qr_fm_build")
+    if kmer_k == 8:
+        _check(lib().qr_fm_build(_ptr(text2b), n, _ptr(sa), device, _stream(stream), C.byref(out)), "qr_fm_build")
+    else:
+        _check(lib().qr_fm_build_ex(_ptr(text2b), n, _ptr(sa), kmer_k, device, _stream(stream), C.byref(out)),
+               "qr_fm_build_ex")
     return Fm(out.value)
 
 
@@ -309,9 +319,10 @@ def load_index(path: str, device: int = 0) -> Index:
 def qr_fm_export_kmer(fm: Fm):
     import numpy as np
 
-    t = np.empty(2 * 65536, dtype=np.uint32)
+    ne = 1 << (2 * fm.kmer_k)
+    t = np.empty(2 * ne, dtype=np.uint32)
     _check(lib().qr_fm_export_kmer(fm.ptr, _ptr(t)), "qr_fm_export_kmer")
-    return t.reshape(65536, 2)
+    return t.reshape(ne, 2)
 
 
 def qr_clone_to_device(h: Index, device: int, stream=None) -> Index:

@@ -117,7 +117,7 @@ qr_status alloc_index(int sigma, uint64_t n, int device, qr_index** out, int lay
 uint64_t super_bytes_of(const qr_index* h) { return h->n_super * (h->sigma == 2 ? 4 : 16); }
 
 qr_status fm_build_device(const uint64_t* d_text, uint64_t n, const uint32_t* d_sa_given, int device, cudaStream_t st,
-                          qr_fm** out);
+                          qr_fm** out, int kmer_k);
 __global__ void k_mask_tail_bits(uint64_t* words, uint64_t n);
 __global__ void k_mask_tail_chars(uint64_t* words, uint64_t n);
 cudaError_t launch_bi_gather(const qr_index* h, const uint64_t* q, uint64_t* out, uint64_t m, int mode, cudaStream_t st);
@@ -472,8 +472,17 @@ QR_EXPORT qr_status qr_gather_ceiling(const qr_index* h, const uint64_t* q, uint
   return e ? cuda_fail(e, "qr_gather_ceiling launch") : QR_OK;
 }
 
+QR_EXPORT qr_status qr_fm_build_ex(const uint64_t* text2b, uint64_t n, const uint32_t* sa_or_null, int kmer_k,
+                                   int device, void* stream, qr_fm** out);
+
 QR_EXPORT qr_status qr_fm_build(const uint64_t* text2b, uint64_t n, const uint32_t* sa_or_null, int device,
                                 void* stream, qr_fm** out) {
+  return qr_fm_build_ex(text2b, n, sa_or_null, 8, device, stream, out);
+}
+
+QR_EXPORT qr_status qr_fm_build_ex(const uint64_t* text2b, uint64_t n, const uint32_t* sa_or_null, int kmer_k,
+                                   int device, void* stream, qr_fm** out) {
+  if (kmer_k < 0 || kmer_k > 12) return fail(QR_EINVAL, "qr_fm_build_ex: kmer_k must be 0..12");
   if (!out || !text2b) return fail(QR_EINVAL, "qr_fm_build: null pointer");
   *out = nullptr;
   if (n == 0) return fail(QR_EINVAL, "qr_fm_build: empty text");
@@ -494,7 +503,7 @@ QR_EXPORT qr_status qr_fm_build(const uint64_t* text2b, uint64_t n, const uint32
       cudaFreeAsync(d, st); cudaFreeAsync(dsa, st); return cuda_fail(e, "copy sa");
     }
   }
-  s = fm_build_device(d, n, dsa, device, st, out);
+  s = fm_build_device(d, n, dsa, device, st, out, kmer_k);
   cudaFreeAsync(d, st);
   if (dsa) cudaFreeAsync(dsa, st);
   cudaStreamSynchronize(st);
@@ -612,6 +621,12 @@ QR_EXPORT qr_status qr_import_layout(const void* lines, const void* super, uint6
   return QR_OK;
 }
 
+QR_EXPORT qr_status qr_fm_kmer_width(const qr_fm* fm, int* kmer_k) {
+  if (!fm || !kmer_k) return fail(QR_EINVAL, "qr_fm_kmer_width: null pointer");
+  *kmer_k = fm->kmer_k;
+  return QR_OK;
+}
+
 QR_EXPORT qr_status qr_fm_info(const qr_fm* fm, uint64_t* n, uint64_t* spos, uint64_t C[5], const qr_index** bwt_rank) {
   if (!fm) return fail(QR_EINVAL, "qr_fm_info: null handle");
   if (n) *n = fm->n;
@@ -624,7 +639,7 @@ QR_EXPORT qr_status qr_fm_info(const qr_fm* fm, uint64_t* n, uint64_t* spos, uin
 QR_EXPORT qr_status qr_fm_export_kmer(const qr_fm* fm, uint32_t* host_pairs) {
   if (!fm || !host_pairs) return fail(QR_EINVAL, "qr_fm_export_kmer: null pointer");
   DeviceGuard dg(fm->bwt->device);
-  cudaError_t e = cudaMemcpy(host_pairs, fm->kmer, 65536 * sizeof(uint2), cudaMemcpyDeviceToHost);
+  cudaError_t e = cudaMemcpy(host_pairs, fm->kmer, kmer_entries(fm->kmer_k) * sizeof(uint2), cudaMemcpyDeviceToHost);
   return e ? cuda_fail(e, "qr_fm_export_kmer") : QR_OK;
 }
 
@@ -658,9 +673,9 @@ QR_EXPORT qr_status qr_fm_clone_to_device(const qr_fm* fm, int device, void* str
   qr_status s = qr_clone_to_device(fm->bwt, device, stream, &c->bwt);
   if (s != QR_OK) { delete c; return s; }
   DeviceGuard dg(device);
-  cudaError_t e = cudaMalloc((void**)&c->kmer, (65536 + 2) * sizeof(uint2));   // table + C[0..3] tail
-  if (!e) e = cudaMemcpyPeerAsync(c->kmer, device, fm->kmer, fm->bwt->device, (65536 + 2) * sizeof(uint2),
-                                  (cudaStream_t)stream);
+  const size_t kb = (kmer_entries(fm->kmer_k) + 2) * sizeof(uint2);        // table + C[0..3] tail
+  cudaError_t e = cudaMalloc((void**)&c->kmer, kb);
+  if (!e) e = cudaMemcpyPeerAsync(c->kmer, device, fm->kmer, fm->bwt->device, kb, (cudaStream_t)stream);
   if (!e) e = cudaStreamSynchronize((cudaStream_t)stream);
   if (e) { qr_fm_free(c); return cuda_fail(e, "qr_fm_clone_to_device"); }
   *out = c;

@@ -22,11 +22,12 @@ struct FmParams {
   const uint4* lines;
   const uint32_t* super;
   const uint2* kmer;
+  int K;                // k-mer table width (0: no table)
   uint64_t spos;
   uint64_t N;
   uint64_t last_line;
   uint32_t C[4];        // host copy; the kernels read C from the table tail (Ct) with one load
-  const uint32_t* Ct;   // = (const uint32_t*)(kmer + 65536): C[0..3] stored after the 8-mer table
+  const uint32_t* Ct;   // = (const uint32_t*)(kmer + 4^K): C[0..3] stored after the k-mer table
 };
 
 __device__ __forceinline__ uint32_t text_char(const uint64_t* t, uint64_t i) {
@@ -243,11 +244,11 @@ __device__ __forceinline__ void fm_step(const FmParams& F, uint32_t c, uint32_t&
 }
 
 __global__ void k_kmer_table(FmParams F, uint2* __restrict__ table) {
-  uint32_t key = blockIdx.x * blockDim.x + threadIdx.x;
-  if (key >= 65536u) return;
+  const uint32_t key = blockIdx.x * blockDim.x + threadIdx.x;
+  if (key >= (1u << (2 * F.K))) return;
   uint32_t lo = 0, hi = (uint32_t)F.N;
   uint32_t dummy;
-  for (int t = 0; t < 8 && lo < hi; ++t) fm_step(F, (key >> (2 * t)) & 3u, lo, hi, dummy);   // last char first
+  for (int t = 0; t < F.K && lo < hi; ++t) fm_step(F, (key >> (2 * t)) & 3u, lo, hi, dummy);   // last char first
   if (lo >= hi) lo = hi = 0;
   table[key] = make_uint2(lo, hi);
 }
@@ -347,6 +348,23 @@ __device__ __forceinline__ uint32_t kmer_key8_rc(const uint8_t* first8) { return
 // 2i+1 its reverse complement RC(P)[j] = 3 - P[len-1-j] ("both forward and
 // reverse-complement direction"; NEXT §8(f)1), read from the same bytes in the opposite
 // direction, so no reverse-complemented copy is ever materialised.
+// Table key of width K (<= 12) of the pattern's last K symbols: sum_{t<K} P[len-1-t] << 2t.
+// K = 8 (the paper's table) is one unaligned 8-byte read; other widths read symbol by symbol
+// through the pattern window (no read before the pattern's first byte).
+__device__ __forceinline__ uint32_t kmer_key(int K, PatWindow& P, const uint8_t* p, uint32_t len) {
+  if (K == 8) return kmer_key8(p + len - 8);
+  uint32_t key = 0;
+  for (int t = 0; t < K; ++t) key |= P.at((int64_t)len - 1 - t) << (2 * t);
+  return key;
+}
+// Reverse-complement key: sum_{t<K} (3 - P[t]) << 2t.
+__device__ __forceinline__ uint32_t kmer_key_rc(int K, PatWindow& P, const uint8_t* p) {
+  if (K == 8) return kmer_key8_rc(p);
+  uint32_t key = 0;
+  for (int t = 0; t < K; ++t) key |= (3u - P.at(t)) << (2 * t);
+  return key;
+}
+
 // 4 resident CTAs (64 registers): capping registers for 6 or 8 CTAs/SM spills and runs 2-4x
 // slower on configs[3]/[4] (profiles/r01_fm_occupancy_sweep.jsonl).
 template <bool FIXED, bool WORK, int STRANDS, bool LEAN>
@@ -370,10 +388,10 @@ __global__ void __launch_bounds__(256, 4) k_fm_count(FmParams F, const uint8_t* 
     len = FIXED ? fixed_len : lens[pi];
     const uint8_t* p = pat + (FIXED ? pi * (uint64_t)fixed_len : offs[pi]);
     P.reset(p);
-    if (len >= 8) {
-      uint2 iv = __ldg(F.kmer + (rc ? kmer_key8_rc(p) : kmer_key8(p + len - 8)));
+    if (F.K && len >= (uint32_t)F.K) {
+      uint2 iv = __ldg(F.kmer + (rc ? kmer_key_rc(F.K, P, p) : kmer_key(F.K, P, p, len)));
       lo = iv.x; hi = iv.y;
-      k = (int64_t)len - 9;
+      k = (int64_t)len - 1 - F.K;
     } else {
       lo = 0; hi = (uint32_t)F.N;
       k = (int64_t)len - 1;
@@ -473,18 +491,18 @@ __global__ void __launch_bounds__(256) k_fm_approx1(FmParams F, const uint8_t* _
     uint64_t total = 0;
     uint32_t lo, hi;
     int64_t j;
-    if (len >= 8) {
-      const uint32_t key0 = kmer_key8(p + len - 8);
-      for (int t = 0; t < 8; ++t) {                       // one substitution among the last 8 symbols
+    if (F.K && len >= (uint32_t)F.K) {
+      const uint32_t key0 = kmer_key(F.K, P, p, len);
+      for (int t = 0; t < F.K; ++t) {                     // one substitution among the last K symbols
         const uint32_t f = (key0 >> (2 * t)) & 3u;
         for (uint32_t r = 1; r < 4; ++r) {
           const uint2 iv = __ldg(F.kmer + (key0 ^ ((f ^ ((f + r) & 3u)) << (2 * t))));
-          if (iv.x < iv.y) total += fm_continue(F, P, (int64_t)len - 9, iv.x, iv.y);
+          if (iv.x < iv.y) total += fm_continue(F, P, (int64_t)len - 1 - F.K, iv.x, iv.y);
         }
       }
       const uint2 iv0 = __ldg(F.kmer + key0);
       lo = iv0.x; hi = iv0.y;
-      j = (int64_t)len - 9;
+      j = (int64_t)len - 1 - F.K;
     } else {
       lo = 0; hi = (uint32_t)F.N;
       j = (int64_t)len - 1;
@@ -517,11 +535,12 @@ static FmParams params_of(const qr_fm* fm) {
   F.lines = fm->bwt->lines;
   F.super = fm->bwt->super;
   F.kmer = fm->kmer;
+  F.K = fm->kmer_k;
   F.spos = fm->spos;
   F.N = fm->N;
   F.last_line = fm->bwt->n_lines - 1;
   for (int c = 0; c < 4; ++c) F.C[c] = (uint32_t)fm->C[c];
-  F.Ct = reinterpret_cast<const uint32_t*>(fm->kmer + 65536);
+  F.Ct = reinterpret_cast<const uint32_t*>(fm->kmer + kmer_entries(fm->kmer_k));
   return F;
 }
 
@@ -591,7 +610,7 @@ qr_status fm_count_device(const qr_fm* fm, const uint8_t* pat, const uint32_t* l
 
 // d_text: device copy, >= ceil(n/32) words, zero padded.  d_sa: optional device SA (N u32).
 qr_status fm_build_device(const uint64_t* d_text, uint64_t n, const uint32_t* d_sa_given, int device, cudaStream_t st,
-                          qr_fm** out) {
+                          qr_fm** out, int kmer_k) {
   const uint64_t N = n + 1;
   const int sms = sm_count(device);
   cudaError_t e;
@@ -631,15 +650,17 @@ qr_status fm_build_device(const uint64_t* d_text, uint64_t n, const uint32_t* d_
   fm->C[0] = 1;
   for (int c = 1; c < 4; ++c) fm->C[c] = fm->C[c - 1] + h_aux[c];   // C[c] = 1 + #{t_i < c}
   fm->C[4] = N;
-  if ((e = cudaMalloc((void**)&fm->kmer, (65536 + 2) * sizeof(uint2)))) return bail(cuda_fail(e, "alloc kmer"));
+  fm->kmer_k = kmer_k;
+  const uint64_t ne = kmer_entries(kmer_k);
+  if ((e = cudaMalloc((void**)&fm->kmer, (ne + 2) * sizeof(uint2)))) return bail(cuda_fail(e, "alloc kmer"));
   {
     uint32_t Ch[4] = {(uint32_t)fm->C[0], (uint32_t)fm->C[1], (uint32_t)fm->C[2], (uint32_t)fm->C[3]};
-    if ((e = cudaMemcpyAsync(fm->kmer + 65536, Ch, sizeof(Ch), cudaMemcpyHostToDevice, st)))
+    if ((e = cudaMemcpyAsync(fm->kmer + ne, Ch, sizeof(Ch), cudaMemcpyHostToDevice, st)))
       return bail(cuda_fail(e, "copy C"));
     if ((e = cudaStreamSynchronize(st))) return bail(cuda_fail(e, "copy C"));
   }
   FmParams F = params_of(fm);
-  k_kmer_table<<<65536 / 256, 256, 0, st>>>(F, fm->kmer);
+  if (kmer_k) k_kmer_table<<<(unsigned)((ne + 255) / 256), 256, 0, st>>>(F, fm->kmer);
   if ((e = cudaGetLastError())) return bail(cuda_fail(e, "k_kmer_table"));
   cudaFreeAsync(d_sa, st);
   cudaFreeAsync(d_bwt, st);

@@ -45,7 +45,8 @@ struct qr_fm {
   uint64_t N;           // n + 1
   uint64_t spos;        // BWT row of '$'
   uint64_t C[5];        // C[c] = 1 + #{t_i < c}; C[4] = N
-  uint2* kmer;          // 65536 [lo, hi) intervals after 8 backward steps, then C[0..3] (2 uint2)
+  uint2* kmer;          // 4^K [lo, hi) intervals after K backward steps, then C[0..3] (2 uint2)
+  int kmer_k;           // K: table of K-mers (PAPER.md:918 uses 8; 0 = no table)
 };
 
 namespace qr {
@@ -78,6 +79,7 @@ cudaError_t launch_quadrank_rank(const qr_index* h, const uint64_t* q, const uin
                                  cudaStream_t st);
 cudaError_t launch_quadrank_all4(const qr_index* h, const uint64_t* q, uint64_t* out4, uint64_t m, cudaStream_t st);
 cudaError_t launch_gather(const qr_index* h, const uint64_t* q, uint64_t* out, uint64_t m, int mode, cudaStream_t st);
+inline uint64_t kmer_entries(int k) { return 1ull << (2 * k); }
 qr_status fm_count_device(const qr_fm* fm, const uint8_t* pat, const uint32_t* lengths, uint32_t fixed_len,
                           uint32_t* out, uint32_t* out_rc, uint64_t m, uint64_t* work, cudaStream_t st,
                           int approx = 0);

@@ -318,3 +318,35 @@ def test_cli_fm_count(cuda, tmp_path):
     rcat, roff, rlens = oracle.pack_patterns([revcomp(r) for r in reads])
     assert [r[1] for r in rows] == list(oracle.scan_count(sym, cat, off, lens))
     assert [r[2] for r in rows] == list(oracle.scan_count(sym, rcat, roff, rlens))
+
+
+@pytest.mark.parametrize("k", [0, 1, 5, 8, 10, 12])
+def test_fm_kmer_width_does_not_change_counts(cuda, k):
+    """Seeded vs unseeded counts are identical for every table width, incl. no table,
+    on exact / both-strand / <=1-mismatch counting; the table holds the K-mer interval sizes."""
+    torch = _torch()
+    n = 70000
+    w = gen.dna(81, n, 1)
+    sym = gen.unpack_dna(w, n)
+    fm = qr.qr_fm_build(w, n, kmer_k=k)
+    assert fm.kmer_k == k
+    pats = mixed_patterns(np.random.default_rng(k), sym, 1500)
+    cat, off, lens = oracle.pack_patterns(pats)
+    ref = oracle.scan_count(sym, cat, off, lens)
+    dc, dl = to_dev(cat, cuda), to_dev(lens, cuda)
+    d = torch.empty(lens.size, dtype=torch.int32, device=cuda)
+    qr.qr_fm_count(fm, dc, dl, 0, d, lens.size)
+    d1 = torch.empty(lens.size, dtype=torch.int32, device=cuda)
+    qr.qr_fm_count_approx(fm, dc, dl, 0, 1, d1, lens.size)
+    df, dr = torch.empty_like(d), torch.empty_like(d)
+    qr.qr_fm_count_both(fm, dc, dl, 0, df, dr, lens.size)
+    torch.cuda.synchronize()
+    assert np.array_equal(to_host(d).view(np.uint32), ref)
+    assert np.array_equal(to_host(df).view(np.uint32), ref)
+    rcat, roff, rlens = oracle.pack_patterns([revcomp(p) for p in pats])
+    assert np.array_equal(to_host(dr).view(np.uint32), oracle.scan_count(sym, rcat, roff, rlens))
+    assert np.array_equal(to_host(d1).view(np.uint32), oracle.scan_count_hd1(sym, cat, off, lens))
+    if 0 < k <= 8:
+        t = qr.qr_fm_export_kmer(fm)
+        assert t.shape == (4 ** k, 2)
+        assert int((t[:, 1].astype(np.int64) - t[:, 0]).sum()) == n - k + 1

@@ -16,7 +16,7 @@ def t(fn, reps=5):
     return a.elapsed_time(b) / reps
 for name, n, kind, m, L, seed in (("c4", 1 << 26, 0, 10**7, 32, 4), ("c5", 1 << 30, 1, 10**8, 100, 5)):
     txt = torch.empty((n + 31) // 32 + 1, dtype=torch.uint64, device=dev); gen.dna_dev(seed, n, kind, txt)
-    fm = qr.qr_fm_build(txt, n)
+    fm = qr.qr_fm_build(txt, n, kmer_k=int(os.environ.get("KMER", "8")))
     pats = torch.empty(m * L, dtype=torch.uint8, device=dev); gen.patterns_dev(seed, 0 if kind == 0 else 1, m, L, txt, n, pats)
     out = torch.empty(m, dtype=torch.int32, device=dev)
     ref = None
@@ -26,6 +26,6 @@ for name, n, kind, m, L, seed in (("c4", 1 << 26, 0, 10**7, 32, 4), ("c5", 1 << 
             ms = t(lambda: qr.qr_fm_count(fm, pats, None, L, out, m, st), reps=3 if name == "c5" else 10)
             h = int(out.view(torch.int32).to(torch.int64).sum())
             ref = h if ref is None else ref
-            print(json.dumps(dict(cfg=name, pair=pair, bps=bps, ms=ms, gpat_s=m / ms / 1e6, checksum_ok=(h == ref))), flush=True)
+            print(json.dumps(dict(cfg=name, kmer=fm.kmer_k, pair=pair, bps=bps, ms=ms, gpat_s=m / ms / 1e6, checksum_ok=(h == ref))), flush=True)
     fm.free(); del txt, pats, out; torch.cuda.empty_cache()
 qr.qr_set_tuning("fm_step", 0); qr.qr_set_tuning("fm_blocks_per_sm", 64)
