@@ -673,7 +673,7 @@ QR_EXPORT qr_status qr_fm_clone_to_device(const qr_fm* fm, int device, void* str
   qr_status s = qr_clone_to_device(fm->bwt, device, stream, &c->bwt);
   if (s != QR_OK) { delete c; return s; }
   DeviceGuard dg(device);
-  const size_t kb = (kmer_entries(fm->kmer_k) + 2) * sizeof(uint2);        // table + C[0..3] tail
+  const size_t kb = (kmer_c_offset(fm->kmer_k) + 2) * sizeof(uint2);       // table + C[0..3] tail
   cudaError_t e = cudaMalloc((void**)&c->kmer, kb);
   if (!e) e = cudaMemcpyPeerAsync(c->kmer, device, fm->kmer, fm->bwt->device, kb, (cudaStream_t)stream);
   if (!e) e = cudaStreamSynchronize((cudaStream_t)stream);

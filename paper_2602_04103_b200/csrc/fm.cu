@@ -540,7 +540,7 @@ static FmParams params_of(const qr_fm* fm) {
   F.N = fm->N;
   F.last_line = fm->bwt->n_lines - 1;
   for (int c = 0; c < 4; ++c) F.C[c] = (uint32_t)fm->C[c];
-  F.Ct = reinterpret_cast<const uint32_t*>(fm->kmer + kmer_entries(fm->kmer_k));
+  F.Ct = reinterpret_cast<const uint32_t*>(fm->kmer + kmer_c_offset(fm->kmer_k));
   return F;
 }
 
@@ -652,10 +652,10 @@ qr_status fm_build_device(const uint64_t* d_text, uint64_t n, const uint32_t* d_
   fm->C[4] = N;
   fm->kmer_k = kmer_k;
   const uint64_t ne = kmer_entries(kmer_k);
-  if ((e = cudaMalloc((void**)&fm->kmer, (ne + 2) * sizeof(uint2)))) return bail(cuda_fail(e, "alloc kmer"));
+  if ((e = cudaMalloc((void**)&fm->kmer, (kmer_c_offset(kmer_k) + 2) * sizeof(uint2)))) return bail(cuda_fail(e, "alloc kmer"));
   {
     uint32_t Ch[4] = {(uint32_t)fm->C[0], (uint32_t)fm->C[1], (uint32_t)fm->C[2], (uint32_t)fm->C[3]};
-    if ((e = cudaMemcpyAsync(fm->kmer + ne, Ch, sizeof(Ch), cudaMemcpyHostToDevice, st)))
+    if ((e = cudaMemcpyAsync(fm->kmer + kmer_c_offset(kmer_k), Ch, sizeof(Ch), cudaMemcpyHostToDevice, st)))
       return bail(cuda_fail(e, "copy C"));
     if ((e = cudaStreamSynchronize(st))) return bail(cuda_fail(e, "copy C"));
   }

@@ -80,6 +80,8 @@ cudaError_t launch_quadrank_rank(const qr_index* h, const uint64_t* q, const uin
 cudaError_t launch_quadrank_all4(const qr_index* h, const uint64_t* q, uint64_t* out4, uint64_t m, cudaStream_t st);
 cudaError_t launch_gather(const qr_index* h, const uint64_t* q, uint64_t* out, uint64_t m, int mode, cudaStream_t st);
 inline uint64_t kmer_entries(int k) { return 1ull << (2 * k); }
+// C[0..3] (16 B) follow the table at an even entry index, so that the 16-B load is aligned
+inline uint64_t kmer_c_offset(int k) { return (kmer_entries(k) + 1) & ~1ull; }
 qr_status fm_count_device(const qr_fm* fm, const uint8_t* pat, const uint32_t* lengths, uint32_t fixed_len,
                           uint32_t* out, uint32_t* out_rc, uint64_t m, uint64_t* work, cudaStream_t st,
                           int approx = 0);
