@@ -203,7 +203,9 @@ def bench_birank(ctx, p: float, steps, warmup, with_ceiling: bool, clocks=None, 
             cms = ctx.timed(lambda: qr.qr_gather_ceiling(h, q, out, mode, m, ctx.stream), steps, warmup)
             res[f"ceiling_mode{mode}"] = {"ms": cms, "gq_s": ctx.world * m / cms / 1e6}
     if e2e:
-        me = M2                                    # the full per-GPU batch, host-resident
+        # the full per-GPU batch from pinned host memory at N = 1; at N > 1 each rank stages
+        # M2 / N queries so that the box pins ~16 GB in total, not 16 GB per GPU
+        me = M2 if ctx.world == 1 else max(10**8, M2 // ctx.world)
         qh = torch.empty(me, dtype=torch.uint64).pin_memory()
         qh.copy_(q[:me])
         oh = torch.empty(me, dtype=torch.uint64).pin_memory()
