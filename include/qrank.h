@@ -170,13 +170,24 @@ qr_status qr_fm_count_work(const qr_fm* fm, const uint8_t* patterns, const uint3
  * arithmetic and the same loads as qr_rank, no popcount and no superblock read;
  * out[k] = XOR of the loaded words.  mode 0: exactly the sectors qr_rank reads (32 B or
  * 64 B); mode 1: the full 64-B line always; mode 2: mode 0 plus qr_rank's superblock-word
- * read (BiRank; on QuadRank mode 2 = mode 0).  Device pointers only. */
+ * read (BiRank; on QuadRank mode 2 = mode 0); mode 3: the cluster shared-memory rank kernel's
+ * own launch shape and loads without the superblock read (BiRank16 with a superblock cache,
+ * qr_super_cache_bytes > 0; else QR_EINVAL).  Device pointers only. */
 qr_status qr_gather_ceiling(const qr_index* h, const uint64_t* q, uint64_t* out, uint64_t m, int mode, void* stream);
 
 /* ------------------------------------------------------------------ handles */
 
 /* sigma (2 or 4), n, and the layout's device bytes (lines + superblock array). */
 qr_status qr_info(const qr_index* h, uint64_t* n, int* sigma, uint64_t* line_bytes, uint64_t* super_bytes);
+
+/* Bytes of the re-encoded superblock table that the cluster rank kernels keep in shared
+ * memory (2 CTAs x *cta_bytes; sbcache.cu), or 0 when this handle's rank calls
+ * read the superblock words from global memory (layouts without an L1 array, n >= 2^35, or a
+ * table larger than two CTAs' shared memory).  A cache of s_i / s_{i,c}
+ * (PAPER.md:513): results never depend on it. */
+qr_status qr_super_cache_bytes(const qr_index* h, uint64_t* cta_bytes);
+/* Number of 2-CTA clusters those kernels launch (as many as fit at once; 0 without a cache). */
+qr_status qr_super_cache_clusters(const qr_index* h, int* clusters);
 
 /* Copy the layout to buffers of qr_info's sizes (host, or device — e.g. to broadcast a built
  * structure to other GPUs; either may be NULL).  Synchronous. */
@@ -219,7 +230,13 @@ const char* qr_last_error(void);
  * 2 = lean step),
  * "index64" (1: always use the 64-bit line-index path that n >= 2^36 (sigma=2) / 2^37
  * (sigma=4) selects, so that it can be tested on small n),
- * "l2_fetch_granularity" (cudaLimitMaxL2FetchGranularity of the current device, bytes).
+ * "l2_fetch_granularity" (cudaLimitMaxL2FetchGranularity of the current device, bytes),
+ * "rank_smem" (superblock words of rank / rank_all4 from the 2-CTA cluster shared-memory
+ * table when the handle has one: 0 never, 1 (default) for batches of >= 2^22 queries, 2 always),
+ * "rank_dyn" (1, default: those kernels take work in chunks from a global counter; 0: static
+ * grid-stride order), "rank_smem_k" (their queries per lane pair per group: 0 = auto (BiRank 4,
+ * QuadRank 2), 1, 2, 4 with 1024-thread CTAs, 6 with 768, 8 with 512), "rank_smem_clusters" (0 = as many 2-CTA
+ * clusters as fit at once, else that many).
  * QR_EINVAL for an unknown key or out-of-range value. */
 qr_status qr_set_tuning(const char* key, int64_t value);
 

@@ -29,6 +29,7 @@ EXPORTS = (
     "qr_fm_count_work", "qr_gather_ceiling", "qr_info", "qr_export_layout", "qr_fm_info", "qr_fm_export_kmer",
     "qr_clone_to_device", "qr_fm_clone_to_device", "qr_sync", "qr_free", "qr_fm_free", "qr_last_error",
     "qr_version", "qr_set_tuning", "qr_build", "qr_layout", "qr_rank_chain", "qr_import_layout", "qr_fm_build_ex", "qr_fm_kmer_width",
+    "qr_super_cache_bytes", "qr_super_cache_clusters",
 )
 
 
@@ -79,6 +80,8 @@ def lib():
             "qr_import_layout": ([V, V, U64, I32, I32, V, PP], I32),
             "qr_fm_build_ex": ([V, U64, V, I32, I32, V, PP], I32),
             "qr_fm_kmer_width": ([V, C.POINTER(C.c_int)], I32),
+            "qr_super_cache_bytes": ([V, C.POINTER(U64)], I32),
+            "qr_super_cache_clusters": ([V, C.POINTER(C.c_int)], I32),
         }
         for name, (args, res) in sig.items():
             f = getattr(L, name)
@@ -335,6 +338,20 @@ def qr_fm_clone_to_device(fm: Fm, device: int, stream=None) -> Fm:
     out = C.c_void_p()
     _check(lib().qr_fm_clone_to_device(fm.ptr, device, _stream(stream), C.byref(out)), "qr_fm_clone_to_device")
     return Fm(out.value)
+
+
+def qr_super_cache_bytes(h: "Index") -> int:
+    """Shared-memory bytes per CTA of the superblock table the rank kernels use (0 = none)."""
+    v = C.c_uint64(0)
+    _check(lib().qr_super_cache_bytes(h.ptr, C.byref(v)), "qr_super_cache_bytes")
+    return int(v.value)
+
+
+def qr_super_cache_clusters(h: "Index") -> int:
+    """2-CTA clusters the shared-memory rank kernels launch (0 = no table)."""
+    v = C.c_int(0)
+    _check(lib().qr_super_cache_clusters(h.ptr, C.byref(v)), "qr_super_cache_clusters")
+    return int(v.value)
 
 
 def qr_sync(stream=None):

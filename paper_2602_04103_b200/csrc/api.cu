@@ -24,6 +24,10 @@ int g_fm_blocks_per_sm = 64;    // 256-thread CTAs per SM of the FM grid (severa
 int g_rank_s_lane = 1;
 int g_fm_lean = 0;              // FM step flavour: 0 auto (by L2 residency), 1 de-duplicating, 2 lean
 int g_index64 = 0;              // 1: force the 64-bit line-index path (tests the n >= 2^36/2^37 code on small n)          // lane of a pair that loads the superblock word
+int g_rank_smem = 1;            // superblock words from cluster shared memory: 0 never, 1 large batches, 2 always
+int g_rank_dyn = 1;             // cluster rank kernels: 1 = dynamic (atomic chunk) work order, 0 = static grid stride
+int g_rank_smem_clusters = 0;   // cluster rank kernels: 0 = as many 2-CTA clusters as fit (occupancy API), else this many
+int g_rank_smem_k = 0;          // cluster rank kernels: queries per lane pair per group (0 auto, 1, 2, 4 @1024 thr, 6 @768, 8 @512)
 int g_rank_pair = 1;            // 1: lane-pair kernels (one L2 request per query); 0: one lane per query
 uint64_t g_stage_chunk = 1ull << 23;   // queries per chunk on the staged host path (sweep: profiles/r01_e2e_sweep)
 int g_stage_slots = 3;                 // device buffers / internal streams of the staged path
@@ -295,6 +299,19 @@ QR_EXPORT qr_status qr_set_tuning(const char* key, int64_t value) {
   } else if (!strcmp(key, "rank_s_lane")) {
     if (value != 0 && value != 1) return fail(QR_EINVAL, "rank_s_lane must be 0 or 1");
     g_rank_s_lane = (int)value;
+  } else if (!strcmp(key, "rank_smem")) {
+    if (value < 0 || value > 2) return fail(QR_EINVAL, "rank_smem must be 0 (off), 1 (auto) or 2 (always)");
+    g_rank_smem = (int)value;
+  } else if (!strcmp(key, "rank_smem_k")) {
+    if (value != 0 && value != 1 && value != 2 && value != 4 && value != 6 && value != 8)
+      return fail(QR_EINVAL, "rank_smem_k must be 0 (auto), 1, 2, 4, 6 or 8");
+    g_rank_smem_k = (int)value;
+  } else if (!strcmp(key, "rank_smem_clusters")) {
+    if (value < 0 || value > 4096) return fail(QR_EINVAL, "rank_smem_clusters must be 0..4096");
+    g_rank_smem_clusters = (int)value;
+  } else if (!strcmp(key, "rank_dyn")) {
+    if (value != 0 && value != 1) return fail(QR_EINVAL, "rank_dyn must be 0 or 1");
+    g_rank_dyn = (int)value;
   } else if (!strcmp(key, "fm_step")) {
     if (value < 0 || value > 2) return fail(QR_EINVAL, "fm_step must be 0 (auto), 1 or 2");
     g_fm_lean = (int)value;
@@ -465,10 +482,13 @@ QR_EXPORT qr_status qr_rank_all4(const qr_index* h, const uint64_t* q, uint64_t*
 QR_EXPORT qr_status qr_gather_ceiling(const qr_index* h, const uint64_t* q, uint64_t* out, uint64_t m, int mode,
                                       void* stream) {
   if (!h || (m && (!q || !out))) return fail(QR_EINVAL, "qr_gather_ceiling: null pointer");
-  if (mode < 0 || mode > 2) return fail(QR_EINVAL, "qr_gather_ceiling: mode must be 0, 1 or 2");
+  if (mode < 0 || mode > 3) return fail(QR_EINVAL, "qr_gather_ceiling: mode must be 0..3");
+  if (mode == 3 && (h->sigma != 2 || !h->spack))
+    return fail(QR_EINVAL, "qr_gather_ceiling: mode 3 needs a BiRank16 handle with a superblock cache");
   DeviceGuard dg(h->device);
   if (m && classify({q, out}, h->device) != 1) return fail(QR_EINVAL, "qr_gather_ceiling: device pointers only");
-  cudaError_t e = launch_gather(h, q, out, m, mode, (cudaStream_t)stream);
+  cudaError_t e = mode == 3 ? launch_super_pack_rank(h, q, nullptr, out, m, 3, (cudaStream_t)stream)
+                            : launch_gather(h, q, out, m, mode, (cudaStream_t)stream);
   return e ? cuda_fail(e, "qr_gather_ceiling launch") : QR_OK;
 }
 
@@ -588,6 +608,19 @@ QR_EXPORT qr_status qr_info(const qr_index* h, uint64_t* n, int* sigma, uint64_t
   return QR_OK;
 }
 
+QR_EXPORT qr_status qr_super_cache_bytes(const qr_index* h, uint64_t* cta_bytes) {
+  if (!h || !cta_bytes) return fail(QR_EINVAL, "qr_super_cache_bytes: null pointer");
+  *cta_bytes = super_pack_cta_bytes(h);
+  return QR_OK;
+}
+
+QR_EXPORT qr_status qr_super_cache_clusters(const qr_index* h, int* clusters) {
+  if (!h || !clusters) return fail(QR_EINVAL, "qr_super_cache_clusters: null pointer");
+  DeviceGuard dg(h->device);
+  *clusters = super_pack_clusters(h);
+  return QR_OK;
+}
+
 QR_EXPORT qr_status qr_export_layout(const qr_index* h, void* host_lines, void* host_super) {
   if (!h) return fail(QR_EINVAL, "qr_export_layout: null handle");
   DeviceGuard dg(h->device);
@@ -615,6 +648,7 @@ QR_EXPORT qr_status qr_import_layout(const void* lines, const void* super, uint6
   cudaStream_t st = (cudaStream_t)stream;
   cudaError_t e = cudaMemcpyAsync(h->lines, lines, h->n_lines * 64, cudaMemcpyDefault, st);
   if (!e && super_bytes_of(h)) e = cudaMemcpyAsync(h->super, super, super_bytes_of(h), cudaMemcpyDefault, st);
+  if (!e && (s = build_super_pack(h, st)) != QR_OK) { qr_free(h); return s; }
   if (!e) e = cudaStreamSynchronize(st);
   if (e) { qr_free(h); return cuda_fail(e, "qr_import_layout"); }
   *out = h;
@@ -657,6 +691,7 @@ QR_EXPORT qr_status qr_clone_to_device(const qr_index* h, int device, void* stre
   if (can) cudaDeviceEnablePeerAccess(h->device, 0), cudaGetLastError();
   cudaError_t e = cudaMemcpyPeerAsync(c->lines, device, h->lines, h->device, h->n_lines * 64, st);
   if (!e && super_bytes_of(h)) e = cudaMemcpyPeerAsync(c->super, device, h->super, h->device, super_bytes_of(h), st);
+  if (!e && (s = build_super_pack(c, st)) != QR_OK) { qr_free(c); return s; }
   if (!e) e = cudaStreamSynchronize(st);
   if (e) { qr_free(c); return cuda_fail(e, "qr_clone_to_device"); }
   *out = c;
@@ -693,6 +728,7 @@ QR_EXPORT void qr_free(qr_index* h) {
   DeviceGuard dg(h->device);
   if (h->lines) cudaFree(h->lines);
   if (h->super) cudaFree(h->super);
+  if (h->spack) cudaFree(h->spack);
   delete h;
 }
 

@@ -86,6 +86,7 @@ qr_status birank_build_device(const uint64_t* d_bits, uint64_t n, int device, cu
   k_bi_write<<<g, 256, 0, st>>>(reinterpret_cast<const uint16_t*>(d_bits), L, c1, R, h->lines, h->super);
   if ((e = cudaGetLastError())) return bail(e, "k_bi_write");
   cudaFreeAsync(c1, st); cudaFreeAsync(tot, st); cudaFreeAsync(R, st); cudaFreeAsync(tmp, st);
+  if ((rs = build_super_pack(h, st)) != QR_OK) { qr_free(h); return rs; }
   *out = h;
   return QR_OK;
 }
@@ -342,6 +343,7 @@ static cudaError_t bi_rank_k(const qr_index* h, const uint64_t* q, const uint8_t
 cudaError_t launch_birank_rank(const qr_index* h, const uint64_t* q, const uint8_t* c, uint64_t* out, uint64_t m,
                                cudaStream_t st) {
   if (m == 0) return cudaSuccess;
+  if (use_super_pack(h, m)) return launch_super_pack_rank(h, q, c, out, m, 0, st);
   switch (g_rank_k) {
     case 1: return bi_rank_k<1>(h, q, c, out, m, st);
     case 2: return bi_rank_k<2>(h, q, c, out, m, st);

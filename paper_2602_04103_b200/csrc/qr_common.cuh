@@ -37,6 +37,8 @@ struct qr_index {
   uint4* lines;         // n_lines * 64 B, 256-B aligned (cudaMalloc)
   uint32_t* super;      // sigma=2: u32[n_super]; sigma=4: u32[4*n_super] (s_{i,c} at 4i+c)
   int sm_count;
+  uint64_t* spack;      // superblock array re-encoded for the shared-memory rank kernels (sbcache.cu), or null
+  uint64_t spack_half;  // groups held by each CTA of the 2-CTA cluster
 };
 
 struct qr_fm {
@@ -85,6 +87,12 @@ inline uint64_t kmer_c_offset(int k) { return (kmer_entries(k) + 1) & ~1ull; }
 qr_status fm_count_device(const qr_fm* fm, const uint8_t* pat, const uint32_t* lengths, uint32_t fixed_len,
                           uint32_t* out, uint32_t* out_rc, uint64_t m, uint64_t* work, cudaStream_t st,
                           int approx = 0);
+qr_status build_super_pack(qr_index* h, cudaStream_t st);
+uint64_t super_pack_cta_bytes(const qr_index* h);
+int super_pack_clusters(const qr_index* h);
+bool use_super_pack(const qr_index* h, uint64_t m);
+cudaError_t launch_super_pack_rank(const qr_index* h, const uint64_t* q, const uint8_t* c, uint64_t* out, uint64_t m,
+                                   int what, cudaStream_t st);
 qr_status birank_build_device(const uint64_t* d_bits, uint64_t n, int device, cudaStream_t st, qr_index** out);
 
 // grid for a grid-stride kernel: a multiple of the SM count

@@ -129,6 +129,7 @@ qr_status quadrank_build_device(const uint64_t* d_text, uint64_t n, int device, 
   k_qd_write<<<g, 256, 0, st>>>(d_text, L, c96, R, h->lines, h->super);
   if ((e = cudaGetLastError())) return bail(e, "k_qd_write");
   cudaFreeAsync(c96, st); cudaFreeAsync(tot, st); cudaFreeAsync(R, st); cudaFreeAsync(tmp, st);
+  if ((rs = build_super_pack(h, st)) != QR_OK) { qr_free(h); return rs; }
   *out = h;
   return QR_OK;
 }
@@ -526,6 +527,7 @@ static cudaError_t qd_gather_k(const qr_index* h, const uint64_t* q, uint64_t* o
 cudaError_t launch_quadrank_rank(const qr_index* h, const uint64_t* q, const uint8_t* c, uint64_t* out, uint64_t m,
                                  cudaStream_t st) {
   if (m == 0) return cudaSuccess;
+  if (use_super_pack(h, m)) return launch_super_pack_rank(h, q, c, out, m, 0, st);
   switch (g_rank_k) {
     case 1: return qd_rank_k<1>(h, q, c, out, m, st);
     case 2: return qd_rank_k<2>(h, q, c, out, m, st);
@@ -535,6 +537,7 @@ cudaError_t launch_quadrank_rank(const qr_index* h, const uint64_t* q, const uin
 }
 cudaError_t launch_quadrank_all4(const qr_index* h, const uint64_t* q, uint64_t* out4, uint64_t m, cudaStream_t st) {
   if (m == 0) return cudaSuccess;
+  if (use_super_pack(h, m)) return launch_super_pack_rank(h, q, nullptr, out4, m, 1, st);
   switch (g_rank_k) {
     case 1: return qd_all4_k<1>(h, q, out4, m, st);
     case 2: return qd_all4_k<2>(h, q, out4, m, st);

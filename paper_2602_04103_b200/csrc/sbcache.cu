@@ -1,0 +1,598 @@
+// sbcache.cu — rank kernels that read the superblock words from distributed shared memory.
+//
+// Why: on B200 a random query on an HBM-resident layout costs L2 *requests*, not bytes (DESIGN.md
+// §6): the lane-pair kernels issue one request for the 64-B line, plus one for the superblock
+// word s_{j>>7} / s_{j>>8,c}.  That second request is an L2 hit,
+// yet it takes the same miss-path slot in the SM and costs ~16% (gather ceiling with vs without
+// it, profiles/r01_s_probe.jsonl).  Here the superblock array is held in the shared memory of a
+// 2-CTA cluster (one CTA per SM, 1024 threads) for the whole launch, so the only global request
+// of a query is its line.
+//
+// The array is re-encoded losslessly so that it fits two CTAs' shared memory at the BASELINE
+// sizes (n = 2^34 bits: 270,601 superblocks; n = 2^32 chars: 74,899 x 4):
+//   BiRank16  — one u64 per group of 6 superblocks: bits [0,24) = s_{6g}; byte k (k = 1..5) at
+//               bits [16+8k, 24+8k) = s_{6g+k} - s_{6g} <= 5*31 = 155 (each superblock adds at
+//               most 128*496/2^11 = 31 to s).  Needs s < 2^24, i.e. n < 2^35.
+//   QuadRank16 — per group of 8 superblocks and per symbol c one u64: bits [0,22) = s_{8g,c};
+//               6-bit field k (k = 1..7) at bits [16+6k, 22+6k) = s_{8g+k,c} - s_{8g,c} <= 7*7
+//               (each superblock adds at most 256*224/2^13 = 7).  Needs s < 2^22, i.e. n < 2^35.
+// Group g lives in CTA (g & 1) of the cluster at local slot g >> 1; in global memory the packed
+// table is stored CTA-major (slots of CTA 0, then of CTA 1) so that each CTA preloads one
+// contiguous range.  The per-query arithmetic (Eq. 1, Listing 1) is unchanged: see birank.cu /
+// quadrank.cu — only where s comes from differs.
+#include <cooperative_groups.h>
+
+#include <map>
+#include <mutex>
+#include <tuple>
+
+#include "qr_common.cuh"
+
+namespace qr {
+
+
+// ------------------------------------------------------------------ packing (build time)
+
+__global__ void k_bi_pack_super(const uint32_t* __restrict__ super, uint64_t n_super, uint64_t groups, uint64_t half,
+                                uint64_t* __restrict__ pack) {
+  for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < groups; g += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t i0 = 6 * g;
+    const uint32_t s0 = super[i0];
+    uint64_t w = s0;
+#pragma unroll
+    for (int k = 1; k < 6; ++k)
+      if (i0 + k < n_super) w |= (uint64_t)(super[i0 + k] - s0) << (16 + 8 * k);
+    pack[(g & 1) * half + (g >> 1)] = w;
+  }
+}
+
+__global__ void k_qd_pack_super(const uint32_t* __restrict__ super, uint64_t n_super, uint64_t groups, uint64_t half,
+                                uint64_t* __restrict__ pack) {
+  for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < 4 * groups; t += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t g = t >> 2;
+    const uint32_t c = (uint32_t)(t & 3);
+    const uint64_t i0 = 8 * g;
+    const uint32_t s0 = super[4 * i0 + c];
+    uint64_t w = s0;
+#pragma unroll
+    for (int k = 1; k < 8; ++k)
+      if (i0 + k < n_super) w |= (uint64_t)(super[4 * (i0 + k) + c] - s0) << (16 + 6 * k);
+    pack[4 * ((g & 1) * half + (g >> 1)) + c] = w;
+  }
+}
+
+static int max_dyn_smem(int device) {
+  static std::mutex mu;
+  static int cache[64] = {};
+  std::lock_guard<std::mutex> g(mu);
+  if (device < 0 || device >= 64) return 0;
+  if (!cache[device]) {
+    int v = 0;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, device) != cudaSuccess || v <= 0) v = 1;
+    cache[device] = v;
+  }
+  return cache[device];
+}
+
+// Bytes of shared memory one CTA of the cluster needs, or 0 when the layout cannot use the cache.
+uint64_t super_pack_cta_bytes(const qr_index* h) {
+  if (!h->spack) return 0;
+  return h->spack_half * (h->sigma == 2 ? 8 : 32);
+}
+
+// Build h->spack from h->super (stream-ordered).  Leaves spack null (no error) when the layout
+// is outside the encoding's range or the half table exceeds a CTA's shared memory.
+qr_status build_super_pack(qr_index* h, cudaStream_t st) {
+  h->spack = nullptr;
+  h->spack_half = 0;
+  if (h->layout != QR_LAYOUT_BIRANK16 && h->layout != QR_LAYOUT_QUADRANK16) return QR_OK;
+  if (h->n >= (1ull << 35) || h->n_super == 0) return QR_OK;     // anchors: 24 / 22 bits
+  const bool bi = h->sigma == 2;
+  const uint64_t groups = bi ? (h->n_super + 5) / 6 : (h->n_super + 7) / 8;
+  // slots per CTA; even for BiRank so that CTA 1's range starts 16-B aligned
+  const uint64_t half = bi ? (((groups + 1) / 2 + 1) & ~1ull) : (groups + 1) / 2;
+  const uint64_t cta_bytes = half * (bi ? 8 : 32);
+  if (cta_bytes + 1024 > (uint64_t)max_dyn_smem(h->device)) return QR_OK;
+  cudaError_t e = cudaMalloc((void**)&h->spack, 2 * cta_bytes);
+  if (e) { h->spack = nullptr; return cuda_fail(e, "alloc packed superblocks"); }
+  cudaMemsetAsync(h->spack, 0, 2 * cta_bytes, st);
+  const unsigned g = grid_stride_blocks(bi ? groups : 4 * groups, 256, h->sm_count, 8);
+  if (bi) k_bi_pack_super<<<g, 256, 0, st>>>(h->super, h->n_super, groups, half, h->spack);
+  else    k_qd_pack_super<<<g, 256, 0, st>>>(h->super, h->n_super, groups, half, h->spack);
+  if ((e = cudaGetLastError())) { cudaFree(h->spack); h->spack = nullptr; return cuda_fail(e, "pack superblocks"); }
+  h->spack_half = half;
+  return QR_OK;
+}
+
+// ------------------------------------------------------------------ cluster helpers
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_barrier() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t map_to_rank(uint32_t saddr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ uint64_t ld_dsmem_u64(uint32_t addr) {
+  uint64_t v;
+  asm volatile("ld.shared::cluster.u64 %0, [%1];" : "=l"(v) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ void ld_dsmem_v2u64(uint32_t addr, uint64_t& a, uint64_t& b) {
+  asm volatile("ld.shared::cluster.v2.u64 {%0,%1}, [%2];" : "=l"(a), "=l"(b) : "r"(addr));
+}
+
+// Preload this CTA's half of the packed table (contiguous, 16-B aligned, even word count) and make both halves
+// visible cluster-wide.  Returns the shared::cluster addresses of slot 0 in CTA 0 and CTA 1.
+__device__ __forceinline__ void sc_preload(const uint64_t* __restrict__ pack, uint64_t half_words, uint64_t* smem,
+                                           uint32_t& base0, uint32_t& base1) {
+  const uint32_t r = cluster_rank();
+  const uint4* src = reinterpret_cast<const uint4*>(pack + r * half_words);
+  uint4* dst = reinterpret_cast<uint4*>(smem);
+  for (uint32_t i = threadIdx.x; i < (uint32_t)(half_words >> 1); i += blockDim.x) dst[i] = __ldg(src + i);
+  const uint32_t local = (uint32_t)__cvta_generic_to_shared(smem);
+  base0 = map_to_rank(local, 0);
+  base1 = map_to_rank(local, 1);
+  cluster_barrier();
+}
+
+// s_i of BiRank16 superblock i from the packed table.
+__device__ __forceinline__ uint32_t bi_s_from_pack(uint32_t sb, uint32_t base0, uint32_t base1) {
+  const uint32_t g = sb / 6u, k = sb - 6u * g;
+  const uint64_t v = ld_dsmem_u64(((g & 1u) ? base1 : base0) + (g >> 1) * 8u);
+  const uint32_t lo = (uint32_t)v & 0xffffffu;
+  return k ? lo + ((uint32_t)(v >> (16u + 8u * k)) & 0xffu) : lo;
+}
+__device__ __forceinline__ uint32_t qd_s_field(uint64_t v, uint32_t k) {
+  const uint32_t lo = (uint32_t)v & 0x3fffffu;
+  return k ? lo + ((uint32_t)(v >> (16u + 6u * k)) & 0x3fu) : lo;
+}
+
+// ------------------------------------------------------------------ BiRank16 rank (Eq. 1)
+// Same lane-pair structure as k_bi_rank2 (birank.cu), q < 2^36 index math; lane 1 of the pair
+// reads s from the cluster's shared memory.
+template <int K>
+__device__ __forceinline__ void sc_load_q(const uint64_t* __restrict__ q, uint64_t i0, uint64_t step, uint64_t m,
+                                          uint64_t (&qn)[K]) {
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    const uint64_t idx = i0 + (uint64_t)k * step;
+    qn[k] = idx < m ? ld_stream_u64(q + idx) : 0;
+  }
+}
+
+// Work order.  Static (DYN = false): the grid-stride order of k_bi_rank2 — the pair of global
+// lane-pair index P handles queries P, P + npair, ...  Dynamic (DYN = true): each warp takes
+// chunks of SC_CHUNK_STEPS groups of 16 K consecutive queries from a global counter (one
+// atomicAdd per chunk), so SMs that run faster take more chunks instead of waiting at the end.
+constexpr uint32_t SC_CHUNK_STEPS = 8;
+
+struct ScSched {
+  uint64_t gb;          // first query index of the warp's current group
+  uint64_t stride;      // distance between the K sub-groups of a group
+  uint64_t step;        // static: advance per group
+  uint32_t r;           // dynamic: group within the chunk
+};
+
+template <int K, bool DYN>
+__device__ __forceinline__ uint64_t sc_grab(unsigned long long* ctr) {
+  uint64_t b = 0;
+  if ((threadIdx.x & 31u) == 0) b = atomicAdd(ctr, (unsigned long long)(16u * K * SC_CHUNK_STEPS));
+  return __shfl_sync(0xffffffffu, b, 0);
+}
+
+template <int K, bool DYN>
+__device__ __forceinline__ ScSched sc_first(unsigned long long* ctr) {
+  ScSched s;
+  if (DYN) {
+    s.gb = sc_grab<K, DYN>(ctr);
+    s.stride = 16;
+    s.step = 16 * K;
+    s.r = 0;
+  } else {
+    const uint64_t npair = ((uint64_t)gridDim.x * blockDim.x) >> 1;
+    const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    s.gb = (tid & ~31ull) >> 1;
+    s.stride = npair;
+    s.step = npair * K;
+    s.r = 0;
+  }
+  return s;
+}
+
+template <int K, bool DYN>
+__device__ __forceinline__ ScSched sc_next(ScSched s, unsigned long long* ctr) {
+  if (DYN) {
+    if (++s.r == SC_CHUNK_STEPS) { s.gb = sc_grab<K, DYN>(ctr); s.r = 0; }
+    else s.gb += s.step;
+  } else {
+    s.gb += s.step;
+  }
+  return s;
+}
+
+// VAR bit 0: no superblock read (the shape's own gather ceiling, qr_gather_ceiling mode 3);
+// VAR bit 1: dynamic work order.
+template <int K, int THREADS, bool HAS_C, int VAR>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
+    k_bi_rank2c(const uint4* __restrict__ lines, const uint64_t* __restrict__ pack, uint64_t half_words,
+                const uint64_t* __restrict__ q, const uint8_t* __restrict__ cs, uint64_t* __restrict__ out, uint64_t m,
+                uint64_t last_line, unsigned long long* ctr) {
+  constexpr bool NOS = VAR & 1, DYN = (VAR & 2) != 0;
+  extern __shared__ uint64_t sc_smem[];
+  uint32_t base0, base1;
+  sc_preload(pack, half_words, sc_smem, base0, base1);
+  const uint32_t half = threadIdx.x & 1u;
+  const uint32_t pw = (threadIdx.x & 31u) >> 1;           // pair within the warp
+  ScSched sc = sc_first<K, DYN>(ctr);
+  uint64_t qn[K];
+  sc_load_q<K>(q, sc.gb + pw, sc.stride, m, qn);
+  while (sc.gb < m) {
+    const uint64_t i0 = sc.gb + pw;
+    uint64_t qq[K];
+    uint32_t jj[K], pp[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      qq[k] = qn[k];
+      uint32_t j = (uint32_t)(qq[k] >> 4) / 31u;                // floor(q/496), q < 2^36
+      j = j > (uint32_t)last_line ? (uint32_t)last_line : j;     // q > n: memory-safe clamp
+      const uint64_t p = 16 + qq[k] - (uint64_t)j * BI_B;
+      pp[k] = p > 511 ? 511u : (uint32_t)p;
+      jj[k] = j;
+    }
+    uint64_t w[K][4];
+    uint32_t s[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      w[k][0] = w[k][1] = w[k][2] = w[k][3] = 0;
+      if (half == 0 || pp[k] >= 256) ld_sector_na(lines + 4 * (uint64_t)jj[k] + 2 * half, w[k][0], w[k][1], w[k][2], w[k][3]);
+      s[k] = (half && !NOS) ? bi_s_from_pack(jj[k] >> BI_SB_LOG, base0, base1) : 0u;
+    }
+    const uint64_t stride = sc.stride;
+    sc = sc_next<K, DYN>(sc, ctr);
+    sc_load_q<K>(q, sc.gb + pw, sc.stride, m, qn);
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const uint64_t idx = i0 + (uint64_t)k * stride;
+      const bool right = pp[k] >= 256;
+      const int x = (int)(pp[k] & 255u);
+      const bool mine = half ? right : !right;
+      const uint64_t inv = half ? 0ull : ~0ull;
+      uint32_t cnt = 0;
+#pragma unroll
+      for (int t = 0; t < 4; ++t) cnt += __popcll(w[k][t] & (prefix_mask(x, t) ^ inv));
+      cnt = mine ? cnt : 0u;
+      uint64_t v = (half ? (uint64_t)cnt : (w[k][0] & 0xffffull) - cnt) + ((uint64_t)s[k] << BI_SHIFT);
+      if (NOS) v = w[k][0] ^ w[k][1] ^ w[k][2] ^ w[k][3];
+      v += __shfl_xor_sync(0xffffffffu, v, 1);
+      if (HAS_C) {
+        if (half == 0 && idx < m && cs[idx] == 0) v = qq[k] - v;
+      }
+      if (half == 0 && idx < m) st_stream_u64(out + idx, v);
+    }
+  }
+  cluster_barrier();   // the peer may still read this CTA's half of the table
+}
+
+// ------------------------------------------------------------------ QuadRank16 rank(q,c), rank_4(q)
+template <int K, bool WITH_C>
+__device__ __forceinline__ void sc_load_qc(const uint64_t* __restrict__ q, const uint8_t* __restrict__ cs, uint64_t i0,
+                                           uint64_t step, uint64_t m, uint64_t (&qn)[K], uint32_t (&cn)[K]) {
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    const uint64_t idx = i0 + (uint64_t)k * step;
+    qn[k] = idx < m ? ld_stream_u64(q + idx) : 0;
+    if (WITH_C) cn[k] = idx < m ? ld_stream_u8(cs + idx) & 3u : 0u;
+  }
+}
+
+template <int K>
+__device__ __forceinline__ void qd_locate32(const uint64_t (&qq)[K], uint64_t last_line, uint32_t (&jj)[K],
+                                            uint32_t (&pp)[K]) {
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    uint32_t j = (uint32_t)(qq[k] >> 5) / 7u;                  // floor(q/224), q < 2^37
+    j = j > (uint32_t)last_line ? (uint32_t)last_line : j;
+    const uint64_t p = 32 + qq[k] - (uint64_t)j * QD_B;
+    pp[k] = p > 255 ? 255u : (uint32_t)p;
+    jj[k] = j;
+  }
+}
+
+template <int K, int THREADS, bool DYN>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
+    k_qd_rank2c(const uint4* __restrict__ lines, const uint64_t* __restrict__ pack, uint64_t half_words,
+                const uint64_t* __restrict__ q, const uint8_t* __restrict__ cs, uint64_t* __restrict__ out, uint64_t m,
+                uint64_t last_line, unsigned long long* ctr) {
+  extern __shared__ uint64_t sc_smem[];
+  uint32_t base0, base1;
+  sc_preload(pack, half_words, sc_smem, base0, base1);
+  const uint32_t half = threadIdx.x & 1u;
+  const uint32_t pw = (threadIdx.x & 31u) >> 1;
+  ScSched sc = sc_first<K, DYN>(ctr);
+  uint64_t qn[K];
+  uint32_t cn[K];
+  sc_load_qc<K, true>(q, cs, sc.gb + pw, sc.stride, m, qn, cn);
+  while (sc.gb < m) {
+    const uint64_t i0 = sc.gb + pw;
+    uint64_t qq[K];
+    uint32_t jj[K], pp[K], cc[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) { qq[k] = qn[k]; cc[k] = cn[k]; }
+    qd_locate32<K>(qq, last_line, jj, pp);
+    uint64_t w[K][4];
+    uint32_t s[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      w[k][0] = w[k][1] = w[k][2] = w[k][3] = 0;
+      if (half == 0 || pp[k] >= 128) ld_sector_na(lines + 4 * (uint64_t)jj[k] + 2 * half, w[k][0], w[k][1], w[k][2], w[k][3]);
+      s[k] = 0;
+      if (half) {
+        const uint32_t sb = jj[k] >> QD_SB_LOG, g = sb >> 3;
+        s[k] = qd_s_field(ld_dsmem_u64(((g & 1u) ? base1 : base0) + (g >> 1) * 32u + 8u * cc[k]), sb & 7u);
+      }
+    }
+    const uint64_t stride = sc.stride;
+    sc = sc_next<K, DYN>(sc, ctr);
+    sc_load_qc<K, true>(q, cs, sc.gb + pw, sc.stride, m, qn, cn);
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const uint64_t idx = i0 + (uint64_t)k * stride;
+      const bool right = pp[k] >= 128;
+      const bool mine = half ? right : !right;
+      const uint64_t cl = 0ull - (uint64_t)(cc[k] & 1u), ch = 0ull - (uint64_t)(cc[k] >> 1);
+      const int x = (int)(pp[k] & 127u);
+      const uint64_t inv = half ? 0ull : ~0ull;
+      uint32_t cnt = 0;
+#pragma unroll
+      for (int t = 0; t < 2; ++t) cnt += __popcll((w[k][2 * t] ^ cl) & (w[k][2 * t + 1] ^ ch) & (prefix_mask(x, t) ^ inv));
+      cnt = mine ? cnt : 0u;
+      const uint64_t dw = (cc[k] & 2u) ? w[k][1] : w[k][0];
+      const uint64_t delta = (dw >> (16 * (cc[k] & 1u))) & 0xffffull;      // u16 slot c + (c & 2)
+      uint64_t v = (half ? (uint64_t)cnt : delta - cnt) + ((uint64_t)s[k] << QD_SHIFT);
+      v += __shfl_xor_sync(0xffffffffu, v, 1);
+      if (half == 0 && idx < m) st_stream_u64(out + idx, v);
+    }
+  }
+  cluster_barrier();
+}
+
+template <int K, int THREADS, bool DYN>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
+    k_qd_all4_2c(const uint4* __restrict__ lines, const uint64_t* __restrict__ pack, uint64_t half_words,
+                 const uint64_t* __restrict__ q, uint64_t* __restrict__ out4, uint64_t m, uint64_t last_line,
+                 unsigned long long* ctr) {
+  extern __shared__ uint64_t sc_smem[];
+  uint32_t base0, base1;
+  sc_preload(pack, half_words, sc_smem, base0, base1);
+  const uint32_t half = threadIdx.x & 1u;
+  const uint32_t pw = (threadIdx.x & 31u) >> 1;
+  ScSched sc = sc_first<K, DYN>(ctr);
+  uint64_t qn[K];
+  uint32_t cn[K];
+  sc_load_qc<K, false>(q, nullptr, sc.gb + pw, sc.stride, m, qn, cn);
+  while (sc.gb < m) {
+    const uint64_t i0 = sc.gb + pw;
+    uint64_t qq[K];
+    uint32_t jj[K], pp[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) qq[k] = qn[k];
+    qd_locate32<K>(qq, last_line, jj, pp);
+    uint64_t w[K][4];
+    uint32_t s0[K], s1[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      w[k][0] = w[k][1] = w[k][2] = w[k][3] = 0;
+      if (half == 0 || pp[k] >= 128) ld_sector_na(lines + 4 * (uint64_t)jj[k] + 2 * half, w[k][0], w[k][1], w[k][2], w[k][3]);
+      // lane 0: s_A, s_C; lane 1: s_G, s_T (adjacent u64 fields of the group)
+      const uint32_t sb = jj[k] >> QD_SB_LOG, g = sb >> 3;
+      uint64_t va, vb;
+      ld_dsmem_v2u64(((g & 1u) ? base1 : base0) + (g >> 1) * 32u + 16u * half, va, vb);
+      s0[k] = qd_s_field(va, sb & 7u);
+      s1[k] = qd_s_field(vb, sb & 7u);
+    }
+    const uint64_t stride = sc.stride;
+    sc = sc_next<K, DYN>(sc, ctr);
+    sc_load_qc<K, false>(q, nullptr, sc.gb + pw, sc.stride, m, qn, cn);
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const uint64_t idx = i0 + (uint64_t)k * stride;
+      const bool right = pp[k] >= 128;
+      const int x = (int)(pp[k] & 127u);
+      const uint64_t inv = half ? 0ull : ~0ull;
+      uint32_t nl = 0, nh = 0, nt = 0;
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {
+        const uint64_t msk = prefix_mask(x, t) ^ inv;
+        const uint64_t l = ~w[k][2 * t] & msk, hh = ~w[k][2 * t + 1] & msk;   // planes store the negation
+        nl += __popcll(l);
+        nh += __popcll(hh);
+        nt += __popcll(l & hh);
+      }
+      const uint32_t len = half ? (uint32_t)x : 128u - (uint32_t)x;
+      const uint32_t packed = (len - nl - nh + nt) | ((nl - nt) << 8) | ((nh - nt) << 16) | (nt << 24);
+      const uint32_t other = __shfl_xor_sync(0xffffffffu, packed, 1);
+      const uint32_t dgt = __shfl_xor_sync(0xffffffffu, (uint32_t)w[k][1], 1);
+      const uint32_t cnt = (right == (half == 1)) ? packed : other;
+      const uint32_t dl = half ? dgt : (uint32_t)w[k][0];
+      const uint32_t c0 = (cnt >> (16 * half)) & 0xffu, c1 = (cnt >> (16 * half + 8)) & 0xffu;
+      const uint64_t b0 = ((uint64_t)s0[k] << QD_SHIFT) + (dl & 0xffffu);
+      const uint64_t b1 = ((uint64_t)s1[k] << QD_SHIFT) + (dl >> 16);
+      const uint64_t r0 = right ? b0 + c0 : b0 - c0, r1 = right ? b1 + c1 : b1 - c1;
+      if (idx < m) asm volatile("st.global.L1::no_allocate.v2.u64 [%0], {%1,%2};" ::"l"(out4 + 4 * idx + 2 * half),
+                                "l"(r0), "l"(r1) : "memory");
+    }
+  }
+  cluster_barrier();
+}
+
+// ------------------------------------------------------------------ launchers
+
+extern int g_rank_k;
+extern int g_index64;
+extern int g_rank_smem;
+extern int g_rank_pair;
+
+// grid: as many 2-CTA clusters as fit at once (one CTA per SM); cached per (kernel, smem, device).
+// The kernel's dynamic shared-memory limit only ever grows (a later, smaller table must not lower
+// it below what a cached larger launch needs).
+template <typename Kern>
+static unsigned sc_grid(Kern kern, int threads, size_t smem, int device, int sms) {
+  static std::mutex mu;
+  static std::map<std::tuple<const void*, size_t, int>, unsigned> cache;
+  static std::map<std::pair<const void*, int>, size_t> limit;
+  std::lock_guard<std::mutex> g(mu);
+  size_t& lim = limit[std::make_pair((const void*)kern, device)];
+  if (smem > lim) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    lim = smem;
+  }
+  const auto key = std::make_tuple((const void*)kern, smem, device);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(sms & ~1));
+  cfg.blockDim = dim3((unsigned)threads);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute attr;
+  attr.id = cudaLaunchAttributeClusterDimension;
+  attr.val.clusterDim.x = 2; attr.val.clusterDim.y = 1; attr.val.clusterDim.z = 1;
+  cfg.attrs = &attr;
+  cfg.numAttrs = 1;
+  int clusters = 0;
+  if (cudaOccupancyMaxActiveClusters(&clusters, kern, &cfg) != cudaSuccess || clusters <= 0) {
+    cudaGetLastError();
+    clusters = sms / 2;
+  }
+  return cache[key] = 2u * (unsigned)clusters;
+}
+
+// Co-resident 2-CTA clusters of the BiRank rank kernel at this handle's table size (diagnostics).
+int super_pack_clusters(const qr_index* h) {
+  if (!h->spack) return 0;
+  auto kern = k_bi_rank2c<4, 1024, false, 2>;
+  return (int)(sc_grid(kern, 1024, super_pack_cta_bytes(h), h->device, h->sm_count) / 2);
+}
+
+// Whether a launch of m queries takes the shared-memory path (g_rank_smem: 0 never, 1 when it
+// pays — large batches, where the table preload is amortised —, 2 whenever the table exists).
+bool use_super_pack(const qr_index* h, uint64_t m) {
+  if (!h->spack || g_index64 || !g_rank_pair || g_rank_smem == 0) return false;
+  if (g_rank_smem == 2) return true;
+  return m >= (1ull << 22);
+}
+
+extern int g_rank_dyn;
+extern int g_rank_smem_k;
+
+extern int g_rank_smem_clusters;
+
+template <typename Kern, typename... Args>
+static void sc_go(Kern kern, int threads, const qr_index* h, size_t smem, cudaStream_t st, Args... args) {
+  unsigned grid = sc_grid(kern, threads, smem, h->device, h->sm_count);
+  if (g_rank_smem_clusters > 0) grid = 2u * (unsigned)g_rank_smem_clusters;
+  kern<<<grid, threads, smem, st>>>(args...);
+}
+
+// (K, threads per CTA): in-flight queries per SM = threads / 2 * K; registers per thread are
+// capped at 65536 / threads by the one-CTA-per-SM launch bound.
+template <int K, int T>
+static void sc_launch_kt(const qr_index* h, const uint64_t* q, const uint8_t* c, uint64_t* out, uint64_t m, int what,
+                         unsigned long long* ctr, bool dyn, cudaStream_t st) {
+  const size_t smem = super_pack_cta_bytes(h);
+  const uint64_t hw = h->spack_half * (h->sigma == 2 ? 1 : 4);     // u64 words per CTA
+  const uint64_t last = h->n_lines - 1;
+  const uint4* L = h->lines;
+  const uint64_t* P = h->spack;
+  if (h->sigma == 2) {
+    if (c) {
+      if (dyn) sc_go(k_bi_rank2c<K, T, true, 2>, T, h, smem, st, L, P, hw, q, c, out, m, last, ctr);
+      else     sc_go(k_bi_rank2c<K, T, true, 0>, T, h, smem, st, L, P, hw, q, c, out, m, last, ctr);
+    } else if (what == 3) {
+      if (dyn) sc_go(k_bi_rank2c<K, T, false, 3>, T, h, smem, st, L, P, hw, q, c, out, m, last, ctr);
+      else     sc_go(k_bi_rank2c<K, T, false, 1>, T, h, smem, st, L, P, hw, q, c, out, m, last, ctr);
+    } else {
+      if (dyn) sc_go(k_bi_rank2c<K, T, false, 2>, T, h, smem, st, L, P, hw, q, c, out, m, last, ctr);
+      else     sc_go(k_bi_rank2c<K, T, false, 0>, T, h, smem, st, L, P, hw, q, c, out, m, last, ctr);
+    }
+  } else if (what == 0) {
+    if (dyn) sc_go(k_qd_rank2c<K, T, true>, T, h, smem, st, L, P, hw, q, c, out, m, last, ctr);
+    else     sc_go(k_qd_rank2c<K, T, false>, T, h, smem, st, L, P, hw, q, c, out, m, last, ctr);
+  } else {
+    if (dyn) sc_go(k_qd_all4_2c<K, T, true>, T, h, smem, st, L, P, hw, q, out, m, last, ctr);
+    else     sc_go(k_qd_all4_2c<K, T, false>, T, h, smem, st, L, P, hw, q, out, m, last, ctr);
+  }
+}
+
+// what: 0 = rank (sigma 2 or 4), 1 = rank_4 (sigma 4), 3 = BiRank gather ceiling of this kernel shape
+// Work counters of the dynamic order.  A per-device ring of counters, each with the event of its
+// last use: a launch takes the next slot, makes its stream wait for that event (so a slot is never
+// shared by two launches in flight, whatever streams they run on), zeroes it stream-ordered and
+// records the event again after the kernel.  No allocation per launch: cudaMallocAsync /
+// cudaFreeAsync on the staged path's streams added cross-stream dependencies (e2e 5.98 -> 2.64 Gq/s).
+constexpr int CTR_SLOTS = 64;
+struct CtrRing {
+  std::mutex mu;
+  unsigned long long* d = nullptr;
+  cudaEvent_t ev[CTR_SLOTS] = {};
+  uint32_t next = 0;
+};
+
+static CtrRing* ctr_ring(int device) {
+  static std::mutex mu;
+  static std::map<int, CtrRing*> rings;
+  std::lock_guard<std::mutex> g(mu);
+  CtrRing*& r = rings[device];
+  if (!r) {
+    CtrRing* n = new CtrRing();
+    if (cudaMalloc((void**)&n->d, CTR_SLOTS * 128) != cudaSuccess) { delete n; return nullptr; }
+    for (int i = 0; i < CTR_SLOTS; ++i)
+      if (cudaEventCreateWithFlags(&n->ev[i], cudaEventDisableTiming) != cudaSuccess) { delete n; return nullptr; }
+    r = n;
+  }
+  return r;
+}
+
+cudaError_t launch_super_pack_rank(const qr_index* h, const uint64_t* q, const uint8_t* c, uint64_t* out, uint64_t m,
+                                   int what, cudaStream_t st) {
+  if (m == 0) return cudaSuccess;
+  const bool dyn = g_rank_dyn != 0;
+  CtrRing* ring = nullptr;
+  if (dyn && !(ring = ctr_ring(h->device))) return cudaErrorMemoryAllocation;
+  // the ring lock spans slot choice, wait, zeroing, launch and event record (host-side only)
+  std::unique_lock<std::mutex> lk;
+  if (ring) lk = std::unique_lock<std::mutex>(ring->mu);
+  unsigned long long* ctr = nullptr;
+  uint32_t slot = 0;
+  cudaError_t e;
+  if (ring) {
+    slot = ring->next++ % CTR_SLOTS;
+    ctr = ring->d + 16 * slot;                       // one 128-B line per counter
+    if ((e = cudaStreamWaitEvent(st, ring->ev[slot], 0))) return e;
+    if ((e = cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), st))) return e;
+  }
+  // default K (measured, profiles/r01_smem_probe_k.jsonl): BiRank 4 (fits 64 registers), QuadRank 2
+  // (K = 4 spills at the 64-register cap of 1024-thread CTAs)
+  const int k = g_rank_smem_k ? g_rank_smem_k : (h->sigma == 2 ? 4 : 2);
+  switch (k) {
+    case 1: sc_launch_kt<1, 1024>(h, q, c, out, m, what, ctr, dyn, st); break;
+    case 2: sc_launch_kt<2, 1024>(h, q, c, out, m, what, ctr, dyn, st); break;
+    case 8: sc_launch_kt<8, 512>(h, q, c, out, m, what, ctr, dyn, st); break;
+    case 6: sc_launch_kt<6, 768>(h, q, c, out, m, what, ctr, dyn, st); break;
+    default: sc_launch_kt<4, 1024>(h, q, c, out, m, what, ctr, dyn, st); break;
+  }
+  e = cudaGetLastError();
+  if (ring) {
+    cudaError_t e2 = cudaEventRecord(ring->ev[slot], st);
+    if (!e) e = e2;
+  }
+  return e;
+}
+
+}  // namespace qr

@@ -1,0 +1,283 @@
+"""GPU parity of the cluster shared-memory rank kernels (sbcache.cu) against the CPU oracle.
+
+These kernels read the superblock words s_i / s_{i,c} from a
+lossless re-encoding held in the shared memory of a 2-CTA cluster (6 superblocks per u64 for
+BiRank16, 8 per u64 and symbol for QuadRank16).  The cases below put queries on every
+superblock boundary of texts whose superblock counts straddle the group size (6 / 8) and the
+CTA split (odd / even group counts), and use the texts that make the per-superblock increments
+maximal (all-ones: +31 per BiRank superblock; a single repeated symbol: +7 per QuadRank
+superblock), so every field of the encoding reaches its largest value.  Outputs must be
+bit-identical to the oracle and to the global-memory kernels.
+"""
+import numpy as np
+import pytest
+
+import gen
+import oracle
+import paper_2602_04103_b200 as qr
+from _util import B, B4, S, S4, boundary_queries, to_dev, to_host
+
+pytestmark = pytest.mark.gpu
+
+SB_COUNTS = [1, 2, 5, 6, 7, 11, 12, 13, 17, 24, 25, 61]
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+@pytest.fixture
+def smem_mode():
+    yield
+    qr.qr_set_tuning("rank_smem", 1)
+    qr.qr_set_tuning("rank_smem_k", 0)
+    qr.qr_set_tuning("rank_dyn", 1)
+    qr.qr_set_tuning("rank_smem_clusters", 0)
+
+
+def _rank(h, q, c, dev, mode):
+    torch = _torch()
+    qr.qr_set_tuning("rank_smem", mode)
+    dq = to_dev(q, dev)
+    out = torch.empty_like(dq)
+    qr.qr_rank(h, dq, None if c is None else to_dev(c, dev), out)
+    torch.cuda.synchronize()
+    return to_host(out)
+
+
+def _rank4(h, q, dev, mode):
+    torch = _torch()
+    qr.qr_set_tuning("rank_smem", mode)
+    dq = to_dev(q, dev)
+    out = torch.empty((q.size, 4), dtype=torch.uint64, device=dev)
+    qr.qr_rank_all4(h, dq, out)
+    torch.cuda.synchronize()
+    return to_host(out)
+
+
+def _bits(kind, n, seed):
+    if kind == "ones":
+        return np.full(max(1, (n + 63) // 64), np.uint64(0xFFFFFFFFFFFFFFFF))
+    return gen.bits(seed, n, kind)
+
+
+@pytest.mark.parametrize("k", SB_COUNTS)
+@pytest.mark.parametrize("kind", [0.5, "ones", 0.01])
+def test_birank_smem_parity(cuda, smem_mode, k, kind):
+    for n in (k * S - 1, k * S, k * S + 1 + 977 * k):
+        w = _bits(kind, n, 300 + k)
+        h = qr.qr_birank_build(w, n)
+        L = n // B + 1
+        groups = ((L - 1) // 128 + 1 + 5) // 6
+        assert qr.qr_super_cache_bytes(h) == 8 * (((groups + 1) // 2 + 1) & ~1)
+        q = np.concatenate([boundary_queries(n, B, S, 240, limit=4000), gen.queries(11 + k, n, 50000)])
+        ora = oracle.BitsOracle(w, n)
+        got = _rank(h, q, None, cuda, 2)
+        ref = ora.rank(q)
+        bad = np.nonzero(got != ref)[0]
+        assert bad.size == 0, f"n={n} {kind}: {bad.size} mismatches, q={q[bad[:4]]} got={got[bad[:4]]} ref={ref[bad[:4]]}"
+        assert np.array_equal(got, _rank(h, q, None, cuda, 0))
+        c = (gen.queries(5, 1, q.size, with_c=True)[1] & 1).astype(np.uint8)
+        assert np.array_equal(_rank(h, q, c, cuda, 2), ora.rank(q, c))
+
+
+@pytest.mark.parametrize("k", SB_COUNTS)
+@pytest.mark.parametrize("kind", ["iid", "G", "T"])
+def test_quadrank_smem_parity(cuda, smem_mode, k, kind):
+    for n in (k * S4 - 1, k * S4 + 1 + 501 * k):
+        if kind == "iid":
+            t = gen.dna(400 + k, n)
+        else:
+            word = {"G": 0xAAAAAAAAAAAAAAAA, "T": 0xFFFFFFFFFFFFFFFF}[kind]
+            t = np.full(max(1, (n + 31) // 32), np.uint64(word))
+        h = qr.qr_quadrank_build(t, n)
+        L = n // B4 + 1
+        groups = ((L - 1) // 256 + 1 + 7) // 8
+        assert qr.qr_super_cache_bytes(h) == 32 * ((groups + 1) // 2)
+        q, c = gen.queries(21 + k, n, 40000, with_c=True)
+        bq = boundary_queries(n, B4, S4, 96, limit=4000)
+        q = np.concatenate([q, bq, bq, bq, bq])
+        c = np.concatenate([c, np.repeat(np.arange(4, dtype=np.uint8), bq.size)])
+        ora = oracle.DnaOracle(t, n)
+        got = _rank(h, q, c, cuda, 2)
+        ref = ora.rank(q, c)
+        bad = np.nonzero(got != ref)[0]
+        assert bad.size == 0, f"n={n} {kind}: {bad.size} mismatches, q={q[bad[:4]]} c={c[bad[:4]]}"
+        assert np.array_equal(got, _rank(h, q, c, cuda, 0))
+        g4 = _rank4(h, q, cuda, 2)
+        assert np.array_equal(g4, ora.rank_all4(q))
+        assert np.array_equal(g4, _rank4(h, q, cuda, 0))
+
+
+@pytest.mark.parametrize("dyn", [0, 1])
+@pytest.mark.parametrize("rank_k", [0, 1, 2, 4, 6, 8])
+def test_smem_kernels_rank_k(cuda, smem_mode, rank_k, dyn):
+    """Every (K, threads) instantiation of the cluster kernels, static and dynamic work order
+    (results never depend on them)."""
+    qr.qr_set_tuning("rank_smem_k", rank_k)
+    qr.qr_set_tuning("rank_dyn", dyn)
+    n = 9 * S + 4321
+    w = gen.bits(77, n)
+    q = np.concatenate([gen.queries(78, n, 123457), boundary_queries(n, B, S, 240)])
+    h = qr.qr_birank_build(w, n)
+    assert np.array_equal(_rank(h, q, None, cuda, 2), oracle.BitsOracle(w, n).rank(q))
+    n4 = 13 * S4 + 99
+    t = gen.dna(79, n4)
+    q4, c4 = gen.queries(80, n4, 123457, with_c=True)
+    h4 = qr.qr_quadrank_build(t, n4)
+    ora4 = oracle.DnaOracle(t, n4)
+    assert np.array_equal(_rank(h4, q4, c4, cuda, 2), ora4.rank(q4, c4))
+    assert np.array_equal(_rank4(h4, q4, cuda, 2), ora4.rank_all4(q4))
+
+
+def test_smem_auto_mode_large_batch_and_clone_import(cuda, smem_mode):
+    """Default mode (1) takes the cluster path at m >= 2^22: checked on a 2^27-bit text, also on
+    handles re-created by qr_import_layout and qr_clone_to_device (they rebuild the table)."""
+    torch = _torch()
+    n = (1 << 27) + 12345
+    w = gen.bits(90, n)
+    h = qr.qr_birank_build(w, n)
+    m = (1 << 22) + 777
+    q = gen.queries(91, n, m)
+    ref = oracle.BitsOracle(w, n).rank(q)
+    qr.qr_set_tuning("rank_smem", 1)
+    dq = to_dev(q, cuda)
+    lines, sup = qr.qr_export_layout(h)
+    for hh in (h, qr.qr_import_layout(lines, sup, n, qr.QR_LAYOUT_BIRANK16), qr.qr_clone_to_device(h, 0)):
+        assert qr.qr_super_cache_bytes(hh) > 0
+        out = torch.empty_like(dq)
+        qr.qr_rank(hh, dq, None, out)
+        torch.cuda.synchronize()
+        assert np.array_equal(to_host(out), ref)
+
+
+def test_no_cache_for_variants_and_fallback(cuda, smem_mode):
+    """Layouts without an L1 array have no table; rank_smem = 2 then uses the global kernels."""
+    n = 5 * S + 3
+    w = gen.bits(93, n)
+    hv = qr.qr_build(w, n, qr.QR_LAYOUT_BIRANK64X2)
+    assert qr.qr_super_cache_bytes(hv) == 0
+    q = gen.queries(94, n, 10000)
+    assert np.array_equal(_rank(hv, q, None, cuda, 2), oracle.BitsOracle(w, n).rank(q))
+
+
+def test_cache_capacity_limit(cuda, smem_mode):
+    """The table is built iff half of it fits one CTA's opt-in shared memory (minus 1 KiB); at
+    n = 2^34 (configs[1]) it must exist.  Beyond the limit rank still matches the oracle."""
+    torch = _torch()
+    optin = getattr(torch.cuda.get_device_properties(0), "shared_memory_per_block_optin", 232448)
+
+    def expect(n):
+        L = n // B + 1
+        groups = ((L - 1) // 128 + 1 + 5) // 6
+        half = 8 * (((groups + 1) // 2 + 1) & ~1)
+        return half if half + 1024 <= optin else 0
+
+    for n in ((1 << 34), (1 << 34) + (1 << 32)):
+        bits = torch.empty((n + 63) // 64, dtype=torch.uint64, device=cuda)
+        gen.bits_dev(95, n, 0.5, bits)
+        h = qr.qr_birank_build(bits, n)
+        del bits
+        assert qr.qr_super_cache_bytes(h) == expect(n)
+        if n == (1 << 34):
+            assert expect(n) > 0
+        m = 1 << 22
+        q = torch.empty(m, dtype=torch.uint64, device=cuda)
+        gen.queries_dev(96, n, m, q)
+        out = torch.empty_like(q)
+        qr.qr_set_tuning("rank_smem", 2)
+        qr.qr_rank(h, q, None, out)
+        qr.qr_set_tuning("rank_smem", 0)
+        out0 = torch.empty_like(q)
+        qr.qr_rank(h, q, None, out0)
+        torch.cuda.synchronize()
+        assert torch.equal(out, out0)
+        h.free()
+        del q, out, out0
+        torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("clusters", [1, 3, 200])
+def test_smem_cluster_count_does_not_change_results(cuda, smem_mode, clusters):
+    """Fewer clusters than SMs (1, 3) or more than fit at once (200: a second wave) — both work
+    orders must still cover every query exactly once."""
+    qr.qr_set_tuning("rank_smem_clusters", clusters)
+    n = 7 * S + 99
+    w = gen.bits(81, n)
+    q = gen.queries(82, n, 300001)
+    h = qr.qr_birank_build(w, n)
+    ref = oracle.BitsOracle(w, n).rank(q)
+    for dyn in (0, 1):
+        qr.qr_set_tuning("rank_dyn", dyn)
+        assert np.array_equal(_rank(h, q, None, cuda, 2), ref)
+    assert qr.qr_super_cache_clusters(h) > 0
+
+
+def test_smem_concurrent_streams_and_staged_host_path(cuda, smem_mode):
+    """The dynamic work order's counters are per launch (an event-guarded ring): launches of the
+    cluster kernels on several streams at once, and the staged host-pointer path (chunks on the
+    library's internal streams), all give the oracle's answers."""
+    torch = _torch()
+    qr.qr_set_tuning("rank_smem", 2)
+    n = 11 * S + 321
+    w = gen.bits(61, n)
+    h = qr.qr_birank_build(w, n)
+    q = gen.queries(62, n, 300000)
+    ref = oracle.BitsOracle(w, n).rank(q)
+    dq = to_dev(q, cuda)
+    streams = [torch.cuda.Stream() for _ in range(6)]
+    outs = [torch.empty_like(dq) for _ in streams]
+    torch.cuda.synchronize()
+    for rep in range(12):                      # more launches than streams: slots are reused
+        for s, o in zip(streams, outs):
+            with torch.cuda.stream(s):
+                qr.qr_rank(h, dq, None, o, stream=s)
+    torch.cuda.synchronize()
+    for o in outs:
+        assert np.array_equal(to_host(o), ref)
+    qr.qr_set_tuning("stage_chunk", 65536)     # 5 chunks over the internal streams
+    try:
+        host_out = np.zeros(q.size, np.uint64)
+        qr.qr_rank(h, q, None, host_out)
+        qr.qr_sync()
+        assert np.array_equal(host_out, ref)
+        n4 = 5 * S4 + 77
+        t = gen.dna(63, n4)
+        h4 = qr.qr_quadrank_build(t, n4)
+        q4, c4 = gen.queries(64, n4, 300000, with_c=True)
+        o4 = np.zeros((q4.size, 4), np.uint64)
+        qr.qr_rank_all4(h4, q4, o4)
+        o1 = np.zeros(q4.size, np.uint64)
+        qr.qr_rank(h4, q4, c4, o1)
+        qr.qr_sync()
+        ora4 = oracle.DnaOracle(t, n4)
+        assert np.array_equal(o4, ora4.rank_all4(q4))
+        assert np.array_equal(o1, ora4.rank(q4, c4))
+    finally:
+        qr.qr_set_tuning("stage_chunk", 1 << 23)
+
+
+def test_smem_limit_never_lowered(cuda, smem_mode):
+    """Regression: a launch with a small table must not lower the kernel's shared-memory limit
+    below what an earlier (cached) larger table needs."""
+    torch = _torch()
+    qr.qr_set_tuning("rank_smem", 2)
+    hs = []
+    for n in ((1 << 32) + 5, 3 * S + 1, (1 << 32) + 5):
+        bits = torch.empty((n + 63) // 64 + 1, dtype=torch.uint64, device=cuda)
+        gen.bits_dev(70, n, 0.5, bits)
+        h = qr.qr_birank_build(bits, n)
+        m = 100000
+        q = torch.empty(m, dtype=torch.uint64, device=cuda)
+        gen.queries_dev(71, n, m, q)
+        out = torch.empty_like(q)
+        qr.qr_rank(h, q, None, out)
+        qr.qr_set_tuning("rank_smem", 0)
+        out0 = torch.empty_like(q)
+        qr.qr_rank(h, q, None, out0)
+        qr.qr_set_tuning("rank_smem", 2)
+        torch.cuda.synchronize()
+        assert torch.equal(out, out0)
+        hs.append(h)
