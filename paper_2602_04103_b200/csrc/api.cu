@@ -22,6 +22,7 @@ int g_rank_k = 2;               // independent queries per lane (pair) per itera
 int g_rank_blocks_per_sm = 64;  // 256-thread CTAs per SM of the grid (several waves)
 int g_fm_blocks_per_sm = 64;    // 256-thread CTAs per SM of the FM grid (several waves)
 int g_rank_s_lane = 1;
+int g_fm_smem = 1;              // FM superblock words from shared memory: 0 off, 1 auto, 2 packed table whenever it fits
 int g_fm_lean = 0;              // FM step flavour: 0 auto (by L2 residency), 1 de-duplicating, 2 lean
 int g_index64 = 0;              // 1: force the 64-bit line-index path (tests the n >= 2^36/2^37 code on small n)          // lane of a pair that loads the superblock word
 int g_rank_smem = 1;            // superblock words from cluster shared memory: 0 never, 1 large batches, 2 always
@@ -312,6 +313,9 @@ QR_EXPORT qr_status qr_set_tuning(const char* key, int64_t value) {
   } else if (!strcmp(key, "rank_dyn")) {
     if (value != 0 && value != 1) return fail(QR_EINVAL, "rank_dyn must be 0 or 1");
     g_rank_dyn = (int)value;
+  } else if (!strcmp(key, "fm_smem")) {
+    if (value < 0 || value > 2) return fail(QR_EINVAL, "fm_smem must be 0 (off), 1 (auto) or 2 (packed)");
+    g_fm_smem = (int)value;
   } else if (!strcmp(key, "fm_step")) {
     if (value < 0 || value > 2) return fail(QR_EINVAL, "fm_step must be 0 (auto), 1 or 2");
     g_fm_lean = (int)value;

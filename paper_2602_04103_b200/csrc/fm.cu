@@ -28,7 +28,36 @@ struct FmParams {
   uint64_t last_line;
   uint32_t C[4];        // host copy; the kernels read C from the table tail (Ct) with one load
   const uint32_t* Ct;   // = (const uint32_t*)(kmer + 4^K): C[0..3] stored after the k-mer table
+  const uint64_t* spack;  // packed superblock table (sbcache.cu encoding, 2 parts), or null
+  uint32_t spack_half;    // groups per part
+  uint32_t n_super;
 };
+
+// Superblock word s_{sb,c}.  SMS 0: global memory (an L2 request per read);
+// SMS 1: the raw u32 x 4 array copied into shared memory at CTA start; SMS 2: the packed table
+// (sbcache.cu: 8 superblocks per u64 per symbol) copied into shared memory.  The FM step reads
+// s twice (lo and hi), so 1 and 2 remove up to two L2 requests / L1 wavefront sets per step.
+template <int SMS>
+__device__ __forceinline__ uint32_t fm_super(const FmParams& F, uint32_t sb, uint32_t c) {
+  if (SMS == 0) return __ldg(F.super + 4 * sb + c);
+  extern __shared__ uint64_t fm_smem[];
+  if (SMS == 1) return reinterpret_cast<const uint32_t*>(fm_smem)[4 * sb + c];
+  const uint32_t g = sb >> 3, k = sb & 7u;
+  const uint64_t v = fm_smem[4 * ((g & 1u) * F.spack_half + (g >> 1)) + c];
+  const uint32_t lo = (uint32_t)v & 0x3fffffu;
+  return k ? lo + ((uint32_t)(v >> (16u + 6u * k)) & 0x3fu) : lo;
+}
+
+template <int SMS>
+__device__ __forceinline__ void fm_preload_super(const FmParams& F) {
+  if (SMS == 0) return;
+  extern __shared__ uint64_t fm_smem[];
+  const uint4* src = reinterpret_cast<const uint4*>(SMS == 1 ? reinterpret_cast<const uint64_t*>(F.super) : F.spack);
+  const uint32_t n16 = SMS == 1 ? F.n_super : 4u * F.spack_half;       // 16-B units
+  uint4* dst = reinterpret_cast<uint4*>(fm_smem);
+  for (uint32_t i = threadIdx.x; i < n16; i += blockDim.x) dst[i] = __ldg(src + i);
+  __syncthreads();
+}
 
 __device__ __forceinline__ uint32_t text_char(const uint64_t* t, uint64_t i) {
   return (uint32_t)(t[i >> 5] >> (2 * (i & 31))) & 3u;
@@ -196,6 +225,7 @@ __global__ void k_sym_counts(const uint64_t* __restrict__ text, uint64_t n, unsi
 // often share a line ("cache lines are automatically reused"); then the line's
 // sectors and the superblock word are loaded once and reused from registers, which halves the
 // L1 wavefronts of a step when the structure is L2-resident.  N < 2^32: u32 arithmetic.
+template <int SMS = 0>
 __device__ __forceinline__ void fm_step(const FmParams& F, uint32_t c, uint32_t& lo, uint32_t& hi, uint32_t& lines) {
   uint32_t jl = (lo >> 5) / 7u;                                  // floor(lo/224)
   uint32_t jh = (hi >> 5) / 7u;
@@ -211,9 +241,9 @@ __device__ __forceinline__ void fm_step(const FmParams& F, uint32_t c, uint32_t&
   if (rl_) ld_sector(Ll + 2, bl[0], bl[1], bl[2], bl[3]);
   if (!same) ld_sector(Lh, ah[0], ah[1], ah[2], ah[3]);
   if (rh_ && !(same && rl_)) ld_sector(Lh + 2, bh[0], bh[1], bh[2], bh[3]);
-  const uint32_t sl = __ldg(F.super + 4 * (jl >> QD_SB_LOG) + c);
+  const uint32_t sl = fm_super<SMS>(F, jl >> QD_SB_LOG, c);
   const bool same_sb = (jl >> QD_SB_LOG) == (jh >> QD_SB_LOG);
-  uint32_t sh = same_sb ? sl : __ldg(F.super + 4 * (jh >> QD_SB_LOG) + c);
+  uint32_t sh = same_sb ? sl : fm_super<SMS>(F, jh >> QD_SB_LOG, c);
   if (same) {
 #pragma unroll
     for (int t = 0; t < 4; ++t) ah[t] = al[t];
@@ -301,14 +331,15 @@ __device__ __forceinline__ uint32_t pick4(uint4 v, uint32_t c) {
   return (c & 2u) ? ((c & 1u) ? v.w : v.z) : ((c & 1u) ? v.y : v.x);
 }
 
+template <int SMS>
 __device__ __forceinline__ void fm_step_lean(const FmParams& F, uint4 C4, uint32_t c, uint32_t& lo, uint32_t& hi,
                                              uint32_t& lines) {
   const uint64_t cl = 0ull - (uint64_t)(c & 1u), ch = 0ull - (uint64_t)(c >> 1);
   const uint32_t jl = (lo >> 5) / 7u, jh = (hi >> 5) / 7u;   // lo, hi <= N: j <= last_line
   const uint32_t pl = 32u + lo - jl * (uint32_t)QD_B, ph = 32u + hi - jh * (uint32_t)QD_B;
   // one superblock-word load when both ranks fall in the same superblock (nearly always)
-  const uint32_t sl = __ldg(F.super + 4 * (jl >> QD_SB_LOG) + c);
-  const uint32_t sh = (jl >> QD_SB_LOG) == (jh >> QD_SB_LOG) ? sl : __ldg(F.super + 4 * (jh >> QD_SB_LOG) + c);
+  const uint32_t sl = fm_super<SMS>(F, jl >> QD_SB_LOG, c);
+  const uint32_t sh = (jl >> QD_SB_LOG) == (jh >> QD_SB_LOG) ? sl : fm_super<SMS>(F, jh >> QD_SB_LOG, c);
   uint32_t rl = fm_rank_lean(F, jl, pl, c, cl, ch, sl);
   uint32_t rh = fm_rank_lean(F, jh, ph, c, cl, ch, sh);
   lines = jl == jh ? 1u : 2u;
@@ -367,12 +398,13 @@ __device__ __forceinline__ uint32_t kmer_key_rc(int K, PatWindow& P, const uint8
 
 // 4 resident CTAs (64 registers): capping registers for 6 or 8 CTAs/SM spills and runs 2-4x
 // slower on configs[3]/[4] (profiles/r01_fm_occupancy_sweep.jsonl).
-template <bool FIXED, bool WORK, int STRANDS, bool LEAN>
+template <bool FIXED, bool WORK, int STRANDS, bool LEAN, int SMS>
 __global__ void __launch_bounds__(256, 4) k_fm_count(FmParams F, const uint8_t* __restrict__ pat,
                                                      const uint64_t* __restrict__ offs, const uint32_t* __restrict__ lens,
                                                      uint32_t fixed_len, uint32_t* __restrict__ out,
                                                      uint32_t* __restrict__ out_rc, uint64_t m,
                                                      unsigned long long* __restrict__ work) {
+  fm_preload_super<SMS>(F);
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   const uint64_t ntask = m * STRANDS;
   const uint4 C4 = __ldg(reinterpret_cast<const uint4*>(F.Ct));
@@ -402,8 +434,8 @@ __global__ void __launch_bounds__(256, 4) k_fm_count(FmParams F, const uint8_t* 
     if (k >= 0 && lo < hi) {                             // one backward step (LF mapping)
       const uint32_t c = rc ? 3u - P.at((int64_t)len - 1 - k) : P.at(k);
       uint32_t nl;
-      if (LEAN) fm_step_lean(F, C4, c, lo, hi, nl);
-      else      fm_step(F, c, lo, hi, nl);
+      if (LEAN) fm_step_lean<SMS>(F, C4, c, lo, hi, nl);
+      else      fm_step<SMS>(F, c, lo, hi, nl);
       --k;
       if (WORK) { n_steps += 1; n_lines += nl; }
     }
@@ -541,6 +573,9 @@ static FmParams params_of(const qr_fm* fm) {
   F.last_line = fm->bwt->n_lines - 1;
   for (int c = 0; c < 4; ++c) F.C[c] = (uint32_t)fm->C[c];
   F.Ct = reinterpret_cast<const uint32_t*>(fm->kmer + kmer_c_offset(fm->kmer_k));
+  F.spack = fm->bwt->spack;
+  F.spack_half = (uint32_t)fm->bwt->spack_half;
+  F.n_super = (uint32_t)fm->bwt->n_super;
   return F;
 }
 
@@ -559,16 +594,56 @@ static bool use_lean(const qr_fm* fm) {
   return fm->bwt->n_lines * 64 <= (uint64_t)l2_bytes(fm->bwt->device) / 2;
 }
 
+extern int g_fm_smem;
+
+// Shared-memory superblock mode of the count kernel: the raw array when it fits the per-CTA
+// budget that keeps 4 CTAs per SM (configs[3]: 18.7 KB), else the packed table if it does, else
+// global memory (knob "fm_smem": 0 off, 1 auto (default), 2 the packed table whenever it fits a CTA).
+constexpr uint64_t FM_SMEM_BUDGET = 48 * 1024;
+static int fm_smem_mode(const qr_fm* fm, size_t* bytes) {
+  const qr_index* b = fm->bwt;
+  const uint64_t raw = b->n_super * 16, packed = super_pack_cta_bytes(b) * 2;
+  *bytes = 0;
+  if (g_fm_smem == 0) return 0;
+  if (g_fm_smem == 1) {
+    if (raw <= FM_SMEM_BUDGET) { *bytes = raw; return 1; }
+    if (b->spack && packed <= FM_SMEM_BUDGET) { *bytes = packed; return 2; }
+    return 0;
+  }
+  if (b->spack && packed + 1024 <= 227 * 1024) { *bytes = packed; return 2; }
+  return 0;
+}
+
+template <bool FIXED, bool WORK, int STRANDS, bool LEAN, int SMS>
+static void launch_fm1(unsigned g, size_t smem, cudaStream_t st, const FmParams& F, const uint8_t* pat,
+                       const uint64_t* offs, const uint32_t* lens, uint32_t fixed_len, uint32_t* out, uint32_t* out_rc,
+                       uint64_t m, unsigned long long* w) {
+  auto kern = k_fm_count<FIXED, WORK, STRANDS, LEAN, SMS>;
+  if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  kern<<<g, 256, smem, st>>>(F, pat, offs, lens, fixed_len, out, out_rc, m, w);
+}
+
+template <bool FIXED, bool WORK, int STRANDS, bool LEAN>
+static void launch_fm2(int sms_mode, unsigned g, size_t smem, cudaStream_t st, const FmParams& F, const uint8_t* pat,
+                       const uint64_t* offs, const uint32_t* lens, uint32_t fixed_len, uint32_t* out, uint32_t* out_rc,
+                       uint64_t m, unsigned long long* w) {
+  if (sms_mode == 1)      launch_fm1<FIXED, WORK, STRANDS, LEAN, 1>(g, smem, st, F, pat, offs, lens, fixed_len, out, out_rc, m, w);
+  else if (sms_mode == 2) launch_fm1<FIXED, WORK, STRANDS, LEAN, 2>(g, smem, st, F, pat, offs, lens, fixed_len, out, out_rc, m, w);
+  else                    launch_fm1<FIXED, WORK, STRANDS, LEAN, 0>(g, 0, st, F, pat, offs, lens, fixed_len, out, out_rc, m, w);
+}
+
 template <bool FIXED, bool WORK>
-static void launch_fm(bool lean, unsigned g, cudaStream_t st, const FmParams& F, const uint8_t* pat, const uint64_t* offs,
-                      const uint32_t* lens, uint32_t fixed_len, uint32_t* out, uint32_t* out_rc, uint64_t m,
-                      unsigned long long* w) {
+static void launch_fm(const qr_fm* fm, bool lean, unsigned g, cudaStream_t st, const FmParams& F, const uint8_t* pat,
+                      const uint64_t* offs, const uint32_t* lens, uint32_t fixed_len, uint32_t* out, uint32_t* out_rc,
+                      uint64_t m, unsigned long long* w) {
+  size_t smem = 0;
+  const int sm = fm_smem_mode(fm, &smem);
   if (lean) {
-    if (out_rc) k_fm_count<FIXED, WORK, 2, true><<<g, 256, 0, st>>>(F, pat, offs, lens, fixed_len, out, out_rc, m, w);
-    else        k_fm_count<FIXED, WORK, 1, true><<<g, 256, 0, st>>>(F, pat, offs, lens, fixed_len, out, out_rc, m, w);
+    if (out_rc) launch_fm2<FIXED, WORK, 2, true>(sm, g, smem, st, F, pat, offs, lens, fixed_len, out, out_rc, m, w);
+    else        launch_fm2<FIXED, WORK, 1, true>(sm, g, smem, st, F, pat, offs, lens, fixed_len, out, out_rc, m, w);
   } else {
-    if (out_rc) k_fm_count<FIXED, WORK, 2, false><<<g, 256, 0, st>>>(F, pat, offs, lens, fixed_len, out, out_rc, m, w);
-    else        k_fm_count<FIXED, WORK, 1, false><<<g, 256, 0, st>>>(F, pat, offs, lens, fixed_len, out, out_rc, m, w);
+    if (out_rc) launch_fm2<FIXED, WORK, 2, false>(sm, g, smem, st, F, pat, offs, lens, fixed_len, out, out_rc, m, w);
+    else        launch_fm2<FIXED, WORK, 1, false>(sm, g, smem, st, F, pat, offs, lens, fixed_len, out, out_rc, m, w);
   }
 }
 
@@ -583,8 +658,8 @@ qr_status fm_count_device(const qr_fm* fm, const uint8_t* pat, const uint32_t* l
   cudaError_t e;
   if (!lengths) {
     if (approx) k_fm_approx1<true><<<g, 256, 0, st>>>(F, pat, nullptr, nullptr, fixed_len, out, m);
-    else if (work) launch_fm<true, true>(use_lean(fm), g, st, F, pat, nullptr, nullptr, fixed_len, out, out_rc, m, w);
-    else      launch_fm<true, false>(use_lean(fm), g, st, F, pat, nullptr, nullptr, fixed_len, out, out_rc, m, w);
+    else if (work) launch_fm<true, true>(fm, use_lean(fm), g, st, F, pat, nullptr, nullptr, fixed_len, out, out_rc, m, w);
+    else      launch_fm<true, false>(fm, use_lean(fm), g, st, F, pat, nullptr, nullptr, fixed_len, out, out_rc, m, w);
     if ((e = cudaGetLastError())) return cuda_fail(e, "k_fm_count");
     return QR_OK;
   }
@@ -599,8 +674,8 @@ qr_status fm_count_device(const qr_fm* fm, const uint8_t* pat, const uint32_t* l
     cudaFreeAsync(offs, st); cudaFreeAsync(tmp, st); return cuda_fail(e, "scan");
   }
   if (approx) k_fm_approx1<false><<<g, 256, 0, st>>>(F, pat, offs, lengths, 0, out, m);
-  else if (work) launch_fm<false, true>(use_lean(fm), g, st, F, pat, offs, lengths, 0, out, out_rc, m, w);
-  else      launch_fm<false, false>(use_lean(fm), g, st, F, pat, offs, lengths, 0, out, out_rc, m, w);
+  else if (work) launch_fm<false, true>(fm, use_lean(fm), g, st, F, pat, offs, lengths, 0, out, out_rc, m, w);
+  else      launch_fm<false, false>(fm, use_lean(fm), g, st, F, pat, offs, lengths, 0, out, out_rc, m, w);
   e = cudaGetLastError();
   cudaFreeAsync(offs, st);
   cudaFreeAsync(tmp, st);

@@ -350,3 +350,41 @@ def test_fm_kmer_width_does_not_change_counts(cuda, k):
         t = qr.qr_fm_export_kmer(fm)
         assert t.shape == (4 ** k, 2)
         assert int((t[:, 1].astype(np.int64) - t[:, 0]).sum()) == n - k + 1
+
+
+@pytest.mark.parametrize("step", [1, 2])
+@pytest.mark.parametrize("fm_smem", [0, 1, 2])
+def test_fm_superblock_source_does_not_change_results(cuda, fm_smem, step):
+    """The count kernel's superblock words from global memory (0), from the raw array copied to
+    shared memory (1, auto for small BWTs) or from the packed 8-per-u64 table in shared memory
+    (2): a 3*10^6-symbol text spans 53 superblocks = 7 packed groups (odd: unequal halves), so
+    every field of the packed encoding is read.  Exact + both strands, variable and fixed length."""
+    torch = _torch()
+    n = 3_000_000
+    w = gen.dna(37, n, 0)
+    sym = gen.unpack_dna(w, n)
+    ora = oracle.FmOracle(sym)
+    fm = qr.qr_fm_build(w, n)
+    pats = mixed_patterns(np.random.default_rng(7), sym, 4000)
+    cat, off, lens = oracle.pack_patterns(pats)
+    ref = ora.count(cat, off, lens)
+    L, m = 48, 6000
+    fixed = gen.patterns(10, 0, m, L, w, n)
+    ref_fixed = ora.count(fixed, np.arange(m, dtype=np.uint64) * L, np.full(m, L, np.uint32))
+    rc = np.concatenate([(3 - fixed[i * L:(i + 1) * L][::-1]).astype(np.uint8) for i in range(m)])
+    ref_rc = ora.count(rc, np.arange(m, dtype=np.uint64) * L, np.full(m, L, np.uint32))
+    qr.qr_set_tuning("fm_smem", fm_smem)
+    qr.qr_set_tuning("fm_step", step)
+    try:
+        d = torch.empty(lens.size, dtype=torch.int32, device=cuda)
+        qr.qr_fm_count(fm, to_dev(cat, cuda), to_dev(lens, cuda), 0, d, lens.size)
+        db = torch.empty(m, dtype=torch.int32, device=cuda)
+        dr = torch.empty(m, dtype=torch.int32, device=cuda)
+        qr.qr_fm_count_both(fm, to_dev(fixed, cuda), None, L, db, dr, m)
+        torch.cuda.synchronize()
+    finally:
+        qr.qr_set_tuning("fm_smem", 1)
+        qr.qr_set_tuning("fm_step", DEFAULT_FM_STEP)
+    assert np.array_equal(to_host(d).view(np.uint32), ref)
+    assert np.array_equal(to_host(db).view(np.uint32), ref_fixed)
+    assert np.array_equal(to_host(dr).view(np.uint32), ref_rc)
