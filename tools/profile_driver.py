@@ -1,5 +1,6 @@
 """One launch of each hot kernel at the bench's configs and default launch configuration, for
-ncu --set full captures (kernel order: bi_rank2, bi_gather2 x3, qd_rank2, qd_all4_2, b64_rank,
+ncu --set full captures (kernel order: bi_rank2c (BiRank16 rank, cluster shared-memory superblocks),
+bi_gather2 x3 (ceiling modes 0-2), bi_rank2c<VAR=3> (ceiling mode 3), qd_rank2c, qd_all4_2c, b64_rank,
 q64_rank, fm_count (c4, lean), fm_count (c5, de-duplicating), fm_count both strands, fm_approx1)."""
 import os
 import sys
@@ -22,7 +23,7 @@ q = torch.empty(M, dtype=torch.uint64, device=dev)
 gen.queries_dev(2, n, M, q)
 out = torch.empty_like(q)
 qr.qr_rank(h, q, None, out, M, st)
-for mode in (0, 1, 2):
+for mode in (0, 1, 2, 3):
     qr.qr_gather_ceiling(h, q, out, mode, M, st)
 torch.cuda.synchronize()
 h.free()
