@@ -113,15 +113,17 @@ qr_status qr_rank_chain(const qr_index* h, const uint64_t* q, const uint8_t* c, 
  * array of T$ on the GPU (prefix doubling over device radix sorts) unless sa_or_null gives
  * it (n+1 u32 entries, host or device), the BWT with '$' stored as A and its row spos kept
  * (lines 919-920), C[c] = 1 + #{t_i < c}, QuadRank16 over the n+1 BWT symbols, and the
- * 8-mer interval table (line 918; key = 2 bits per char, last pattern char in the low bits).
+ * k-mer interval table (line 918 uses 8-mers; the default width here depends on n, see
+ * qr_fm_build_ex; key = 2 bits per char, last pattern char in the low bits).
  * text2b: ceil(n/32) words (host or device).  Requires 1 <= n and n + 1 < 2^32. */
 qr_status qr_fm_build(const uint64_t* text2b, uint64_t n, const uint32_t* sa_or_null, int device, void* stream,
                       qr_fm** out);
 
-/* As qr_fm_build with a k-mer seed table of width kmer_k (0..12; 0 = no table, every search
- * starts from [0, n+1); qr_fm_build uses the paper's 8).  The table holds 4^kmer_k intervals
- * (8 B each: 512 KiB at 8, 8 MiB at 10, 128 MiB at 12).  Counts never depend on kmer_k
- * (S:366); wider tables skip more backward steps.  QR_EINVAL outside 0..12. */
+/* As qr_fm_build with a k-mer seed table of width kmer_k (0..14; 0 = no table, every search
+ * starts from [0, n+1)).  qr_fm_build picks the paper's 8 for n < 2^20, 10 for
+ * n < 2^24 and 12 above (on B200 the wider table replaces more backward steps
+ * by one lookup).  The table holds 4^kmer_k intervals (8 B each: 512 KiB at 8, 8 MiB at 10,
+ * 128 MiB at 12, 2 GiB at 14).  Counts never depend on kmer_k.  QR_EINVAL outside 0..14. */
 qr_status qr_fm_build_ex(const uint64_t* text2b, uint64_t n, const uint32_t* sa_or_null, int kmer_k, int device,
                          void* stream, qr_fm** out);
 

@@ -241,10 +241,10 @@ def qr_rank_all4(h: Index, q, out4, m: int | None = None, stream=None):
     return out4
 
 
-def qr_fm_build(text2b, n: int, sa=None, device: int = 0, stream=None, kmer_k: int = 8) -> Fm:
-    """qr_fm_build (kmer_k = 8, the paper's table) or qr_fm_build_ex (other widths)."""
+def qr_fm_build(text2b, n: int, sa=None, device: int = 0, stream=None, kmer_k: int | None = None) -> Fm:
+    """qr_fm_build (kmer_k None: the library's default width for n) or qr_fm_build_ex (explicit width)."""
     out = C.c_void_p()
-    if kmer_k == 8:
+    if kmer_k is None:
         _check(lib().qr_fm_build(_ptr(text2b), n, _ptr(sa), device, _stream(stream), C.byref(out)), "qr_fm_build")
     else:
         _check(lib().qr_fm_build_ex(_ptr(text2b), n, _ptr(sa), kmer_k, device, _stream(stream), C.byref(out)),

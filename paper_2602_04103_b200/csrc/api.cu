@@ -22,6 +22,7 @@ int g_rank_k = 2;               // independent queries per lane (pair) per itera
 int g_rank_blocks_per_sm = 64;  // 256-thread CTAs per SM of the grid (several waves)
 int g_fm_blocks_per_sm = 64;    // 256-thread CTAs per SM of the FM grid (several waves)
 int g_rank_s_lane = 1;
+int g_fm_dyn = 1;               // FM count: 1 = persistent grid + warp chunks from a global counter, 0 = static grid stride
 int g_fm_smem = 1;              // FM superblock words from shared memory: 0 off, 1 auto, 2 packed table whenever it fits
 int g_fm_lean = 0;              // FM step flavour: 0 auto (by L2 residency), 1 de-duplicating, 2 lean
 int g_index64 = 0;              // 1: force the 64-bit line-index path (tests the n >= 2^36/2^37 code on small n)          // lane of a pair that loads the superblock word
@@ -313,6 +314,9 @@ QR_EXPORT qr_status qr_set_tuning(const char* key, int64_t value) {
   } else if (!strcmp(key, "rank_dyn")) {
     if (value != 0 && value != 1) return fail(QR_EINVAL, "rank_dyn must be 0 or 1");
     g_rank_dyn = (int)value;
+  } else if (!strcmp(key, "fm_dyn")) {
+    if (value != 0 && value != 1) return fail(QR_EINVAL, "fm_dyn must be 0 or 1");
+    g_fm_dyn = (int)value;
   } else if (!strcmp(key, "fm_smem")) {
     if (value < 0 || value > 2) return fail(QR_EINVAL, "fm_smem must be 0 (off), 1 (auto) or 2 (packed)");
     g_fm_smem = (int)value;
@@ -499,14 +503,20 @@ QR_EXPORT qr_status qr_gather_ceiling(const qr_index* h, const uint64_t* q, uint
 QR_EXPORT qr_status qr_fm_build_ex(const uint64_t* text2b, uint64_t n, const uint32_t* sa_or_null, int kmer_k,
                                    int device, void* stream, qr_fm** out);
 
+// Default k-mer table width: the paper's 8 for small texts; on B200 wider tables replace
+// more backward steps by one lookup and HBM holds them easily: 10 (8 MiB) from n = 2^20, 12
+// (128 MiB) from n = 2^24 — configs[3] 5.61 -> 6.57 G patterns/s, configs[4] 0.94 -> 0.99
+// (profiles/r01_fm_k_probe*.jsonl).  Counts never depend on it.
+int fm_default_kmer_k(uint64_t n) { return n < (1ull << 20) ? 8 : n < (1ull << 24) ? 10 : 12; }
+
 QR_EXPORT qr_status qr_fm_build(const uint64_t* text2b, uint64_t n, const uint32_t* sa_or_null, int device,
                                 void* stream, qr_fm** out) {
-  return qr_fm_build_ex(text2b, n, sa_or_null, 8, device, stream, out);
+  return qr_fm_build_ex(text2b, n, sa_or_null, fm_default_kmer_k(n), device, stream, out);
 }
 
 QR_EXPORT qr_status qr_fm_build_ex(const uint64_t* text2b, uint64_t n, const uint32_t* sa_or_null, int kmer_k,
                                    int device, void* stream, qr_fm** out) {
-  if (kmer_k < 0 || kmer_k > 12) return fail(QR_EINVAL, "qr_fm_build_ex: kmer_k must be 0..12");
+  if (kmer_k < 0 || kmer_k > 14) return fail(QR_EINVAL, "qr_fm_build_ex: kmer_k must be 0..14");
   if (!out || !text2b) return fail(QR_EINVAL, "qr_fm_build: null pointer");
   *out = nullptr;
   if (n == 0) return fail(QR_EINVAL, "qr_fm_build: empty text");

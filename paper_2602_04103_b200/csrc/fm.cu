@@ -384,13 +384,19 @@ __device__ __forceinline__ uint32_t kmer_key8_rc(const uint8_t* first8) { return
 // through the pattern window (no read before the pattern's first byte).
 __device__ __forceinline__ uint32_t kmer_key(int K, PatWindow& P, const uint8_t* p, uint32_t len) {
   if (K == 8) return kmer_key8(p + len - 8);
+  if (K > 8 && len >= 16) {
+    // P[len-K .. len-8) are the last K-8 bytes of the 8 bytes ending at len-8 (no read before p)
+    const uint32_t hi8 = kmer_key8(p + len - 16) & ((1u << (2 * (K - 8))) - 1u);
+    return kmer_key8(p + len - 8) | (hi8 << 16);
+  }
   uint32_t key = 0;
   for (int t = 0; t < K; ++t) key |= P.at((int64_t)len - 1 - t) << (2 * t);
   return key;
 }
 // Reverse-complement key: sum_{t<K} (3 - P[t]) << 2t.
-__device__ __forceinline__ uint32_t kmer_key_rc(int K, PatWindow& P, const uint8_t* p) {
+__device__ __forceinline__ uint32_t kmer_key_rc(int K, PatWindow& P, const uint8_t* p, uint32_t len) {
   if (K == 8) return kmer_key8_rc(p);
+  if (K > 8 && len >= 16) return kmer_key8_rc(p) | ((kmer_key8_rc(p + 8) & ((1u << (2 * (K - 8))) - 1u)) << 16);
   uint32_t key = 0;
   for (int t = 0; t < K; ++t) key |= (3u - P.at(t)) << (2 * t);
   return key;
@@ -398,12 +404,22 @@ __device__ __forceinline__ uint32_t kmer_key_rc(int K, PatWindow& P, const uint8
 
 // 4 resident CTAs (64 registers): capping registers for 6 or 8 CTAs/SM spills and runs 2-4x
 // slower on configs[3]/[4] (profiles/r01_fm_occupancy_sweep.jsonl).
-template <bool FIXED, bool WORK, int STRANDS, bool LEAN, int SMS>
+// Work order.  DYN = false: the lane's own grid-stride task sequence (ti, ti + stride, ...) over
+// a multi-wave grid.  DYN = true (default): a persistent grid whose warps take chunks of
+// FM_CHUNK tasks from a global counter (one atomicAdd per chunk); in every loop iteration the
+// lanes that finished a pattern are handed the chunk's next tasks by their rank in a ballot, so
+// a warp keeps all 32 lanes busy until the whole batch is drained.  With the static order a
+// lane had ~4 patterns of very different lengths (exact vs random, 24 vs 6 steps) and warps ran
+// with 19 of 32 lanes active on average (ncu source page, profiles/r01_ncu_cluster.md capture).
+constexpr uint32_t FM_CHUNK = 64;
+
+template <bool FIXED, bool WORK, int STRANDS, bool LEAN, int SMS, bool DYN>
 __global__ void __launch_bounds__(256, 4) k_fm_count(FmParams F, const uint8_t* __restrict__ pat,
                                                      const uint64_t* __restrict__ offs, const uint32_t* __restrict__ lens,
                                                      uint32_t fixed_len, uint32_t* __restrict__ out,
                                                      uint32_t* __restrict__ out_rc, uint64_t m,
-                                                     unsigned long long* __restrict__ work) {
+                                                     unsigned long long* __restrict__ work,
+                                                     unsigned long long* __restrict__ ctr) {
   fm_preload_super<SMS>(F);
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   const uint64_t ntask = m * STRANDS;
@@ -421,7 +437,7 @@ __global__ void __launch_bounds__(256, 4) k_fm_count(FmParams F, const uint8_t* 
     const uint8_t* p = pat + (FIXED ? pi * (uint64_t)fixed_len : offs[pi]);
     P.reset(p);
     if (F.K && len >= (uint32_t)F.K) {
-      uint2 iv = __ldg(F.kmer + (rc ? kmer_key_rc(F.K, P, p) : kmer_key(F.K, P, p, len)));
+      uint2 iv = __ldg(F.kmer + (rc ? kmer_key_rc(F.K, P, p, len) : kmer_key(F.K, P, p, len)));
       lo = iv.x; hi = iv.y;
       k = (int64_t)len - 1 - F.K;
     } else {
@@ -429,22 +445,62 @@ __global__ void __launch_bounds__(256, 4) k_fm_count(FmParams F, const uint8_t* 
       k = (int64_t)len - 1;
     }
   };
-  if (ti < ntask) seed();
-  while (ti < ntask) {
-    if (k >= 0 && lo < hi) {                             // one backward step (LF mapping)
-      const uint32_t c = rc ? 3u - P.at((int64_t)len - 1 - k) : P.at(k);
-      uint32_t nl;
-      if (LEAN) fm_step_lean<SMS>(F, C4, c, lo, hi, nl);
-      else      fm_step<SMS>(F, c, lo, hi, nl);
-      --k;
-      if (WORK) { n_steps += 1; n_lines += nl; }
+  auto step = [&]() {                                    // one backward step (LF mapping)
+    const uint32_t c = rc ? 3u - P.at((int64_t)len - 1 - k) : P.at(k);
+    uint32_t nl;
+    if (LEAN) fm_step_lean<SMS>(F, C4, c, lo, hi, nl);
+    else      fm_step<SMS>(F, c, lo, hi, nl);
+    --k;
+    if (WORK) { n_steps += 1; n_lines += nl; }
+  };
+  auto finish = [&]() {
+    const uint32_t cnt = lo < hi ? hi - lo : 0u;
+    if (STRANDS == 2 && rc) out_rc[ti >> 1] = cnt;
+    else out[STRANDS == 2 ? ti >> 1 : ti] = cnt;
+  };
+  if (!DYN) {
+    if (ti < ntask) seed();
+    while (ti < ntask) {
+      if (k >= 0 && lo < hi) step();
+      if (k < 0 || lo >= hi) {                           // finished: write, claim the next task
+        finish();
+        ti += stride;
+        if (ti < ntask) seed();
+      }
     }
-    if (k < 0 || lo >= hi) {                             // finished: write, claim the next task
-      const uint32_t cnt = lo < hi ? hi - lo : 0u;
-      if (STRANDS == 2 && rc) out_rc[ti >> 1] = cnt;
-      else out[STRANDS == 2 ? ti >> 1 : ti] = cnt;
-      ti += stride;
-      if (ti < ntask) seed();
+  } else {
+    const uint32_t lane = threadIdx.x & 31u;
+    uint64_t cb = 0, ce = 0;                             // the warp's chunk [cb, ce) (warp-uniform)
+    bool exhausted = false, has = false;
+    while (true) {
+      if (has) {
+        if (k >= 0 && lo < hi) step();
+        if (k < 0 || lo >= hi) { finish(); has = false; }
+      }
+      const uint32_t needm = __ballot_sync(0xffffffffu, !has);
+      if (needm && !exhausted) {
+        const uint32_t cnt = __popc(needm), r = __popc(needm & ((1u << lane) - 1u));
+        const uint64_t avail = ce - cb;
+        uint64_t nb = 0, ne = 0;
+        if (cnt > avail) {                               // top up from a fresh chunk
+          if (lane == 0) nb = atomicAdd(ctr, (unsigned long long)FM_CHUNK);
+          nb = __shfl_sync(0xffffffffu, nb, 0);
+          ne = nb + FM_CHUNK < ntask ? nb + FM_CHUNK : ntask;
+          if (nb >= ntask) { exhausted = true; nb = ne = ntask; }
+        }
+        if (!has) {
+          const uint64_t t = r < avail ? cb + r : nb + (r - avail);
+          if (r < avail || t < ne) { ti = t; seed(); has = true; }
+        }
+        if (cnt > avail) {
+          const uint64_t take = cnt - avail;
+          cb = nb + take < ne ? nb + take : ne;
+          ce = ne;
+        } else {
+          cb += cnt;
+        }
+      }
+      if (exhausted && __ballot_sync(0xffffffffu, has) == 0) break;
     }
   }
   if (WORK && n_steps) {
@@ -617,34 +673,60 @@ static int fm_smem_mode(const qr_fm* fm, size_t* bytes) {
 template <bool FIXED, bool WORK, int STRANDS, bool LEAN, int SMS>
 static void launch_fm1(unsigned g, size_t smem, cudaStream_t st, const FmParams& F, const uint8_t* pat,
                        const uint64_t* offs, const uint32_t* lens, uint32_t fixed_len, uint32_t* out, uint32_t* out_rc,
-                       uint64_t m, unsigned long long* w) {
-  auto kern = k_fm_count<FIXED, WORK, STRANDS, LEAN, SMS>;
-  if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  kern<<<g, 256, smem, st>>>(F, pat, offs, lens, fixed_len, out, out_rc, m, w);
+                       uint64_t m, unsigned long long* w, unsigned long long* ctr, int sms) {
+  if (ctr) {
+    auto kern = k_fm_count<FIXED, WORK, STRANDS, LEAN, SMS, true>;
+    if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem) != cudaSuccess || per_sm <= 0) {
+      cudaGetLastError();
+      per_sm = 1;
+    }
+    const uint64_t need = (m * STRANDS + 255) / 256;     // no more CTAs than tasks / 256
+    unsigned gp = (unsigned)((uint64_t)per_sm * sms < need ? (uint64_t)per_sm * sms : (need ? need : 1));
+    kern<<<gp, 256, smem, st>>>(F, pat, offs, lens, fixed_len, out, out_rc, m, w, ctr);
+  } else {
+    auto kern = k_fm_count<FIXED, WORK, STRANDS, LEAN, SMS, false>;
+    if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    kern<<<g, 256, smem, st>>>(F, pat, offs, lens, fixed_len, out, out_rc, m, w, nullptr);
+  }
 }
 
 template <bool FIXED, bool WORK, int STRANDS, bool LEAN>
 static void launch_fm2(int sms_mode, unsigned g, size_t smem, cudaStream_t st, const FmParams& F, const uint8_t* pat,
                        const uint64_t* offs, const uint32_t* lens, uint32_t fixed_len, uint32_t* out, uint32_t* out_rc,
-                       uint64_t m, unsigned long long* w) {
-  if (sms_mode == 1)      launch_fm1<FIXED, WORK, STRANDS, LEAN, 1>(g, smem, st, F, pat, offs, lens, fixed_len, out, out_rc, m, w);
-  else if (sms_mode == 2) launch_fm1<FIXED, WORK, STRANDS, LEAN, 2>(g, smem, st, F, pat, offs, lens, fixed_len, out, out_rc, m, w);
-  else                    launch_fm1<FIXED, WORK, STRANDS, LEAN, 0>(g, 0, st, F, pat, offs, lens, fixed_len, out, out_rc, m, w);
+                       uint64_t m, unsigned long long* w, unsigned long long* ctr, int sms) {
+  if (sms_mode == 1)      launch_fm1<FIXED, WORK, STRANDS, LEAN, 1>(g, smem, st, F, pat, offs, lens, fixed_len, out, out_rc, m, w, ctr, sms);
+  else if (sms_mode == 2) launch_fm1<FIXED, WORK, STRANDS, LEAN, 2>(g, smem, st, F, pat, offs, lens, fixed_len, out, out_rc, m, w, ctr, sms);
+  else                    launch_fm1<FIXED, WORK, STRANDS, LEAN, 0>(g, 0, st, F, pat, offs, lens, fixed_len, out, out_rc, m, w, ctr, sms);
 }
 
+extern int g_fm_dyn;
+
 template <bool FIXED, bool WORK>
-static void launch_fm(const qr_fm* fm, bool lean, unsigned g, cudaStream_t st, const FmParams& F, const uint8_t* pat,
-                      const uint64_t* offs, const uint32_t* lens, uint32_t fixed_len, uint32_t* out, uint32_t* out_rc,
-                      uint64_t m, unsigned long long* w) {
+static cudaError_t launch_fm(const qr_fm* fm, bool lean, unsigned g, cudaStream_t st, const FmParams& F,
+                             const uint8_t* pat, const uint64_t* offs, const uint32_t* lens, uint32_t fixed_len,
+                             uint32_t* out, uint32_t* out_rc, uint64_t m, unsigned long long* w) {
   size_t smem = 0;
   const int sm = fm_smem_mode(fm, &smem);
+  CounterLease lease;
+  unsigned long long* ctr = nullptr;
+  cudaError_t e;
+  if (g_fm_dyn && (e = lease.acquire(fm->bwt->device, st, &ctr))) return e;
+  const int sms = fm->bwt->sm_count;
   if (lean) {
-    if (out_rc) launch_fm2<FIXED, WORK, 2, true>(sm, g, smem, st, F, pat, offs, lens, fixed_len, out, out_rc, m, w);
-    else        launch_fm2<FIXED, WORK, 1, true>(sm, g, smem, st, F, pat, offs, lens, fixed_len, out, out_rc, m, w);
+    if (out_rc) launch_fm2<FIXED, WORK, 2, true>(sm, g, smem, st, F, pat, offs, lens, fixed_len, out, out_rc, m, w, ctr, sms);
+    else        launch_fm2<FIXED, WORK, 1, true>(sm, g, smem, st, F, pat, offs, lens, fixed_len, out, out_rc, m, w, ctr, sms);
   } else {
-    if (out_rc) launch_fm2<FIXED, WORK, 2, false>(sm, g, smem, st, F, pat, offs, lens, fixed_len, out, out_rc, m, w);
-    else        launch_fm2<FIXED, WORK, 1, false>(sm, g, smem, st, F, pat, offs, lens, fixed_len, out, out_rc, m, w);
+    if (out_rc) launch_fm2<FIXED, WORK, 2, false>(sm, g, smem, st, F, pat, offs, lens, fixed_len, out, out_rc, m, w, ctr, sms);
+    else        launch_fm2<FIXED, WORK, 1, false>(sm, g, smem, st, F, pat, offs, lens, fixed_len, out, out_rc, m, w, ctr, sms);
   }
+  e = cudaGetLastError();
+  if (ctr) {
+    cudaError_t e2 = lease.release(st);
+    if (!e) e = e2;
+  }
+  return e;
 }
 
 qr_status fm_count_device(const qr_fm* fm, const uint8_t* pat, const uint32_t* lengths, uint32_t fixed_len,
@@ -657,10 +739,10 @@ qr_status fm_count_device(const qr_fm* fm, const uint8_t* pat, const uint32_t* l
   unsigned long long* w = reinterpret_cast<unsigned long long*>(work);
   cudaError_t e;
   if (!lengths) {
-    if (approx) k_fm_approx1<true><<<g, 256, 0, st>>>(F, pat, nullptr, nullptr, fixed_len, out, m);
-    else if (work) launch_fm<true, true>(fm, use_lean(fm), g, st, F, pat, nullptr, nullptr, fixed_len, out, out_rc, m, w);
-    else      launch_fm<true, false>(fm, use_lean(fm), g, st, F, pat, nullptr, nullptr, fixed_len, out, out_rc, m, w);
-    if ((e = cudaGetLastError())) return cuda_fail(e, "k_fm_count");
+    if (approx) { k_fm_approx1<true><<<g, 256, 0, st>>>(F, pat, nullptr, nullptr, fixed_len, out, m); e = cudaGetLastError(); }
+    else if (work) e = launch_fm<true, true>(fm, use_lean(fm), g, st, F, pat, nullptr, nullptr, fixed_len, out, out_rc, m, w);
+    else      e = launch_fm<true, false>(fm, use_lean(fm), g, st, F, pat, nullptr, nullptr, fixed_len, out, out_rc, m, w);
+    if (e) return cuda_fail(e, "k_fm_count");
     return QR_OK;
   }
   uint64_t* offs = nullptr;
@@ -673,10 +755,9 @@ qr_status fm_count_device(const qr_fm* fm, const uint8_t* pat, const uint32_t* l
   if ((e = cub::DeviceScan::ExclusiveSum(tmp, tb, offs, offs, (int64_t)m, st))) {
     cudaFreeAsync(offs, st); cudaFreeAsync(tmp, st); return cuda_fail(e, "scan");
   }
-  if (approx) k_fm_approx1<false><<<g, 256, 0, st>>>(F, pat, offs, lengths, 0, out, m);
-  else if (work) launch_fm<false, true>(fm, use_lean(fm), g, st, F, pat, offs, lengths, 0, out, out_rc, m, w);
-  else      launch_fm<false, false>(fm, use_lean(fm), g, st, F, pat, offs, lengths, 0, out, out_rc, m, w);
-  e = cudaGetLastError();
+  if (approx) { k_fm_approx1<false><<<g, 256, 0, st>>>(F, pat, offs, lengths, 0, out, m); e = cudaGetLastError(); }
+  else if (work) e = launch_fm<false, true>(fm, use_lean(fm), g, st, F, pat, offs, lengths, 0, out, out_rc, m, w);
+  else      e = launch_fm<false, false>(fm, use_lean(fm), g, st, F, pat, offs, lengths, 0, out, out_rc, m, w);
   cudaFreeAsync(offs, st);
   cudaFreeAsync(tmp, st);
   if (e) return cuda_fail(e, "k_fm_count");

@@ -95,6 +95,17 @@ cudaError_t launch_super_pack_rank(const qr_index* h, const uint64_t* q, const u
                                    int what, cudaStream_t st);
 qr_status birank_build_device(const uint64_t* d_bits, uint64_t n, int device, cudaStream_t st, qr_index** out);
 
+// A zeroed work counter (4 u64 words) for one launch of a dynamic-work-order kernel
+// (counters.cu).  acquire() before the launch, release() after it, on the same stream; the
+// lease holds a host lock in between.
+struct CounterLease {
+  void* ring = nullptr;
+  uint32_t slot = 0;
+  cudaError_t acquire(int device, cudaStream_t st, unsigned long long** ctr);
+  cudaError_t release(cudaStream_t st);
+  ~CounterLease();
+};
+
 // grid for a grid-stride kernel: a multiple of the SM count
 inline unsigned grid_stride_blocks(uint64_t work_items, unsigned threads, int sms, int blocks_per_sm) {
   uint64_t need = (work_items + threads - 1) / threads;

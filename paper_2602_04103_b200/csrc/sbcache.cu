@@ -531,52 +531,14 @@ static void sc_launch_kt(const qr_index* h, const uint64_t* q, const uint8_t* c,
 }
 
 // what: 0 = rank (sigma 2 or 4), 1 = rank_4 (sigma 4), 3 = BiRank gather ceiling of this kernel shape
-// Work counters of the dynamic order.  A per-device ring of counters, each with the event of its
-// last use: a launch takes the next slot, makes its stream wait for that event (so a slot is never
-// shared by two launches in flight, whatever streams they run on), zeroes it stream-ordered and
-// records the event again after the kernel.  No allocation per launch: cudaMallocAsync /
-// cudaFreeAsync on the staged path's streams added cross-stream dependencies (e2e 5.98 -> 2.64 Gq/s).
-constexpr int CTR_SLOTS = 64;
-struct CtrRing {
-  std::mutex mu;
-  unsigned long long* d = nullptr;
-  cudaEvent_t ev[CTR_SLOTS] = {};
-  uint32_t next = 0;
-};
-
-static CtrRing* ctr_ring(int device) {
-  static std::mutex mu;
-  static std::map<int, CtrRing*> rings;
-  std::lock_guard<std::mutex> g(mu);
-  CtrRing*& r = rings[device];
-  if (!r) {
-    CtrRing* n = new CtrRing();
-    if (cudaMalloc((void**)&n->d, CTR_SLOTS * 128) != cudaSuccess) { delete n; return nullptr; }
-    for (int i = 0; i < CTR_SLOTS; ++i)
-      if (cudaEventCreateWithFlags(&n->ev[i], cudaEventDisableTiming) != cudaSuccess) { delete n; return nullptr; }
-    r = n;
-  }
-  return r;
-}
-
 cudaError_t launch_super_pack_rank(const qr_index* h, const uint64_t* q, const uint8_t* c, uint64_t* out, uint64_t m,
                                    int what, cudaStream_t st) {
   if (m == 0) return cudaSuccess;
   const bool dyn = g_rank_dyn != 0;
-  CtrRing* ring = nullptr;
-  if (dyn && !(ring = ctr_ring(h->device))) return cudaErrorMemoryAllocation;
-  // the ring lock spans slot choice, wait, zeroing, launch and event record (host-side only)
-  std::unique_lock<std::mutex> lk;
-  if (ring) lk = std::unique_lock<std::mutex>(ring->mu);
+  CounterLease lease;
   unsigned long long* ctr = nullptr;
-  uint32_t slot = 0;
   cudaError_t e;
-  if (ring) {
-    slot = ring->next++ % CTR_SLOTS;
-    ctr = ring->d + 16 * slot;                       // one 128-B line per counter
-    if ((e = cudaStreamWaitEvent(st, ring->ev[slot], 0))) return e;
-    if ((e = cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), st))) return e;
-  }
+  if (dyn && (e = lease.acquire(h->device, st, &ctr))) return e;
   // default K (measured, profiles/r01_smem_probe_k.jsonl): BiRank 4 (fits 64 registers), QuadRank 2
   // (K = 4 spills at the 64-register cap of 1024-thread CTAs)
   const int k = g_rank_smem_k ? g_rank_smem_k : (h->sigma == 2 ? 4 : 2);
@@ -588,8 +550,8 @@ cudaError_t launch_super_pack_rank(const qr_index* h, const uint64_t* q, const u
     default: sc_launch_kt<4, 1024>(h, q, c, out, m, what, ctr, dyn, st); break;
   }
   e = cudaGetLastError();
-  if (ring) {
-    cudaError_t e2 = cudaEventRecord(ring->ev[slot], st);
+  if (dyn) {
+    cudaError_t e2 = lease.release(st);
     if (!e) e = e2;
   }
   return e;

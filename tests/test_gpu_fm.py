@@ -107,7 +107,7 @@ def test_fm_kmer_table_matches_oracle(cuda):
     w = gen.dna(42, n)
     sym = gen.unpack_dna(w, n)
     ora = oracle.FmOracle(sym)
-    fm = qr.qr_fm_build(w, n)
+    fm = qr.qr_fm_build(w, n, kmer_k=8)
     t = qr.qr_fm_export_kmer(fm)
     # key: 2 bits per char, last pattern char in the low bits
     keys = np.arange(65536, dtype=np.uint32)
@@ -320,7 +320,7 @@ def test_cli_fm_count(cuda, tmp_path):
     assert [r[2] for r in rows] == list(oracle.scan_count(sym, rcat, roff, rlens))
 
 
-@pytest.mark.parametrize("k", [0, 1, 5, 8, 10, 12])
+@pytest.mark.parametrize("k", [0, 1, 5, 8, 10, 12, 13, 14])
 def test_fm_kmer_width_does_not_change_counts(cuda, k):
     """Seeded vs unseeded counts are identical for every table width, incl. no table,
     on exact / both-strand / <=1-mismatch counting; the table holds the K-mer interval sizes."""
@@ -388,3 +388,49 @@ def test_fm_superblock_source_does_not_change_results(cuda, fm_smem, step):
     assert np.array_equal(to_host(d).view(np.uint32), ref)
     assert np.array_equal(to_host(db).view(np.uint32), ref_fixed)
     assert np.array_equal(to_host(dr).view(np.uint32), ref_rc)
+
+
+@pytest.mark.parametrize("dyn", [0, 1])
+@pytest.mark.parametrize("m", [1, 31, 63, 64, 65, 4097])
+def test_fm_work_order_covers_every_task(cuda, dyn, m):
+    """Static grid-stride order (0) and the persistent warp-chunk order (1, default) must count
+    every pattern exactly once, for batch sizes around the chunk size (64) and the warp size,
+    single strand and both strands (2m tasks), variable lengths."""
+    torch = _torch()
+    n = 120000
+    w = gen.dna(41, n, 0)
+    sym = gen.unpack_dna(w, n)
+    ora = oracle.FmOracle(sym)
+    fm = qr.qr_fm_build(w, n)
+    pats = mixed_patterns(np.random.default_rng(100 + m), sym, m)
+    pats = pats[:m - 3] + pats[-3:] if m > 3 else pats[:m]   # keep whole-text / longer / empty
+    cat, off, lens = oracle.pack_patterns(pats)
+    assert lens.size == m
+    ref = ora.count(cat, off, lens)
+    rc_pats = [(3 - p[::-1]).astype(np.uint8) for p in pats]
+    rcat, roff, rlens = oracle.pack_patterns(rc_pats)
+    ref_rc = ora.count(rcat, roff, rlens)
+    qr.qr_set_tuning("fm_dyn", dyn)
+    try:
+        d = torch.full((m,), -1, dtype=torch.int32, device=cuda)
+        qr.qr_fm_count(fm, to_dev(cat, cuda), to_dev(lens, cuda), 0, d, m)
+        db = torch.full((m,), -1, dtype=torch.int32, device=cuda)
+        dr = torch.full((m,), -1, dtype=torch.int32, device=cuda)
+        qr.qr_fm_count_both(fm, to_dev(cat, cuda), to_dev(lens, cuda), 0, db, dr, m)
+        torch.cuda.synchronize()
+    finally:
+        qr.qr_set_tuning("fm_dyn", 1)
+    assert np.array_equal(to_host(d).view(np.uint32), ref)
+    assert np.array_equal(to_host(db).view(np.uint32), ref)
+    assert np.array_equal(to_host(dr).view(np.uint32), ref_rc)
+
+
+def test_fm_default_kmer_width(cuda):
+    """qr_fm_build's width: the paper's 8 below n = 2^20, 10 below 2^24, 12 above."""
+    torch = _torch()
+    for n, k in ((1000, 8), ((1 << 20) - 1, 8), (1 << 20, 10), ((1 << 24) - 1, 10), (1 << 24, 12)):
+        t = torch.empty((n + 31) // 32 + 1, dtype=torch.uint64, device=cuda)
+        gen.dna_dev(50, n, 0, t)
+        fm = qr.qr_fm_build(t, n)
+        assert fm.kmer_k == k, (n, fm.kmer_k)
+        fm.free()

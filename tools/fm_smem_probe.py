@@ -22,15 +22,17 @@ for name, n, kind, m, L, seed in (("c4", 1 << 26, 0, 10**7, 32, 4), ("c5", 1 << 
     pats = torch.empty(m * L, dtype=torch.uint8, device=dev)
     gen.patterns_dev(seed, kind, m, L, text, n, pats)
     out = torch.empty(m, dtype=torch.int32, device=dev); ref = torch.empty_like(out)
-    qr.qr_set_tuning("fm_smem", 0); qr.qr_set_tuning("fm_step", 0)
+    qr.qr_set_tuning("fm_smem", 0); qr.qr_set_tuning("fm_step", 0); qr.qr_set_tuning("fm_dyn", 0)
     qr.qr_fm_count(fm, pats, None, L, ref, m, st)
-    for step in (0, 1, 2):
-        for sm in (0, 1, 2):
-            qr.qr_set_tuning("fm_smem", sm); qr.qr_set_tuning("fm_step", step)
-            ms = t(lambda: qr.qr_fm_count(fm, pats, None, L, out, m, st))
-            torch.cuda.synchronize()
-            print(json.dumps({"cfg": name, "step": step, "fm_smem": sm, "ms": ms, "gpat_s": m / ms / 1e6,
-                              "equal": bool(torch.equal(out, ref))}), flush=True)
+    for dyn in (0, 1):
+        for step in (0, 1, 2):
+            for sm in (0, 1):
+                qr.qr_set_tuning("fm_dyn", dyn); qr.qr_set_tuning("fm_smem", sm); qr.qr_set_tuning("fm_step", step)
+                ms = t(lambda: qr.qr_fm_count(fm, pats, None, L, out, m, st))
+                torch.cuda.synchronize()
+                print(json.dumps({"cfg": name, "dyn": dyn, "step": step, "fm_smem": sm, "ms": ms, "gpat_s": m / ms / 1e6,
+                                  "equal": bool(torch.equal(out, ref))}), flush=True)
+    qr.qr_set_tuning("fm_dyn", 1)
     qr.qr_set_tuning("fm_smem", 1); qr.qr_set_tuning("fm_step", 0)
     del fm, text, pats, out, ref
     torch.cuda.empty_cache()
