@@ -239,7 +239,9 @@ const char* qr_last_error(void);
  * table when the handle has one: 0 never, 1 (default) for batches of >= 2^22 queries, 2 always),
  * "rank_dyn" (1, default: those kernels take work in chunks from a global counter; 0: static
  * grid-stride order), "rank_smem_k" (their queries per lane pair per group: 0 = auto (BiRank 4,
- * QuadRank 2), 1, 2, 4 with 1024-thread CTAs, 6 with 768, 8 with 512), "rank_smem_clusters" (0 = as many 2-CTA
+ * QuadRank 2), 1, 2, 3, 4 with 1024-thread CTAs, 6 with 768, 8 with 512; resets
+ * "rank_smem_threads"), "rank_smem_threads" (CTA size for the current K: 1024 for K 1-4, 768 for
+ * K 4 or 6, 512 for K 8; 0 = the default for K), "rank_smem_clusters" (0 = as many 2-CTA
  * clusters as fit at once, else that many).
  * QR_EINVAL for an unknown key or out-of-range value. */
 qr_status qr_set_tuning(const char* key, int64_t value);

@@ -29,6 +29,7 @@ int g_index64 = 0;              // 1: force the 64-bit line-index path (tests th
 int g_rank_smem = 1;            // superblock words from cluster shared memory: 0 never, 1 large batches, 2 always
 int g_rank_dyn = 1;             // cluster rank kernels: 1 = dynamic (atomic chunk) work order, 0 = static grid stride
 int g_rank_smem_clusters = 0;   // cluster rank kernels: 0 = as many 2-CTA clusters as fit (occupancy API), else this many
+int g_rank_smem_threads = 0;    // cluster rank kernels: CTA size (0 auto: 1024, 768 for K = 6, 512 for K = 8)
 int g_rank_smem_k = 0;          // cluster rank kernels: queries per lane pair per group (0 auto, 1, 2, 4 @1024 thr, 6 @768, 8 @512)
 int g_rank_pair = 1;            // 1: lane-pair kernels (one L2 request per query); 0: one lane per query
 uint64_t g_stage_chunk = 1ull << 23;   // queries per chunk on the staged host path (sweep: profiles/r01_e2e_sweep)
@@ -305,9 +306,17 @@ QR_EXPORT qr_status qr_set_tuning(const char* key, int64_t value) {
     if (value < 0 || value > 2) return fail(QR_EINVAL, "rank_smem must be 0 (off), 1 (auto) or 2 (always)");
     g_rank_smem = (int)value;
   } else if (!strcmp(key, "rank_smem_k")) {
-    if (value != 0 && value != 1 && value != 2 && value != 4 && value != 6 && value != 8)
-      return fail(QR_EINVAL, "rank_smem_k must be 0 (auto), 1, 2, 4, 6 or 8");
+    if (value != 0 && value != 1 && value != 2 && value != 3 && value != 4 && value != 6 && value != 8)
+      return fail(QR_EINVAL, "rank_smem_k must be 0 (auto), 1, 2, 3, 4, 6 or 8");
     g_rank_smem_k = (int)value;
+    g_rank_smem_threads = 0;
+  } else if (!strcmp(key, "rank_smem_threads")) {
+    // instantiated (K, threads) pairs: K 1-4 @1024, 4 and 6 @768, 8 @512 (set rank_smem_k first)
+    const int k = g_rank_smem_k;
+    const bool ok = value == 0 || (value == 1024 && k >= 1 && k <= 4) || (value == 768 && (k == 4 || k == 6)) ||
+                    (value == 512 && k == 8);
+    if (!ok) return fail(QR_EINVAL, "rank_smem_threads: no kernel for K=%d with %lld threads", k, (long long)value);
+    g_rank_smem_threads = (int)value;
   } else if (!strcmp(key, "rank_smem_clusters")) {
     if (value < 0 || value > 4096) return fail(QR_EINVAL, "rank_smem_clusters must be 0..4096");
     g_rank_smem_clusters = (int)value;

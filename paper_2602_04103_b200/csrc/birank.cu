@@ -13,6 +13,7 @@
 #include <cub/device/device_scan.cuh>
 
 #include "qr_common.cuh"
+#include "sched.cuh"
 
 namespace qr {
 
@@ -217,18 +218,20 @@ __global__ void __launch_bounds__(256) k_bi_gather(const uint4* __restrict__ lin
 // with a two-sector mask, i.e. 1 request per query instead of 1.52.  Each lane counts its own
 // half (Eq. 1's two cases are exactly the two sectors) and one shuffle adds the halves.
 // Loop bounds are warp-uniform so that the shuffle sees every lane.
-template <int K, bool SMALLQ, bool HAS_C, uint32_t S_LANE = 1>
+template <int K, bool SMALLQ, bool HAS_C, uint32_t S_LANE, bool DYN>
 __global__ void __launch_bounds__(256) k_bi_rank2(const uint4* __restrict__ lines, const uint32_t* __restrict__ super,
                                                   const uint64_t* __restrict__ q, const uint8_t* __restrict__ cs,
-                                                  uint64_t* __restrict__ out, uint64_t m, uint64_t last_line) {
-  const uint64_t npair = ((uint64_t)gridDim.x * blockDim.x) >> 1;
+                                                  uint64_t* __restrict__ out, uint64_t m, uint64_t last_line,
+                                                  unsigned long long* ctr) {
   const uint32_t half = threadIdx.x & 1u;
-  const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-  uint64_t i0 = tid >> 1;
-  uint64_t iw = (tid & ~31ull) >> 1;                      // first pair of this warp (uniform)
+  const uint32_t pw = sc_unit_in_warp<16>();
+  ScSched sc = sc_first<K, DYN, 16>(ctr);
+  uint64_t i0 = sc.gb + pw, npair = sc.stride;                      // first pair of this warp (uniform)
   uint64_t qn[K];
   load_q_group<K>(q, i0, npair, m, qn);
-  for (; iw < m; iw += npair * K, i0 += npair * K) {
+  while (sc.gb < m) {
+    i0 = sc.gb + pw;
+    npair = sc.stride;
     uint64_t qq[K], jj[K];
     uint32_t pp[K];
 #pragma unroll
@@ -242,7 +245,8 @@ __global__ void __launch_bounds__(256) k_bi_rank2(const uint4* __restrict__ line
       if (half == 0 || pp[k] >= 256) ld_sector_na(lines + 4 * jj[k] + 2 * half, w[k][0], w[k][1], w[k][2], w[k][3]);
       s[k] = half == S_LANE ? __ldg(super + (jj[k] >> BI_SB_LOG)) : 0u;
     }
-    load_q_group<K>(q, i0 + npair * K, npair, m, qn);
+    sc = sc_next<K, DYN, 16>(sc, ctr);
+    load_q_group<K>(q, sc.gb + pw, sc.stride, m, qn);
 #pragma unroll
     for (int k = 0; k < K; ++k) {
       const uint64_t idx = i0 + (uint64_t)k * npair;
@@ -269,18 +273,19 @@ __global__ void __launch_bounds__(256) k_bi_rank2(const uint4* __restrict__ line
 // left of the anchor — measured 36.9 vs 35.6 Gq/s for lane 0 on configs[1], profiles/r01_s_probe.)
 // Gather ceiling with the same lane-pair loads (MODE 0: the sectors rank2 reads; MODE 1: both
 // sectors always; MODE 2: the sectors rank2 reads plus its superblock-word load).
-template <int K, bool SMALLQ, int MODE>
+template <int K, bool SMALLQ, int MODE, bool DYN>
 __global__ void __launch_bounds__(256) k_bi_gather2(const uint4* __restrict__ lines, const uint32_t* __restrict__ super,
                                                     const uint64_t* __restrict__ q, uint64_t* __restrict__ out, uint64_t m,
-                                                    uint64_t last_line) {
-  const uint64_t npair = ((uint64_t)gridDim.x * blockDim.x) >> 1;
+                                                    uint64_t last_line, unsigned long long* ctr) {
   const uint32_t half = threadIdx.x & 1u;
-  const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-  uint64_t i0 = tid >> 1;
-  uint64_t iw = (tid & ~31ull) >> 1;
+  const uint32_t pw = sc_unit_in_warp<16>();
+  ScSched sc = sc_first<K, DYN, 16>(ctr);
+  uint64_t i0 = sc.gb + pw, npair = sc.stride;
   uint64_t qn[K];
   load_q_group<K>(q, i0, npair, m, qn);
-  for (; iw < m; iw += npair * K, i0 += npair * K) {
+  while (sc.gb < m) {
+    i0 = sc.gb + pw;
+    npair = sc.stride;
     uint64_t qq[K], jj[K];
     uint32_t pp[K];
 #pragma unroll
@@ -294,7 +299,8 @@ __global__ void __launch_bounds__(256) k_bi_gather2(const uint4* __restrict__ li
         ld_sector_na(lines + 4 * jj[k] + 2 * half, w[k][0], w[k][1], w[k][2], w[k][3]);
       if (MODE == 2 && half == 0) w[k][0] ^= __ldg(super + (jj[k] >> BI_SB_LOG));
     }
-    load_q_group<K>(q, i0 + npair * K, npair, m, qn);
+    sc = sc_next<K, DYN, 16>(sc, ctr);
+    load_q_group<K>(q, sc.gb + pw, sc.stride, m, qn);
 #pragma unroll
     for (int k = 0; k < K; ++k) {
       const uint64_t idx = i0 + (uint64_t)k * npair;
@@ -320,15 +326,18 @@ static cudaError_t bi_rank_k(const qr_index* h, const uint64_t* q, const uint8_t
   const uint64_t last = h->n_lines - 1;
   if (g_rank_pair) {
     const bool s0 = g_rank_s_lane == 0;
+    const bool dyn = use_dyn_order(m);
+    const int dev = h->device, sms = h->sm_count;
+#define QR_BI2(SQ, HC, SL) launch_ordered(k_bi_rank2<K, SQ, HC, SL, false>, k_bi_rank2<K, SQ, HC, SL, true>, dyn, dev, sms, \
+                                          g, st, (const uint4*)h->lines, (const uint32_t*)h->super, q, c, out, m, last)
     if (small) {
-      if (c) k_bi_rank2<K, true, true><<<g, 256, 0, st>>>(h->lines, h->super, q, c, out, m, last);
-      else if (s0) k_bi_rank2<K, true, false, 0><<<g, 256, 0, st>>>(h->lines, h->super, q, c, out, m, last);
-      else   k_bi_rank2<K, true, false><<<g, 256, 0, st>>>(h->lines, h->super, q, c, out, m, last);
-    } else {
-      if (c) k_bi_rank2<K, false, true><<<g, 256, 0, st>>>(h->lines, h->super, q, c, out, m, last);
-      else   k_bi_rank2<K, false, false><<<g, 256, 0, st>>>(h->lines, h->super, q, c, out, m, last);
+      if (c) return QR_BI2(true, true, 1);
+      if (s0) return QR_BI2(true, false, 0);
+      return QR_BI2(true, false, 1);
     }
-    return cudaGetLastError();
+    if (c) return QR_BI2(false, true, 1);
+    return QR_BI2(false, false, 1);
+#undef QR_BI2
   }
   if (small) {
     if (c) k_bi_rank<K, true, true><<<g, 256, 0, st>>>(h->lines, h->super, q, c, out, m, last);
@@ -360,16 +369,13 @@ static cudaError_t bi_gather_k(const qr_index* h, const uint64_t* q, uint64_t* o
   unsigned g = grid_stride_blocks((2 * m + per_thread - 1) / per_thread, 256, h->sm_count, g_rank_blocks_per_sm);
   const uint64_t last = h->n_lines - 1;
   if (g_rank_pair) {
-    if (small) {
-      if (mode == 2)      k_bi_gather2<K, true, 2><<<g, 256, 0, st>>>(h->lines, h->super, q, out, m, last);
-      else if (mode == 1) k_bi_gather2<K, true, 1><<<g, 256, 0, st>>>(h->lines, h->super, q, out, m, last);
-      else                k_bi_gather2<K, true, 0><<<g, 256, 0, st>>>(h->lines, h->super, q, out, m, last);
-    } else {
-      if (mode == 2)      k_bi_gather2<K, false, 2><<<g, 256, 0, st>>>(h->lines, h->super, q, out, m, last);
-      else if (mode == 1) k_bi_gather2<K, false, 1><<<g, 256, 0, st>>>(h->lines, h->super, q, out, m, last);
-      else                k_bi_gather2<K, false, 0><<<g, 256, 0, st>>>(h->lines, h->super, q, out, m, last);
-    }
-    return cudaGetLastError();
+    const bool dyn = use_dyn_order(m);
+    const int dev = h->device, sms = h->sm_count;
+#define QR_BG2(SQ, MO) launch_ordered(k_bi_gather2<K, SQ, MO, false>, k_bi_gather2<K, SQ, MO, true>, dyn, dev, sms, g, st, \
+                                      (const uint4*)h->lines, (const uint32_t*)h->super, q, out, m, last)
+    if (small) return mode == 2 ? QR_BG2(true, 2) : mode == 1 ? QR_BG2(true, 1) : QR_BG2(true, 0);
+    return mode == 2 ? QR_BG2(false, 2) : mode == 1 ? QR_BG2(false, 1) : QR_BG2(false, 0);
+#undef QR_BG2
   }
   if (mode == 2) mode = 0;
   if (small) {

@@ -17,6 +17,7 @@
 #include <cub/device/device_scan.cuh>
 
 #include "qr_common.cuh"
+#include "sched.cuh"
 
 namespace qr {
 
@@ -317,19 +318,21 @@ __global__ void __launch_bounds__(256) k_qd_gather(const uint4* __restrict__ lin
 // lane 2i loads sector 0 (deltas + data chars [0,96)), lane 2i+1 loads sector 1 (data chars
 // [96,224)) only for queries right of the anchor; both loads are in the same warp instruction,
 // so the L1 sends one request per 64-B line.  Each lane counts its own case of Listing 1.
-template <int K, bool SMALLQ, uint32_t S_LANE = 1>
+template <int K, bool SMALLQ, bool DYN, uint32_t S_LANE = 1>
 __global__ void __launch_bounds__(256) k_qd_rank2(const uint4* __restrict__ lines, const uint32_t* __restrict__ super,
                                                   const uint64_t* __restrict__ q, const uint8_t* __restrict__ cs,
-                                                  uint64_t* __restrict__ out, uint64_t m, uint64_t last_line) {
-  const uint64_t npair = ((uint64_t)gridDim.x * blockDim.x) >> 1;
+                                                  uint64_t* __restrict__ out, uint64_t m, uint64_t last_line,
+                                                  unsigned long long* ctr) {
   const uint32_t half = threadIdx.x & 1u;
-  const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-  uint64_t i0 = tid >> 1;
-  uint64_t iw = (tid & ~31ull) >> 1;
+  const uint32_t pw = sc_unit_in_warp<16>();
+  ScSched sc = sc_first<K, DYN, 16>(ctr);
+  uint64_t i0 = sc.gb + pw, npair = sc.stride;
   uint64_t qn[K];
   uint32_t cn[K];
   qd_load_group<K, true>(q, cs, i0, npair, m, qn, cn);
-  for (; iw < m; iw += npair * K, i0 += npair * K) {
+  while (sc.gb < m) {
+    i0 = sc.gb + pw;
+    npair = sc.stride;
     uint64_t qq[K], jj[K];
     uint32_t pp[K], cc[K];
 #pragma unroll
@@ -343,7 +346,8 @@ __global__ void __launch_bounds__(256) k_qd_rank2(const uint4* __restrict__ line
       if (half == 0 || pp[k] >= 128) ld_sector_na(lines + 4 * jj[k] + 2 * half, w[k][0], w[k][1], w[k][2], w[k][3]);
       s[k] = half == S_LANE ? __ldg(super + 4 * (jj[k] >> QD_SB_LOG) + cc[k]) : 0u;
     }
-    qd_load_group<K, true>(q, cs, i0 + npair * K, npair, m, qn, cn);
+    sc = sc_next<K, DYN, 16>(sc, ctr);
+    qd_load_group<K, true>(q, cs, sc.gb + pw, sc.stride, m, qn, cn);
 #pragma unroll
     for (int k = 0; k < K; ++k) {
       const uint64_t idx = i0 + (uint64_t)k * npair;
@@ -361,19 +365,20 @@ __global__ void __launch_bounds__(256) k_qd_rank2(const uint4* __restrict__ line
   }
 }
 
-template <int K, bool SMALLQ>
+template <int K, bool SMALLQ, bool DYN>
 __global__ void __launch_bounds__(256) k_qd_all4_2(const uint4* __restrict__ lines, const uint32_t* __restrict__ super,
                                                    const uint64_t* __restrict__ q, uint64_t* __restrict__ out4,
-                                                   uint64_t m, uint64_t last_line) {
-  const uint64_t npair = ((uint64_t)gridDim.x * blockDim.x) >> 1;
+                                                   uint64_t m, uint64_t last_line, unsigned long long* ctr) {
   const uint32_t half = threadIdx.x & 1u;
-  const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-  uint64_t i0 = tid >> 1;
-  uint64_t iw = (tid & ~31ull) >> 1;
+  const uint32_t pw = sc_unit_in_warp<16>();
+  ScSched sc = sc_first<K, DYN, 16>(ctr);
+  uint64_t i0 = sc.gb + pw, npair = sc.stride;
   uint64_t qn[K];
   uint32_t cn[K];
   qd_load_group<K, false>(q, nullptr, i0, npair, m, qn, cn);
-  for (; iw < m; iw += npair * K, i0 += npair * K) {
+  while (sc.gb < m) {
+    i0 = sc.gb + pw;
+    npair = sc.stride;
     uint64_t qq[K], jj[K];
     uint32_t pp[K];
 #pragma unroll
@@ -388,7 +393,8 @@ __global__ void __launch_bounds__(256) k_qd_all4_2(const uint4* __restrict__ lin
       // lane 0 reads s_A, s_C and lane 1 s_G, s_T: one 16-B segment, one request for the pair
       s[k] = __ldg(reinterpret_cast<const uint2*>(super) + 2 * (jj[k] >> QD_SB_LOG) + half);
     }
-    qd_load_group<K, false>(q, nullptr, i0 + npair * K, npair, m, qn, cn);
+    sc = sc_next<K, DYN, 16>(sc, ctr);
+    qd_load_group<K, false>(q, nullptr, sc.gb + pw, sc.stride, m, qn, cn);
 #pragma unroll
     for (int k = 0; k < K; ++k) {
       const uint64_t idx = i0 + (uint64_t)k * npair;
@@ -423,18 +429,20 @@ __global__ void __launch_bounds__(256) k_qd_all4_2(const uint4* __restrict__ lin
   }
 }
 
-template <int K, bool SMALLQ, int MODE>
+template <int K, bool SMALLQ, int MODE, bool DYN>
 __global__ void __launch_bounds__(256) k_qd_gather2(const uint4* __restrict__ lines, const uint64_t* __restrict__ q,
-                                                    uint64_t* __restrict__ out, uint64_t m, uint64_t last_line) {
-  const uint64_t npair = ((uint64_t)gridDim.x * blockDim.x) >> 1;
+                                                    uint64_t* __restrict__ out, uint64_t m, uint64_t last_line,
+                                                    unsigned long long* ctr) {
   const uint32_t half = threadIdx.x & 1u;
-  const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-  uint64_t i0 = tid >> 1;
-  uint64_t iw = (tid & ~31ull) >> 1;
+  const uint32_t pw = sc_unit_in_warp<16>();
+  ScSched sc = sc_first<K, DYN, 16>(ctr);
+  uint64_t i0 = sc.gb + pw, npair = sc.stride;
   uint64_t qn[K];
   uint32_t cn[K];
   qd_load_group<K, false>(q, nullptr, i0, npair, m, qn, cn);
-  for (; iw < m; iw += npair * K, i0 += npair * K) {
+  while (sc.gb < m) {
+    i0 = sc.gb + pw;
+    npair = sc.stride;
     uint64_t qq[K], jj[K];
     uint32_t pp[K];
 #pragma unroll
@@ -447,7 +455,8 @@ __global__ void __launch_bounds__(256) k_qd_gather2(const uint4* __restrict__ li
       if (MODE == 1 || half == 0 || pp[k] >= 128)
         ld_sector_na(lines + 4 * jj[k] + 2 * half, w[k][0], w[k][1], w[k][2], w[k][3]);
     }
-    qd_load_group<K, false>(q, nullptr, i0 + npair * K, npair, m, qn, cn);
+    sc = sc_next<K, DYN, 16>(sc, ctr);
+    qd_load_group<K, false>(q, nullptr, sc.gb + pw, sc.stride, m, qn, cn);
 #pragma unroll
     for (int k = 0; k < K; ++k) {
       const uint64_t idx = i0 + (uint64_t)k * npair;
@@ -475,8 +484,13 @@ static cudaError_t qd_rank_k(const qr_index* h, const uint64_t* q, const uint8_t
   const uint64_t last = h->n_lines - 1;
   const bool small = h->n < (1ull << 37) && !g_index64;
   if (g_rank_pair) {
-    if (small) k_qd_rank2<K, true><<<g, 256, 0, st>>>(h->lines, h->super, q, c, out, m, last);
-    else       k_qd_rank2<K, false><<<g, 256, 0, st>>>(h->lines, h->super, q, c, out, m, last);
+    const bool dyn = use_dyn_order(m);
+    const uint4* L = h->lines;
+    const uint32_t* S = h->super;
+    if (small) return launch_ordered(k_qd_rank2<K, true, false>, k_qd_rank2<K, true, true>, dyn, h->device, h->sm_count,
+                                     g, st, L, S, q, c, out, m, last);
+    return launch_ordered(k_qd_rank2<K, false, false>, k_qd_rank2<K, false, true>, dyn, h->device, h->sm_count, g, st,
+                          L, S, q, c, out, m, last);
   } else {
     if (small) k_qd_rank<K, true><<<g, 256, 0, st>>>(h->lines, h->super, q, c, out, m, last);
     else       k_qd_rank<K, false><<<g, 256, 0, st>>>(h->lines, h->super, q, c, out, m, last);
@@ -489,8 +503,13 @@ static cudaError_t qd_all4_k(const qr_index* h, const uint64_t* q, uint64_t* out
   const uint64_t last = h->n_lines - 1;
   const bool small = h->n < (1ull << 37) && !g_index64;
   if (g_rank_pair) {
-    if (small) k_qd_all4_2<K, true><<<g, 256, 0, st>>>(h->lines, h->super, q, out4, m, last);
-    else       k_qd_all4_2<K, false><<<g, 256, 0, st>>>(h->lines, h->super, q, out4, m, last);
+    const bool dyn = use_dyn_order(m);
+    const uint4* L = h->lines;
+    const uint32_t* S = h->super;
+    if (small) return launch_ordered(k_qd_all4_2<K, true, false>, k_qd_all4_2<K, true, true>, dyn, h->device,
+                                     h->sm_count, g, st, L, S, q, out4, m, last);
+    return launch_ordered(k_qd_all4_2<K, false, false>, k_qd_all4_2<K, false, true>, dyn, h->device, h->sm_count, g, st,
+                          L, S, q, out4, m, last);
   } else {
     if (small) k_qd_all4<K, true><<<g, 256, 0, st>>>(h->lines, h->super, q, out4, m, last);
     else       k_qd_all4<K, false><<<g, 256, 0, st>>>(h->lines, h->super, q, out4, m, last);
@@ -505,14 +524,14 @@ static cudaError_t qd_gather_k(const qr_index* h, const uint64_t* q, uint64_t* o
   const bool small = h->n < (1ull << 37) && !g_index64;
   if (mode == 2) mode = 0;   // (superblock-inclusive ceiling: BiRank only)
   if (g_rank_pair) {
-    if (small) {
-      if (mode) k_qd_gather2<K, true, 1><<<g, 256, 0, st>>>(h->lines, q, out, m, last);
-      else      k_qd_gather2<K, true, 0><<<g, 256, 0, st>>>(h->lines, q, out, m, last);
-    } else {
-      if (mode) k_qd_gather2<K, false, 1><<<g, 256, 0, st>>>(h->lines, q, out, m, last);
-      else      k_qd_gather2<K, false, 0><<<g, 256, 0, st>>>(h->lines, q, out, m, last);
-    }
-    return cudaGetLastError();
+    const bool dyn = use_dyn_order(m);
+    const uint4* L = h->lines;
+    const int dev = h->device, sms = h->sm_count;
+#define QR_QG2(SQ, MO) launch_ordered(k_qd_gather2<K, SQ, MO, false>, k_qd_gather2<K, SQ, MO, true>, dyn, dev, sms, g, st, \
+                                      L, q, out, m, last)
+    if (small) return mode ? QR_QG2(true, 1) : QR_QG2(true, 0);
+    return mode ? QR_QG2(false, 1) : QR_QG2(false, 0);
+#undef QR_QG2
   }
   if (small) {
     if (mode) k_qd_gather<K, true, 1><<<g, 256, 0, st>>>(h->lines, q, out, m, last);

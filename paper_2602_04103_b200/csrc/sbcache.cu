@@ -27,6 +27,7 @@
 #include <tuple>
 
 #include "qr_common.cuh"
+#include "sched.cuh"
 
 namespace qr {
 
@@ -167,56 +168,6 @@ __device__ __forceinline__ void sc_load_q(const uint64_t* __restrict__ q, uint64
   }
 }
 
-// Work order.  Static (DYN = false): the grid-stride order of k_bi_rank2 — the pair of global
-// lane-pair index P handles queries P, P + npair, ...  Dynamic (DYN = true): each warp takes
-// chunks of SC_CHUNK_STEPS groups of 16 K consecutive queries from a global counter (one
-// atomicAdd per chunk), so SMs that run faster take more chunks instead of waiting at the end.
-constexpr uint32_t SC_CHUNK_STEPS = 8;
-
-struct ScSched {
-  uint64_t gb;          // first query index of the warp's current group
-  uint64_t stride;      // distance between the K sub-groups of a group
-  uint64_t step;        // static: advance per group
-  uint32_t r;           // dynamic: group within the chunk
-};
-
-template <int K, bool DYN>
-__device__ __forceinline__ uint64_t sc_grab(unsigned long long* ctr) {
-  uint64_t b = 0;
-  if ((threadIdx.x & 31u) == 0) b = atomicAdd(ctr, (unsigned long long)(16u * K * SC_CHUNK_STEPS));
-  return __shfl_sync(0xffffffffu, b, 0);
-}
-
-template <int K, bool DYN>
-__device__ __forceinline__ ScSched sc_first(unsigned long long* ctr) {
-  ScSched s;
-  if (DYN) {
-    s.gb = sc_grab<K, DYN>(ctr);
-    s.stride = 16;
-    s.step = 16 * K;
-    s.r = 0;
-  } else {
-    const uint64_t npair = ((uint64_t)gridDim.x * blockDim.x) >> 1;
-    const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-    s.gb = (tid & ~31ull) >> 1;
-    s.stride = npair;
-    s.step = npair * K;
-    s.r = 0;
-  }
-  return s;
-}
-
-template <int K, bool DYN>
-__device__ __forceinline__ ScSched sc_next(ScSched s, unsigned long long* ctr) {
-  if (DYN) {
-    if (++s.r == SC_CHUNK_STEPS) { s.gb = sc_grab<K, DYN>(ctr); s.r = 0; }
-    else s.gb += s.step;
-  } else {
-    s.gb += s.step;
-  }
-  return s;
-}
-
 // VAR bit 0: no superblock read (the shape's own gather ceiling, qr_gather_ceiling mode 3);
 // VAR bit 1: dynamic work order.
 template <int K, int THREADS, bool HAS_C, int VAR>
@@ -230,7 +181,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   sc_preload(pack, half_words, sc_smem, base0, base1);
   const uint32_t half = threadIdx.x & 1u;
   const uint32_t pw = (threadIdx.x & 31u) >> 1;           // pair within the warp
-  ScSched sc = sc_first<K, DYN>(ctr);
+  ScSched sc = sc_first<K, DYN, 16>(ctr);
   uint64_t qn[K];
   sc_load_q<K>(q, sc.gb + pw, sc.stride, m, qn);
   while (sc.gb < m) {
@@ -255,7 +206,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       s[k] = (half && !NOS) ? bi_s_from_pack(jj[k] >> BI_SB_LOG, base0, base1) : 0u;
     }
     const uint64_t stride = sc.stride;
-    sc = sc_next<K, DYN>(sc, ctr);
+    sc = sc_next<K, DYN, 16>(sc, ctr);
     sc_load_q<K>(q, sc.gb + pw, sc.stride, m, qn);
 #pragma unroll
     for (int k = 0; k < K; ++k) {
@@ -315,7 +266,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   sc_preload(pack, half_words, sc_smem, base0, base1);
   const uint32_t half = threadIdx.x & 1u;
   const uint32_t pw = (threadIdx.x & 31u) >> 1;
-  ScSched sc = sc_first<K, DYN>(ctr);
+  ScSched sc = sc_first<K, DYN, 16>(ctr);
   uint64_t qn[K];
   uint32_t cn[K];
   sc_load_qc<K, true>(q, cs, sc.gb + pw, sc.stride, m, qn, cn);
@@ -339,7 +290,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       }
     }
     const uint64_t stride = sc.stride;
-    sc = sc_next<K, DYN>(sc, ctr);
+    sc = sc_next<K, DYN, 16>(sc, ctr);
     sc_load_qc<K, true>(q, cs, sc.gb + pw, sc.stride, m, qn, cn);
 #pragma unroll
     for (int k = 0; k < K; ++k) {
@@ -373,7 +324,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   sc_preload(pack, half_words, sc_smem, base0, base1);
   const uint32_t half = threadIdx.x & 1u;
   const uint32_t pw = (threadIdx.x & 31u) >> 1;
-  ScSched sc = sc_first<K, DYN>(ctr);
+  ScSched sc = sc_first<K, DYN, 16>(ctr);
   uint64_t qn[K];
   uint32_t cn[K];
   sc_load_qc<K, false>(q, nullptr, sc.gb + pw, sc.stride, m, qn, cn);
@@ -398,7 +349,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       s1[k] = qd_s_field(vb, sb & 7u);
     }
     const uint64_t stride = sc.stride;
-    sc = sc_next<K, DYN>(sc, ctr);
+    sc = sc_next<K, DYN, 16>(sc, ctr);
     sc_load_qc<K, false>(q, nullptr, sc.gb + pw, sc.stride, m, qn, cn);
 #pragma unroll
     for (int k = 0; k < K; ++k) {
@@ -490,6 +441,7 @@ bool use_super_pack(const qr_index* h, uint64_t m) {
 
 extern int g_rank_dyn;
 extern int g_rank_smem_k;
+extern int g_rank_smem_threads;
 
 extern int g_rank_smem_clusters;
 
@@ -542,12 +494,16 @@ cudaError_t launch_super_pack_rank(const qr_index* h, const uint64_t* q, const u
   // default K (measured, profiles/r01_smem_probe_k.jsonl): BiRank 4 (fits 64 registers), QuadRank 2
   // (K = 4 spills at the 64-register cap of 1024-thread CTAs)
   const int k = g_rank_smem_k ? g_rank_smem_k : (h->sigma == 2 ? 4 : 2);
-  switch (k) {
-    case 1: sc_launch_kt<1, 1024>(h, q, c, out, m, what, ctr, dyn, st); break;
-    case 2: sc_launch_kt<2, 1024>(h, q, c, out, m, what, ctr, dyn, st); break;
-    case 8: sc_launch_kt<8, 512>(h, q, c, out, m, what, ctr, dyn, st); break;
-    case 6: sc_launch_kt<6, 768>(h, q, c, out, m, what, ctr, dyn, st); break;
-    default: sc_launch_kt<4, 1024>(h, q, c, out, m, what, ctr, dyn, st); break;
+  const int t = g_rank_smem_threads ? g_rank_smem_threads : (k == 6 ? 768 : k == 8 ? 512 : 1024);
+  switch (k * 10000 + t) {
+    case 11024: sc_launch_kt<1, 1024>(h, q, c, out, m, what, ctr, dyn, st); break;
+    case 21024: sc_launch_kt<2, 1024>(h, q, c, out, m, what, ctr, dyn, st); break;
+    case 31024: sc_launch_kt<3, 1024>(h, q, c, out, m, what, ctr, dyn, st); break;
+    case 40768: sc_launch_kt<4, 768>(h, q, c, out, m, what, ctr, dyn, st); break;
+    case 60768: sc_launch_kt<6, 768>(h, q, c, out, m, what, ctr, dyn, st); break;
+    case 80512: sc_launch_kt<8, 512>(h, q, c, out, m, what, ctr, dyn, st); break;
+    case 41024: sc_launch_kt<4, 1024>(h, q, c, out, m, what, ctr, dyn, st); break;
+    default: break;   // not instantiated: rejected by qr_set_tuning's pair check
   }
   e = cudaGetLastError();
   if (dyn) {

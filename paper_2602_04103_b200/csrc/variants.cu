@@ -19,6 +19,7 @@
 #include <cub/device/device_scan.cuh>
 
 #include "qr_common.cuh"
+#include "sched.cuh"
 
 namespace qr {
 
@@ -180,16 +181,17 @@ __device__ __forceinline__ void v_load_q(const uint64_t* __restrict__ q, const u
 
 // BiRank64x2: one lane per query, one 32-B sector.  Count over the sector's 192 data bits
 // (3 words) of [x, 96) or [96, x): mask = prefix(x) XOR prefix(96), the symmetric difference.
-template <int K, int MODE>   // MODE 0: rank; 1: gather ceiling (same load, no popcount)
+template <int K, int MODE, bool DYN>   // MODE 0: rank; 1: gather ceiling (same load, no popcount)
 __global__ void __launch_bounds__(256) k_b64_rank(const uint4* __restrict__ lines, const uint64_t* __restrict__ q,
                                                   const uint8_t* __restrict__ cs, uint64_t* __restrict__ out,
-                                                  uint64_t m, uint64_t last_line) {
-  const uint64_t nthr = (uint64_t)gridDim.x * blockDim.x;
-  uint64_t i0 = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+                                                  uint64_t m, uint64_t last_line, unsigned long long* ctr) {
+  const uint32_t u = sc_unit_in_warp<32>();
+  ScSched sc = sc_first<K, DYN, 32>(ctr);
   uint64_t qn[K];
   uint32_t cn[K];
-  v_load_q<K>(q, cs, i0, nthr, m, qn, cn);
-  for (; i0 < m; i0 += nthr * K) {
+  v_load_q<K>(q, cs, sc.gb + u, sc.stride, m, qn, cn);
+  while (sc.gb < m) {
+    const uint64_t i0 = sc.gb + u, nthr = sc.stride;
     uint64_t qq[K], w[K][4];
     uint32_t xx[K], cc[K];
 #pragma unroll
@@ -204,7 +206,8 @@ __global__ void __launch_bounds__(256) k_b64_rank(const uint4* __restrict__ line
       xx[k] = (uint32_t)r - 192u * h;
       ld_sector_na(lines + 4 * j + 2 * h, w[k][0], w[k][1], w[k][2], w[k][3]);
     }
-    v_load_q<K>(q, cs, i0 + nthr * K, nthr, m, qn, cn);
+    sc = sc_next<K, DYN, 32>(sc, ctr);
+    v_load_q<K>(q, cs, sc.gb + u, sc.stride, m, qn, cn);
 #pragma unroll
     for (int k = 0; k < K; ++k) {
       const uint64_t idx = i0 + (uint64_t)k * nthr;
@@ -226,19 +229,18 @@ __global__ void __launch_bounds__(256) k_b64_rank(const uint4* __restrict__ line
 
 // QuadRank64: lane pairs (lane 0: sector 0 with the four counts, lane 1: sector 1 with the
 // 128 chars) -> one request per query.  ALL4 = 1 returns the four ranks.
-template <int K, int MODE>   // MODE 0: rank(q,c); 1: rank_4(q); 2: gather ceiling
+template <int K, int MODE, bool DYN>   // MODE 0: rank(q,c); 1: rank_4(q); 2: gather ceiling
 __global__ void __launch_bounds__(256) k_q64_rank(const uint4* __restrict__ lines, const uint64_t* __restrict__ q,
                                                   const uint8_t* __restrict__ cs, uint64_t* __restrict__ out,
-                                                  uint64_t m, uint64_t last_line) {
-  const uint64_t npair = ((uint64_t)gridDim.x * blockDim.x) >> 1;
+                                                  uint64_t m, uint64_t last_line, unsigned long long* ctr) {
   const uint32_t half = threadIdx.x & 1u;
-  const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-  uint64_t i0 = tid >> 1;
-  uint64_t iw = (tid & ~31ull) >> 1;
+  const uint32_t u = sc_unit_in_warp<16>();
+  ScSched sc = sc_first<K, DYN, 16>(ctr);
   uint64_t qn[K];
   uint32_t cn[K];
-  v_load_q<K>(q, MODE == 0 ? cs : nullptr, i0, npair, m, qn, cn);
-  for (; iw < m; iw += npair * K, i0 += npair * K) {
+  v_load_q<K>(q, MODE == 0 ? cs : nullptr, sc.gb + u, sc.stride, m, qn, cn);
+  while (sc.gb < m) {
+    const uint64_t i0 = sc.gb + u, npair = sc.stride;
     uint64_t qq[K], w[K][4];
     uint32_t cc[K];
 #pragma unroll
@@ -250,7 +252,8 @@ __global__ void __launch_bounds__(256) k_q64_rank(const uint4* __restrict__ line
       ld_sector_na(lines + 4 * j + 2 * half, w[k][0], w[k][1], w[k][2], w[k][3]);
       if (j << 7 != (qq[k] & ~127ull)) qq[k] = (j << 7) | 127;   // q > n: clamp inside the last line
     }
-    v_load_q<K>(q, MODE == 0 ? cs : nullptr, i0 + npair * K, npair, m, qn, cn);
+    sc = sc_next<K, DYN, 16>(sc, ctr);
+    v_load_q<K>(q, MODE == 0 ? cs : nullptr, sc.gb + u, sc.stride, m, qn, cn);
 #pragma unroll
     for (int k = 0; k < K; ++k) {
       const uint64_t idx = i0 + (uint64_t)k * npair;
@@ -291,21 +294,55 @@ __global__ void __launch_bounds__(256) k_q64_rank(const uint4* __restrict__ line
   }
 }
 
+// persistent grid for the dynamic order: as many 256-thread CTAs as fit at once
+template <typename Kern>
+static unsigned resident_blocks(Kern kern, int sms) {
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0) != cudaSuccess || per_sm <= 0) {
+    cudaGetLastError();
+    per_sm = 1;
+  }
+  return (unsigned)(per_sm * sms);
+}
+
+template <int K, bool DYN>
+static void v_launch2(const qr_index* h, const uint64_t* q, const uint8_t* c, uint64_t* out, uint64_t m, int what,
+                      unsigned long long* ctr, cudaStream_t st) {
+  const uint64_t last = h->n_lines - 1;
+  const bool b64 = h->layout == QR_LAYOUT_BIRANK64X2;
+  // static order: a multi-wave grid sized from the work; dynamic: the resident grid (capped by the work)
+  const uint64_t lanes = b64 ? (m + K - 1) / K : (2 * m + K - 1) / K;
+  unsigned g = grid_stride_blocks(lanes, 256, h->sm_count, g_rank_blocks_per_sm);
+  auto go = [&](auto kern, const uint8_t* cc) {
+    unsigned gg = g;
+    if (DYN) { const unsigned r = resident_blocks(kern, h->sm_count); gg = r < g ? r : g; }
+    kern<<<gg, 256, 0, st>>>(h->lines, q, cc, out, m, last, ctr);
+  };
+  if (b64) {
+    if (what == 2) go(k_b64_rank<K, 1, DYN>, nullptr);
+    else           go(k_b64_rank<K, 0, DYN>, c);
+  } else {
+    if (what == 0)      go(k_q64_rank<K, 0, DYN>, c);
+    else if (what == 1) go(k_q64_rank<K, 1, DYN>, nullptr);
+    else                go(k_q64_rank<K, 2, DYN>, nullptr);
+  }
+}
+
 template <int K>
 static cudaError_t v_launch(const qr_index* h, const uint64_t* q, const uint8_t* c, uint64_t* out, uint64_t m,
                             int what, cudaStream_t st) {
-  const uint64_t last = h->n_lines - 1;
-  if (h->layout == QR_LAYOUT_BIRANK64X2) {
-    unsigned g = grid_stride_blocks((m + K - 1) / K, 256, h->sm_count, g_rank_blocks_per_sm);
-    if (what == 2) k_b64_rank<K, 1><<<g, 256, 0, st>>>(h->lines, q, nullptr, out, m, last);
-    else           k_b64_rank<K, 0><<<g, 256, 0, st>>>(h->lines, q, c, out, m, last);
-  } else {
-    unsigned g = grid_stride_blocks((2 * m + K - 1) / K, 256, h->sm_count, g_rank_blocks_per_sm);
-    if (what == 0)      k_q64_rank<K, 0><<<g, 256, 0, st>>>(h->lines, q, c, out, m, last);
-    else if (what == 1) k_q64_rank<K, 1><<<g, 256, 0, st>>>(h->lines, q, nullptr, out, m, last);
-    else                k_q64_rank<K, 2><<<g, 256, 0, st>>>(h->lines, q, nullptr, out, m, last);
+  if (!use_dyn_order(m)) {
+    v_launch2<K, false>(h, q, c, out, m, what, nullptr, st);
+    return cudaGetLastError();
   }
-  return cudaGetLastError();
+  CounterLease lease;
+  unsigned long long* ctr = nullptr;
+  cudaError_t e;
+  if ((e = lease.acquire(h->device, st, &ctr))) return e;
+  v_launch2<K, true>(h, q, c, out, m, what, ctr, st);
+  e = cudaGetLastError();
+  cudaError_t e2 = lease.release(st);
+  return e ? e : e2;
 }
 
 // what: 0 = rank, 1 = rank_4 (QuadRank64), 2 = gather ceiling

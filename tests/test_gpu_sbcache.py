@@ -281,3 +281,52 @@ def test_smem_limit_never_lowered(cuda, smem_mode):
         torch.cuda.synchronize()
         assert torch.equal(out, out0)
         hs.append(h)
+
+
+@pytest.mark.parametrize("dyn", [0, 1])
+def test_global_kernels_dynamic_order_large_batch(cuda, smem_mode, dyn):
+    """The global-memory lane-pair kernels (rank_smem = 0) and the layout variants take the
+    dynamic work order for batches >= 2^22: every query answered once, bit-identical to the
+    oracle; the gather ceilings load the same words in either order."""
+    torch = _torch()
+    qr.qr_set_tuning("rank_smem", 0)
+    qr.qr_set_tuning("rank_dyn", dyn)
+    m = (1 << 22) + 999
+    n = 21 * S + 5
+    w = gen.bits(110, n)
+    q = gen.queries(111, n, m)
+    ora = oracle.BitsOracle(w, n)
+    ref = ora.rank(q)
+    dq = to_dev(q, cuda)
+    c = (gen.queries(112, 1, m, with_c=True)[1] & 1).astype(np.uint8)
+    for layout in (qr.QR_LAYOUT_BIRANK16, qr.QR_LAYOUT_BIRANK64X2):
+        h = qr.qr_build(w, n, layout)
+        out = torch.empty_like(dq)
+        qr.qr_rank(h, dq, None, out)
+        torch.cuda.synchronize()
+        assert np.array_equal(to_host(out), ref), layout
+        qr.qr_rank(h, dq, to_dev(c, cuda), out)
+        torch.cuda.synchronize()
+        assert np.array_equal(to_host(out), ora.rank(q, c)), layout
+        g = {}
+        for d in (0, 1):
+            qr.qr_set_tuning("rank_dyn", d)
+            qr.qr_gather_ceiling(h, dq, out, 0)
+            torch.cuda.synchronize()
+            g[d] = to_host(out).copy()
+        qr.qr_set_tuning("rank_dyn", dyn)
+        assert np.array_equal(g[0], g[1]), layout
+    n4 = 9 * S4 + 3
+    t = gen.dna(113, n4)
+    q4, c4 = gen.queries(114, n4, m, with_c=True)
+    ora4 = oracle.DnaOracle(t, n4)
+    dq4 = to_dev(q4, cuda)
+    for layout in (qr.QR_LAYOUT_QUADRANK16, qr.QR_LAYOUT_QUADRANK64):
+        h4 = qr.qr_build(t, n4, layout)
+        o = torch.empty_like(dq4)
+        qr.qr_rank(h4, dq4, to_dev(c4, cuda), o)
+        o4 = torch.empty((m, 4), dtype=torch.uint64, device=cuda)
+        qr.qr_rank_all4(h4, dq4, o4)
+        torch.cuda.synchronize()
+        assert np.array_equal(to_host(o), ora4.rank(q4, c4)), layout
+        assert np.array_equal(to_host(o4), ora4.rank_all4(q4)), layout

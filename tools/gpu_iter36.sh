@@ -1,0 +1,7 @@
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out
+make -s all > gpurun_out/make.log 2>&1
+timeout 900 python tools/variant_probe.py > gpurun_out/variant_probe.jsonl 2>&1
+echo "probe exit $?" >> gpurun_out/variant_probe.jsonl
+timeout 1500 python -m pytest tests/test_gpu_variants.py tests/test_gpu_sbcache.py -q --timeout 1200 -x -rf > gpurun_out/pytest_var.log 2>&1
+echo "pytest exit $?" >> gpurun_out/pytest_var.log
