@@ -8,7 +8,7 @@ NVCC    ?= /usr/local/cuda/bin/nvcc
 HOSTCC  := gcc
 ARCH    := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS := -O3 -lineinfo $(ARCH) -std=c++17 -Xcompiler -fPIC -Xcompiler -fvisibility=hidden \
-           -Xptxas -v --expt-relaxed-constexpr -Iinclude
+           -Xptxas -v --expt-relaxed-constexpr -Iinclude $(QR_EXTRA)
 CFLAGS  := -O2 -fPIC -fopenmp -std=c11 -Wall -Wno-unused-function
 
 PKG     := paper_2602_04103_b200

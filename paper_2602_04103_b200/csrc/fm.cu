@@ -412,9 +412,12 @@ __device__ __forceinline__ uint32_t kmer_key_rc(int K, PatWindow& P, const uint8
 // lane had ~4 patterns of very different lengths (exact vs random, 24 vs 6 steps) and warps ran
 // with 19 of 32 lanes active on average (ncu source page, profiles/r01_ncu_cluster.md capture).
 constexpr uint32_t FM_CHUNK = 64;
+#ifndef QR_FM_MINB
+#define QR_FM_MINB 4
+#endif
 
 template <bool FIXED, bool WORK, int STRANDS, bool LEAN, int SMS, bool DYN>
-__global__ void __launch_bounds__(256, 4) k_fm_count(FmParams F, const uint8_t* __restrict__ pat,
+__global__ void __launch_bounds__(256, QR_FM_MINB) k_fm_count(FmParams F, const uint8_t* __restrict__ pat,
                                                      const uint64_t* __restrict__ offs, const uint32_t* __restrict__ lens,
                                                      uint32_t fixed_len, uint32_t* __restrict__ out,
                                                      uint32_t* __restrict__ out_rc, uint64_t m,
