@@ -566,15 +566,32 @@ __device__ __forceinline__ uint32_t fm_continue(const FmParams& F, PatWindow& P,
   return lo < hi ? hi - lo : 0u;
 }
 
+// Next pattern index of a lane.  Static: grid stride.  Dynamic (ctr != null): the lanes that reach
+// this point together (__activemask) take consecutive indices with one atomicAdd by the first of
+// them, so a lane that finishes its pattern starts another at once instead of idling until the
+// slowest pattern of the static assignment (the work per pattern varies by branch count).
+__device__ __forceinline__ uint64_t approx_next(unsigned long long* ctr, uint64_t cur, uint64_t stride) {
+  if (!ctr) return cur + stride;
+  const uint32_t am = __activemask();
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t leader = __ffs(am) - 1u;
+  unsigned long long b = 0;
+  if (lane == leader) b = atomicAdd(ctr, (unsigned long long)__popc(am));
+  b = __shfl_sync(am, b, leader);
+  return b + __popc(am & ((1u << lane) - 1u));
+}
+
 template <bool FIXED>
 __global__ void __launch_bounds__(256) k_fm_approx1(FmParams F, const uint8_t* __restrict__ pat,
                                                     const uint64_t* __restrict__ offs,
                                                     const uint32_t* __restrict__ lens, uint32_t fixed_len,
-                                                    uint32_t* __restrict__ out, uint64_t m) {
+                                                    uint32_t* __restrict__ out, uint64_t m,
+                                                    unsigned long long* __restrict__ ctr) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   const uint4 C4 = __ldg(reinterpret_cast<const uint4*>(F.Ct));
   const uint32_t Cs[4] = {C4.x, C4.y, C4.z, C4.w};
-  for (uint64_t pi = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; pi < m; pi += stride) {
+  for (uint64_t pi = ctr ? approx_next(ctr, 0, 0) : blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; pi < m;
+       pi = approx_next(ctr, pi, stride)) {
     const uint32_t len = FIXED ? fixed_len : lens[pi];
     const uint8_t* p = pat + (FIXED ? pi * (uint64_t)fixed_len : offs[pi]);
     PatWindow P;
@@ -732,6 +749,31 @@ static cudaError_t launch_fm(const qr_fm* fm, bool lean, unsigned g, cudaStream_
   return e;
 }
 
+template <bool FIXED>
+static cudaError_t launch_approx(const qr_fm* fm, unsigned g, cudaStream_t st, const FmParams& F, const uint8_t* pat,
+                                 const uint64_t* offs, const uint32_t* lens, uint32_t fixed_len, uint32_t* out,
+                                 uint64_t m) {
+  auto kern = k_fm_approx1<FIXED>;
+  if (!g_fm_dyn) {
+    kern<<<g, 256, 0, st>>>(F, pat, offs, lens, fixed_len, out, m, nullptr);
+    return cudaGetLastError();
+  }
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0) != cudaSuccess || per_sm <= 0) {
+    cudaGetLastError();
+    per_sm = 1;
+  }
+  const unsigned res = (unsigned)per_sm * (unsigned)fm->bwt->sm_count;
+  CounterLease lease;
+  unsigned long long* ctr = nullptr;
+  cudaError_t e = lease.acquire(fm->bwt->device, st, &ctr);
+  if (e) return e;
+  kern<<<res < g ? res : g, 256, 0, st>>>(F, pat, offs, lens, fixed_len, out, m, ctr);
+  e = cudaGetLastError();
+  cudaError_t e2 = lease.release(st);
+  return e ? e : e2;
+}
+
 qr_status fm_count_device(const qr_fm* fm, const uint8_t* pat, const uint32_t* lengths, uint32_t fixed_len,
                           uint32_t* out, uint32_t* out_rc, uint64_t m, uint64_t* work, cudaStream_t st, int approx) {
   if (m == 0) return QR_OK;
@@ -742,7 +784,7 @@ qr_status fm_count_device(const qr_fm* fm, const uint8_t* pat, const uint32_t* l
   unsigned long long* w = reinterpret_cast<unsigned long long*>(work);
   cudaError_t e;
   if (!lengths) {
-    if (approx) { k_fm_approx1<true><<<g, 256, 0, st>>>(F, pat, nullptr, nullptr, fixed_len, out, m); e = cudaGetLastError(); }
+    if (approx) e = launch_approx<true>(fm, g, st, F, pat, nullptr, nullptr, fixed_len, out, m);
     else if (work) e = launch_fm<true, true>(fm, use_lean(fm), g, st, F, pat, nullptr, nullptr, fixed_len, out, out_rc, m, w);
     else      e = launch_fm<true, false>(fm, use_lean(fm), g, st, F, pat, nullptr, nullptr, fixed_len, out, out_rc, m, w);
     if (e) return cuda_fail(e, "k_fm_count");
@@ -758,7 +800,7 @@ qr_status fm_count_device(const qr_fm* fm, const uint8_t* pat, const uint32_t* l
   if ((e = cub::DeviceScan::ExclusiveSum(tmp, tb, offs, offs, (int64_t)m, st))) {
     cudaFreeAsync(offs, st); cudaFreeAsync(tmp, st); return cuda_fail(e, "scan");
   }
-  if (approx) { k_fm_approx1<false><<<g, 256, 0, st>>>(F, pat, offs, lengths, 0, out, m); e = cudaGetLastError(); }
+  if (approx) e = launch_approx<false>(fm, g, st, F, pat, offs, lengths, 0, out, m);
   else if (work) e = launch_fm<false, true>(fm, use_lean(fm), g, st, F, pat, offs, lengths, 0, out, out_rc, m, w);
   else      e = launch_fm<false, false>(fm, use_lean(fm), g, st, F, pat, offs, lengths, 0, out, out_rc, m, w);
   cudaFreeAsync(offs, st);

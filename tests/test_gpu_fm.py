@@ -21,6 +21,12 @@ def _torch():
     return torch
 
 
+@pytest.fixture
+def fm_dyn_reset():
+    yield
+    qr.qr_set_tuning("fm_dyn", 1)
+
+
 def pack2(sym: np.ndarray) -> np.ndarray:
     n = sym.size
     w = np.zeros((n + 31) // 32 + 1, np.uint64)
@@ -258,11 +264,14 @@ def test_fm_count_both_strands(cuda):
     assert (np.maximum(ref_f, ref_r) >= 1).mean() > 0.1          # error-free reads match one strand
 
 
-@pytest.mark.parametrize("n,kind", [(1, 0), (30, 0), (1000, 0), (60000, 1), (131072 + 5, 0)])
-def test_fm_count_approx_one_mismatch(cuda, n, kind):
-    """<=1-substitution counts (rank_4-driven branching + 8-mer table variants) vs the oracle's
-    direct Hamming-distance scan; max_mismatches=0 equals exact counting."""
+@pytest.mark.parametrize("dyn", [0, 1])
+@pytest.mark.parametrize("n,kind", [(1, 0), (30, 0), (1000, 0), (60000, 1), (131072 + 5, 0), ((1 << 20) + 7, 0)])
+def test_fm_count_approx_one_mismatch(cuda, n, kind, dyn, fm_dyn_reset):
+    """<=1-substitution counts (rank_4-driven branching + k-mer table variants; K = 8, and 10 at
+    n >= 2^20) vs the oracle's direct Hamming-distance scan, static and dynamic pattern order;
+    max_mismatches=0 equals exact counting."""
     torch = _torch()
+    qr.qr_set_tuning("fm_dyn", dyn)
     w = gen.dna(71 + n, n, kind)
     sym = gen.unpack_dna(w, n)
     fm = qr.qr_fm_build(w, n)
