@@ -231,7 +231,9 @@ const char* qr_last_error(void);
  * "fm_step" (0 = auto by L2 residency of the BWT layout, 1 = line-de-duplicating step,
  * 2 = lean step), "fm_smem" (superblock words of the FM count kernel from shared memory: 0 off,
  * 1 auto (default: the raw array or the packed table when either fits 48 KB per CTA), 2 the
- * packed table whenever it fits a CTA),
+ * packed table whenever it fits a CTA), "fm_dyn" (1 default: persistent grid, warps take
+ * pattern chunks from a global counter; 0: static grid stride), "fm_seed" (k-mer seeds computed
+ * by a parallel pre-pass: 0 auto = when the BWT layout fits half the L2, 1 never, 2 always),
  * "index64" (1: always use the 64-bit line-index path that n >= 2^36 (sigma=2) / 2^37
  * (sigma=4) selects, so that it can be tested on small n),
  * "l2_fetch_granularity" (cudaLimitMaxL2FetchGranularity of the current device, bytes),

@@ -23,6 +23,7 @@ int g_rank_blocks_per_sm = 64;  // 256-thread CTAs per SM of the grid (several w
 int g_fm_blocks_per_sm = 64;    // 256-thread CTAs per SM of the FM grid (several waves)
 int g_rank_s_lane = 1;
 int g_fm_dyn = 1;               // FM count: 1 = persistent grid + warp chunks from a global counter, 0 = static grid stride
+int g_fm_seed = 0;              // FM seed pre-pass (dynamic order only): 0 auto (L2-resident BWT), 1 never, 2 always
 int g_fm_smem = 1;              // FM superblock words from shared memory: 0 off, 1 auto, 2 packed table whenever it fits
 int g_fm_lean = 0;              // FM step flavour: 0 auto (by L2 residency), 1 de-duplicating, 2 lean
 int g_index64 = 0;              // 1: force the 64-bit line-index path (tests the n >= 2^36/2^37 code on small n)          // lane of a pair that loads the superblock word
@@ -326,6 +327,9 @@ QR_EXPORT qr_status qr_set_tuning(const char* key, int64_t value) {
   } else if (!strcmp(key, "fm_dyn")) {
     if (value != 0 && value != 1) return fail(QR_EINVAL, "fm_dyn must be 0 or 1");
     g_fm_dyn = (int)value;
+  } else if (!strcmp(key, "fm_seed")) {
+    if (value < 0 || value > 2) return fail(QR_EINVAL, "fm_seed must be 0 (auto), 1 (never) or 2 (always)");
+    g_fm_seed = (int)value;
   } else if (!strcmp(key, "fm_smem")) {
     if (value < 0 || value > 2) return fail(QR_EINVAL, "fm_smem must be 0 (off), 1 (auto) or 2 (packed)");
     g_fm_smem = (int)value;

@@ -11,6 +11,8 @@
 // a lane refills itself from its grid-stride pattern sequence as soon as its pattern finishes,
 // so lanes never wait for the slowest pattern of a static batch (the GPU analogue of the
 // paper's swap-pop active list).
+#include <mutex>
+
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 
@@ -404,6 +406,31 @@ __device__ __forceinline__ uint32_t kmer_key_rc(int K, PatWindow& P, const uint8
 
 // 4 resident CTAs (64 registers): capping registers for 6 or 8 CTAs/SM spills and runs 2-4x
 // slower on configs[3]/[4] (profiles/r01_fm_occupancy_sweep.jsonl).
+// Seed pre-pass of the dynamic-order count kernel: one thread per task computes the k-mer table
+// interval of its (virtual) pattern — the key of the last K symbols, or of the reverse
+// complement's, and one table lookup — fully in parallel, so that the search loop's refill path
+// is a single 8-byte load.  Inline seeding ran in ~94% of the loop iterations with ~3 of 32
+// lanes active and cost ~40% of the kernel's instructions (ncu source page, configs[3]).
+template <bool FIXED, int STRANDS>
+__global__ void __launch_bounds__(256) k_fm_seed(FmParams F, const uint8_t* __restrict__ pat,
+                                                 const uint64_t* __restrict__ offs, const uint32_t* __restrict__ lens,
+                                                 uint32_t fixed_len, uint64_t m, uint2* __restrict__ seeds) {
+  const uint64_t ntask = m * STRANDS;
+  for (uint64_t ti = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; ti < ntask; ti += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t pi = STRANDS == 2 ? ti >> 1 : ti;
+    const uint32_t rc = STRANDS == 2 ? (uint32_t)(ti & 1) : 0u;
+    const uint32_t len = FIXED ? fixed_len : lens[pi];
+    const uint8_t* p = pat + (FIXED ? pi * (uint64_t)fixed_len : offs[pi]);
+    uint2 iv = make_uint2(0u, (uint32_t)F.N);
+    if (F.K && len >= (uint32_t)F.K) {
+      PatWindow P;
+      P.reset(p);
+      iv = __ldg(F.kmer + (rc ? kmer_key_rc(F.K, P, p, len) : kmer_key(F.K, P, p, len)));
+    }
+    seeds[ti] = iv;
+  }
+}
+
 // Work order.  DYN = false: the lane's own grid-stride task sequence (ti, ti + stride, ...) over
 // a multi-wave grid.  DYN = true (default): a persistent grid whose warps take chunks of
 // FM_CHUNK tasks from a global counter (one atomicAdd per chunk); in every loop iteration the
@@ -422,7 +449,8 @@ __global__ void __launch_bounds__(256, QR_FM_MINB) k_fm_count(FmParams F, const 
                                                      uint32_t fixed_len, uint32_t* __restrict__ out,
                                                      uint32_t* __restrict__ out_rc, uint64_t m,
                                                      unsigned long long* __restrict__ work,
-                                                     unsigned long long* __restrict__ ctr) {
+                                                     unsigned long long* __restrict__ ctr,
+                                                     const uint2* __restrict__ seeds) {
   fm_preload_super<SMS>(F);
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   const uint64_t ntask = m * STRANDS;
@@ -439,14 +467,16 @@ __global__ void __launch_bounds__(256, QR_FM_MINB) k_fm_count(FmParams F, const 
     len = FIXED ? fixed_len : lens[pi];
     const uint8_t* p = pat + (FIXED ? pi * (uint64_t)fixed_len : offs[pi]);
     P.reset(p);
-    if (F.K && len >= (uint32_t)F.K) {
-      uint2 iv = __ldg(F.kmer + (rc ? kmer_key_rc(F.K, P, p, len) : kmer_key(F.K, P, p, len)));
-      lo = iv.x; hi = iv.y;
-      k = (int64_t)len - 1 - F.K;
-    } else {
-      lo = 0; hi = (uint32_t)F.N;
-      k = (int64_t)len - 1;
-    }
+    const bool tab = F.K && len >= (uint32_t)F.K;
+    uint2 iv;
+    if (DYN && seeds) iv = __ldg(seeds + ti);             // precomputed by k_fm_seed
+    else iv = tab ? __ldg(F.kmer + (rc ? kmer_key_rc(F.K, P, p, len) : kmer_key(F.K, P, p, len)))
+                  : make_uint2(0u, (uint32_t)F.N);
+    lo = iv.x; hi = iv.y;
+    k = (int64_t)len - 1 - (tab ? F.K : 0);
+    // issue the load of the first searched symbol's word now, so that it overlaps the seed load
+    // instead of following it (the first step's symbol is otherwise a dependent miss)
+    if (DYN && seeds && k >= 0) (void)P.at(rc ? (int64_t)len - 1 - k : k);
   };
   auto step = [&]() {                                    // one backward step (LF mapping)
     const uint32_t c = rc ? 3u - P.at((int64_t)len - 1 - k) : P.at(k);
@@ -664,10 +694,13 @@ int l2_bytes(int device);
 // (no line de-duplication); it wins when the BWT layout is L2-resident (instruction bound,
 // configs[3]: 4.55 -> 5.53 G patterns/s) and loses when it is HBM-resident (request bound,
 // configs[4]: 0.81 -> 0.76).  Auto = lean iff the layout fits in half of the L2.
+static bool bwt_l2_resident(const qr_fm* fm) {
+  return fm->bwt->n_lines * 64 <= (uint64_t)l2_bytes(fm->bwt->device) / 2;
+}
 static bool use_lean(const qr_fm* fm) {
   if (g_fm_lean == 1) return false;
   if (g_fm_lean == 2) return true;
-  return fm->bwt->n_lines * 64 <= (uint64_t)l2_bytes(fm->bwt->device) / 2;
+  return bwt_l2_resident(fm);
 }
 
 extern int g_fm_smem;
@@ -693,9 +726,12 @@ static int fm_smem_mode(const qr_fm* fm, size_t* bytes) {
 template <bool FIXED, bool WORK, int STRANDS, bool LEAN, int SMS>
 static void launch_fm1(unsigned g, size_t smem, cudaStream_t st, const FmParams& F, const uint8_t* pat,
                        const uint64_t* offs, const uint32_t* lens, uint32_t fixed_len, uint32_t* out, uint32_t* out_rc,
-                       uint64_t m, unsigned long long* w, unsigned long long* ctr, int sms) {
+                       uint64_t m, unsigned long long* w, unsigned long long* ctr, int sms, uint2* seeds) {
   if (ctr) {
     auto kern = k_fm_count<FIXED, WORK, STRANDS, LEAN, SMS, true>;
+    if (seeds)
+      k_fm_seed<FIXED, STRANDS><<<grid_stride_blocks(m * STRANDS, 256, sms, 16), 256, 0, st>>>(F, pat, offs, lens,
+                                                                                             fixed_len, m, seeds);
     if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int per_sm = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem) != cudaSuccess || per_sm <= 0) {
@@ -704,24 +740,42 @@ static void launch_fm1(unsigned g, size_t smem, cudaStream_t st, const FmParams&
     }
     const uint64_t need = (m * STRANDS + 255) / 256;     // no more CTAs than tasks / 256
     unsigned gp = (unsigned)((uint64_t)per_sm * sms < need ? (uint64_t)per_sm * sms : (need ? need : 1));
-    kern<<<gp, 256, smem, st>>>(F, pat, offs, lens, fixed_len, out, out_rc, m, w, ctr);
+    kern<<<gp, 256, smem, st>>>(F, pat, offs, lens, fixed_len, out, out_rc, m, w, ctr, seeds);
   } else {
     auto kern = k_fm_count<FIXED, WORK, STRANDS, LEAN, SMS, false>;
     if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    kern<<<g, 256, smem, st>>>(F, pat, offs, lens, fixed_len, out, out_rc, m, w, nullptr);
+    kern<<<g, 256, smem, st>>>(F, pat, offs, lens, fixed_len, out, out_rc, m, w, nullptr, nullptr);
   }
 }
 
 template <bool FIXED, bool WORK, int STRANDS, bool LEAN>
 static void launch_fm2(int sms_mode, unsigned g, size_t smem, cudaStream_t st, const FmParams& F, const uint8_t* pat,
                        const uint64_t* offs, const uint32_t* lens, uint32_t fixed_len, uint32_t* out, uint32_t* out_rc,
-                       uint64_t m, unsigned long long* w, unsigned long long* ctr, int sms) {
-  if (sms_mode == 1)      launch_fm1<FIXED, WORK, STRANDS, LEAN, 1>(g, smem, st, F, pat, offs, lens, fixed_len, out, out_rc, m, w, ctr, sms);
-  else if (sms_mode == 2) launch_fm1<FIXED, WORK, STRANDS, LEAN, 2>(g, smem, st, F, pat, offs, lens, fixed_len, out, out_rc, m, w, ctr, sms);
-  else                    launch_fm1<FIXED, WORK, STRANDS, LEAN, 0>(g, 0, st, F, pat, offs, lens, fixed_len, out, out_rc, m, w, ctr, sms);
+                       uint64_t m, unsigned long long* w, unsigned long long* ctr, int sms, uint2* seeds) {
+  if (sms_mode == 1)      launch_fm1<FIXED, WORK, STRANDS, LEAN, 1>(g, smem, st, F, pat, offs, lens, fixed_len, out, out_rc, m, w, ctr, sms, seeds);
+  else if (sms_mode == 2) launch_fm1<FIXED, WORK, STRANDS, LEAN, 2>(g, smem, st, F, pat, offs, lens, fixed_len, out, out_rc, m, w, ctr, sms, seeds);
+  else                    launch_fm1<FIXED, WORK, STRANDS, LEAN, 0>(g, 0, st, F, pat, offs, lens, fixed_len, out, out_rc, m, w, ctr, sms, seeds);
 }
 
 extern int g_fm_dyn;
+extern int g_fm_seed;
+
+// Keep up to 8 GiB of freed stream-ordered allocations in the device's default pool (its default
+// release threshold of 0 returns them to the driver at every synchronisation, so a per-call
+// scratch buffer would be re-mapped on every call).
+static void keep_pool_memory(int device) {
+  static std::mutex mu;
+  static bool done[64] = {};
+  std::lock_guard<std::mutex> g(mu);
+  if (device < 0 || device >= 64 || done[device]) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    uint64_t thr = 8ull << 30;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  cudaGetLastError();
+  done[device] = true;
+}
 
 template <bool FIXED, bool WORK>
 static cudaError_t launch_fm(const qr_fm* fm, bool lean, unsigned g, cudaStream_t st, const FmParams& F,
@@ -731,21 +785,32 @@ static cudaError_t launch_fm(const qr_fm* fm, bool lean, unsigned g, cudaStream_
   const int sm = fm_smem_mode(fm, &smem);
   CounterLease lease;
   unsigned long long* ctr = nullptr;
+  uint2* seeds = nullptr;
   cudaError_t e;
-  if (g_fm_dyn && (e = lease.acquire(fm->bwt->device, st, &ctr))) return e;
+  if (g_fm_dyn) {
+    // seed pre-pass: pays when the search is instruction-bound (L2-resident BWT: configs[3] 6.57
+    // -> 7.21 G patterns/s) and costs when it is latency-bound (HBM: configs[4] 0.99 -> 0.86)
+    const bool pre = g_fm_seed == 2 || (g_fm_seed == 0 && bwt_l2_resident(fm));
+    if (pre) {
+      keep_pool_memory(fm->bwt->device);
+      if ((e = cudaMallocAsync((void**)&seeds, m * (out_rc ? 2 : 1) * sizeof(uint2), st))) return e;
+    }
+    if ((e = lease.acquire(fm->bwt->device, st, &ctr))) { if (seeds) cudaFreeAsync(seeds, st); return e; }
+  }
   const int sms = fm->bwt->sm_count;
   if (lean) {
-    if (out_rc) launch_fm2<FIXED, WORK, 2, true>(sm, g, smem, st, F, pat, offs, lens, fixed_len, out, out_rc, m, w, ctr, sms);
-    else        launch_fm2<FIXED, WORK, 1, true>(sm, g, smem, st, F, pat, offs, lens, fixed_len, out, out_rc, m, w, ctr, sms);
+    if (out_rc) launch_fm2<FIXED, WORK, 2, true>(sm, g, smem, st, F, pat, offs, lens, fixed_len, out, out_rc, m, w, ctr, sms, seeds);
+    else        launch_fm2<FIXED, WORK, 1, true>(sm, g, smem, st, F, pat, offs, lens, fixed_len, out, out_rc, m, w, ctr, sms, seeds);
   } else {
-    if (out_rc) launch_fm2<FIXED, WORK, 2, false>(sm, g, smem, st, F, pat, offs, lens, fixed_len, out, out_rc, m, w, ctr, sms);
-    else        launch_fm2<FIXED, WORK, 1, false>(sm, g, smem, st, F, pat, offs, lens, fixed_len, out, out_rc, m, w, ctr, sms);
+    if (out_rc) launch_fm2<FIXED, WORK, 2, false>(sm, g, smem, st, F, pat, offs, lens, fixed_len, out, out_rc, m, w, ctr, sms, seeds);
+    else        launch_fm2<FIXED, WORK, 1, false>(sm, g, smem, st, F, pat, offs, lens, fixed_len, out, out_rc, m, w, ctr, sms, seeds);
   }
   e = cudaGetLastError();
   if (ctr) {
     cudaError_t e2 = lease.release(st);
     if (!e) e = e2;
   }
+  if (seeds) cudaFreeAsync(seeds, st);
   return e;
 }
 

@@ -399,12 +399,13 @@ def test_fm_superblock_source_does_not_change_results(cuda, fm_smem, step):
     assert np.array_equal(to_host(dr).view(np.uint32), ref_rc)
 
 
-@pytest.mark.parametrize("dyn", [0, 1])
+@pytest.mark.parametrize("dyn,seed", [(0, 0), (1, 1), (1, 2)])
 @pytest.mark.parametrize("m", [1, 31, 63, 64, 65, 4097])
-def test_fm_work_order_covers_every_task(cuda, dyn, m):
-    """Static grid-stride order (0) and the persistent warp-chunk order (1, default) must count
-    every pattern exactly once, for batch sizes around the chunk size (64) and the warp size,
-    single strand and both strands (2m tasks), variable lengths."""
+def test_fm_work_order_covers_every_task(cuda, dyn, seed, m):
+    """Static grid-stride order (0) and the persistent warp-chunk order (1, default; seeds
+    computed inline (fm_seed 1) or by the parallel pre-pass (2)) must count every pattern exactly
+    once, for batch sizes around the chunk size (64) and the warp size, single strand and both
+    strands (2m tasks), variable lengths."""
     torch = _torch()
     n = 120000
     w = gen.dna(41, n, 0)
@@ -420,6 +421,7 @@ def test_fm_work_order_covers_every_task(cuda, dyn, m):
     rcat, roff, rlens = oracle.pack_patterns(rc_pats)
     ref_rc = ora.count(rcat, roff, rlens)
     qr.qr_set_tuning("fm_dyn", dyn)
+    qr.qr_set_tuning("fm_seed", seed)
     try:
         d = torch.full((m,), -1, dtype=torch.int32, device=cuda)
         qr.qr_fm_count(fm, to_dev(cat, cuda), to_dev(lens, cuda), 0, d, m)
@@ -429,6 +431,7 @@ def test_fm_work_order_covers_every_task(cuda, dyn, m):
         torch.cuda.synchronize()
     finally:
         qr.qr_set_tuning("fm_dyn", 1)
+        qr.qr_set_tuning("fm_seed", 0)
     assert np.array_equal(to_host(d).view(np.uint32), ref)
     assert np.array_equal(to_host(db).view(np.uint32), ref)
     assert np.array_equal(to_host(dr).view(np.uint32), ref_rc)

@@ -22,7 +22,7 @@ for name, n, kind, m, L, seed, pkind in (("c4", 1 << 26, 0, 10**7, 32, 4, 0), ("
     pats = torch.empty(m * L, dtype=torch.uint8, device=dev)
     gen.patterns_dev(seed, pkind, m, L, text, n, pats)
     ref = None
-    for K in (8, 12, 13, 14):
+    for K in (8, 12, 14):
         t0 = time.perf_counter()
         fm = qr.qr_fm_build(text, n, kmer_k=K)
         bt = time.perf_counter() - t0
