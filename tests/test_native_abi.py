@@ -81,3 +81,42 @@ def test_binding_rejects_wrong_dtypes():
         qr.qr_rank(h, np.zeros(10, np.uint64), None, np.zeros(5, np.uint64))
     with pytest.raises(qr.QrError):
         qr.qr_rank_all4(h, np.zeros(10, np.uint64), np.zeros(10, np.uint64))
+
+
+def test_tuning_knob_validation():
+    """Every launch knob accepts its documented values and rejects the rest (QR_EINVAL, message
+    set); the (K, CTA threads) pairs of the cluster kernels are checked against the instantiated
+    set.  Defaults are restored afterwards (knobs are process-wide)."""
+    L = qr.lib()
+    ok = {
+        "rank_smem": [0, 1, 2], "rank_dyn": [0, 1], "rank_smem_k": [0, 1, 2, 3, 4, 6, 8],
+        "rank_smem_clusters": [0, 1, 74, 4096], "fm_dyn": [0, 1], "fm_seed": [0, 1, 2], "fm_smem": [0, 1, 2],
+        "fm_step": [0, 1, 2], "rank_pair": [0, 1], "rank_s_lane": [0, 1], "index64": [0, 1],
+        "rank_k": [1, 2, 4, 8], "rank_blocks_per_sm": [1, 64], "fm_blocks_per_sm": [1, 64],
+        "stage_slots": [2, 4], "stage_chunk": [1024, 1 << 23],
+    }
+    bad = {
+        "rank_smem": [-1, 3], "rank_dyn": [2], "rank_smem_k": [5, 7, 16], "rank_smem_clusters": [-1, 4097],
+        "fm_dyn": [2], "fm_seed": [3], "fm_smem": [3], "fm_step": [3], "rank_pair": [2], "rank_s_lane": [2],
+        "index64": [2], "rank_k": [0, 3], "rank_blocks_per_sm": [0, 65], "fm_blocks_per_sm": [0, 65],
+        "stage_slots": [1, 5], "stage_chunk": [1023],
+    }
+    try:
+        for key, vals in ok.items():
+            for v in vals:
+                assert L.qr_set_tuning(key.encode(), v) == qr.QR_OK, (key, v)
+        for key, vals in bad.items():
+            for v in vals:
+                assert L.qr_set_tuning(key.encode(), v) == qr.QR_EINVAL, (key, v)
+                assert key.encode() in L.qr_last_error() or b"must" in L.qr_last_error(), (key, L.qr_last_error())
+        # (K, threads) pairs: 4 @ 768 and 6 @ 768 and 8 @ 512 exist; 2 @ 768 and 8 @ 1024 do not
+        for k, t, st in ((4, 768, qr.QR_OK), (6, 768, qr.QR_OK), (8, 512, qr.QR_OK), (2, 768, qr.QR_EINVAL),
+                         (8, 1024, qr.QR_EINVAL), (3, 1024, qr.QR_OK)):
+            assert L.qr_set_tuning(b"rank_smem_k", k) == qr.QR_OK
+            assert L.qr_set_tuning(b"rank_smem_threads", t) == st, (k, t)
+    finally:
+        for key, v in (("rank_smem", 1), ("rank_dyn", 1), ("rank_smem_k", 0), ("rank_smem_clusters", 0), ("fm_dyn", 1),
+                       ("fm_seed", 0), ("fm_smem", 1), ("fm_step", 0), ("rank_pair", 1), ("rank_s_lane", 1),
+                       ("index64", 0), ("rank_k", 2), ("rank_blocks_per_sm", 64), ("fm_blocks_per_sm", 64),
+                       ("stage_slots", 3), ("stage_chunk", 1 << 23)):
+            L.qr_set_tuning(key.encode(), v)
