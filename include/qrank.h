@@ -237,8 +237,13 @@ const char* qr_last_error(void);
  * "index64" (1: always use the 64-bit line-index path that n >= 2^36 (sigma=2) / 2^37
  * (sigma=4) selects, so that it can be tested on small n),
  * "l2_fetch_granularity" (cudaLimitMaxL2FetchGranularity of the current device, bytes),
+ * "rank_pair" (kernel shape: 0 one lane per query, 1 lane pairs, 2 (default) by structure size:
+ * one lane per query while the line array fits 0.6 x L2, lane pairs up to 2.2 x L2, the cluster
+ * kernel beyond), "rank_lane_table" (1 default: the one-lane kernels read the superblock words
+ * from a per-CTA shared-memory copy of the packed table when it is <= 32 KB; 0: from L2),
  * "rank_smem" (superblock words of rank / rank_all4 from the 2-CTA cluster shared-memory
- * table when the handle has one: 0 never, 1 (default) for batches of >= 2^22 queries, 2 always),
+ * table when the handle has one: 0 never, 1 (default) by structure size and for batches of >= 2^22
+ * queries, 2 always),
  * "rank_dyn" (1, default: those kernels take work in chunks from a global counter; 0: static
  * grid-stride order), "rank_smem_k" (their queries per lane pair per group: 0 = auto (BiRank 4,
  * QuadRank 2), 1, 2, 3, 4 with 1024-thread CTAs, 6 with 768, 8 with 512; resets

@@ -314,17 +314,18 @@ __global__ void __launch_bounds__(256) k_bi_gather2(const uint4* __restrict__ li
 extern int g_rank_k;              // tuning knobs (api.cu)
 extern int g_rank_blocks_per_sm;
 extern int g_rank_pair;
+extern int g_rank_lane_table;
 extern int g_index64;
 extern int g_rank_s_lane;
 
 template <int K>
 static cudaError_t bi_rank_k(const qr_index* h, const uint64_t* q, const uint8_t* c, uint64_t* out, uint64_t m,
-                             cudaStream_t st) {
+                             bool pair, cudaStream_t st) {
   const bool small = h->n < (1ull << 36) && !g_index64;
-  const uint64_t per_thread = g_rank_pair ? K : 2 * K;   // pair kernels: 2 threads per query
+  const uint64_t per_thread = pair ? K : 2 * K;          // pair kernels: 2 threads per query
   unsigned g = grid_stride_blocks((2 * m + per_thread - 1) / per_thread, 256, h->sm_count, g_rank_blocks_per_sm);
   const uint64_t last = h->n_lines - 1;
-  if (g_rank_pair) {
+  if (pair) {
     const bool s0 = g_rank_s_lane == 0;
     const bool dyn = use_dyn_order(m);
     const int dev = h->device, sms = h->sm_count;
@@ -352,12 +353,18 @@ static cudaError_t bi_rank_k(const qr_index* h, const uint64_t* q, const uint8_t
 cudaError_t launch_birank_rank(const qr_index* h, const uint64_t* q, const uint8_t* c, uint64_t* out, uint64_t m,
                                cudaStream_t st) {
   if (m == 0) return cudaSuccess;
-  if (use_super_pack(h, m)) return launch_super_pack_rank(h, q, c, out, m, 0, st);
+  const int shape = rank_shape(h, m);
+  if (shape == RANK_CLUSTER) return launch_super_pack_rank(h, q, c, out, m, 0, st);
+  if (shape == RANK_LANE && g_rank_lane_table) {
+    const cudaError_t e = launch_lane_table_rank(h, q, c, out, m, 0, st);
+    if (e != cudaErrorNotSupported) return e;
+  }
+  const bool pair = shape == RANK_PAIR;
   switch (g_rank_k) {
-    case 1: return bi_rank_k<1>(h, q, c, out, m, st);
-    case 2: return bi_rank_k<2>(h, q, c, out, m, st);
-    case 8: return bi_rank_k<8>(h, q, c, out, m, st);
-    default: return bi_rank_k<4>(h, q, c, out, m, st);
+    case 1: return bi_rank_k<1>(h, q, c, out, m, pair, st);
+    case 2: return bi_rank_k<2>(h, q, c, out, m, pair, st);
+    case 8: return bi_rank_k<8>(h, q, c, out, m, pair, st);
+    default: return bi_rank_k<4>(h, q, c, out, m, pair, st);
   }
 }
 

@@ -90,7 +90,10 @@ qr_status fm_count_device(const qr_fm* fm, const uint8_t* pat, const uint32_t* l
 qr_status build_super_pack(qr_index* h, cudaStream_t st);
 uint64_t super_pack_cta_bytes(const qr_index* h);
 int super_pack_clusters(const qr_index* h);
-bool use_super_pack(const qr_index* h, uint64_t m);
+enum { RANK_LANE = 0, RANK_PAIR = 1, RANK_CLUSTER = 2 };
+int rank_shape(const qr_index* h, uint64_t m);
+cudaError_t launch_lane_table_rank(const qr_index* h, const uint64_t* q, const uint8_t* c, uint64_t* out, uint64_t m,
+                                   int what, cudaStream_t st);
 cudaError_t launch_super_pack_rank(const qr_index* h, const uint64_t* q, const uint8_t* c, uint64_t* out, uint64_t m,
                                    int what, cudaStream_t st);
 qr_status birank_build_device(const uint64_t* d_bits, uint64_t n, int device, cudaStream_t st, qr_index** out);

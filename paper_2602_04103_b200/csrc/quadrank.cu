@@ -470,20 +470,21 @@ __global__ void __launch_bounds__(256) k_qd_gather2(const uint4* __restrict__ li
 extern int g_rank_k;
 extern int g_rank_blocks_per_sm;
 extern int g_rank_pair;
+extern int g_rank_lane_table;
 extern int g_index64;
 
 template <int K>
-static unsigned qd_grid(const qr_index* h, uint64_t m) {
-  const uint64_t per_thread = g_rank_pair ? K : 2 * K;
+static unsigned qd_grid(const qr_index* h, uint64_t m, bool pair) {
+  const uint64_t per_thread = pair ? K : 2 * K;
   return grid_stride_blocks((2 * m + per_thread - 1) / per_thread, 256, h->sm_count, g_rank_blocks_per_sm);
 }
 template <int K>
 static cudaError_t qd_rank_k(const qr_index* h, const uint64_t* q, const uint8_t* c, uint64_t* out, uint64_t m,
-                             cudaStream_t st) {
-  unsigned g = qd_grid<K>(h, m);
+                             bool pair, cudaStream_t st) {
+  unsigned g = qd_grid<K>(h, m, pair);
   const uint64_t last = h->n_lines - 1;
   const bool small = h->n < (1ull << 37) && !g_index64;
-  if (g_rank_pair) {
+  if (pair) {
     const bool dyn = use_dyn_order(m);
     const uint4* L = h->lines;
     const uint32_t* S = h->super;
@@ -498,11 +499,12 @@ static cudaError_t qd_rank_k(const qr_index* h, const uint64_t* q, const uint8_t
   return cudaGetLastError();
 }
 template <int K>
-static cudaError_t qd_all4_k(const qr_index* h, const uint64_t* q, uint64_t* out4, uint64_t m, cudaStream_t st) {
-  unsigned g = qd_grid<K>(h, m);
+static cudaError_t qd_all4_k(const qr_index* h, const uint64_t* q, uint64_t* out4, uint64_t m, bool pair,
+                             cudaStream_t st) {
+  unsigned g = qd_grid<K>(h, m, pair);
   const uint64_t last = h->n_lines - 1;
   const bool small = h->n < (1ull << 37) && !g_index64;
-  if (g_rank_pair) {
+  if (pair) {
     const bool dyn = use_dyn_order(m);
     const uint4* L = h->lines;
     const uint32_t* S = h->super;
@@ -519,7 +521,7 @@ static cudaError_t qd_all4_k(const qr_index* h, const uint64_t* q, uint64_t* out
 template <int K>
 static cudaError_t qd_gather_k(const qr_index* h, const uint64_t* q, uint64_t* out, uint64_t m, int mode,
                                cudaStream_t st) {
-  unsigned g = qd_grid<K>(h, m);
+  unsigned g = qd_grid<K>(h, m, g_rank_pair != 0);
   const uint64_t last = h->n_lines - 1;
   const bool small = h->n < (1ull << 37) && !g_index64;
   if (mode == 2) mode = 0;   // (superblock-inclusive ceiling: BiRank only)
@@ -546,22 +548,34 @@ static cudaError_t qd_gather_k(const qr_index* h, const uint64_t* q, uint64_t* o
 cudaError_t launch_quadrank_rank(const qr_index* h, const uint64_t* q, const uint8_t* c, uint64_t* out, uint64_t m,
                                  cudaStream_t st) {
   if (m == 0) return cudaSuccess;
-  if (use_super_pack(h, m)) return launch_super_pack_rank(h, q, c, out, m, 0, st);
+  const int shape = rank_shape(h, m);
+  if (shape == RANK_CLUSTER) return launch_super_pack_rank(h, q, c, out, m, 0, st);
+  if (shape == RANK_LANE && g_rank_lane_table) {
+    const cudaError_t e = launch_lane_table_rank(h, q, c, out, m, 0, st);
+    if (e != cudaErrorNotSupported) return e;
+  }
+  const bool pair = shape == RANK_PAIR;
   switch (g_rank_k) {
-    case 1: return qd_rank_k<1>(h, q, c, out, m, st);
-    case 2: return qd_rank_k<2>(h, q, c, out, m, st);
-    case 8: return qd_rank_k<8>(h, q, c, out, m, st);
-    default: return qd_rank_k<4>(h, q, c, out, m, st);
+    case 1: return qd_rank_k<1>(h, q, c, out, m, pair, st);
+    case 2: return qd_rank_k<2>(h, q, c, out, m, pair, st);
+    case 8: return qd_rank_k<8>(h, q, c, out, m, pair, st);
+    default: return qd_rank_k<4>(h, q, c, out, m, pair, st);
   }
 }
 cudaError_t launch_quadrank_all4(const qr_index* h, const uint64_t* q, uint64_t* out4, uint64_t m, cudaStream_t st) {
   if (m == 0) return cudaSuccess;
-  if (use_super_pack(h, m)) return launch_super_pack_rank(h, q, nullptr, out4, m, 1, st);
+  const int shape = rank_shape(h, m);
+  if (shape == RANK_CLUSTER) return launch_super_pack_rank(h, q, nullptr, out4, m, 1, st);
+  if (shape == RANK_LANE && g_rank_lane_table) {
+    const cudaError_t e = launch_lane_table_rank(h, q, nullptr, out4, m, 1, st);
+    if (e != cudaErrorNotSupported) return e;
+  }
+  const bool pair = shape == RANK_PAIR;
   switch (g_rank_k) {
-    case 1: return qd_all4_k<1>(h, q, out4, m, st);
-    case 2: return qd_all4_k<2>(h, q, out4, m, st);
-    case 8: return qd_all4_k<8>(h, q, out4, m, st);
-    default: return qd_all4_k<4>(h, q, out4, m, st);
+    case 1: return qd_all4_k<1>(h, q, out4, m, pair, st);
+    case 2: return qd_all4_k<2>(h, q, out4, m, pair, st);
+    case 8: return qd_all4_k<8>(h, q, out4, m, pair, st);
+    default: return qd_all4_k<4>(h, q, out4, m, pair, st);
   }
 }
 cudaError_t launch_qd_gather(const qr_index* h, const uint64_t* q, uint64_t* out, uint64_t m, int mode,

@@ -383,6 +383,158 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   cluster_barrier();
 }
 
+// ------------------------------------------------------------------ one lane per query, table per CTA
+// For L2-resident structures (rank_shape LANE) the line requests are cheap L2 hits and the cost
+// is instructions: one lane per query beats lane pairs (135 vs 98 Gq/s at 33 MB, profiles/
+// r01_regime_probe.jsonl).  These kernels take the superblock word from a private copy of the
+// whole packed table in each CTA's shared memory (small at these sizes: <= 32 KB), so that the
+// line is the query's only global request.  Line loads as in k_bi_rank / k_qd_rank: sector 0
+// always, sector 1 for queries right of the anchor (the L1 merges both into one L2 request).
+constexpr uint64_t LANE_TABLE_MAX = 32 * 1024;
+extern int g_rank_blocks_per_sm;
+
+__device__ __forceinline__ void lane_preload(const uint64_t* __restrict__ pack, uint32_t words, uint64_t* smem) {
+  const uint4* src = reinterpret_cast<const uint4*>(pack);
+  uint4* dst = reinterpret_cast<uint4*>(smem);
+  for (uint32_t i = threadIdx.x; i < words / 2; i += blockDim.x) dst[i] = __ldg(src + i);
+  __syncthreads();
+}
+
+// packed BiRank group g lives at part (g & 1), slot g >> 1 (half = slots per part)
+__device__ __forceinline__ uint32_t bi_s_local(const uint64_t* smem, uint32_t half, uint32_t sb) {
+  const uint32_t g = sb / 6u, k = sb - 6u * g;
+  const uint64_t v = smem[(g & 1u) * half + (g >> 1)];
+  const uint32_t lo = (uint32_t)v & 0xffffffu;
+  return k ? lo + ((uint32_t)(v >> (16u + 8u * k)) & 0xffu) : lo;
+}
+
+template <int K, bool HAS_C, bool DYN>
+__global__ void __launch_bounds__(256) k_bi_rank1s(const uint4* __restrict__ lines, const uint64_t* __restrict__ pack,
+                                                   uint32_t words, uint32_t half, const uint64_t* __restrict__ q,
+                                                   const uint8_t* __restrict__ cs, uint64_t* __restrict__ out, uint64_t m,
+                                                   uint64_t last_line, unsigned long long* ctr) {
+  extern __shared__ uint64_t lt_smem[];
+  lane_preload(pack, words, lt_smem);
+  const uint32_t u = sc_unit_in_warp<32>();
+  ScSched sc = sc_first<K, DYN, 32>(ctr);
+  uint64_t qn[K];
+  sc_load_q<K>(q, sc.gb + u, sc.stride, m, qn);
+  while (sc.gb < m) {
+    const uint64_t i0 = sc.gb + u, stride = sc.stride;
+    uint64_t qq[K], a[K][4], b[K][4];
+    uint32_t jj[K], pp[K], s[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      qq[k] = qn[k];
+      uint32_t j = (uint32_t)(qq[k] >> 4) / 31u;                // floor(q/496), q < 2^36
+      j = j > (uint32_t)last_line ? (uint32_t)last_line : j;     // q > n: memory-safe clamp
+      const uint64_t p = 16 + qq[k] - (uint64_t)j * BI_B;
+      pp[k] = p > 511 ? 511u : (uint32_t)p;
+      jj[k] = j;
+      const uint4* ln = lines + 4 * (uint64_t)j;
+      ld_sector_na(ln, a[k][0], a[k][1], a[k][2], a[k][3]);
+      b[k][0] = b[k][1] = b[k][2] = b[k][3] = 0;
+      if (pp[k] >= 256) ld_sector_na(ln + 2, b[k][0], b[k][1], b[k][2], b[k][3]);
+      s[k] = bi_s_local(lt_smem, half, j >> BI_SB_LOG);
+    }
+    sc = sc_next<K, DYN, 32>(sc, ctr);
+    sc_load_q<K>(q, sc.gb + u, sc.stride, m, qn);
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const uint64_t idx = i0 + (uint64_t)k * stride;
+      const bool right = pp[k] >= 256;
+      const int x = (int)(pp[k] & 255u);
+      const uint64_t inv = right ? 0ull : ~0ull;
+      uint32_t cnt = 0;
+#pragma unroll
+      for (int t = 0; t < 4; ++t) cnt += __popcll((right ? b[k][t] : a[k][t]) & (prefix_mask(x, t) ^ inv));
+      const uint64_t base = ((uint64_t)s[k] << BI_SHIFT) + (a[k][0] & 0xffffull);
+      uint64_t r = right ? base + cnt : base - cnt;
+      if (HAS_C) {
+        if (idx < m && cs[idx] == 0) r = qq[k] - r;
+      }
+      if (idx < m) st_stream_u64(out + idx, r);
+    }
+  }
+}
+
+// packed QuadRank group g: 4 u64 (one per symbol) at part (g & 1), slot g >> 1
+__device__ __forceinline__ const uint64_t* qd_group_local(const uint64_t* smem, uint32_t half, uint32_t g) {
+  return smem + 4 * ((g & 1u) * half + (g >> 1));
+}
+
+template <int K, int MODE, bool DYN>   // MODE 0: rank(q,c); 1: rank_4(q)
+__global__ void __launch_bounds__(256) k_qd_rank1s(const uint4* __restrict__ lines, const uint64_t* __restrict__ pack,
+                                                   uint32_t words, uint32_t half, const uint64_t* __restrict__ q,
+                                                   const uint8_t* __restrict__ cs, uint64_t* __restrict__ out, uint64_t m,
+                                                   uint64_t last_line, unsigned long long* ctr) {
+  extern __shared__ uint64_t lt_smem[];
+  lane_preload(pack, words, lt_smem);
+  const uint32_t u = sc_unit_in_warp<32>();
+  ScSched sc = sc_first<K, DYN, 32>(ctr);
+  uint64_t qn[K];
+  uint32_t cn[K];
+  sc_load_qc<K, MODE == 0>(q, cs, sc.gb + u, sc.stride, m, qn, cn);
+  while (sc.gb < m) {
+    const uint64_t i0 = sc.gb + u, stride = sc.stride;
+    uint64_t qq[K], a[K][4], b[K][4];
+    uint32_t jj[K], pp[K], cc[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) { qq[k] = qn[k]; cc[k] = MODE == 0 ? cn[k] : 0u; }
+    qd_locate32<K>(qq, last_line, jj, pp);
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const uint4* ln = lines + 4 * (uint64_t)jj[k];
+      ld_sector_na(ln, a[k][0], a[k][1], a[k][2], a[k][3]);
+      b[k][0] = b[k][1] = b[k][2] = b[k][3] = 0;
+      if (pp[k] >= 128) ld_sector_na(ln + 2, b[k][0], b[k][1], b[k][2], b[k][3]);
+    }
+    sc = sc_next<K, DYN, 32>(sc, ctr);
+    sc_load_qc<K, MODE == 0>(q, cs, sc.gb + u, sc.stride, m, qn, cn);
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const uint64_t idx = i0 + (uint64_t)k * stride;
+      const bool right = pp[k] >= 128;
+      const int x = (int)(pp[k] & 127u);
+      const uint64_t inv = right ? 0ull : ~0ull;
+      const uint64_t* w = right ? b[k] : a[k];
+      const uint32_t sb = jj[k] >> QD_SB_LOG, g = sb >> 3, sk = sb & 7u;
+      const uint64_t* grp = qd_group_local(lt_smem, half, g);
+      if (MODE == 0) {
+        const uint32_t c = cc[k];
+        const uint64_t cl = 0ull - (uint64_t)(c & 1u), ch = 0ull - (uint64_t)(c >> 1);
+        uint32_t cnt = 0;
+#pragma unroll
+        for (int t = 0; t < 2; ++t) cnt += __popcll((w[2 * t] ^ cl) & (w[2 * t + 1] ^ ch) & (prefix_mask(x, t) ^ inv));
+        const uint64_t dw = (c & 2u) ? a[k][1] : a[k][0];
+        const uint64_t delta = (dw >> (16 * (c & 1u))) & 0xffffull;        // u16 slot c + (c & 2)
+        const uint64_t base = ((uint64_t)qd_s_field(grp[c], sk) << QD_SHIFT) + delta;
+        if (idx < m) st_stream_u64(out + idx, right ? base + cnt : base - cnt);
+      } else {
+        uint32_t nl = 0, nh = 0, nt = 0;
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+          const uint64_t msk = prefix_mask(x, t) ^ inv;
+          const uint64_t l = ~w[2 * t] & msk, hh = ~w[2 * t + 1] & msk;   // planes store the negation
+          nl += __popcll(l);
+          nh += __popcll(hh);
+          nt += __popcll(l & hh);
+        }
+        const uint32_t len = right ? (uint32_t)x : 128u - (uint32_t)x;
+        const uint32_t cnt[4] = {len - nl - nh + nt, nl - nt, nh - nt, nt};
+        uint64_t r[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const uint64_t dw = (c & 2) ? a[k][1] : a[k][0];
+          const uint64_t base = ((uint64_t)qd_s_field(grp[c], sk) << QD_SHIFT) + ((dw >> (16 * (c & 1))) & 0xffffull);
+          r[c] = right ? base + cnt[c] : base - cnt[c];
+        }
+        if (idx < m) st_stream_v4u64(out + 4 * idx, r[0], r[1], r[2], r[3]);
+      }
+    }
+  }
+}
+
 // ------------------------------------------------------------------ launchers
 
 extern int g_rank_k;
@@ -431,12 +583,26 @@ int super_pack_clusters(const qr_index* h) {
   return (int)(sc_grid(kern, 1024, super_pack_cta_bytes(h), h->device, h->sm_count) / 2);
 }
 
-// Whether a launch of m queries takes the shared-memory path (g_rank_smem: 0 never, 1 when it
-// pays — large batches, where the table preload is amortised —, 2 whenever the table exists).
-bool use_super_pack(const qr_index* h, uint64_t m) {
-  if (!h->spack || g_index64 || !g_rank_pair || g_rank_smem == 0) return false;
-  if (g_rank_smem == 2) return true;
-  return m >= (1ull << 22);
+int l2_bytes(int device);
+
+// Kernel shape of a rank / rank_4 launch (measured crossovers in
+// profiles/r01_regime_probe.jsonl):
+//   LANE    — one lane per query, superblock word from L2: best while the line array is mostly
+//             L2-resident (<= 0.6 x L2: 135 vs 98 Gq/s for lane pairs at 33 MB);
+//   PAIR    — lane pairs (one L2 request per line), global superblock words, dynamic order:
+//             best up to ~2.2 x L2 (264 MB: 62 vs 54 Gq/s for the cluster kernel);
+//   CLUSTER — lane pairs with the superblock words in 2-CTA cluster shared memory: best on
+//             HBM-resident structures (2 GB: 46.2 vs 38.8 Gq/s), batches >= 2^22.
+// Knobs: rank_pair 0 = always LANE, 1 = PAIR / CLUSTER by rank_smem only, 2 = by size (default);
+// rank_smem 0 = never CLUSTER, 1 = by size and batch, 2 = whenever the table exists.
+int rank_shape(const qr_index* h, uint64_t m) {
+  if (g_rank_pair == 0) return RANK_LANE;
+  const bool can = h->spack && !g_index64;
+  if (can && g_rank_smem == 2) return RANK_CLUSTER;
+  const double lines = (double)h->n_lines * 64.0, l2 = (double)l2_bytes(h->device);
+  if (g_rank_pair == 2 && lines <= 0.6 * l2) return RANK_LANE;
+  if (can && g_rank_smem == 1 && m >= (1ull << 22) && (g_rank_pair == 1 || lines > 2.2 * l2)) return RANK_CLUSTER;
+  return RANK_PAIR;
 }
 
 extern int g_rank_dyn;
@@ -480,6 +646,32 @@ static void sc_launch_kt(const qr_index* h, const uint64_t* q, const uint8_t* c,
     if (dyn) sc_go(k_qd_all4_2c<K, T, true>, T, h, smem, st, L, P, hw, q, out, m, last, ctr);
     else     sc_go(k_qd_all4_2c<K, T, false>, T, h, smem, st, L, P, hw, q, out, m, last, ctr);
   }
+}
+
+// One-lane kernels with the per-CTA table (rank_shape LANE).  Returns cudaErrorNotSupported when
+// the handle has no table small enough (the caller then uses the global-memory lane kernels).
+cudaError_t launch_lane_table_rank(const qr_index* h, const uint64_t* q, const uint8_t* c, uint64_t* out, uint64_t m,
+                                   int what, cudaStream_t st) {
+  if (!h->spack || g_index64) return cudaErrorNotSupported;
+  const uint64_t total = 2 * super_pack_cta_bytes(h);
+  if (total > LANE_TABLE_MAX) return cudaErrorNotSupported;
+  const uint32_t words = (uint32_t)(total / 8), half = (uint32_t)h->spack_half;
+  const uint64_t last = h->n_lines - 1;
+  const bool dyn = use_dyn_order(m);
+  constexpr int K = 2;
+  const unsigned g = grid_stride_blocks((m + K - 1) / K, 256, h->sm_count, g_rank_blocks_per_sm);
+  const uint4* L = h->lines;
+  const uint64_t* P = h->spack;
+  auto go = [&](auto ks, auto kd, const uint8_t* cc) -> cudaError_t {
+    return launch_ordered_smem(ks, kd, dyn, h->device, h->sm_count, g, (size_t)total, st, L, P, words, half, q, cc, out,
+                               m, last);
+  };
+  if (h->sigma == 2) {
+    if (c) return go(k_bi_rank1s<K, true, false>, k_bi_rank1s<K, true, true>, c);
+    return go(k_bi_rank1s<K, false, false>, k_bi_rank1s<K, false, true>, c);
+  }
+  if (what == 0) return go(k_qd_rank1s<K, 0, false>, k_qd_rank1s<K, 0, true>, c);
+  return go(k_qd_rank1s<K, 1, false>, k_qd_rank1s<K, 1, true>, nullptr);
 }
 
 // what: 0 = rank (sigma 2 or 4), 1 = rank_4 (sigma 4), 3 = BiRank gather ceiling of this kernel shape

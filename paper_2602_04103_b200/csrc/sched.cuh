@@ -97,4 +97,28 @@ cudaError_t launch_ordered(KS ks, KD kd, bool dyn, int device, int sms, unsigned
   return e ? e : e2;
 }
 
+// As launch_ordered, with `smem` bytes of dynamic shared memory per CTA (<= 48 KB).
+template <typename KS, typename KD, typename... Args>
+cudaError_t launch_ordered_smem(KS ks, KD kd, bool dyn, int device, int sms, unsigned grid_static, size_t smem,
+                                cudaStream_t st, Args... args) {
+  if (!dyn) {
+    ks<<<grid_static, 256, smem, st>>>(args..., (unsigned long long*)nullptr);
+    return cudaGetLastError();
+  }
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kd, 256, smem) != cudaSuccess || per_sm <= 0) {
+    cudaGetLastError();
+    per_sm = 1;
+  }
+  const unsigned res = (unsigned)per_sm * (unsigned)sms;
+  CounterLease lease;
+  unsigned long long* ctr = nullptr;
+  cudaError_t e = lease.acquire(device, st, &ctr);
+  if (e) return e;
+  kd<<<res < grid_static ? res : grid_static, 256, smem, st>>>(args..., ctr);
+  e = cudaGetLastError();
+  cudaError_t e2 = lease.release(st);
+  return e ? e : e2;
+}
+
 }  // namespace qr

@@ -36,7 +36,7 @@ def test_random_sizes_layouts_knobs(cuda, trial):
     bps = int(rng.choice([1, 3, 16, 64]))
     qr.qr_set_tuning("rank_k", k)
     qr.qr_set_tuning("rank_blocks_per_sm", bps)
-    qr.qr_set_tuning("rank_pair", int(rng.integers(0, 2)))
+    qr.qr_set_tuning("rank_pair", int(rng.integers(0, 3)))
     try:
         h = qr.qr_build(w, n, layout)
         dq = to_dev(q, cuda)
@@ -57,7 +57,7 @@ def test_random_sizes_layouts_knobs(cuda, trial):
     finally:
         qr.qr_set_tuning("rank_k", 2)
         qr.qr_set_tuning("rank_blocks_per_sm", 64)
-        qr.qr_set_tuning("rank_pair", 1)
+        qr.qr_set_tuning("rank_pair", 2)
 
 
 @pytest.mark.parametrize("trial", range(8))

@@ -109,7 +109,7 @@ def test_birank_device_input_and_host_query_path(cuda):
     assert np.array_equal(op.numpy(), ref)
 
 
-@pytest.mark.parametrize("pair", [0, 1])
+@pytest.mark.parametrize("pair", [0, 1, 2])
 @pytest.mark.parametrize("k", [1, 2, 4, 8])
 def test_birank_tuning_does_not_change_results(cuda, k, pair):
     torch = _torch()
@@ -131,13 +131,13 @@ def test_birank_tuning_does_not_change_results(cuda, k, pair):
     finally:
         qr.qr_set_tuning("rank_k", 2)
         qr.qr_set_tuning("rank_blocks_per_sm", 64)
-        qr.qr_set_tuning("rank_pair", 1)
+        qr.qr_set_tuning("rank_pair", 2)
     ora = oracle.BitsOracle(w, n)
     assert np.array_equal(to_host(out), ora.rank(q))
     assert np.array_equal(to_host(out2), ora.rank(q, c))
 
 
-@pytest.mark.parametrize("pair", [0, 1])
+@pytest.mark.parametrize("pair", [0, 1, 2])
 @pytest.mark.parametrize("k", [1, 2, 8])
 def test_quadrank_tuning_does_not_change_results(cuda, k, pair):
     torch = _torch()
@@ -162,7 +162,7 @@ def test_quadrank_tuning_does_not_change_results(cuda, k, pair):
     finally:
         qr.qr_set_tuning("rank_k", 2)
         qr.qr_set_tuning("rank_blocks_per_sm", 64)
-        qr.qr_set_tuning("rank_pair", 1)
+        qr.qr_set_tuning("rank_pair", 2)
     ora = oracle.DnaOracle(w, n)
     assert np.array_equal(to_host(out), ora.rank(q, c))
     assert np.array_equal(to_host(o4), ora.rank_all4(q))
@@ -171,7 +171,7 @@ def test_quadrank_tuning_does_not_change_results(cuda, k, pair):
     assert np.array_equal(to_host(g), np.bitwise_xor.reduce(u64[(q // B4).astype(np.int64)], axis=1))
 
 
-@pytest.mark.parametrize("pair", [0, 1])
+@pytest.mark.parametrize("pair", [0, 1, 2])
 def test_gather_ceiling_loads_the_same_sectors(cuda, pair):
     torch = _torch()
     qr.qr_set_tuning("rank_pair", pair)
@@ -192,7 +192,7 @@ def test_gather_ceiling_loads_the_same_sectors(cuda, pair):
         b = np.bitwise_xor.reduce(u64[j, 4:], axis=1)
         exp = a ^ np.where((p >= 256) | (mode == 1), b, 0).astype(np.uint64)
         assert np.array_equal(to_host(out), exp)
-    qr.qr_set_tuning("rank_pair", 1)
+    qr.qr_set_tuning("rank_pair", 2)
 
 
 # ------------------------------------------------------------------ QuadRank
@@ -341,7 +341,7 @@ def test_edge_cases_and_contract(cuda):
     assert fm2.C == fm.C and fm2.spos == fm.spos
 
 
-@pytest.mark.parametrize("pair", [0, 1])
+@pytest.mark.parametrize("pair", [0, 1, 2])
 def test_index64_path(cuda, pair):
     """The 64-bit line-index path (selected for n >= 2^36 / 2^37) forced on small n: bit-exact."""
     torch = _torch()
@@ -363,7 +363,7 @@ def test_index64_path(cuda, pair):
         torch.cuda.synchronize()
     finally:
         qr.qr_set_tuning("index64", 0)
-        qr.qr_set_tuning("rank_pair", 1)
+        qr.qr_set_tuning("rank_pair", 2)
     assert np.array_equal(to_host(ob), oracle.BitsOracle(w, n).rank(q))
     ora = oracle.DnaOracle(t, n)
     assert np.array_equal(to_host(oq), ora.rank(q, c))

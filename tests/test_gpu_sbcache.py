@@ -330,3 +330,31 @@ def test_global_kernels_dynamic_order_large_batch(cuda, smem_mode, dyn):
         torch.cuda.synchronize()
         assert np.array_equal(to_host(o), ora4.rank(q4, c4)), layout
         assert np.array_equal(to_host(o4), ora4.rank_all4(q4)), layout
+
+
+@pytest.mark.parametrize("lane_table", [0, 1])
+@pytest.mark.parametrize("m", [100003, (1 << 22) + 5])
+def test_lane_kernels_l2_resident(cuda, smem_mode, lane_table, m):
+    """L2-resident structures take one lane per query (rank_shape LANE): superblock words from a
+    per-CTA shared-memory copy of the packed table (rank_lane_table 1, default) or from L2 (0);
+    static (m < 2^22) and dynamic order; rank, rank with c, QuadRank rank and rank_4."""
+    qr.qr_set_tuning("rank_lane_table", lane_table)
+    try:
+        n = 37 * S + 1234
+        w = gen.bits(120, n, 1.0 if m < 200000 else 0.5)
+        q = gen.queries(121, n, m)
+        h = qr.qr_birank_build(w, n)
+        ora = oracle.BitsOracle(w, n)
+        got = _rank(h, q, None, cuda, 1)
+        assert np.array_equal(got, ora.rank(q))
+        c = (gen.queries(122, 1, m, with_c=True)[1] & 1).astype(np.uint8)
+        assert np.array_equal(_rank(h, q, c, cuda, 1), ora.rank(q, c))
+        n4 = 29 * S4 + 77
+        t = gen.dna(123, n4)
+        q4, c4 = gen.queries(124, n4, m, with_c=True)
+        h4 = qr.qr_quadrank_build(t, n4)
+        ora4 = oracle.DnaOracle(t, n4)
+        assert np.array_equal(_rank(h4, q4, c4, cuda, 1), ora4.rank(q4, c4))
+        assert np.array_equal(_rank4(h4, q4, cuda, 1), ora4.rank_all4(q4))
+    finally:
+        qr.qr_set_tuning("rank_lane_table", 1)
