@@ -223,34 +223,45 @@ void qr_fm_free(qr_fm* fm);
 /* Thread-local message of the last failure on this thread ("" if none). */
 const char* qr_last_error(void);
 
-/* Process-wide launch-configuration knobs for measurement sweeps (results never depend on
- * them; not synchronised — set them before issuing work from other threads): "rank_k" (1, 2, 4 or 8 independent queries per thread per iteration),
- * "rank_blocks_per_sm" and "fm_blocks_per_sm" (256-thread CTAs per SM of the grid-stride
- * rank / FM kernels, 1..64), "stage_chunk" (queries per chunk of the staged host path),
- * "stage_slots" (2..4 device buffers / internal streams of the staged host path),
- * "fm_step" (0 = auto by L2 residency of the BWT layout, 1 = line-de-duplicating step,
- * 2 = lean step), "fm_smem" (superblock words of the FM count kernel from shared memory: 0 off,
- * 1 auto (default: the raw array or the packed table when either fits 48 KB per CTA), 2 the
- * packed table whenever it fits a CTA), "fm_dyn" (1 default: persistent grid, warps take
- * pattern chunks from a global counter; 0: static grid stride), "fm_seed" (k-mer seeds computed
- * by a parallel pre-pass: 0 auto = when the BWT layout fits half the L2, 1 never, 2 always),
- * "index64" (1: always use the 64-bit line-index path that n >= 2^36 (sigma=2) / 2^37
- * (sigma=4) selects, so that it can be tested on small n),
- * "l2_fetch_granularity" (cudaLimitMaxL2FetchGranularity of the current device, bytes),
- * "rank_pair" (kernel shape: 0 one lane per query, 1 lane pairs, 2 (default) by structure size:
- * one lane per query while the line array fits 0.6 x L2, lane pairs up to 2.2 x L2, the cluster
- * kernel beyond), "rank_lane_table" (1 default: the one-lane kernels read the superblock words
- * from a per-CTA shared-memory copy of the packed table when it is <= 32 KB; 0: from L2),
- * "rank_smem" (superblock words of rank / rank_all4 from the 2-CTA cluster shared-memory
- * table when the handle has one: 0 never, 1 (default) by structure size and for batches of >= 2^22
- * queries, 2 always),
- * "rank_dyn" (1, default: those kernels take work in chunks from a global counter; 0: static
- * grid-stride order), "rank_smem_k" (their queries per lane pair per group: 0 = auto (BiRank 4,
- * QuadRank 2), 1, 2, 3, 4 with 1024-thread CTAs, 6 with 768, 8 with 512; resets
- * "rank_smem_threads"), "rank_smem_threads" (CTA size for the current K: 1024 for K 1-4, 768 for
- * K 4 or 6, 512 for K 8; 0 = the default for K), "rank_smem_clusters" (0 = as many 2-CTA
- * clusters as fit at once, else that many).
- * QR_EINVAL for an unknown key or out-of-range value. */
+/* Process-wide launch-configuration knobs for measurement sweeps.  Results never depend on
+ * them; they are not synchronised (set them before issuing work from other threads).
+ * QR_EINVAL for an unknown key or an out-of-range value.
+ *
+ * Rank kernel shape:
+ *   "rank_pair"        0 one lane per query, 1 lane pairs, 2 (default) by structure size: one
+ *                      lane per query while the line array fits 0.6 x L2, lane pairs up to
+ *                      2.2 x L2, the cluster kernel beyond.
+ *   "rank_lane_table"  1 (default): the one-lane kernels read the superblock words from a
+ *                      per-CTA shared-memory copy of the packed table when it is <= 32 KB; 0: L2.
+ *   "rank_smem"        the 2-CTA cluster shared-memory kernels: 0 never, 1 (default) by
+ *                      structure size for batches >= 2^22, 2 whenever the table exists.
+ *   "rank_s_lane"      global lane-pair kernels: which lane of a pair loads the superblock word.
+ *   "index64"          1: always the 64-bit line-index path that n >= 2^36 (sigma=2) / 2^37
+ *                      (sigma=4) selects, so that it can be tested on small n.
+ * Rank launch configuration:
+ *   "rank_k"           1, 2, 4, 8: queries per thread (lane pair) per iteration, global kernels.
+ *   "rank_blocks_per_sm", "fm_blocks_per_sm"  1..64: 256-thread CTAs per SM of the static
+ *                      (multi-wave, grid-stride) order.
+ *   "rank_dyn"         1 (default): batches >= 2^22 take work in chunks from a global counter
+ *                      on a resident grid; 0: the static grid-stride order.
+ *   "rank_smem_k"      cluster kernels' queries per lane pair: 0 auto (BiRank 4, QuadRank 2),
+ *                      1-4 with 1024-thread CTAs, 6 with 768, 8 with 512 (resets the next knob).
+ *   "rank_smem_threads"  cluster kernels' CTA size for the current K (1024 for K 1-4, 768 for
+ *                      K 4 or 6, 512 for K 8; 0 = the default for K).
+ *   "rank_smem_clusters" 0: as many 2-CTA clusters as fit at once, else that many.
+ *   "l2_fetch_granularity"  cudaLimitMaxL2FetchGranularity of the current device (bytes).
+ * QuadFm:
+ *   "fm_step"          0 auto by L2 residency of the BWT layout, 1 line-de-duplicating step,
+ *                      2 lean step.
+ *   "fm_dyn"           1 (default): persistent grid, warps take pattern chunks from a global
+ *                      counter; 0: static grid stride.
+ *   "fm_seed"          k-mer seeds by a parallel pre-pass: 0 auto (BWT layout fits half the
+ *                      L2), 1 never, 2 always.
+ *   "fm_smem"          superblock words of the count kernel from shared memory: 0 off, 1 auto
+ *                      (the raw array or the packed table when either fits 48 KB per CTA), 2 the
+ *                      packed table whenever it fits a CTA.
+ * Staged host-pointer path:
+ *   "stage_chunk"      queries per chunk (>= 1024);  "stage_slots"  2..4 buffers / streams. */
 qr_status qr_set_tuning(const char* key, int64_t value);
 
 /* Library version string. */
