@@ -38,6 +38,17 @@ static CtrRing* ctr_ring(int device) {
 }
 
 cudaError_t CounterLease::acquire(int device, cudaStream_t st, unsigned long long** ctr) {
+  // Inside a stream capture (CUDA graphs) the ring's cross-stream event wait is not allowed:
+  // the counter is a stream-ordered allocation of the graph instead (memory node; a graph
+  // exec never runs concurrently with itself), zeroed and freed inside the same capture.
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(st, &cap) == cudaSuccess && cap == cudaStreamCaptureStatusActive) {
+    cudaError_t e = cudaMallocAsync((void**)ctr, CTR_WORDS * sizeof(unsigned long long), st);
+    if (!e) e = cudaMemsetAsync(*ctr, 0, CTR_WORDS * sizeof(unsigned long long), st);
+    if (!e) own = *ctr;
+    return e;
+  }
+  cudaGetLastError();
   CtrRing* r = ctr_ring(device);
   if (!r) return cudaErrorMemoryAllocation;
   r->mu.lock();
@@ -51,6 +62,11 @@ cudaError_t CounterLease::acquire(int device, cudaStream_t st, unsigned long lon
 }
 
 cudaError_t CounterLease::release(cudaStream_t st) {
+  if (own) {
+    cudaError_t e = cudaFreeAsync(own, st);
+    own = nullptr;
+    return e;
+  }
   if (!ring) return cudaSuccess;
   CtrRing* r = static_cast<CtrRing*>(ring);
   cudaError_t e = cudaEventRecord(r->ev[slot], st);

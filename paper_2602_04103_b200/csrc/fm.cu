@@ -763,7 +763,12 @@ extern int g_fm_seed;
 // Keep up to 8 GiB of freed stream-ordered allocations in the device's default pool (its default
 // release threshold of 0 returns them to the driver at every synchronisation, so a per-call
 // scratch buffer would be re-mapped on every call).
-static void keep_pool_memory(int device) {
+static void keep_pool_memory(int device, cudaStream_t st) {
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(st, &cap) != cudaSuccess || cap != cudaStreamCaptureStatusNone) {
+    cudaGetLastError();
+    return;                                  // not during a capture (a device-wide setting)
+  }
   static std::mutex mu;
   static bool done[64] = {};
   std::lock_guard<std::mutex> g(mu);
@@ -792,7 +797,7 @@ static cudaError_t launch_fm(const qr_fm* fm, bool lean, unsigned g, cudaStream_
     // -> 7.21 G patterns/s) and costs when it is latency-bound (HBM: configs[4] 0.99 -> 0.86)
     const bool pre = g_fm_seed == 2 || (g_fm_seed == 0 && bwt_l2_resident(fm));
     if (pre) {
-      keep_pool_memory(fm->bwt->device);
+      keep_pool_memory(fm->bwt->device, st);
       if ((e = cudaMallocAsync((void**)&seeds, m * (out_rc ? 2 : 1) * sizeof(uint2), st))) return e;
     }
     if ((e = lease.acquire(fm->bwt->device, st, &ctr))) { if (seeds) cudaFreeAsync(seeds, st); return e; }

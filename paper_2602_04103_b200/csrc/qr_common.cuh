@@ -104,6 +104,7 @@ qr_status birank_build_device(const uint64_t* d_bits, uint64_t n, int device, cu
 struct CounterLease {
   void* ring = nullptr;
   uint32_t slot = 0;
+  unsigned long long* own = nullptr;   // graph-capture path: a stream-ordered allocation
   cudaError_t acquire(int device, cudaStream_t st, unsigned long long** ctr);
   cudaError_t release(cudaStream_t st);
   ~CounterLease();

@@ -358,3 +358,64 @@ def test_lane_kernels_l2_resident(cuda, smem_mode, lane_table, m):
         assert np.array_equal(_rank4(h4, q4, cuda, 1), ora4.rank_all4(q4))
     finally:
         qr.qr_set_tuning("rank_lane_table", 1)
+
+
+def test_cuda_graph_capture_of_dynamic_order_launches(cuda, smem_mode):
+    """qr_rank (cluster kernel, dynamic order: m >= 2^22), qr_rank_all4 and qr_fm_count captured
+    into CUDA graphs and replayed: the work counters become graph-owned allocations during a
+    capture, so replays give the oracle's answers."""
+    torch = _torch()
+    n = (1 << 27) + 99
+    w = gen.bits(130, n)
+    h = qr.qr_birank_build(w, n)
+    m = (1 << 22) + 3
+    q = gen.queries(131, n, m)
+    ref = oracle.BitsOracle(w, n).rank(q)
+    dq = to_dev(q, cuda)
+    out = torch.zeros_like(dq)
+    s = torch.cuda.Stream()
+    qr.qr_rank(h, dq, None, out, stream=s)            # warm-up outside the capture (one-time setup)
+    torch.cuda.synchronize()
+    for mode in (2, 1):                               # cluster kernel, then the size-chosen shape
+        qr.qr_set_tuning("rank_smem", mode)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            qr.qr_rank(h, dq, None, out, stream=torch.cuda.current_stream())
+        for _ in range(3):
+            out.zero_()
+            g.replay()
+            torch.cuda.synchronize()
+            assert np.array_equal(to_host(out), ref), mode
+    n4 = 7 * S4 + 5
+    t = gen.dna(132, n4)
+    h4 = qr.qr_quadrank_build(t, n4)
+    q4 = gen.queries(133, n4, m)
+    dq4 = to_dev(q4, cuda)
+    o4 = torch.zeros((m, 4), dtype=torch.uint64, device=cuda)
+    qr.qr_rank_all4(h4, dq4, o4, stream=s)
+    torch.cuda.synchronize()
+    g4 = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g4, stream=s):
+        qr.qr_rank_all4(h4, dq4, o4, stream=torch.cuda.current_stream())
+    o4.zero_()
+    g4.replay()
+    torch.cuda.synchronize()
+    assert np.array_equal(to_host(o4), oracle.DnaOracle(t, n4).rank_all4(q4))
+    nf = 200000
+    tf = gen.dna(134, nf)
+    fm = qr.qr_fm_build(tf, nf)
+    L, mp = 24, 5000
+    pats = gen.patterns(135, 0, mp, L, tf, nf)
+    dp = to_dev(pats, cuda)
+    d = torch.zeros(mp, dtype=torch.int32, device=cuda)
+    qr.qr_fm_count(fm, dp, None, L, d, mp, stream=s)
+    torch.cuda.synchronize()
+    gf = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(gf, stream=s):
+        qr.qr_fm_count(fm, dp, None, L, d, mp, stream=torch.cuda.current_stream())
+    d.zero_()
+    gf.replay()
+    torch.cuda.synchronize()
+    ref_fm = oracle.FmOracle(gen.unpack_dna(tf, nf)).count(pats, np.arange(mp, dtype=np.uint64) * L,
+                                                          np.full(mp, L, np.uint32))
+    assert np.array_equal(to_host(d).view(np.uint32), ref_fm)
