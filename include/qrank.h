@@ -49,16 +49,19 @@ typedef int32_t qr_status;
 
 typedef struct qr_index qr_index;   /* a rank layout (QR_LAYOUT_*)                             */
 
-/* Rank layouts.  BIRANK16 / QUADRANK16 are the paper's headline structures (§3, §4); the two
- * others are its no-L1-array variants (NEXT §8(f)4): BiRank64x2 (33.3%: each
- * 32-B sector = u64 rank to the sector's middle + 192 data bits, so a query reads one sector
- * and no superblock word) and QuadRank64 (100%: four u64 ranks to the middle
- * of 128 characters in sector 0, the characters as two transposed negated plane pairs in
- * sector 1).  All layouts answer every query identically. */
+/* Rank layouts.  BIRANK16 / QUADRANK16 are the paper's headline structures (§3, §4); the others
+ * are variants the paper evaluates (NEXT §8(f)4): BiRank64x2 (33.3%: each 32-B
+ * sector = u64 rank to the sector's middle + 192 data bits, so a query reads one sector and no
+ * superblock word), QuadRank64 (100%: four u64 ranks to the middle of 128
+ * characters in sector 0, the characters as two transposed negated plane pairs in sector 1) and
+ * BiRank16x2 (6.72%: each 32-B sector = u16 delta to its middle + 240 data
+ * bits, superblocks as BiRank16, so a query reads one sector and the superblock word).  All
+ * layouts answer every query identically. */
 #define QR_LAYOUT_BIRANK16    1
 #define QR_LAYOUT_BIRANK64X2  2
 #define QR_LAYOUT_QUADRANK16  3
 #define QR_LAYOUT_QUADRANK64  4
+#define QR_LAYOUT_BIRANK16X2  5
 typedef struct qr_fm qr_fm;         /* QuadFm: QuadRank over the BWT + C + spos + 8-mer table */
 
 /* ------------------------------------------------------------------ build */

@@ -86,7 +86,8 @@ uint64_t super_pack_cta_bytes(const qr_index* h) {
 qr_status build_super_pack(qr_index* h, cudaStream_t st) {
   h->spack = nullptr;
   h->spack_half = 0;
-  if (h->layout != QR_LAYOUT_BIRANK16 && h->layout != QR_LAYOUT_QUADRANK16) return QR_OK;
+  if (h->layout != QR_LAYOUT_BIRANK16 && h->layout != QR_LAYOUT_QUADRANK16 && h->layout != QR_LAYOUT_BIRANK16X2)
+    return QR_OK;
   if (h->n >= (1ull << 35) || h->n_super == 0) return QR_OK;     // anchors: 24 / 22 bits
   const bool bi = h->sigma == 2;
   const uint64_t groups = bi ? (h->n_super + 5) / 6 : (h->n_super + 7) / 8;
@@ -535,6 +536,112 @@ __global__ void __launch_bounds__(256) k_qd_rank1s(const uint4* __restrict__ lin
   }
 }
 
+// ------------------------------------------------------------------ BiRank16x2 (one sector per query)
+// Query q (variants.cu: layout): j = q / 480, d = q - 480 j, sector h = [d >= 240], x = d - 240 h;
+// the sector's anchor is its data bit 120 = sector bit 136, its delta the sector's low 16 bits:
+// rank = 2^11 s_{j>>7} + delta +- popc(sector bits between 16 + x and 136) (PAPER.md:484-485:
+// at most 120 bits, "only a quarter of the cache line").  One lane per query, one 32-B load.
+// SRC: 0 superblock word from L2, 1 from a per-CTA copy of the packed table; the cluster kernel
+// below reads it from 2-CTA cluster shared memory.  MODE 1 = the gather ceiling (same load).
+template <int K>
+__device__ __forceinline__ void b16x2_locate(uint64_t q, uint64_t last_line, uint32_t& j, uint32_t& h, uint32_t& x) {
+  uint32_t jj = q < (1ull << 37) ? (uint32_t)(q >> 5) / 15u    // floor(q/480) in 32 bits
+                                 : (uint32_t)(q / B16X2_B);    // (lines < 2^32: n < 2^40)
+  jj = jj > (uint32_t)last_line ? (uint32_t)last_line : jj;   // q > n: memory-safe clamp
+  uint64_t d = q - (uint64_t)jj * B16X2_B;
+  d = d > B16X2_B - 1 ? B16X2_B - 1 : d;
+  h = d >= 240 ? 1u : 0u;
+  x = (uint32_t)d - 240u * h;
+  j = jj;
+}
+
+__device__ __forceinline__ uint64_t b16x2_value(const uint64_t (&w)[4], uint32_t x, uint32_t s) {
+  uint32_t cnt = 0;
+#pragma unroll
+  for (int t = 0; t < 4; ++t) cnt += __popcll(w[t] & (prefix_mask(16 + (int)x, t) ^ prefix_mask(136, t)));
+  const uint64_t base = ((uint64_t)s << BI_SHIFT) + (w[0] & 0xffffull);
+  return x >= 120 ? base + cnt : base - cnt;
+}
+
+template <int K, int SRC, int MODE, bool HAS_C, bool DYN>
+__global__ void __launch_bounds__(256) k_b16x2_rank(const uint4* __restrict__ lines, const uint32_t* __restrict__ super,
+                                                    const uint64_t* __restrict__ pack, uint32_t words, uint32_t half,
+                                                    const uint64_t* __restrict__ q, const uint8_t* __restrict__ cs,
+                                                    uint64_t* __restrict__ out, uint64_t m, uint64_t last_line,
+                                                    unsigned long long* ctr) {
+  extern __shared__ uint64_t lt_smem[];
+  if (SRC == 1) lane_preload(pack, words, lt_smem);
+  const uint32_t u = sc_unit_in_warp<32>();
+  ScSched sc = sc_first<K, DYN, 32>(ctr);
+  uint64_t qn[K];
+  sc_load_q<K>(q, sc.gb + u, sc.stride, m, qn);
+  while (sc.gb < m) {
+    const uint64_t i0 = sc.gb + u, stride = sc.stride;
+    uint64_t qq[K], w[K][4];
+    uint32_t xx[K], s[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      qq[k] = qn[k];
+      uint32_t j, h, x;
+      b16x2_locate<K>(qq[k], last_line, j, h, x);
+      xx[k] = x;
+      ld_sector_na(lines + 4 * (uint64_t)j + 2 * h, w[k][0], w[k][1], w[k][2], w[k][3]);
+      s[k] = MODE == 1 ? 0u : SRC == 1 ? bi_s_local(lt_smem, half, j >> BI_SB_LOG) : __ldg(super + (j >> BI_SB_LOG));
+    }
+    sc = sc_next<K, DYN, 32>(sc, ctr);
+    sc_load_q<K>(q, sc.gb + u, sc.stride, m, qn);
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const uint64_t idx = i0 + (uint64_t)k * stride;
+      uint64_t r = MODE == 1 ? (w[k][0] ^ w[k][1] ^ w[k][2] ^ w[k][3]) : b16x2_value(w[k], xx[k], s[k]);
+      if (HAS_C && MODE == 0) {
+        if (idx < m && cs[idx] == 0) r = qq[k] - r;
+      }
+      if (idx < m) st_stream_u64(out + idx, r);
+    }
+  }
+}
+
+template <int K, int THREADS, bool HAS_C, bool DYN>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
+    k_b16x2_rank_c(const uint4* __restrict__ lines, const uint64_t* __restrict__ pack, uint64_t half_words,
+                   const uint64_t* __restrict__ q, const uint8_t* __restrict__ cs, uint64_t* __restrict__ out, uint64_t m,
+                   uint64_t last_line, unsigned long long* ctr) {
+  extern __shared__ uint64_t sc_smem[];
+  uint32_t base0, base1;
+  sc_preload(pack, half_words, sc_smem, base0, base1);
+  const uint32_t u = sc_unit_in_warp<32>();
+  ScSched sc = sc_first<K, DYN, 32>(ctr);
+  uint64_t qn[K];
+  sc_load_q<K>(q, sc.gb + u, sc.stride, m, qn);
+  while (sc.gb < m) {
+    const uint64_t i0 = sc.gb + u, stride = sc.stride;
+    uint64_t qq[K], w[K][4];
+    uint32_t xx[K], s[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      qq[k] = qn[k];
+      uint32_t j, h, x;
+      b16x2_locate<K>(qq[k], last_line, j, h, x);
+      xx[k] = x;
+      ld_sector_na(lines + 4 * (uint64_t)j + 2 * h, w[k][0], w[k][1], w[k][2], w[k][3]);
+      s[k] = bi_s_from_pack(j >> BI_SB_LOG, base0, base1);
+    }
+    sc = sc_next<K, DYN, 32>(sc, ctr);
+    sc_load_q<K>(q, sc.gb + u, sc.stride, m, qn);
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const uint64_t idx = i0 + (uint64_t)k * stride;
+      uint64_t r = b16x2_value(w[k], xx[k], s[k]);
+      if (HAS_C) {
+        if (idx < m && cs[idx] == 0) r = qq[k] - r;
+      }
+      if (idx < m) st_stream_u64(out + idx, r);
+    }
+  }
+  cluster_barrier();
+}
+
 // ------------------------------------------------------------------ launchers
 
 extern int g_rank_k;
@@ -606,6 +713,7 @@ int rank_shape(const qr_index* h, uint64_t m) {
 }
 
 extern int g_rank_dyn;
+extern int g_rank_lane_table;
 extern int g_rank_smem_k;
 extern int g_rank_smem_threads;
 
@@ -703,6 +811,60 @@ cudaError_t launch_super_pack_rank(const qr_index* h, const uint64_t* q, const u
     if (!e) e = e2;
   }
   return e;
+}
+
+
+// BiRank16x2 dispatch (what: 0 rank, 2 gather ceiling).  Superblock-word source by structure
+// size, as rank_shape: per-CTA table while the line array is L2-resident and the table small;
+// cluster shared memory for HBM-resident arrays and batches >= 2^22 (rank_smem); else L2.
+cudaError_t launch_b16x2_rank(const qr_index* h, const uint64_t* q, const uint8_t* c, uint64_t* out, uint64_t m,
+                              int what, cudaStream_t st) {
+  if (m == 0) return cudaSuccess;
+  constexpr int K = 4;
+  const uint64_t last = h->n_lines - 1;
+  const bool dyn = use_dyn_order(m);
+  const unsigned g = grid_stride_blocks((m + K - 1) / K, 256, h->sm_count, g_rank_blocks_per_sm);
+  const uint4* L = h->lines;
+  const uint32_t* S = h->super;
+  const uint64_t table = h->spack ? 2 * super_pack_cta_bytes(h) : 0;
+  const double lines = (double)h->n_lines * 64.0, l2 = (double)l2_bytes(h->device);
+  if (what == 2)
+    return launch_ordered(k_b16x2_rank<K, 0, 1, false, false>, k_b16x2_rank<K, 0, 1, false, true>, dyn, h->device,
+                          h->sm_count, g, st, L, S, h->spack, 0u, 0u, q, c, out, m, last);
+  const bool can_cluster = h->spack && !g_index64;
+  const bool cluster = can_cluster && (g_rank_smem == 2 || (g_rank_smem == 1 && m >= (1ull << 22) && lines > 0.6 * l2));
+  if (cluster) {
+    CounterLease lease;
+    unsigned long long* ctr = nullptr;
+    cudaError_t e;
+    if (g_rank_dyn && (e = lease.acquire(h->device, st, &ctr))) return e;
+    const size_t smem = super_pack_cta_bytes(h);
+    const uint64_t hw = h->spack_half;
+    if (c) {
+      if (ctr) sc_go(k_b16x2_rank_c<K, 1024, true, true>, 1024, h, smem, st, L, h->spack, hw, q, c, out, m, last, ctr);
+      else     sc_go(k_b16x2_rank_c<K, 1024, true, false>, 1024, h, smem, st, L, h->spack, hw, q, c, out, m, last, ctr);
+    } else {
+      if (ctr) sc_go(k_b16x2_rank_c<K, 1024, false, true>, 1024, h, smem, st, L, h->spack, hw, q, c, out, m, last, ctr);
+      else     sc_go(k_b16x2_rank_c<K, 1024, false, false>, 1024, h, smem, st, L, h->spack, hw, q, c, out, m, last, ctr);
+    }
+    e = cudaGetLastError();
+    if (ctr) {
+      cudaError_t e2 = lease.release(st);
+      if (!e) e = e2;
+    }
+    return e;
+  }
+  if (h->spack && table <= LANE_TABLE_MAX && g_rank_lane_table) {
+    const uint32_t words = (uint32_t)(table / 8), half = (uint32_t)h->spack_half;
+    if (c) return launch_ordered_smem(k_b16x2_rank<K, 1, 0, true, false>, k_b16x2_rank<K, 1, 0, true, true>, dyn, h->device,
+                                      h->sm_count, g, (size_t)table, st, L, S, h->spack, words, half, q, c, out, m, last);
+    return launch_ordered_smem(k_b16x2_rank<K, 1, 0, false, false>, k_b16x2_rank<K, 1, 0, false, true>, dyn, h->device,
+                               h->sm_count, g, (size_t)table, st, L, S, h->spack, words, half, q, c, out, m, last);
+  }
+  if (c) return launch_ordered(k_b16x2_rank<K, 0, 0, true, false>, k_b16x2_rank<K, 0, 0, true, true>, dyn, h->device,
+                               h->sm_count, g, st, L, S, h->spack, 0u, 0u, q, c, out, m, last);
+  return launch_ordered(k_b16x2_rank<K, 0, 0, false, false>, k_b16x2_rank<K, 0, 0, false, true>, dyn, h->device,
+                        h->sm_count, g, st, L, S, h->spack, 0u, 0u, q, c, out, m, last);
 }
 
 }  // namespace qr

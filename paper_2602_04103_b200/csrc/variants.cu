@@ -96,6 +96,84 @@ qr_status birank64x2_build_device(const uint64_t* d_bits, uint64_t n, int device
   return QR_OK;
 }
 
+// ------------------------------------------------------------------ BiRank16x2 build
+// BiRank16x2 (6.72%): "stores two 16-bit deltas, to 1/4th and 3/4th into the
+// block", so a query popcounts at most a quarter of the line.  B200 reading (R24):
+// the two halves are the two 32-B sectors, each self-contained except for the superblock word:
+//   sector h of line j = [u16 d_{j,h} | 240 data bits],  data bits [480 j + 240 h, +240),
+//   d_{j,h} = rank(480 j + 240 h + 120) - 2^11 s_{j>>7},  s_i = floor(rank(128 i * 480) / 2^11)
+// (128 lines per superblock as in BiRank16: d <= 127*480 + 360 + 2047 = 63,367 < 2^16).  Line
+// j's data are text u16 words [30 j, 30 j + 30) (480 = 30 * 16); a query reads ONE sector.
+__global__ void k_b16x2_count(const uint16_t* __restrict__ t16, uint64_t L, uint32_t* __restrict__ part,
+                              uint64_t* __restrict__ tot) {
+  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < L; j += (uint64_t)gridDim.x * blockDim.x) {
+    const uint16_t* w = t16 + 30 * j;
+    uint32_t c[30];
+#pragma unroll
+    for (int k = 0; k < 30; ++k) c[k] = __popc((uint32_t)w[k]);
+    uint32_t a0 = __popc((uint32_t)w[7] & 0xffu), a1 = __popc((uint32_t)w[22] & 0xffu), h0 = 0, h1 = 0;
+#pragma unroll
+    for (int k = 0; k < 7; ++k) { a0 += c[k]; a1 += c[15 + k]; }
+#pragma unroll
+    for (int k = 0; k < 15; ++k) { h0 += c[k]; h1 += c[15 + k]; }
+    part[2 * j] = a0;              // rank(240 h + 120) - rank(0) within the line, h = 0
+    part[2 * j + 1] = h0 + a1;     // ... h = 1
+    tot[j] = h0 + h1;
+  }
+}
+
+__global__ void k_b16x2_write(const uint16_t* __restrict__ t16, uint64_t L, const uint64_t* __restrict__ R,
+                              const uint32_t* __restrict__ part, uint4* __restrict__ lines, uint32_t* __restrict__ super) {
+  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < L; j += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t sb = R[(j >> BI_SB_LOG) << BI_SB_LOG] >> BI_SHIFT;
+    if ((j & ((1u << BI_SB_LOG) - 1)) == 0) super[j >> BI_SB_LOG] = (uint32_t)sb;
+    const uint16_t* w = t16 + 30 * j;
+    uint4* dst = lines + 4 * j;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const uint32_t d = (uint32_t)(R[j] + part[2 * j + h] - (sb << BI_SHIFT));
+      uint32_t u[8];
+      u[0] = d | ((uint32_t)w[15 * h] << 16);
+#pragma unroll
+      for (int k = 1; k < 8; ++k) u[k] = (uint32_t)w[15 * h + 2 * k - 1] | ((uint32_t)w[15 * h + 2 * k] << 16);
+      dst[2 * h] = make_uint4(u[0], u[1], u[2], u[3]);
+      dst[2 * h + 1] = make_uint4(u[4], u[5], u[6], u[7]);
+    }
+  }
+}
+
+qr_status birank16x2_build_device(const uint64_t* d_bits, uint64_t n, int device, cudaStream_t st, qr_index** out) {
+  qr_index* h = nullptr;
+  qr_status rs = alloc_index(2, n, device, &h, QR_LAYOUT_BIRANK16X2);
+  if (rs != QR_OK) return rs;
+  const uint64_t L = h->n_lines;
+  uint64_t *tot = nullptr, *R = nullptr;
+  uint32_t* part = nullptr;
+  void* tmp = nullptr;
+  size_t tb = 0;
+  cudaError_t e;
+  auto bail = [&](cudaError_t err, const char* what) {
+    cudaFreeAsync(tot, st); cudaFreeAsync(R, st); cudaFreeAsync(part, st); cudaFreeAsync(tmp, st);
+    qr_free(h);
+    return cuda_fail(err, what);
+  };
+  if ((e = cudaMallocAsync((void**)&tot, L * 8, st))) return bail(e, "alloc tot");
+  if ((e = cudaMallocAsync((void**)&R, L * 8, st))) return bail(e, "alloc R");
+  if ((e = cudaMallocAsync((void**)&part, 2 * L * 4, st))) return bail(e, "alloc part");
+  const unsigned g = grid_stride_blocks(L, 256, h->sm_count, 16);
+  const uint16_t* t16 = reinterpret_cast<const uint16_t*>(d_bits);
+  k_b16x2_count<<<g, 256, 0, st>>>(t16, L, part, tot);
+  if ((e = cub::DeviceScan::ExclusiveSum(nullptr, tb, tot, R, (int64_t)L, st))) return bail(e, "scan size");
+  if ((e = cudaMallocAsync(&tmp, tb, st))) return bail(e, "alloc scan tmp");
+  if ((e = cub::DeviceScan::ExclusiveSum(tmp, tb, tot, R, (int64_t)L, st))) return bail(e, "scan");
+  k_b16x2_write<<<g, 256, 0, st>>>(t16, L, R, part, h->lines, h->super);
+  if ((e = cudaGetLastError())) return bail(e, "k_b16x2_write");
+  cudaFreeAsync(tot, st); cudaFreeAsync(R, st); cudaFreeAsync(part, st); cudaFreeAsync(tmp, st);
+  if ((rs = build_super_pack(h, st)) != QR_OK) { qr_free(h); return rs; }
+  *out = h;
+  return QR_OK;
+}
+
 // ------------------------------------------------------------------ QuadRank64 build
 
 __global__ void k_q64_count(const uint64_t* __restrict__ t, uint64_t L, uint64_t* __restrict__ tot,
@@ -349,6 +427,7 @@ static cudaError_t v_launch(const qr_index* h, const uint64_t* q, const uint8_t*
 cudaError_t launch_variant(const qr_index* h, const uint64_t* q, const uint8_t* c, uint64_t* out, uint64_t m, int what,
                            cudaStream_t st) {
   if (m == 0) return cudaSuccess;
+  if (h->layout == QR_LAYOUT_BIRANK16X2) return launch_b16x2_rank(h, q, c, out, m, what, st);
   switch (g_rank_k) {
     case 1: return v_launch<1>(h, q, c, out, m, what, st);
     case 4: return v_launch<4>(h, q, c, out, m, what, st);
@@ -386,6 +465,22 @@ struct RankOne {
       for (int t = 0; t < 4; ++t) cnt += __popcll((right ? b[t] : a[t]) & (prefix_mask(x, t) ^ (right ? 0ull : ~0ull)));
       const uint64_t base = ((uint64_t)s << BI_SHIFT) + (a[0] & 0xffffull);
       const uint64_t r = right ? base + cnt : base - cnt;
+      return c == 0 ? q - r : r;
+    }
+    if (h.layout == QR_LAYOUT_BIRANK16X2) {
+      uint64_t j = q / B16X2_B;
+      j = j > last ? last : j;
+      uint64_t d = q - j * B16X2_B;
+      d = d > B16X2_B - 1 ? B16X2_B - 1 : d;
+      const uint32_t hh = d >= 240 ? 1u : 0u;
+      const int x = (int)(d - 240 * hh);
+      ld_sector_na(h.lines + 4 * j + 2 * hh, a[0], a[1], a[2], a[3]);
+      const uint32_t s = __ldg(h.super + (j >> BI_SB_LOG));
+      uint32_t cnt = 0;
+#pragma unroll
+      for (int t = 0; t < 4; ++t) cnt += __popcll(a[t] & (prefix_mask(16 + x, t) ^ prefix_mask(136, t)));
+      const uint64_t base = ((uint64_t)s << BI_SHIFT) + (a[0] & 0xffffull);
+      const uint64_t r = x >= 120 ? base + cnt : base - cnt;
       return c == 0 ? q - r : r;
     }
     if (h.layout == QR_LAYOUT_BIRANK64X2) {

@@ -127,11 +127,11 @@ def _chain_reference(rank_fn, q, n, L):
 
 
 @pytest.mark.parametrize("layout", [qr.QR_LAYOUT_BIRANK16, qr.QR_LAYOUT_BIRANK64X2, qr.QR_LAYOUT_QUADRANK16,
-                                    qr.QR_LAYOUT_QUADRANK64])
+                                    qr.QR_LAYOUT_QUADRANK64, qr.QR_LAYOUT_BIRANK16X2])
 def test_rank_chain_latency_mode(cuda, layout):
     torch = _torch()
     n = 3 * 63488 + 1001
-    bits = layout in (qr.QR_LAYOUT_BIRANK16, qr.QR_LAYOUT_BIRANK64X2)
+    bits = layout in (qr.QR_LAYOUT_BIRANK16, qr.QR_LAYOUT_BIRANK64X2, qr.QR_LAYOUT_BIRANK16X2)
     w = gen.bits(21, n) if bits else gen.dna(22, n)
     h = qr.qr_build(w, n, layout)
     m, L = 40003, 37                                  # ragged last chain
@@ -154,13 +154,13 @@ def test_rank_chain_latency_mode(cuda, layout):
 
 
 @pytest.mark.parametrize("layout", [qr.QR_LAYOUT_BIRANK16, qr.QR_LAYOUT_BIRANK64X2, qr.QR_LAYOUT_QUADRANK16,
-                                    qr.QR_LAYOUT_QUADRANK64])
+                                    qr.QR_LAYOUT_QUADRANK64, qr.QR_LAYOUT_BIRANK16X2])
 def test_save_load_roundtrip(cuda, layout, tmp_path):
     """Checkpoint/resume: export -> .npz -> import gives a handle that answers identically, and the
     build is deterministic (byte-identical layout on a rebuild)."""
     torch = _torch()
     n = 2 * 63488 * 2 + 999
-    bits = layout in (qr.QR_LAYOUT_BIRANK16, qr.QR_LAYOUT_BIRANK64X2)
+    bits = layout in (qr.QR_LAYOUT_BIRANK16, qr.QR_LAYOUT_BIRANK64X2, qr.QR_LAYOUT_BIRANK16X2)
     w = gen.bits(31, n) if bits else gen.dna(32, n)
     h = qr.qr_build(w, n, layout)
     p = str(tmp_path / "idx.npz")
@@ -178,3 +178,95 @@ def test_save_load_roundtrip(cuda, layout, tmp_path):
     qr.qr_rank(h2, dq, dc, o2)
     torch.cuda.synchronize()
     assert np.array_equal(to_host(o1), to_host(o2))
+
+
+# ------------------------------------------------------------------ BiRank16x2
+B16X2_SIZES = [0, 1, 119, 120, 121, 239, 240, 241, 359, 360, 361, 479, 480, 481, 959, 960, 961,
+               128 * 480 - 1, 128 * 480, 128 * 480 + 1, 6 * 128 * 480 + 7, 13 * 128 * 480 + 3333, (1 << 22) + 3]
+
+
+@pytest.mark.parametrize("n", B16X2_SIZES)
+@pytest.mark.parametrize("p", [0.5, 1.0, 0.01])
+def test_birank16x2_parity(cuda, n, p):
+    """BiRank16x2: every q on small n, boundaries of the 1/4 / 3/4 anchors (120, 360), the sector
+    split (240), lines (480) and superblocks (128 lines) on larger n; all-ones makes every delta
+    and superblock increment maximal; rank with c (c = 0 -> q - rank)."""
+    torch = _torch()
+    w = gen.bits(5000 + n, n, p)
+    h = qr.qr_build(w, n, qr.QR_LAYOUT_BIRANK16X2)
+    L = n // 480 + 1
+    assert h.layout == qr.QR_LAYOUT_BIRANK16X2
+    assert h.line_bytes == 64 * L and h.super_bytes == 4 * ((L - 1) // 128 + 1)
+    ora = oracle.BitsOracle(w, n)
+    if n <= 100000:
+        q = np.arange(n + 1, dtype=np.uint64)
+    else:
+        q = np.concatenate([gen.queries(6, n, 200000), boundary_queries(n, 240, 128 * 480, 120)])
+    dq = to_dev(q, cuda)
+    out = torch.empty_like(dq)
+    qr.qr_rank(h, dq, None, out)
+    c = (gen.queries(7, 1, q.size, with_c=True)[1] & 1).astype(np.uint8)
+    out2 = torch.empty_like(dq)
+    qr.qr_rank(h, dq, to_dev(c, cuda), out2)
+    torch.cuda.synchronize()
+    assert np.array_equal(to_host(out), ora.rank(q))
+    assert np.array_equal(to_host(out2), ora.rank(q, c))
+
+
+def test_birank16x2_layout_closed_forms(cuda):
+    """Decode every sector: d_{j,h} + 2^11 s_{j>>7} = rank(480 j + 240 h + 120) (the 1/4 and 3/4
+    anchors), s_i = rank(128 i * 480) >> 11, data = text u16 words; byte
+    accounting 6.72% at n = 2^34."""
+    for n, p in [(9 * 128 * 480 + 1234, 0.5), (3 * 128 * 480 + 17, 1.0)]:
+        w = gen.bits(77, n, p)
+        h = qr.qr_build(w, n, qr.QR_LAYOUT_BIRANK16X2)
+        lines, sup = qr.qr_export_layout(h)
+        L = n // 480 + 1
+        u16 = lines.view(np.uint16).reshape(L, 2, 16)
+        ora = oracle.BitsOracle(w, n)
+        for hh in (0, 1):
+            anchors = np.minimum(np.arange(L, dtype=np.uint64) * 480 + 240 * hh + 120, n)
+            d = u16[:, hh, 0].astype(np.uint64) + (sup[np.arange(L) // 128].astype(np.uint64) << 11)
+            assert np.array_equal(d, ora.rank(anchors)), hh
+        sb = np.minimum(np.arange(sup.size, dtype=np.uint64) * 128 * 480, n)
+        assert np.array_equal(sup.astype(np.uint64), ora.rank(sb) >> 11)
+        text16 = np.zeros(30 * L, np.uint16)
+        t = w.view(np.uint16)[: min(w.size * 4, 30 * L)]
+        text16[: t.size] = t
+        assert np.array_equal(u16[:, :, 1:].reshape(-1), text16)
+    n = 1 << 34
+    L = n // 480 + 1
+    overhead = (64 * L + 4 * ((L - 1) // 128 + 1)) * 8 / n - 1
+    assert abs(overhead - 0.0672) < 0.0005
+
+
+@pytest.mark.parametrize("src", ["table", "global", "cluster"])
+def test_birank16x2_superblock_sources(cuda, src):
+    """The three superblock-word sources (per-CTA table, L2, 2-CTA cluster shared memory) and the
+    dynamic order on a batch >= 2^22; the gather ceiling loads the query's sector."""
+    torch = _torch()
+    knobs = {"table": [("rank_lane_table", 1), ("rank_smem", 0)], "global": [("rank_lane_table", 0), ("rank_smem", 0)],
+             "cluster": [("rank_smem", 2)]}[src]
+    n = 23 * 128 * 480 + 999
+    w = gen.bits(88, n)
+    h = qr.qr_build(w, n, qr.QR_LAYOUT_BIRANK16X2)
+    m = (1 << 22) + 17
+    q = gen.queries(89, n, m)
+    dq = to_dev(q, cuda)
+    try:
+        for k, v in knobs:
+            qr.qr_set_tuning(k, v)
+        out = torch.empty_like(dq)
+        qr.qr_rank(h, dq, None, out)
+        c = (gen.queries(90, 1, m, with_c=True)[1] & 1).astype(np.uint8)
+        out2 = torch.empty_like(dq)
+        qr.qr_rank(h, dq, to_dev(c, cuda), out2)
+        g = torch.empty_like(dq)
+        qr.qr_gather_ceiling(h, dq, g, 0)
+        torch.cuda.synchronize()
+    finally:
+        qr.qr_set_tuning("rank_lane_table", 1)
+        qr.qr_set_tuning("rank_smem", 1)
+    ora = oracle.BitsOracle(w, n)
+    assert np.array_equal(to_host(out), ora.rank(q))
+    assert np.array_equal(to_host(out2), ora.rank(q, c))

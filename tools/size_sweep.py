@@ -20,16 +20,20 @@ M = 2 * 10**8
 q = torch.empty(M, dtype=torch.uint64, device=dev); out = torch.empty_like(q)
 c = torch.empty(M, dtype=torch.uint8, device=dev)
 for lg in (20, 24, 26, 28, 30, 32, 34, 35, 36):
+    if len(sys.argv) > 1 and sys.argv[1] == "bits_only" and lg > 36: break
     n = 1 << lg
     bits = torch.empty((n + 63) // 64, dtype=torch.uint64, device=dev); gen.bits_dev(7, n, 0.5, bits)
     gen.queries_dev(8, n, M, q)
     r = {"sigma": 2, "log2_n": lg}
-    for name, layout in (("birank16", qr.QR_LAYOUT_BIRANK16), ("birank64x2", qr.QR_LAYOUT_BIRANK64X2)):
+    for name, layout in (("birank16", qr.QR_LAYOUT_BIRANK16), ("birank16x2", qr.QR_LAYOUT_BIRANK16X2),
+                         ("birank64x2", qr.QR_LAYOUT_BIRANK64X2)):
         h = qr.qr_build(bits, n, layout)
         r[name + "_gq_s"] = M / t(lambda: qr.qr_rank(h, q, None, out, M, st)) / 1e6
         r[name + "_bytes"] = h.line_bytes + h.super_bytes
         if layout == qr.QR_LAYOUT_BIRANK16:
             r["smem_cache"] = qr.qr_super_cache_bytes(h) > 0
+        if layout == qr.QR_LAYOUT_BIRANK16X2:
+            r["birank16x2_ceiling_gq_s"] = M / t(lambda: qr.qr_gather_ceiling(h, q, out, 0, M, st)) / 1e6
         h.free()
     del bits; torch.cuda.empty_cache()
     print(json.dumps(r), flush=True)
