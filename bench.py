@@ -387,19 +387,18 @@ def bench_variants(ctx, steps, warmup):
     del bits
     text = torch.empty((N3 + 31) // 32, dtype=torch.uint64, device=ctx.dev)
     gen.dna_dev(SEED[3], N3, 0, text)
-    h = qr.qr_build(text, N3, qr.QR_LAYOUT_QUADRANK64, device=ctx.gpu)
-    del text
     c = torch.empty(M3, dtype=torch.uint8, device=ctx.dev)
     gen.queries_dev(SEED[3], N3, M3, q, c, i0=ctx.rank * M3)
-    ms = ctx.timed(lambda: qr.qr_rank(h, q, c, out, M3, ctx.stream), steps, warmup)
-    del out
     o4 = torch.empty((M3, 4), dtype=torch.uint64, device=ctx.dev)
-    ms4 = ctx.timed(lambda: qr.qr_rank_all4(h, q, o4, M3, ctx.stream), steps, warmup)
-    res["c3_quadrank64"] = {"rank": {"ms": ms, "gq_s": ctx.world * M3 / ms / 1e6},
-                            "rank_all4": {"ms": ms4, "gq_s": ctx.world * M3 / ms4 / 1e6},
-                            "bytes": h.line_bytes, "overhead": h.line_bytes / (N3 / 4) - 1}
-    h.free()
-    del q, c, o4
+    for key, layout in (("c3_quadrank64", qr.QR_LAYOUT_QUADRANK64), ("c3_quadrank16x2", qr.QR_LAYOUT_QUADRANK16X2)):
+        h = qr.qr_build(text, N3, layout, device=ctx.gpu)
+        ms = ctx.timed(lambda: qr.qr_rank(h, q, c, out, M3, ctx.stream), steps, warmup)
+        ms4 = ctx.timed(lambda: qr.qr_rank_all4(h, q, o4, M3, ctx.stream), steps, warmup)
+        res[key] = {"rank": {"ms": ms, "gq_s": ctx.world * M3 / ms / 1e6},
+                    "rank_all4": {"ms": ms4, "gq_s": ctx.world * M3 / ms4 / 1e6},
+                    "bytes": h.line_bytes + h.super_bytes, "overhead": (h.line_bytes + h.super_bytes) / (N3 / 4) - 1}
+        h.free()
+    del text, q, c, o4, out
     torch.cuda.empty_cache()
     return res
 

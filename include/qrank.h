@@ -55,13 +55,16 @@ typedef struct qr_index qr_index;   /* a rank layout (QR_LAYOUT_*)              
  * superblock word), QuadRank64 (100%: four u64 ranks to the middle of 128
  * characters in sector 0, the characters as two transposed negated plane pairs in sector 1) and
  * BiRank16x2 (6.72%: each 32-B sector = u16 delta to its middle + 240 data
- * bits, superblocks as BiRank16, so a query reads one sector and the superblock word).  All
- * layouts answer every query identically. */
+ * bits, superblocks as BiRank16, so a query reads one sector and the superblock word), and
+ * QuadRank16x2 (B200 sector-local σ=4 variant, 33.3%: each 32-B sector = four u16 deltas to its
+ * middle + 96 packed characters, superblocks as QuadRank16; rank and rank_4 read one sector).
+ * All layouts answer every query identically. */
 #define QR_LAYOUT_BIRANK16    1
 #define QR_LAYOUT_BIRANK64X2  2
 #define QR_LAYOUT_QUADRANK16  3
 #define QR_LAYOUT_QUADRANK64  4
 #define QR_LAYOUT_BIRANK16X2  5
+#define QR_LAYOUT_QUADRANK16X2 6
 typedef struct qr_fm qr_fm;         /* QuadFm: QuadRank over the BWT + C + spos + 8-mer table */
 
 /* ------------------------------------------------------------------ build */

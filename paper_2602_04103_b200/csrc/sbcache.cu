@@ -86,7 +86,8 @@ uint64_t super_pack_cta_bytes(const qr_index* h) {
 qr_status build_super_pack(qr_index* h, cudaStream_t st) {
   h->spack = nullptr;
   h->spack_half = 0;
-  if (h->layout != QR_LAYOUT_BIRANK16 && h->layout != QR_LAYOUT_QUADRANK16 && h->layout != QR_LAYOUT_BIRANK16X2)
+  if (h->layout != QR_LAYOUT_BIRANK16 && h->layout != QR_LAYOUT_QUADRANK16 && h->layout != QR_LAYOUT_BIRANK16X2 &&
+      h->layout != QR_LAYOUT_QUADRANK16X2)
     return QR_OK;
   if (h->n >= (1ull << 35) || h->n_super == 0) return QR_OK;     // anchors: 24 / 22 bits
   const bool bi = h->sigma == 2;
@@ -642,6 +643,169 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   cluster_barrier();
 }
 
+// ------------------------------------------------------------------ QuadRank16x2 (one sector per query)
+// Query (variants.cu: layout): j = q / 192, d = q - 192 j, sector h = [d >= 96], x = d - 96 h;
+// anchor = the sector's char 48; its word 0 holds the four u16 deltas (c at bits 16 c), words
+// 1..3 the 96 chars packed 2 bits each.  rank(q,c) = 2^13 s_{j>>8,c} + d_c +- #c in the chars
+// between x and 48 (<= 48 chars); rank_4 from three plane popcounts (A = len - L - H + T).
+__device__ __forceinline__ void q16x2_locate(uint64_t q, uint64_t last_line, uint32_t& j, uint32_t& h, uint32_t& x) {
+  uint32_t jj = q < (1ull << 38) ? (uint32_t)(q >> 6) / 3u : (uint32_t)(q / Q16X2_B);   // floor(q/192)
+  jj = jj > (uint32_t)last_line ? (uint32_t)last_line : jj;
+  uint64_t d = q - (uint64_t)jj * Q16X2_B;
+  d = d > Q16X2_B - 1 ? Q16X2_B - 1 : d;
+  h = d >= 96 ? 1u : 0u;
+  x = (uint32_t)d - 96u * h;
+  j = jj;
+}
+
+// mask of the 2-bit fields of chars between x and 48 (symmetric difference of two prefixes) in data word t
+__device__ __forceinline__ uint64_t q16x2_range(uint32_t x, int t) { return prefix_mask(2 * (int)x, t) ^ prefix_mask(96, t); }
+
+__device__ __forceinline__ uint64_t q16x2_rank1(const uint64_t (&w)[4], uint32_t x, uint32_t c, uint32_t s) {
+  const uint64_t pat = (uint64_t)c * 0x5555555555555555ull;
+  uint32_t cnt = 0;
+#pragma unroll
+  for (int t = 0; t < 3; ++t) {
+    const uint64_t e = ~(w[1 + t] ^ pat);
+    cnt += __popcll(e & (e >> 1) & 0x5555555555555555ull & q16x2_range(x, t));
+  }
+  const uint64_t base = ((uint64_t)s << QD_SHIFT) + ((w[0] >> (16 * c)) & 0xffffull);
+  return x >= 48 ? base + cnt : base - cnt;
+}
+
+__device__ __forceinline__ void q16x2_rank4(const uint64_t (&w)[4], uint32_t x, const uint32_t (&s)[4], uint64_t (&r)[4]) {
+  uint32_t nl = 0, nh = 0, nt = 0;
+#pragma unroll
+  for (int t = 0; t < 3; ++t) {
+    const uint64_t msk = 0x5555555555555555ull & q16x2_range(x, t);
+    const uint64_t l = w[1 + t] & msk, hh = (w[1 + t] >> 1) & msk;
+    nl += __popcll(l);
+    nh += __popcll(hh);
+    nt += __popcll(l & hh);
+  }
+  const uint32_t len = x >= 48 ? x - 48u : 48u - x;
+  const uint32_t cnt[4] = {len - nl - nh + nt, nl - nt, nh - nt, nt};
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const uint64_t base = ((uint64_t)s[c] << QD_SHIFT) + ((w[0] >> (16 * c)) & 0xffffull);
+    r[c] = x >= 48 ? base + cnt[c] : base - cnt[c];
+  }
+}
+
+template <int K, int SRC, int MODE, bool DYN>   // SRC 0: s from L2, 1: per-CTA table; MODE 0 rank, 1 rank_4, 2 gather
+__global__ void __launch_bounds__(256) k_q16x2_rank(const uint4* __restrict__ lines, const uint32_t* __restrict__ super,
+                                                    const uint64_t* __restrict__ pack, uint32_t words, uint32_t half,
+                                                    const uint64_t* __restrict__ q, const uint8_t* __restrict__ cs,
+                                                    uint64_t* __restrict__ out, uint64_t m, uint64_t last_line,
+                                                    unsigned long long* ctr) {
+  extern __shared__ uint64_t lt_smem[];
+  if (SRC == 1) lane_preload(pack, words, lt_smem);
+  const uint32_t u = sc_unit_in_warp<32>();
+  ScSched sc = sc_first<K, DYN, 32>(ctr);
+  uint64_t qn[K];
+  uint32_t cn[K];
+  sc_load_qc<K, MODE == 0>(q, cs, sc.gb + u, sc.stride, m, qn, cn);
+  while (sc.gb < m) {
+    const uint64_t i0 = sc.gb + u, stride = sc.stride;
+    uint64_t w[K][4];
+    uint32_t xx[K], jj[K], cc[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      uint32_t j, h, x;
+      q16x2_locate(qn[k], last_line, j, h, x);
+      xx[k] = x; jj[k] = j; cc[k] = MODE == 0 ? cn[k] : 0u;
+      ld_sector_na(lines + 4 * (uint64_t)j + 2 * h, w[k][0], w[k][1], w[k][2], w[k][3]);
+    }
+    sc = sc_next<K, DYN, 32>(sc, ctr);
+    sc_load_qc<K, MODE == 0>(q, cs, sc.gb + u, sc.stride, m, qn, cn);
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const uint64_t idx = i0 + (uint64_t)k * stride;
+      if (idx >= m) continue;
+      const uint32_t sb = jj[k] >> QD_SB_LOG;
+      if (MODE == 2) {
+        st_stream_u64(out + idx, w[k][0] ^ w[k][1] ^ w[k][2] ^ w[k][3]);
+      } else if (MODE == 0) {
+        const uint32_t c = cc[k];
+        const uint32_t s = SRC == 1 ? qd_s_field(qd_group_local(lt_smem, half, sb >> 3)[c], sb & 7u)
+                                    : __ldg(super + 4 * sb + c);
+        st_stream_u64(out + idx, q16x2_rank1(w[k], xx[k], c, s));
+      } else {
+        uint32_t s4[4];
+        if (SRC == 1) {
+          const uint64_t* grp = qd_group_local(lt_smem, half, sb >> 3);
+#pragma unroll
+          for (int c = 0; c < 4; ++c) s4[c] = qd_s_field(grp[c], sb & 7u);
+        } else {
+          const uint4 v = __ldg(reinterpret_cast<const uint4*>(super) + sb);
+          s4[0] = v.x; s4[1] = v.y; s4[2] = v.z; s4[3] = v.w;
+        }
+        uint64_t r[4];
+        q16x2_rank4(w[k], xx[k], s4, r);
+        st_stream_v4u64(out + 4 * idx, r[0], r[1], r[2], r[3]);
+      }
+    }
+  }
+}
+
+template <int K, int THREADS, int MODE, bool DYN>   // MODE 0 rank, 1 rank_4
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
+    k_q16x2_rank_c(const uint4* __restrict__ lines, const uint64_t* __restrict__ pack, uint64_t half_words,
+                   const uint64_t* __restrict__ q, const uint8_t* __restrict__ cs, uint64_t* __restrict__ out, uint64_t m,
+                   uint64_t last_line, unsigned long long* ctr) {
+  extern __shared__ uint64_t sc_smem[];
+  uint32_t base0, base1;
+  sc_preload(pack, half_words, sc_smem, base0, base1);
+  const uint32_t u = sc_unit_in_warp<32>();
+  ScSched sc = sc_first<K, DYN, 32>(ctr);
+  uint64_t qn[K];
+  uint32_t cn[K];
+  sc_load_qc<K, MODE == 0>(q, cs, sc.gb + u, sc.stride, m, qn, cn);
+  while (sc.gb < m) {
+    const uint64_t i0 = sc.gb + u, stride = sc.stride;
+    uint64_t w[K][4];
+    uint32_t xx[K], cc[K], s[K][MODE == 0 ? 1 : 4];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      uint32_t j, h, x;
+      q16x2_locate(qn[k], last_line, j, h, x);
+      xx[k] = x; cc[k] = MODE == 0 ? cn[k] : 0u;
+      ld_sector_na(lines + 4 * (uint64_t)j + 2 * h, w[k][0], w[k][1], w[k][2], w[k][3]);
+      const uint32_t sb = j >> QD_SB_LOG, g = sb >> 3;
+      const uint32_t addr = ((g & 1u) ? base1 : base0) + (g >> 1) * 32u;
+      if (MODE == 0) {
+        s[k][0] = qd_s_field(ld_dsmem_u64(addr + 8u * cc[k]), sb & 7u);
+      } else {
+        uint64_t v0, v1, v2, v3;
+        ld_dsmem_v2u64(addr, v0, v1);
+        ld_dsmem_v2u64(addr + 16u, v2, v3);
+        s[k][MODE == 0 ? 0 : 0] = qd_s_field(v0, sb & 7u);
+        s[k][MODE == 0 ? 0 : 1] = qd_s_field(v1, sb & 7u);
+        s[k][MODE == 0 ? 0 : 2] = qd_s_field(v2, sb & 7u);
+        s[k][MODE == 0 ? 0 : 3] = qd_s_field(v3, sb & 7u);
+      }
+    }
+    sc = sc_next<K, DYN, 32>(sc, ctr);
+    sc_load_qc<K, MODE == 0>(q, cs, sc.gb + u, sc.stride, m, qn, cn);
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const uint64_t idx = i0 + (uint64_t)k * stride;
+      if (idx >= m) continue;
+      if (MODE == 0) {
+        st_stream_u64(out + idx, q16x2_rank1(w[k], xx[k], cc[k], s[k][0]));
+      } else {
+        uint32_t s4[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) s4[c] = s[k][MODE == 0 ? 0 : c];
+        uint64_t r[4];
+        q16x2_rank4(w[k], xx[k], s4, r);
+        st_stream_v4u64(out + 4 * idx, r[0], r[1], r[2], r[3]);
+      }
+    }
+  }
+  cluster_barrier();
+}
+
 // ------------------------------------------------------------------ launchers
 
 extern int g_rank_k;
@@ -865,6 +1029,61 @@ cudaError_t launch_b16x2_rank(const qr_index* h, const uint64_t* q, const uint8_
                                h->sm_count, g, st, L, S, h->spack, 0u, 0u, q, c, out, m, last);
   return launch_ordered(k_b16x2_rank<K, 0, 0, false, false>, k_b16x2_rank<K, 0, 0, false, true>, dyn, h->device,
                         h->sm_count, g, st, L, S, h->spack, 0u, 0u, q, c, out, m, last);
+}
+
+
+// QuadRank16x2 dispatch (what: 0 rank, 1 rank_4, 2 gather ceiling); superblock source as BiRank16x2.
+cudaError_t launch_q16x2_rank(const qr_index* h, const uint64_t* q, const uint8_t* c, uint64_t* out, uint64_t m,
+                              int what, cudaStream_t st) {
+  if (m == 0) return cudaSuccess;
+  constexpr int K = 2;
+  const uint64_t last = h->n_lines - 1;
+  const bool dyn = use_dyn_order(m);
+  const unsigned g = grid_stride_blocks((m + K - 1) / K, 256, h->sm_count, g_rank_blocks_per_sm);
+  const uint4* L = h->lines;
+  const uint32_t* S = h->super;
+  const uint64_t table = h->spack ? 2 * super_pack_cta_bytes(h) : 0;
+  const double lines = (double)h->n_lines * 64.0, l2 = (double)l2_bytes(h->device);
+  if (what == 2)
+    return launch_ordered(k_q16x2_rank<K, 0, 2, false>, k_q16x2_rank<K, 0, 2, true>, dyn, h->device, h->sm_count, g, st,
+                          L, S, h->spack, 0u, 0u, q, c, out, m, last);
+  const bool can_cluster = h->spack && !g_index64;
+  const bool cluster = can_cluster && (g_rank_smem == 2 || (g_rank_smem == 1 && m >= (1ull << 22) && lines > 0.6 * l2));
+  if (cluster) {
+    CounterLease lease;
+    unsigned long long* ctr = nullptr;
+    cudaError_t e;
+    if (g_rank_dyn && (e = lease.acquire(h->device, st, &ctr))) return e;
+    const size_t smem = super_pack_cta_bytes(h);
+    const uint64_t hw = 4 * h->spack_half;
+    const uint64_t* P = h->spack;
+    if (what == 0) {
+      if (ctr) sc_go(k_q16x2_rank_c<K, 1024, 0, true>, 1024, h, smem, st, L, P, hw, q, c, out, m, last, ctr);
+      else     sc_go(k_q16x2_rank_c<K, 1024, 0, false>, 1024, h, smem, st, L, P, hw, q, c, out, m, last, ctr);
+    } else {
+      if (ctr) sc_go(k_q16x2_rank_c<K, 1024, 1, true>, 1024, h, smem, st, L, P, hw, q, c, out, m, last, ctr);
+      else     sc_go(k_q16x2_rank_c<K, 1024, 1, false>, 1024, h, smem, st, L, P, hw, q, c, out, m, last, ctr);
+    }
+    e = cudaGetLastError();
+    if (ctr) {
+      cudaError_t e2 = lease.release(st);
+      if (!e) e = e2;
+    }
+    return e;
+  }
+  if (h->spack && table <= LANE_TABLE_MAX && g_rank_lane_table) {
+    const uint32_t words = (uint32_t)(table / 8), half = (uint32_t)h->spack_half;
+    if (what == 0)
+      return launch_ordered_smem(k_q16x2_rank<K, 1, 0, false>, k_q16x2_rank<K, 1, 0, true>, dyn, h->device, h->sm_count, g,
+                                 (size_t)table, st, L, S, h->spack, words, half, q, c, out, m, last);
+    return launch_ordered_smem(k_q16x2_rank<K, 1, 1, false>, k_q16x2_rank<K, 1, 1, true>, dyn, h->device, h->sm_count, g,
+                               (size_t)table, st, L, S, h->spack, words, half, q, c, out, m, last);
+  }
+  if (what == 0)
+    return launch_ordered(k_q16x2_rank<K, 0, 0, false>, k_q16x2_rank<K, 0, 0, true>, dyn, h->device, h->sm_count, g, st,
+                          L, S, h->spack, 0u, 0u, q, c, out, m, last);
+  return launch_ordered(k_q16x2_rank<K, 0, 1, false>, k_q16x2_rank<K, 0, 1, true>, dyn, h->device, h->sm_count, g, st,
+                        L, S, h->spack, 0u, 0u, q, c, out, m, last);
 }
 
 }  // namespace qr

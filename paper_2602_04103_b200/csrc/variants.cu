@@ -174,6 +174,100 @@ qr_status birank16x2_build_device(const uint64_t* d_bits, uint64_t n, int device
   return QR_OK;
 }
 
+// ------------------------------------------------------------------ QuadRank16x2 build
+// QuadRank16x2 (B200 sector-local variant, NEXT §8(f)4, R25; 33.3%): the σ=4 analogue
+// of BiRank16x2.  Each 32-B sector is self-contained except for the superblock words:
+//   sector h of line j = [u16 d_{j,h,c} for c = A, C, G, T | 96 chars packed 2 bits each],
+//   chars 192 j + 96 h .. +96 (text u64 words [6 j + 3 h, +3)),
+//   d_{j,h,c} = rank(192 j + 96 h + 48, c) - 2^13 s_{j>>8,c},  s_{i,c} = floor(rank(256 i 192, c)/2^13)
+// (256 lines per superblock as QuadRank16: d <= 255*192 + 144 + 8191 = 57,295 < 2^16).  A query
+// reads ONE sector for rank and for rank_4 and counts at most 48 characters.
+__device__ __forceinline__ void q16x2_count_word(uint64_t w, uint64_t range, uint32_t (&a)[4]) {
+  const uint64_t M = 0x5555555555555555ull & range;
+  const uint64_t lo = w & M, hi = (w >> 1) & M;
+  const uint32_t c3 = __popcll(lo & hi), l1 = __popcll(lo), h1 = __popcll(hi), len = __popcll(M);
+  a[3] += c3; a[1] += l1 - c3; a[2] += h1 - c3; a[0] += len - l1 - h1 + c3;
+}
+
+// per line: counts to each sector's anchor (chars [0,48) and [0,144)) packed 8 bits x 4, and totals
+__global__ void k_q16x2_count(const uint64_t* __restrict__ t, uint64_t L, uint64_t* __restrict__ tot,
+                              uint32_t* __restrict__ part) {
+  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < L; j += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t* w = t + 6 * j;
+    uint32_t a[4] = {0, 0, 0, 0};
+    q16x2_count_word(w[0], ~0ull, a);
+    q16x2_count_word(w[1], 0xffffffffull, a);                    // chars [32, 48)
+    part[2 * j] = a[0] | (a[1] << 8) | (a[2] << 16) | (a[3] << 24);
+    q16x2_count_word(w[1], ~0xffffffffull, a);
+    q16x2_count_word(w[2], ~0ull, a);
+    q16x2_count_word(w[3], ~0ull, a);
+    q16x2_count_word(w[4], 0xffffffffull, a);                    // chars [128, 144)
+    part[2 * j + 1] = a[0] | (a[1] << 8) | (a[2] << 16) | (a[3] << 24);
+    q16x2_count_word(w[4], ~0xffffffffull, a);
+    q16x2_count_word(w[5], ~0ull, a);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) tot[(uint64_t)c * L + j] = a[c];
+  }
+}
+
+__global__ void k_q16x2_write(const uint64_t* __restrict__ t, uint64_t L, const uint64_t* __restrict__ R,
+                              const uint32_t* __restrict__ part, uint4* __restrict__ lines, uint32_t* __restrict__ super) {
+  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < L; j += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t j0 = (j >> QD_SB_LOG) << QD_SB_LOG;
+    uint64_t sb[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      sb[c] = R[(uint64_t)c * L + j0] >> QD_SHIFT;
+      if (j == j0) super[4 * (j >> QD_SB_LOG) + c] = (uint32_t)sb[c];
+    }
+    const uint64_t* w = t + 6 * j;
+    ulonglong2* dst = reinterpret_cast<ulonglong2*>(lines + 4 * j);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const uint32_t pc = part[2 * j + h];
+      uint64_t d = 0;
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        d |= (R[(uint64_t)c * L + j] + ((pc >> (8 * c)) & 0xffu) - (sb[c] << QD_SHIFT)) << (16 * c);
+      dst[2 * h] = make_ulonglong2(d, w[3 * h]);
+      dst[2 * h + 1] = make_ulonglong2(w[3 * h + 1], w[3 * h + 2]);
+    }
+  }
+}
+
+qr_status quadrank16x2_build_device(const uint64_t* d_text, uint64_t n, int device, cudaStream_t st, qr_index** out) {
+  qr_index* h = nullptr;
+  qr_status rs = alloc_index(4, n, device, &h, QR_LAYOUT_QUADRANK16X2);
+  if (rs != QR_OK) return rs;
+  const uint64_t L = h->n_lines;
+  uint64_t *tot = nullptr, *R = nullptr;
+  uint32_t* part = nullptr;
+  void* tmp = nullptr;
+  size_t tb = 0;
+  cudaError_t e;
+  auto bail = [&](cudaError_t err, const char* what) {
+    cudaFreeAsync(tot, st); cudaFreeAsync(R, st); cudaFreeAsync(part, st); cudaFreeAsync(tmp, st);
+    qr_free(h);
+    return cuda_fail(err, what);
+  };
+  if ((e = cudaMallocAsync((void**)&tot, 4 * L * 8, st))) return bail(e, "alloc tot");
+  if ((e = cudaMallocAsync((void**)&R, 4 * L * 8, st))) return bail(e, "alloc R");
+  if ((e = cudaMallocAsync((void**)&part, 2 * L * 4, st))) return bail(e, "alloc part");
+  const unsigned g = grid_stride_blocks(L, 256, h->sm_count, 16);
+  k_q16x2_count<<<g, 256, 0, st>>>(d_text, L, tot, part);
+  if ((e = cub::DeviceScan::ExclusiveSum(nullptr, tb, tot, R, (int64_t)L, st))) return bail(e, "scan size");
+  if ((e = cudaMallocAsync(&tmp, tb, st))) return bail(e, "alloc scan tmp");
+  for (int c = 0; c < 4; ++c)
+    if ((e = cub::DeviceScan::ExclusiveSum(tmp, tb, tot + (uint64_t)c * L, R + (uint64_t)c * L, (int64_t)L, st)))
+      return bail(e, "scan");
+  k_q16x2_write<<<g, 256, 0, st>>>(d_text, L, R, part, h->lines, h->super);
+  if ((e = cudaGetLastError())) return bail(e, "k_q16x2_write");
+  cudaFreeAsync(tot, st); cudaFreeAsync(R, st); cudaFreeAsync(part, st); cudaFreeAsync(tmp, st);
+  if ((rs = build_super_pack(h, st)) != QR_OK) { qr_free(h); return rs; }
+  *out = h;
+  return QR_OK;
+}
+
 // ------------------------------------------------------------------ QuadRank64 build
 
 __global__ void k_q64_count(const uint64_t* __restrict__ t, uint64_t L, uint64_t* __restrict__ tot,
@@ -428,6 +522,7 @@ cudaError_t launch_variant(const qr_index* h, const uint64_t* q, const uint8_t* 
                            cudaStream_t st) {
   if (m == 0) return cudaSuccess;
   if (h->layout == QR_LAYOUT_BIRANK16X2) return launch_b16x2_rank(h, q, c, out, m, what, st);
+  if (h->layout == QR_LAYOUT_QUADRANK16X2) return launch_q16x2_rank(h, q, c, out, m, what, st);
   switch (g_rank_k) {
     case 1: return v_launch<1>(h, q, c, out, m, what, st);
     case 4: return v_launch<4>(h, q, c, out, m, what, st);
@@ -515,6 +610,25 @@ struct RankOne {
       const uint64_t dw = (c & 2u) ? a[1] : a[0];
       const uint64_t base = ((uint64_t)s << QD_SHIFT) + ((dw >> (16 * (c & 1u))) & 0xffffull);
       return right ? base + cnt : base - cnt;
+    }
+    if (h.layout == QR_LAYOUT_QUADRANK16X2) {
+      uint64_t j = q / Q16X2_B;
+      j = j > last ? last : j;
+      uint64_t d = q - j * Q16X2_B;
+      d = d > Q16X2_B - 1 ? Q16X2_B - 1 : d;
+      const uint32_t hh = d >= 96 ? 1u : 0u;
+      const uint32_t x = (uint32_t)d - 96u * hh;
+      ld_sector_na(h.lines + 4 * j + 2 * hh, a[0], a[1], a[2], a[3]);
+      const uint32_t s = __ldg(h.super + 4 * (j >> QD_SB_LOG) + (c & 3u));
+      const uint64_t pat = (uint64_t)(c & 3u) * 0x5555555555555555ull;
+      uint32_t cnt = 0;
+#pragma unroll
+      for (int t = 0; t < 3; ++t) {
+        const uint64_t e = ~(a[1 + t] ^ pat);
+        cnt += __popcll(e & (e >> 1) & 0x5555555555555555ull & (prefix_mask(2 * (int)x, t) ^ prefix_mask(96, t)));
+      }
+      const uint64_t base = ((uint64_t)s << QD_SHIFT) + ((a[0] >> (16 * (c & 3u))) & 0xffffull);
+      return x >= 48 ? base + cnt : base - cnt;
     }
     // QuadRank64
     uint64_t j = q >> 7;

@@ -127,7 +127,7 @@ def _chain_reference(rank_fn, q, n, L):
 
 
 @pytest.mark.parametrize("layout", [qr.QR_LAYOUT_BIRANK16, qr.QR_LAYOUT_BIRANK64X2, qr.QR_LAYOUT_QUADRANK16,
-                                    qr.QR_LAYOUT_QUADRANK64, qr.QR_LAYOUT_BIRANK16X2])
+                                    qr.QR_LAYOUT_QUADRANK64, qr.QR_LAYOUT_BIRANK16X2, qr.QR_LAYOUT_QUADRANK16X2])
 def test_rank_chain_latency_mode(cuda, layout):
     torch = _torch()
     n = 3 * 63488 + 1001
@@ -154,7 +154,7 @@ def test_rank_chain_latency_mode(cuda, layout):
 
 
 @pytest.mark.parametrize("layout", [qr.QR_LAYOUT_BIRANK16, qr.QR_LAYOUT_BIRANK64X2, qr.QR_LAYOUT_QUADRANK16,
-                                    qr.QR_LAYOUT_QUADRANK64, qr.QR_LAYOUT_BIRANK16X2])
+                                    qr.QR_LAYOUT_QUADRANK64, qr.QR_LAYOUT_BIRANK16X2, qr.QR_LAYOUT_QUADRANK16X2])
 def test_save_load_roundtrip(cuda, layout, tmp_path):
     """Checkpoint/resume: export -> .npz -> import gives a handle that answers identically, and the
     build is deterministic (byte-identical layout on a rebuild)."""
@@ -270,3 +270,100 @@ def test_birank16x2_superblock_sources(cuda, src):
     ora = oracle.BitsOracle(w, n)
     assert np.array_equal(to_host(out), ora.rank(q))
     assert np.array_equal(to_host(out2), ora.rank(q, c))
+
+
+# ------------------------------------------------------------------ QuadRank16x2 (B200 sector-local σ=4 variant)
+Q16X2_SIZES = [0, 1, 47, 48, 49, 95, 96, 97, 143, 144, 145, 191, 192, 193, 383, 384, 385,
+               256 * 192 - 1, 256 * 192, 256 * 192 + 1, 9 * 256 * 192 + 77, 17 * 256 * 192 + 4321, (1 << 21) + 5]
+
+
+def _q16x2_text(kind, n, seed):
+    if kind == "iid":
+        return gen.dna(seed, n)
+    word = {"G": 0xAAAAAAAAAAAAAAAA, "T": 0xFFFFFFFFFFFFFFFF}[kind]
+    return np.full(max(1, (n + 31) // 32), np.uint64(word))
+
+
+@pytest.mark.parametrize("n", Q16X2_SIZES)
+@pytest.mark.parametrize("kind", ["iid", "G"])
+def test_quadrank16x2_parity(cuda, n, kind):
+    """rank(q,c) for every (q,c) on small n, boundaries of the sector anchors (48, 144), the sector
+    split (96), lines (192) and superblocks (256 lines) on larger n; rank_4; a single repeated
+    symbol makes every delta and superblock increment maximal."""
+    torch = _torch()
+    w = _q16x2_text(kind, n, 6000 + n)
+    h = qr.qr_build(w, n, qr.QR_LAYOUT_QUADRANK16X2)
+    L = n // 192 + 1
+    assert h.layout == qr.QR_LAYOUT_QUADRANK16X2
+    assert h.line_bytes == 64 * L and h.super_bytes == 16 * ((L - 1) // 256 + 1)
+    ora = oracle.DnaOracle(w, n)
+    if n <= 40000:
+        q = np.repeat(np.arange(n + 1, dtype=np.uint64), 4)
+        c = np.tile(np.arange(4, dtype=np.uint8), n + 1)
+    else:
+        q, c = gen.queries(8, n, 200000, with_c=True)
+        bq = boundary_queries(n, 96, 256 * 192, 48)
+        q = np.concatenate([q, np.repeat(bq, 4)])
+        c = np.concatenate([c, np.tile(np.arange(4, dtype=np.uint8), bq.size)])
+    dq = to_dev(q, cuda)
+    out = torch.empty_like(dq)
+    qr.qr_rank(h, dq, to_dev(c, cuda), out)
+    o4 = torch.empty((q.size, 4), dtype=torch.uint64, device=cuda)
+    qr.qr_rank_all4(h, dq, o4)
+    torch.cuda.synchronize()
+    assert np.array_equal(to_host(out), ora.rank(q, c))
+    assert np.array_equal(to_host(o4), ora.rank_all4(q))
+
+
+def test_quadrank16x2_layout_closed_forms(cuda):
+    """Decode every sector: d_{j,h,c} + 2^13 s_{j>>8,c} = rank(192 j + 96 h + 48, c), s_{i,c} =
+    rank(256 i 192, c) >> 13, data = text words [6j + 3h, +3); 33.3% overhead (+ superblocks)."""
+    for n in (11 * 256 * 192 + 999, 2 * 256 * 192 + 5):
+        w = gen.dna(91, n)
+        h = qr.qr_build(w, n, qr.QR_LAYOUT_QUADRANK16X2)
+        lines, sup = qr.qr_export_layout(h)
+        L = n // 192 + 1
+        u64 = lines.view(np.uint64).reshape(L, 2, 4)
+        sup = sup.view(np.uint32).reshape(-1, 4)
+        ora = oracle.DnaOracle(w, n)
+        for hh in (0, 1):
+            raw = np.arange(L, dtype=np.uint64) * 192 + 96 * hh + 48
+            anchors = np.minimum(raw, n)
+            for c in range(4):
+                d = (u64[:, hh, 0] >> np.uint64(16 * c)) & np.uint64(0xffff)
+                full = d + (sup[np.arange(L) // 256, c].astype(np.uint64) << np.uint64(13))
+                # an anchor past n counts the padding characters, which are A (reading R4)
+                want = ora.rank(anchors, np.full(L, c, np.uint8)) + (raw - anchors if c == 0 else 0)
+                assert np.array_equal(full, want), (hh, c)
+        text = np.zeros(6 * L, np.uint64)
+        text[: min(w.size, 6 * L)] = w[: 6 * L]
+        assert np.array_equal(u64[:, :, 1:].reshape(-1), text)
+
+
+@pytest.mark.parametrize("src", ["table", "global", "cluster"])
+def test_quadrank16x2_superblock_sources(cuda, src):
+    torch = _torch()
+    knobs = {"table": [("rank_lane_table", 1), ("rank_smem", 0)], "global": [("rank_lane_table", 0), ("rank_smem", 0)],
+             "cluster": [("rank_smem", 2)]}[src]
+    n = 21 * 256 * 192 + 321
+    w = gen.dna(92, n)
+    h = qr.qr_build(w, n, qr.QR_LAYOUT_QUADRANK16X2)
+    m = (1 << 22) + 9
+    q, c = gen.queries(93, n, m, with_c=True)
+    dq = to_dev(q, cuda)
+    try:
+        for k, v in knobs:
+            qr.qr_set_tuning(k, v)
+        out = torch.empty_like(dq)
+        qr.qr_rank(h, dq, to_dev(c, cuda), out)
+        o4 = torch.empty((m, 4), dtype=torch.uint64, device=cuda)
+        qr.qr_rank_all4(h, dq, o4)
+        g = torch.empty_like(dq)
+        qr.qr_gather_ceiling(h, dq, g, 0)
+        torch.cuda.synchronize()
+    finally:
+        qr.qr_set_tuning("rank_lane_table", 1)
+        qr.qr_set_tuning("rank_smem", 1)
+    ora = oracle.DnaOracle(w, n)
+    assert np.array_equal(to_host(out), ora.rank(q, c))
+    assert np.array_equal(to_host(o4), ora.rank_all4(q))

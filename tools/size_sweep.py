@@ -19,8 +19,7 @@ def t(fn, reps=3):
 M = 2 * 10**8
 q = torch.empty(M, dtype=torch.uint64, device=dev); out = torch.empty_like(q)
 c = torch.empty(M, dtype=torch.uint8, device=dev)
-for lg in (20, 24, 26, 28, 30, 32, 34, 35, 36):
-    if len(sys.argv) > 1 and sys.argv[1] == "bits_only" and lg > 36: break
+for lg in ((20, 24, 26, 28, 30, 32, 34, 35, 36) if "dna_only" not in sys.argv else ()):
     n = 1 << lg
     bits = torch.empty((n + 63) // 64, dtype=torch.uint64, device=dev); gen.bits_dev(7, n, 0.5, bits)
     gen.queries_dev(8, n, M, q)
@@ -43,7 +42,8 @@ for lg in (20, 24, 26, 28, 30, 32, 33, 34):
     text = torch.empty((n + 31) // 32, dtype=torch.uint64, device=dev); gen.dna_dev(9, n, 0, text)
     gen.queries_dev(10, n, M, q, c)
     r = {"sigma": 4, "log2_n": lg}
-    for name, layout in (("quadrank16", qr.QR_LAYOUT_QUADRANK16), ("quadrank64", qr.QR_LAYOUT_QUADRANK64)):
+    for name, layout in (("quadrank16", qr.QR_LAYOUT_QUADRANK16), ("quadrank16x2", qr.QR_LAYOUT_QUADRANK16X2),
+                         ("quadrank64", qr.QR_LAYOUT_QUADRANK64)):
         h = qr.qr_build(text, n, layout)
         r[name + "_gq_s"] = M / t(lambda: qr.qr_rank(h, q, c, out, M, st)) / 1e6
         r[name + "_all4_gq_s"] = M / t(lambda: qr.qr_rank_all4(h, q, o4, M, st)) / 1e6
