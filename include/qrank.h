@@ -136,6 +136,13 @@ qr_status qr_fm_build_ex(const uint64_t* text2b, uint64_t n, const uint32_t* sa_
 /* The k-mer table width of an FM handle. */
 qr_status qr_fm_kmer_width(const qr_fm* fm, int* kmer_k);
 
+/* As qr_fm_build_ex with the rank layout of the BWT: QR_LAYOUT_QUADRANK16 (the paper's QuadFm,
+ * 2.29 bits/bp) or QR_LAYOUT_QUADRANK16X2 (the sector-local B200 variant, 33.4%: every rank of
+ * a backward step reads one 32-B sector).  kmer_k = -1 takes qr_fm_build's
+ * default width.  Counts never depend on either.  QR_EINVAL for another layout. */
+qr_status qr_fm_build_opts(const uint64_t* text2b, uint64_t n, const uint32_t* sa_or_null, int kmer_k, int bwt_layout,
+                           int device, void* stream, qr_fm** out);
+
 /* out[k] = number of (overlapping) occurrences of pattern k in T, as u32 (backward search:
  * lo = C[c] + Occ(c, lo), hi = C[c] + Occ(c, hi), Occ(c,x) = rank(x,c) - [c = A and x > spos];
  * seeded by the 8-mer table when the pattern has >= 8 symbols).  patterns: concatenated, one

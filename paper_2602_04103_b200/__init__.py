@@ -30,7 +30,7 @@ EXPORTS = (
     "qr_fm_count_work", "qr_gather_ceiling", "qr_info", "qr_export_layout", "qr_fm_info", "qr_fm_export_kmer",
     "qr_clone_to_device", "qr_fm_clone_to_device", "qr_sync", "qr_free", "qr_fm_free", "qr_last_error",
     "qr_version", "qr_set_tuning", "qr_build", "qr_layout", "qr_rank_chain", "qr_import_layout", "qr_fm_build_ex", "qr_fm_kmer_width",
-    "qr_super_cache_bytes", "qr_super_cache_clusters",
+    "qr_super_cache_bytes", "qr_super_cache_clusters", "qr_fm_build_opts",
 )
 
 
@@ -81,6 +81,7 @@ def lib():
             "qr_import_layout": ([V, V, U64, I32, I32, V, PP], I32),
             "qr_fm_build_ex": ([V, U64, V, I32, I32, V, PP], I32),
             "qr_fm_kmer_width": ([V, C.POINTER(C.c_int)], I32),
+            "qr_fm_build_opts": ([V, U64, V, I32, I32, I32, V, PP], I32),
             "qr_super_cache_bytes": ([V, C.POINTER(U64)], I32),
             "qr_super_cache_clusters": ([V, C.POINTER(C.c_int)], I32),
         }
@@ -242,9 +243,16 @@ def qr_rank_all4(h: Index, q, out4, m: int | None = None, stream=None):
     return out4
 
 
-def qr_fm_build(text2b, n: int, sa=None, device: int = 0, stream=None, kmer_k: int | None = None) -> Fm:
-    """qr_fm_build (kmer_k None: the library's default width for n) or qr_fm_build_ex (explicit width)."""
+def qr_fm_build(text2b, n: int, sa=None, device: int = 0, stream=None, kmer_k: int | None = None,
+                bwt_layout: int | None = None) -> Fm:
+    """qr_fm_build (kmer_k None: the library's default width for n), qr_fm_build_ex (explicit width) or
+    qr_fm_build_opts (explicit BWT rank layout, QR_LAYOUT_QUADRANK16 or QR_LAYOUT_QUADRANK16X2)."""
     out = C.c_void_p()
+    if bwt_layout is not None:
+        k = kmer_k if kmer_k is not None else -1          # -1: the library's default width for n
+        _check(lib().qr_fm_build_opts(_ptr(text2b), n, _ptr(sa), k, bwt_layout, device, _stream(stream), C.byref(out)),
+               "qr_fm_build_opts")
+        return Fm(out.value)
     if kmer_k is None:
         _check(lib().qr_fm_build(_ptr(text2b), n, _ptr(sa), device, _stream(stream), C.byref(out)), "qr_fm_build")
     else:

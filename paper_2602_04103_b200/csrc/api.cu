@@ -128,7 +128,7 @@ qr_status alloc_index(int sigma, uint64_t n, int device, qr_index** out, int lay
 uint64_t super_bytes_of(const qr_index* h) { return h->n_super * (h->sigma == 2 ? 4 : 16); }
 
 qr_status fm_build_device(const uint64_t* d_text, uint64_t n, const uint32_t* d_sa_given, int device, cudaStream_t st,
-                          qr_fm** out, int kmer_k);
+                          qr_fm** out, int kmer_k, int bwt_layout);
 __global__ void k_mask_tail_bits(uint64_t* words, uint64_t n);
 __global__ void k_mask_tail_chars(uint64_t* words, uint64_t n);
 cudaError_t launch_bi_gather(const qr_index* h, const uint64_t* q, uint64_t* out, uint64_t m, int mode, cudaStream_t st);
@@ -529,23 +529,34 @@ QR_EXPORT qr_status qr_gather_ceiling(const qr_index* h, const uint64_t* q, uint
   return e ? cuda_fail(e, "qr_gather_ceiling launch") : QR_OK;
 }
 
-QR_EXPORT qr_status qr_fm_build_ex(const uint64_t* text2b, uint64_t n, const uint32_t* sa_or_null, int kmer_k,
-                                   int device, void* stream, qr_fm** out);
-
 // Default k-mer table width: the paper's 8 for small texts; on B200 wider tables replace
 // more backward steps by one lookup and HBM holds them easily: 10 (8 MiB) from n = 2^20, 12
 // (128 MiB) from n = 2^24 — configs[3] 5.61 -> 6.57 G patterns/s, configs[4] 0.94 -> 0.99
 // (profiles/r01_fm_k_probe*.jsonl).  Counts never depend on it.
 int fm_default_kmer_k(uint64_t n) { return n < (1ull << 20) ? 8 : n < (1ull << 24) ? 10 : 12; }
 
+QR_EXPORT qr_status qr_fm_build_ex(const uint64_t* text2b, uint64_t n, const uint32_t* sa_or_null, int kmer_k,
+                                   int device, void* stream, qr_fm** out);
+
 QR_EXPORT qr_status qr_fm_build(const uint64_t* text2b, uint64_t n, const uint32_t* sa_or_null, int device,
                                 void* stream, qr_fm** out) {
   return qr_fm_build_ex(text2b, n, sa_or_null, fm_default_kmer_k(n), device, stream, out);
 }
 
+QR_EXPORT qr_status qr_fm_build_opts(const uint64_t* text2b, uint64_t n, const uint32_t* sa_or_null, int kmer_k,
+                                     int bwt_layout, int device, void* stream, qr_fm** out);
+
 QR_EXPORT qr_status qr_fm_build_ex(const uint64_t* text2b, uint64_t n, const uint32_t* sa_or_null, int kmer_k,
                                    int device, void* stream, qr_fm** out) {
+  return qr_fm_build_opts(text2b, n, sa_or_null, kmer_k, QR_LAYOUT_QUADRANK16, device, stream, out);
+}
+
+QR_EXPORT qr_status qr_fm_build_opts(const uint64_t* text2b, uint64_t n, const uint32_t* sa_or_null, int kmer_k,
+                                     int bwt_layout, int device, void* stream, qr_fm** out) {
+  if (kmer_k == -1) kmer_k = fm_default_kmer_k(n);
   if (kmer_k < 0 || kmer_k > 14) return fail(QR_EINVAL, "qr_fm_build_ex: kmer_k must be 0..14");
+  if (bwt_layout != QR_LAYOUT_QUADRANK16 && bwt_layout != QR_LAYOUT_QUADRANK16X2)
+    return fail(QR_EINVAL, "qr_fm_build_opts: bwt_layout must be QR_LAYOUT_QUADRANK16 or QR_LAYOUT_QUADRANK16X2");
   if (!out || !text2b) return fail(QR_EINVAL, "qr_fm_build: null pointer");
   *out = nullptr;
   if (n == 0) return fail(QR_EINVAL, "qr_fm_build: empty text");
@@ -566,7 +577,7 @@ QR_EXPORT qr_status qr_fm_build_ex(const uint64_t* text2b, uint64_t n, const uin
       cudaFreeAsync(d, st); cudaFreeAsync(dsa, st); return cuda_fail(e, "copy sa");
     }
   }
-  s = fm_build_device(d, n, dsa, device, st, out, kmer_k);
+  s = fm_build_device(d, n, dsa, device, st, out, kmer_k, bwt_layout);
   cudaFreeAsync(d, st);
   if (dsa) cudaFreeAsync(dsa, st);
   cudaStreamSynchronize(st);

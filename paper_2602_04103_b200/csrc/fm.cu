@@ -30,6 +30,7 @@ struct FmParams {
   uint64_t last_line;
   uint32_t C[4];        // host copy; the kernels read C from the table tail (Ct) with one load
   const uint32_t* Ct;   // = (const uint32_t*)(kmer + 4^K): C[0..3] stored after the k-mer table
+  int bw;                 // BWT rank layout: 0 QuadRank16, 1 QuadRank16x2 (sector-local)
   const uint64_t* spack;  // packed superblock table (sbcache.cu encoding, 2 parts), or null
   uint32_t spack_half;    // groups per part
   uint32_t n_super;
@@ -228,7 +229,7 @@ __global__ void k_sym_counts(const uint64_t* __restrict__ text, uint64_t n, unsi
 // sectors and the superblock word are loaded once and reused from registers, which halves the
 // L1 wavefronts of a step when the structure is L2-resident.  N < 2^32: u32 arithmetic.
 template <int SMS = 0>
-__device__ __forceinline__ void fm_step(const FmParams& F, uint32_t c, uint32_t& lo, uint32_t& hi, uint32_t& lines) {
+__device__ __forceinline__ void fm_step16(const FmParams& F, uint32_t c, uint32_t& lo, uint32_t& hi, uint32_t& lines) {
   uint32_t jl = (lo >> 5) / 7u;                                  // floor(lo/224)
   uint32_t jh = (hi >> 5) / 7u;
   jl = jl > (uint32_t)F.last_line ? (uint32_t)F.last_line : jl;
@@ -275,12 +276,68 @@ __device__ __forceinline__ void fm_step(const FmParams& F, uint32_t c, uint32_t&
   hi = Cc + rh;
 }
 
+// ---- the same step over a QuadRank16x2 BWT (variants.cu, reading R25): every rank reads one
+// 32-B sector (four u16 deltas to the sector's char 48 + 96 packed chars); lo and hi share the
+// load when they fall in the same sector.  Superblock words as QuadRank16 (fm_super).
+__device__ __forceinline__ void x2_locate(uint32_t x, uint32_t last_line, uint32_t& j, uint32_t& h, uint32_t& p) {
+  uint32_t jj = (x >> 6) / 3u;                                    // floor(x/192)
+  jj = jj > last_line ? last_line : jj;
+  uint32_t d = x - jj * (uint32_t)Q16X2_B;
+  d = d > (uint32_t)Q16X2_B - 1 ? (uint32_t)Q16X2_B - 1 : d;
+  h = d >= 96 ? 1u : 0u;
+  p = d - 96u * h;
+  j = jj;
+}
+// count of symbol c among the sector's chars between p and its anchor 48, signed by the side
+__device__ __forceinline__ uint32_t x2_rank(const uint64_t (&w)[4], uint32_t p, uint32_t c, uint32_t s) {
+  const uint64_t pat = (uint64_t)c * 0x5555555555555555ull;
+  uint32_t cnt = 0;
+#pragma unroll
+  for (int t = 0; t < 3; ++t) {
+    const uint64_t e = ~(w[1 + t] ^ pat);
+    cnt += __popcll(e & (e >> 1) & 0x5555555555555555ull & (prefix_mask(2 * (int)p, t) ^ prefix_mask(96, t)));
+  }
+  const uint32_t base = (s << QD_SHIFT) + (uint32_t)((w[0] >> (16 * c)) & 0xffffull);
+  return p >= 48 ? base + cnt : base - cnt;
+}
+
+template <int SMS = 0>
+__device__ __forceinline__ void fm_step_x2(const FmParams& F, uint32_t c, uint32_t& lo, uint32_t& hi, uint32_t& lines) {
+  uint32_t jl, hl, pl, jh, hh, ph;
+  x2_locate(lo, (uint32_t)F.last_line, jl, hl, pl);
+  x2_locate(hi, (uint32_t)F.last_line, jh, hh, ph);
+  const bool same = jl == jh && hl == hh;
+  uint64_t a[4], b[4] = {0, 0, 0, 0};
+  ld_sector(F.lines + 4 * (uint64_t)jl + 2 * hl, a[0], a[1], a[2], a[3]);
+  if (!same) ld_sector(F.lines + 4 * (uint64_t)jh + 2 * hh, b[0], b[1], b[2], b[3]);
+  const uint32_t sl = fm_super<SMS>(F, jl >> QD_SB_LOG, c);
+  const uint32_t sh = (jl >> QD_SB_LOG) == (jh >> QD_SB_LOG) ? sl : fm_super<SMS>(F, jh >> QD_SB_LOG, c);
+  if (same) {
+#pragma unroll
+    for (int t = 0; t < 4; ++t) b[t] = a[t];
+  }
+  lines = jl == jh ? 1u : 2u;
+  uint32_t rl = x2_rank(a, pl, c, sl), rh = x2_rank(b, ph, c, sh);
+  if (c == 0) { rl -= (lo > (uint32_t)F.spos); rh -= (hi > (uint32_t)F.spos); }
+  const uint32_t Cc = __ldg(F.Ct + c);
+  lo = Cc + rl;
+  hi = Cc + rh;
+}
+
+// one backward step over either BWT layout (BW 0: QuadRank16 de-duplicating step, 1: QuadRank16x2)
+template <int SMS = 0, int BW = 0>
+__device__ __forceinline__ void fm_step(const FmParams& F, uint32_t c, uint32_t& lo, uint32_t& hi, uint32_t& lines) {
+  if (BW == 1) fm_step_x2<SMS>(F, c, lo, hi, lines);
+  else         fm_step16<SMS>(F, c, lo, hi, lines);
+}
+
+template <int BW>
 __global__ void k_kmer_table(FmParams F, uint2* __restrict__ table) {
   const uint32_t key = blockIdx.x * blockDim.x + threadIdx.x;
   if (key >= (1u << (2 * F.K))) return;
   uint32_t lo = 0, hi = (uint32_t)F.N;
   uint32_t dummy;
-  for (int t = 0; t < F.K && lo < hi; ++t) fm_step(F, (key >> (2 * t)) & 3u, lo, hi, dummy);   // last char first
+  for (int t = 0; t < F.K && lo < hi; ++t) fm_step<0, BW>(F, (key >> (2 * t)) & 3u, lo, hi, dummy);   // last char first
   if (lo >= hi) lo = hi = 0;
   table[key] = make_uint2(lo, hi);
 }
@@ -443,7 +500,7 @@ constexpr uint32_t FM_CHUNK = 64;
 #define QR_FM_MINB 4
 #endif
 
-template <bool FIXED, bool WORK, int STRANDS, bool LEAN, int SMS, bool DYN>
+template <bool FIXED, bool WORK, int STRANDS, bool LEAN, int SMS, bool DYN, int BW = 0>
 __global__ void __launch_bounds__(256, QR_FM_MINB) k_fm_count(FmParams F, const uint8_t* __restrict__ pat,
                                                      const uint64_t* __restrict__ offs, const uint32_t* __restrict__ lens,
                                                      uint32_t fixed_len, uint32_t* __restrict__ out,
@@ -481,8 +538,9 @@ __global__ void __launch_bounds__(256, QR_FM_MINB) k_fm_count(FmParams F, const 
   auto step = [&]() {                                    // one backward step (LF mapping)
     const uint32_t c = rc ? 3u - P.at((int64_t)len - 1 - k) : P.at(k);
     uint32_t nl;
-    if (LEAN) fm_step_lean<SMS>(F, C4, c, lo, hi, nl);
-    else      fm_step<SMS>(F, c, lo, hi, nl);
+    if (BW == 1)   fm_step<SMS, 1>(F, c, lo, hi, nl);
+    else if (LEAN) fm_step_lean<SMS>(F, C4, c, lo, hi, nl);
+    else           fm_step<SMS, 0>(F, c, lo, hi, nl);
     --k;
     if (WORK) { n_steps += 1; n_lines += nl; }
   };
@@ -554,6 +612,33 @@ __global__ void __launch_bounds__(256, QR_FM_MINB) k_fm_count(FmParams F, const 
 // the others branch from the exact path with rank_4.  Each branch continues as an exact
 // backward search and usually dies within a few steps.
 
+// rank_4 over a QuadRank16x2 BWT at row x (one sector; plane popcounts as q16x2_rank4).
+__device__ __forceinline__ void fm_occ4_x2(const FmParams& F, uint32_t x, uint32_t occ[4]) {
+  uint32_t j, h, p;
+  x2_locate(x, (uint32_t)F.last_line, j, h, p);
+  uint64_t w[4];
+  ld_sector(F.lines + 4 * (uint64_t)j + 2 * h, w[0], w[1], w[2], w[3]);
+  const uint4 sv = __ldg(reinterpret_cast<const uint4*>(F.super) + (j >> QD_SB_LOG));
+  uint32_t nl = 0, nh = 0, nt = 0;
+#pragma unroll
+  for (int t = 0; t < 3; ++t) {
+    const uint64_t msk = 0x5555555555555555ull & (prefix_mask(2 * (int)p, t) ^ prefix_mask(96, t));
+    const uint64_t l = w[1 + t] & msk, hh = (w[1 + t] >> 1) & msk;
+    nl += __popcll(l);
+    nh += __popcll(hh);
+    nt += __popcll(l & hh);
+  }
+  const uint32_t len = p >= 48 ? p - 48u : 48u - p;
+  const uint32_t cnt[4] = {len - nl - nh + nt, nl - nt, nh - nt, nt};
+  const uint32_t s4[4] = {sv.x, sv.y, sv.z, sv.w};
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const uint32_t base = (s4[c] << QD_SHIFT) + (uint32_t)((w[0] >> (16 * c)) & 0xffffull);
+    occ[c] = p >= 48 ? base + cnt[c] : base - cnt[c];
+  }
+  occ[0] -= (x > (uint32_t)F.spos);
+}
+
 // rank_4 over the BWT at row x (Occ of all four symbols, '$' correction on A).
 __device__ __forceinline__ void fm_occ4(const FmParams& F, uint32_t x, uint32_t occ[4]) {
   uint32_t j = (x >> 5) / 7u;
@@ -590,9 +675,10 @@ __device__ __forceinline__ void fm_occ4(const FmParams& F, uint32_t x, uint32_t 
 }
 
 // exact backward search of P[0..k] from [lo, hi); returns the final interval size
+template <int BW>
 __device__ __forceinline__ uint32_t fm_continue(const FmParams& F, PatWindow& P, int64_t k, uint32_t lo, uint32_t hi) {
   uint32_t nl;
-  for (; k >= 0 && lo < hi; --k) fm_step(F, P.at(k), lo, hi, nl);
+  for (; k >= 0 && lo < hi; --k) fm_step<0, BW>(F, P.at(k), lo, hi, nl);
   return lo < hi ? hi - lo : 0u;
 }
 
@@ -611,7 +697,7 @@ __device__ __forceinline__ uint64_t approx_next(unsigned long long* ctr, uint64_
   return b + __popc(am & ((1u << lane) - 1u));
 }
 
-template <bool FIXED>
+template <bool FIXED, int BW>
 __global__ void __launch_bounds__(256) k_fm_approx1(FmParams F, const uint8_t* __restrict__ pat,
                                                     const uint64_t* __restrict__ offs,
                                                     const uint32_t* __restrict__ lens, uint32_t fixed_len,
@@ -635,7 +721,7 @@ __global__ void __launch_bounds__(256) k_fm_approx1(FmParams F, const uint8_t* _
         const uint32_t f = (key0 >> (2 * t)) & 3u;
         for (uint32_t r = 1; r < 4; ++r) {
           const uint2 iv = __ldg(F.kmer + (key0 ^ ((f ^ ((f + r) & 3u)) << (2 * t))));
-          if (iv.x < iv.y) total += fm_continue(F, P, (int64_t)len - 1 - F.K, iv.x, iv.y);
+          if (iv.x < iv.y) total += fm_continue<BW>(F, P, (int64_t)len - 1 - F.K, iv.x, iv.y);
         }
       }
       const uint2 iv0 = __ldg(F.kmer + key0);
@@ -647,13 +733,13 @@ __global__ void __launch_bounds__(256) k_fm_approx1(FmParams F, const uint8_t* _
     }
     for (; j >= 0 && lo < hi; --j) {                     // exact path; branch on the mismatch at j
       uint32_t ol[4], oh[4];
-      fm_occ4(F, lo, ol);
-      fm_occ4(F, hi, oh);
+      if (BW == 1) { fm_occ4_x2(F, lo, ol); fm_occ4_x2(F, hi, oh); }
+      else         { fm_occ4(F, lo, ol); fm_occ4(F, hi, oh); }
       const uint32_t cj = P.at(j);
 #pragma unroll
       for (uint32_t c = 0; c < 4; ++c) {
         const uint32_t a = Cs[c] + ol[c], b = Cs[c] + oh[c];
-        if (c != cj && a < b) total += fm_continue(F, P, j - 1, a, b);
+        if (c != cj && a < b) total += fm_continue<BW>(F, P, j - 1, a, b);
       }
       lo = Cs[cj] + ol[cj];
       hi = Cs[cj] + oh[cj];
@@ -680,6 +766,7 @@ static FmParams params_of(const qr_fm* fm) {
   for (int c = 0; c < 4; ++c) F.C[c] = (uint32_t)fm->C[c];
   F.Ct = reinterpret_cast<const uint32_t*>(fm->kmer + kmer_c_offset(fm->kmer_k));
   F.spack = fm->bwt->spack;
+  F.bw = fm->bwt->layout == QR_LAYOUT_QUADRANK16X2 ? 1 : 0;
   F.spack_half = (uint32_t)fm->bwt->spack_half;
   F.n_super = (uint32_t)fm->bwt->n_super;
   return F;
@@ -728,7 +815,8 @@ static void launch_fm1(unsigned g, size_t smem, cudaStream_t st, const FmParams&
                        const uint64_t* offs, const uint32_t* lens, uint32_t fixed_len, uint32_t* out, uint32_t* out_rc,
                        uint64_t m, unsigned long long* w, unsigned long long* ctr, int sms, uint2* seeds) {
   if (ctr) {
-    auto kern = k_fm_count<FIXED, WORK, STRANDS, LEAN, SMS, true>;
+    // QuadRank16x2 BWT: one step flavour (the sector-shared step), LEAN ignored
+    auto kern = F.bw ? k_fm_count<FIXED, WORK, STRANDS, false, SMS, true, 1> : k_fm_count<FIXED, WORK, STRANDS, LEAN, SMS, true, 0>;
     if (seeds)
       k_fm_seed<FIXED, STRANDS><<<grid_stride_blocks(m * STRANDS, 256, sms, 16), 256, 0, st>>>(F, pat, offs, lens,
                                                                                              fixed_len, m, seeds);
@@ -742,7 +830,7 @@ static void launch_fm1(unsigned g, size_t smem, cudaStream_t st, const FmParams&
     unsigned gp = (unsigned)((uint64_t)per_sm * sms < need ? (uint64_t)per_sm * sms : (need ? need : 1));
     kern<<<gp, 256, smem, st>>>(F, pat, offs, lens, fixed_len, out, out_rc, m, w, ctr, seeds);
   } else {
-    auto kern = k_fm_count<FIXED, WORK, STRANDS, LEAN, SMS, false>;
+    auto kern = F.bw ? k_fm_count<FIXED, WORK, STRANDS, false, SMS, false, 1> : k_fm_count<FIXED, WORK, STRANDS, LEAN, SMS, false, 0>;
     if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     kern<<<g, 256, smem, st>>>(F, pat, offs, lens, fixed_len, out, out_rc, m, w, nullptr, nullptr);
   }
@@ -823,7 +911,7 @@ template <bool FIXED>
 static cudaError_t launch_approx(const qr_fm* fm, unsigned g, cudaStream_t st, const FmParams& F, const uint8_t* pat,
                                  const uint64_t* offs, const uint32_t* lens, uint32_t fixed_len, uint32_t* out,
                                  uint64_t m) {
-  auto kern = k_fm_approx1<FIXED>;
+  auto kern = F.bw ? k_fm_approx1<FIXED, 1> : k_fm_approx1<FIXED, 0>;
   if (!g_fm_dyn) {
     kern<<<g, 256, 0, st>>>(F, pat, offs, lens, fixed_len, out, m, nullptr);
     return cudaGetLastError();
@@ -881,7 +969,7 @@ qr_status fm_count_device(const qr_fm* fm, const uint8_t* pat, const uint32_t* l
 
 // d_text: device copy, >= ceil(n/32) words, zero padded.  d_sa: optional device SA (N u32).
 qr_status fm_build_device(const uint64_t* d_text, uint64_t n, const uint32_t* d_sa_given, int device, cudaStream_t st,
-                          qr_fm** out, int kmer_k) {
+                          qr_fm** out, int kmer_k, int bwt_layout) {
   const uint64_t N = n + 1;
   const int sms = sm_count(device);
   cudaError_t e;
@@ -897,7 +985,8 @@ qr_status fm_build_device(const uint64_t* d_text, uint64_t n, const uint32_t* d_
     return s;
   };
   const uint64_t L = N / QD_B + 1;
-  const uint64_t bwt_words = 7 * L;            // the QuadRank builder reads 7 words per line
+  const uint64_t Lx = N / Q16X2_B + 1;
+  const uint64_t bwt_words = 7 * L > 6 * Lx ? 7 * L : 6 * Lx;   // words the QuadRank16 / 16x2 builders read
   if ((e = cudaMallocAsync((void**)&d_aux, 5 * 8, st))) return bail(cuda_fail(e, "alloc aux"));
   cudaMemsetAsync(d_aux, 0, 5 * 8, st);
   if (!d_sa_given) {
@@ -911,7 +1000,8 @@ qr_status fm_build_device(const uint64_t* d_text, uint64_t n, const uint32_t* d_
                                                                           d_bwt, d_aux);
   k_sym_counts<<<grid_stride_blocks((n + 31) / 32, 256, sms, 8), 256, 0, st>>>(d_text, n, d_aux + 1);
   if ((e = cudaGetLastError())) return bail(cuda_fail(e, "k_bwt"));
-  qr_status s = quadrank_build_device(d_bwt, N, device, st, &fm->bwt);
+  qr_status s = bwt_layout == QR_LAYOUT_QUADRANK16X2 ? quadrank16x2_build_device(d_bwt, N, device, st, &fm->bwt)
+                                                     : quadrank_build_device(d_bwt, N, device, st, &fm->bwt);
   if (s != QR_OK) return bail(s);
   cudaMemcpyAsync(h_aux, d_aux, 5 * 8, cudaMemcpyDeviceToHost, st);
   if ((e = cudaStreamSynchronize(st))) return bail(cuda_fail(e, "fm build sync"));
@@ -931,7 +1021,10 @@ qr_status fm_build_device(const uint64_t* d_text, uint64_t n, const uint32_t* d_
     if ((e = cudaStreamSynchronize(st))) return bail(cuda_fail(e, "copy C"));
   }
   FmParams F = params_of(fm);
-  if (kmer_k) k_kmer_table<<<(unsigned)((ne + 255) / 256), 256, 0, st>>>(F, fm->kmer);
+  if (kmer_k) {
+    if (F.bw) k_kmer_table<1><<<(unsigned)((ne + 255) / 256), 256, 0, st>>>(F, fm->kmer);
+    else      k_kmer_table<0><<<(unsigned)((ne + 255) / 256), 256, 0, st>>>(F, fm->kmer);
+  }
   if ((e = cudaGetLastError())) return bail(cuda_fail(e, "k_kmer_table"));
   cudaFreeAsync(d_sa, st);
   cudaFreeAsync(d_bwt, st);

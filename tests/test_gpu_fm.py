@@ -446,3 +446,52 @@ def test_fm_default_kmer_width(cuda):
         fm = qr.qr_fm_build(t, n)
         assert fm.kmer_k == k, (n, fm.kmer_k)
         fm.free()
+
+
+@pytest.mark.parametrize("n,kind", [(1, 0), (7, 0), (100, 0), (1000, 0), (50000, 0), (25000, 1), (3_000_000, 0)])
+@pytest.mark.parametrize("dyn", [0, 1])
+def test_fm_over_quadrank16x2(cuda, n, kind, dyn, fm_dyn_reset):
+    """QuadFm over the sector-local QuadRank16x2 BWT (qr_fm_build_opts): the k-mer table, exact
+    counts (variable lengths, one and both strands), <= 1-substitution counts and the work
+    instrumentation must equal the oracle / the QuadRank16-backed index, static and dynamic order."""
+    torch = _torch()
+    w = gen.dna(700 + n, n, kind)
+    sym = gen.unpack_dna(w, n)
+    ora = oracle.FmOracle(sym)
+    fm = qr.qr_fm_build(w, n, bwt_layout=qr.QR_LAYOUT_QUADRANK16X2)
+    fm16 = qr.qr_fm_build(w, n)
+    assert fm.kmer_k == fm16.kmer_k and fm.spos == ora.spos
+    assert np.array_equal(qr.qr_fm_export_kmer(fm), qr.qr_fm_export_kmer(fm16))
+    qr.qr_set_tuning("fm_dyn", dyn)
+    pats = mixed_patterns(np.random.default_rng(n), sym, 1500)
+    cat, off, lens = oracle.pack_patterns(pats)
+    ref = ora.count(cat, off, lens)
+    d = torch.empty(lens.size, dtype=torch.int32, device=cuda)
+    qr.qr_fm_count(fm, to_dev(cat, cuda), to_dev(lens, cuda), 0, d, lens.size)
+    db = torch.empty(lens.size, dtype=torch.int32, device=cuda)
+    dr = torch.empty(lens.size, dtype=torch.int32, device=cuda)
+    qr.qr_fm_count_both(fm, to_dev(cat, cuda), to_dev(lens, cuda), 0, db, dr, lens.size)
+    d1 = torch.empty(lens.size, dtype=torch.int32, device=cuda)
+    qr.qr_fm_count_approx(fm, to_dev(cat, cuda), to_dev(lens, cuda), 0, 1, d1, lens.size)
+    torch.cuda.synchronize()
+    assert np.array_equal(to_host(d).view(np.uint32), ref)
+    assert np.array_equal(to_host(db).view(np.uint32), ref)
+    rc = [(3 - p[::-1]).astype(np.uint8) for p in pats]
+    rcat, roff, rlens = oracle.pack_patterns(rc)
+    assert np.array_equal(to_host(dr).view(np.uint32), ora.count(rcat, roff, rlens))
+    if n <= 50000:
+        assert np.array_equal(to_host(d1).view(np.uint32), oracle.scan_count_hd1(sym, cat, off, lens))
+    else:
+        d1b = torch.empty(lens.size, dtype=torch.int32, device=cuda)
+        qr.qr_fm_count_approx(fm16, to_dev(cat, cuda), to_dev(lens, cuda), 0, 1, d1b, lens.size)
+        torch.cuda.synchronize()
+        assert np.array_equal(to_host(d1), to_host(d1b))
+    if n >= 1000:
+        L, m = 32, 3000
+        fx = gen.patterns(11, 0, m, L, w, n)
+        dw = torch.empty(m, dtype=torch.int32, device=cuda)
+        work = torch.zeros(2, dtype=torch.uint64, device=cuda)
+        qr.qr_fm_count_work(fm, to_dev(fx, cuda), None, L, dw, m, work)
+        torch.cuda.synchronize()
+        assert np.array_equal(to_host(dw).view(np.uint32),
+                              ora.count(fx, np.arange(m, dtype=np.uint64) * L, np.full(m, L, np.uint32)))
