@@ -269,7 +269,7 @@ def bench_quadrank(ctx, steps, warmup):
             "rank_all4": {"ms": ms4, "gq_s": ctx.world * m / ms4 / 1e6}}
 
 
-def bench_fm(ctx, n, kind, m_total, length, seed, steps, warmup, rank_queries=0):
+def bench_fm(ctx, n, kind, m_total, length, seed, steps, warmup, rank_queries=0, bwt_layout=None):
     import gen
     import paper_2602_04103_b200 as qr
 
@@ -277,7 +277,7 @@ def bench_fm(ctx, n, kind, m_total, length, seed, steps, warmup, rank_queries=0)
     text = torch.empty((n + 31) // 32 + 1, dtype=torch.uint64, device=ctx.dev)
     gen.dna_dev(seed, n, kind, text)
     t0 = time.perf_counter()
-    fm = qr.qr_fm_build(text, n, device=ctx.gpu)
+    fm = qr.qr_fm_build(text, n, device=ctx.gpu, bwt_layout=bwt_layout)
     build_s = time.perf_counter() - t0
     i0, m = shard(m_total, ctx.world, ctx.rank)
     pats = torch.empty(m * length, dtype=torch.uint8, device=ctx.dev)
@@ -539,6 +539,9 @@ def main():
         rows["c3_quadrank"] = bench_quadrank(ctx, K, W)
         rows["c4_quadfm"] = bench_fm(ctx, N4, 0, M4, L4, SEED[4], K, W)
         rows["c5_quadfm"] = bench_fm(ctx, N5, 1, M5, L5, SEED[5], K, W, rank_queries=10**9)
+        # the same searches over the sector-local QuadRank16x2 BWT (B200 variant)
+        rows["c4_quadfm_bwt16x2"] = bench_fm(ctx, N4, 0, M4, L4, SEED[4], K, W, bwt_layout=qr.QR_LAYOUT_QUADRANK16X2)
+        rows["c5_quadfm_bwt16x2"] = bench_fm(ctx, N5, 1, M5, L5, SEED[5], K, W, bwt_layout=qr.QR_LAYOUT_QUADRANK16X2)
         rows["c5_reads_150bp_both_strands"] = bench_reads(ctx, N5, 10**7, 150, 55, K, W)
         # the paper's FM workload at its own scale: a 3.1 Gbp text (block-repeat
         # stand-in for CHM13v2; n+1 < 2^32), 150-bp reads at 1% substitutions, both strands

@@ -289,14 +289,13 @@ __device__ __forceinline__ void x2_locate(uint32_t x, uint32_t last_line, uint32
   j = jj;
 }
 // count of symbol c among the sector's chars between p and its anchor 48, signed by the side
+__device__ __forceinline__ uint64_t x2_range(uint32_t p, int t) {
+  return (prefix_mask((int)p, t) ^ prefix_mask(48, t)) & (t ? 0xffffffffull : ~0ull);
+}
 __device__ __forceinline__ uint32_t x2_rank(const uint64_t (&w)[4], uint32_t p, uint32_t c, uint32_t s) {
-  const uint64_t pat = (uint64_t)c * 0x5555555555555555ull;
-  uint32_t cnt = 0;
-#pragma unroll
-  for (int t = 0; t < 3; ++t) {
-    const uint64_t e = ~(w[1 + t] ^ pat);
-    cnt += __popcll(e & (e >> 1) & 0x5555555555555555ull & (prefix_mask(2 * (int)p, t) ^ prefix_mask(96, t)));
-  }
+  const uint64_t nl = (c & 1u) ? 0ull : ~0ull, nh = (c & 2u) ? 0ull : ~0ull;   // planes (variants.cu)
+  const uint32_t cnt = __popcll((w[1] ^ nl) & (w[2] ^ nh) & x2_range(p, 0)) +
+                       __popcll((w[3] ^ nl) & ((w[3] >> 32) ^ nh) & x2_range(p, 1));
   const uint32_t base = (s << QD_SHIFT) + (uint32_t)((w[0] >> (16 * c)) & 0xffffull);
   return p >= 48 ? base + cnt : base - cnt;
 }
@@ -619,15 +618,10 @@ __device__ __forceinline__ void fm_occ4_x2(const FmParams& F, uint32_t x, uint32
   uint64_t w[4];
   ld_sector(F.lines + 4 * (uint64_t)j + 2 * h, w[0], w[1], w[2], w[3]);
   const uint4 sv = __ldg(reinterpret_cast<const uint4*>(F.super) + (j >> QD_SB_LOG));
-  uint32_t nl = 0, nh = 0, nt = 0;
-#pragma unroll
-  for (int t = 0; t < 3; ++t) {
-    const uint64_t msk = 0x5555555555555555ull & (prefix_mask(2 * (int)p, t) ^ prefix_mask(96, t));
-    const uint64_t l = w[1 + t] & msk, hh = (w[1 + t] >> 1) & msk;
-    nl += __popcll(l);
-    nh += __popcll(hh);
-    nt += __popcll(l & hh);
-  }
+  const uint64_t m0 = x2_range(p, 0), m1 = x2_range(p, 1);
+  const uint64_t l0 = w[1] & m0, h0 = w[2] & m0, l1 = w[3] & m1, h1 = (w[3] >> 32) & m1;
+  const uint32_t nl = __popcll(l0) + __popcll(l1), nh = __popcll(h0) + __popcll(h1);
+  const uint32_t nt = __popcll(l0 & h0) + __popcll(l1 & h1);
   const uint32_t len = p >= 48 ? p - 48u : 48u - p;
   const uint32_t cnt[4] = {len - nl - nh + nt, nl - nt, nh - nt, nt};
   const uint32_t s4[4] = {sv.x, sv.y, sv.z, sv.w};

@@ -646,7 +646,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
 // ------------------------------------------------------------------ QuadRank16x2 (one sector per query)
 // Query (variants.cu: layout): j = q / 192, d = q - 192 j, sector h = [d >= 96], x = d - 96 h;
 // anchor = the sector's char 48; its word 0 holds the four u16 deltas (c at bits 16 c), words
-// 1..3 the 96 chars packed 2 bits each.  rank(q,c) = 2^13 s_{j>>8,c} + d_c +- #c in the chars
+// 1..3 the 96 chars as transposed bit planes (variants.cu).  rank(q,c) = 2^13 s_{j>>8,c} + d_c +- #c in the chars
 // between x and 48 (<= 48 chars); rank_4 from three plane popcounts (A = len - L - H + T).
 __device__ __forceinline__ void q16x2_locate(uint64_t q, uint64_t last_line, uint32_t& j, uint32_t& h, uint32_t& x) {
   uint32_t jj = q < (1ull << 38) ? (uint32_t)(q >> 6) / 3u : (uint32_t)(q / Q16X2_B);   // floor(q/192)
@@ -658,31 +658,25 @@ __device__ __forceinline__ void q16x2_locate(uint64_t q, uint64_t last_line, uin
   j = jj;
 }
 
-// mask of the 2-bit fields of chars between x and 48 (symmetric difference of two prefixes) in data word t
-__device__ __forceinline__ uint64_t q16x2_range(uint32_t x, int t) { return prefix_mask(2 * (int)x, t) ^ prefix_mask(96, t); }
+// mask of the chars between x and 48 (symmetric difference of two prefixes) in plane word t
+// (t = 0: chars 0..63; t = 1: chars 64..95 in the low 32 bits)
+__device__ __forceinline__ uint64_t q16x2_range(uint32_t x, int t) {
+  return (prefix_mask((int)x, t) ^ prefix_mask(48, t)) & (t ? 0xffffffffull : ~0ull);
+}
 
 __device__ __forceinline__ uint64_t q16x2_rank1(const uint64_t (&w)[4], uint32_t x, uint32_t c, uint32_t s) {
-  const uint64_t pat = (uint64_t)c * 0x5555555555555555ull;
-  uint32_t cnt = 0;
-#pragma unroll
-  for (int t = 0; t < 3; ++t) {
-    const uint64_t e = ~(w[1 + t] ^ pat);
-    cnt += __popcll(e & (e >> 1) & 0x5555555555555555ull & q16x2_range(x, t));
-  }
+  const uint64_t nl = (c & 1u) ? 0ull : ~0ull, nh = (c & 2u) ? 0ull : ~0ull;
+  const uint32_t cnt = __popcll((w[1] ^ nl) & (w[2] ^ nh) & q16x2_range(x, 0)) +
+                       __popcll((w[3] ^ nl) & ((w[3] >> 32) ^ nh) & q16x2_range(x, 1));
   const uint64_t base = ((uint64_t)s << QD_SHIFT) + ((w[0] >> (16 * c)) & 0xffffull);
   return x >= 48 ? base + cnt : base - cnt;
 }
 
 __device__ __forceinline__ void q16x2_rank4(const uint64_t (&w)[4], uint32_t x, const uint32_t (&s)[4], uint64_t (&r)[4]) {
-  uint32_t nl = 0, nh = 0, nt = 0;
-#pragma unroll
-  for (int t = 0; t < 3; ++t) {
-    const uint64_t msk = 0x5555555555555555ull & q16x2_range(x, t);
-    const uint64_t l = w[1 + t] & msk, hh = (w[1 + t] >> 1) & msk;
-    nl += __popcll(l);
-    nh += __popcll(hh);
-    nt += __popcll(l & hh);
-  }
+  const uint64_t m0 = q16x2_range(x, 0), m1 = q16x2_range(x, 1);
+  const uint64_t l0 = w[1] & m0, h0 = w[2] & m0, l1 = w[3] & m1, h1 = (w[3] >> 32) & m1;
+  const uint32_t nl = __popcll(l0) + __popcll(l1), nh = __popcll(h0) + __popcll(h1);
+  const uint32_t nt = __popcll(l0 & h0) + __popcll(l1 & h1);
   const uint32_t len = x >= 48 ? x - 48u : 48u - x;
   const uint32_t cnt[4] = {len - nl - nh + nt, nl - nt, nh - nt, nt};
 #pragma unroll

@@ -177,8 +177,9 @@ qr_status birank16x2_build_device(const uint64_t* d_bits, uint64_t n, int device
 // ------------------------------------------------------------------ QuadRank16x2 build
 // QuadRank16x2 (B200 sector-local variant, NEXT §8(f)4, R25; 33.3%): the σ=4 analogue
 // of BiRank16x2.  Each 32-B sector is self-contained except for the superblock words:
-//   sector h of line j = [u16 d_{j,h,c} for c = A, C, G, T | 96 chars packed 2 bits each],
-//   chars 192 j + 96 h .. +96 (text u64 words [6 j + 3 h, +3)),
+//   sector h of line j = [u16 d_{j,h,c} for c = A, C, G, T | 96 chars as transposed bit planes],
+//   chars 192 j + 96 h .. +96 (text u64 words [6 j + 3 h, +3)): word 1 = low bits of chars 0..63,
+//   word 2 = their high bits, word 3 = low bits of chars 64..95 | high bits << 32,
 //   d_{j,h,c} = rank(192 j + 96 h + 48, c) - 2^13 s_{j>>8,c},  s_{i,c} = floor(rank(256 i 192, c)/2^13)
 // (256 lines per superblock as QuadRank16: d <= 255*192 + 144 + 8191 = 57,295 < 2^16).  A query
 // reads ONE sector for rank and for rank_4 and counts at most 48 characters.
@@ -229,8 +230,11 @@ __global__ void k_q16x2_write(const uint64_t* __restrict__ t, uint64_t L, const 
 #pragma unroll
       for (int c = 0; c < 4; ++c)
         d |= (R[(uint64_t)c * L + j] + ((pc >> (8 * c)) & 0xffu) - (sb[c] << QD_SHIFT)) << (16 * c);
-      dst[2 * h] = make_ulonglong2(d, w[3 * h]);
-      dst[2 * h + 1] = make_ulonglong2(w[3 * h + 1], w[3 * h + 2]);
+      const uint64_t a = w[3 * h], b = w[3 * h + 1], c2 = w[3 * h + 2];
+      const uint64_t lo01 = even_bits64(a) | (even_bits64(b) << 32), hi01 = even_bits64(a >> 1) | (even_bits64(b >> 1) << 32);
+      const uint64_t p2 = even_bits64(c2) | (even_bits64(c2 >> 1) << 32);
+      dst[2 * h] = make_ulonglong2(d, lo01);
+      dst[2 * h + 1] = make_ulonglong2(hi01, p2);
     }
   }
 }
@@ -620,13 +624,10 @@ struct RankOne {
       const uint32_t x = (uint32_t)d - 96u * hh;
       ld_sector_na(h.lines + 4 * j + 2 * hh, a[0], a[1], a[2], a[3]);
       const uint32_t s = __ldg(h.super + 4 * (j >> QD_SB_LOG) + (c & 3u));
-      const uint64_t pat = (uint64_t)(c & 3u) * 0x5555555555555555ull;
-      uint32_t cnt = 0;
-#pragma unroll
-      for (int t = 0; t < 3; ++t) {
-        const uint64_t e = ~(a[1 + t] ^ pat);
-        cnt += __popcll(e & (e >> 1) & 0x5555555555555555ull & (prefix_mask(2 * (int)x, t) ^ prefix_mask(96, t)));
-      }
+      const uint64_t nl = (c & 1u) ? 0ull : ~0ull, nh = (c & 2u) ? 0ull : ~0ull;
+      const uint32_t cnt = __popcll((a[1] ^ nl) & (a[2] ^ nh) & (prefix_mask((int)x, 0) ^ prefix_mask(48, 0))) +
+                           __popcll((a[3] ^ nl) & ((a[3] >> 32) ^ nh) & (prefix_mask((int)x, 1) ^ prefix_mask(48, 1)) &
+                                    0xffffffffull);
       const uint64_t base = ((uint64_t)s << QD_SHIFT) + ((a[0] >> (16 * (c & 3u))) & 0xffffull);
       return x >= 48 ? base + cnt : base - cnt;
     }

@@ -317,7 +317,8 @@ def test_quadrank16x2_parity(cuda, n, kind):
 
 def test_quadrank16x2_layout_closed_forms(cuda):
     """Decode every sector: d_{j,h,c} + 2^13 s_{j>>8,c} = rank(192 j + 96 h + 48, c), s_{i,c} =
-    rank(256 i 192, c) >> 13, data = text words [6j + 3h, +3); 33.3% overhead (+ superblocks)."""
+    rank(256 i 192, c) >> 13, data = the bit planes of text chars 192 j + 96 h .. +96 (low / high
+    planes of chars 0..63 in words 1 / 2, both planes of chars 64..95 in word 3)."""
     for n in (11 * 256 * 192 + 999, 2 * 256 * 192 + 5):
         w = gen.dna(91, n)
         h = qr.qr_build(w, n, qr.QR_LAYOUT_QUADRANK16X2)
@@ -337,7 +338,13 @@ def test_quadrank16x2_layout_closed_forms(cuda):
                 assert np.array_equal(full, want), (hh, c)
         text = np.zeros(6 * L, np.uint64)
         text[: min(w.size, 6 * L)] = w[: 6 * L]
-        assert np.array_equal(u64[:, :, 1:].reshape(-1), text)
+        chars = gen.unpack_dna(text, 192 * L).reshape(L, 2, 96).astype(np.uint64)
+        bitpos = np.uint64(1) << np.arange(64, dtype=np.uint64)
+        lo = ((chars & 1)[..., :64] * bitpos).sum(axis=-1, dtype=np.uint64)
+        hi = ((chars >> 1)[..., :64] * bitpos).sum(axis=-1, dtype=np.uint64)
+        p2 = ((chars & 1)[..., 64:] * bitpos[:32]).sum(axis=-1, dtype=np.uint64) | \
+            (((chars >> 1)[..., 64:] * bitpos[:32]).sum(axis=-1, dtype=np.uint64) << np.uint64(32))
+        assert np.array_equal(u64[:, :, 1], lo) and np.array_equal(u64[:, :, 2], hi) and np.array_equal(u64[:, :, 3], p2)
 
 
 @pytest.mark.parametrize("src", ["table", "global", "cluster"])
