@@ -1,5 +1,6 @@
 """One launch of each hot kernel at the bench's configs and default launch configuration, for
 ncu --set full captures (kernel order: bi_rank2c (BiRank16 rank, cluster shared-memory superblocks),
+BiRank16x2 / QuadRank16x2 rank (cluster kernels) after the QuadRank64 rank,
 bi_gather2 x3 (ceiling modes 0-2), bi_rank2c<VAR=3> (ceiling mode 3), qd_rank2c, qd_all4_2c, b64_rank,
 q64_rank, fm_count (c4, lean), fm_count (c5, de-duplicating), fm_count both strands, fm_approx1)."""
 import os
@@ -28,6 +29,7 @@ for mode in (0, 1, 2, 3):
 torch.cuda.synchronize()
 h.free()
 hb = qr.qr_build(bits, n, qr.QR_LAYOUT_BIRANK64X2)
+hb16 = qr.qr_build(bits, n, qr.QR_LAYOUT_BIRANK16X2)
 del bits
 n4 = 1 << 32
 t = torch.empty((n4 + 31) // 32, dtype=torch.uint64, device=dev)
@@ -42,13 +44,16 @@ torch.cuda.synchronize()
 h.free()
 del o4
 hq = qr.qr_build(t, n4, qr.QR_LAYOUT_QUADRANK64)
+hq16 = qr.qr_build(t, n4, qr.QR_LAYOUT_QUADRANK16X2)
 del t
 qb = torch.empty(M, dtype=torch.uint64, device=dev)
 gen.queries_dev(2, n, M, qb)
 qr.qr_rank(hb, qb, None, out, M, st)
 qr.qr_rank(hq, q, c, out, M, st)
+qr.qr_rank(hb16, qb, None, out, M, st)
+qr.qr_rank(hq16, q, c, out, M, st)
 torch.cuda.synchronize()
-hb.free(); hq.free()
+hb.free(); hq.free(); hb16.free(); hq16.free()
 del q, c, qb, out
 n = 1 << 26
 t = torch.empty((n + 31) // 32 + 1, dtype=torch.uint64, device=dev)
