@@ -32,7 +32,6 @@ int g_rank_dyn = 1;             // cluster rank kernels: 1 = dynamic (atomic chu
 int g_rank_smem_clusters = 0;   // cluster rank kernels: 0 = as many 2-CTA clusters as fit (occupancy API), else this many
 int g_rank_smem_threads = 0;    // cluster rank kernels: CTA size (0 auto: 1024, 768 for K = 6, 512 for K = 8)
 int g_rank_smem_k = 0;          // cluster rank kernels: queries per lane pair per group (0 auto, 1, 2, 4 @1024 thr, 6 @768, 8 @512)
-int g_rank_lane_k = 0;          // one-lane table kernels: queries per lane (0 auto by batch size, 2, 4, 8)
 int g_rank_lane_table = 1;      // one-lane kernels take the superblock words from a per-CTA shared-memory table when small
 int g_rank_pair = 2;            // kernel shape: 2 by structure size (default), 1 lane pairs (one L2 request per query), 0 one lane per query
 uint64_t g_stage_chunk = 1ull << 23;   // queries per chunk on the staged host path (sweep: profiles/r01_e2e_sweep)
@@ -328,9 +327,6 @@ QR_EXPORT qr_status qr_set_tuning(const char* key, int64_t value) {
   } else if (!strcmp(key, "rank_smem_clusters")) {
     if (value < 0 || value > 4096) return fail(QR_EINVAL, "rank_smem_clusters must be 0..4096");
     g_rank_smem_clusters = (int)value;
-  } else if (!strcmp(key, "rank_lane_k")) {
-    if (value != 0 && value != 2 && value != 4 && value != 8) return fail(QR_EINVAL, "rank_lane_k must be 0, 2, 4 or 8");
-    g_rank_lane_k = (int)value;
   } else if (!strcmp(key, "rank_lane_table")) {
     if (value != 0 && value != 1) return fail(QR_EINVAL, "rank_lane_table must be 0 or 1");
     g_rank_lane_table = (int)value;

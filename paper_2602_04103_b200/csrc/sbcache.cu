@@ -394,7 +394,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
 // always, sector 1 for queries right of the anchor (the L1 merges both into one L2 request).
 constexpr uint64_t LANE_TABLE_MAX = 32 * 1024;
 extern int g_rank_blocks_per_sm;
-extern int g_rank_lane_k;
 
 __device__ __forceinline__ void lane_preload(const uint64_t* __restrict__ pack, uint32_t words, uint64_t* smem) {
   const uint4* src = reinterpret_cast<const uint4*>(pack);
@@ -917,13 +916,15 @@ static void sc_launch_kt(const qr_index* h, const uint64_t* q, const uint8_t* c,
 
 // One-lane kernels with the per-CTA table (rank_shape LANE).  Returns cudaErrorNotSupported when
 // the handle has no table small enough (the caller then uses the global-memory lane kernels).
-template <int K>
-static cudaError_t lane_table_k(const qr_index* h, const uint64_t* q, const uint8_t* c, uint64_t* out, uint64_t m,
-                                int what, cudaStream_t st) {
+cudaError_t launch_lane_table_rank(const qr_index* h, const uint64_t* q, const uint8_t* c, uint64_t* out, uint64_t m,
+                                   int what, cudaStream_t st) {
+  if (!h->spack || g_index64) return cudaErrorNotSupported;
   const uint64_t total = 2 * super_pack_cta_bytes(h);
+  if (total > LANE_TABLE_MAX) return cudaErrorNotSupported;
   const uint32_t words = (uint32_t)(total / 8), half = (uint32_t)h->spack_half;
   const uint64_t last = h->n_lines - 1;
   const bool dyn = use_dyn_order(m);
+  constexpr int K = 2;
   const unsigned g = grid_stride_blocks((m + K - 1) / K, 256, h->sm_count, g_rank_blocks_per_sm);
   const uint4* L = h->lines;
   const uint64_t* P = h->spack;
@@ -937,21 +938,6 @@ static cudaError_t lane_table_k(const qr_index* h, const uint64_t* q, const uint
   }
   if (what == 0) return go(k_qd_rank1s<K, 0, false>, k_qd_rank1s<K, 0, true>, c);
   return go(k_qd_rank1s<K, 1, false>, k_qd_rank1s<K, 1, true>, nullptr);
-}
-
-cudaError_t launch_lane_table_rank(const qr_index* h, const uint64_t* q, const uint8_t* c, uint64_t* out, uint64_t m,
-                                   int what, cudaStream_t st) {
-  if (!h->spack || g_index64) return cudaErrorNotSupported;
-  if (2 * super_pack_cta_bytes(h) > LANE_TABLE_MAX) return cudaErrorNotSupported;
-  // K: queries in flight per lane.  Large batches: 2 (occupancy); small ones (< 2^22): auto picks
-  // the K that puts the whole batch in flight in about one wave (knob "rank_lane_k").
-  int k = g_rank_lane_k;
-  if (k == 0) k = m >= (1ull << 22) ? 2 : m >= (1ull << 20) ? 4 : 2;
-  switch (k) {
-    case 4: return lane_table_k<4>(h, q, c, out, m, what, st);
-    case 8: return lane_table_k<8>(h, q, c, out, m, what, st);
-    default: return lane_table_k<2>(h, q, c, out, m, what, st);
-  }
 }
 
 // what: 0 = rank (sigma 2 or 4), 1 = rank_4 (sigma 4), 3 = BiRank gather ceiling of this kernel shape
