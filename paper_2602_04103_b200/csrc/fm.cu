@@ -842,7 +842,7 @@ static void launch_fm2(int sms_mode, unsigned g, size_t smem, cudaStream_t st, c
 extern int g_fm_dyn;
 extern int g_fm_seed;
 
-// Keep up to 8 GiB of freed stream-ordered allocations in the device's default pool (its default
+// Keep up to 2 GiB of freed stream-ordered allocations in the device's default pool (its default
 // release threshold of 0 returns them to the driver at every synchronisation, so a per-call
 // scratch buffer would be re-mapped on every call).
 static void keep_pool_memory(int device, cudaStream_t st) {
@@ -857,7 +857,7 @@ static void keep_pool_memory(int device, cudaStream_t st) {
   if (device < 0 || device >= 64 || done[device]) return;
   cudaMemPool_t pool;
   if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
-    uint64_t thr = 8ull << 30;
+    uint64_t thr = 2ull << 30;
     cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
   }
   cudaGetLastError();
