@@ -422,13 +422,13 @@ QR_EXPORT qr_status qr_build(const uint64_t* text, uint64_t n, int layout, int d
   if (!out || (!text && n)) return fail(QR_EINVAL, "qr_build: null pointer");
   *out = nullptr;
   if (n >= (1ull << 48)) return fail(QR_ECAPACITY, "qr_build: n >= 2^48");
+  const bool b16x2 = layout == QR_LAYOUT_BIRANK16X2, q16x2 = layout == QR_LAYOUT_QUADRANK16X2;
+  if (b16x2 && n >= (1ull << 40)) return fail(QR_ECAPACITY, "qr_build: BiRank16x2 needs n < 2^40 (u32 line index)");
+  if (q16x2 && n >= (1ull << 39)) return fail(QR_ECAPACITY, "qr_build: QuadRank16x2 needs n < 2^39 (u32 line index)");
   DeviceGuard dg(device);
   if (!dg.ok) return fail(QR_EINVAL, "qr_build: bad device %d", device);
   cudaStream_t st = (cudaStream_t)stream;
   const bool bits = layout == QR_LAYOUT_BIRANK64X2 || layout == QR_LAYOUT_BIRANK16X2;
-  const bool b16x2 = layout == QR_LAYOUT_BIRANK16X2, q16x2 = layout == QR_LAYOUT_QUADRANK16X2;
-  if (b16x2 && n >= (1ull << 40)) return fail(QR_ECAPACITY, "qr_build: BiRank16x2 needs n < 2^40 (u32 line index)");
-  if (q16x2 && n >= (1ull << 39)) return fail(QR_ECAPACITY, "qr_build: QuadRank16x2 needs n < 2^39 (u32 line index)");
   const uint64_t L = b16x2 ? n / B16X2_B + 1 : q16x2 ? n / Q16X2_B + 1 : bits ? n / 384 + 1 : n / 128 + 1;
   const uint64_t words = bits ? (n + 63) >> 6 : (n + 31) >> 5;
   uint64_t padded = b16x2 ? (60 * L + 7) / 8 + 1 : q16x2 ? 6 * L : bits ? 6 * L : 4 * L;

@@ -61,6 +61,11 @@ def test_argument_validation_without_gpu():
     assert L.qr_fm_build(C.c_void_p(8), (1 << 32) - 1, None, 0, None, C.byref(out)) == qr.QR_ECAPACITY
     assert L.qr_fm_build(C.c_void_p(8), 0, None, 0, None, C.byref(out)) == qr.QR_EINVAL
     assert L.qr_birank_build(None, 10, 0, None, C.byref(out)) == qr.QR_EINVAL
+    assert L.qr_build(C.c_void_p(8), 1 << 40, qr.QR_LAYOUT_BIRANK16X2, 0, None, C.byref(out)) == qr.QR_ECAPACITY
+    assert L.qr_build(C.c_void_p(8), 1 << 39, qr.QR_LAYOUT_QUADRANK16X2, 0, None, C.byref(out)) == qr.QR_ECAPACITY
+    assert L.qr_build(C.c_void_p(8), 10, 7, 0, None, C.byref(out)) == qr.QR_EINVAL          # unknown layout
+    assert L.qr_fm_build_opts(C.c_void_p(8), 10, None, 8, qr.QR_LAYOUT_BIRANK16, 0, None, C.byref(out)) == qr.QR_EINVAL
+    assert L.qr_fm_build_opts(C.c_void_p(8), 10, None, 15, qr.QR_LAYOUT_QUADRANK16, 0, None, C.byref(out)) == qr.QR_EINVAL
     assert L.qr_set_tuning(b"rank_k", 3) == qr.QR_EINVAL
     assert L.qr_set_tuning(b"nope", 1) == qr.QR_EINVAL
     assert L.qr_set_tuning(b"rank_k", 4) == qr.QR_OK
