@@ -55,7 +55,7 @@ class Clocks:
 
     FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
+              "clocks_event_reasons.sw_power_cap,temperature.gpu,temperature.memory,clocks.mem,serial")
 
     def __init__(self, gpu_index: int):
         self.idx = gpu_index
@@ -78,7 +78,7 @@ class Clocks:
         time.sleep(0.25)
         self.proc.terminate()
         self.proc.wait()
-        sm, mx, reasons = [], None, set()
+        sm, mx, reasons, tg, tm, mem, serial = [], None, set(), [], [], [], None
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for line in open(self.path):
             p = [x.strip() for x in line.split(",")]
@@ -92,9 +92,17 @@ class Clocks:
             for k, name in enumerate(names):
                 if p[5 + k].lower().startswith("active"):
                     reasons.add(name)
+            for lst, k in ((tg, 9), (tm, 10), (mem, 11)):       # GPU / HBM temperature, memory clock
+                try:
+                    lst.append(float(p[k]))
+                except (ValueError, IndexError):
+                    pass
+            if len(p) > 12:
+                serial = p[12]
         os.unlink(self.path)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+        med = lambda v: statistics.median(v) if v else None   # noqa: E731
+        return {"sm_mhz": med(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm),
+                "gpu_temp_c": med(tg), "hbm_temp_c": med(tm), "mem_mhz": med(mem), "gpu_serial": serial}
 
 
 class Ctx:
@@ -152,15 +160,17 @@ class Ctx:
         torch.cuda.synchronize()
         if clocks:
             clocks.start()
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(self.stream)
-        for _ in range(steps):
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
+        ev[0].record(self.stream)
+        for i in range(steps):
             fn()
-        e1.record(self.stream)
+            ev[i + 1].record(self.stream)
         torch.cuda.synchronize()
         self.barrier()
-        ms = e0.elapsed_time(e1) / steps
+        ms = ev[0].elapsed_time(ev[-1]) / steps
+        # per-step times (median and minimum beside the mean), kept for the caller
+        per = sorted(ev[i].elapsed_time(ev[i + 1]) for i in range(steps))
+        self.last_step_ms = {"median": self.max_over_ranks(per[len(per) // 2]), "min": self.max_over_ranks(per[0])}
         return self.max_over_ranks(ms)
 
 
@@ -197,7 +207,8 @@ def bench_birank(ctx, p: float, steps, warmup, with_ceiling: bool, clocks=None, 
     torch.cuda.synchronize()
     ms = ctx.timed(lambda: qr.qr_rank(h, q, None, out, m, ctx.stream), steps, warmup, clocks)
     clk = clocks.stop() if clocks else None
-    res = {"ms": ms, "m_per_gpu": m, "gq_s": ctx.world * m / ms / 1e6, "launches": steps, "clocks": clk}
+    res = {"ms": ms, "m_per_gpu": m, "gq_s": ctx.world * m / ms / 1e6, "launches": steps, "clocks": clk,
+           "step_ms": dict(ctx.last_step_ms)}
     res["smem_cache_cta_bytes"] = qr.qr_super_cache_bytes(h)
     if with_ceiling:
         # modes 0-2: the global-memory lane-pair kernel's loads (lines only, full lines, lines +
@@ -582,7 +593,9 @@ def main():
     ceil0 = max(c2[k]["gq_s"] for k in ("ceiling_mode0", "ceiling_mode3") if k in c2)
     line = {
         "metric": METRIC, "value": round(value, 4), "unit": "Gqueries/s", "n_gpus": ctx.world, "steps": K,
-        "warmup": W, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "warmup": W, "ms_per_step": round(ms, 4),
+        "ms_per_step_median": round(c2["step_ms"]["median"], 4), "ms_per_step_min": round(c2["step_ms"]["min"], 4),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "u64", "data": "synthetic (seeded counter-based generators, gen/qrgen.h)",
         "config": workload_config(ctx.world),
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
