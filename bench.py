@@ -389,7 +389,8 @@ def bench_variants(ctx, steps, warmup):
     q = torch.empty(M2, dtype=torch.uint64, device=ctx.dev)
     gen.queries_dev(SEED[2], N2, M2, q, i0=ctx.rank * M2)
     out = torch.empty_like(q)
-    for key, layout in (("c2_birank64x2", qr.QR_LAYOUT_BIRANK64X2), ("c2_birank16x2", qr.QR_LAYOUT_BIRANK16X2)):
+    for key, layout in (("c2_birank64x2", qr.QR_LAYOUT_BIRANK64X2), ("c2_birank16x2", qr.QR_LAYOUT_BIRANK16X2),
+                        ("c2_birank32x2", qr.QR_LAYOUT_BIRANK32X2)):
         h = qr.qr_build(bits, N2, layout, device=ctx.gpu)
         ms = ctx.timed(lambda: qr.qr_rank(h, q, None, out, M2, ctx.stream), steps, warmup)
         res[key] = {"ms": ms, "gq_s": ctx.world * M2 / ms / 1e6, "bytes": h.line_bytes + h.super_bytes,

@@ -57,7 +57,10 @@ typedef struct qr_index qr_index;   /* a rank layout (QR_LAYOUT_*)              
  * BiRank16x2 (6.72%: each 32-B sector = u16 delta to its middle + 240 data
  * bits, superblocks as BiRank16, so a query reads one sector and the superblock word), and
  * QuadRank16x2 (B200 sector-local σ=4 variant, 33.3%: each 32-B sector = four u16 deltas to its
- * middle + 96 packed characters, superblocks as QuadRank16; rank and rank_4 read one sector).
+ * middle + 96 characters as bit planes, superblocks as QuadRank16; rank and rank_4 read one
+ * sector) and BiRank32x2 (14.3%: each 32-B sector = u32 delta to its middle +
+ * 224 data bits, a u64 L1 entry per 2^23 lines — small enough to sit in every CTA's shared
+ * memory for any n, so a query reads one sector and nothing else).
  * All layouts answer every query identically. */
 #define QR_LAYOUT_BIRANK16    1
 #define QR_LAYOUT_BIRANK64X2  2
@@ -65,6 +68,7 @@ typedef struct qr_index qr_index;   /* a rank layout (QR_LAYOUT_*)              
 #define QR_LAYOUT_QUADRANK64  4
 #define QR_LAYOUT_BIRANK16X2  5
 #define QR_LAYOUT_QUADRANK16X2 6
+#define QR_LAYOUT_BIRANK32X2  7
 typedef struct qr_fm qr_fm;         /* QuadFm: QuadRank over the BWT + C + spos + 8-mer table */
 
 /* ------------------------------------------------------------------ build */

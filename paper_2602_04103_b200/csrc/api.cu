@@ -109,6 +109,7 @@ qr_status alloc_index(int sigma, uint64_t n, int device, qr_index** out, int lay
     case QR_LAYOUT_QUADRANK16: B = QD_B; sb = QD_SB_LOG; break;
     case QR_LAYOUT_BIRANK64X2: B = 384; break;      // 2 x 192 data bits per line
     case QR_LAYOUT_BIRANK16X2: B = B16X2_B; sb = BI_SB_LOG; break;   // 2 x 240 data bits, BiRank16 superblocks
+    case QR_LAYOUT_BIRANK32X2: B = B32X2_B; sb = B32X2_SB_LOG; break; // 2 x 224 data bits, u64 L1 per 2^23 lines
     case QR_LAYOUT_QUADRANK16X2: B = Q16X2_B; sb = QD_SB_LOG; break; // 2 x 96 chars, QuadRank16 superblocks
     default: B = 128; break;                        // QuadRank64: 128 chars per line
   }
@@ -125,7 +126,9 @@ qr_status alloc_index(int sigma, uint64_t n, int device, qr_index** out, int lay
   return QR_OK;
 }
 
-uint64_t super_bytes_of(const qr_index* h) { return h->n_super * (h->sigma == 2 ? 4 : 16); }
+uint64_t super_bytes_of(const qr_index* h) {
+  return h->n_super * (h->layout == QR_LAYOUT_BIRANK32X2 ? 8 : h->sigma == 2 ? 4 : 16);
+}
 
 qr_status fm_build_device(const uint64_t* d_text, uint64_t n, const uint32_t* d_sa_given, int device, cudaStream_t st,
                           qr_fm** out, int kmer_k, int bwt_layout);
@@ -137,13 +140,14 @@ cudaError_t launch_qd_gather(const qr_index* h, const uint64_t* q, uint64_t* out
 cudaError_t launch_gather(const qr_index* h, const uint64_t* q, uint64_t* out, uint64_t m, int mode, cudaStream_t st) {
   if (h->layout == QR_LAYOUT_BIRANK16X2) return launch_b16x2_rank(h, q, nullptr, out, m, 2, st);   // same sector loads
   if (h->layout == QR_LAYOUT_QUADRANK16X2) return launch_q16x2_rank(h, q, nullptr, out, m, 2, st);
+  if (h->layout == QR_LAYOUT_BIRANK32X2) return launch_b32x2_rank(h, q, nullptr, out, m, 2, st);
   if (h->layout == QR_LAYOUT_BIRANK64X2 || h->layout == QR_LAYOUT_QUADRANK64)
     return launch_variant(h, q, nullptr, out, m, 2, st);   // the variants' loads (modes coincide)
   return h->sigma == 2 ? launch_bi_gather(h, q, out, m, mode, st) : launch_qd_gather(h, q, out, m, mode, st);
 }
 static bool is_variant(const qr_index* h) {
   return h->layout == QR_LAYOUT_BIRANK64X2 || h->layout == QR_LAYOUT_QUADRANK64 || h->layout == QR_LAYOUT_BIRANK16X2 ||
-         h->layout == QR_LAYOUT_QUADRANK16X2;
+         h->layout == QR_LAYOUT_QUADRANK16X2 || h->layout == QR_LAYOUT_BIRANK32X2;
 }
 
 // RAII device guard
@@ -417,21 +421,24 @@ QR_EXPORT qr_status qr_build(const uint64_t* text, uint64_t n, int layout, int d
   if (layout == QR_LAYOUT_BIRANK16) return qr_birank_build(text, n, device, stream, out);
   if (layout == QR_LAYOUT_QUADRANK16) return qr_quadrank_build(text, n, device, stream, out);
   if (layout != QR_LAYOUT_BIRANK64X2 && layout != QR_LAYOUT_QUADRANK64 && layout != QR_LAYOUT_BIRANK16X2 &&
-      layout != QR_LAYOUT_QUADRANK16X2)
+      layout != QR_LAYOUT_QUADRANK16X2 && layout != QR_LAYOUT_BIRANK32X2)
     return fail(QR_EINVAL, "qr_build: bad layout %d", layout);
   if (!out || (!text && n)) return fail(QR_EINVAL, "qr_build: null pointer");
   *out = nullptr;
   if (n >= (1ull << 48)) return fail(QR_ECAPACITY, "qr_build: n >= 2^48");
   const bool b16x2 = layout == QR_LAYOUT_BIRANK16X2, q16x2 = layout == QR_LAYOUT_QUADRANK16X2;
+  const bool b32x2 = layout == QR_LAYOUT_BIRANK32X2;
+  if (b32x2 && n >= BI_MAX_N) return fail(QR_ECAPACITY, "qr_build: BiRank32x2 needs n < 2^43");
   if (b16x2 && n >= (1ull << 40)) return fail(QR_ECAPACITY, "qr_build: BiRank16x2 needs n < 2^40 (u32 line index)");
   if (q16x2 && n >= (1ull << 39)) return fail(QR_ECAPACITY, "qr_build: QuadRank16x2 needs n < 2^39 (u32 line index)");
   DeviceGuard dg(device);
   if (!dg.ok) return fail(QR_EINVAL, "qr_build: bad device %d", device);
   cudaStream_t st = (cudaStream_t)stream;
-  const bool bits = layout == QR_LAYOUT_BIRANK64X2 || layout == QR_LAYOUT_BIRANK16X2;
-  const uint64_t L = b16x2 ? n / B16X2_B + 1 : q16x2 ? n / Q16X2_B + 1 : bits ? n / 384 + 1 : n / 128 + 1;
+  const bool bits = layout == QR_LAYOUT_BIRANK64X2 || layout == QR_LAYOUT_BIRANK16X2 || b32x2;
+  const uint64_t L = b16x2 ? n / B16X2_B + 1 : b32x2 ? n / B32X2_B + 1 : q16x2 ? n / Q16X2_B + 1
+                   : bits ? n / 384 + 1 : n / 128 + 1;
   const uint64_t words = bits ? (n + 63) >> 6 : (n + 31) >> 5;
-  uint64_t padded = b16x2 ? (60 * L + 7) / 8 + 1 : q16x2 ? 6 * L : bits ? 6 * L : 4 * L;
+  uint64_t padded = b16x2 ? (60 * L + 7) / 8 + 1 : b32x2 ? 7 * L + 1 : q16x2 ? 6 * L : bits ? 6 * L : 4 * L;
   if (padded < words) padded = words;
   uint64_t* d = nullptr;
   qr_status s = stage_input(text, words, padded, st, &d);
@@ -439,6 +446,7 @@ QR_EXPORT qr_status qr_build(const uint64_t* text, uint64_t n, int layout, int d
   if (bits) k_mask_tail_bits<<<1, 1, 0, st>>>(d, n);
   else      k_mask_tail_chars<<<1, 1, 0, st>>>(d, n);
   s = b16x2 ? birank16x2_build_device(d, n, device, st, out)
+      : b32x2 ? birank32x2_build_device(d, n, device, st, out)
       : q16x2 ? quadrank16x2_build_device(d, n, device, st, out)
       : bits ? birank64x2_build_device(d, n, device, st, out) : quadrank64_build_device(d, n, device, st, out);
   cudaFreeAsync(d, st);
@@ -691,10 +699,11 @@ QR_EXPORT qr_status qr_import_layout(const void* lines, const void* super, uint6
                                      void* stream, qr_index** out) {
   if (!out || !lines) return fail(QR_EINVAL, "qr_import_layout: null pointer");
   *out = nullptr;
-  if (layout < QR_LAYOUT_BIRANK16 || layout > QR_LAYOUT_QUADRANK16X2) return fail(QR_EINVAL, "qr_import_layout: bad layout");
+  if (layout < QR_LAYOUT_BIRANK16 || layout > QR_LAYOUT_BIRANK32X2) return fail(QR_EINVAL, "qr_import_layout: bad layout");
   DeviceGuard dg(device);
   if (!dg.ok) return fail(QR_EINVAL, "qr_import_layout: bad device %d", device);
-  const int sigma = (layout == QR_LAYOUT_BIRANK16 || layout == QR_LAYOUT_BIRANK64X2 || layout == QR_LAYOUT_BIRANK16X2) ? 2 : 4;
+  const int sigma = (layout == QR_LAYOUT_BIRANK16 || layout == QR_LAYOUT_BIRANK64X2 || layout == QR_LAYOUT_BIRANK16X2 ||
+                     layout == QR_LAYOUT_BIRANK32X2) ? 2 : 4;
   qr_index* h = nullptr;
   qr_status s = alloc_index(sigma, n, device, &h, layout);
   if (s != QR_OK) return s;

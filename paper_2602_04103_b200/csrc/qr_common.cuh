@@ -14,6 +14,8 @@ constexpr uint32_t BI_SHIFT = 11;       // s_i = floor(rank(iS)/2^11), PAPER.md:
 constexpr uint32_t BI_ANCHOR = 240;     // b_j to data bit 240 = line bit 256
 constexpr uint64_t BI_MAX_N = 1ull << 43;
 constexpr uint64_t Q16X2_B = 192;       // QuadRank16x2: 2 sectors x 96 chars (B200 sector-local variant)
+constexpr uint64_t B32X2_B = 448;       // BiRank32x2: 2 sectors x 224 data bits
+constexpr uint32_t B32X2_SB_LOG = 23;   // 2^23 lines per L1 entry: deltas < 2^23 * 448 + 336 < 2^32
 constexpr uint64_t B16X2_B = 480;       // BiRank16x2: 2 sectors x 240 data bits
 
 // ---- QuadRank16 geometry (§4, Listing 1) ----
@@ -72,6 +74,9 @@ uint64_t super_bytes_of(const qr_index* h);
 qr_status birank64x2_build_device(const uint64_t* d_bits, uint64_t n, int device, cudaStream_t st, qr_index** out);
 qr_status birank16x2_build_device(const uint64_t* d_bits, uint64_t n, int device, cudaStream_t st, qr_index** out);
 cudaError_t launch_b16x2_rank(const qr_index* h, const uint64_t* q, const uint8_t* c, uint64_t* out, uint64_t m,
+                              int what, cudaStream_t st);
+qr_status birank32x2_build_device(const uint64_t* d_bits, uint64_t n, int device, cudaStream_t st, qr_index** out);
+cudaError_t launch_b32x2_rank(const qr_index* h, const uint64_t* q, const uint8_t* c, uint64_t* out, uint64_t m,
                               int what, cudaStream_t st);
 qr_status quadrank16x2_build_device(const uint64_t* d_text, uint64_t n, int device, cudaStream_t st, qr_index** out);
 cudaError_t launch_q16x2_rank(const qr_index* h, const uint64_t* q, const uint8_t* c, uint64_t* out, uint64_t m,

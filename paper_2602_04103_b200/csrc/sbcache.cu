@@ -643,6 +643,63 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   cluster_barrier();
 }
 
+// ------------------------------------------------------------------ BiRank32x2 (one sector per query)
+// Query: j = q / 448, d = q - 448 j, sector h = [d >= 224], x = d - 224 h; the sector's u32 delta
+// is relative to L1[j >> 23], its anchor is data bit 112 = sector bit 144:
+// rank = L1 + delta +- popc(sector bits between 32 + x and 144).  The whole L1 array is copied
+// into each CTA's shared memory (<= 18.7 KB for any n < 2^43), so a query's only global load is
+// its sector.  MODE 1: gather ceiling (same load).
+template <int K, int MODE, bool HAS_C, bool DYN>
+__global__ void __launch_bounds__(256) k_b32x2_rank(const uint4* __restrict__ lines, const uint64_t* __restrict__ l1,
+                                                    uint32_t l1_words, const uint64_t* __restrict__ q,
+                                                    const uint8_t* __restrict__ cs, uint64_t* __restrict__ out, uint64_t m,
+                                                    uint64_t last_line, unsigned long long* ctr) {
+  extern __shared__ uint64_t lt_smem[];
+  for (uint32_t i = threadIdx.x; i < l1_words; i += blockDim.x) lt_smem[i] = __ldg(l1 + i);
+  __syncthreads();
+  const uint32_t u = sc_unit_in_warp<32>();
+  ScSched sc = sc_first<K, DYN, 32>(ctr);
+  uint64_t qn[K];
+  sc_load_q<K>(q, sc.gb + u, sc.stride, m, qn);
+  while (sc.gb < m) {
+    const uint64_t i0 = sc.gb + u, stride = sc.stride;
+    uint64_t qq[K], w[K][4], base[K];
+    uint32_t xx[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      qq[k] = qn[k];
+      uint64_t j = qq[k] < (1ull << 37) ? (uint64_t)((uint32_t)(qq[k] >> 6) / 7u) : qq[k] / B32X2_B;   // floor(q/448)
+      j = j > last_line ? last_line : j;
+      uint64_t d = qq[k] - j * B32X2_B;
+      d = d > B32X2_B - 1 ? B32X2_B - 1 : d;
+      const uint32_t h = d >= 224 ? 1u : 0u;
+      xx[k] = (uint32_t)d - 224u * h;
+      ld_sector_na(lines + 4 * j + 2 * h, w[k][0], w[k][1], w[k][2], w[k][3]);
+      base[k] = MODE == 1 ? 0ull : lt_smem[j >> B32X2_SB_LOG];
+    }
+    sc = sc_next<K, DYN, 32>(sc, ctr);
+    sc_load_q<K>(q, sc.gb + u, sc.stride, m, qn);
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const uint64_t idx = i0 + (uint64_t)k * stride;
+      uint64_t r;
+      if (MODE == 1) {
+        r = w[k][0] ^ w[k][1] ^ w[k][2] ^ w[k][3];
+      } else {
+        uint32_t cnt = 0;
+#pragma unroll
+        for (int t = 0; t < 4; ++t) cnt += __popcll(w[k][t] & (prefix_mask(32 + (int)xx[k], t) ^ prefix_mask(144, t)));
+        const uint64_t b = base[k] + (w[k][0] & 0xffffffffull);
+        r = xx[k] >= 112 ? b + cnt : b - cnt;
+        if (HAS_C) {
+          if (idx < m && cs[idx] == 0) r = qq[k] - r;
+        }
+      }
+      if (idx < m) st_stream_u64(out + idx, r);
+    }
+  }
+}
+
 // ------------------------------------------------------------------ QuadRank16x2 (one sector per query)
 // Query (variants.cu: layout): j = q / 192, d = q - 192 j, sector h = [d >= 96], x = d - 96 h;
 // anchor = the sector's char 48; its word 0 holds the four u16 deltas (c at bits 16 c), words
@@ -1078,6 +1135,29 @@ cudaError_t launch_q16x2_rank(const qr_index* h, const uint64_t* q, const uint8_
                           L, S, h->spack, 0u, 0u, q, c, out, m, last);
   return launch_ordered(k_q16x2_rank<K, 0, 1, false>, k_q16x2_rank<K, 0, 1, true>, dyn, h->device, h->sm_count, g, st,
                         L, S, h->spack, 0u, 0u, q, c, out, m, last);
+}
+
+
+// BiRank32x2 dispatch (what: 0 rank, 2 gather ceiling).
+cudaError_t launch_b32x2_rank(const qr_index* h, const uint64_t* q, const uint8_t* c, uint64_t* out, uint64_t m,
+                              int what, cudaStream_t st) {
+  if (m == 0) return cudaSuccess;
+  constexpr int K = 4;
+  const uint64_t last = h->n_lines - 1;
+  const bool dyn = use_dyn_order(m);
+  const unsigned g = grid_stride_blocks((m + K - 1) / K, 256, h->sm_count, g_rank_blocks_per_sm);
+  const uint4* L = h->lines;
+  const uint64_t* l1 = reinterpret_cast<const uint64_t*>(h->super);
+  const uint32_t words = (uint32_t)h->n_super;
+  const size_t smem = ((size_t)words * 8 + 15) & ~(size_t)15;
+  if (what == 2)
+    return launch_ordered_smem(k_b32x2_rank<K, 1, false, false>, k_b32x2_rank<K, 1, false, true>, dyn, h->device,
+                               h->sm_count, g, smem, st, L, l1, words, q, c, out, m, last);
+  if (c)
+    return launch_ordered_smem(k_b32x2_rank<K, 0, true, false>, k_b32x2_rank<K, 0, true, true>, dyn, h->device,
+                               h->sm_count, g, smem, st, L, l1, words, q, c, out, m, last);
+  return launch_ordered_smem(k_b32x2_rank<K, 0, false, false>, k_b32x2_rank<K, 0, false, true>, dyn, h->device,
+                             h->sm_count, g, smem, st, L, l1, words, q, c, out, m, last);
 }
 
 }  // namespace qr

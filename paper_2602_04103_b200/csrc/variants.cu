@@ -174,6 +174,78 @@ qr_status birank16x2_build_device(const uint64_t* d_bits, uint64_t n, int device
   return QR_OK;
 }
 
+// ------------------------------------------------------------------ BiRank32x2 build
+// BiRank32x2 (14.3%): "stores two 32-bit L2 values, shrinking the L1 array".
+// B200 reading (R26): sector h of line j = [u32 d_{j,h} | 224 data bits 448 j + 224 h ..],
+// d_{j,h} = rank(448 j + 224 h + 112) - L1[j >> 23], L1[i] = rank(2^23 * 448 * i) (u64): deltas
+// stay below 2^23 * 448 + 336 < 2^32, and the L1 array (8 B per 3.76 G bits, 18.7 KB at n = 2^43)
+// fits every CTA's shared memory.  Line j's data = text u32 words [14 j, 14 j + 14).
+__global__ void k_b32x2_count(const uint32_t* __restrict__ t32, uint64_t L, uint32_t* __restrict__ part,
+                              uint64_t* __restrict__ tot) {
+  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < L; j += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t* w = t32 + 14 * j;
+    uint32_t c[14];
+#pragma unroll
+    for (int k = 0; k < 14; ++k) c[k] = __popc(w[k]);
+    // anchors at data bits 112 and 336: words 0..2 + low 16 bits of word 3 (resp. 7..9 + word 10 low)
+    uint32_t a0 = __popc(w[3] & 0xffffu), a1 = __popc(w[10] & 0xffffu), h0 = 0, h1 = 0;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) { a0 += c[k]; a1 += c[7 + k]; }
+#pragma unroll
+    for (int k = 0; k < 7; ++k) { h0 += c[k]; h1 += c[7 + k]; }
+    part[2 * j] = a0;
+    part[2 * j + 1] = h0 + a1;
+    tot[j] = h0 + h1;
+  }
+}
+
+__global__ void k_b32x2_write(const uint32_t* __restrict__ t32, uint64_t L, const uint64_t* __restrict__ R,
+                              const uint32_t* __restrict__ part, uint4* __restrict__ lines, uint64_t* __restrict__ l1) {
+  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < L; j += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t base = R[(j >> B32X2_SB_LOG) << B32X2_SB_LOG];
+    if ((j & ((1ull << B32X2_SB_LOG) - 1)) == 0) l1[j >> B32X2_SB_LOG] = base;
+    const uint32_t* w = t32 + 14 * j;
+    uint4* dst = lines + 4 * j;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const uint32_t d = (uint32_t)(R[j] + part[2 * j + h] - base);
+      dst[2 * h] = make_uint4(d, w[7 * h], w[7 * h + 1], w[7 * h + 2]);
+      dst[2 * h + 1] = make_uint4(w[7 * h + 3], w[7 * h + 4], w[7 * h + 5], w[7 * h + 6]);
+    }
+  }
+}
+
+qr_status birank32x2_build_device(const uint64_t* d_bits, uint64_t n, int device, cudaStream_t st, qr_index** out) {
+  qr_index* h = nullptr;
+  qr_status rs = alloc_index(2, n, device, &h, QR_LAYOUT_BIRANK32X2);
+  if (rs != QR_OK) return rs;
+  const uint64_t L = h->n_lines;
+  uint64_t *tot = nullptr, *R = nullptr;
+  uint32_t* part = nullptr;
+  void* tmp = nullptr;
+  size_t tb = 0;
+  cudaError_t e;
+  auto bail = [&](cudaError_t err, const char* what) {
+    cudaFreeAsync(tot, st); cudaFreeAsync(R, st); cudaFreeAsync(part, st); cudaFreeAsync(tmp, st);
+    qr_free(h);
+    return cuda_fail(err, what);
+  };
+  if ((e = cudaMallocAsync((void**)&tot, L * 8, st))) return bail(e, "alloc tot");
+  if ((e = cudaMallocAsync((void**)&R, L * 8, st))) return bail(e, "alloc R");
+  if ((e = cudaMallocAsync((void**)&part, 2 * L * 4, st))) return bail(e, "alloc part");
+  const unsigned g = grid_stride_blocks(L, 256, h->sm_count, 16);
+  const uint32_t* t32 = reinterpret_cast<const uint32_t*>(d_bits);
+  k_b32x2_count<<<g, 256, 0, st>>>(t32, L, part, tot);
+  if ((e = cub::DeviceScan::ExclusiveSum(nullptr, tb, tot, R, (int64_t)L, st))) return bail(e, "scan size");
+  if ((e = cudaMallocAsync(&tmp, tb, st))) return bail(e, "alloc scan tmp");
+  if ((e = cub::DeviceScan::ExclusiveSum(tmp, tb, tot, R, (int64_t)L, st))) return bail(e, "scan");
+  k_b32x2_write<<<g, 256, 0, st>>>(t32, L, R, part, h->lines, reinterpret_cast<uint64_t*>(h->super));
+  if ((e = cudaGetLastError())) return bail(e, "k_b32x2_write");
+  cudaFreeAsync(tot, st); cudaFreeAsync(R, st); cudaFreeAsync(part, st); cudaFreeAsync(tmp, st);
+  *out = h;
+  return QR_OK;
+}
+
 // ------------------------------------------------------------------ QuadRank16x2 build
 // QuadRank16x2 (B200 sector-local variant, NEXT §8(f)4, R25; 33.3%): the σ=4 analogue
 // of BiRank16x2.  Each 32-B sector is self-contained except for the superblock words:
@@ -527,6 +599,7 @@ cudaError_t launch_variant(const qr_index* h, const uint64_t* q, const uint8_t* 
   if (m == 0) return cudaSuccess;
   if (h->layout == QR_LAYOUT_BIRANK16X2) return launch_b16x2_rank(h, q, c, out, m, what, st);
   if (h->layout == QR_LAYOUT_QUADRANK16X2) return launch_q16x2_rank(h, q, c, out, m, what, st);
+  if (h->layout == QR_LAYOUT_BIRANK32X2) return launch_b32x2_rank(h, q, c, out, m, what, st);
   switch (g_rank_k) {
     case 1: return v_launch<1>(h, q, c, out, m, what, st);
     case 4: return v_launch<4>(h, q, c, out, m, what, st);
@@ -580,6 +653,22 @@ struct RankOne {
       for (int t = 0; t < 4; ++t) cnt += __popcll(a[t] & (prefix_mask(16 + x, t) ^ prefix_mask(136, t)));
       const uint64_t base = ((uint64_t)s << BI_SHIFT) + (a[0] & 0xffffull);
       const uint64_t r = x >= 120 ? base + cnt : base - cnt;
+      return c == 0 ? q - r : r;
+    }
+    if (h.layout == QR_LAYOUT_BIRANK32X2) {
+      uint64_t j = q / B32X2_B;
+      j = j > last ? last : j;
+      uint64_t d = q - j * B32X2_B;
+      d = d > B32X2_B - 1 ? B32X2_B - 1 : d;
+      const uint32_t hh = d >= 224 ? 1u : 0u;
+      const int x = (int)(d - 224 * hh);
+      ld_sector_na(h.lines + 4 * j + 2 * hh, a[0], a[1], a[2], a[3]);
+      const uint64_t base = __ldg(reinterpret_cast<const unsigned long long*>(h.super) + (j >> B32X2_SB_LOG)) +
+                            (a[0] & 0xffffffffull);
+      uint32_t cnt = 0;
+#pragma unroll
+      for (int t = 0; t < 4; ++t) cnt += __popcll(a[t] & (prefix_mask(32 + x, t) ^ prefix_mask(144, t)));
+      const uint64_t r = x >= 112 ? base + cnt : base - cnt;
       return c == 0 ? q - r : r;
     }
     if (h.layout == QR_LAYOUT_BIRANK64X2) {

@@ -127,11 +127,12 @@ def _chain_reference(rank_fn, q, n, L):
 
 
 @pytest.mark.parametrize("layout", [qr.QR_LAYOUT_BIRANK16, qr.QR_LAYOUT_BIRANK64X2, qr.QR_LAYOUT_QUADRANK16,
-                                    qr.QR_LAYOUT_QUADRANK64, qr.QR_LAYOUT_BIRANK16X2, qr.QR_LAYOUT_QUADRANK16X2])
+                                    qr.QR_LAYOUT_QUADRANK64, qr.QR_LAYOUT_BIRANK16X2, qr.QR_LAYOUT_QUADRANK16X2,
+                                    qr.QR_LAYOUT_BIRANK32X2])
 def test_rank_chain_latency_mode(cuda, layout):
     torch = _torch()
     n = 3 * 63488 + 1001
-    bits = layout in (qr.QR_LAYOUT_BIRANK16, qr.QR_LAYOUT_BIRANK64X2, qr.QR_LAYOUT_BIRANK16X2)
+    bits = layout in (qr.QR_LAYOUT_BIRANK16, qr.QR_LAYOUT_BIRANK64X2, qr.QR_LAYOUT_BIRANK16X2, qr.QR_LAYOUT_BIRANK32X2)
     w = gen.bits(21, n) if bits else gen.dna(22, n)
     h = qr.qr_build(w, n, layout)
     m, L = 40003, 37                                  # ragged last chain
@@ -154,13 +155,14 @@ def test_rank_chain_latency_mode(cuda, layout):
 
 
 @pytest.mark.parametrize("layout", [qr.QR_LAYOUT_BIRANK16, qr.QR_LAYOUT_BIRANK64X2, qr.QR_LAYOUT_QUADRANK16,
-                                    qr.QR_LAYOUT_QUADRANK64, qr.QR_LAYOUT_BIRANK16X2, qr.QR_LAYOUT_QUADRANK16X2])
+                                    qr.QR_LAYOUT_QUADRANK64, qr.QR_LAYOUT_BIRANK16X2, qr.QR_LAYOUT_QUADRANK16X2,
+                                    qr.QR_LAYOUT_BIRANK32X2])
 def test_save_load_roundtrip(cuda, layout, tmp_path):
     """Checkpoint/resume: export -> .npz -> import gives a handle that answers identically, and the
     build is deterministic (byte-identical layout on a rebuild)."""
     torch = _torch()
     n = 2 * 63488 * 2 + 999
-    bits = layout in (qr.QR_LAYOUT_BIRANK16, qr.QR_LAYOUT_BIRANK64X2, qr.QR_LAYOUT_BIRANK16X2)
+    bits = layout in (qr.QR_LAYOUT_BIRANK16, qr.QR_LAYOUT_BIRANK64X2, qr.QR_LAYOUT_BIRANK16X2, qr.QR_LAYOUT_BIRANK32X2)
     w = gen.bits(31, n) if bits else gen.dna(32, n)
     h = qr.qr_build(w, n, layout)
     p = str(tmp_path / "idx.npz")
@@ -374,3 +376,67 @@ def test_quadrank16x2_superblock_sources(cuda, src):
     ora = oracle.DnaOracle(w, n)
     assert np.array_equal(to_host(out), ora.rank(q, c))
     assert np.array_equal(to_host(o4), ora.rank_all4(q))
+
+
+# ------------------------------------------------------------------ BiRank32x2
+B32X2_SIZES = [0, 1, 111, 112, 113, 223, 224, 225, 335, 336, 337, 447, 448, 449, 895, 896, 897,
+               5000, 3 * 448 * 1000 + 77, (1 << 22) + 3]
+
+
+@pytest.mark.parametrize("n", B32X2_SIZES)
+@pytest.mark.parametrize("p", [0.5, 1.0, 0.01])
+def test_birank32x2_parity(cuda, n, p):
+    """BiRank32x2: every q on small n, the anchors (112, 336), the sector split (224) and lines
+    (448) on larger n; rank with c."""
+    torch = _torch()
+    w = gen.bits(7000 + n, n, p)
+    h = qr.qr_build(w, n, qr.QR_LAYOUT_BIRANK32X2)
+    L = n // 448 + 1
+    assert h.layout == qr.QR_LAYOUT_BIRANK32X2
+    assert h.line_bytes == 64 * L and h.super_bytes == 8 * ((L - 1) // (1 << 23) + 1)
+    ora = oracle.BitsOracle(w, n)
+    q = np.arange(n + 1, dtype=np.uint64) if n <= 100000 else \
+        np.concatenate([gen.queries(9, n, 200000), boundary_queries(n, 224, 448 * 1000, 112)])
+    dq = to_dev(q, cuda)
+    out = torch.empty_like(dq)
+    qr.qr_rank(h, dq, None, out)
+    c = (gen.queries(10, 1, q.size, with_c=True)[1] & 1).astype(np.uint8)
+    out2 = torch.empty_like(dq)
+    qr.qr_rank(h, dq, to_dev(c, cuda), out2)
+    torch.cuda.synchronize()
+    assert np.array_equal(to_host(out), ora.rank(q))
+    assert np.array_equal(to_host(out2), ora.rank(q, c))
+
+
+def test_birank32x2_layout_and_l1_boundary(cuda):
+    """Decode sectors (d_{j,h} + L1[j >> 23] = rank(448 j + 224 h + 112)); a 2^32 + 5-bit text
+    crosses the first L1 boundary (2^23 lines = 3.76e9 bits): queries around it and uniform ones,
+    dynamic order (m >= 2^22), vs the oracle."""
+    torch = _torch()
+    n = 9 * 448 + 100
+    w = gen.bits(3, n, 0.5)
+    h = qr.qr_build(w, n, qr.QR_LAYOUT_BIRANK32X2)
+    lines, l1 = qr.qr_export_layout(h)
+    L = n // 448 + 1
+    u32 = lines.view(np.uint32).reshape(L, 2, 8)
+    ora = oracle.BitsOracle(w, n)
+    for hh in (0, 1):
+        anchors = np.minimum(np.arange(L, dtype=np.uint64) * 448 + 224 * hh + 112, n)
+        assert np.array_equal(u32[:, hh, 0].astype(np.uint64) + l1.view(np.uint64)[0], ora.rank(anchors))
+    n = (1 << 32) + 5
+    bits = torch.empty((n + 63) // 64, dtype=torch.uint64, device=cuda)
+    gen.bits_dev(11, n, 0.5, bits)
+    h = qr.qr_build(bits, n, qr.QR_LAYOUT_BIRANK32X2)
+    assert h.super_bytes == 16
+    wh = bits.cpu().numpy()
+    del bits
+    ora = oracle.BitsOracle(wh, n)
+    edge = 448 * (1 << 23)
+    qe = np.arange(edge - 2000, edge + 2000, dtype=np.uint64)
+    m = (1 << 22) + 11
+    q = np.concatenate([gen.queries(12, n, m - qe.size - 2), qe, np.array([0, n], np.uint64)])
+    dq = to_dev(q, cuda)
+    out = torch.empty_like(dq)
+    qr.qr_rank(h, dq, None, out)
+    torch.cuda.synchronize()
+    assert np.array_equal(to_host(out), ora.rank(q))

@@ -25,7 +25,7 @@ for lg in ((20, 24, 26, 28, 30, 32, 34, 35, 36) if "dna_only" not in sys.argv el
     gen.queries_dev(8, n, M, q)
     r = {"sigma": 2, "log2_n": lg}
     for name, layout in (("birank16", qr.QR_LAYOUT_BIRANK16), ("birank16x2", qr.QR_LAYOUT_BIRANK16X2),
-                         ("birank64x2", qr.QR_LAYOUT_BIRANK64X2)):
+                         ("birank32x2", qr.QR_LAYOUT_BIRANK32X2), ("birank64x2", qr.QR_LAYOUT_BIRANK64X2)):
         h = qr.qr_build(bits, n, layout)
         r[name + "_gq_s"] = M / t(lambda: qr.qr_rank(h, q, None, out, M, st)) / 1e6
         r[name + "_bytes"] = h.line_bytes + h.super_bytes
@@ -37,7 +37,7 @@ for lg in ((20, 24, 26, 28, 30, 32, 34, 35, 36) if "dna_only" not in sys.argv el
     del bits; torch.cuda.empty_cache()
     print(json.dumps(r), flush=True)
 o4 = torch.empty((M, 4), dtype=torch.uint64, device=dev)
-for lg in (20, 24, 26, 28, 30, 32, 33, 34):
+for lg in ((20, 24, 26, 28, 30, 32, 33, 34) if "bits_only" not in sys.argv else ()):
     n = 1 << lg
     text = torch.empty((n + 31) // 32, dtype=torch.uint64, device=dev); gen.dna_dev(9, n, 0, text)
     gen.queries_dev(10, n, M, q, c)
