@@ -356,7 +356,7 @@ def bench_reads(ctx, n, m_total, length, seed, steps, warmup):
             "fm_build_s": round(build_s, 2)}
 
 
-def bench_approx(ctx, n, m_total, length, seed, steps, warmup):
+def bench_approx(ctx, n, m_total, length, seed, steps, warmup, bwt_layout=None):
     """<=1-substitution counting (rank_4-driven, NEXT §8(f)3) on the configs[3] text/patterns."""
     import gen
     import paper_2602_04103_b200 as qr
@@ -364,7 +364,7 @@ def bench_approx(ctx, n, m_total, length, seed, steps, warmup):
     torch = ctx.torch
     text = torch.empty((n + 31) // 32 + 1, dtype=torch.uint64, device=ctx.dev)
     gen.dna_dev(seed, n, 0, text)
-    fm = qr.qr_fm_build(text, n, device=ctx.gpu)
+    fm = qr.qr_fm_build(text, n, device=ctx.gpu, bwt_layout=bwt_layout)
     i0, m = shard(m_total, ctx.world, ctx.rank)
     pats = torch.empty(m * length, dtype=torch.uint8, device=ctx.dev)
     gen.patterns_dev(seed, 0, m, length, text, n, pats, i0=i0)
@@ -559,6 +559,8 @@ def main():
         # stand-in for CHM13v2; n+1 < 2^32), 150-bp reads at 1% substitutions, both strands
         rows["genome_scale_reads_3.1Gbp"] = bench_reads_safe(ctx, 3_100_000_000, 10**7, 150, 56, K, W)
         rows["c4_quadfm_approx1"] = bench_approx(ctx, N4, 10**6, L4, SEED[4], K, W)
+        rows["c4_quadfm_approx1_bwt16x2"] = bench_approx(ctx, N4, 10**6, L4, SEED[4], K, W,
+                                                         bwt_layout=qr.QR_LAYOUT_QUADRANK16X2)
         rows["layout_variants"] = bench_variants(ctx, K, W)
         rows["latency_mode"] = bench_latency(ctx, K, W)
         rows["c1_small"] = bench_small(ctx, K, W)

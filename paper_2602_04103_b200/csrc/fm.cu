@@ -713,10 +713,12 @@ __global__ void __launch_bounds__(256) k_fm_approx1(FmParams F, const uint8_t* _
       const uint32_t key0 = kmer_key(F.K, P, p, len);
       for (int t = 0; t < F.K; ++t) {                     // one substitution among the last K symbols
         const uint32_t f = (key0 >> (2 * t)) & 3u;
-        for (uint32_t r = 1; r < 4; ++r) {
-          const uint2 iv = __ldg(F.kmer + (key0 ^ ((f ^ ((f + r) & 3u)) << (2 * t))));
-          if (iv.x < iv.y) total += fm_continue<BW>(F, P, (int64_t)len - 1 - F.K, iv.x, iv.y);
-        }
+        uint2 iv[3];                                       // the three variants' lookups issued together
+#pragma unroll
+        for (uint32_t r = 1; r < 4; ++r) iv[r - 1] = __ldg(F.kmer + (key0 ^ ((f ^ ((f + r) & 3u)) << (2 * t))));
+#pragma unroll
+        for (int r = 0; r < 3; ++r)
+          if (iv[r].x < iv[r].y) total += fm_continue<BW>(F, P, (int64_t)len - 1 - F.K, iv[r].x, iv[r].y);
       }
       const uint2 iv0 = __ldg(F.kmer + key0);
       lo = iv0.x; hi = iv0.y;

@@ -1,0 +1,26 @@
+"""QuadFm <= 1-substitution counting on configs[3] (10^6 x 32), both BWT layouts."""
+import json, os, sys
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import torch  # noqa: E402
+import gen  # noqa: E402
+import paper_2602_04103_b200 as qr  # noqa: E402
+dev = torch.device("cuda:0"); st = torch.cuda.current_stream()
+tag = sys.argv[1] if len(sys.argv) > 1 else ""
+def t(fn, reps=5):
+    for _ in range(3): fn()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(st)
+    for _ in range(reps): fn()
+    b.record(st); torch.cuda.synchronize()
+    return a.elapsed_time(b) / reps
+n, m, L = 1 << 26, 10**6, 32
+text = torch.empty((n + 31) // 32 + 1, dtype=torch.uint64, device=dev); gen.dna_dev(4, n, 0, text)
+pats = torch.empty(m * L, dtype=torch.uint8, device=dev); gen.patterns_dev(4, 0, m, L, text, n, pats)
+for name, lay in (("quadrank16", qr.QR_LAYOUT_QUADRANK16), ("quadrank16x2", qr.QR_LAYOUT_QUADRANK16X2)):
+    fm = qr.qr_fm_build(text, n, bwt_layout=lay)
+    out = torch.empty(m, dtype=torch.int32, device=dev)
+    ms = t(lambda: qr.qr_fm_count_approx(fm, pats, None, L, 1, out, m, st))
+    print(json.dumps({"tag": tag, "bwt": name, "ms": ms, "gpat_s": m / ms / 1e6, "checksum": int(out.to(torch.int64).sum())}), flush=True)
+    del fm
