@@ -669,6 +669,24 @@ __device__ __forceinline__ void fm_occ4(const FmParams& F, uint32_t x, uint32_t 
 }
 
 // exact backward search of P[0..k] from [lo, hi); returns the final interval size
+// the same for three intervals continuing over the same symbols P[k], P[k-1], ...: their steps
+// are independent, so each position issues the loads of all live intervals before consuming any
+template <int BW>
+__device__ __forceinline__ uint32_t fm_continue3(const FmParams& F, PatWindow& P, int64_t k, uint32_t (&lo)[3],
+                                                 uint32_t (&hi)[3]) {
+  uint32_t nl;
+  for (; k >= 0 && (lo[0] < hi[0] || lo[1] < hi[1] || lo[2] < hi[2]); --k) {
+    const uint32_t c = P.at(k);
+#pragma unroll
+    for (int r = 0; r < 3; ++r)
+      if (lo[r] < hi[r]) fm_step<0, BW>(F, c, lo[r], hi[r], nl);
+  }
+  uint32_t t = 0;
+#pragma unroll
+  for (int r = 0; r < 3; ++r) t += lo[r] < hi[r] ? hi[r] - lo[r] : 0u;
+  return t;
+}
+
 template <int BW>
 __device__ __forceinline__ uint32_t fm_continue(const FmParams& F, PatWindow& P, int64_t k, uint32_t lo, uint32_t hi) {
   uint32_t nl;
@@ -716,9 +734,8 @@ __global__ void __launch_bounds__(256) k_fm_approx1(FmParams F, const uint8_t* _
         uint2 iv[3];                                       // the three variants' lookups issued together
 #pragma unroll
         for (uint32_t r = 1; r < 4; ++r) iv[r - 1] = __ldg(F.kmer + (key0 ^ ((f ^ ((f + r) & 3u)) << (2 * t))));
-#pragma unroll
-        for (int r = 0; r < 3; ++r)
-          if (iv[r].x < iv[r].y) total += fm_continue<BW>(F, P, (int64_t)len - 1 - F.K, iv[r].x, iv[r].y);
+        uint32_t vl[3] = {iv[0].x, iv[1].x, iv[2].x}, vh[3] = {iv[0].y, iv[1].y, iv[2].y};
+        total += fm_continue3<BW>(F, P, (int64_t)len - 1 - F.K, vl, vh);
       }
       const uint2 iv0 = __ldg(F.kmer + key0);
       lo = iv0.x; hi = iv0.y;
@@ -732,11 +749,14 @@ __global__ void __launch_bounds__(256) k_fm_approx1(FmParams F, const uint8_t* _
       if (BW == 1) { fm_occ4_x2(F, lo, ol); fm_occ4_x2(F, hi, oh); }
       else         { fm_occ4(F, lo, ol); fm_occ4(F, hi, oh); }
       const uint32_t cj = P.at(j);
+      uint32_t bl[3], bh[3];                              // the three substituted symbols' intervals
 #pragma unroll
-      for (uint32_t c = 0; c < 4; ++c) {
-        const uint32_t a = Cs[c] + ol[c], b = Cs[c] + oh[c];
-        if (c != cj && a < b) total += fm_continue<BW>(F, P, j - 1, a, b);
+      for (uint32_t r = 0; r < 3; ++r) {
+        const uint32_t c = (cj + 1 + r) & 3u;
+        bl[r] = Cs[c] + ol[c];
+        bh[r] = Cs[c] + oh[c];
       }
+      total += fm_continue3<BW>(F, P, j - 1, bl, bh);
       lo = Cs[cj] + ol[cj];
       hi = Cs[cj] + oh[cj];
     }
