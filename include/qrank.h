@@ -22,8 +22,9 @@
  *   - Query arrays (q, c, out, patterns, lengths) are either ALL device pointers on the
  *     handle's device (fast path: one kernel launch, fully asynchronous on `stream`), or ALL
  *     host pointers (staged path: chunked host->device copy, kernel, device->host copy,
- *     double-buffered over two internal streams; `stream` is made to wait for the whole
- *     pipeline; pinned host memory gives overlap, pageable memory works but serialises).
+ *     pipelined over internal streams, 3 by default, knob stage_slots; `stream` is made to
+ *     wait for the whole pipeline; pinned host memory gives overlap, pageable memory works
+ *     but serialises).
  *     Mixed spaces are QR_EINVAL.
  *   - `stream` is a cudaStream_t passed as void* (NULL = the legacy default stream).
  *

@@ -26,7 +26,7 @@ int g_fm_dyn = 1;               // FM count: 1 = persistent grid + warp chunks f
 int g_fm_seed = 0;              // FM seed pre-pass (dynamic order only): 0 auto (L2-resident BWT), 1 never, 2 always
 int g_fm_smem = 1;              // FM superblock words from shared memory: 0 off, 1 auto, 2 packed table whenever it fits
 int g_fm_lean = 0;              // FM step flavour: 0 auto (by L2 residency), 1 de-duplicating, 2 lean
-int g_index64 = 0;              // 1: force the 64-bit line-index path (tests the n >= 2^36/2^37 code on small n)          // lane of a pair that loads the superblock word
+int g_index64 = 0;              // 1: force the 64-bit line-index path (tests the n >= 2^36/2^37 code on small n)
 int g_rank_smem = 1;            // superblock words from cluster shared memory: 0 never, 1 large batches, 2 always
 int g_rank_dyn = 1;             // cluster rank kernels: 1 = dynamic (atomic chunk) work order, 0 = static grid stride
 int g_rank_smem_clusters = 0;   // cluster rank kernels: 0 = as many 2-CTA clusters as fit (occupancy API), else this many
@@ -179,7 +179,7 @@ static qr_status stage_input(const uint64_t* src, uint64_t words, uint64_t padde
 }
 
 // ---- staged host-pointer pipeline ----------------------------------------------------------
-// S slots (default 2), one internal stream each: chunk k uses slot k%S on stream k%S, so the H2D
+// S slots (default 3, knob stage_slots), one internal stream each: chunk k uses slot k%S on stream k%S, so the H2D
 // copy and kernel of one chunk overlap the kernel and D2H copy of the others (separate copy
 // engines).  In-order streams make slot reuse safe across chunks and across calls.
 constexpr int MAX_SLOTS = 4;
@@ -588,7 +588,8 @@ QR_EXPORT qr_status qr_fm_build_opts(const uint64_t* text2b, uint64_t n, const u
   s = fm_build_device(d, n, dsa, device, st, out, kmer_k, bwt_layout);
   cudaFreeAsync(d, st);
   if (dsa) cudaFreeAsync(dsa, st);
-  cudaStreamSynchronize(st);
+  const cudaError_t e = cudaStreamSynchronize(st);
+  if (s == QR_OK && e) { qr_fm_free(*out); *out = nullptr; return cuda_fail(e, "qr_fm_build"); }
   return s;
 }
 
