@@ -197,12 +197,22 @@ static Stager* stager_for(int device) {
   std::lock_guard<std::mutex> g(g_stagers_mu);
   if ((int)g_stagers.size() <= device) g_stagers.resize(device + 1, nullptr);
   if (!g_stagers[device]) {
-    Stager* S = new Stager();
-    for (int i = 0; i < MAX_SLOTS; ++i) {
-      cudaStreamCreateWithFlags(&S->s[i], cudaStreamNonBlocking);
-      cudaEventCreateWithFlags(&S->ev_done[i], cudaEventDisableTiming);
+    Stager* S = new (std::nothrow) Stager();
+    if (!S) return nullptr;
+    bool ok = cudaEventCreateWithFlags(&S->ev_start, cudaEventDisableTiming) == cudaSuccess;
+    for (int i = 0; i < MAX_SLOTS && ok; ++i)
+      ok = cudaStreamCreateWithFlags(&S->s[i], cudaStreamNonBlocking) == cudaSuccess &&
+           cudaEventCreateWithFlags(&S->ev_done[i], cudaEventDisableTiming) == cudaSuccess;
+    if (!ok) {   // the staged path never falls back to the legacy stream
+      for (int i = 0; i < MAX_SLOTS; ++i) {
+        if (S->s[i]) cudaStreamDestroy(S->s[i]);
+        if (S->ev_done[i]) cudaEventDestroy(S->ev_done[i]);
+      }
+      if (S->ev_start) cudaEventDestroy(S->ev_start);
+      delete S;
+      cudaGetLastError();
+      return nullptr;
     }
-    cudaEventCreateWithFlags(&S->ev_start, cudaEventDisableTiming);
     g_stagers[device] = S;
   }
   return g_stagers[device];
@@ -218,6 +228,7 @@ template <typename Launch>
 static qr_status run_staged(int device, cudaStream_t user, uint64_t m, const std::vector<StageArray>& arrays,
                             Launch launch) {
   Stager* S = stager_for(device);
+  if (!S) return fail(QR_ECUDA, "staged path: cannot create internal streams/events on device %d", device);
   std::lock_guard<std::mutex> g(S->mu);
   size_t per_item = 0;
   for (auto& a : arrays) per_item += (a.item_bytes + 15) & ~size_t(15);

@@ -31,7 +31,12 @@ static CtrRing* ctr_ring(int device) {
     CtrRing* n = new CtrRing();
     if (cudaMalloc((void**)&n->d, CTR_SLOTS * 128) != cudaSuccess) { delete n; return nullptr; }
     for (int i = 0; i < CTR_SLOTS; ++i)
-      if (cudaEventCreateWithFlags(&n->ev[i], cudaEventDisableTiming) != cudaSuccess) { delete n; return nullptr; }
+      if (cudaEventCreateWithFlags(&n->ev[i], cudaEventDisableTiming) != cudaSuccess) {
+        for (int j = 0; j < i; ++j) cudaEventDestroy(n->ev[j]);
+        cudaFree(n->d);
+        delete n;
+        return nullptr;
+      }
     r = n;
   }
   return r;
