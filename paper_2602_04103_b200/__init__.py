@@ -231,6 +231,10 @@ def qr_rank(h: Index, q, c, out, m: int | None = None, stream=None):
 
 def qr_rank_chain(h: Index, q, c, out, chain_len: int, m: int | None = None, stream=None):
     m = (q.numel() if hasattr(q, "numel") else q.size) if m is None else m
+    _need(q, 8, m, "qr_rank_chain q")
+    _need(out, 8, m, "qr_rank_chain out")
+    if c is not None:
+        _need(c, 1, m, "qr_rank_chain c")
     _check(lib().qr_rank_chain(h.ptr, _ptr(q), _ptr(c), _ptr(out), m, chain_len, _stream(stream)), "qr_rank_chain")
     return out
 
@@ -261,30 +265,39 @@ def qr_fm_build(text2b, n: int, sa=None, device: int = 0, stream=None, kmer_k: i
     return Fm(out.value)
 
 
-def qr_fm_count(fm: Fm, patterns, lengths, fixed_len: int, out, m: int, stream=None):
-    _need(out, 4, m, "qr_fm_count out")
+def _need_fm(where: str, patterns, lengths, fixed_len: int, m: int, *outs):
+    for o in outs:
+        _need(o, 4, m, f"{where} out")
     if lengths is not None:
-        _need(lengths, 4, m, "qr_fm_count lengths")
+        _need(lengths, 4, m, f"{where} lengths")
     else:
-        _need(patterns, 1, m * fixed_len, "qr_fm_count patterns")
+        _need(patterns, 1, m * fixed_len, f"{where} patterns")
+
+
+def qr_fm_count(fm: Fm, patterns, lengths, fixed_len: int, out, m: int, stream=None):
+    _need_fm("qr_fm_count", patterns, lengths, fixed_len, m, out)
     _check(lib().qr_fm_count(fm.ptr, _ptr(patterns), _ptr(lengths), fixed_len, _ptr(out), m, _stream(stream)),
            "qr_fm_count")
     return out
 
 
 def qr_fm_count_both(fm: Fm, patterns, lengths, fixed_len: int, out_fwd, out_rc, m: int, stream=None):
+    _need_fm("qr_fm_count_both", patterns, lengths, fixed_len, m, out_fwd, out_rc)
     _check(lib().qr_fm_count_both(fm.ptr, _ptr(patterns), _ptr(lengths), fixed_len, _ptr(out_fwd), _ptr(out_rc), m,
                                   _stream(stream)), "qr_fm_count_both")
     return out_fwd, out_rc
 
 
 def qr_fm_count_approx(fm: Fm, patterns, lengths, fixed_len: int, max_mismatches: int, out, m: int, stream=None):
+    _need_fm("qr_fm_count_approx", patterns, lengths, fixed_len, m, out)
     _check(lib().qr_fm_count_approx(fm.ptr, _ptr(patterns), _ptr(lengths), fixed_len, max_mismatches, _ptr(out), m,
                                     _stream(stream)), "qr_fm_count_approx")
     return out
 
 
 def qr_fm_count_work(fm: Fm, patterns, lengths, fixed_len: int, out, m: int, work, stream=None):
+    _need_fm("qr_fm_count_work", patterns, lengths, fixed_len, m, out)
+    _need(work, 8, 2, "qr_fm_count_work work")
     _check(lib().qr_fm_count_work(fm.ptr, _ptr(patterns), _ptr(lengths), fixed_len, _ptr(out), m, _ptr(work),
                                   _stream(stream)), "qr_fm_count_work")
     return out
@@ -292,6 +305,8 @@ def qr_fm_count_work(fm: Fm, patterns, lengths, fixed_len: int, out, m: int, wor
 
 def qr_gather_ceiling(h: Index, q, out, mode: int = 0, m: int | None = None, stream=None):
     m = (q.numel() if hasattr(q, "numel") else q.size) if m is None else m
+    _need(q, 8, m, "qr_gather_ceiling q")
+    _need(out, 8, m, "qr_gather_ceiling out")
     _check(lib().qr_gather_ceiling(h.ptr, _ptr(q), _ptr(out), m, mode, _stream(stream)), "qr_gather_ceiling")
     return out
 

@@ -86,6 +86,21 @@ def test_binding_rejects_wrong_dtypes():
         qr.qr_rank(h, np.zeros(10, np.uint64), None, np.zeros(5, np.uint64))
     with pytest.raises(qr.QrError):
         qr.qr_rank_all4(h, np.zeros(10, np.uint64), np.zeros(10, np.uint64))
+    with pytest.raises(qr.QrError):
+        qr.qr_rank_chain(h, np.zeros(10, np.uint64), None, np.zeros(10, np.uint32), 5)
+    with pytest.raises(qr.QrError):
+        qr.qr_gather_ceiling(h, np.zeros(10, np.uint64), np.zeros(9, np.uint64))
+    fm = object.__new__(qr.Fm)
+    pats = np.zeros(10 * 32, np.uint8)
+    with pytest.raises(qr.QrError):      # patterns too short for m * fixed_len
+        qr.qr_fm_count(fm, pats[:-1], None, 32, np.zeros(10, np.uint32), 10)
+    with pytest.raises(qr.QrError):      # reverse-complement output too short
+        qr.qr_fm_count_both(fm, pats, None, 32, np.zeros(10, np.uint32), np.zeros(9, np.uint32), 10)
+    with pytest.raises(qr.QrError):      # u64 counts where the ABI writes u32
+        qr.qr_fm_count_approx(fm, pats, None, 32, 1, np.zeros(10, np.uint64), 10)
+    with pytest.raises(qr.QrError):      # lengths must be u32
+        qr.qr_fm_count_work(fm, pats, np.full(10, 32, np.int64), 0, np.zeros(10, np.uint32), 10,
+                            np.zeros(2, np.uint64))
 
 
 def test_tuning_knob_validation():
