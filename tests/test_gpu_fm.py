@@ -108,6 +108,55 @@ def test_fm_build_and_count_parity(cuda, n, kind):
     assert np.array_equal(hout, ref)
 
 
+def _repetitive(name: str, n: int) -> np.ndarray:
+    rng = np.random.default_rng(n)
+    if name == "all_A":
+        return np.zeros(n, np.uint8)
+    if name == "all_T":
+        return np.full(n, 3, np.uint8)
+    if name == "period4":
+        return np.resize(np.array([0, 1, 2, 3], np.uint8), n)
+    if name == "period2_tail":                     # (AC)^k then one G: every group splits late
+        s = np.resize(np.array([0, 1], np.uint8), n); s[-1] = 2
+        return s
+    if name == "period37":
+        return np.resize(rng.integers(0, 4, 37).astype(np.uint8), n)
+    if name == "doubled":                          # a random half repeated: groups of two to the end
+        h = rng.integers(0, 4, n // 2).astype(np.uint8)
+        return np.concatenate([h, h, rng.integers(0, 4, n - 2 * (n // 2)).astype(np.uint8)])
+    raise ValueError(name)
+
+
+@pytest.mark.parametrize("name", ["all_A", "all_T", "period4", "period2_tail", "period37", "doubled"])
+@pytest.mark.parametrize("n", [1, 21, 22, 43, 1000, 6001])
+def test_fm_build_repetitive_texts(cuda, name, n):
+    """The GPU suffix sort (prefix doubling with discarding) on texts whose suffix groups stay
+    large for many rounds: the BWT, spos and C must equal the oracle's (which sorts by doubling +
+    qsort), checked through the BWT rank at every q and c, plus counts of every pattern shape."""
+    torch = _torch()
+    sym = _repetitive(name, n)
+    w = pack2(sym)
+    ora = oracle.FmOracle(sym)
+    fm = qr.qr_fm_build(w, n)
+    assert fm.spos == ora.spos
+    assert fm.C == [int(x) for x in ora.C]
+    bw = ora.bwt.copy(); bw[bw == 4] = 0
+    bora = oracle.DnaOracle(pack2(bw), n + 1)
+    q = np.repeat(np.arange(n + 2, dtype=np.uint64), 4)
+    c = np.tile(np.arange(4, dtype=np.uint8), n + 2)
+    out = torch.empty(q.size, dtype=torch.uint64, device=cuda)
+    qr.qr_rank(fm.bwt, to_dev(q, cuda), to_dev(c, cuda), out)
+    torch.cuda.synchronize()
+    assert np.array_equal(to_host(out), bora.rank(q, c))
+    pats = mixed_patterns(np.random.default_rng(7), sym, 200)
+    cat, off, lens = oracle.pack_patterns(pats)
+    ref = ora.count(cat, off, lens)
+    dout = torch.empty(lens.size, dtype=torch.int32, device=cuda)
+    qr.qr_fm_count(fm, to_dev(cat, cuda), to_dev(lens, cuda), 0, dout, lens.size)
+    torch.cuda.synchronize()
+    assert np.array_equal(to_host(dout).view(np.uint32), ref)
+
+
 def test_fm_kmer_table_matches_oracle(cuda):
     n = 300000
     w = gen.dna(42, n)
