@@ -114,41 +114,52 @@ struct MaxU32 {
   __device__ __forceinline__ uint32_t operator()(uint32_t a, uint32_t b) const { return a > b ? a : b; }
 };
 
-// Place the sorted active items: SA[pos[k]] = V[k], rank[V[k]] = group start; flag[k] = 1 while
-// item k's group still has another member (stays active).
+// Place the sorted active items: SA[pos[k]] = V[k], rank[V[k]] = its new group start (rounds
+// after the first write it only where it changed: the group's first subgroup keeps the old start,
+// the key's high part); flag[k] = 1 while item k's group still has another member (stays active).
 __global__ void k_sa_place(const uint64_t* __restrict__ K, const uint32_t* __restrict__ V,
                            const uint32_t* __restrict__ pos, const uint32_t* __restrict__ gs, uint64_t A,
-                           uint32_t* __restrict__ sa, uint32_t* __restrict__ rank, uint32_t* __restrict__ flag) {
+                           int gshift, uint32_t* __restrict__ sa, uint32_t* __restrict__ rank,
+                           uint32_t* __restrict__ flag) {
   for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < A; k += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t v = V[k];
+    const uint32_t v = V[k], g = gs[k];
+    const uint64_t key = K[k];
     sa[pos[k]] = v;
-    rank[v] = gs[k];
-    const bool single = sa_head(K, k) && (k + 1 == A || K[k + 1] != K[k]);
+    if (gshift == 0 || (uint32_t)(key >> gshift) != g) rank[v] = g;
+    const bool single = (k == 0 || key != K[k - 1]) && (k + 1 == A || K[k + 1] != key);
     flag[k] = single ? 0u : 1u;
   }
 }
 
-// Keep the active items: pos_out[off[k]] = pos[k] where item k is not a singleton (off = the
-// exclusive sum of flag); the count of survivors goes to *count.
-__global__ void k_sa_compact(const uint64_t* __restrict__ K, const uint32_t* __restrict__ pos,
+// Keep the active items, in SA-position order: survivor k goes to slot off[k] (off = the
+// exclusive sum of flag) with its SA position, group start and suffix index, so the next
+// round's keys read them sequentially; the count of survivors goes to *count.
+__global__ void k_sa_compact(const uint64_t* __restrict__ K, const uint32_t* __restrict__ V,
+                             const uint32_t* __restrict__ pos, const uint32_t* __restrict__ gs,
                              const uint32_t* __restrict__ off, uint64_t A, uint32_t* __restrict__ pos_out,
+                             uint32_t* __restrict__ g_out, uint32_t* __restrict__ i_out,
                              unsigned long long* __restrict__ count) {
   for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < A; k += (uint64_t)gridDim.x * blockDim.x) {
     const bool single = sa_head(K, k) && (k + 1 == A || K[k + 1] != K[k]);
-    if (!single) pos_out[off[k]] = pos[k];
+    if (!single) {
+      const uint32_t o = off[k];
+      pos_out[o] = pos[k];
+      g_out[o] = gs[k];
+      i_out[o] = V[k];
+    }
     if (k + 1 == A) *count = (unsigned long long)off[k] + (single ? 0u : 1u);
   }
 }
 
-// doubling key of active item k: (group start of SA[pos[k]], rank of the suffix h further on + 1,
-// or 0 past the end), packed in 2*b bits
-__global__ void k_sa_keys(const uint32_t* __restrict__ sa, const uint32_t* __restrict__ pos,
+// doubling key of active item k (suffix i = ii[k], group start gg[k]): (gg[k], rank of the suffix
+// h further on + 1, or 0 past the end), packed in 2*b bits
+__global__ void k_sa_keys(const uint32_t* __restrict__ gg, const uint32_t* __restrict__ ii,
                           const uint32_t* __restrict__ rank, uint64_t A, uint64_t N, uint64_t h, int b,
                           uint64_t* __restrict__ keys, uint32_t* __restrict__ vals) {
   for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < A; k += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t i = sa[pos[k]];
+    const uint32_t i = ii[k];
     const uint64_t r2 = ((uint64_t)i + h < N) ? (uint64_t)rank[i + h] + 1 : 0;
-    keys[k] = ((uint64_t)rank[i] << b) | r2;
+    keys[k] = ((uint64_t)gg[k] << b) | r2;
     vals[k] = i;
   }
 }
@@ -163,7 +174,7 @@ static int bits_for(uint64_t x) {  // bits needed to represent values 0..x
 static qr_status build_sa(const uint64_t* d_text, uint64_t n, int sms, cudaStream_t st, uint32_t* d_sa) {
   const uint64_t N = n + 1;
   uint64_t *ka = nullptr, *kb = nullptr;
-  uint32_t *va = nullptr, *vb = nullptr, *rank = nullptr, *gs = nullptr, *pa = nullptr;
+  uint32_t *va = nullptr, *vb = nullptr, *rank = nullptr, *gs = nullptr, *pa = nullptr, *pb = nullptr;
   unsigned long long* count = nullptr;
   unsigned long long* h_count = nullptr;
   void* tmp = nullptr;
@@ -171,7 +182,7 @@ static qr_status build_sa(const uint64_t* d_text, uint64_t n, int sms, cudaStrea
   cudaError_t e;
   auto cleanup = [&]() {
     cudaFreeAsync(ka, st); cudaFreeAsync(kb, st); cudaFreeAsync(va, st); cudaFreeAsync(vb, st);
-    cudaFreeAsync(rank, st); cudaFreeAsync(gs, st); cudaFreeAsync(pa, st);
+    cudaFreeAsync(rank, st); cudaFreeAsync(gs, st); cudaFreeAsync(pa, st); cudaFreeAsync(pb, st);
     cudaFreeAsync(count, st); cudaFreeAsync(tmp, st);
     if (h_count) cudaFreeHost(h_count);
   };
@@ -183,6 +194,7 @@ static qr_status build_sa(const uint64_t* d_text, uint64_t n, int sms, cudaStrea
   if ((e = cudaMallocAsync((void**)&rank, N * 4, st))) return bail(e, "sa rank");
   if ((e = cudaMallocAsync((void**)&gs, N * 4, st))) return bail(e, "sa group starts");
   if ((e = cudaMallocAsync((void**)&pa, N * 4, st))) return bail(e, "sa positions");
+  if ((e = cudaMallocAsync((void**)&pb, N * 4, st))) return bail(e, "sa positions");
   if ((e = cudaMallocAsync((void**)&count, 8, st))) return bail(e, "sa count");
   if ((e = cudaMallocHost((void**)&h_count, 8))) return bail(e, "sa host count");
   {
@@ -203,24 +215,28 @@ static qr_status build_sa(const uint64_t* d_text, uint64_t n, int sms, cudaStrea
   k_sa_iota<<<grid(N), 256, 0, st>>>(pa, N);
   uint64_t A = N, h = 21;
   int bits = 63;
+  uint64_t* kin = ka;                        // keys of the round are written here
+  uint32_t* carry = nullptr;                 // survivors' group starts [0, N) and suffixes [N, 2N)
   for (int round = 0; round < 64 && A; ++round) {
-    cub::DoubleBuffer<uint64_t> K(ka, kb);
+    if (round) k_sa_keys<<<grid(A), 256, 0, st>>>(carry, carry + N, rank, A, N, h >> 1, b, kin, va);
+    cub::DoubleBuffer<uint64_t> K(kin, kin == ka ? kb : ka);
     cub::DoubleBuffer<uint32_t> V(va, vb);
-    if (round) k_sa_keys<<<grid(A), 256, 0, st>>>(d_sa, pa, rank, A, N, h >> 1, b, ka, va);
     size_t tb = tmp_bytes;
     if ((e = cub::DeviceRadixSort::SortPairs(tmp, tb, K, V, (int64_t)A, 0, bits, st))) return bail(e, "sort");
     k_sa_heads<<<grid(A), 256, 0, st>>>(K.Current(), pa, A, gs);
     tb = tmp_bytes;
     if ((e = cub::DeviceScan::InclusiveScan(tmp, tb, gs, gs, MaxU32(), (int64_t)A, st))) return bail(e, "scan");
     uint32_t* flag = V.Alternate();          // free after the sort; becomes the offsets
-    k_sa_place<<<grid(A), 256, 0, st>>>(K.Current(), V.Current(), pa, gs, A, d_sa, rank, flag);
+    k_sa_place<<<grid(A), 256, 0, st>>>(K.Current(), V.Current(), pa, gs, A, round ? b : 0, d_sa, rank, flag);
     tb = tmp_bytes;
     if ((e = cub::DeviceScan::ExclusiveSum(tmp, tb, flag, flag, (int64_t)A, st))) return bail(e, "scan");
-    k_sa_compact<<<grid(A), 256, 0, st>>>(K.Current(), pa, flag, A, gs, count);   // gs is free again
+    carry = reinterpret_cast<uint32_t*>(K.Alternate());   // free after the sort: 2N u32
+    k_sa_compact<<<grid(A), 256, 0, st>>>(K.Current(), V.Current(), pa, gs, flag, A, pb, carry, carry + N, count);
     cudaMemcpyAsync(h_count, count, 8, cudaMemcpyDeviceToHost, st);
     if ((e = cudaStreamSynchronize(st))) return bail(e, "sa round sync");
     A = *h_count;
-    uint32_t* t = pa; pa = gs; gs = t;
+    uint32_t* t = pa; pa = pb; pb = t;
+    kin = K.Current();                       // the next round's keys go to the buffer not holding `carry`
     h *= 2;                                  // keys of the next round look h/2 = this round's reach ahead
     bits = 2 * b;
   }
