@@ -163,19 +163,30 @@ struct DeviceGuard {
 };
 
 // Copy `words` u64 of a host-or-device input into a fresh zero-padded device buffer of
-// `padded_words` u64 (stream-ordered).  Caller frees with cudaFreeAsync.
+// `padded_words` u64 (stream-ordered).  Caller releases it with free_staged.  Plain cudaMalloc:
+// the stream-ordered pool maps / unmaps GB-sized blocks ~50x slower (profiles/r01_alloc_probe.jsonl).
 static qr_status stage_input(const uint64_t* src, uint64_t words, uint64_t padded_words, cudaStream_t st,
                              uint64_t** dst) {
   cudaError_t e;
   uint64_t* d = nullptr;
-  if ((e = cudaMallocAsync((void**)&d, padded_words * 8, st))) return cuda_fail(e, "alloc staged input");
+  if ((e = cudaMalloc((void**)&d, padded_words * 8))) return cuda_fail(e, "alloc staged input");
   if (padded_words > words) cudaMemsetAsync(d + words, 0, (padded_words - words) * 8, st);
   if (words && (e = cudaMemcpyAsync(d, src, words * 8, cudaMemcpyDefault, st))) {
-    cudaFreeAsync(d, st);
+    cudaStreamSynchronize(st);
+    cudaFree(d);
     return cuda_fail(e, "copy input");
   }
   *dst = d;
   return QR_OK;
+}
+
+// Release a build temporary once the work queued on `st` that reads it has finished.
+// Returns the synchronisation's status (an asynchronous fault of the build surfaces here).
+static cudaError_t free_staged(void* d, cudaStream_t st) {
+  if (!d) return cudaSuccess;
+  const cudaError_t e = cudaStreamSynchronize(st);
+  cudaFree(d);
+  return e;
 }
 
 // ---- staged host-pointer pipeline ----------------------------------------------------------
@@ -397,9 +408,9 @@ QR_EXPORT qr_status qr_birank_build(const uint64_t* bits, uint64_t n, int device
   qr_status s = stage_input(bits, words, padded, st, &d);
   if (s != QR_OK) return s;
   s = birank_build_device(d, n, device, st, out);
-  cudaFreeAsync(d, st);
+  const cudaError_t fe = free_staged(d, st);
   if (s == QR_OK) {
-    cudaError_t e = cudaStreamSynchronize(st);
+    cudaError_t e = fe ? fe : cudaStreamSynchronize(st);
     if (e) { qr_free(*out); *out = nullptr; return cuda_fail(e, "qr_birank_build"); }
   }
   return s;
@@ -420,9 +431,9 @@ QR_EXPORT qr_status qr_quadrank_build(const uint64_t* text2b, uint64_t n, int de
   qr_status s = stage_input(text2b, words, padded, st, &d);
   if (s != QR_OK) return s;
   s = quadrank_build_device(d, n, device, st, out);
-  cudaFreeAsync(d, st);
+  const cudaError_t fe = free_staged(d, st);
   if (s == QR_OK) {
-    cudaError_t e = cudaStreamSynchronize(st);
+    cudaError_t e = fe ? fe : cudaStreamSynchronize(st);
     if (e) { qr_free(*out); *out = nullptr; return cuda_fail(e, "qr_quadrank_build"); }
   }
   return s;
@@ -460,9 +471,9 @@ QR_EXPORT qr_status qr_build(const uint64_t* text, uint64_t n, int layout, int d
       : b32x2 ? birank32x2_build_device(d, n, device, st, out)
       : q16x2 ? quadrank16x2_build_device(d, n, device, st, out)
       : bits ? birank64x2_build_device(d, n, device, st, out) : quadrank64_build_device(d, n, device, st, out);
-  cudaFreeAsync(d, st);
+  const cudaError_t fe = free_staged(d, st);
   if (s == QR_OK) {
-    cudaError_t e = cudaStreamSynchronize(st);
+    cudaError_t e = fe ? fe : cudaStreamSynchronize(st);
     if (e) { qr_free(*out); *out = nullptr; return cuda_fail(e, "qr_build"); }
   }
   return s;
@@ -591,15 +602,15 @@ QR_EXPORT qr_status qr_fm_build_opts(const uint64_t* text2b, uint64_t n, const u
   uint32_t* dsa = nullptr;
   if (sa_or_null) {
     cudaError_t e;
-    if ((e = cudaMallocAsync((void**)&dsa, (n + 1) * 4, st))) { cudaFreeAsync(d, st); return cuda_fail(e, "alloc sa"); }
+    if ((e = cudaMalloc((void**)&dsa, (n + 1) * 4))) { free_staged(d, st); return cuda_fail(e, "alloc sa"); }
     if ((e = cudaMemcpyAsync(dsa, sa_or_null, (n + 1) * 4, cudaMemcpyDefault, st))) {
-      cudaFreeAsync(d, st); cudaFreeAsync(dsa, st); return cuda_fail(e, "copy sa");
+      free_staged(d, st); free_staged(dsa, st); return cuda_fail(e, "copy sa");
     }
   }
   s = fm_build_device(d, n, dsa, device, st, out, kmer_k, bwt_layout);
-  cudaFreeAsync(d, st);
-  if (dsa) cudaFreeAsync(dsa, st);
-  const cudaError_t e = cudaStreamSynchronize(st);
+  cudaError_t e = free_staged(d, st);
+  free_staged(dsa, st);
+  if (!e) e = cudaStreamSynchronize(st);
   if (s == QR_OK && e) { qr_fm_free(*out); *out = nullptr; return cuda_fail(e, "qr_fm_build"); }
   return s;
 }

@@ -170,7 +170,10 @@ static int bits_for(uint64_t x) {  // bits needed to represent values 0..x
   return b ? b : 1;
 }
 
-// d_sa: N u32 outputs.  Temporaries are stream-ordered allocations.
+// d_sa: N u32 outputs.  The temporaries (40 B per suffix + the sort's scratch) are one
+// cudaMalloc arena: the stream-ordered pool maps and unmaps large blocks ~50x slower (43 GB:
+// 0.27 s to map and 0.26-1.2 s to release vs 0.004 / 0.01 s, profiles/r01_alloc_probe.jsonl).
+// The caller's stream is synchronised every round (survivor count) and before the free.
 static qr_status build_sa(const uint64_t* d_text, uint64_t n, int sms, cudaStream_t st, uint32_t* d_sa) {
   const uint64_t N = n + 1;
   uint64_t *ka = nullptr, *kb = nullptr;
@@ -178,25 +181,14 @@ static qr_status build_sa(const uint64_t* d_text, uint64_t n, int sms, cudaStrea
   unsigned long long* count = nullptr;
   unsigned long long* h_count = nullptr;
   void* tmp = nullptr;
+  char* arena = nullptr;
   size_t tmp_bytes = 0;
   cudaError_t e;
   auto cleanup = [&]() {
-    cudaFreeAsync(ka, st); cudaFreeAsync(kb, st); cudaFreeAsync(va, st); cudaFreeAsync(vb, st);
-    cudaFreeAsync(rank, st); cudaFreeAsync(gs, st); cudaFreeAsync(pa, st); cudaFreeAsync(pb, st);
-    cudaFreeAsync(count, st); cudaFreeAsync(tmp, st);
+    if (arena) { cudaStreamSynchronize(st); cudaFree(arena); }
     if (h_count) cudaFreeHost(h_count);
   };
   auto bail = [&](cudaError_t err, const char* what) { cleanup(); return cuda_fail(err, what); };
-  if ((e = cudaMallocAsync((void**)&ka, N * 8, st))) return bail(e, "sa keys");
-  if ((e = cudaMallocAsync((void**)&kb, N * 8, st))) return bail(e, "sa keys");
-  if ((e = cudaMallocAsync((void**)&va, N * 4, st))) return bail(e, "sa vals");
-  if ((e = cudaMallocAsync((void**)&vb, N * 4, st))) return bail(e, "sa vals");
-  if ((e = cudaMallocAsync((void**)&rank, N * 4, st))) return bail(e, "sa rank");
-  if ((e = cudaMallocAsync((void**)&gs, N * 4, st))) return bail(e, "sa group starts");
-  if ((e = cudaMallocAsync((void**)&pa, N * 4, st))) return bail(e, "sa positions");
-  if ((e = cudaMallocAsync((void**)&pb, N * 4, st))) return bail(e, "sa positions");
-  if ((e = cudaMallocAsync((void**)&count, 8, st))) return bail(e, "sa count");
-  if ((e = cudaMallocHost((void**)&h_count, 8))) return bail(e, "sa host count");
   {
     size_t need = 0, need2 = 0, need3 = 0;
     cub::DoubleBuffer<uint64_t> K(ka, kb);
@@ -207,7 +199,19 @@ static qr_status build_sa(const uint64_t* d_text, uint64_t n, int sms, cudaStrea
     tmp_bytes = need > need2 ? need : need2;
     tmp_bytes = tmp_bytes > need3 ? tmp_bytes : need3;
   }
-  if ((e = cudaMallocAsync(&tmp, tmp_bytes, st))) return bail(e, "sa tmp");
+  const size_t u32N = (N * 4 + 255) & ~(size_t)255, u64N = (N * 8 + 255) & ~(size_t)255;
+  const size_t arena_bytes = 2 * u64N + 6 * u32N + 256 + ((tmp_bytes + 255) & ~(size_t)255);
+  if ((e = cudaMalloc((void**)&arena, arena_bytes))) { arena = nullptr; return bail(e, "sa scratch"); }
+  if ((e = cudaMallocHost((void**)&h_count, 8))) return bail(e, "sa host count");
+  {
+    char* p = arena;
+    ka = reinterpret_cast<uint64_t*>(p); p += u64N;
+    kb = reinterpret_cast<uint64_t*>(p); p += u64N;
+    uint32_t** u32s[6] = {&va, &vb, &rank, &gs, &pa, &pb};
+    for (auto q : u32s) { *q = reinterpret_cast<uint32_t*>(p); p += u32N; }
+    count = reinterpret_cast<unsigned long long*>(p); p += 256;
+    tmp = p;
+  }
   const int b = bits_for(N);
   auto grid = [&](uint64_t items) { return grid_stride_blocks(items, 256, sms, 16); };
   // round 0: every suffix active, keyed by its first 21 characters
@@ -1056,22 +1060,28 @@ qr_status fm_build_device(const uint64_t* d_text, uint64_t n, const uint32_t* d_
   unsigned long long h_aux[5];
   qr_fm* fm = new (std::nothrow) qr_fm();
   if (!fm) return fail(QR_ENOMEM, "qr_fm_build: host allocation");
+  // build temporaries: plain cudaMalloc (see build_sa), freed after the stream is drained
+  auto release = [&]() {
+    cudaStreamSynchronize(st);
+    cudaFree(d_sa); cudaFree(d_bwt); cudaFree(d_aux);
+    d_sa = nullptr; d_bwt = nullptr; d_aux = nullptr;
+  };
   auto bail = [&](qr_status s) {
-    cudaFreeAsync(d_sa, st); cudaFreeAsync(d_bwt, st); cudaFreeAsync(d_aux, st);
+    release();
     qr_fm_free(fm);
     return s;
   };
   const uint64_t L = N / QD_B + 1;
   const uint64_t Lx = N / Q16X2_B + 1;
   const uint64_t bwt_words = 7 * L > 6 * Lx ? 7 * L : 6 * Lx;   // words the QuadRank16 / 16x2 builders read
-  if ((e = cudaMallocAsync((void**)&d_aux, 5 * 8, st))) return bail(cuda_fail(e, "alloc aux"));
+  if ((e = cudaMalloc((void**)&d_aux, 5 * 8))) return bail(cuda_fail(e, "alloc aux"));
   cudaMemsetAsync(d_aux, 0, 5 * 8, st);
   if (!d_sa_given) {
-    if ((e = cudaMallocAsync((void**)&d_sa, N * 4, st))) return bail(cuda_fail(e, "alloc sa"));
+    if ((e = cudaMalloc((void**)&d_sa, N * 4))) return bail(cuda_fail(e, "alloc sa"));
     qr_status s = build_sa(d_text, n, sms, st, d_sa);
     if (s != QR_OK) return bail(s);
   }
-  if ((e = cudaMallocAsync((void**)&d_bwt, bwt_words * 8, st))) return bail(cuda_fail(e, "alloc bwt"));
+  if ((e = cudaMalloc((void**)&d_bwt, bwt_words * 8))) return bail(cuda_fail(e, "alloc bwt"));
   cudaMemsetAsync(d_bwt, 0, bwt_words * 8, st);
   k_bwt<<<grid_stride_blocks((N + 31) / 32, 256, sms, 16), 256, 0, st>>>(d_text, d_sa_given ? d_sa_given : d_sa, N,
                                                                           d_bwt, d_aux);
@@ -1103,10 +1113,8 @@ qr_status fm_build_device(const uint64_t* d_text, uint64_t n, const uint32_t* d_
     else      k_kmer_table<0><<<(unsigned)((ne + 255) / 256), 256, 0, st>>>(F, fm->kmer);
   }
   if ((e = cudaGetLastError())) return bail(cuda_fail(e, "k_kmer_table"));
-  cudaFreeAsync(d_sa, st);
-  cudaFreeAsync(d_bwt, st);
-  cudaFreeAsync(d_aux, st);
-  if ((e = cudaStreamSynchronize(st))) { qr_fm_free(fm); return cuda_fail(e, "fm build"); }
+  if ((e = cudaStreamSynchronize(st))) { release(); qr_fm_free(fm); return cuda_fail(e, "fm build"); }
+  release();
   *out = fm;
   return QR_OK;
 }
