@@ -34,6 +34,8 @@ def test_config2_birank_full(cuda, p, seed):
     gen.bits_dev(seed, n, p, bits)
     h = qr.qr_birank_build(bits, n)
     del bits
+    # byte accounting (SURVEY §8(a) a3 from P:396-441): 34,636,834 lines + 270,601 superblocks
+    assert (h.line_bytes, h.super_bytes) == (2_216_757_376, 1_082_404)
     q = torch.empty(m, dtype=torch.uint64, device=cuda)
     gen.queries_dev(2, n, m, q)
     out = torch.empty_like(q)
@@ -65,6 +67,8 @@ def test_config3_quadrank_full(cuda):
     gen.dna_dev(3, n, 0, txt)
     h = qr.qr_quadrank_build(txt, n)
     del txt
+    # byte accounting (SURVEY §8(a) a3 from P:507-539): 19,173,962 lines + 74,899 superblocks
+    assert (h.line_bytes, h.super_bytes) == (1_227_133_568, 1_198_384)
     q = torch.empty(m, dtype=torch.uint64, device=cuda)
     c = torch.empty(m, dtype=torch.uint8, device=cuda)
     gen.queries_dev(3, n, m, q, c)
@@ -104,11 +108,13 @@ def _splitmix_np(seed, tag, idx):
         return z ^ (z >> np.uint64(31))
 
 
-def _fm_full(cuda, n, kind, m, L, seed, nsample):
+def _fm_full(cuda, n, kind, m, L, seed, nsample, bwt_bytes=None):
     torch = _torch()
     txt = torch.empty((n + 31) // 32 + 1, dtype=torch.uint64, device=cuda)
     gen.dna_dev(seed, n, kind, txt)
     fm = qr.qr_fm_build(txt, n)
+    if bwt_bytes is not None:                              # QuadRank over the n+1 BWT symbols
+        assert (fm.bwt.line_bytes, fm.bwt.super_bytes) == bwt_bytes
     pats = torch.empty(m * L, dtype=torch.uint8, device=cuda)
     gen.patterns_dev(seed, 0 if kind == 0 else 1, m, L, txt, n, pats)
     out = torch.empty(m, dtype=torch.int32, device=cuda)
@@ -130,13 +136,13 @@ def _fm_full(cuda, n, kind, m, L, seed, nsample):
 
 def test_config4_quadfm_full(cuda):
     n, m, L = 1 << 26, 10**7, 32
-    counts = _fm_full(cuda, n, 0, m, L, 4, 256)
+    counts = _fm_full(cuda, n, 0, m, L, 4, 256, bwt_bytes=(19_174_016, 18_736))
     assert counts[0::2].min() >= 1                        # every exact substring occurs (all 5e6)
 
 
 def test_config5_quadfm_full(cuda):
     n, m, L = 1 << 30, 10**8, 100
-    counts = _fm_full(cuda, n, 1, m, L, 5, 48)
+    counts = _fm_full(cuda, n, 1, m, L, 5, 48, bwt_bytes=(306_783_424, 299_600))
     # patterns drawn with 0 substitutions are exact substrings: count >= 1 (all of them)
     s = (_splitmix_np(5, 11, np.arange(m)) >= np.uint64(0x5555555555555556)).astype(np.int8)
     assert counts[s == 0].min() >= 1
