@@ -82,3 +82,54 @@ def broadcast_index(h, n: int, layout: int, dist, device, src: int = 0):
     if rank == src:
         return h
     return qr_import_layout(lines, sup if sb else None, n, layout, device=device.index if hasattr(device, "index") else 0)
+
+
+def gpu_local_cpus(device: int = 0) -> dict:
+    """CPUs and NUMA node local to a GPU's PCI device (sysfs), intersected with the CPUs this
+    process may run on.  Pinned host buffers allocated while running there land on the GPU's
+    node, so host<->device copies do not cross the socket interconnect."""
+    import torch
+
+    p = torch.cuda.get_device_properties(device)
+    bus = f"{p.pci_domain_id:04x}:{p.pci_bus_id:02x}:{p.pci_device_id:02x}.0"
+    base = f"/sys/bus/pci/devices/{bus}"
+    cpus, node = set(), -1
+    try:
+        with open(f"{base}/local_cpulist") as f:
+            for part in f.read().strip().split(","):
+                if "-" in part:
+                    a, b = part.split("-")
+                    cpus.update(range(int(a), int(b) + 1))
+                elif part:
+                    cpus.add(int(part))
+        with open(f"{base}/numa_node") as f:
+            node = int(f.read().strip())
+    except OSError:
+        pass
+    import os
+
+    cpus &= set(os.sched_getaffinity(0))
+    return {"pci": bus, "numa_node": node, "cpus": sorted(cpus)}
+
+
+class on_gpu_local_cpus:
+    """Context manager: run the block on the GPU-local CPUs (e.g. while allocating pinned host
+    memory), then restore the previous affinity.  A no-op when sysfs has no locality data."""
+
+    def __init__(self, device: int = 0):
+        self.device = device
+
+    def __enter__(self):
+        import os
+
+        self.prev = os.sched_getaffinity(0)
+        self.info = gpu_local_cpus(self.device)
+        if self.info["cpus"] and len(self.info["cpus"]) < len(self.prev):
+            os.sched_setaffinity(0, self.info["cpus"])
+        return self.info
+
+    def __exit__(self, *exc):
+        import os
+
+        os.sched_setaffinity(0, self.prev)
+        return False
