@@ -174,7 +174,7 @@ class Ctx:
         return self.max_over_ranks(ms)
 
 
-from paper_2602_04103_b200.multigpu import shard  # noqa: E402  (contiguous shard of a global index range)
+from paper_2602_04103_b200.multigpu import on_gpu_local_cpus, shard  # noqa: E402  (contiguous shard of a global index range)
 
 
 # ------------------------------------------------------------------ rows
@@ -220,9 +220,10 @@ def bench_birank(ctx, p: float, steps, warmup, with_ceiling: bool, clocks=None, 
         # the full per-GPU batch from pinned host memory at N = 1; at N > 1 each rank stages
         # M2 / N queries so that the box pins ~16 GB in total, not 16 GB per GPU
         me = M2 if ctx.world == 1 else max(10**8, M2 // ctx.world)
-        qh = torch.empty(me, dtype=torch.uint64).pin_memory()
+        with on_gpu_local_cpus(ctx.dev.index or 0):     # pinned pages on the GPU's NUMA node
+            qh = torch.empty(me, dtype=torch.uint64).pin_memory()
+            oh = torch.empty(me, dtype=torch.uint64).pin_memory()
         qh.copy_(q[:me])
-        oh = torch.empty(me, dtype=torch.uint64).pin_memory()
 
         def call():
             qr.qr_rank(h, qh, None, oh, me, ctx.stream)

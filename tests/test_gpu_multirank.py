@@ -71,3 +71,18 @@ def test_broadcast_replication_and_sharding(cuda, layout):
         ref = oracle.DnaOracle(gen.dna(61, n), n).rank(allq, allc)
     got = np.concatenate([np.frombuffer(r[1], np.uint64) for r in res])
     assert np.array_equal(got, ref)
+
+
+def test_gpu_local_cpus_and_affinity_restore(cuda):
+    """The NUMA helper returns CPUs this process may use and always restores the affinity."""
+    import os
+
+    from paper_2602_04103_b200.multigpu import gpu_local_cpus, on_gpu_local_cpus
+
+    before = os.sched_getaffinity(0)
+    info = gpu_local_cpus(0)
+    assert set(info["cpus"]) <= before and info["pci"].count(":") == 2
+    with on_gpu_local_cpus(0) as inf:
+        assert os.sched_getaffinity(0) <= before
+        assert inf["pci"] == info["pci"]
+    assert os.sched_getaffinity(0) == before
