@@ -45,6 +45,7 @@ def lib():
             "or_sa_count": [u8p, C.c_uint64, u32p, u8p, u64p, u32p, C.c_uint64, u32p],
             "or_scan_count": [u8p, C.c_uint64, u8p, u64p, u32p, C.c_uint64, u32p],
             "or_scan_count_hd1": [u8p, C.c_uint64, u8p, u64p, u32p, C.c_uint64, u32p],
+            "or_scan_count_hdk": [u8p, C.c_uint64, u8p, u64p, u32p, C.c_uint64, C.c_uint32, u32p],
             "or_threads": [],
         }
         for name, args in sig.items():
@@ -193,5 +194,17 @@ def scan_count_hd1(sym: np.ndarray, cat, off, lens) -> np.ndarray:
     lens = np.ascontiguousarray(lens, dtype=np.uint32)
     out = np.empty(lens.size, dtype=np.uint32)
     lib().or_scan_count_hd1(_p(sym, u8p), sym.size, _p(cat, u8p), _p(off, u64p), _p(lens, u32p), lens.size,
+                            _p(out, u32p))
+    return out
+
+
+def scan_count_hdk(sym: np.ndarray, cat, off, lens, k: int) -> np.ndarray:
+    """Positions where each pattern matches with at most k substitutions (direct scan)."""
+    sym = np.ascontiguousarray(sym, dtype=np.uint8)
+    cat = np.ascontiguousarray(cat, dtype=np.uint8)
+    off = np.ascontiguousarray(off, dtype=np.uint64)
+    lens = np.ascontiguousarray(lens, dtype=np.uint32)
+    out = np.empty(lens.size, dtype=np.uint32)
+    lib().or_scan_count_hdk(_p(sym, u8p), sym.size, _p(cat, u8p), _p(off, u64p), _p(lens, u32p), lens.size, int(k),
                             _p(out, u32p))
     return out

@@ -293,4 +293,26 @@ EXPORT void or_scan_count_hd1(const uint8_t* s, uint64_t n, const uint8_t* pat, 
   }
 }
 
+/* Approximate occurrences with up to k substitutions (NEXT §8(f)3 widened beyond one
+ * substitution): the number of text positions i in [0, n-L] where s[i..i+L)
+ * differs from P in at most k symbols (Hamming distance <= k).  Direct scan of every position;
+ * L = 0 counts n+1. */
+EXPORT void or_scan_count_hdk(const uint8_t* s, uint64_t n, const uint8_t* pat, const uint64_t* off,
+                              const uint32_t* len, uint64_t m, uint32_t k, uint32_t* out) {
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int64_t t = 0; t < (int64_t)m; ++t) {
+    const uint8_t* P = pat + off[t];
+    uint32_t L = len[t];
+    uint64_t cnt = 0;
+    if (L == 0) cnt = n + 1;
+    else if (L <= n)
+      for (uint64_t i = 0; i + L <= n; ++i) {
+        uint32_t mism = 0;
+        for (uint32_t j = 0; j < L && mism <= k; ++j) mism += (s[i + j] != P[j]);
+        cnt += (mism <= k);
+      }
+    out[t] = (uint32_t)cnt;
+  }
+}
+
 EXPORT int or_threads(void) { return omp_get_max_threads(); }

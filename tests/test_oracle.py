@@ -293,3 +293,40 @@ def test_hd1_scan_vs_bruteforce_and_variant_sum():
                               for j in range(L) for d in (1, 2, 3)]
             vc, vo, vl = oracle.pack_patterns(variants)
             assert int(f.count(vc, vo, vl).astype(np.int64).sum()) == g
+
+
+def test_hdk_scan_pins():
+    """<=k-substitution counts (k = 0..3): Python brute force on tiny texts; k = 0 and 1 agree
+    with the exact scan and the <=1 scan; k >= L counts every position; and the identity
+    count_hdk(P) = sum of the exact counts (backward search over the simple BWT) of every string
+    within Hamming distance k of P, enumerated over all 4^L strings for L <= 5."""
+    import itertools
+
+    rng = np.random.default_rng(31)
+    for t in range(10):
+        n = int(rng.integers(1, 260))
+        sym = rng.integers(0, 4, n).astype(np.uint8) if t % 2 else np.tile(rng.integers(0, 4, 3), 100)[:n].astype(np.uint8)
+        f = oracle.FmOracle(sym)
+        pats = [rng.integers(0, 4, int(rng.integers(0, 9))).astype(np.uint8) for _ in range(14)]
+        pats += [sym[a:a + 5].copy() for a in rng.integers(0, n, 6)]
+        cat, off, lens = oracle.pack_patterns(pats)
+        by_k = {k: oracle.scan_count_hdk(sym, cat, off, lens, k) for k in range(4)}
+        assert np.array_equal(by_k[0], oracle.scan_count(sym, cat, off, lens))
+        assert np.array_equal(by_k[1], oracle.scan_count_hd1(sym, cat, off, lens))
+        for i, p in enumerate(pats):
+            L = len(p)
+            for k in range(4):
+                g = int(by_k[k][i])
+                if L == 0:
+                    assert g == n + 1
+                    continue
+                brute = sum(1 for a in range(n - L + 1) if int((sym[a:a + L] != p).sum()) <= k)
+                assert g == brute
+                if k >= L:
+                    assert g == max(0, n - L + 1)
+                if k >= 2 and L <= 5:
+                    near = [np.array(v, np.uint8) for v in itertools.product(range(4), repeat=L)
+                            if sum(int(a != b) for a, b in zip(v, p)) <= k]
+                    vc, vo, vl = oracle.pack_patterns(near)
+                    assert int(f.count(vc, vo, vl).astype(np.int64).sum()) == g
+            assert all(by_k[k][i] <= by_k[k + 1][i] for k in range(3))
