@@ -170,9 +170,11 @@ qr_status qr_fm_count_both(const qr_fm* fm, const uint8_t* patterns, const uint3
 
 /* Approximate counting (NEXT §8(f)3; rank_4's motivation): out[k] = number of
  * text positions where pattern k matches with at most max_mismatches substitutions (Hamming
- * distance; 0 or 1 — QR_EINVAL otherwise).  max_mismatches = 1 branches on every pattern
- * position with one rank_4 at lo and one at hi (the four extensions of the exact interval) and
- * reads the 24 single-substitution variants of the last 8 symbols from the 8-mer table.
+ * distance; 0..3 — QR_EINVAL otherwise; 0 is qr_fm_count).  max_mismatches = 1 branches on
+ * every pattern position with one rank_4 at lo and one at hi (the four extensions of the exact
+ * interval) and reads the 3K single-substitution variants of the last K symbols from the k-mer
+ * table.  2 and 3 backtrack from the full interval with rank_4 at every node (one frame per
+ * mismatch level, no seeding); their work grows steeply with the pattern length and k.
  * Arguments and memory spaces as qr_fm_count. */
 qr_status qr_fm_count_approx(const qr_fm* fm, const uint8_t* patterns, const uint32_t* lengths, uint32_t fixed_len,
                              uint32_t max_mismatches, uint32_t* out, uint64_t m, void* stream);

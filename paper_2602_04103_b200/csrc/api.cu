@@ -668,7 +668,7 @@ QR_EXPORT qr_status qr_fm_count(const qr_fm* fm, const uint8_t* patterns, const 
 QR_EXPORT qr_status qr_fm_count_approx(const qr_fm* fm, const uint8_t* patterns, const uint32_t* lengths,
                                        uint32_t fixed_len, uint32_t max_mismatches, uint32_t* out, uint64_t m,
                                        void* stream) {
-  if (max_mismatches > 1) return fail(QR_EINVAL, "qr_fm_count_approx: max_mismatches must be 0 or 1");
+  if (max_mismatches > 3) return fail(QR_EINVAL, "qr_fm_count_approx: max_mismatches must be 0..3");
   return fm_count_impl(fm, patterns, lengths, fixed_len, out, nullptr, m, nullptr, stream, (int)max_mismatches);
 }
 

@@ -830,6 +830,72 @@ __global__ void __launch_bounds__(256) k_fm_approx1(FmParams F, const uint8_t* _
   }
 }
 
+// ---- approximate counting with <= KMAX substitutions, KMAX = 2, 3 ---------------------------
+// Backtracking over the BWT with rank_4 at every node: a node is an interval
+// [lo, hi) after the pattern's last symbols with mm substitutions so far; one rank_4 at lo and
+// one at hi give all four children, the child on the pattern's symbol keeps mm and the other
+// three (when mm < KMAX) are new nodes with mm + 1.  The search keeps one frame per mismatch
+// level: frame f walks the exact path of its node and, at each position, first descends into
+// the mismatched children (frame f + 1) before stepping on, so the state is KMAX + 1 frames
+// whatever the pattern length.  Frames at mm = KMAX finish as plain exact searches.  No k-mer
+// seeding: a substitution may fall inside the seed, and the table's intervals cannot be extended
+// from an arbitrary node.  Leaves are distinct strings, so their interval sizes add up to the
+// number of text positions within Hamming distance KMAX.
+template <bool FIXED, int BW, int KMAX>
+__global__ void __launch_bounds__(256) k_fm_approxk(FmParams F, const uint8_t* __restrict__ pat,
+                                                    const uint64_t* __restrict__ offs,
+                                                    const uint32_t* __restrict__ lens, uint32_t fixed_len,
+                                                    uint32_t* __restrict__ out, uint64_t m,
+                                                    unsigned long long* __restrict__ ctr) {
+  constexpr uint32_t UNX = 8;   // not 4: a frame whose branches are all tried has fd = 4
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  const uint4 C4 = __ldg(reinterpret_cast<const uint4*>(F.Ct));
+  const uint32_t Cs[4] = {C4.x, C4.y, C4.z, C4.w};
+  for (uint64_t pi = ctr ? approx_next(ctr, 0, 0) : blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; pi < m;
+       pi = approx_next(ctr, pi, stride)) {
+    const uint32_t len = FIXED ? fixed_len : lens[pi];
+    const uint8_t* p = pat + (FIXED ? pi * (uint64_t)fixed_len : offs[pi]);
+    PatWindow P;
+    P.reset(p);
+    uint32_t flo[KMAX + 1], fhi[KMAX + 1], fpos[KMAX + 1], fd[KMAX + 1];   // fd: next branch symbol, UNX = unexpanded
+    uint32_t clo[KMAX][4], chi[KMAX][4];                                   // children of frames 0 .. KMAX-1
+    uint64_t total = 0;
+    int f = 0;
+    flo[0] = 0; fhi[0] = (uint32_t)F.N; fpos[0] = len; fd[0] = UNX;
+    while (f >= 0) {
+      if (fd[f] == UNX) {
+        if (flo[f] >= fhi[f]) { --f; continue; }
+        if (fpos[f] == 0) { total += fhi[f] - flo[f]; --f; continue; }
+        if (f == KMAX) {                                   // no substitution left: exact search
+          total += fm_continue<BW>(F, P, (int64_t)fpos[f] - 1, flo[f], fhi[f]);
+          --f;
+          continue;
+        }
+        uint32_t ol[4], oh[4];
+        if (BW == 1) { fm_occ4_x2(F, flo[f], ol); fm_occ4_x2(F, fhi[f], oh); }
+        else         { fm_occ4(F, flo[f], ol); fm_occ4(F, fhi[f], oh); }
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          clo[f][c] = Cs[c] + ol[c];
+          chi[f][c] = Cs[c] + oh[c];
+        }
+        fd[f] = 0;
+      }
+      const uint32_t pc = P.at((int64_t)fpos[f] - 1);
+      uint32_t d = fd[f];
+      while (d < 4 && (d == pc || clo[f][d] >= chi[f][d])) ++d;
+      if (d < 4) {                                         // descend into the substitution d
+        fd[f] = d + 1;
+        flo[f + 1] = clo[f][d]; fhi[f + 1] = chi[f][d]; fpos[f + 1] = fpos[f] - 1; fd[f + 1] = UNX;
+        ++f;
+        continue;
+      }
+      flo[f] = clo[f][pc]; fhi[f] = chi[f][pc]; fpos[f] -= 1; fd[f] = UNX;   // step on the pattern's symbol
+    }
+    out[pi] = (uint32_t)total;
+  }
+}
+
 __global__ void k_u32_to_u64(const uint32_t* __restrict__ a, uint64_t* __restrict__ b, uint64_t m) {
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m; i += (uint64_t)gridDim.x * blockDim.x)
     b[i] = a[i];
@@ -991,8 +1057,10 @@ static cudaError_t launch_fm(const qr_fm* fm, bool lean, unsigned g, cudaStream_
 template <bool FIXED>
 static cudaError_t launch_approx(const qr_fm* fm, unsigned g, cudaStream_t st, const FmParams& F, const uint8_t* pat,
                                  const uint64_t* offs, const uint32_t* lens, uint32_t fixed_len, uint32_t* out,
-                                 uint64_t m) {
-  auto kern = F.bw ? k_fm_approx1<FIXED, 1> : k_fm_approx1<FIXED, 0>;
+                                 uint64_t m, int kmax) {
+  auto kern = kmax == 1 ? (F.bw ? k_fm_approx1<FIXED, 1> : k_fm_approx1<FIXED, 0>)
+            : kmax == 2 ? (F.bw ? k_fm_approxk<FIXED, 1, 2> : k_fm_approxk<FIXED, 0, 2>)
+                        : (F.bw ? k_fm_approxk<FIXED, 1, 3> : k_fm_approxk<FIXED, 0, 3>);
   if (!g_fm_dyn) {
     kern<<<g, 256, 0, st>>>(F, pat, offs, lens, fixed_len, out, m, nullptr);
     return cudaGetLastError();
@@ -1023,7 +1091,7 @@ qr_status fm_count_device(const qr_fm* fm, const uint8_t* pat, const uint32_t* l
   unsigned long long* w = reinterpret_cast<unsigned long long*>(work);
   cudaError_t e;
   if (!lengths) {
-    if (approx) e = launch_approx<true>(fm, g, st, F, pat, nullptr, nullptr, fixed_len, out, m);
+    if (approx) e = launch_approx<true>(fm, g, st, F, pat, nullptr, nullptr, fixed_len, out, m, approx);
     else if (work) e = launch_fm<true, true>(fm, use_lean(fm), g, st, F, pat, nullptr, nullptr, fixed_len, out, out_rc, m, w);
     else      e = launch_fm<true, false>(fm, use_lean(fm), g, st, F, pat, nullptr, nullptr, fixed_len, out, out_rc, m, w);
     if (e) return cuda_fail(e, "k_fm_count");
@@ -1039,7 +1107,7 @@ qr_status fm_count_device(const qr_fm* fm, const uint8_t* pat, const uint32_t* l
   if ((e = cub::DeviceScan::ExclusiveSum(tmp, tb, offs, offs, (int64_t)m, st))) {
     cudaFreeAsync(offs, st); cudaFreeAsync(tmp, st); return cuda_fail(e, "scan");
   }
-  if (approx) e = launch_approx<false>(fm, g, st, F, pat, offs, lengths, 0, out, m);
+  if (approx) e = launch_approx<false>(fm, g, st, F, pat, offs, lengths, 0, out, m, approx);
   else if (work) e = launch_fm<false, true>(fm, use_lean(fm), g, st, F, pat, offs, lengths, 0, out, out_rc, m, w);
   else      e = launch_fm<false, false>(fm, use_lean(fm), g, st, F, pat, offs, lengths, 0, out, out_rc, m, w);
   cudaFreeAsync(offs, st);

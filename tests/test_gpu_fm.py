@@ -354,7 +354,7 @@ def test_fm_count_approx_one_mismatch(cuda, n, kind, dyn, fm_dyn_reset):
     qr.qr_sync()
     assert np.array_equal(h, oracle.scan_count_hd1(sym, fx, np.arange(m, dtype=np.uint64) * L, np.full(m, L, np.uint32)))
     with pytest.raises(qr.QrError):
-        qr.qr_fm_count_approx(fm, fx, None, L, 2, h, m)
+        qr.qr_fm_count_approx(fm, fx, None, L, 4, h, m)
 
 
 def test_cli_fm_count(cuda, tmp_path):
@@ -544,3 +544,64 @@ def test_fm_over_quadrank16x2(cuda, n, kind, dyn, fm_dyn_reset):
         torch.cuda.synchronize()
         assert np.array_equal(to_host(dw).view(np.uint32),
                               ora.count(fx, np.arange(m, dtype=np.uint64) * L, np.full(m, L, np.uint32)))
+
+
+@pytest.mark.parametrize("kmax", [2, 3])
+@pytest.mark.parametrize("bwt_layout", [None, qr.QR_LAYOUT_QUADRANK16X2])
+@pytest.mark.parametrize("dyn", [0, 1])
+@pytest.mark.parametrize("n,kind", [(1, 0), (40, 0), (3000, 0), (50000, 1), (131072 + 9, 0)])
+def test_fm_count_approx_k_mismatches(cuda, n, kind, dyn, bwt_layout, kmax, fm_dyn_reset):
+    """<=2 and <=3-substitution counts (rank_4 backtracking, one frame per mismatch level) vs the
+    oracle's direct Hamming-distance scan, variable and fixed lengths, device and host pointers,
+    both BWT layouts, static and dynamic pattern order; monotone in k."""
+    torch = _torch()
+    qr.qr_set_tuning("fm_dyn", dyn)
+    w = gen.dna(91 + n, n, kind)
+    sym = gen.unpack_dna(w, n)
+    fm = qr.qr_fm_build(w, n, bwt_layout=bwt_layout)
+    rng = np.random.default_rng(n + kmax)
+    pats = []
+    for i in range(400):
+        L = int(rng.integers(0, 13)) if i % 4 == 0 else int(rng.integers(1, 28))
+        if i % 2 and n >= L:                               # substring with 0..4 substitutions
+            a = int(rng.integers(0, max(1, n - L + 1)))
+            p = sym[a:a + L].copy()
+            for _s in range(int(rng.integers(0, 5))):
+                if p.size:
+                    k = int(rng.integers(0, p.size)); p[k] = (p[k] + 1 + rng.integers(0, 3)) % 4
+        else:
+            p = rng.integers(0, 4, L).astype(np.uint8)
+        pats.append(p)
+    pats.append(sym.copy())
+    pats.append(np.concatenate([sym, sym[:2]]))
+    cat, off, lens = oracle.pack_patterns(pats)
+    ref = oracle.scan_count_hdk(sym, cat, off, lens, kmax)
+    d = torch.empty(lens.size, dtype=torch.int32, device=cuda)
+    qr.qr_fm_count_approx(fm, to_dev(cat, cuda), to_dev(lens, cuda), 0, kmax, d, lens.size)
+    torch.cuda.synchronize()
+    got = to_host(d).view(np.uint32)
+    bad = np.nonzero(got != ref)[0]
+    assert bad.size == 0, f"{bad.size} mismatches: {[(len(pats[i]), got[i], ref[i]) for i in bad[:5]]}"
+    assert np.all(ref >= oracle.scan_count_hdk(sym, cat, off, lens, kmax - 1))
+    # fixed length, host pointers (staged path)
+    L, m = 20, 300
+    fx = np.concatenate([sym[a:a + L] if n >= L else rng.integers(0, 4, L).astype(np.uint8)
+                         for a in rng.integers(0, max(1, n - L + 1), m)]).astype(np.uint8)
+    if fx.size < m * L:
+        fx = np.resize(fx, m * L)
+    foff = np.arange(m, dtype=np.uint64) * L
+    fref = oracle.scan_count_hdk(sym, fx, foff, np.full(m, L, np.uint32), kmax)
+    h = np.zeros(m, np.uint32)
+    qr.qr_fm_count_approx(fm, fx, None, L, kmax, h, m)
+    qr.qr_sync()
+    assert np.array_equal(h, fref)
+
+
+def test_fm_count_approx_rejects_k_above_3(cuda):
+    torch = _torch()
+    w = gen.dna(5, 1000)
+    fm = qr.qr_fm_build(w, 1000)
+    d = torch.empty(4, dtype=torch.int32, device=cuda)
+    pats = torch.zeros(4 * 8, dtype=torch.uint8, device=cuda)
+    with pytest.raises(qr.QrError):
+        qr.qr_fm_count_approx(fm, pats, None, 8, 4, d, 4)
