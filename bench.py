@@ -362,8 +362,8 @@ def bench_reads(ctx, n, m_total, length, seed, steps, warmup):
             "fm_build_s": round(build_s, 2)}
 
 
-def bench_approx(ctx, n, m_total, length, seed, steps, warmup, bwt_layout=None):
-    """<=1-substitution counting (rank_4-driven, NEXT §8(f)3) on the configs[3] text/patterns."""
+def bench_approx(ctx, n, m_total, length, seed, steps, warmup, bwt_layout=None, kmax=1):
+    """<=kmax-substitution counting (rank_4-driven, NEXT §8(f)3) on the configs[3] text/patterns."""
     import gen
     import paper_2602_04103_b200 as qr
 
@@ -375,11 +375,11 @@ def bench_approx(ctx, n, m_total, length, seed, steps, warmup, bwt_layout=None):
     pats = torch.empty(m * length, dtype=torch.uint8, device=ctx.dev)
     gen.patterns_dev(seed, 0, m, length, text, n, pats, i0=i0)
     out = torch.empty(m, dtype=torch.int32, device=ctx.dev)
-    ms = ctx.timed(lambda: qr.qr_fm_count_approx(fm, pats, None, length, 1, out, m, ctx.stream), steps, warmup)
+    ms = ctx.timed(lambda: qr.qr_fm_count_approx(fm, pats, None, length, kmax, out, m, ctx.stream), steps, warmup)
     fm.free()
     del text, pats, out
     torch.cuda.empty_cache()
-    return {"ms": ms, "patterns_per_s": m_total / ms * 1e3, "max_mismatches": 1, "patterns": m_total,
+    return {"ms": ms, "patterns_per_s": m_total / ms * 1e3, "max_mismatches": kmax, "patterns": m_total,
             "pattern_len": length}
 
 
@@ -567,6 +567,7 @@ def main():
         rows["c4_quadfm_approx1"] = bench_approx(ctx, N4, 10**6, L4, SEED[4], K, W)
         rows["c4_quadfm_approx1_bwt16x2"] = bench_approx(ctx, N4, 10**6, L4, SEED[4], K, W,
                                                          bwt_layout=qr.QR_LAYOUT_QUADRANK16X2)
+        rows["c4_quadfm_approx2"] = bench_approx(ctx, N4, 10**6, L4, SEED[4], K, W, kmax=2)
         rows["layout_variants"] = bench_variants(ctx, K, W)
         rows["latency_mode"] = bench_latency(ctx, K, W)
         rows["c1_small"] = bench_small(ctx, K, W)

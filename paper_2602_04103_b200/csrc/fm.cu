@@ -837,17 +837,68 @@ __global__ void __launch_bounds__(256) k_fm_approx1(FmParams F, const uint8_t* _
 // three (when mm < KMAX) are new nodes with mm + 1.  The search keeps one frame per mismatch
 // level: frame f walks the exact path of its node and, at each position, first descends into
 // the mismatched children (frame f + 1) before stepping on, so the state is KMAX + 1 frames
-// whatever the pattern length.  Frames at mm = KMAX finish as plain exact searches.  No k-mer
-// seeding: a substitution may fall inside the seed, and the table's intervals cannot be extended
-// from an arbitrary node.  Leaves are distinct strings, so their interval sizes add up to the
-// number of text positions within Hamming distance KMAX.
+// whatever the pattern length.  Frames at mm = KMAX finish as plain exact searches.  Leaves are
+// distinct strings, so their interval sizes add up to the number of text positions within
+// Hamming distance KMAX.
+//
+// Seeding: the first K levels of the tree (the pattern's last K symbols) are not expanded node
+// by node; every K-mer within distance KMAX of the pattern's last K symbols is looked up in the
+// k-mer table instead (1 + 3K + 9 C(K,2) [+ 27 C(K,3)] lookups), and the search continues from
+// each non-empty interval with the substitutions it has left.
+template <int BW, int KMAX>
+__device__ __forceinline__ uint64_t fm_backtrack(const FmParams& F, PatWindow& P, const uint32_t (&Cs)[4],
+                                                 uint32_t lo, uint32_t hi, uint32_t pos, int f0) {
+  constexpr uint32_t UNX = 8;   // not 4: a frame whose branches are all tried has fd = 4
+  uint32_t flo[KMAX + 1], fhi[KMAX + 1], fpos[KMAX + 1], fd[KMAX + 1];   // fd: next branch symbol, UNX = unexpanded
+  uint32_t clo[KMAX][4], chi[KMAX][4];                                   // children of frames 0 .. KMAX-1
+  uint64_t total = 0;
+  int f = f0;
+  flo[f] = lo; fhi[f] = hi; fpos[f] = pos; fd[f] = UNX;
+  while (f >= f0) {
+    if (fd[f] == UNX) {
+      if (flo[f] >= fhi[f]) { --f; continue; }
+      if (fpos[f] == 0) { total += fhi[f] - flo[f]; --f; continue; }
+      if (f == KMAX) {                                   // no substitution left: exact search
+        total += fm_continue<BW>(F, P, (int64_t)fpos[f] - 1, flo[f], fhi[f]);
+        --f;
+        continue;
+      }
+      uint32_t ol[4], oh[4];
+      if (BW == 1) { fm_occ4_x2(F, flo[f], ol); fm_occ4_x2(F, fhi[f], oh); }
+      else         { fm_occ4(F, flo[f], ol); fm_occ4(F, fhi[f], oh); }
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        clo[f][c] = Cs[c] + ol[c];
+        chi[f][c] = Cs[c] + oh[c];
+      }
+      fd[f] = 0;
+    }
+    const uint32_t pc = P.at((int64_t)fpos[f] - 1);
+    uint32_t d = fd[f];
+    while (d < 4 && (d == pc || clo[f][d] >= chi[f][d])) ++d;
+    if (d < 4) {                                         // descend into the substitution d
+      fd[f] = d + 1;
+      flo[f + 1] = clo[f][d]; fhi[f + 1] = chi[f][d]; fpos[f + 1] = fpos[f] - 1; fd[f + 1] = UNX;
+      ++f;
+      continue;
+    }
+    flo[f] = clo[f][pc]; fhi[f] = chi[f][pc]; fpos[f] -= 1; fd[f] = UNX;   // step on the pattern's symbol
+  }
+  return total;
+}
+
+// key with the symbol at key position t replaced by (old + r) mod 4, r in 1..3
+__device__ __forceinline__ uint32_t kmer_subst(uint32_t key, int t, uint32_t r) {
+  const uint32_t o = (key >> (2 * t)) & 3u;
+  return key ^ ((o ^ ((o + r) & 3u)) << (2 * t));
+}
+
 template <bool FIXED, int BW, int KMAX>
 __global__ void __launch_bounds__(256) k_fm_approxk(FmParams F, const uint8_t* __restrict__ pat,
                                                     const uint64_t* __restrict__ offs,
                                                     const uint32_t* __restrict__ lens, uint32_t fixed_len,
                                                     uint32_t* __restrict__ out, uint64_t m,
                                                     unsigned long long* __restrict__ ctr) {
-  constexpr uint32_t UNX = 8;   // not 4: a frame whose branches are all tried has fd = 4
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   const uint4 C4 = __ldg(reinterpret_cast<const uint4*>(F.Ct));
   const uint32_t Cs[4] = {C4.x, C4.y, C4.z, C4.w};
@@ -857,40 +908,31 @@ __global__ void __launch_bounds__(256) k_fm_approxk(FmParams F, const uint8_t* _
     const uint8_t* p = pat + (FIXED ? pi * (uint64_t)fixed_len : offs[pi]);
     PatWindow P;
     P.reset(p);
-    uint32_t flo[KMAX + 1], fhi[KMAX + 1], fpos[KMAX + 1], fd[KMAX + 1];   // fd: next branch symbol, UNX = unexpanded
-    uint32_t clo[KMAX][4], chi[KMAX][4];                                   // children of frames 0 .. KMAX-1
     uint64_t total = 0;
-    int f = 0;
-    flo[0] = 0; fhi[0] = (uint32_t)F.N; fpos[0] = len; fd[0] = UNX;
-    while (f >= 0) {
-      if (fd[f] == UNX) {
-        if (flo[f] >= fhi[f]) { --f; continue; }
-        if (fpos[f] == 0) { total += fhi[f] - flo[f]; --f; continue; }
-        if (f == KMAX) {                                   // no substitution left: exact search
-          total += fm_continue<BW>(F, P, (int64_t)fpos[f] - 1, flo[f], fhi[f]);
-          --f;
-          continue;
+    const int K = F.K;
+    if (K && len >= (uint32_t)K) {
+      const uint32_t key0 = kmer_key(K, P, p, len);
+      const uint32_t pos = len - (uint32_t)K;
+      auto seed = [&](uint32_t key, int mm) {
+        const uint2 iv = __ldg(F.kmer + key);
+        if (iv.x < iv.y) total += fm_backtrack<BW, KMAX>(F, P, Cs, iv.x, iv.y, pos, mm);
+      };
+      seed(key0, 0);
+      for (int t1 = 0; t1 < K; ++t1)
+        for (uint32_t r1 = 1; r1 < 4; ++r1) {
+          const uint32_t k1 = kmer_subst(key0, t1, r1);
+          seed(k1, 1);
+          for (int t2 = t1 + 1; t2 < K; ++t2)
+            for (uint32_t r2 = 1; r2 < 4; ++r2) {
+              const uint32_t k2 = kmer_subst(k1, t2, r2);
+              seed(k2, 2);
+              if (KMAX >= 3)
+                for (int t3 = t2 + 1; t3 < K; ++t3)
+                  for (uint32_t r3 = 1; r3 < 4; ++r3) seed(kmer_subst(k2, t3, r3), 3);
+            }
         }
-        uint32_t ol[4], oh[4];
-        if (BW == 1) { fm_occ4_x2(F, flo[f], ol); fm_occ4_x2(F, fhi[f], oh); }
-        else         { fm_occ4(F, flo[f], ol); fm_occ4(F, fhi[f], oh); }
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          clo[f][c] = Cs[c] + ol[c];
-          chi[f][c] = Cs[c] + oh[c];
-        }
-        fd[f] = 0;
-      }
-      const uint32_t pc = P.at((int64_t)fpos[f] - 1);
-      uint32_t d = fd[f];
-      while (d < 4 && (d == pc || clo[f][d] >= chi[f][d])) ++d;
-      if (d < 4) {                                         // descend into the substitution d
-        fd[f] = d + 1;
-        flo[f + 1] = clo[f][d]; fhi[f + 1] = chi[f][d]; fpos[f + 1] = fpos[f] - 1; fd[f + 1] = UNX;
-        ++f;
-        continue;
-      }
-      flo[f] = clo[f][pc]; fhi[f] = chi[f][pc]; fpos[f] -= 1; fd[f] = UNX;   // step on the pattern's symbol
+    } else {
+      total = fm_backtrack<BW, KMAX>(F, P, Cs, 0u, (uint32_t)F.N, len, 0);
     }
     out[pi] = (uint32_t)total;
   }
