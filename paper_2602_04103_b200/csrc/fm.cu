@@ -917,19 +917,32 @@ __global__ void __launch_bounds__(256) k_fm_approxk(FmParams F, const uint8_t* _
         const uint2 iv = __ldg(F.kmer + key);
         if (iv.x < iv.y) total += fm_backtrack<BW, KMAX>(F, P, Cs, iv.x, iv.y, pos, mm);
       };
+      // the seeds with all KMAX substitutions inside the K-mer have none left: their three
+      // variants at the last substituted position are looked up together and continue as one
+      // interleaved exact search (fm_continue3)
+      auto last_level = [&](uint32_t key, int t) {
+        uint2 iv[3];
+#pragma unroll
+        for (uint32_t r = 1; r < 4; ++r) iv[r - 1] = __ldg(F.kmer + kmer_subst(key, t, r));
+        uint32_t vl[3] = {iv[0].x, iv[1].x, iv[2].x}, vh[3] = {iv[0].y, iv[1].y, iv[2].y};
+        total += fm_continue3<BW>(F, P, (int64_t)pos - 1, vl, vh);
+      };
       seed(key0, 0);
       for (int t1 = 0; t1 < K; ++t1)
         for (uint32_t r1 = 1; r1 < 4; ++r1) {
           const uint32_t k1 = kmer_subst(key0, t1, r1);
           seed(k1, 1);
-          for (int t2 = t1 + 1; t2 < K; ++t2)
-            for (uint32_t r2 = 1; r2 < 4; ++r2) {
-              const uint32_t k2 = kmer_subst(k1, t2, r2);
-              seed(k2, 2);
-              if (KMAX >= 3)
-                for (int t3 = t2 + 1; t3 < K; ++t3)
-                  for (uint32_t r3 = 1; r3 < 4; ++r3) seed(kmer_subst(k2, t3, r3), 3);
+          for (int t2 = t1 + 1; t2 < K; ++t2) {
+            if (KMAX == 2) {
+              last_level(k1, t2);
+            } else {
+              for (uint32_t r2 = 1; r2 < 4; ++r2) {
+                const uint32_t k2 = kmer_subst(k1, t2, r2);
+                seed(k2, 2);
+                for (int t3 = t2 + 1; t3 < K; ++t3) last_level(k2, t3);
+              }
             }
+          }
         }
     } else {
       total = fm_backtrack<BW, KMAX>(F, P, Cs, 0u, (uint32_t)F.N, len, 0);
