@@ -1,7 +1,7 @@
 """Command line front end (the SPEC's `quadfm count`, on real files).
 
   python -m paper_2602_04103_b200.cli fm-count --fasta genome.fa --fastq reads.fq \
-         [--both-strands] [--max-mismatches 0|1] [--out counts.tsv]
+         [--both-strands] [--max-mismatches 0-3] [--out counts.tsv]
 
 Builds the QuadFm index of the FASTA records (concatenated in file order; matches spanning
 two records are counted like any other substring) on the GPU and writes one line per read:
@@ -72,7 +72,7 @@ def main(argv=None) -> int:
     f.add_argument("--fasta", required=True)
     f.add_argument("--fastq", required=True)
     f.add_argument("--both-strands", action="store_true")
-    f.add_argument("--max-mismatches", type=int, default=0, choices=[0, 1])
+    f.add_argument("--max-mismatches", type=int, default=0, choices=[0, 1, 2, 3])
     f.add_argument("--replace-invalid", type=int, default=None, help="code for non-ACGT characters (default: reject)")
     f.add_argument("--device", type=int, default=0)
     f.add_argument("--bwt-layout", default="quadrank16", choices=["quadrank16", "quadrank16x2"],
