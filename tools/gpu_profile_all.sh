@@ -9,7 +9,7 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
 echo "ncu launches exit $?" >> gpurun_out/ncu_launches.log
 timeout 300 python tools/profile_driver.py > gpurun_out/prof_plain.log 2>&1 && \
 timeout 2400 ncu --set full --clock-control none --import-source on \
-  -k 'regex:k_(bi_rank|bi_gather|qd_rank|qd_all4|fm_count|b64|q64|fm_approx|b16x2|q16x2)' -c 24 -o /tmp/prof_final -f \
+  -k 'regex:k_(bi_rank|bi_gather|qd_rank|qd_all4|fm_count|b64|q64|fm_approx|b16x2|q16x2)' -c 26 -o /tmp/prof_final -f \
   python tools/profile_driver.py > gpurun_out/ncu_full.log 2>&1
 echo "ncu full exit $?" >> gpurun_out/ncu_full.log
 python tools/ncu_summary.py /tmp/prof_final.ncu-rep > gpurun_out/prof_final_summary.md 2>&1

@@ -2,7 +2,7 @@
 ncu --set full captures (kernel order: bi_rank2c (BiRank16 rank, cluster shared-memory superblocks),
 BiRank16x2 / QuadRank16x2 rank (cluster kernels) after the QuadRank64 rank,
 bi_gather2 x3 (ceiling modes 0-2), bi_rank2c<VAR=3> (ceiling mode 3), qd_rank2c, qd_all4_2c, b64_rank,
-q64_rank, fm_count (c4, lean), fm_count (c5, de-duplicating), fm_count both strands, fm_approx1)."""
+q64_rank, fm_count (c4, lean), fm_count (c5, de-duplicating), fm_count both strands, fm_approx1, fm_approxk k=2)."""
 import os
 import sys
 
@@ -92,5 +92,6 @@ pats = torch.empty(m * 32, dtype=torch.uint8, device=dev)
 gen.patterns_dev(4, 0, m, 32, t, n, pats)
 o = torch.empty(m, dtype=torch.int32, device=dev)
 qr.qr_fm_count_approx(fm, pats, None, 32, 1, o, m, st)
+qr.qr_fm_count_approx(fm, pats, None, 32, 2, o, m, st)
 torch.cuda.synchronize()
 print("profile driver done")
