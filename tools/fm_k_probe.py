@@ -22,7 +22,7 @@ for name, n, kind, m, L, seed, pkind in (("c4", 1 << 26, 0, 10**7, 32, 4, 0), ("
     pats = torch.empty(m * L, dtype=torch.uint8, device=dev)
     gen.patterns_dev(seed, pkind, m, L, text, n, pats)
     ref = None
-    for K in (8, 12, 14):
+    for K in [int(x) for x in (sys.argv[1].split(",") if len(sys.argv) > 1 else ["8", "12", "14"])]:
         t0 = time.perf_counter()
         fm = qr.qr_fm_build(text, n, kmer_k=K)
         bt = time.perf_counter() - t0
@@ -37,7 +37,7 @@ for name, n, kind, m, L, seed, pkind in (("c4", 1 << 26, 0, 10**7, 32, 4, 0), ("
         torch.cuda.synchronize()
         if ref is None: ref = res
         print(json.dumps({"cfg": name, "K": K, "ms": ms, "gpat_s": m / ms / 1e6, "build_s": round(bt, 3),
-                          "equal_to_K8": bool(torch.equal(res, ref))}), flush=True)
+                          "equal_to_first": bool(torch.equal(res, ref))}), flush=True)
         del fm
         torch.cuda.empty_cache()
     del text, pats, ref
