@@ -14,6 +14,8 @@
  *   rank(q)    := rank(q, 1)  for sigma = 2
  *   FM count   := number of (overlapping) occurrences, via backward search over a
  *                 plain BWT (App. D)
+ *   count_hdk  := number of text positions within Hamming distance k of the pattern
+ *                 (NEXT §8(f)3), by a direct scan of every position
  *
  * Conventions (DESIGN.md "Readings" 1, 11, 15): bits are LE in u64 words
  * (t_i = bit i%64 of word i/64); DNA is 2-bit LE (char i = bits 2(i%32)..+1 of
@@ -24,8 +26,10 @@
  * Pins (tests/test_oracle.py): brute-force sums on tiny inputs for every q,
  * rank(0)=0, rank(n)=total, increments = t_q, sum_c rank(q,c)=q, all-ones and
  * all-G special cases, naive-comparison suffix sort, brute-force substring
- * counts, SA-binary-search counts, k-mer partition identities, and the worked
- * example of SPEC.md:329.  No function here is "parity unpinned".
+ * counts, SA-binary-search counts, k-mer partition identities, the worked
+ * example of SPEC.md:329, and for count_hd1 / count_hdk Python brute force plus the
+ * sum of exact counts over every string within distance k.  No function here is
+ * "parity unpinned".
  *
  * Parallelism: an OpenMP parallel-for over independent queries/patterns only;
  * each query runs the plain definition unchanged.
