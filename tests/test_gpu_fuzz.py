@@ -92,3 +92,41 @@ def test_random_fm(cuda, trial):
         qr.qr_set_tuning("fm_step", 0)
         qr.qr_set_tuning("fm_blocks_per_sm", 64)
     assert np.array_equal(to_host(d).view(np.uint32), ref)
+
+
+@pytest.mark.parametrize("trial", range(6))
+def test_random_fm_approx(cuda, trial):
+    """Random text sizes / kinds, k-mer widths, BWT layouts, k in 0..3 and work orders: counts
+    within Hamming distance k equal the oracle's direct scan."""
+    import torch
+
+    rng = np.random.default_rng(3000 + trial)
+    n = int(rng.integers(1, 60000))
+    w = gen.dna(int(rng.integers(1 << 30)), n, int(n >= 2 * gen.BLOCK and trial % 2))
+    sym = gen.unpack_dna(w, n)
+    kw = int(rng.choice([0, 4, 8, 10]))
+    lay = [qr.QR_LAYOUT_QUADRANK16, qr.QR_LAYOUT_QUADRANK16X2][trial % 2]
+    fm = qr.qr_fm_build(w, n, kmer_k=kw, bwt_layout=lay)
+    k = trial % 4
+    pats = []
+    for _ in range(300 if k < 3 else 80):
+        L = int(rng.integers(0, 30))
+        if rng.random() < 0.5 and n > L:
+            a = int(rng.integers(0, n - L + 1))
+            p = sym[a:a + L].copy()
+            for _s in range(int(rng.integers(0, 4))):
+                if L:
+                    j = int(rng.integers(0, L)); p[j] = (p[j] + 1 + rng.integers(0, 3)) % 4
+        else:
+            p = rng.integers(0, 4, L).astype(np.uint8)
+        pats.append(p)
+    cat, off, lens = oracle.pack_patterns(pats)
+    ref = oracle.scan_count_hdk(sym, cat, off, lens, k)
+    qr.qr_set_tuning("fm_dyn", int(rng.integers(0, 2)))
+    try:
+        d = torch.empty(lens.size, dtype=torch.int32, device=cuda)
+        qr.qr_fm_count_approx(fm, to_dev(cat, cuda), to_dev(lens, cuda), 0, k, d, lens.size)
+        torch.cuda.synchronize()
+    finally:
+        qr.qr_set_tuning("fm_dyn", 1)
+    assert np.array_equal(to_host(d).view(np.uint32), ref)

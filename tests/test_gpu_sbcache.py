@@ -419,3 +419,29 @@ def test_cuda_graph_capture_of_dynamic_order_launches(cuda, smem_mode):
     ref_fm = oracle.FmOracle(gen.unpack_dna(tf, nf)).count(pats, np.arange(mp, dtype=np.uint64) * L,
                                                           np.full(mp, L, np.uint32))
     assert np.array_equal(to_host(d).view(np.uint32), ref_fm)
+    # approximate counting (k = 1, 2) and both strands, captured the same way
+    sym = gen.unpack_dna(tf, nf)
+    offs, lens = np.arange(mp, dtype=np.uint64) * L, np.full(mp, L, np.uint32)
+    for k in (1, 2):
+        da = torch.zeros(mp, dtype=torch.int32, device=cuda)
+        qr.qr_fm_count_approx(fm, dp, None, L, k, da, mp, stream=s)
+        torch.cuda.synchronize()
+        ga = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(ga, stream=s):
+            qr.qr_fm_count_approx(fm, dp, None, L, k, da, mp, stream=torch.cuda.current_stream())
+        da.zero_()
+        ga.replay()
+        torch.cuda.synchronize()
+        assert np.array_equal(to_host(da).view(np.uint32), oracle.scan_count_hdk(sym, pats, offs, lens, k)), k
+    df, dr = torch.zeros(mp, dtype=torch.int32, device=cuda), torch.zeros(mp, dtype=torch.int32, device=cuda)
+    qr.qr_fm_count_both(fm, dp, None, L, df, dr, mp, stream=s)
+    torch.cuda.synchronize()
+    gb = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(gb, stream=s):
+        qr.qr_fm_count_both(fm, dp, None, L, df, dr, mp, stream=torch.cuda.current_stream())
+    df.zero_(); dr.zero_()
+    gb.replay()
+    torch.cuda.synchronize()
+    rc = np.concatenate([3 - pats[i * L:(i + 1) * L][::-1] for i in range(mp)]).astype(np.uint8)
+    assert np.array_equal(to_host(df).view(np.uint32), ref_fm)
+    assert np.array_equal(to_host(dr).view(np.uint32), oracle.FmOracle(sym).count(rc, offs, lens))
