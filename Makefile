@@ -4,6 +4,7 @@
 #   gen/libqrgen_dev.so    device generators (nvcc, sm_100a)      — harness
 #   oracle/liboracle.so    CPU oracle (plain C, gcc)              — test infrastructure only
 #   paper_2602_04103_b200/lib/libqrank.so   the product C-ABI library (nvcc, sm_100a)
+#   examples/qrank_demo    plain-C user of the C ABI (gcc -std=c99, links libqrank.so only)
 NVCC    ?= /usr/local/cuda/bin/nvcc
 HOSTCC  := gcc
 ARCH    := -gencode arch=compute_100a,code=sm_100a
@@ -16,7 +17,7 @@ QR_SRC  := $(wildcard $(PKG)/csrc/*.cu)
 QR_HDR  := $(wildcard $(PKG)/csrc/*.cuh) include/qrank.h
 QR_OBJ  := $(patsubst $(PKG)/csrc/%.cu,build/qr_%.o,$(QR_SRC))
 
-all: gen/libqrgen_host.so gen/libqrgen_dev.so oracle/liboracle.so $(if $(QR_SRC),$(PKG)/lib/libqrank.so)
+all: gen/libqrgen_host.so gen/libqrgen_dev.so oracle/liboracle.so $(if $(QR_SRC),$(PKG)/lib/libqrank.so examples/qrank_demo)
 
 gen/libqrgen_host.so: gen/qrgen_host.c gen/qrgen.h
 	$(HOSTCC) $(CFLAGS) -shared -o $@ gen/qrgen_host.c
@@ -35,7 +36,11 @@ $(PKG)/lib/libqrank.so: $(QR_OBJ)
 	@mkdir -p $(PKG)/lib
 	$(NVCC) $(ARCH) -shared -o $@ $(QR_OBJ)
 
+examples/qrank_demo: examples/qrank_demo.c include/qrank.h $(PKG)/lib/libqrank.so
+	$(HOSTCC) -O2 -std=c99 -Wall -Wextra -pedantic -Iinclude -o $@ examples/qrank_demo.c \
+	  -L$(PKG)/lib -lqrank -Wl,-rpath,'$$ORIGIN/../$(PKG)/lib'
+
 clean:
-	rm -rf build gen/*.so oracle/*.so $(PKG)/lib/*.so
+	rm -rf build gen/*.so oracle/*.so $(PKG)/lib/*.so examples/qrank_demo
 
 .PHONY: all clean

@@ -63,7 +63,8 @@ def test_argument_validation_without_gpu():
     assert L.qr_birank_build(None, 10, 0, None, C.byref(out)) == qr.QR_EINVAL
     assert L.qr_build(C.c_void_p(8), 1 << 40, qr.QR_LAYOUT_BIRANK16X2, 0, None, C.byref(out)) == qr.QR_ECAPACITY
     assert L.qr_build(C.c_void_p(8), 1 << 39, qr.QR_LAYOUT_QUADRANK16X2, 0, None, C.byref(out)) == qr.QR_ECAPACITY
-    assert L.qr_build(C.c_void_p(8), 10, 7, 0, None, C.byref(out)) == qr.QR_EINVAL          # unknown layout
+    assert L.qr_build(C.c_void_p(8), 10, 99, 0, None, C.byref(out)) == qr.QR_EINVAL         # unknown layout
+    assert b"bad layout" in L.qr_last_error()
     assert L.qr_fm_build_opts(C.c_void_p(8), 10, None, 8, qr.QR_LAYOUT_BIRANK16, 0, None, C.byref(out)) == qr.QR_EINVAL
     assert L.qr_fm_build_opts(C.c_void_p(8), 10, None, 15, qr.QR_LAYOUT_QUADRANK16, 0, None, C.byref(out)) == qr.QR_EINVAL
     assert L.qr_set_tuning(b"rank_k", 3) == qr.QR_EINVAL
@@ -140,3 +141,39 @@ def test_tuning_knob_validation():
                        ("index64", 0), ("rank_k", 2), ("rank_blocks_per_sm", 64), ("fm_blocks_per_sm", 64),
                        ("stage_slots", 3), ("stage_chunk", 1 << 23)):
             L.qr_set_tuning(key.encode(), v)
+
+
+@pytest.mark.parametrize("compiler,std", [("gcc", "-std=c99"), ("g++", "-std=c++17")])
+def test_header_compiles_and_links_from_plain_c(tmp_path, compiler, std):
+    """include/qrank.h is self-contained C (and C++): a translation unit taking the address of
+    every declared function compiles warning-free and links against libqrank.so alone."""
+    import subprocess
+
+    syms = declared_symbols()
+    src = '#include "qrank.h"\n#include <stdio.h>\nint main(void) {\n  const void* fns[] = {\n'
+    src += ",\n".join(f"    (const void*)&{s}" for s in syms) + "\n  };\n"
+    src += '  printf("%d\\n", (int)(sizeof(fns) / sizeof(fns[0])));\n  return 0;\n}\n'
+    f = tmp_path / ("t.c" if compiler == "gcc" else "t.cpp")
+    f.write_text(src)
+    exe = tmp_path / "t"
+    libdir = os.path.dirname(qr.LIB_PATH)
+    r = subprocess.run([compiler, std, "-Wall", "-Wextra", "-Werror", "-I", os.path.join(ROOT, "include"), str(f),
+                        "-o", str(exe), "-L", libdir, "-lqrank", f"-Wl,-rpath,{libdir}"], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr[-3000:]
+    out = subprocess.run([str(exe)], capture_output=True, text=True)
+    assert out.returncode == 0 and int(out.stdout.strip()) == len(syms)
+
+
+def test_c_demo_is_built():
+    assert os.access(os.path.join(ROOT, "examples", "qrank_demo"), os.X_OK)
+
+
+@pytest.mark.gpu
+def test_c_demo_runs(cuda):
+    """examples/qrank_demo.c: BiRank / QuadRank / QuadFm from plain C with host buffers,
+    checked against naive loops inside the program."""
+    import subprocess
+
+    r = subprocess.run([os.path.join(ROOT, "examples", "qrank_demo")], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    assert "qrank_demo OK" in r.stdout
