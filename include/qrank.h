@@ -253,6 +253,11 @@ const char* qr_last_error(void);
  *                      2.2 x L2, the cluster kernel beyond.
  *   "rank_lane_table"  1 (default): the one-lane kernels read the superblock words from a
  *                      per-CTA shared-memory copy of the packed table when it is <= 32 KB; 0: L2.
+ *   "rank_resident"    1 (default): BiRank16 / QuadRank16 structures whose lines and table fit
+ *                      one CTA's shared memory (<= 200 KB, e.g. configs[0]) are copied into every
+ *                      CTA of a one-CTA-per-SM grid and queried from there (lines swizzled over
+ *                      the banks), for batches whose 16 B/query of I/O is >= 2x the bytes all
+ *                      the copies read; 0: lines from L2.
  *   "rank_smem"        the 2-CTA cluster shared-memory kernels: 0 never, 1 (default) by
  *                      structure size for batches >= 2^22, 2 whenever the table exists.
  *   "rank_s_lane"      global lane-pair kernels: which lane of a pair loads the superblock word.

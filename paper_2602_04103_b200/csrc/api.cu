@@ -33,6 +33,7 @@ int g_rank_smem_clusters = 0;   // cluster rank kernels: 0 = as many 2-CTA clust
 int g_rank_smem_threads = 0;    // cluster rank kernels: CTA size (0 auto: 1024, 768 for K = 6, 512 for K = 8)
 int g_rank_smem_k = 0;          // cluster rank kernels: queries per lane pair per group (0 auto, 1, 2, 4 @1024 thr, 6 @768, 8 @512)
 int g_rank_lane_table = 1;      // one-lane kernels take the superblock words from a per-CTA shared-memory table when small
+int g_rank_resident = 1;        // structures that fit one CTA's shared memory are queried from a per-CTA copy
 int g_rank_pair = 2;            // kernel shape: 2 by structure size (default), 1 lane pairs (one L2 request per query), 0 one lane per query
 uint64_t g_stage_chunk = 1ull << 23;   // queries per chunk on the staged host path (sweep: profiles/r01_e2e_sweep)
 int g_stage_slots = 3;                 // device buffers / internal streams of the staged path
@@ -356,6 +357,9 @@ QR_EXPORT qr_status qr_set_tuning(const char* key, int64_t value) {
   } else if (!strcmp(key, "rank_lane_table")) {
     if (value != 0 && value != 1) return fail(QR_EINVAL, "rank_lane_table must be 0 or 1");
     g_rank_lane_table = (int)value;
+  } else if (!strcmp(key, "rank_resident")) {
+    if (value != 0 && value != 1) return fail(QR_EINVAL, "rank_resident must be 0 or 1");
+    g_rank_resident = (int)value;
   } else if (!strcmp(key, "rank_dyn")) {
     if (value != 0 && value != 1) return fail(QR_EINVAL, "rank_dyn must be 0 or 1");
     g_rank_dyn = (int)value;

@@ -402,6 +402,47 @@ __device__ __forceinline__ void lane_preload(const uint64_t* __restrict__ pack, 
   __syncthreads();
 }
 
+// Resident variant (RES): structures whose whole line array fits next to the table in one CTA's
+// shared memory (<= RES_MAX, e.g. configs[0]: 135 KB) are copied in once per CTA, and every query
+// reads its line from shared memory — no L2 request per query, and no hot-spotting of the few
+// L2 lines that all queries of a small structure hit (69 Gq/s at configs[0] with lines from L2).
+// Returns the line array the kernel reads: global (RES = false) or its shared-memory copy.
+template <bool RES>
+__device__ __forceinline__ const uint4* lane_preload_lines(const uint64_t* __restrict__ pack, uint32_t words,
+                                                           const uint4* __restrict__ lines, uint32_t line_u4,
+                                                           uint64_t* smem) {
+  if (!RES) {
+    lane_preload(pack, words, smem);
+    return lines;
+  }
+  const uint4* src = reinterpret_cast<const uint4*>(pack);
+  uint4* dst = reinterpret_cast<uint4*>(smem);
+  for (uint32_t i = threadIdx.x; i < words / 2; i += blockDim.x) dst[i] = __ldg(src + i);
+  // 16-B chunk c of line j is stored at chunk 4j + (c ^ (j & 3)): without the swizzle every
+  // line starts on bank 0 or 16, so a warp's 32 random lines pile onto 8 banks (ncu: ~28 shared
+  // wavefronts per 16-B load, the kernel bound by them); with it the first chunks spread over
+  // all 32 banks
+  uint4* ldst = reinterpret_cast<uint4*>(smem + words);
+  for (uint32_t i = threadIdx.x; i < line_u4; i += blockDim.x)
+    ldst[(i & ~3u) | ((i & 3u) ^ ((i >> 2) & 3u))] = __ldg(lines + i);
+  __syncthreads();
+  return ldst;
+}
+
+// 32-B sector `sec` of line j: global (non-allocating L1) or the swizzled shared-memory copy
+template <bool RES>
+__device__ __forceinline__ void lane_sector(const uint4* lines, uint64_t j, uint32_t sec, uint64_t& w0, uint64_t& w1,
+                                            uint64_t& w2, uint64_t& w3) {
+  if (RES) {
+    const uint32_t sw = (uint32_t)j & 3u, base = 4u * (uint32_t)j;
+    const uint4 x = lines[base + ((2u * sec) ^ sw)], y = lines[base + ((2u * sec + 1u) ^ sw)];
+    w0 = ((uint64_t)x.y << 32) | x.x; w1 = ((uint64_t)x.w << 32) | x.z;
+    w2 = ((uint64_t)y.y << 32) | y.x; w3 = ((uint64_t)y.w << 32) | y.z;
+  } else {
+    ld_sector_na(lines + 4 * j + 2 * sec, w0, w1, w2, w3);
+  }
+}
+
 // packed BiRank group g lives at part (g & 1), slot g >> 1 (half = slots per part)
 __device__ __forceinline__ uint32_t bi_s_local(const uint64_t* smem, uint32_t half, uint32_t sb) {
   const uint32_t g = sb / 6u, k = sb - 6u * g;
@@ -410,13 +451,14 @@ __device__ __forceinline__ uint32_t bi_s_local(const uint64_t* smem, uint32_t ha
   return k ? lo + ((uint32_t)(v >> (16u + 8u * k)) & 0xffu) : lo;
 }
 
-template <int K, bool HAS_C, bool DYN>
-__global__ void __launch_bounds__(256) k_bi_rank1s(const uint4* __restrict__ lines, const uint64_t* __restrict__ pack,
+template <int K, bool HAS_C, bool DYN, bool RES = false>
+__global__ void __launch_bounds__(RES ? 1024 : 256) k_bi_rank1s(const uint4* __restrict__ lines_g,
+                                                   const uint64_t* __restrict__ pack,
                                                    uint32_t words, uint32_t half, const uint64_t* __restrict__ q,
                                                    const uint8_t* __restrict__ cs, uint64_t* __restrict__ out, uint64_t m,
                                                    uint64_t last_line, unsigned long long* ctr) {
   extern __shared__ uint64_t lt_smem[];
-  lane_preload(pack, words, lt_smem);
+  const uint4* lines = lane_preload_lines<RES>(pack, words, lines_g, RES ? 4u * (uint32_t)(last_line + 1) : 0u, lt_smem);
   const uint32_t u = sc_unit_in_warp<32>();
   ScSched sc = sc_first<K, DYN, 32>(ctr);
   uint64_t qn[K];
@@ -433,10 +475,9 @@ __global__ void __launch_bounds__(256) k_bi_rank1s(const uint4* __restrict__ lin
       const uint64_t p = 16 + qq[k] - (uint64_t)j * BI_B;
       pp[k] = p > 511 ? 511u : (uint32_t)p;
       jj[k] = j;
-      const uint4* ln = lines + 4 * (uint64_t)j;
-      ld_sector_na(ln, a[k][0], a[k][1], a[k][2], a[k][3]);
+      lane_sector<RES>(lines, j, 0, a[k][0], a[k][1], a[k][2], a[k][3]);
       b[k][0] = b[k][1] = b[k][2] = b[k][3] = 0;
-      if (pp[k] >= 256) ld_sector_na(ln + 2, b[k][0], b[k][1], b[k][2], b[k][3]);
+      if (pp[k] >= 256) lane_sector<RES>(lines, j, 1, b[k][0], b[k][1], b[k][2], b[k][3]);
       s[k] = bi_s_local(lt_smem, half, j >> BI_SB_LOG);
     }
     sc = sc_next<K, DYN, 32>(sc, ctr);
@@ -465,13 +506,14 @@ __device__ __forceinline__ const uint64_t* qd_group_local(const uint64_t* smem, 
   return smem + 4 * ((g & 1u) * half + (g >> 1));
 }
 
-template <int K, int MODE, bool DYN>   // MODE 0: rank(q,c); 1: rank_4(q)
-__global__ void __launch_bounds__(256) k_qd_rank1s(const uint4* __restrict__ lines, const uint64_t* __restrict__ pack,
+template <int K, int MODE, bool DYN, bool RES = false>   // MODE 0: rank(q,c); 1: rank_4(q)
+__global__ void __launch_bounds__(RES ? 1024 : 256) k_qd_rank1s(const uint4* __restrict__ lines_g,
+                                                   const uint64_t* __restrict__ pack,
                                                    uint32_t words, uint32_t half, const uint64_t* __restrict__ q,
                                                    const uint8_t* __restrict__ cs, uint64_t* __restrict__ out, uint64_t m,
                                                    uint64_t last_line, unsigned long long* ctr) {
   extern __shared__ uint64_t lt_smem[];
-  lane_preload(pack, words, lt_smem);
+  const uint4* lines = lane_preload_lines<RES>(pack, words, lines_g, RES ? 4u * (uint32_t)(last_line + 1) : 0u, lt_smem);
   const uint32_t u = sc_unit_in_warp<32>();
   ScSched sc = sc_first<K, DYN, 32>(ctr);
   uint64_t qn[K];
@@ -486,10 +528,9 @@ __global__ void __launch_bounds__(256) k_qd_rank1s(const uint4* __restrict__ lin
     qd_locate32<K>(qq, last_line, jj, pp);
 #pragma unroll
     for (int k = 0; k < K; ++k) {
-      const uint4* ln = lines + 4 * (uint64_t)jj[k];
-      ld_sector_na(ln, a[k][0], a[k][1], a[k][2], a[k][3]);
+      lane_sector<RES>(lines, jj[k], 0, a[k][0], a[k][1], a[k][2], a[k][3]);
       b[k][0] = b[k][1] = b[k][2] = b[k][3] = 0;
-      if (pp[k] >= 128) ld_sector_na(ln + 2, b[k][0], b[k][1], b[k][2], b[k][3]);
+      if (pp[k] >= 128) lane_sector<RES>(lines, jj[k], 1, b[k][0], b[k][1], b[k][2], b[k][3]);
     }
     sc = sc_next<K, DYN, 32>(sc, ctr);
     sc_load_qc<K, MODE == 0>(q, cs, sc.gb + u, sc.stride, m, qn, cn);
@@ -973,6 +1014,36 @@ static void sc_launch_kt(const qr_index* h, const uint64_t* q, const uint8_t* c,
 
 // One-lane kernels with the per-CTA table (rank_shape LANE).  Returns cudaErrorNotSupported when
 // the handle has no table small enough (the caller then uses the global-memory lane kernels).
+extern int g_rank_resident;
+
+// largest dynamic shared memory per CTA this device allows (opt-in), capped at 200 KB
+static uint64_t res_max_bytes(int device) {
+  static std::mutex mu;
+  static std::map<int, uint64_t> cache;
+  std::lock_guard<std::mutex> g(mu);
+  auto it = cache.find(device);
+  if (it != cache.end()) return it->second;
+  int v = 0;
+  if (cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, device) != cudaSuccess || v <= 0) {
+    cudaGetLastError();
+    v = 0;
+  }
+  const uint64_t r = (uint64_t)v < 200 * 1024 ? (uint64_t)v : 200 * 1024;
+  return cache[device] = r;
+}
+
+// raise a kernel's dynamic shared-memory limit to `bytes` (never lowers it; per kernel and device)
+static void res_smem_limit(const void* kern, size_t bytes, int device) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, size_t> limit;
+  std::lock_guard<std::mutex> g(mu);
+  size_t& lim = limit[std::make_pair(kern, device)];
+  if (bytes > lim) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    lim = bytes;
+  }
+}
+
 cudaError_t launch_lane_table_rank(const qr_index* h, const uint64_t* q, const uint8_t* c, uint64_t* out, uint64_t m,
                                    int what, cudaStream_t st) {
   if (!h->spack || g_index64) return cudaErrorNotSupported;
@@ -982,6 +1053,24 @@ cudaError_t launch_lane_table_rank(const qr_index* h, const uint64_t* q, const u
   const uint64_t last = h->n_lines - 1;
   const bool dyn = use_dyn_order(m);
   constexpr int K = 2;
+  // resident structure: table + lines in every CTA's shared memory, when it fits and the batch
+  // moves at least 2x the bytes the preload reads (one copy per SM; 16 B of query I/O per query).
+  // Measured crossover (profiles/r01_small_probe.jsonl): at 135 KB, 10^6 queries lose (59 vs 68
+  // Gq/s from L2) and 10^7 win (128 vs 93); at 17 KB 10^6 already win (68 vs 36: the L2 path
+  // hot-spots on the few lines every query hits)
+  const uint64_t res_bytes = total + h->n_lines * 64;
+  if (g_rank_resident && (total % 16) == 0 && res_bytes <= res_max_bytes(h->device) &&
+      m * 16 >= 2 * res_bytes * (uint64_t)h->sm_count) {
+    const unsigned grid = (unsigned)h->sm_count;                 // one 1024-thread CTA per SM
+    auto go_res = [&](auto kern, const uint8_t* cc) -> cudaError_t {
+      res_smem_limit((const void*)kern, (size_t)res_bytes, h->device);
+      kern<<<grid, 1024, (size_t)res_bytes, st>>>(h->lines, h->spack, words, half, q, cc, out, m, last, nullptr);
+      return cudaGetLastError();
+    };
+    if (h->sigma == 2) return c ? go_res(k_bi_rank1s<K, true, false, true>, c) : go_res(k_bi_rank1s<K, false, false, true>, c);
+    if (what == 0) return go_res(k_qd_rank1s<K, 0, false, true>, c);
+    return go_res(k_qd_rank1s<K, 1, false, true>, nullptr);
+  }
   const unsigned g = grid_stride_blocks((m + K - 1) / K, 256, h->sm_count, g_rank_blocks_per_sm);
   const uint4* L = h->lines;
   const uint64_t* P = h->spack;

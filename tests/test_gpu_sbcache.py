@@ -445,3 +445,35 @@ def test_cuda_graph_capture_of_dynamic_order_launches(cuda, smem_mode):
     rc = np.concatenate([3 - pats[i * L:(i + 1) * L][::-1] for i in range(mp)]).astype(np.uint8)
     assert np.array_equal(to_host(df).view(np.uint32), ref_fm)
     assert np.array_equal(to_host(dr).view(np.uint32), oracle.FmOracle(sym).count(rc, offs, lens))
+
+
+@pytest.mark.parametrize("resident", [1, 0])
+@pytest.mark.parametrize("nb,n4", [(1, 1), (1000, 700), (1 << 20, 1 << 19), (1_400_000, 600_000), (3_000_000, 1_000_000)])
+def test_resident_structure_parity(cuda, smem_mode, resident, nb, n4):
+    """Structures small enough for one CTA's shared memory (configs[0]-sized and up to the
+    200 KB limit; the last size does not fit and takes the L2 path) queried from the per-CTA copy
+    (rank_resident 1) or from L2 (0): rank, rank with c, QuadRank rank and rank_4 on batches large
+    enough for the resident path, boundary queries included."""
+    qr.qr_set_tuning("rank_resident", resident)
+    try:
+        # the resident path needs 16 B/query >= 2x (148 copies of the structure): 3.5M queries
+        # cover the largest structures that fit
+        m = 3_500_000 if nb >= (1 << 20) else 300000
+        w = gen.bits(140 + nb % 7, nb)
+        q = np.concatenate([gen.queries(141, nb, m), boundary_queries(nb, B, S, 240, limit=5000)])
+        h = qr.qr_birank_build(w, nb)
+        ora = oracle.BitsOracle(w, nb)
+        assert np.array_equal(_rank(h, q, None, cuda, 1), ora.rank(q))
+        c = (gen.queries(142, 1, q.size, with_c=True)[1] & 1).astype(np.uint8)
+        assert np.array_equal(_rank(h, q, c, cuda, 1), ora.rank(q, c))
+        t = gen.dna(143 + n4 % 5, n4)
+        m = 3_500_000 if n4 >= (1 << 19) else 300000
+        q4, c4 = gen.queries(144, n4, m, with_c=True)
+        bq = boundary_queries(n4, B4, S4, 96, limit=5000)
+        q4 = np.concatenate([q4, bq]); c4 = np.concatenate([c4, (bq % 4).astype(np.uint8)])
+        h4 = qr.qr_quadrank_build(t, n4)
+        ora4 = oracle.DnaOracle(t, n4)
+        assert np.array_equal(_rank(h4, q4, c4, cuda, 1), ora4.rank(q4, c4))
+        assert np.array_equal(_rank4(h4, q4, cuda, 1), ora4.rank_all4(q4))
+    finally:
+        qr.qr_set_tuning("rank_resident", 1)
