@@ -70,7 +70,7 @@ typedef struct qr_index qr_index;   /* a rank layout (QR_LAYOUT_*)              
 #define QR_LAYOUT_BIRANK16X2  5
 #define QR_LAYOUT_QUADRANK16X2 6
 #define QR_LAYOUT_BIRANK32X2  7
-typedef struct qr_fm qr_fm;         /* QuadFm: QuadRank over the BWT + C + spos + 8-mer table */
+typedef struct qr_fm qr_fm;         /* QuadFm: QuadRank over the BWT + C + spos + k-mer table */
 
 /* ------------------------------------------------------------------ build */
 
@@ -150,7 +150,7 @@ qr_status qr_fm_build_opts(const uint64_t* text2b, uint64_t n, const uint32_t* s
 
 /* out[k] = number of (overlapping) occurrences of pattern k in T, as u32 (backward search:
  * lo = C[c] + Occ(c, lo), hi = C[c] + Occ(c, hi), Occ(c,x) = rank(x,c) - [c = A and x > spos];
- * seeded by the 8-mer table when the pattern has >= 8 symbols).  patterns: concatenated, one
+ * seeded by the k-mer table when the pattern has >= K symbols).  patterns: concatenated, one
  * byte per symbol (0..3, taken mod 4).  lengths: u32[m], pattern k starts at the exclusive
  * prefix sum of lengths (computed on the device); or lengths = NULL and every pattern has
  * fixed_len symbols.  An empty pattern counts n + 1.  Patterns are counted as given (no
