@@ -642,23 +642,43 @@ static qr_status fm_count_impl(const qr_fm* fm, const uint8_t* patterns, const u
                              out_rc ? (uint32_t*)d[2] : nullptr, cnt, nullptr, s, approx);
     });
   }
-  // variable lengths from host: one whole copy (offsets depend on every earlier length)
-  uint64_t total = 0;
-  for (uint64_t i = 0; i < m; ++i) total += lengths[i];
+  // variable lengths from host: chunks of <= 2^22 patterns and <= 256 MiB of symbols (one longer
+  // pattern makes a chunk of its own), each copied, counted and copied back in order on `st`,
+  // so device memory stays bounded whatever the batch
+  constexpr uint64_t CHUNK_PATS = 1ull << 22, CHUNK_BYTES = 1ull << 28;
+  uint64_t longest = 0;
+  for (uint64_t i = 0; i < m; ++i) longest = lengths[i] > longest ? lengths[i] : longest;
+  const uint64_t cap = longest > CHUNK_BYTES ? longest : CHUNK_BYTES;
+  const uint64_t pc = m < CHUNK_PATS ? m : CHUNK_PATS;
   uint8_t* dp = nullptr;
   uint32_t *dl = nullptr, *dout = nullptr;
   cudaError_t e;
-  if ((e = cudaMallocAsync((void**)&dp, total + 8, st)) || (e = cudaMallocAsync((void**)&dl, m * 4, st)) ||
-      (e = cudaMallocAsync((void**)&dout, m * 8, st))) {
+  if ((e = cudaMallocAsync((void**)&dp, cap + 8, st)) || (e = cudaMallocAsync((void**)&dl, pc * 4, st)) ||
+      (e = cudaMallocAsync((void**)&dout, pc * 8, st))) {
     cudaFreeAsync(dp, st); cudaFreeAsync(dl, st); cudaFreeAsync(dout, st);
     return cuda_fail(e, "qr_fm_count: staging alloc");
   }
-  if (total) cudaMemcpyAsync(dp, patterns, total, cudaMemcpyHostToDevice, st);
-  cudaMemcpyAsync(dl, lengths, m * 4, cudaMemcpyHostToDevice, st);
-  qr_status s = fm_count_device(fm, dp, dl, 0, dout, out_rc ? dout + m : nullptr, m, nullptr, st, approx);
-  if (s == QR_OK) {
-    cudaMemcpyAsync(out, dout, m * 4, cudaMemcpyDeviceToHost, st);
-    if (out_rc) cudaMemcpyAsync(out_rc, dout + m, m * 4, cudaMemcpyDeviceToHost, st);
+  qr_status s = QR_OK;
+  uint64_t byte0 = 0;
+  for (uint64_t lo = 0; lo < m && s == QR_OK;) {
+    uint64_t hi = lo, bytes = 0;
+    while (hi < m && hi - lo < CHUNK_PATS && (hi == lo || bytes + lengths[hi] <= cap)) bytes += lengths[hi++];
+    const uint64_t cnt = hi - lo;
+    if (bytes && (e = cudaMemcpyAsync(dp, patterns + byte0, bytes, cudaMemcpyHostToDevice, st))) {
+      s = cuda_fail(e, "qr_fm_count: staged H2D");
+      break;
+    }
+    if ((e = cudaMemcpyAsync(dl, lengths + lo, cnt * 4, cudaMemcpyHostToDevice, st))) {
+      s = cuda_fail(e, "qr_fm_count: staged H2D");
+      break;
+    }
+    s = fm_count_device(fm, dp, dl, 0, dout, out_rc ? dout + cnt : nullptr, cnt, nullptr, st, approx);
+    if (s == QR_OK && (e = cudaMemcpyAsync(out + lo, dout, cnt * 4, cudaMemcpyDeviceToHost, st)))
+      s = cuda_fail(e, "qr_fm_count: staged D2H");
+    if (s == QR_OK && out_rc && (e = cudaMemcpyAsync(out_rc + lo, dout + cnt, cnt * 4, cudaMemcpyDeviceToHost, st)))
+      s = cuda_fail(e, "qr_fm_count: staged D2H");
+    byte0 += bytes;
+    lo = hi;
   }
   cudaFreeAsync(dp, st); cudaFreeAsync(dl, st); cudaFreeAsync(dout, st);
   return s;

@@ -605,3 +605,29 @@ def test_fm_count_approx_rejects_k_above_3(cuda):
     pats = torch.zeros(4 * 8, dtype=torch.uint8, device=cuda)
     with pytest.raises(qr.QrError):
         qr.qr_fm_count_approx(fm, pats, None, 8, 4, d, 4)
+
+
+def test_fm_host_variable_length_chunks(cuda):
+    """Host-pointer batches with per-pattern lengths are staged in chunks of <= 2^22 patterns:
+    a batch just over one chunk (forward and both strands) equals the oracle on every pattern."""
+    n = 5000
+    w = gen.dna(404, n)
+    sym = gen.unpack_dna(w, n)
+    ora = oracle.FmOracle(sym)
+    rng = np.random.default_rng(404)
+    m = (1 << 22) + 1003
+    lens = rng.integers(0, 13, m).astype(np.uint32)
+    cat = rng.integers(0, 4, int(lens.sum())).astype(np.uint8)
+    off = np.concatenate([[0], np.cumsum(lens[:-1], dtype=np.uint64)]).astype(np.uint64)
+    ref = ora.count(cat, off, lens)
+    out = np.zeros(m, np.uint32)
+    qr.qr_fm_count(fm := qr.qr_fm_build(w, n), cat, lens, 0, out, m)
+    qr.qr_sync()
+    assert np.array_equal(out, ref)
+    rc_cat = np.concatenate([3 - cat[int(o):int(o) + int(L)][::-1] for o, L in zip(off[-2000:], lens[-2000:])])
+    rc_off = np.concatenate([[0], np.cumsum(lens[-2000:][:-1], dtype=np.uint64)]).astype(np.uint64)
+    of, orc = np.zeros(m, np.uint32), np.zeros(m, np.uint32)
+    qr.qr_fm_count_both(fm, cat, lens, 0, of, orc, m)
+    qr.qr_sync()
+    assert np.array_equal(of, ref)
+    assert np.array_equal(orc[-2000:], ora.count(rc_cat.astype(np.uint8), rc_off, lens[-2000:]))
