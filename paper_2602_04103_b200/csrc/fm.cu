@@ -774,8 +774,14 @@ __device__ __forceinline__ uint64_t approx_next(unsigned long long* ctr, uint64_
   return b + __popc(am & ((1u << lane) - 1u));
 }
 
+#ifdef QR_APPROX_MINB
+#define QR_APPROX_LB __launch_bounds__(256, QR_APPROX_MINB)
+#else
+#define QR_APPROX_LB __launch_bounds__(256)
+#endif
+
 template <bool FIXED, int BW>
-__global__ void __launch_bounds__(256) k_fm_approx1(FmParams F, const uint8_t* __restrict__ pat,
+__global__ void QR_APPROX_LB k_fm_approx1(FmParams F, const uint8_t* __restrict__ pat,
                                                     const uint64_t* __restrict__ offs,
                                                     const uint32_t* __restrict__ lens, uint32_t fixed_len,
                                                     uint32_t* __restrict__ out, uint64_t m,
@@ -894,7 +900,7 @@ __device__ __forceinline__ uint32_t kmer_subst(uint32_t key, int t, uint32_t r) 
 }
 
 template <bool FIXED, int BW, int KMAX>
-__global__ void __launch_bounds__(256) k_fm_approxk(FmParams F, const uint8_t* __restrict__ pat,
+__global__ void QR_APPROX_LB k_fm_approxk(FmParams F, const uint8_t* __restrict__ pat,
                                                     const uint64_t* __restrict__ offs,
                                                     const uint32_t* __restrict__ lens, uint32_t fixed_len,
                                                     uint32_t* __restrict__ out, uint64_t m,
