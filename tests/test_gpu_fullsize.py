@@ -156,3 +156,32 @@ def test_fm_beyond_2_31_rows(cuda):
     n = (1 << 31) + 7
     counts = _fm_full(cuda, n, 0, 10**6, 40, 9, 24)
     assert counts[0::2].min() >= 1
+
+
+def test_birank_beyond_2_36_bits(cuda):
+    """n >= 2^36 bits takes the 64-bit line-index kernels for real (not through the index64
+    knob): 2^36 + 777 bits (8.6 GB), 10^7 queries + the boundary set, sampled runs and the last
+    line against the oracle; every output satisfies 0 <= rank(q) <= q."""
+    torch = _torch()
+    n, m = (1 << 36) + 777, 10**7
+    bits = torch.empty((n + 63) // 64, dtype=torch.uint64, device=cuda)
+    gen.bits_dev(36, n, 0.5, bits)
+    h = qr.qr_birank_build(bits, n)
+    del bits
+    q = torch.empty(m, dtype=torch.uint64, device=cuda)
+    gen.queries_dev(37, n, m, q)
+    out = torch.empty_like(q)
+    qr.qr_rank(h, q, None, out)
+    torch.cuda.synchronize()
+    assert bool((out.view(torch.int64) <= q.view(torch.int64)).all())
+    ora = oracle.BitsOracle(gen.bits(36, n, 0.5), n)
+    for off in sample_offsets(m, 36)[:16]:
+        qs = gen.queries(37, n, RUN, i0=int(off))
+        assert np.array_equal(to_host(out[off:off + RUN]), ora.rank(qs)), f"offset {off}"
+    bq = np.concatenate([boundary_queries(n, B, S, 240, limit=20000),
+                         np.arange(n - 3000, n + 1, dtype=np.uint64)])
+    dq = to_dev(bq, cuda)
+    ob = torch.empty_like(dq)
+    qr.qr_rank(h, dq, None, ob)
+    torch.cuda.synchronize()
+    assert np.array_equal(to_host(ob), ora.rank(bq))
