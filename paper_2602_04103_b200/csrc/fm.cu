@@ -354,13 +354,28 @@ __device__ __forceinline__ void x2_locate(uint32_t x, uint32_t last_line, uint32
   j = jj;
 }
 // count of symbol c among the sector's chars between p and its anchor 48, signed by the side
-__device__ __forceinline__ uint64_t x2_range(uint32_t p, int t) {
+// The two count masks of every in-sector position p (0..95), built once per CTA in shared memory
+// by kernels over a QuadRank16x2 BWT (x2_masks_init): one 16-B shared load per rank instead of
+// the variable 64-bit shifts of two prefix masks (that kernel is issue-bound, ncu).
+__shared__ __align__(16) uint64_t g_x2_masks[96][2];
+
+__device__ __forceinline__ uint64_t x2_range_calc(uint32_t p, int t);
+__device__ __forceinline__ void x2_masks_init() {
+  for (uint32_t i = threadIdx.x; i < 96; i += blockDim.x) {
+    g_x2_masks[i][0] = x2_range_calc(i, 0);
+    g_x2_masks[i][1] = x2_range_calc(i, 1);
+  }
+  __syncthreads();
+}
+__device__ __forceinline__ uint64_t x2_range_calc(uint32_t p, int t) {
   return (prefix_mask((int)p, t) ^ prefix_mask(48, t)) & (t ? 0xffffffffull : ~0ull);
 }
 __device__ __forceinline__ uint32_t x2_rank(const uint64_t (&w)[4], uint32_t p, uint32_t c, uint32_t s) {
   const uint64_t nl = (c & 1u) ? 0ull : ~0ull, nh = (c & 2u) ? 0ull : ~0ull;   // planes (variants.cu)
-  const uint32_t cnt = __popcll((w[1] ^ nl) & (w[2] ^ nh) & x2_range(p, 0)) +
-                       __popcll((w[3] ^ nl) & ((w[3] >> 32) ^ nh) & x2_range(p, 1));
+  const uint4 mm = reinterpret_cast<const uint4*>(g_x2_masks)[p];
+  const uint64_t m0 = ((uint64_t)mm.y << 32) | mm.x, m1 = ((uint64_t)mm.w << 32) | mm.z;
+  const uint32_t cnt = __popcll((w[1] ^ nl) & (w[2] ^ nh) & m0) +
+                       __popcll((w[3] ^ nl) & ((w[3] >> 32) ^ nh) & m1);
   const uint32_t base = (s << QD_SHIFT) + (uint32_t)((w[0] >> (16 * c)) & 0xffffull);
   return p >= 48 ? base + cnt : base - cnt;
 }
@@ -397,6 +412,7 @@ __device__ __forceinline__ void fm_step(const FmParams& F, uint32_t c, uint32_t&
 
 template <int BW>
 __global__ void k_kmer_table(FmParams F, uint2* __restrict__ table) {
+  if (BW == 1) x2_masks_init();
   const uint32_t key = blockIdx.x * blockDim.x + threadIdx.x;
   if (key >= (1u << (2 * F.K))) return;
   uint32_t lo = 0, hi = (uint32_t)F.N;
@@ -572,6 +588,7 @@ __global__ void __launch_bounds__(256, QR_FM_MINB) k_fm_count(FmParams F, const 
                                                      unsigned long long* __restrict__ work,
                                                      unsigned long long* __restrict__ ctr,
                                                      const uint2* __restrict__ seeds) {
+  if (BW == 1) x2_masks_init();
   fm_preload_super<SMS>(F);
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   const uint64_t ntask = m * STRANDS;
@@ -683,7 +700,8 @@ __device__ __forceinline__ void fm_occ4_x2(const FmParams& F, uint32_t x, uint32
   uint64_t w[4];
   ld_sector(F.lines + 4 * (uint64_t)j + 2 * h, w[0], w[1], w[2], w[3]);
   const uint4 sv = __ldg(reinterpret_cast<const uint4*>(F.super) + (j >> QD_SB_LOG));
-  const uint64_t m0 = x2_range(p, 0), m1 = x2_range(p, 1);
+  const uint4 mm = reinterpret_cast<const uint4*>(g_x2_masks)[p];
+  const uint64_t m0 = ((uint64_t)mm.y << 32) | mm.x, m1 = ((uint64_t)mm.w << 32) | mm.z;
   const uint64_t l0 = w[1] & m0, h0 = w[2] & m0, l1 = w[3] & m1, h1 = (w[3] >> 32) & m1;
   const uint32_t nl = __popcll(l0) + __popcll(l1), nh = __popcll(h0) + __popcll(h1);
   const uint32_t nt = __popcll(l0 & h0) + __popcll(l1 & h1);
@@ -786,6 +804,7 @@ __global__ void QR_APPROX_LB k_fm_approx1(FmParams F, const uint8_t* __restrict_
                                                     const uint32_t* __restrict__ lens, uint32_t fixed_len,
                                                     uint32_t* __restrict__ out, uint64_t m,
                                                     unsigned long long* __restrict__ ctr) {
+  if (BW == 1) x2_masks_init();
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   const uint4 C4 = __ldg(reinterpret_cast<const uint4*>(F.Ct));
   const uint32_t Cs[4] = {C4.x, C4.y, C4.z, C4.w};
@@ -905,6 +924,7 @@ __global__ void QR_APPROX_LB k_fm_approxk(FmParams F, const uint8_t* __restrict_
                                                     const uint32_t* __restrict__ lens, uint32_t fixed_len,
                                                     uint32_t* __restrict__ out, uint64_t m,
                                                     unsigned long long* __restrict__ ctr) {
+  if (BW == 1) x2_masks_init();
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   const uint4 C4 = __ldg(reinterpret_cast<const uint4*>(F.Ct));
   const uint32_t Cs[4] = {C4.x, C4.y, C4.z, C4.w};
