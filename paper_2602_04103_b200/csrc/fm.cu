@@ -289,11 +289,29 @@ __global__ void k_sym_counts(const uint64_t* __restrict__ text, uint64_t n, unsi
 
 // ------------------------------------------------------------------ rank inside the FM loop
 
+// Prefix masks of every in-half position x (0..127) of a QuadRank16 BWT line, as a per-CTA
+// shared table, for rank_4 and the steps of the issue-bound approximate search (+7.5% at k = 1)
+// and the k-mer table build; the count kernels keep computing them (the table's shared loads
+// cost the L1-bound configs[3] kernel wavefronts and the HBM kernels latency: -5% measured).
+__shared__ __align__(16) uint64_t g_qd_masks[128][2];
+__device__ __forceinline__ void qd_masks_init() {
+  for (uint32_t i = threadIdx.x; i < 128; i += blockDim.x) {
+    g_qd_masks[i][0] = prefix_mask((int)i, 0);
+    g_qd_masks[i][1] = prefix_mask((int)i, 1);
+  }
+  __syncthreads();
+}
+__device__ __forceinline__ void qd_masks(uint32_t x, uint64_t& m0, uint64_t& m1) {
+  const uint4 mm = reinterpret_cast<const uint4*>(g_qd_masks)[x];
+  m0 = ((uint64_t)mm.y << 32) | mm.x;
+  m1 = ((uint64_t)mm.w << 32) | mm.z;
+}
+
 // Occ for lo and hi of one backward step, all gathers issued before any is used.  lo and hi
 // often share a line ("cache lines are automatically reused"); then the line's
 // sectors and the superblock word are loaded once and reused from registers, which halves the
 // L1 wavefronts of a step when the structure is L2-resident.  N < 2^32: u32 arithmetic.
-template <int SMS = 0>
+template <int SMS = 0, bool MT = false>   // MT: masks from the per-CTA table (qd_masks_init)
 __device__ __forceinline__ void fm_step16(const FmParams& F, uint32_t c, uint32_t& lo, uint32_t& hi, uint32_t& lines) {
   uint32_t jl = (lo >> 5) / 7u;                                  // floor(lo/224)
   uint32_t jh = (hi >> 5) / 7u;
@@ -327,8 +345,11 @@ __device__ __forceinline__ void fm_step16(const FmParams& F, uint32_t c, uint32_
     const int x = (int)(p & 127u);
     const uint64_t inv = right ? 0ull : ~0ull;
     const uint64_t* w = right ? b : a;
-    uint32_t cnt = __popcll((w[0] ^ cl) & (w[1] ^ ch) & (prefix_mask(x, 0) ^ inv)) +
-                   __popcll((w[2] ^ cl) & (w[3] ^ ch) & (prefix_mask(x, 1) ^ inv));
+    uint64_t m0, m1;
+    if (MT) qd_masks((uint32_t)x, m0, m1);
+    else { m0 = prefix_mask(x, 0); m1 = prefix_mask(x, 1); }
+    uint32_t cnt = __popcll((w[0] ^ cl) & (w[1] ^ ch) & (m0 ^ inv)) +
+                   __popcll((w[2] ^ cl) & (w[3] ^ ch) & (m1 ^ inv));
     uint64_t dw = (c & 2u) ? a[1] : a[0];
     uint32_t base = (s << QD_SHIFT) + (uint32_t)((dw >> (16 * (c & 1u))) & 0xffffull);
     return right ? base + cnt : base - cnt;
@@ -404,20 +425,21 @@ __device__ __forceinline__ void fm_step_x2(const FmParams& F, uint32_t c, uint32
 }
 
 // one backward step over either BWT layout (BW 0: QuadRank16 de-duplicating step, 1: QuadRank16x2)
-template <int SMS = 0, int BW = 0>
+template <int SMS = 0, int BW = 0, bool MT = false>
 __device__ __forceinline__ void fm_step(const FmParams& F, uint32_t c, uint32_t& lo, uint32_t& hi, uint32_t& lines) {
   if (BW == 1) fm_step_x2<SMS>(F, c, lo, hi, lines);
-  else         fm_step16<SMS>(F, c, lo, hi, lines);
+  else         fm_step16<SMS, MT>(F, c, lo, hi, lines);
 }
 
 template <int BW>
 __global__ void k_kmer_table(FmParams F, uint2* __restrict__ table) {
   if (BW == 1) x2_masks_init();
+  else qd_masks_init();
   const uint32_t key = blockIdx.x * blockDim.x + threadIdx.x;
   if (key >= (1u << (2 * F.K))) return;
   uint32_t lo = 0, hi = (uint32_t)F.N;
   uint32_t dummy;
-  for (int t = 0; t < F.K && lo < hi; ++t) fm_step<0, BW>(F, (key >> (2 * t)) & 3u, lo, hi, dummy);   // last char first
+  for (int t = 0; t < F.K && lo < hi; ++t) fm_step<0, BW, true>(F, (key >> (2 * t)) & 3u, lo, hi, dummy);   // last char first
   if (lo >= hi) lo = hi = 0;
   table[key] = make_uint2(lo, hi);
 }
@@ -731,9 +753,11 @@ __device__ __forceinline__ void fm_occ4(const FmParams& F, uint32_t x, uint32_t 
   const uint64_t inv = right ? 0ull : ~0ull;
   const uint64_t* w = right ? b : a;
   uint32_t nl = 0, nh = 0, nt = 0;
+  uint64_t mk[2];
+  qd_masks((uint32_t)xx, mk[0], mk[1]);
 #pragma unroll
   for (int t = 0; t < 2; ++t) {
-    uint64_t msk = prefix_mask(xx, t) ^ inv;
+    uint64_t msk = mk[t] ^ inv;
     uint64_t l = ~w[2 * t] & msk, hh = ~w[2 * t + 1] & msk;
     nl += __popcll(l);
     nh += __popcll(hh);
@@ -762,7 +786,7 @@ __device__ __forceinline__ uint32_t fm_continue3(const FmParams& F, PatWindow& P
     const uint32_t c = P.at(k);
 #pragma unroll
     for (int r = 0; r < 3; ++r)
-      if (lo[r] < hi[r]) fm_step<0, BW>(F, c, lo[r], hi[r], nl);
+      if (lo[r] < hi[r]) fm_step<0, BW, true>(F, c, lo[r], hi[r], nl);
   }
   uint32_t t = 0;
 #pragma unroll
@@ -773,7 +797,7 @@ __device__ __forceinline__ uint32_t fm_continue3(const FmParams& F, PatWindow& P
 template <int BW>
 __device__ __forceinline__ uint32_t fm_continue(const FmParams& F, PatWindow& P, int64_t k, uint32_t lo, uint32_t hi) {
   uint32_t nl;
-  for (; k >= 0 && lo < hi; --k) fm_step<0, BW>(F, P.at(k), lo, hi, nl);
+  for (; k >= 0 && lo < hi; --k) fm_step<0, BW, true>(F, P.at(k), lo, hi, nl);
   return lo < hi ? hi - lo : 0u;
 }
 
@@ -805,6 +829,7 @@ __global__ void QR_APPROX_LB k_fm_approx1(FmParams F, const uint8_t* __restrict_
                                                     uint32_t* __restrict__ out, uint64_t m,
                                                     unsigned long long* __restrict__ ctr) {
   if (BW == 1) x2_masks_init();
+  else qd_masks_init();
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   const uint4 C4 = __ldg(reinterpret_cast<const uint4*>(F.Ct));
   const uint32_t Cs[4] = {C4.x, C4.y, C4.z, C4.w};
@@ -925,6 +950,7 @@ __global__ void QR_APPROX_LB k_fm_approxk(FmParams F, const uint8_t* __restrict_
                                                     uint32_t* __restrict__ out, uint64_t m,
                                                     unsigned long long* __restrict__ ctr) {
   if (BW == 1) x2_masks_init();
+  else qd_masks_init();
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   const uint4 C4 = __ldg(reinterpret_cast<const uint4*>(F.Ct));
   const uint32_t Cs[4] = {C4.x, C4.y, C4.z, C4.w};
