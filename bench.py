@@ -362,6 +362,32 @@ def bench_reads(ctx, n, m_total, length, seed, steps, warmup):
             "fm_build_s": round(build_s, 2)}
 
 
+def bench_reads_approx(ctx, n, m_total, length, seed, steps, warmup, kmax):
+    """The paper's read workload (150 bp, 1% substitutions, either strand) counted
+    within kmax substitutions on both strands in one launch (qr_fm_count_approx_both)."""
+    import gen
+    import paper_2602_04103_b200 as qr
+
+    torch = ctx.torch
+    text = torch.empty((n + 31) // 32 + 1, dtype=torch.uint64, device=ctx.dev)
+    gen.dna_dev(5, n, 1, text)
+    fm = qr.qr_fm_build(text, n, device=ctx.gpu)
+    i0, m = shard(m_total, ctx.world, ctx.rank)
+    pats = torch.empty(m * length, dtype=torch.uint8, device=ctx.dev)
+    gen.patterns_dev(seed, 2, m, length, text, n, pats, i0=i0)
+    of = torch.empty(m, dtype=torch.int32, device=ctx.dev)
+    orc = torch.empty_like(of)
+    ms = ctx.timed(lambda: qr.qr_fm_count_approx_both(fm, pats, None, length, kmax, of, orc, m, ctx.stream), steps,
+                   warmup)
+    hit = int(((of > 0) | (orc > 0)).sum())
+    fm.free()
+    del text, pats, of, orc
+    torch.cuda.empty_cache()
+    return {"ms": ms, "reads_per_s": m_total / ms * 1e3, "searches_per_s": 2 * m_total / ms * 1e3,
+            "max_mismatches": kmax, "read_len": length, "reads": m_total, "frac_reads_matching": hit / max(m, 1),
+            "text_len": n}
+
+
 def bench_approx(ctx, n, m_total, length, seed, steps, warmup, bwt_layout=None, kmax=1):
     """<=kmax-substitution counting (rank_4-driven, NEXT §8(f)3) on the configs[3] text/patterns."""
     import gen
@@ -568,6 +594,8 @@ def main():
         rows["c4_quadfm_approx1_bwt16x2"] = bench_approx(ctx, N4, 10**6, L4, SEED[4], K, W,
                                                          bwt_layout=qr.QR_LAYOUT_QUADRANK16X2)
         rows["c4_quadfm_approx2"] = bench_approx(ctx, N4, 10**6, L4, SEED[4], K, W, kmax=2)
+        rows["c5_reads_150bp_both_strands_approx1"] = bench_reads_approx(ctx, N5, 10**6, 150, 55, K, W, 1)
+        rows["c5_reads_150bp_both_strands_approx2"] = bench_reads_approx(ctx, N5, 10**5, 150, 55, K, W, 2)
         rows["layout_variants"] = bench_variants(ctx, K, W)
         rows["latency_mode"] = bench_latency(ctx, K, W)
         rows["c1_small"] = bench_small(ctx, K, W)

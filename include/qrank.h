@@ -179,6 +179,15 @@ qr_status qr_fm_count_both(const qr_fm* fm, const uint8_t* patterns, const uint3
 qr_status qr_fm_count_approx(const qr_fm* fm, const uint8_t* patterns, const uint32_t* lengths, uint32_t fixed_len,
                              uint32_t max_mismatches, uint32_t* out, uint64_t m, void* stream);
 
+/* Both strands of every pattern within max_mismatches substitutions (0..3), in one launch:
+ * out_fwd[k] as qr_fm_count_approx, out_rc[k] the same count for the reverse complement
+ * RC(P)[j] = 3 - P[len-1-j] (read from the same bytes, never materialised) —
+ * the paper's read workload with its 1% substitutions.  Arguments as
+ * qr_fm_count_approx; out_rc: u32[m], same memory space as out_fwd. */
+qr_status qr_fm_count_approx_both(const qr_fm* fm, const uint8_t* patterns, const uint32_t* lengths,
+                                  uint32_t fixed_len, uint32_t max_mismatches, uint32_t* out_fwd, uint32_t* out_rc,
+                                  uint64_t m, void* stream);
+
 /* As qr_fm_count (device pointers only), additionally accumulating into work[0] the number of
  * backward steps executed after seeding and into work[1] the number of distinct 64-B lines
  * those steps touch (1 or 2 per step) — the algorithmic-bytes denominator of SURVEY §8(d).

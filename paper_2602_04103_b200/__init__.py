@@ -30,7 +30,7 @@ EXPORTS = (
     "qr_fm_count_work", "qr_gather_ceiling", "qr_info", "qr_export_layout", "qr_fm_info", "qr_fm_export_kmer",
     "qr_clone_to_device", "qr_fm_clone_to_device", "qr_sync", "qr_free", "qr_fm_free", "qr_last_error",
     "qr_version", "qr_set_tuning", "qr_build", "qr_layout", "qr_rank_chain", "qr_import_layout", "qr_fm_build_ex", "qr_fm_kmer_width",
-    "qr_super_cache_bytes", "qr_super_cache_clusters", "qr_fm_build_opts",
+    "qr_super_cache_bytes", "qr_super_cache_clusters", "qr_fm_build_opts", "qr_fm_count_approx_both",
 )
 
 
@@ -62,6 +62,7 @@ def lib():
             "qr_fm_count_work": ([V, V, V, U32, V, U64, V, V], I32),
             "qr_fm_count_both": ([V, V, V, U32, V, V, U64, V], I32),
             "qr_fm_count_approx": ([V, V, V, U32, U32, V, U64, V], I32),
+            "qr_fm_count_approx_both": ([V, V, V, U32, U32, V, V, U64, V], I32),
             "qr_gather_ceiling": ([V, V, V, U64, I32, V], I32),
             "qr_info": ([V, C.POINTER(U64), C.POINTER(C.c_int), C.POINTER(U64), C.POINTER(U64)], I32),
             "qr_export_layout": ([V, V, V], I32),
@@ -293,6 +294,14 @@ def qr_fm_count_approx(fm: Fm, patterns, lengths, fixed_len: int, max_mismatches
     _check(lib().qr_fm_count_approx(fm.ptr, _ptr(patterns), _ptr(lengths), fixed_len, max_mismatches, _ptr(out), m,
                                     _stream(stream)), "qr_fm_count_approx")
     return out
+
+
+def qr_fm_count_approx_both(fm: Fm, patterns, lengths, fixed_len: int, max_mismatches: int, out_fwd, out_rc, m: int,
+                            stream=None):
+    _need_fm("qr_fm_count_approx_both", patterns, lengths, fixed_len, m, out_fwd, out_rc)
+    _check(lib().qr_fm_count_approx_both(fm.ptr, _ptr(patterns), _ptr(lengths), fixed_len, max_mismatches,
+                                         _ptr(out_fwd), _ptr(out_rc), m, _stream(stream)), "qr_fm_count_approx_both")
+    return out_fwd, out_rc
 
 
 def qr_fm_count_work(fm: Fm, patterns, lengths, fixed_len: int, out, m: int, work, stream=None):

@@ -696,6 +696,14 @@ QR_EXPORT qr_status qr_fm_count_approx(const qr_fm* fm, const uint8_t* patterns,
   return fm_count_impl(fm, patterns, lengths, fixed_len, out, nullptr, m, nullptr, stream, (int)max_mismatches);
 }
 
+QR_EXPORT qr_status qr_fm_count_approx_both(const qr_fm* fm, const uint8_t* patterns, const uint32_t* lengths,
+                                            uint32_t fixed_len, uint32_t max_mismatches, uint32_t* out_fwd,
+                                            uint32_t* out_rc, uint64_t m, void* stream) {
+  if (max_mismatches > 3) return fail(QR_EINVAL, "qr_fm_count_approx_both: max_mismatches must be 0..3");
+  if (!out_rc) return fail(QR_EINVAL, "qr_fm_count_approx_both: null out_rc");
+  return fm_count_impl(fm, patterns, lengths, fixed_len, out_fwd, out_rc, m, nullptr, stream, (int)max_mismatches);
+}
+
 QR_EXPORT qr_status qr_fm_count_both(const qr_fm* fm, const uint8_t* patterns, const uint32_t* lengths,
                                      uint32_t fixed_len, uint32_t* out_fwd, uint32_t* out_rc, uint64_t m, void* stream) {
   if (!out_rc) return fail(QR_EINVAL, "qr_fm_count_both: null out_rc");

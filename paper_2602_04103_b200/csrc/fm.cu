@@ -563,6 +563,19 @@ __device__ __forceinline__ uint32_t kmer_key_rc(int K, PatWindow& P, const uint8
   return key;
 }
 
+// Pattern symbols of one strand for the approximate-search kernels: STRANDS = 2 tasks with rc = 1
+// read the reverse complement RC(P)[k] = 3 - P[len-1-k] from the same bytes.
+template <int STRANDS>
+struct StrandWindow {
+  PatWindow P;
+  uint32_t len, rc;
+  __device__ __forceinline__ void reset(const uint8_t* p, uint32_t l, uint32_t r) { P.reset(p); len = l; rc = r; }
+  __device__ __forceinline__ uint32_t at(int64_t k) {
+    if (STRANDS == 1) return P.at(k);
+    return rc ? 3u - P.at((int64_t)len - 1 - k) : P.at(k);
+  }
+};
+
 // 4 resident CTAs (64 registers): capping registers for 6 or 8 CTAs/SM spills and runs 2-4x
 // slower on configs[3]/[4] (profiles/r01_fm_occupancy_sweep.jsonl).
 // Seed pre-pass of the dynamic-order count kernel: one thread per task computes the k-mer table
@@ -778,8 +791,8 @@ __device__ __forceinline__ void fm_occ4(const FmParams& F, uint32_t x, uint32_t 
 // exact backward search of P[0..k] from [lo, hi); returns the final interval size
 // the same for three intervals continuing over the same symbols P[k], P[k-1], ...: their steps
 // are independent, so each position issues the loads of all live intervals before consuming any
-template <int BW>
-__device__ __forceinline__ uint32_t fm_continue3(const FmParams& F, PatWindow& P, int64_t k, uint32_t (&lo)[3],
+template <int BW, class W>
+__device__ __forceinline__ uint32_t fm_continue3(const FmParams& F, W& P, int64_t k, uint32_t (&lo)[3],
                                                  uint32_t (&hi)[3]) {
   uint32_t nl;
   for (; k >= 0 && (lo[0] < hi[0] || lo[1] < hi[1] || lo[2] < hi[2]); --k) {
@@ -794,8 +807,8 @@ __device__ __forceinline__ uint32_t fm_continue3(const FmParams& F, PatWindow& P
   return t;
 }
 
-template <int BW>
-__device__ __forceinline__ uint32_t fm_continue(const FmParams& F, PatWindow& P, int64_t k, uint32_t lo, uint32_t hi) {
+template <int BW, class W>
+__device__ __forceinline__ uint32_t fm_continue(const FmParams& F, W& P, int64_t k, uint32_t lo, uint32_t hi) {
   uint32_t nl;
   for (; k >= 0 && lo < hi; --k) fm_step<0, BW, true>(F, P.at(k), lo, hi, nl);
   return lo < hi ? hi - lo : 0u;
@@ -822,28 +835,31 @@ __device__ __forceinline__ uint64_t approx_next(unsigned long long* ctr, uint64_
 #define QR_APPROX_LB __launch_bounds__(256)
 #endif
 
-template <bool FIXED, int BW>
+template <bool FIXED, int BW, int STRANDS>
 __global__ void QR_APPROX_LB k_fm_approx1(FmParams F, const uint8_t* __restrict__ pat,
                                                     const uint64_t* __restrict__ offs,
                                                     const uint32_t* __restrict__ lens, uint32_t fixed_len,
-                                                    uint32_t* __restrict__ out, uint64_t m,
-                                                    unsigned long long* __restrict__ ctr) {
+                                                    uint32_t* __restrict__ out, uint32_t* __restrict__ out_rc,
+                                                    uint64_t m, unsigned long long* __restrict__ ctr) {
   if (BW == 1) x2_masks_init();
   else qd_masks_init();
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   const uint4 C4 = __ldg(reinterpret_cast<const uint4*>(F.Ct));
   const uint32_t Cs[4] = {C4.x, C4.y, C4.z, C4.w};
-  for (uint64_t pi = ctr ? approx_next(ctr, 0, 0) : blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; pi < m;
-       pi = approx_next(ctr, pi, stride)) {
+  const uint64_t ntask = m * STRANDS;
+  for (uint64_t ti = ctr ? approx_next(ctr, 0, 0) : blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; ti < ntask;
+       ti = approx_next(ctr, ti, stride)) {
+    const uint64_t pi = STRANDS == 2 ? ti >> 1 : ti;
+    const uint32_t rc = STRANDS == 2 ? (uint32_t)(ti & 1) : 0u;
     const uint32_t len = FIXED ? fixed_len : lens[pi];
     const uint8_t* p = pat + (FIXED ? pi * (uint64_t)fixed_len : offs[pi]);
-    PatWindow P;
-    P.reset(p);
+    StrandWindow<STRANDS> P;
+    P.reset(p, len, rc);
     uint64_t total = 0;
     uint32_t lo, hi;
     int64_t j;
     if (F.K && len >= (uint32_t)F.K) {
-      const uint32_t key0 = kmer_key(F.K, P, p, len);
+      const uint32_t key0 = rc ? kmer_key_rc(F.K, P.P, p, len) : kmer_key(F.K, P.P, p, len);
       for (int t = 0; t < F.K; ++t) {                     // one substitution among the last K symbols
         const uint32_t f = (key0 >> (2 * t)) & 3u;
         uint2 iv[3];                                       // the three variants' lookups issued together
@@ -876,7 +892,8 @@ __global__ void QR_APPROX_LB k_fm_approx1(FmParams F, const uint8_t* __restrict_
       hi = Cs[cj] + oh[cj];
     }
     if (lo < hi) total += hi - lo;
-    out[pi] = (uint32_t)total;
+    if (STRANDS == 2 && rc) out_rc[pi] = (uint32_t)total;
+    else out[pi] = (uint32_t)total;
   }
 }
 
@@ -895,8 +912,8 @@ __global__ void QR_APPROX_LB k_fm_approx1(FmParams F, const uint8_t* __restrict_
 // by node; every K-mer within distance KMAX of the pattern's last K symbols is looked up in the
 // k-mer table instead (1 + 3K + 9 C(K,2) [+ 27 C(K,3)] lookups), and the search continues from
 // each non-empty interval with the substitutions it has left.
-template <int BW, int KMAX>
-__device__ __forceinline__ uint64_t fm_backtrack(const FmParams& F, PatWindow& P, const uint32_t (&Cs)[4],
+template <int BW, int KMAX, class W>
+__device__ __forceinline__ uint64_t fm_backtrack(const FmParams& F, W& P, const uint32_t (&Cs)[4],
                                                  uint32_t lo, uint32_t hi, uint32_t pos, int f0) {
   constexpr uint32_t UNX = 8;   // not 4: a frame whose branches are all tried has fd = 4
   uint32_t flo[KMAX + 1], fhi[KMAX + 1], fpos[KMAX + 1], fd[KMAX + 1];   // fd: next branch symbol, UNX = unexpanded
@@ -943,27 +960,30 @@ __device__ __forceinline__ uint32_t kmer_subst(uint32_t key, int t, uint32_t r) 
   return key ^ ((o ^ ((o + r) & 3u)) << (2 * t));
 }
 
-template <bool FIXED, int BW, int KMAX>
+template <bool FIXED, int BW, int KMAX, int STRANDS>
 __global__ void QR_APPROX_LB k_fm_approxk(FmParams F, const uint8_t* __restrict__ pat,
                                                     const uint64_t* __restrict__ offs,
                                                     const uint32_t* __restrict__ lens, uint32_t fixed_len,
-                                                    uint32_t* __restrict__ out, uint64_t m,
-                                                    unsigned long long* __restrict__ ctr) {
+                                                    uint32_t* __restrict__ out, uint32_t* __restrict__ out_rc,
+                                                    uint64_t m, unsigned long long* __restrict__ ctr) {
   if (BW == 1) x2_masks_init();
   else qd_masks_init();
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   const uint4 C4 = __ldg(reinterpret_cast<const uint4*>(F.Ct));
   const uint32_t Cs[4] = {C4.x, C4.y, C4.z, C4.w};
-  for (uint64_t pi = ctr ? approx_next(ctr, 0, 0) : blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; pi < m;
-       pi = approx_next(ctr, pi, stride)) {
+  const uint64_t ntask = m * STRANDS;
+  for (uint64_t ti = ctr ? approx_next(ctr, 0, 0) : blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; ti < ntask;
+       ti = approx_next(ctr, ti, stride)) {
+    const uint64_t pi = STRANDS == 2 ? ti >> 1 : ti;
+    const uint32_t rc = STRANDS == 2 ? (uint32_t)(ti & 1) : 0u;
     const uint32_t len = FIXED ? fixed_len : lens[pi];
     const uint8_t* p = pat + (FIXED ? pi * (uint64_t)fixed_len : offs[pi]);
-    PatWindow P;
-    P.reset(p);
+    StrandWindow<STRANDS> P;
+    P.reset(p, len, rc);
     uint64_t total = 0;
     const int K = F.K;
     if (K && len >= (uint32_t)K) {
-      const uint32_t key0 = kmer_key(K, P, p, len);
+      const uint32_t key0 = rc ? kmer_key_rc(K, P.P, p, len) : kmer_key(K, P.P, p, len);
       const uint32_t pos = len - (uint32_t)K;
       auto seed = [&](uint32_t key, int mm) {
         const uint2 iv = __ldg(F.kmer + key);
@@ -999,7 +1019,8 @@ __global__ void QR_APPROX_LB k_fm_approxk(FmParams F, const uint8_t* __restrict_
     } else {
       total = fm_backtrack<BW, KMAX>(F, P, Cs, 0u, (uint32_t)F.N, len, 0);
     }
-    out[pi] = (uint32_t)total;
+    if (STRANDS == 2 && rc) out_rc[pi] = (uint32_t)total;
+    else out[pi] = (uint32_t)total;
   }
 }
 
@@ -1161,15 +1182,15 @@ static cudaError_t launch_fm(const qr_fm* fm, bool lean, unsigned g, cudaStream_
   return e;
 }
 
-template <bool FIXED>
-static cudaError_t launch_approx(const qr_fm* fm, unsigned g, cudaStream_t st, const FmParams& F, const uint8_t* pat,
-                                 const uint64_t* offs, const uint32_t* lens, uint32_t fixed_len, uint32_t* out,
-                                 uint64_t m, int kmax) {
-  auto kern = kmax == 1 ? (F.bw ? k_fm_approx1<FIXED, 1> : k_fm_approx1<FIXED, 0>)
-            : kmax == 2 ? (F.bw ? k_fm_approxk<FIXED, 1, 2> : k_fm_approxk<FIXED, 0, 2>)
-                        : (F.bw ? k_fm_approxk<FIXED, 1, 3> : k_fm_approxk<FIXED, 0, 3>);
+template <bool FIXED, int STRANDS>
+static cudaError_t launch_approx_s(const qr_fm* fm, unsigned g, cudaStream_t st, const FmParams& F, const uint8_t* pat,
+                                   const uint64_t* offs, const uint32_t* lens, uint32_t fixed_len, uint32_t* out,
+                                   uint32_t* out_rc, uint64_t m, int kmax) {
+  auto kern = kmax == 1 ? (F.bw ? k_fm_approx1<FIXED, 1, STRANDS> : k_fm_approx1<FIXED, 0, STRANDS>)
+            : kmax == 2 ? (F.bw ? k_fm_approxk<FIXED, 1, 2, STRANDS> : k_fm_approxk<FIXED, 0, 2, STRANDS>)
+                        : (F.bw ? k_fm_approxk<FIXED, 1, 3, STRANDS> : k_fm_approxk<FIXED, 0, 3, STRANDS>);
   if (!g_fm_dyn) {
-    kern<<<g, 256, 0, st>>>(F, pat, offs, lens, fixed_len, out, m, nullptr);
+    kern<<<g, 256, 0, st>>>(F, pat, offs, lens, fixed_len, out, out_rc, m, nullptr);
     return cudaGetLastError();
   }
   int per_sm = 0;
@@ -1182,10 +1203,18 @@ static cudaError_t launch_approx(const qr_fm* fm, unsigned g, cudaStream_t st, c
   unsigned long long* ctr = nullptr;
   cudaError_t e = lease.acquire(fm->bwt->device, st, &ctr);
   if (e) return e;
-  kern<<<res < g ? res : g, 256, 0, st>>>(F, pat, offs, lens, fixed_len, out, m, ctr);
+  kern<<<res < g ? res : g, 256, 0, st>>>(F, pat, offs, lens, fixed_len, out, out_rc, m, ctr);
   e = cudaGetLastError();
   cudaError_t e2 = lease.release(st);
   return e ? e : e2;
+}
+
+template <bool FIXED>
+static cudaError_t launch_approx(const qr_fm* fm, unsigned g, cudaStream_t st, const FmParams& F, const uint8_t* pat,
+                                 const uint64_t* offs, const uint32_t* lens, uint32_t fixed_len, uint32_t* out,
+                                 uint32_t* out_rc, uint64_t m, int kmax) {
+  if (out_rc) return launch_approx_s<FIXED, 2>(fm, g, st, F, pat, offs, lens, fixed_len, out, out_rc, m, kmax);
+  return launch_approx_s<FIXED, 1>(fm, g, st, F, pat, offs, lens, fixed_len, out, nullptr, m, kmax);
 }
 
 qr_status fm_count_device(const qr_fm* fm, const uint8_t* pat, const uint32_t* lengths, uint32_t fixed_len,
@@ -1198,7 +1227,7 @@ qr_status fm_count_device(const qr_fm* fm, const uint8_t* pat, const uint32_t* l
   unsigned long long* w = reinterpret_cast<unsigned long long*>(work);
   cudaError_t e;
   if (!lengths) {
-    if (approx) e = launch_approx<true>(fm, g, st, F, pat, nullptr, nullptr, fixed_len, out, m, approx);
+    if (approx) e = launch_approx<true>(fm, g, st, F, pat, nullptr, nullptr, fixed_len, out, out_rc, m, approx);
     else if (work) e = launch_fm<true, true>(fm, use_lean(fm), g, st, F, pat, nullptr, nullptr, fixed_len, out, out_rc, m, w);
     else      e = launch_fm<true, false>(fm, use_lean(fm), g, st, F, pat, nullptr, nullptr, fixed_len, out, out_rc, m, w);
     if (e) return cuda_fail(e, "k_fm_count");
@@ -1214,7 +1243,7 @@ qr_status fm_count_device(const qr_fm* fm, const uint8_t* pat, const uint32_t* l
   if ((e = cub::DeviceScan::ExclusiveSum(tmp, tb, offs, offs, (int64_t)m, st))) {
     cudaFreeAsync(offs, st); cudaFreeAsync(tmp, st); return cuda_fail(e, "scan");
   }
-  if (approx) e = launch_approx<false>(fm, g, st, F, pat, offs, lengths, 0, out, m, approx);
+  if (approx) e = launch_approx<false>(fm, g, st, F, pat, offs, lengths, 0, out, out_rc, m, approx);
   else if (work) e = launch_fm<false, true>(fm, use_lean(fm), g, st, F, pat, offs, lengths, 0, out, out_rc, m, w);
   else      e = launch_fm<false, false>(fm, use_lean(fm), g, st, F, pat, offs, lengths, 0, out, out_rc, m, w);
   cudaFreeAsync(offs, st);

@@ -631,3 +631,49 @@ def test_fm_host_variable_length_chunks(cuda):
     qr.qr_sync()
     assert np.array_equal(of, ref)
     assert np.array_equal(orc[-2000:], ora.count(rc_cat.astype(np.uint8), rc_off, lens[-2000:]))
+
+
+@pytest.mark.parametrize("kmax", [0, 1, 2, 3])
+@pytest.mark.parametrize("bwt_layout", [None, qr.QR_LAYOUT_QUADRANK16X2])
+@pytest.mark.parametrize("n,kind", [(40, 0), (20000, 0), (60000, 1)])
+def test_fm_count_approx_both_strands(cuda, n, kind, bwt_layout, kmax, fm_dyn_reset):
+    """Both strands within k substitutions in one launch: forward counts equal the oracle's
+    Hamming scan of P, reverse counts the scan of 3 - P reversed; device variable lengths, host
+    fixed lengths (reads of the paper's shape), both work orders."""
+    torch = _torch()
+    w = gen.dna(505 + n, n, kind)
+    sym = gen.unpack_dna(w, n)
+    fm = qr.qr_fm_build(w, n, bwt_layout=bwt_layout)
+    rng = np.random.default_rng(n + kmax)
+    pats = [rng.integers(0, 4, int(rng.integers(0, 26))).astype(np.uint8) for _ in range(150)]
+    for _ in range(150):
+        L = int(rng.integers(1, 26)); a = int(rng.integers(0, max(1, n - L + 1)))
+        p = sym[a:a + L].copy()
+        if rng.random() < 0.5:
+            p = (3 - p[::-1]).astype(np.uint8)                 # a reverse-strand occurrence
+        for _s in range(int(rng.integers(0, 3))):
+            if p.size:
+                k = int(rng.integers(0, p.size)); p[k] = (p[k] + 1 + rng.integers(0, 3)) % 4
+        pats.append(p)
+    rcs = [(3 - p[::-1]).astype(np.uint8) for p in pats]
+    cat, off, lens = oracle.pack_patterns(pats)
+    rcat, roff, rlens = oracle.pack_patterns(rcs)
+    ref_f = oracle.scan_count_hdk(sym, cat, off, lens, kmax)
+    ref_r = oracle.scan_count_hdk(sym, rcat, roff, rlens, kmax)
+    for dyn in (0, 1):
+        qr.qr_set_tuning("fm_dyn", dyn)
+        df = torch.empty(lens.size, dtype=torch.int32, device=cuda)
+        dr = torch.empty(lens.size, dtype=torch.int32, device=cuda)
+        qr.qr_fm_count_approx_both(fm, to_dev(cat, cuda), to_dev(lens, cuda), 0, kmax, df, dr, lens.size)
+        torch.cuda.synchronize()
+        assert np.array_equal(to_host(df).view(np.uint32), ref_f), dyn
+        assert np.array_equal(to_host(dr).view(np.uint32), ref_r), dyn
+    L, m = 30, 200
+    reads = gen.patterns(9, 2, m, L, w, n) if n > L else rng.integers(0, 4, m * L).astype(np.uint8)
+    roffs = np.arange(m, dtype=np.uint64) * L
+    rr = np.concatenate([3 - reads[i * L:(i + 1) * L][::-1] for i in range(m)]).astype(np.uint8)
+    hf, hr = np.zeros(m, np.uint32), np.zeros(m, np.uint32)
+    qr.qr_fm_count_approx_both(fm, reads, None, L, kmax, hf, hr, m)
+    qr.qr_sync()
+    assert np.array_equal(hf, oracle.scan_count_hdk(sym, reads, roffs, np.full(m, L, np.uint32), kmax))
+    assert np.array_equal(hr, oracle.scan_count_hdk(sym, rr, roffs, np.full(m, L, np.uint32), kmax))
