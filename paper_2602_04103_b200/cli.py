@@ -19,7 +19,8 @@ import numpy as np
 def _fm_count(args) -> int:
     import torch
 
-    from . import QR_LAYOUT_QUADRANK16, QR_LAYOUT_QUADRANK16X2, io, qr_fm_build, qr_fm_count_approx, qr_fm_count_both, qr_sync
+    from . import (QR_LAYOUT_QUADRANK16, QR_LAYOUT_QUADRANK16X2, io, qr_fm_build, qr_fm_count_approx,
+                   qr_fm_count_approx_both, qr_fm_count_both, qr_sync)
 
     t0 = time.perf_counter()
     recs = io.read_fasta(args.fasta, replace_invalid=args.replace_invalid)
@@ -38,13 +39,10 @@ def _fm_count(args) -> int:
     dcat, dlens = torch.from_numpy(cat).to(dev), torch.from_numpy(lens).to(dev)
     fwd = torch.empty(m, dtype=torch.int32, device=dev)
     rc = torch.empty(m, dtype=torch.int32, device=dev) if args.both_strands else None
-    if args.max_mismatches:
+    if args.max_mismatches and rc is not None:
+        qr_fm_count_approx_both(fm, dcat, dlens, 0, args.max_mismatches, fwd, rc, m)
+    elif args.max_mismatches:
         qr_fm_count_approx(fm, dcat, dlens, 0, args.max_mismatches, fwd, m)
-        if rc is not None:
-            rcat = np.concatenate([io.reverse_complement(cat[o:o + L]) for o, L in
-                                   zip(np.concatenate([[0], np.cumsum(lens[:-1], dtype=np.uint64)]).astype(np.int64), lens)])
-            qr_fm_count_approx(fm, torch.from_numpy(np.concatenate([rcat, np.zeros(8, np.uint8)])).to(dev), dlens, 0,
-                               args.max_mismatches, rc, m)
     elif rc is not None:
         qr_fm_count_both(fm, dcat, dlens, 0, fwd, rc, m)
     else:

@@ -376,6 +376,12 @@ def test_cli_fm_count(cuda, tmp_path):
     rcat, roff, rlens = oracle.pack_patterns([revcomp(r) for r in reads])
     assert [r[1] for r in rows] == list(oracle.scan_count(sym, cat, off, lens))
     assert [r[2] for r in rows] == list(oracle.scan_count(sym, rcat, roff, rlens))
+    # both strands within 2 substitutions (one launch, qr_fm_count_approx_both)
+    assert cli.main(["fm-count", "--fasta", str(fa), "--fastq", str(fq), "--both-strands", "--max-mismatches", "2",
+                     "--out", str(out)]) == 0
+    rows = [tuple(int(x) for x in line.split("\t")) for line in out.read_text().splitlines()]
+    assert [r[1] for r in rows] == list(oracle.scan_count_hdk(sym, cat, off, lens, 2))
+    assert [r[2] for r in rows] == list(oracle.scan_count_hdk(sym, rcat, roff, rlens, 2))
 
 
 @pytest.mark.parametrize("k", [0, 1, 5, 8, 10, 12, 13, 14])
