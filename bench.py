@@ -527,6 +527,7 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
+    oracle.set_threads(len(os.sched_getaffinity(0)))   # torchrun sets OMP_NUM_THREADS=1 per rank
     ora, q, prep = cpu_oracle_rank(per_step_q=1 << 24)
     for _ in range(args.warmup):
         ora.rank(q)
@@ -614,6 +615,7 @@ def main():
     if ctx.rank == 0 and ctx.world == 1 and not args.no_cpu:
         import oracle
 
+        oracle.set_threads(len(os.sched_getaffinity(0)))
         ora, q, prep = cpu_oracle_rank(per_step_q=1 << 27)
         t0 = time.perf_counter()
         reps = 0

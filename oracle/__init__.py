@@ -47,6 +47,7 @@ def lib():
             "or_scan_count_hd1": [u8p, C.c_uint64, u8p, u64p, u32p, C.c_uint64, u32p],
             "or_scan_count_hdk": [u8p, C.c_uint64, u8p, u64p, u32p, C.c_uint64, C.c_uint32, u32p],
             "or_threads": [],
+            "or_set_threads": [C.c_int],
         }
         for name, args in sig.items():
             f = getattr(L, name)
@@ -65,6 +66,11 @@ def _p(a, t):
 
 def threads() -> int:
     return int(lib().or_threads())
+
+
+def set_threads(n: int) -> None:
+    """Parallel-for width of the oracle (all host cores for the timed CPU baseline)."""
+    lib().or_set_threads(int(n))
 
 
 # ------------------------------------------------------------------ sigma = 2

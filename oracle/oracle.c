@@ -320,3 +320,6 @@ EXPORT void or_scan_count_hdk(const uint8_t* s, uint64_t n, const uint8_t* pat, 
 }
 
 EXPORT int or_threads(void) { return omp_get_max_threads(); }
+/* Threads of the parallel-for over queries (a launcher such as torchrun may have set
+ * OMP_NUM_THREADS=1 for every rank; the host baseline runs on rank 0 alone). */
+EXPORT void or_set_threads(int n) { if (n > 0) omp_set_num_threads(n); }

@@ -15,7 +15,7 @@ def _run(env_extra):
 
 
 def test_reference_arm_json_line():
-    r = _run({})
+    r = _run({"OMP_NUM_THREADS": "1"})          # as torchrun sets it for every rank
     assert r.returncode == 0, r.stderr[-2000:]
     lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
     assert len(lines) == 1
@@ -27,7 +27,8 @@ def test_reference_arm_json_line():
     assert d["higher_is_better"] is True and d["steps"] == 1 and d["warmup"] == 1
     assert d["config"]["workload"].startswith("configs[1]")
     cb = d["cpu_baseline"]
-    assert cb["kind"] == "oracle" and cb["value"] == d["value"] and cb["cores"] >= 1 and cb["sample"]
+    assert cb["kind"] == "oracle" and cb["value"] == d["value"] and cb["sample"]
+    assert cb["cores"] == len(os.sched_getaffinity(0))   # all host cores, whatever OMP_NUM_THREADS says
     assert d["e2e"] == {"value": d["value"], "unit": d["unit"], "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
 
 
