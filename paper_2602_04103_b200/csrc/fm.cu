@@ -834,9 +834,15 @@ __device__ __forceinline__ uint64_t approx_next(unsigned long long* ctr, uint64_
 #else
 #define QR_APPROX_LB __launch_bounds__(256)
 #endif
+// k = 1 runs 4 CTAs per SM (64 registers): +10% on the HBM-resident 150-bp reads, where the
+// search waits on DRAM (profiles/r01_reads_approx_minblocks.jsonl); k = 2, 3 keep the compiler's
+// choice (4 CTAs: -3% / -7%)
+#ifndef QR_APPROX1_MINB
+#define QR_APPROX1_MINB 4
+#endif
 
 template <bool FIXED, int BW, int STRANDS>
-__global__ void QR_APPROX_LB k_fm_approx1(FmParams F, const uint8_t* __restrict__ pat,
+__global__ void __launch_bounds__(256, QR_APPROX1_MINB) k_fm_approx1(FmParams F, const uint8_t* __restrict__ pat,
                                                     const uint64_t* __restrict__ offs,
                                                     const uint32_t* __restrict__ lens, uint32_t fixed_len,
                                                     uint32_t* __restrict__ out, uint32_t* __restrict__ out_rc,
