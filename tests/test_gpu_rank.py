@@ -394,3 +394,57 @@ def test_concurrent_streams_share_a_handle(cuda):
     for o in outs:
         assert np.array_equal(to_host(o), ref)
     assert np.array_equal(host_out, ref)
+
+
+def test_concurrent_host_threads(cuda):
+    """The header's promise: handles are usable from many host threads at once (ctypes drops the
+    GIL inside the library).  Four threads, each on its own stream, run device-pointer rank
+    batches (dynamic order: shared counter ring), staged host-pointer batches (shared internal
+    streams) and FM counts against one BiRank and one FM handle; every result matches."""
+    import threading
+
+    import torch
+
+    n = (1 << 27) + 5
+    w = gen.bits(600, n)
+    h = qr.qr_birank_build(w, n)
+    ora = oracle.BitsOracle(w, n)
+    nf = 100000
+    tf = gen.dna(601, nf)
+    fm = qr.qr_fm_build(tf, nf)
+    L, mp = 20, 20000
+    pats = gen.patterns(602, 0, mp, L, tf, nf)
+    ref_fm = oracle.FmOracle(gen.unpack_dna(tf, nf)).count(pats, np.arange(mp, dtype=np.uint64) * L,
+                                                          np.full(mp, L, np.uint32))
+    errors = []
+
+    def work(tid):
+        try:
+            s = torch.cuda.Stream()
+            for it in range(3):
+                m = (1 << 22) + 17 * tid + it
+                q = gen.queries(610 + 10 * tid + it, n, m)
+                dq = to_dev(q, cuda)
+                out = torch.empty_like(dq)
+                qr.qr_rank(h, dq, None, out, stream=s)
+                hq = gen.queries(700 + 10 * tid + it, n, 300000)
+                hout = np.zeros(hq.size, np.uint64)
+                qr.qr_rank(h, hq, None, hout, stream=s)
+                d = torch.empty(mp, dtype=torch.int32, device=cuda)
+                qr.qr_fm_count(fm, to_dev(pats, cuda), None, L, d, mp, stream=s)
+                s.synchronize()
+                if not np.array_equal(to_host(out), ora.rank(q)):
+                    errors.append((tid, it, "device rank"))
+                if not np.array_equal(hout, ora.rank(hq)):
+                    errors.append((tid, it, "staged rank"))
+                if not np.array_equal(to_host(d).view(np.uint32), ref_fm):
+                    errors.append((tid, it, "fm count"))
+        except Exception as e:  # noqa: BLE001
+            errors.append((tid, repr(e)))
+
+    ts = [threading.Thread(target=work, args=(t,)) for t in range(4)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errors, errors
