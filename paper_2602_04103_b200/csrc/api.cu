@@ -34,6 +34,8 @@ int g_rank_smem_threads = 0;    // cluster rank kernels: CTA size (0 auto: 1024,
 int g_rank_smem_k = 0;          // cluster rank kernels: queries per lane pair per group (0 auto, 1, 2, 4 @1024 thr, 6 @768, 8 @512)
 int g_rank_lane_table = 1;      // one-lane kernels take the superblock words from a per-CTA shared-memory table when small
 int g_rank_resident = 1;        // structures that fit one CTA's shared memory are queried from a per-CTA copy
+int g_rank_big_pack = 0;        // 1: also build the large-n (CS-CTA cluster) BiRank16 table below n = 2^35 (tests)
+int g_rank_big_cs = 0;          // cluster size of that table: 0 smallest that fits, else 4, 8 or 16
 int g_rank_pair = 2;            // kernel shape: 2 by structure size (default), 1 lane pairs (one L2 request per query), 0 one lane per query
 uint64_t g_stage_chunk = 1ull << 23;   // queries per chunk on the staged host path (sweep: profiles/r01_e2e_sweep)
 int g_stage_slots = 3;                 // device buffers / internal streams of the staged path
@@ -360,6 +362,12 @@ QR_EXPORT qr_status qr_set_tuning(const char* key, int64_t value) {
   } else if (!strcmp(key, "rank_resident")) {
     if (value != 0 && value != 1) return fail(QR_EINVAL, "rank_resident must be 0 or 1");
     g_rank_resident = (int)value;
+  } else if (!strcmp(key, "rank_big_pack")) {
+    if (value != 0 && value != 1) return fail(QR_EINVAL, "rank_big_pack must be 0 or 1");
+    g_rank_big_pack = (int)value;
+  } else if (!strcmp(key, "rank_big_cs")) {
+    if (value != 0 && value != 4 && value != 8 && value != 16) return fail(QR_EINVAL, "rank_big_cs must be 0, 4, 8 or 16");
+    g_rank_big_cs = (int)value;
   } else if (!strcmp(key, "rank_dyn")) {
     if (value != 0 && value != 1) return fail(QR_EINVAL, "rank_dyn must be 0 or 1");
     g_rank_dyn = (int)value;
@@ -847,6 +855,7 @@ QR_EXPORT void qr_free(qr_index* h) {
   if (h->lines) cudaFree(h->lines);
   if (h->super) cudaFree(h->super);
   if (h->spack) cudaFree(h->spack);
+  if (h->spack_big) cudaFree(h->spack_big);
   delete h;
 }
 

@@ -316,6 +316,7 @@ extern int g_rank_blocks_per_sm;
 extern int g_rank_pair;
 extern int g_rank_lane_table;
 extern int g_index64;
+extern int g_rank_smem;
 extern int g_rank_s_lane;
 
 template <int K>
@@ -353,6 +354,8 @@ static cudaError_t bi_rank_k(const qr_index* h, const uint64_t* q, const uint8_t
 cudaError_t launch_birank_rank(const qr_index* h, const uint64_t* q, const uint8_t* c, uint64_t* out, uint64_t m,
                                cudaStream_t st) {
   if (m == 0) return cudaSuccess;
+  // n >= 2^35 (or forced for tests): superblock words from a CS-CTA cluster table (sbcache.cu)
+  if (h->spack_big && g_rank_smem != 0 && m >= (1ull << 22) && !g_index64) return launch_big_pack_rank(h, q, c, out, m, st);
   const int shape = rank_shape(h, m);
   if (shape == RANK_CLUSTER) return launch_super_pack_rank(h, q, c, out, m, 0, st);
   if (shape == RANK_LANE && g_rank_lane_table) {

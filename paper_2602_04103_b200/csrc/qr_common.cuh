@@ -43,6 +43,9 @@ struct qr_index {
   int sm_count;
   uint64_t* spack;      // superblock array re-encoded for the shared-memory rank kernels (sbcache.cu), or null
   uint64_t spack_half;  // groups held by each CTA of the 2-CTA cluster
+  uint64_t* spack_big = nullptr;   // BiRank16 n >= 2^35: 5-superblock groups over a CS-CTA cluster (sbcache.cu)
+  uint64_t spack_big_slots = 0;    // groups per CTA
+  uint32_t spack_big_cs = 0;       // cluster size (4, 8 or 16)
 };
 
 struct qr_fm {
@@ -100,6 +103,8 @@ inline uint64_t kmer_c_offset(int k) { return (kmer_entries(k) + 1) & ~1ull; }
 qr_status fm_count_device(const qr_fm* fm, const uint8_t* pat, const uint32_t* lengths, uint32_t fixed_len,
                           uint32_t* out, uint32_t* out_rc, uint64_t m, uint64_t* work, cudaStream_t st,
                           int approx = 0);
+cudaError_t launch_big_pack_rank(const qr_index* h, const uint64_t* q, const uint8_t* c, uint64_t* out, uint64_t m,
+                                 cudaStream_t st);
 qr_status build_super_pack(qr_index* h, cudaStream_t st);
 uint64_t super_pack_cta_bytes(const qr_index* h);
 int super_pack_clusters(const qr_index* h);

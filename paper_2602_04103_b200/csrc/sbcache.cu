@@ -83,9 +83,12 @@ uint64_t super_pack_cta_bytes(const qr_index* h) {
 
 // Build h->spack from h->super (stream-ordered).  Leaves spack null (no error) when the layout
 // is outside the encoding's range or the half table exceeds a CTA's shared memory.
+qr_status build_super_pack_big(qr_index* h, cudaStream_t st);
+
 qr_status build_super_pack(qr_index* h, cudaStream_t st) {
   h->spack = nullptr;
   h->spack_half = 0;
+  if (qr_status sb = build_super_pack_big(h, st)) return sb;
   if (h->layout != QR_LAYOUT_BIRANK16 && h->layout != QR_LAYOUT_QUADRANK16 && h->layout != QR_LAYOUT_BIRANK16X2 &&
       h->layout != QR_LAYOUT_QUADRANK16X2)
     return QR_OK;
@@ -104,6 +107,60 @@ qr_status build_super_pack(qr_index* h, cudaStream_t st) {
   else    k_qd_pack_super<<<g, 256, 0, st>>>(h->super, h->n_super, groups, half, h->spack);
   if ((e = cudaGetLastError())) { cudaFree(h->spack); h->spack = nullptr; return cuda_fail(e, "pack superblocks"); }
   h->spack_half = half;
+  return QR_OK;
+}
+
+// ------------------------------------------------------------------ BiRank16 beyond 2^35 bits
+// The 2-CTA table above needs s < 2^24 (n < 2^35) and half of it must fit one CTA (n <= ~2^34.4).
+// For larger bit vectors (the paper's own 4 GiB, is n = 2^35) the superblock words go
+// to a wider cluster instead: groups of 5 superblocks per u64 — bits [0,32) s_{5g}, byte k-1 at
+// bit 32 + 8(k-1) = s_{5g+k} - s_{5g} (k = 1..4, <= 4 * 31) — group g at CTA g % CS, slot g / CS,
+// CS = 4, 8 or 16 CTAs of one cluster (<= 112 KB each: n up to 2^36 bits).
+__global__ void k_bi_pack_super5(const uint32_t* __restrict__ super, uint64_t n_super, uint64_t groups,
+                                 uint64_t slots, uint32_t cs_log, uint64_t* __restrict__ pack) {
+  for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < groups; g += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t i0 = 5 * g;
+    const uint32_t s0 = super[i0];
+    uint64_t w = s0;
+#pragma unroll
+    for (int k = 1; k < 5; ++k)
+      if (i0 + k < n_super) w |= (uint64_t)(super[i0 + k] - s0) << (24 + 8 * k);
+    pack[(g & ((1ull << cs_log) - 1)) * slots + (g >> cs_log)] = w;
+  }
+}
+
+extern int g_rank_big_pack;
+extern int g_rank_big_cs;
+
+qr_status build_super_pack_big(qr_index* h, cudaStream_t st) {
+  h->spack_big = nullptr;
+  h->spack_big_slots = 0;
+  h->spack_big_cs = 0;
+  if (h->layout != QR_LAYOUT_BIRANK16 || h->n_super == 0) return QR_OK;
+  if (h->n < (1ull << 35) && !g_rank_big_pack) return QR_OK;
+  const uint64_t groups = (h->n_super + 4) / 5;
+  const uint64_t cap = (uint64_t)max_dyn_smem(h->device);
+  uint32_t cs = 0;
+  // the smallest cluster whose per-CTA part is <= 112 KB: a larger part leaves the L1 too little
+  // room for the line misses in flight (n = 2^35: 35.4 Gq/s at 4 CTAs x 216 KB, 42.5 at 8 x 108 KB,
+  // 38.6 at 16 x 54 KB; profiles/r01_big_cs_probe.jsonl)
+  constexpr uint64_t PART_MAX = 112 * 1024;
+  for (uint32_t c = 4; c <= 16; c *= 2) {
+    const uint64_t slots = (((groups + c - 1) / c) + 1) & ~1ull;      // even: 16-B copies
+    const bool fits = slots * 8 + 1024 <= cap;
+    if (g_rank_big_cs ? (c == (uint32_t)g_rank_big_cs && fits) : (fits && slots * 8 <= PART_MAX)) { cs = c; break; }
+  }
+  if (!cs) return QR_OK;                                              // n > ~2^36: global kernels
+  const uint32_t cs_log = cs == 4 ? 2 : cs == 8 ? 3 : 4;
+  const uint64_t slots = (((groups + cs - 1) / cs) + 1) & ~1ull;
+  cudaError_t e = cudaMalloc((void**)&h->spack_big, cs * slots * 8);
+  if (e) { h->spack_big = nullptr; return cuda_fail(e, "alloc large superblock table"); }
+  cudaMemsetAsync(h->spack_big, 0, cs * slots * 8, st);
+  k_bi_pack_super5<<<grid_stride_blocks(groups, 256, h->sm_count, 8), 256, 0, st>>>(h->super, h->n_super, groups, slots,
+                                                                                    cs_log, h->spack_big);
+  if ((e = cudaGetLastError())) { cudaFree(h->spack_big); h->spack_big = nullptr; return cuda_fail(e, "pack superblocks"); }
+  h->spack_big_slots = slots;
+  h->spack_big_cs = cs;
   return QR_OK;
 }
 
@@ -231,6 +288,78 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     }
   }
   cluster_barrier();   // the peer may still read this CTA's half of the table
+}
+
+// BiRank16 rank over the CS-CTA table (n >= 2^35): the k_bi_rank2c structure with 64-bit line
+// indices and lane 1 of a pair reading s from the CTA g % CS of its cluster.
+template <int K, int THREADS, bool HAS_C>
+__global__ void __launch_bounds__(THREADS, 1)
+    k_bi_rank2v(const uint4* __restrict__ lines, const uint64_t* __restrict__ pack, uint64_t slots, uint32_t cs_log,
+                const uint64_t* __restrict__ q, const uint8_t* __restrict__ cs, uint64_t* __restrict__ out, uint64_t m,
+                uint64_t last_line, unsigned long long* ctr) {
+  extern __shared__ uint64_t sc_smem[];
+  {
+    const uint4* src = reinterpret_cast<const uint4*>(pack + (uint64_t)cluster_rank() * slots);
+    uint4* dst = reinterpret_cast<uint4*>(sc_smem);
+    for (uint32_t i = threadIdx.x; i < (uint32_t)(slots >> 1); i += blockDim.x) dst[i] = __ldg(src + i);
+    cluster_barrier();
+  }
+  const uint32_t local = (uint32_t)__cvta_generic_to_shared(sc_smem);
+  const uint32_t csm = (1u << cs_log) - 1u;
+  const uint32_t half = threadIdx.x & 1u;
+  const uint32_t pw = (threadIdx.x & 31u) >> 1;
+  ScSched sc = sc_first<K, true, 16>(ctr);
+  uint64_t qn[K];
+  sc_load_q<K>(q, sc.gb + pw, sc.stride, m, qn);
+  while (sc.gb < m) {
+    const uint64_t i0 = sc.gb + pw;
+    uint64_t qq[K], jj[K];
+    uint32_t pp[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      qq[k] = qn[k];
+      uint64_t j = qq[k] / BI_B;
+      j = j > last_line ? last_line : j;                           // q > n: memory-safe clamp
+      const uint64_t p = 16 + qq[k] - j * BI_B;
+      pp[k] = p > 511 ? 511u : (uint32_t)p;
+      jj[k] = j;
+    }
+    uint64_t w[K][4];
+    uint32_t s[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      w[k][0] = w[k][1] = w[k][2] = w[k][3] = 0;
+      if (half == 0 || pp[k] >= 256) ld_sector_na(lines + 4 * jj[k] + 2 * half, w[k][0], w[k][1], w[k][2], w[k][3]);
+      s[k] = 0;
+      if (half) {
+        const uint32_t sb = (uint32_t)(jj[k] >> BI_SB_LOG), g = sb / 5u, kk = sb - 5u * g;
+        const uint64_t v = ld_dsmem_u64(map_to_rank(local, g & csm) + (g >> cs_log) * 8u);
+        s[k] = kk ? (uint32_t)v + ((uint32_t)(v >> (24u + 8u * kk)) & 0xffu) : (uint32_t)v;
+      }
+    }
+    const uint64_t stride = sc.stride;
+    sc = sc_next<K, true, 16>(sc, ctr);
+    sc_load_q<K>(q, sc.gb + pw, sc.stride, m, qn);
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const uint64_t idx = i0 + (uint64_t)k * stride;
+      const bool right = pp[k] >= 256;
+      const int x = (int)(pp[k] & 255u);
+      const bool mine = half ? right : !right;
+      const uint64_t inv = half ? 0ull : ~0ull;
+      uint32_t cnt = 0;
+#pragma unroll
+      for (int t = 0; t < 4; ++t) cnt += __popcll(w[k][t] & (prefix_mask(x, t) ^ inv));
+      cnt = mine ? cnt : 0u;
+      uint64_t v = (half ? (uint64_t)cnt : (w[k][0] & 0xffffull) - cnt) + ((uint64_t)s[k] << BI_SHIFT);
+      v += __shfl_xor_sync(0xffffffffu, v, 1);
+      if (HAS_C) {
+        if (half == 0 && idx < m && cs[idx] == 0) v = qq[k] - v;
+      }
+      if (half == 0 && idx < m) st_stream_u64(out + idx, v);
+    }
+  }
+  cluster_barrier();   // the peers may still read this CTA's part of the table
 }
 
 // ------------------------------------------------------------------ QuadRank16 rank(q,c), rank_4(q)
@@ -1084,6 +1213,64 @@ cudaError_t launch_lane_table_rank(const qr_index* h, const uint64_t* q, const u
   }
   if (what == 0) return go(k_qd_rank1s<K, 0, false>, k_qd_rank1s<K, 0, true>, c);
   return go(k_qd_rank1s<K, 1, false>, k_qd_rank1s<K, 1, true>, nullptr);
+}
+
+// rank over the CS-CTA table (h->spack_big): dynamic order, 1024-thread CTAs, one per SM, as many
+// CS-clusters as the occupancy API allows.
+cudaError_t launch_big_pack_rank(const qr_index* h, const uint64_t* q, const uint8_t* c, uint64_t* out, uint64_t m,
+                                 cudaStream_t st) {
+  if (m == 0) return cudaSuccess;
+  const uint32_t cs = h->spack_big_cs, cs_log = cs == 4 ? 2 : cs == 8 ? 3 : 4;
+  const size_t smem = (size_t)h->spack_big_slots * 8;
+  auto kern = c ? k_bi_rank2v<4, 1024, true> : k_bi_rank2v<4, 1024, false>;
+  static std::mutex mu;
+  static std::map<std::tuple<const void*, int, uint32_t, size_t>, unsigned> grids;
+  unsigned grid = 0;
+  {
+    std::lock_guard<std::mutex> g(mu);
+    const auto key = std::make_tuple((const void*)kern, h->device, cs, smem);
+    auto it = grids.find(key);
+    if (it != grids.end()) {
+      grid = it->second;
+    } else {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (cs > 8) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3((unsigned)h->sm_count / cs * cs);
+      cfg.blockDim = dim3(1024);
+      cfg.dynamicSmemBytes = smem;
+      cudaLaunchAttribute attr;
+      attr.id = cudaLaunchAttributeClusterDimension;
+      attr.val.clusterDim.x = cs; attr.val.clusterDim.y = 1; attr.val.clusterDim.z = 1;
+      cfg.attrs = &attr;
+      cfg.numAttrs = 1;
+      int clusters = 0;
+      if (cudaOccupancyMaxActiveClusters(&clusters, kern, &cfg) != cudaSuccess || clusters <= 0) {
+        cudaGetLastError();
+        clusters = 1;
+      }
+      grid = grids[key] = (unsigned)clusters * cs;
+    }
+  }
+  CounterLease lease;
+  unsigned long long* ctr = nullptr;
+  cudaError_t e = lease.acquire(h->device, st, &ctr);
+  if (e) return e;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(1024);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr;
+  attr.id = cudaLaunchAttributeClusterDimension;
+  attr.val.clusterDim.x = cs; attr.val.clusterDim.y = 1; attr.val.clusterDim.z = 1;
+  cfg.attrs = &attr;
+  cfg.numAttrs = 1;
+  e = cudaLaunchKernelEx(&cfg, kern, (const uint4*)h->lines, (const uint64_t*)h->spack_big, (uint64_t)h->spack_big_slots,
+                         cs_log, q, c, out, m, (uint64_t)(h->n_lines - 1), ctr);
+  if (!e) e = cudaGetLastError();
+  cudaError_t e2 = lease.release(st);
+  return e ? e : e2;
 }
 
 // what: 0 = rank (sigma 2 or 4), 1 = rank_4 (sigma 4), 3 = BiRank gather ceiling of this kernel shape

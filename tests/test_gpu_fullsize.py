@@ -185,3 +185,31 @@ def test_birank_beyond_2_36_bits(cuda):
     qr.qr_rank(h, dq, None, ob)
     torch.cuda.synchronize()
     assert np.array_equal(to_host(ob), ora.rank(bq))
+
+
+def test_birank_2_35_bits_cluster_table(cuda):
+    """The paper's own bit-vector size (4 GiB): n = 2^35 + 777 takes the 4-CTA
+    cluster table kernel; sampled and boundary queries vs the oracle."""
+    torch = _torch()
+    n, m = (1 << 35) + 777, 10**7
+    bits = torch.empty((n + 63) // 64, dtype=torch.uint64, device=cuda)
+    gen.bits_dev(35, n, 0.5, bits)
+    h = qr.qr_birank_build(bits, n)
+    del bits
+    q = torch.empty(m, dtype=torch.uint64, device=cuda)
+    gen.queries_dev(38, n, m, q)
+    out = torch.empty_like(q)
+    qr.qr_rank(h, q, None, out)
+    torch.cuda.synchronize()
+    assert bool((out.view(torch.int64) <= q.view(torch.int64)).all())
+    ora = oracle.BitsOracle(gen.bits(35, n, 0.5), n)
+    for off in sample_offsets(m, 35)[:16]:
+        qs = gen.queries(38, n, RUN, i0=int(off))
+        assert np.array_equal(to_host(out[off:off + RUN]), ora.rank(qs)), f"offset {off}"
+    bq = np.concatenate([boundary_queries(n, B, S, 240, limit=20000), np.arange(n - 3000, n + 1, dtype=np.uint64)])
+    bq = np.concatenate([bq, gen.queries(39, n, (1 << 22) - bq.size + 5)])   # >= 2^22: the cluster path
+    dq = to_dev(bq, cuda)
+    ob = torch.empty_like(dq)
+    qr.qr_rank(h, dq, None, ob)
+    torch.cuda.synchronize()
+    assert np.array_equal(to_host(ob), ora.rank(bq))

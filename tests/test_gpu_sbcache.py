@@ -477,3 +477,25 @@ def test_resident_structure_parity(cuda, smem_mode, resident, nb, n4):
         assert np.array_equal(_rank4(h4, q4, cuda, 1), ora4.rank_all4(q4))
     finally:
         qr.qr_set_tuning("rank_resident", 1)
+
+
+@pytest.mark.parametrize("cs", [4, 8, 16])
+@pytest.mark.parametrize("n_sb,extra", [(1, 5), (37, 1234), (401, 77)])
+def test_large_table_cluster_kernel_parity(cuda, smem_mode, cs, n_sb, extra):
+    """The BiRank16 table for n >= 2^35 (5-superblock groups with a 32-bit base over a 4/8/16-CTA
+    cluster), forced onto small n: rank and rank with c on >= 2^22 queries + the boundary set."""
+    qr.qr_set_tuning("rank_big_pack", 1)
+    qr.qr_set_tuning("rank_big_cs", cs)
+    try:
+        n = n_sb * S + extra
+        w = gen.bits(800 + n_sb, n)
+        h = qr.qr_birank_build(w, n)
+    finally:
+        qr.qr_set_tuning("rank_big_pack", 0)
+        qr.qr_set_tuning("rank_big_cs", 0)
+    m = (1 << 22) + 11
+    q = np.concatenate([gen.queries(801, n, m), boundary_queries(n, B, S, 240, limit=20000)])
+    ora = oracle.BitsOracle(w, n)
+    assert np.array_equal(_rank(h, q, None, cuda, 1), ora.rank(q))
+    c = (gen.queries(802, 1, q.size, with_c=True)[1] & 1).astype(np.uint8)
+    assert np.array_equal(_rank(h, q, c, cuda, 1), ora.rank(q, c))
