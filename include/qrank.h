@@ -267,6 +267,10 @@ const char* qr_last_error(void);
  *                      CTA of a one-CTA-per-SM grid and queried from there (lines swizzled over
  *                      the banks), for batches whose 16 B/query of I/O is >= 2x the bytes all
  *                      the copies read; 0: lines from L2.
+ *   "rank_big_pack"    1: also build the large-n BiRank16 superblock table (normally only for
+ *                      n >= 2^35: 5 superblocks per u64, 32-bit base, split over a 4/8/16-CTA
+ *                      cluster, <= 112 KB per CTA) for handles built afterwards — for tests.
+ *   "rank_big_cs"      0 (default): the smallest cluster size meeting that bound; 4, 8, 16: force.
  *   "rank_smem"        the 2-CTA cluster shared-memory kernels: 0 never, 1 (default) by
  *                      structure size for batches >= 2^22, 2 whenever the table exists.
  *   "rank_s_lane"      global lane-pair kernels: which lane of a pair loads the superblock word.
