@@ -18,7 +18,7 @@ def t(fn, reps=3):
 n, L = 1 << 30, 150
 text = torch.empty((n + 31) // 32 + 1, dtype=torch.uint64, device=dev); gen.dna_dev(5, n, 1, text)
 for name, lay in (("quadrank16", qr.QR_LAYOUT_QUADRANK16), ("quadrank16x2", qr.QR_LAYOUT_QUADRANK16X2)):
-    fm = qr.qr_fm_build(text, n, bwt_layout=lay)
+    fm = qr.qr_fm_build(text, n, bwt_layout=lay, kmer_k=int(os.environ.get("QR_PROBE_K", "-1")))
     for k, m in ((0, 10**7), (1, 10**6), (2, 10**5)):
         pats = torch.empty(m * L, dtype=torch.uint8, device=dev); gen.patterns_dev(55, 2, m, L, text, n, pats)
         of = torch.empty(m, dtype=torch.int32, device=dev); orc = torch.empty_like(of)
