@@ -91,12 +91,12 @@ __global__ void k_sa_init(const uint64_t* __restrict__ text, uint64_t n, uint64_
 // is the sorted position of the first member of suffix i's group (its group start), so for a
 // singleton it is its final SA position; pos[k] is the SA position the k-th active item occupies
 // (increasing in k, and each group is a contiguous run), so after a round's sort the k-th item
-// lands at SA[pos[k]].  On the block-repeat text of configs[4] ~25% of the suffixes survive the
+// lands at SA[pos[k]].  On the block-repeat text of configs[4] ~39% of the suffixes survive the
 // first round and ~1% the fifth, against a full 2^30-item sort in every round before.
 
-__global__ void k_sa_iota(uint32_t* __restrict__ pos, uint64_t N) {
-  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < N; j += (uint64_t)gridDim.x * blockDim.x)
-    pos[j] = (uint32_t)j;
+// pos == nullptr: the identity (round 0, every suffix active in SA order)
+__device__ __forceinline__ uint32_t sa_pos(const uint32_t* __restrict__ pos, uint64_t k) {
+  return pos ? pos[k] : (uint32_t)k;
 }
 
 __device__ __forceinline__ bool sa_head(const uint64_t* __restrict__ K, uint64_t k) {
@@ -107,7 +107,7 @@ __device__ __forceinline__ bool sa_head(const uint64_t* __restrict__ K, uint64_t
 __global__ void k_sa_heads(const uint64_t* __restrict__ K, const uint32_t* __restrict__ pos, uint64_t A,
                            uint32_t* __restrict__ gs) {
   for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < A; k += (uint64_t)gridDim.x * blockDim.x)
-    gs[k] = sa_head(K, k) ? pos[k] : 0u;
+    gs[k] = sa_head(K, k) ? sa_pos(pos, k) : 0u;
 }
 
 struct MaxU32 {
@@ -124,7 +124,7 @@ __global__ void k_sa_place(const uint64_t* __restrict__ K, const uint32_t* __res
   for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < A; k += (uint64_t)gridDim.x * blockDim.x) {
     const uint32_t v = V[k], g = gs[k];
     const uint64_t key = K[k];
-    sa[pos[k]] = v;
+    sa[sa_pos(pos, k)] = v;
     if (gshift == 0 || (uint32_t)(key >> gshift) != g) rank[v] = g;
     const bool single = (k == 0 || key != K[k - 1]) && (k + 1 == A || K[k + 1] != key);
     flag[k] = single ? 0u : 1u;
@@ -143,12 +143,20 @@ __global__ void k_sa_compact(const uint64_t* __restrict__ K, const uint32_t* __r
     const bool single = sa_head(K, k) && (k + 1 == A || K[k + 1] != K[k]);
     if (!single) {
       const uint32_t o = off[k];
-      pos_out[o] = pos[k];
+      pos_out[o] = sa_pos(pos, k);
       g_out[o] = gs[k];
       i_out[o] = V[k];
     }
     if (k + 1 == A) *count = (unsigned long long)off[k] + (single ? 0u : 1u);
   }
+}
+
+// survivors of a round from the exclusive sum of its flags: off[A-1] + [item A-1 stays active]
+__global__ void k_sa_survivors(const uint64_t* __restrict__ K, const uint32_t* __restrict__ off, uint64_t A,
+                               unsigned long long* __restrict__ count) {
+  const uint64_t k = A - 1;
+  const bool single = sa_head(K, k) && (k + 1 == A || K[k + 1] != K[k]);
+  *count = (unsigned long long)off[k] + (single ? 0u : 1u);
 }
 
 // doubling key of active item k (suffix i = ii[k], group start gg[k]): (gg[k], rank of the suffix
@@ -170,8 +178,9 @@ static int bits_for(uint64_t x) {  // bits needed to represent values 0..x
   return b ? b : 1;
 }
 
-// d_sa: N u32 outputs.  The temporaries (40 B per suffix + the sort's scratch) are one
-// cudaMalloc arena: the stream-ordered pool maps and unmaps large blocks ~50x slower (43 GB:
+// d_sa: N u32 outputs.  The temporaries (32 B per suffix + the sort's scratch, then 8 B per
+// survivor of round 0) are
+// cudaMalloc arenas: the stream-ordered pool maps and unmaps large blocks ~50x slower (43 GB:
 // 0.27 s to map and 0.26-1.2 s to release vs 0.004 / 0.01 s, profiles/r01_alloc_probe.jsonl).
 // The caller's stream is synchronised every round (survivor count) and before the free.
 static qr_status build_sa(const uint64_t* d_text, uint64_t n, int sms, cudaStream_t st, uint32_t* d_sa) {
@@ -184,8 +193,11 @@ static qr_status build_sa(const uint64_t* d_text, uint64_t n, int sms, cudaStrea
   char* arena = nullptr;
   size_t tmp_bytes = 0;
   cudaError_t e;
+  char* pos_arena = nullptr;             // the two survivor lists, sized after round 0
   auto cleanup = [&]() {
-    if (arena) { cudaStreamSynchronize(st); cudaFree(arena); }
+    if (arena || pos_arena) cudaStreamSynchronize(st);
+    if (arena) cudaFree(arena);
+    if (pos_arena) cudaFree(pos_arena);
     if (h_count) cudaFreeHost(h_count);
   };
   auto bail = [&](cudaError_t err, const char* what) { cleanup(); return cuda_fail(err, what); };
@@ -200,14 +212,14 @@ static qr_status build_sa(const uint64_t* d_text, uint64_t n, int sms, cudaStrea
     tmp_bytes = tmp_bytes > need3 ? tmp_bytes : need3;
   }
   const size_t u32N = (N * 4 + 255) & ~(size_t)255, u64N = (N * 8 + 255) & ~(size_t)255;
-  const size_t arena_bytes = 2 * u64N + 6 * u32N + 256 + ((tmp_bytes + 255) & ~(size_t)255);
+  const size_t arena_bytes = 2 * u64N + 4 * u32N + 256 + ((tmp_bytes + 255) & ~(size_t)255);
   if ((e = cudaMalloc((void**)&arena, arena_bytes))) { arena = nullptr; return bail(e, "sa scratch"); }
   if ((e = cudaMallocHost((void**)&h_count, 8))) return bail(e, "sa host count");
   {
     char* p = arena;
     ka = reinterpret_cast<uint64_t*>(p); p += u64N;
     kb = reinterpret_cast<uint64_t*>(p); p += u64N;
-    uint32_t** u32s[6] = {&va, &vb, &rank, &gs, &pa, &pb};
+    uint32_t** u32s[4] = {&va, &vb, &rank, &gs};
     for (auto q : u32s) { *q = reinterpret_cast<uint32_t*>(p); p += u32N; }
     count = reinterpret_cast<unsigned long long*>(p); p += 256;
     tmp = p;
@@ -216,7 +228,6 @@ static qr_status build_sa(const uint64_t* d_text, uint64_t n, int sms, cudaStrea
   auto grid = [&](uint64_t items) { return grid_stride_blocks(items, 256, sms, 16); };
   // round 0: every suffix active, keyed by its first 21 characters
   k_sa_init<<<grid(N), 256, 0, st>>>(d_text, n, ka, va);
-  k_sa_iota<<<grid(N), 256, 0, st>>>(pa, N);
   uint64_t A = N, h = 21;
   int bits = 63;
   uint64_t* kin = ka;                        // keys of the round are written here
@@ -227,15 +238,28 @@ static qr_status build_sa(const uint64_t* d_text, uint64_t n, int sms, cudaStrea
     cub::DoubleBuffer<uint32_t> V(va, vb);
     size_t tb = tmp_bytes;
     if ((e = cub::DeviceRadixSort::SortPairs(tmp, tb, K, V, (int64_t)A, 0, bits, st))) return bail(e, "sort");
-    k_sa_heads<<<grid(A), 256, 0, st>>>(K.Current(), pa, A, gs);
+    k_sa_heads<<<grid(A), 256, 0, st>>>(K.Current(), round ? pa : nullptr, A, gs);
     tb = tmp_bytes;
     if ((e = cub::DeviceScan::InclusiveScan(tmp, tb, gs, gs, MaxU32(), (int64_t)A, st))) return bail(e, "scan");
     uint32_t* flag = V.Alternate();          // free after the sort; becomes the offsets
-    k_sa_place<<<grid(A), 256, 0, st>>>(K.Current(), V.Current(), pa, gs, A, round ? b : 0, d_sa, rank, flag);
+    k_sa_place<<<grid(A), 256, 0, st>>>(K.Current(), V.Current(), round ? pa : nullptr, gs, A, round ? b : 0, d_sa, rank,
+                                        flag);
     tb = tmp_bytes;
     if ((e = cub::DeviceScan::ExclusiveSum(tmp, tb, flag, flag, (int64_t)A, st))) return bail(e, "scan");
     carry = reinterpret_cast<uint32_t*>(K.Alternate());   // free after the sort: 2N u32
-    k_sa_compact<<<grid(A), 256, 0, st>>>(K.Current(), V.Current(), pa, gs, flag, A, pb, carry, carry + N, count);
+    if (round == 0) {
+      // the survivor lists are sized by round 0's survivors (peak 32 + 8 * A1/N bytes per suffix
+      // instead of 40, so that n up to 2^32 - 2 builds within a B200's HBM)
+      k_sa_survivors<<<1, 1, 0, st>>>(K.Current(), flag, A, count);
+      cudaMemcpyAsync(h_count, count, 8, cudaMemcpyDeviceToHost, st);
+      if ((e = cudaStreamSynchronize(st))) return bail(e, "sa round sync");
+      const size_t u32A = ((*h_count ? *h_count : 1) * 4 + 255) & ~(size_t)255;
+      if ((e = cudaMalloc((void**)&pos_arena, 2 * u32A))) { pos_arena = nullptr; return bail(e, "sa positions"); }
+      pb = reinterpret_cast<uint32_t*>(pos_arena);
+      pa = reinterpret_cast<uint32_t*>(pos_arena + u32A);
+    }
+    k_sa_compact<<<grid(A), 256, 0, st>>>(K.Current(), V.Current(), round ? pa : nullptr, gs, flag, A, pb, carry,
+                                          carry + N, count);
     cudaMemcpyAsync(h_count, count, 8, cudaMemcpyDeviceToHost, st);
     if ((e = cudaStreamSynchronize(st))) return bail(e, "sa round sync");
     A = *h_count;

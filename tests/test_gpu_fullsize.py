@@ -213,3 +213,11 @@ def test_birank_2_35_bits_cluster_table(cuda):
     qr.qr_rank(h, dq, None, ob)
     torch.cuda.synchronize()
     assert np.array_equal(to_host(ob), ora.rank(bq))
+
+
+def test_fm_near_u32_limit(cuda):
+    """n = 4.0e9 symbols (n + 1 < 2^32, the FM capacity): the GPU suffix sort must fit in HBM
+    (32 B per suffix + 8 B per survivor of its first round) and the counts stay exact."""
+    n = 4_000_000_000
+    counts = _fm_full(cuda, n, 0, 10**6, 40, 12, 6)
+    assert counts[0::2].min() >= 1
