@@ -259,6 +259,29 @@ def bench_birank(ctx, p: float, steps, warmup, with_ceiling: bool, clocks=None, 
     return res
 
 
+def bench_birank_size(ctx, log2n, steps, warmup):
+    """BiRank16 rank at the paper's own bit-vector size (4 GiB = 2^35 bits): the 4/8-CTA
+    cluster superblock table path, 10^9 uniform queries per GPU."""
+    import gen
+    import paper_2602_04103_b200 as qr
+
+    torch = ctx.torch
+    n = 1 << log2n
+    bits = torch.empty((n + 63) // 64, dtype=torch.uint64, device=ctx.dev)
+    gen.bits_dev(SEED[2], n, 0.5, bits)
+    h = qr.qr_birank_build(bits, n, device=ctx.gpu)
+    del bits
+    m = M2
+    q = torch.empty(m, dtype=torch.uint64, device=ctx.dev)
+    gen.queries_dev(SEED[2], n, m, q, i0=ctx.rank * m)
+    out = torch.empty_like(q)
+    ms = ctx.timed(lambda: qr.qr_rank(h, q, None, out, m, ctx.stream), steps, warmup)
+    h.free()
+    del q, out
+    torch.cuda.empty_cache()
+    return {"ms": ms, "gq_s": ctx.world * m / ms / 1e6, "n_bits": n}
+
+
 def bench_quadrank(ctx, steps, warmup):
     import gen
     import paper_2602_04103_b200 as qr
@@ -581,6 +604,7 @@ def main():
     rows = {}
     if args.rows == "all":
         rows["c2_p0.01"] = bench_birank(ctx, 0.01, K, W, with_ceiling=False)
+        rows["birank16_2^35_paper_size"] = bench_birank_size(ctx, 35, K, W)
         rows["c3_quadrank"] = bench_quadrank(ctx, K, W)
         rows["c4_quadfm"] = bench_fm(ctx, N4, 0, M4, L4, SEED[4], K, W)
         rows["c5_quadfm"] = bench_fm(ctx, N5, 1, M5, L5, SEED[5], K, W, rank_queries=10**9)
