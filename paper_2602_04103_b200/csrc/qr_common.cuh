@@ -103,6 +103,8 @@ inline uint64_t kmer_c_offset(int k) { return (kmer_entries(k) + 1) & ~1ull; }
 qr_status fm_count_device(const qr_fm* fm, const uint8_t* pat, const uint32_t* lengths, uint32_t fixed_len,
                           uint32_t* out, uint32_t* out_rc, uint64_t m, uint64_t* work, cudaStream_t st,
                           int approx = 0);
+cudaError_t launch_big_pack_qd(const qr_index* h, const uint64_t* q, const uint8_t* c, uint64_t* out, uint64_t m,
+                               int what, cudaStream_t st);
 cudaError_t launch_big_pack_rank(const qr_index* h, const uint64_t* q, const uint8_t* c, uint64_t* out, uint64_t m,
                                  cudaStream_t st);
 qr_status build_super_pack(qr_index* h, cudaStream_t st);

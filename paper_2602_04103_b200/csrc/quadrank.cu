@@ -472,6 +472,7 @@ extern int g_rank_blocks_per_sm;
 extern int g_rank_pair;
 extern int g_rank_lane_table;
 extern int g_index64;
+extern int g_rank_smem;
 
 template <int K>
 static unsigned qd_grid(const qr_index* h, uint64_t m, bool pair) {
@@ -548,6 +549,7 @@ static cudaError_t qd_gather_k(const qr_index* h, const uint64_t* q, uint64_t* o
 cudaError_t launch_quadrank_rank(const qr_index* h, const uint64_t* q, const uint8_t* c, uint64_t* out, uint64_t m,
                                  cudaStream_t st) {
   if (m == 0) return cudaSuccess;
+  if (h->spack_big && g_rank_smem != 0 && m >= (1ull << 22) && !g_index64) return launch_big_pack_qd(h, q, c, out, m, 0, st);
   const int shape = rank_shape(h, m);
   if (shape == RANK_CLUSTER) return launch_super_pack_rank(h, q, c, out, m, 0, st);
   if (shape == RANK_LANE && g_rank_lane_table) {
@@ -564,6 +566,7 @@ cudaError_t launch_quadrank_rank(const qr_index* h, const uint64_t* q, const uin
 }
 cudaError_t launch_quadrank_all4(const qr_index* h, const uint64_t* q, uint64_t* out4, uint64_t m, cudaStream_t st) {
   if (m == 0) return cudaSuccess;
+  if (h->spack_big && g_rank_smem != 0 && m >= (1ull << 22) && !g_index64) return launch_big_pack_qd(h, q, nullptr, out4, m, 1, st);
   const int shape = rank_shape(h, m);
   if (shape == RANK_CLUSTER) return launch_super_pack_rank(h, q, nullptr, out4, m, 1, st);
   if (shape == RANK_LANE && g_rank_lane_table) {

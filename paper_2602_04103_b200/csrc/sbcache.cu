@@ -129,6 +129,22 @@ __global__ void k_bi_pack_super5(const uint32_t* __restrict__ super, uint64_t n_
   }
 }
 
+// QuadRank16 8-superblock groups (the 2-CTA encoding) placed at CTA g % CS, slot g / CS
+__global__ void k_qd_pack_super_cs(const uint32_t* __restrict__ super, uint64_t n_super, uint64_t groups,
+                                   uint64_t slots, uint32_t cs_log, uint64_t* __restrict__ pack) {
+  for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < 4 * groups; t += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t g = t >> 2;
+    const uint32_t c = (uint32_t)(t & 3);
+    const uint64_t i0 = 8 * g;
+    const uint32_t s0 = super[4 * i0 + c];
+    uint64_t w = s0;
+#pragma unroll
+    for (int k = 1; k < 8; ++k)
+      if (i0 + k < n_super) w |= (uint64_t)(super[4 * (i0 + k) + c] - s0) << (16 + 6 * k);
+    pack[4 * ((g & ((1ull << cs_log) - 1)) * slots + (g >> cs_log)) + c] = w;
+  }
+}
+
 extern int g_rank_big_pack;
 extern int g_rank_big_cs;
 
@@ -136,7 +152,35 @@ qr_status build_super_pack_big(qr_index* h, cudaStream_t st) {
   h->spack_big = nullptr;
   h->spack_big_slots = 0;
   h->spack_big_cs = 0;
-  if (h->layout != QR_LAYOUT_BIRANK16 || h->n_super == 0) return QR_OK;
+  if (h->n_super == 0) return QR_OK;
+  if (h->layout == QR_LAYOUT_QUADRANK16) {
+    // 8-superblock groups of 32 B (22-bit base: n < 2^35 chars), for n whose 2-CTA table does
+    // not fit one CTA per half (n > ~2^32.6), or forced (tests)
+    if (h->n >= (1ull << 35)) return QR_OK;
+    const uint64_t groups = (h->n_super + 7) / 8;
+    const uint64_t half = (groups + 1) / 2;
+    if (!g_rank_big_pack && half * 32 + 1024 <= (uint64_t)max_dyn_smem(h->device)) return QR_OK;
+    constexpr uint64_t PART_MAX = 112 * 1024;
+    uint32_t cs = 0;
+    for (uint32_t c = 4; c <= 16; c *= 2) {
+      const uint64_t slots = (groups + c - 1) / c;
+      const bool fits = slots * 32 + 1024 <= (uint64_t)max_dyn_smem(h->device);
+      if (g_rank_big_cs ? (c == (uint32_t)g_rank_big_cs && fits) : (fits && slots * 32 <= PART_MAX)) { cs = c; break; }
+    }
+    if (!cs) return QR_OK;
+    const uint32_t cs_log = cs == 4 ? 2 : cs == 8 ? 3 : 4;
+    const uint64_t slots = (groups + cs - 1) / cs;
+    cudaError_t e = cudaMalloc((void**)&h->spack_big, cs * slots * 32);
+    if (e) { h->spack_big = nullptr; return cuda_fail(e, "alloc large superblock table"); }
+    cudaMemsetAsync(h->spack_big, 0, cs * slots * 32, st);
+    k_qd_pack_super_cs<<<grid_stride_blocks(4 * groups, 256, h->sm_count, 8), 256, 0, st>>>(
+        h->super, h->n_super, groups, slots, cs_log, h->spack_big);
+    if ((e = cudaGetLastError())) { cudaFree(h->spack_big); h->spack_big = nullptr; return cuda_fail(e, "pack superblocks"); }
+    h->spack_big_slots = slots;
+    h->spack_big_cs = cs;
+    return QR_OK;
+  }
+  if (h->layout != QR_LAYOUT_BIRANK16) return QR_OK;
   if (h->n < (1ull << 35) && !g_rank_big_pack) return QR_OK;
   const uint64_t groups = (h->n_super + 4) / 5;
   const uint64_t cap = (uint64_t)max_dyn_smem(h->device);
@@ -513,6 +557,151 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   }
   cluster_barrier();
 }
+
+// QuadRank16 rank / rank_4 over a CS-CTA cluster table (n > ~2^32.6 chars, where half the
+// 2-CTA table no longer fits one CTA; the paper's 4 GiB text is n = 2^34): the k_qd_rank2c /
+// k_qd_all4_2c bodies with the same 8-superblock groups (22-bit base: n < 2^35) placed at CTA
+// g % CS, slot g / CS, and the dynamic work order.
+template <int K, int THREADS>
+__global__ void __launch_bounds__(THREADS, 1)
+    k_qd_rank2w(const uint4* __restrict__ lines, const uint64_t* __restrict__ pack, uint64_t part_words, uint32_t cs_log,
+                const uint64_t* __restrict__ q, const uint8_t* __restrict__ cs, uint64_t* __restrict__ out, uint64_t m,
+                uint64_t last_line, unsigned long long* ctr) {
+  extern __shared__ uint64_t sc_smem[];
+  {
+    const uint4* src = reinterpret_cast<const uint4*>(pack + (uint64_t)cluster_rank() * part_words);
+    uint4* dst = reinterpret_cast<uint4*>(sc_smem);
+    for (uint32_t i = threadIdx.x; i < (uint32_t)(part_words >> 1); i += blockDim.x) dst[i] = __ldg(src + i);
+    cluster_barrier();
+  }
+  const uint32_t local = (uint32_t)__cvta_generic_to_shared(sc_smem);
+  const uint32_t csm = (1u << cs_log) - 1u;
+  const uint32_t half = threadIdx.x & 1u;
+  const uint32_t pw = (threadIdx.x & 31u) >> 1;
+  ScSched sc = sc_first<K, true, 16>(ctr);
+  uint64_t qn[K];
+  uint32_t cn[K];
+  sc_load_qc<K, true>(q, cs, sc.gb + pw, sc.stride, m, qn, cn);
+  while (sc.gb < m) {
+    const uint64_t i0 = sc.gb + pw;
+    uint64_t qq[K];
+    uint32_t jj[K], pp[K], cc[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) { qq[k] = qn[k]; cc[k] = cn[k]; }
+    qd_locate32<K>(qq, last_line, jj, pp);
+    uint64_t w[K][4];
+    uint32_t s[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      w[k][0] = w[k][1] = w[k][2] = w[k][3] = 0;
+      if (half == 0 || pp[k] >= 128) ld_sector_na(lines + 4 * (uint64_t)jj[k] + 2 * half, w[k][0], w[k][1], w[k][2], w[k][3]);
+      s[k] = 0;
+      if (half) {
+        const uint32_t sb = jj[k] >> QD_SB_LOG, g = sb >> 3;
+        s[k] = qd_s_field(ld_dsmem_u64(map_to_rank(local, g & csm) + (g >> cs_log) * 32u + 8u * cc[k]), sb & 7u);
+      }
+    }
+    const uint64_t stride = sc.stride;
+    sc = sc_next<K, true, 16>(sc, ctr);
+    sc_load_qc<K, true>(q, cs, sc.gb + pw, sc.stride, m, qn, cn);
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const uint64_t idx = i0 + (uint64_t)k * stride;
+      const bool right = pp[k] >= 128;
+      const bool mine = half ? right : !right;
+      const uint64_t cl = 0ull - (uint64_t)(cc[k] & 1u), ch = 0ull - (uint64_t)(cc[k] >> 1);
+      const int x = (int)(pp[k] & 127u);
+      const uint64_t inv = half ? 0ull : ~0ull;
+      uint32_t cnt = 0;
+#pragma unroll
+      for (int t = 0; t < 2; ++t) cnt += __popcll((w[k][2 * t] ^ cl) & (w[k][2 * t + 1] ^ ch) & (prefix_mask(x, t) ^ inv));
+      cnt = mine ? cnt : 0u;
+      const uint64_t dw = (cc[k] & 2u) ? w[k][1] : w[k][0];
+      const uint64_t delta = (dw >> (16 * (cc[k] & 1u))) & 0xffffull;      // u16 slot c + (c & 2)
+      uint64_t v = (half ? (uint64_t)cnt : delta - cnt) + ((uint64_t)s[k] << QD_SHIFT);
+      v += __shfl_xor_sync(0xffffffffu, v, 1);
+      if (half == 0 && idx < m) st_stream_u64(out + idx, v);
+    }
+  }
+  cluster_barrier();
+}
+
+
+template <int K, int THREADS>
+__global__ void __launch_bounds__(THREADS, 1)
+    k_qd_all4_2w(const uint4* __restrict__ lines, const uint64_t* __restrict__ pack, uint64_t part_words, uint32_t cs_log,
+                 const uint64_t* __restrict__ q, uint64_t* __restrict__ out4, uint64_t m, uint64_t last_line,
+                 unsigned long long* ctr) {
+  extern __shared__ uint64_t sc_smem[];
+  {
+    const uint4* src = reinterpret_cast<const uint4*>(pack + (uint64_t)cluster_rank() * part_words);
+    uint4* dst = reinterpret_cast<uint4*>(sc_smem);
+    for (uint32_t i = threadIdx.x; i < (uint32_t)(part_words >> 1); i += blockDim.x) dst[i] = __ldg(src + i);
+    cluster_barrier();
+  }
+  const uint32_t local = (uint32_t)__cvta_generic_to_shared(sc_smem);
+  const uint32_t csm = (1u << cs_log) - 1u;
+  const uint32_t half = threadIdx.x & 1u;
+  const uint32_t pw = (threadIdx.x & 31u) >> 1;
+  ScSched sc = sc_first<K, true, 16>(ctr);
+  uint64_t qn[K];
+  uint32_t cn[K];
+  sc_load_qc<K, false>(q, nullptr, sc.gb + pw, sc.stride, m, qn, cn);
+  while (sc.gb < m) {
+    const uint64_t i0 = sc.gb + pw;
+    uint64_t qq[K];
+    uint32_t jj[K], pp[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) qq[k] = qn[k];
+    qd_locate32<K>(qq, last_line, jj, pp);
+    uint64_t w[K][4];
+    uint32_t s0[K], s1[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      w[k][0] = w[k][1] = w[k][2] = w[k][3] = 0;
+      if (half == 0 || pp[k] >= 128) ld_sector_na(lines + 4 * (uint64_t)jj[k] + 2 * half, w[k][0], w[k][1], w[k][2], w[k][3]);
+      // lane 0: s_A, s_C; lane 1: s_G, s_T (adjacent u64 fields of the group)
+      const uint32_t sb = jj[k] >> QD_SB_LOG, g = sb >> 3;
+      uint64_t va, vb;
+      ld_dsmem_v2u64(map_to_rank(local, g & csm) + (g >> cs_log) * 32u + 16u * half, va, vb);
+      s0[k] = qd_s_field(va, sb & 7u);
+      s1[k] = qd_s_field(vb, sb & 7u);
+    }
+    const uint64_t stride = sc.stride;
+    sc = sc_next<K, true, 16>(sc, ctr);
+    sc_load_qc<K, false>(q, nullptr, sc.gb + pw, sc.stride, m, qn, cn);
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const uint64_t idx = i0 + (uint64_t)k * stride;
+      const bool right = pp[k] >= 128;
+      const int x = (int)(pp[k] & 127u);
+      const uint64_t inv = half ? 0ull : ~0ull;
+      uint32_t nl = 0, nh = 0, nt = 0;
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {
+        const uint64_t msk = prefix_mask(x, t) ^ inv;
+        const uint64_t l = ~w[k][2 * t] & msk, hh = ~w[k][2 * t + 1] & msk;   // planes store the negation
+        nl += __popcll(l);
+        nh += __popcll(hh);
+        nt += __popcll(l & hh);
+      }
+      const uint32_t len = half ? (uint32_t)x : 128u - (uint32_t)x;
+      const uint32_t packed = (len - nl - nh + nt) | ((nl - nt) << 8) | ((nh - nt) << 16) | (nt << 24);
+      const uint32_t other = __shfl_xor_sync(0xffffffffu, packed, 1);
+      const uint32_t dgt = __shfl_xor_sync(0xffffffffu, (uint32_t)w[k][1], 1);
+      const uint32_t cnt = (right == (half == 1)) ? packed : other;
+      const uint32_t dl = half ? dgt : (uint32_t)w[k][0];
+      const uint32_t c0 = (cnt >> (16 * half)) & 0xffu, c1 = (cnt >> (16 * half + 8)) & 0xffu;
+      const uint64_t b0 = ((uint64_t)s0[k] << QD_SHIFT) + (dl & 0xffffu);
+      const uint64_t b1 = ((uint64_t)s1[k] << QD_SHIFT) + (dl >> 16);
+      const uint64_t r0 = right ? b0 + c0 : b0 - c0, r1 = right ? b1 + c1 : b1 - c1;
+      if (idx < m) asm volatile("st.global.L1::no_allocate.v2.u64 [%0], {%1,%2};" ::"l"(out4 + 4 * idx + 2 * half),
+                                "l"(r0), "l"(r1) : "memory");
+    }
+  }
+  cluster_barrier();
+}
+
 
 // ------------------------------------------------------------------ one lane per query, table per CTA
 // For L2-resident structures (rank_shape LANE) the line requests are cheap L2 hits and the cost
@@ -1268,6 +1457,66 @@ cudaError_t launch_big_pack_rank(const qr_index* h, const uint64_t* q, const uin
   cfg.numAttrs = 1;
   e = cudaLaunchKernelEx(&cfg, kern, (const uint4*)h->lines, (const uint64_t*)h->spack_big, (uint64_t)h->spack_big_slots,
                          cs_log, q, c, out, m, (uint64_t)(h->n_lines - 1), ctr);
+  if (!e) e = cudaGetLastError();
+  cudaError_t e2 = lease.release(st);
+  return e ? e : e2;
+}
+
+// QuadRank16 rank (what 0) / rank_4 (what 1) over the CS-CTA table
+cudaError_t launch_big_pack_qd(const qr_index* h, const uint64_t* q, const uint8_t* c, uint64_t* out, uint64_t m,
+                               int what, cudaStream_t st) {
+  if (m == 0) return cudaSuccess;
+  const uint32_t cs = h->spack_big_cs, cs_log = cs == 4 ? 2 : cs == 8 ? 3 : 4;
+  const uint64_t part_words = h->spack_big_slots * 4;
+  const size_t smem = (size_t)part_words * 8;
+  const void* kern = what ? (const void*)k_qd_all4_2w<2, 1024> : (const void*)k_qd_rank2w<2, 1024>;
+  static std::mutex mu;
+  static std::map<std::tuple<const void*, int, uint32_t, size_t>, unsigned> grids;
+  cudaLaunchAttribute attr;
+  attr.id = cudaLaunchAttributeClusterDimension;
+  attr.val.clusterDim.x = cs; attr.val.clusterDim.y = 1; attr.val.clusterDim.z = 1;
+  unsigned grid = 0;
+  {
+    std::lock_guard<std::mutex> g(mu);
+    const auto key = std::make_tuple(kern, h->device, cs, smem);
+    auto it = grids.find(key);
+    if (it != grids.end()) {
+      grid = it->second;
+    } else {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (cs > 8) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3((unsigned)h->sm_count / cs * cs);
+      cfg.blockDim = dim3(1024);
+      cfg.dynamicSmemBytes = smem;
+      cfg.attrs = &attr;
+      cfg.numAttrs = 1;
+      int clusters = 0;
+      if (cudaOccupancyMaxActiveClusters(&clusters, kern, &cfg) != cudaSuccess || clusters <= 0) {
+        cudaGetLastError();
+        clusters = 1;
+      }
+      grid = grids[key] = (unsigned)clusters * cs;
+    }
+  }
+  CounterLease lease;
+  unsigned long long* ctr = nullptr;
+  cudaError_t e = lease.acquire(h->device, st, &ctr);
+  if (e) return e;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(1024);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cfg.attrs = &attr;
+  cfg.numAttrs = 1;
+  const uint64_t last = h->n_lines - 1;
+  if (what)
+    e = cudaLaunchKernelEx(&cfg, k_qd_all4_2w<2, 1024>, (const uint4*)h->lines, (const uint64_t*)h->spack_big, part_words,
+                           cs_log, q, out, m, last, ctr);
+  else
+    e = cudaLaunchKernelEx(&cfg, k_qd_rank2w<2, 1024>, (const uint4*)h->lines, (const uint64_t*)h->spack_big, part_words,
+                           cs_log, q, c, out, m, last, ctr);
   if (!e) e = cudaGetLastError();
   cudaError_t e2 = lease.release(st);
   return e ? e : e2;

@@ -221,3 +221,28 @@ def test_fm_near_u32_limit(cuda):
     n = 4_000_000_000
     counts = _fm_full(cuda, n, 0, 10**6, 40, 12, 6)
     assert counts[0::2].min() >= 1
+
+
+def test_quadrank_2_34_chars_cluster_table(cuda):
+    """The paper's 4 GiB of 2-bit text (n = 2^34 + 99 chars): QuadRank16 takes the CS-CTA cluster
+    table kernels; sampled rank(q, c) / rank_4 runs and the boundary set vs the oracle."""
+    torch = _torch()
+    n, m = (1 << 34) + 99, 1 << 23
+    txt = torch.empty((n + 31) // 32, dtype=torch.uint64, device=cuda)
+    gen.dna_dev(34, n, 0, txt)
+    h = qr.qr_quadrank_build(txt, n)
+    del txt
+    q = torch.empty(m, dtype=torch.uint64, device=cuda)
+    c = torch.empty(m, dtype=torch.uint8, device=cuda)
+    gen.queries_dev(41, n, m, q, c)
+    out = torch.empty_like(q)
+    qr.qr_rank(h, q, c, out)
+    o4 = torch.empty((m, 4), dtype=torch.uint64, device=cuda)
+    qr.qr_rank_all4(h, q, o4)
+    torch.cuda.synchronize()
+    assert bool((o4.view(torch.int64).sum(dim=1) == q.view(torch.int64)).all())
+    ora = oracle.DnaOracle(gen.dna(34, n), n)
+    for off in sample_offsets(m, 34)[:12]:
+        qs, cs = gen.queries(41, n, RUN, i0=int(off), with_c=True)
+        assert np.array_equal(to_host(out[off:off + RUN]), ora.rank(qs, cs)), f"offset {off}"
+        assert np.array_equal(to_host(o4[off:off + RUN]), ora.rank_all4(qs)), f"offset {off}"

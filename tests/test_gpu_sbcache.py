@@ -499,3 +499,26 @@ def test_large_table_cluster_kernel_parity(cuda, smem_mode, cs, n_sb, extra):
     assert np.array_equal(_rank(h, q, None, cuda, 1), ora.rank(q))
     c = (gen.queries(802, 1, q.size, with_c=True)[1] & 1).astype(np.uint8)
     assert np.array_equal(_rank(h, q, c, cuda, 1), ora.rank(q, c))
+
+
+@pytest.mark.parametrize("cs", [4, 8, 16])
+@pytest.mark.parametrize("n_sb,extra", [(1, 3), (23, 777), (300, 5)])
+def test_large_table_cluster_kernel_quadrank(cuda, smem_mode, cs, n_sb, extra):
+    """QuadRank16's 8-superblock groups over a 4/8/16-CTA cluster (n > ~2^32.6 chars), forced
+    onto small n: rank(q, c) and rank_4 on >= 2^22 queries + the boundary set."""
+    qr.qr_set_tuning("rank_big_pack", 1)
+    qr.qr_set_tuning("rank_big_cs", cs)
+    try:
+        n = n_sb * S4 + extra
+        t = gen.dna(900 + n_sb, n)
+        h = qr.qr_quadrank_build(t, n)
+    finally:
+        qr.qr_set_tuning("rank_big_pack", 0)
+        qr.qr_set_tuning("rank_big_cs", 0)
+    m = (1 << 22) + 7
+    q, c = gen.queries(901, n, m, with_c=True)
+    bq = boundary_queries(n, B4, S4, 96, limit=20000)
+    q = np.concatenate([q, bq]); c = np.concatenate([c, (bq % 4).astype(np.uint8)])
+    ora = oracle.DnaOracle(t, n)
+    assert np.array_equal(_rank(h, q, c, cuda, 1), ora.rank(q, c))
+    assert np.array_equal(_rank4(h, q, cuda, 1), ora.rank_all4(q))
