@@ -212,10 +212,11 @@ qr_status qr_gather_ceiling(const qr_index* h, const uint64_t* q, uint64_t* out,
 qr_status qr_info(const qr_index* h, uint64_t* n, int* sigma, uint64_t* line_bytes, uint64_t* super_bytes);
 
 /* Bytes of the re-encoded superblock table that the cluster rank kernels keep in shared
- * memory (2 CTAs x *cta_bytes; sbcache.cu), or 0 when this handle's rank calls
- * read the superblock words from global memory (layouts without an L1 array, n >= 2^35, or a
- * table larger than two CTAs' shared memory).  A cache of s_i / s_{i,c}
- * (PAPER.md:513): results never depend on it. */
+ * memory (2 CTAs x *cta_bytes; sbcache.cu), or 0 when this handle has no 2-CTA
+ * table (layouts without an L1 array, n >= 2^35, or a table larger than two CTAs' shared
+ * memory: large BiRank16 / QuadRank16 handles then use a 4/8/16-CTA cluster table for batches
+ * >= 2^22, else global memory).  A cache of s_i / s_{i,c}:
+ * results never depend on it. */
 qr_status qr_super_cache_bytes(const qr_index* h, uint64_t* cta_bytes);
 /* Number of 2-CTA clusters those kernels launch (as many as fit at once; 0 without a cache). */
 qr_status qr_super_cache_clusters(const qr_index* h, int* clusters);
@@ -267,9 +268,11 @@ const char* qr_last_error(void);
  *                      CTA of a one-CTA-per-SM grid and queried from there (lines swizzled over
  *                      the banks), for batches whose 16 B/query of I/O is >= 2x the bytes all
  *                      the copies read; 0: lines from L2.
- *   "rank_big_pack"    1: also build the large-n BiRank16 superblock table (normally only for
- *                      n >= 2^35: 5 superblocks per u64, 32-bit base, split over a 4/8/16-CTA
- *                      cluster, <= 112 KB per CTA) for handles built afterwards — for tests.
+ *   "rank_big_pack"    1: also build the large-n superblock table for handles built afterwards
+ *                      (normally only when the 2-CTA table cannot be used: BiRank16 n >= 2^35,
+ *                      5 superblocks per u64 with a 32-bit base; QuadRank16 n > ~2^32.6 chars,
+ *                      the 8-superblock groups; split over a 4/8/16-CTA cluster, <= 112 KB per
+ *                      CTA) — for tests.
  *   "rank_big_cs"      0 (default): the smallest cluster size meeting that bound; 4, 8, 16: force.
  *   "rank_smem"        the 2-CTA cluster shared-memory kernels: 0 never, 1 (default) by
  *                      structure size for batches >= 2^22, 2 whenever the table exists.
