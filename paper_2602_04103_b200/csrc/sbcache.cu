@@ -1404,16 +1404,22 @@ cudaError_t launch_lane_table_rank(const qr_index* h, const uint64_t* q, const u
   return go(k_qd_rank1s<K, 1, false>, k_qd_rank1s<K, 1, true>, nullptr);
 }
 
-// rank over the CS-CTA table (h->spack_big): dynamic order, 1024-thread CTAs, one per SM, as many
-// CS-clusters as the occupancy API allows.
-cudaError_t launch_big_pack_rank(const qr_index* h, const uint64_t* q, const uint8_t* c, uint64_t* out, uint64_t m,
-                                 cudaStream_t st) {
-  if (m == 0) return cudaSuccess;
-  const uint32_t cs = h->spack_big_cs, cs_log = cs == 4 ? 2 : cs == 8 ? 3 : 4;
-  const size_t smem = (size_t)h->spack_big_slots * 8;
-  auto kern = c ? k_bi_rank2v<4, 1024, true> : k_bi_rank2v<4, 1024, false>;
+// Launch a 1024-thread kernel over CS-CTA clusters (cluster size at launch time; 16 needs the
+// non-portable opt-in), as many clusters as the occupancy API allows at `smem` bytes per CTA
+// (cached per kernel, device, CS and size), with a leased work counter as the last argument.
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_cs_clusters(void (*kern)(KArgs...), uint32_t cs, size_t smem, const qr_index* h,
+                                      cudaStream_t st, Args... args) {
   static std::mutex mu;
   static std::map<std::tuple<const void*, int, uint32_t, size_t>, unsigned> grids;
+  cudaLaunchAttribute attr;
+  attr.id = cudaLaunchAttributeClusterDimension;
+  attr.val.clusterDim.x = cs; attr.val.clusterDim.y = 1; attr.val.clusterDim.z = 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.blockDim = dim3(1024);
+  cfg.dynamicSmemBytes = smem;
+  cfg.attrs = &attr;
+  cfg.numAttrs = 1;
   unsigned grid = 0;
   {
     std::lock_guard<std::mutex> g(mu);
@@ -1424,15 +1430,7 @@ cudaError_t launch_big_pack_rank(const qr_index* h, const uint64_t* q, const uin
     } else {
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       if (cs > 8) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-      cudaLaunchConfig_t cfg = {};
       cfg.gridDim = dim3((unsigned)h->sm_count / cs * cs);
-      cfg.blockDim = dim3(1024);
-      cfg.dynamicSmemBytes = smem;
-      cudaLaunchAttribute attr;
-      attr.id = cudaLaunchAttributeClusterDimension;
-      attr.val.clusterDim.x = cs; attr.val.clusterDim.y = 1; attr.val.clusterDim.z = 1;
-      cfg.attrs = &attr;
-      cfg.numAttrs = 1;
       int clusters = 0;
       if (cudaOccupancyMaxActiveClusters(&clusters, kern, &cfg) != cudaSuccess || clusters <= 0) {
         cudaGetLastError();
@@ -1445,81 +1443,40 @@ cudaError_t launch_big_pack_rank(const qr_index* h, const uint64_t* q, const uin
   unsigned long long* ctr = nullptr;
   cudaError_t e = lease.acquire(h->device, st, &ctr);
   if (e) return e;
-  cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(1024);
-  cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  cudaLaunchAttribute attr;
-  attr.id = cudaLaunchAttributeClusterDimension;
-  attr.val.clusterDim.x = cs; attr.val.clusterDim.y = 1; attr.val.clusterDim.z = 1;
-  cfg.attrs = &attr;
-  cfg.numAttrs = 1;
-  e = cudaLaunchKernelEx(&cfg, kern, (const uint4*)h->lines, (const uint64_t*)h->spack_big, (uint64_t)h->spack_big_slots,
-                         cs_log, q, c, out, m, (uint64_t)(h->n_lines - 1), ctr);
+  e = cudaLaunchKernelEx(&cfg, kern, args..., ctr);
   if (!e) e = cudaGetLastError();
   cudaError_t e2 = lease.release(st);
   return e ? e : e2;
+}
+
+static uint32_t cs_log_of(uint32_t cs) { return cs == 4 ? 2 : cs == 8 ? 3 : 4; }
+
+// BiRank16 rank over the CS-CTA table (h->spack_big): dynamic order, one 1024-thread CTA per SM.
+cudaError_t launch_big_pack_rank(const qr_index* h, const uint64_t* q, const uint8_t* c, uint64_t* out, uint64_t m,
+                                 cudaStream_t st) {
+  if (m == 0) return cudaSuccess;
+  const uint32_t cs = h->spack_big_cs;
+  const size_t smem = (size_t)h->spack_big_slots * 8;
+  const uint4* L = h->lines;
+  const uint64_t* P = h->spack_big;
+  const uint64_t slots = h->spack_big_slots, last = h->n_lines - 1;
+  if (c) return launch_cs_clusters(k_bi_rank2v<4, 1024, true>, cs, smem, h, st, L, P, slots, cs_log_of(cs), q, c, out, m, last);
+  return launch_cs_clusters(k_bi_rank2v<4, 1024, false>, cs, smem, h, st, L, P, slots, cs_log_of(cs), q, c, out, m, last);
 }
 
 // QuadRank16 rank (what 0) / rank_4 (what 1) over the CS-CTA table
 cudaError_t launch_big_pack_qd(const qr_index* h, const uint64_t* q, const uint8_t* c, uint64_t* out, uint64_t m,
                                int what, cudaStream_t st) {
   if (m == 0) return cudaSuccess;
-  const uint32_t cs = h->spack_big_cs, cs_log = cs == 4 ? 2 : cs == 8 ? 3 : 4;
-  const uint64_t part_words = h->spack_big_slots * 4;
+  const uint32_t cs = h->spack_big_cs;
+  const uint64_t part_words = h->spack_big_slots * 4, last = h->n_lines - 1;
   const size_t smem = (size_t)part_words * 8;
-  const void* kern = what ? (const void*)k_qd_all4_2w<2, 1024> : (const void*)k_qd_rank2w<2, 1024>;
-  static std::mutex mu;
-  static std::map<std::tuple<const void*, int, uint32_t, size_t>, unsigned> grids;
-  cudaLaunchAttribute attr;
-  attr.id = cudaLaunchAttributeClusterDimension;
-  attr.val.clusterDim.x = cs; attr.val.clusterDim.y = 1; attr.val.clusterDim.z = 1;
-  unsigned grid = 0;
-  {
-    std::lock_guard<std::mutex> g(mu);
-    const auto key = std::make_tuple(kern, h->device, cs, smem);
-    auto it = grids.find(key);
-    if (it != grids.end()) {
-      grid = it->second;
-    } else {
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      if (cs > 8) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-      cudaLaunchConfig_t cfg = {};
-      cfg.gridDim = dim3((unsigned)h->sm_count / cs * cs);
-      cfg.blockDim = dim3(1024);
-      cfg.dynamicSmemBytes = smem;
-      cfg.attrs = &attr;
-      cfg.numAttrs = 1;
-      int clusters = 0;
-      if (cudaOccupancyMaxActiveClusters(&clusters, kern, &cfg) != cudaSuccess || clusters <= 0) {
-        cudaGetLastError();
-        clusters = 1;
-      }
-      grid = grids[key] = (unsigned)clusters * cs;
-    }
-  }
-  CounterLease lease;
-  unsigned long long* ctr = nullptr;
-  cudaError_t e = lease.acquire(h->device, st, &ctr);
-  if (e) return e;
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(1024);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = st;
-  cfg.attrs = &attr;
-  cfg.numAttrs = 1;
-  const uint64_t last = h->n_lines - 1;
-  if (what)
-    e = cudaLaunchKernelEx(&cfg, k_qd_all4_2w<2, 1024>, (const uint4*)h->lines, (const uint64_t*)h->spack_big, part_words,
-                           cs_log, q, out, m, last, ctr);
-  else
-    e = cudaLaunchKernelEx(&cfg, k_qd_rank2w<2, 1024>, (const uint4*)h->lines, (const uint64_t*)h->spack_big, part_words,
-                           cs_log, q, c, out, m, last, ctr);
-  if (!e) e = cudaGetLastError();
-  cudaError_t e2 = lease.release(st);
-  return e ? e : e2;
+  const uint4* L = h->lines;
+  const uint64_t* P = h->spack_big;
+  if (what) return launch_cs_clusters(k_qd_all4_2w<2, 1024>, cs, smem, h, st, L, P, part_words, cs_log_of(cs), q, out, m, last);
+  return launch_cs_clusters(k_qd_rank2w<2, 1024>, cs, smem, h, st, L, P, part_words, cs_log_of(cs), q, c, out, m, last);
 }
 
 // what: 0 = rank (sigma 2 or 4), 1 = rank_4 (sigma 4), 3 = BiRank gather ceiling of this kernel shape
