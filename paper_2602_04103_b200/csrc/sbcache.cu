@@ -431,14 +431,24 @@ __device__ __forceinline__ void qd_locate32(const uint64_t (&qq)[K], uint64_t la
   }
 }
 
-template <int K, int THREADS, bool DYN>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
-    k_qd_rank2c(const uint4* __restrict__ lines, const uint64_t* __restrict__ pack, uint64_t half_words,
-                const uint64_t* __restrict__ q, const uint8_t* __restrict__ cs, uint64_t* __restrict__ out, uint64_t m,
-                uint64_t last_line, unsigned long long* ctr) {
-  extern __shared__ uint64_t sc_smem[];
+// Address of QuadRank16 group g's 32-B record in the cluster's shared memory: the 2-CTA table
+// (CTA g & 1, addresses of both CTAs mapped once) or the CS-CTA table (CTA g % CS, mapa per read).
+struct QdTable2 {
   uint32_t base0, base1;
-  sc_preload(pack, half_words, sc_smem, base0, base1);
+  __device__ __forceinline__ uint32_t addr(uint32_t g) const { return ((g & 1u) ? base1 : base0) + (g >> 1) * 32u; }
+};
+struct QdTableCS {
+  uint32_t local, csm, cs_log;
+  __device__ __forceinline__ uint32_t addr(uint32_t g) const { return map_to_rank(local, g & csm) + (g >> cs_log) * 32u; }
+};
+
+// Bodies of the QuadRank16 cluster kernels (rank(q,c) and rank_4), shared by the 2-CTA and the
+// CS-CTA entry points below.
+template <int K, bool DYN, class TBL>
+__device__ __forceinline__ void qd_rank2_body(const uint4* __restrict__ lines, const TBL& tbl,
+                                              const uint64_t* __restrict__ q, const uint8_t* __restrict__ cs,
+                                              uint64_t* __restrict__ out, uint64_t m, uint64_t last_line,
+                                              unsigned long long* ctr) {
   const uint32_t half = threadIdx.x & 1u;
   const uint32_t pw = (threadIdx.x & 31u) >> 1;
   ScSched sc = sc_first<K, DYN, 16>(ctr);
@@ -461,7 +471,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       s[k] = 0;
       if (half) {
         const uint32_t sb = jj[k] >> QD_SB_LOG, g = sb >> 3;
-        s[k] = qd_s_field(ld_dsmem_u64(((g & 1u) ? base1 : base0) + (g >> 1) * 32u + 8u * cc[k]), sb & 7u);
+        s[k] = qd_s_field(ld_dsmem_u64(tbl.addr(g) + 8u * cc[k]), sb & 7u);
       }
     }
     const uint64_t stride = sc.stride;
@@ -486,17 +496,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       if (half == 0 && idx < m) st_stream_u64(out + idx, v);
     }
   }
-  cluster_barrier();
 }
 
-template <int K, int THREADS, bool DYN>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
-    k_qd_all4_2c(const uint4* __restrict__ lines, const uint64_t* __restrict__ pack, uint64_t half_words,
-                 const uint64_t* __restrict__ q, uint64_t* __restrict__ out4, uint64_t m, uint64_t last_line,
-                 unsigned long long* ctr) {
-  extern __shared__ uint64_t sc_smem[];
-  uint32_t base0, base1;
-  sc_preload(pack, half_words, sc_smem, base0, base1);
+template <int K, bool DYN, class TBL>
+__device__ __forceinline__ void qd_all4_2_body(const uint4* __restrict__ lines, const TBL& tbl,
+                                               const uint64_t* __restrict__ q, uint64_t* __restrict__ out4, uint64_t m,
+                                               uint64_t last_line, unsigned long long* ctr) {
   const uint32_t half = threadIdx.x & 1u;
   const uint32_t pw = (threadIdx.x & 31u) >> 1;
   ScSched sc = sc_first<K, DYN, 16>(ctr);
@@ -519,7 +524,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       // lane 0: s_A, s_C; lane 1: s_G, s_T (adjacent u64 fields of the group)
       const uint32_t sb = jj[k] >> QD_SB_LOG, g = sb >> 3;
       uint64_t va, vb;
-      ld_dsmem_v2u64(((g & 1u) ? base1 : base0) + (g >> 1) * 32u + 16u * half, va, vb);
+      ld_dsmem_v2u64(tbl.addr(g) + 16u * half, va, vb);
       s0[k] = qd_s_field(va, sb & 7u);
       s1[k] = qd_s_field(vb, sb & 7u);
     }
@@ -555,6 +560,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                                 "l"(r0), "l"(r1) : "memory");
     }
   }
+}
+
+template <int K, int THREADS, bool DYN>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
+    k_qd_rank2c(const uint4* __restrict__ lines, const uint64_t* __restrict__ pack, uint64_t half_words,
+                const uint64_t* __restrict__ q, const uint8_t* __restrict__ cs, uint64_t* __restrict__ out, uint64_t m,
+                uint64_t last_line, unsigned long long* ctr) {
+  extern __shared__ uint64_t sc_smem[];
+  uint32_t base0, base1;
+  sc_preload(pack, half_words, sc_smem, base0, base1);
+  qd_rank2_body<K, DYN>(lines, QdTable2{base0, base1}, q, cs, out, m, last_line, ctr);
+  cluster_barrier();
+}
+
+template <int K, int THREADS, bool DYN>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
+    k_qd_all4_2c(const uint4* __restrict__ lines, const uint64_t* __restrict__ pack, uint64_t half_words,
+                 const uint64_t* __restrict__ q, uint64_t* __restrict__ out4, uint64_t m, uint64_t last_line,
+                 unsigned long long* ctr) {
+  extern __shared__ uint64_t sc_smem[];
+  uint32_t base0, base1;
+  sc_preload(pack, half_words, sc_smem, base0, base1);
+  qd_all4_2_body<K, DYN>(lines, QdTable2{base0, base1}, q, out4, m, last_line, ctr);
   cluster_barrier();
 }
 
@@ -576,53 +604,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   }
   const uint32_t local = (uint32_t)__cvta_generic_to_shared(sc_smem);
   const uint32_t csm = (1u << cs_log) - 1u;
-  const uint32_t half = threadIdx.x & 1u;
-  const uint32_t pw = (threadIdx.x & 31u) >> 1;
-  ScSched sc = sc_first<K, true, 16>(ctr);
-  uint64_t qn[K];
-  uint32_t cn[K];
-  sc_load_qc<K, true>(q, cs, sc.gb + pw, sc.stride, m, qn, cn);
-  while (sc.gb < m) {
-    const uint64_t i0 = sc.gb + pw;
-    uint64_t qq[K];
-    uint32_t jj[K], pp[K], cc[K];
-#pragma unroll
-    for (int k = 0; k < K; ++k) { qq[k] = qn[k]; cc[k] = cn[k]; }
-    qd_locate32<K>(qq, last_line, jj, pp);
-    uint64_t w[K][4];
-    uint32_t s[K];
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-      w[k][0] = w[k][1] = w[k][2] = w[k][3] = 0;
-      if (half == 0 || pp[k] >= 128) ld_sector_na(lines + 4 * (uint64_t)jj[k] + 2 * half, w[k][0], w[k][1], w[k][2], w[k][3]);
-      s[k] = 0;
-      if (half) {
-        const uint32_t sb = jj[k] >> QD_SB_LOG, g = sb >> 3;
-        s[k] = qd_s_field(ld_dsmem_u64(map_to_rank(local, g & csm) + (g >> cs_log) * 32u + 8u * cc[k]), sb & 7u);
-      }
-    }
-    const uint64_t stride = sc.stride;
-    sc = sc_next<K, true, 16>(sc, ctr);
-    sc_load_qc<K, true>(q, cs, sc.gb + pw, sc.stride, m, qn, cn);
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-      const uint64_t idx = i0 + (uint64_t)k * stride;
-      const bool right = pp[k] >= 128;
-      const bool mine = half ? right : !right;
-      const uint64_t cl = 0ull - (uint64_t)(cc[k] & 1u), ch = 0ull - (uint64_t)(cc[k] >> 1);
-      const int x = (int)(pp[k] & 127u);
-      const uint64_t inv = half ? 0ull : ~0ull;
-      uint32_t cnt = 0;
-#pragma unroll
-      for (int t = 0; t < 2; ++t) cnt += __popcll((w[k][2 * t] ^ cl) & (w[k][2 * t + 1] ^ ch) & (prefix_mask(x, t) ^ inv));
-      cnt = mine ? cnt : 0u;
-      const uint64_t dw = (cc[k] & 2u) ? w[k][1] : w[k][0];
-      const uint64_t delta = (dw >> (16 * (cc[k] & 1u))) & 0xffffull;      // u16 slot c + (c & 2)
-      uint64_t v = (half ? (uint64_t)cnt : delta - cnt) + ((uint64_t)s[k] << QD_SHIFT);
-      v += __shfl_xor_sync(0xffffffffu, v, 1);
-      if (half == 0 && idx < m) st_stream_u64(out + idx, v);
-    }
-  }
+  qd_rank2_body<K, true>(lines, QdTableCS{local, csm, cs_log}, q, cs, out, m, last_line, ctr);
   cluster_barrier();
 }
 
@@ -641,64 +623,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   }
   const uint32_t local = (uint32_t)__cvta_generic_to_shared(sc_smem);
   const uint32_t csm = (1u << cs_log) - 1u;
-  const uint32_t half = threadIdx.x & 1u;
-  const uint32_t pw = (threadIdx.x & 31u) >> 1;
-  ScSched sc = sc_first<K, true, 16>(ctr);
-  uint64_t qn[K];
-  uint32_t cn[K];
-  sc_load_qc<K, false>(q, nullptr, sc.gb + pw, sc.stride, m, qn, cn);
-  while (sc.gb < m) {
-    const uint64_t i0 = sc.gb + pw;
-    uint64_t qq[K];
-    uint32_t jj[K], pp[K];
-#pragma unroll
-    for (int k = 0; k < K; ++k) qq[k] = qn[k];
-    qd_locate32<K>(qq, last_line, jj, pp);
-    uint64_t w[K][4];
-    uint32_t s0[K], s1[K];
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-      w[k][0] = w[k][1] = w[k][2] = w[k][3] = 0;
-      if (half == 0 || pp[k] >= 128) ld_sector_na(lines + 4 * (uint64_t)jj[k] + 2 * half, w[k][0], w[k][1], w[k][2], w[k][3]);
-      // lane 0: s_A, s_C; lane 1: s_G, s_T (adjacent u64 fields of the group)
-      const uint32_t sb = jj[k] >> QD_SB_LOG, g = sb >> 3;
-      uint64_t va, vb;
-      ld_dsmem_v2u64(map_to_rank(local, g & csm) + (g >> cs_log) * 32u + 16u * half, va, vb);
-      s0[k] = qd_s_field(va, sb & 7u);
-      s1[k] = qd_s_field(vb, sb & 7u);
-    }
-    const uint64_t stride = sc.stride;
-    sc = sc_next<K, true, 16>(sc, ctr);
-    sc_load_qc<K, false>(q, nullptr, sc.gb + pw, sc.stride, m, qn, cn);
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-      const uint64_t idx = i0 + (uint64_t)k * stride;
-      const bool right = pp[k] >= 128;
-      const int x = (int)(pp[k] & 127u);
-      const uint64_t inv = half ? 0ull : ~0ull;
-      uint32_t nl = 0, nh = 0, nt = 0;
-#pragma unroll
-      for (int t = 0; t < 2; ++t) {
-        const uint64_t msk = prefix_mask(x, t) ^ inv;
-        const uint64_t l = ~w[k][2 * t] & msk, hh = ~w[k][2 * t + 1] & msk;   // planes store the negation
-        nl += __popcll(l);
-        nh += __popcll(hh);
-        nt += __popcll(l & hh);
-      }
-      const uint32_t len = half ? (uint32_t)x : 128u - (uint32_t)x;
-      const uint32_t packed = (len - nl - nh + nt) | ((nl - nt) << 8) | ((nh - nt) << 16) | (nt << 24);
-      const uint32_t other = __shfl_xor_sync(0xffffffffu, packed, 1);
-      const uint32_t dgt = __shfl_xor_sync(0xffffffffu, (uint32_t)w[k][1], 1);
-      const uint32_t cnt = (right == (half == 1)) ? packed : other;
-      const uint32_t dl = half ? dgt : (uint32_t)w[k][0];
-      const uint32_t c0 = (cnt >> (16 * half)) & 0xffu, c1 = (cnt >> (16 * half + 8)) & 0xffu;
-      const uint64_t b0 = ((uint64_t)s0[k] << QD_SHIFT) + (dl & 0xffffu);
-      const uint64_t b1 = ((uint64_t)s1[k] << QD_SHIFT) + (dl >> 16);
-      const uint64_t r0 = right ? b0 + c0 : b0 - c0, r1 = right ? b1 + c1 : b1 - c1;
-      if (idx < m) asm volatile("st.global.L1::no_allocate.v2.u64 [%0], {%1,%2};" ::"l"(out4 + 4 * idx + 2 * half),
-                                "l"(r0), "l"(r1) : "memory");
-    }
-  }
+  qd_all4_2_body<K, true>(lines, QdTableCS{local, csm, cs_log}, q, out4, m, last_line, ctr);
   cluster_barrier();
 }
 

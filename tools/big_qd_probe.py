@@ -16,7 +16,7 @@ def t(fn, reps=5):
     b.record(st); torch.cuda.synchronize()
     return a.elapsed_time(b) / reps
 m = 10**9
-for lg in (32, 33, 34):
+for lg in [int(x) for x in (sys.argv[1].split(",") if len(sys.argv) > 1 else ["32", "33", "34"])]:
     n = 1 << lg
     txt = torch.empty((n + 31) // 32, dtype=torch.uint64, device=dev); gen.dna_dev(3, n, 0, txt)
     h = qr.qr_quadrank_build(txt, n)
