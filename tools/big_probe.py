@@ -16,7 +16,7 @@ def t(fn, reps=5):
     b.record(st); torch.cuda.synchronize()
     return a.elapsed_time(b) / reps
 m = 10**9
-for lg in (34, 35, 36):
+for lg in [int(x) for x in (sys.argv[1].split(",") if len(sys.argv) > 1 else ["34", "35", "36"])]:
     n = 1 << lg
     bits = torch.empty((n + 63) // 64, dtype=torch.uint64, device=dev); gen.bits_dev(1, n, 0.5, bits)
     h = qr.qr_birank_build(bits, n)
