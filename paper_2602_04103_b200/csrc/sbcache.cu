@@ -335,7 +335,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
 }
 
 // BiRank16 rank over the CS-CTA table (n >= 2^35): the k_bi_rank2c structure with 64-bit line
-// indices and lane 1 of a pair reading s from the CTA g % CS of its cluster.
+// indices and lane 1 of a pair reading s from the CTA g % CS of its cluster.  Kept as its own body:
+// sharing k_bi_rank2c's through a table policy spilled 40 B per thread here and cost 8-9%.
 template <int K, int THREADS, bool HAS_C>
 __global__ void __launch_bounds__(THREADS, 1)
     k_bi_rank2v(const uint4* __restrict__ lines, const uint64_t* __restrict__ pack, uint64_t slots, uint32_t cs_log,
