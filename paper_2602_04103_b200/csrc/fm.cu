@@ -426,7 +426,8 @@ __device__ __forceinline__ uint32_t x2_rank(const uint64_t (&w)[4], uint32_t p, 
 }
 
 template <int SMS = 0>
-__device__ __forceinline__ void fm_step_x2(const FmParams& F, uint32_t c, uint32_t& lo, uint32_t& hi, uint32_t& lines) {
+__device__ __forceinline__ void fm_step_x2(const FmParams& F, uint32_t c, uint32_t& lo, uint32_t& hi, uint32_t& lines,
+                                           const uint4* C4 = nullptr) {
   uint32_t jl, hl, pl, jh, hh, ph;
   x2_locate(lo, (uint32_t)F.last_line, jl, hl, pl);
   x2_locate(hi, (uint32_t)F.last_line, jh, hh, ph);
@@ -443,7 +444,8 @@ __device__ __forceinline__ void fm_step_x2(const FmParams& F, uint32_t c, uint32
   lines = jl == jh ? 1u : 2u;
   uint32_t rl = x2_rank(a, pl, c, sl), rh = x2_rank(b, ph, c, sh);
   if (c == 0) { rl -= (lo > (uint32_t)F.spos); rh -= (hi > (uint32_t)F.spos); }
-  const uint32_t Cc = __ldg(F.Ct + c);
+  // C[c] from registers when the caller holds them (select, no load on the step's critical path)
+  const uint32_t Cc = C4 ? (c & 2u ? (c & 1u ? C4->w : C4->z) : (c & 1u ? C4->y : C4->x)) : __ldg(F.Ct + c);
   lo = Cc + rl;
   hi = Cc + rh;
 }
@@ -678,7 +680,7 @@ __global__ void __launch_bounds__(256, QR_FM_MINB) k_fm_count(FmParams F, const 
   auto step = [&]() {                                    // one backward step (LF mapping)
     const uint32_t c = rc ? 3u - P.at((int64_t)len - 1 - k) : P.at(k);
     uint32_t nl;
-    if (BW == 1)   fm_step<SMS, 1>(F, c, lo, hi, nl);
+    if (BW == 1)   fm_step_x2<SMS>(F, c, lo, hi, nl, &C4);
     else if (LEAN) fm_step_lean<SMS>(F, C4, c, lo, hi, nl);
     else           fm_step<SMS, 0>(F, c, lo, hi, nl);
     --k;
