@@ -46,6 +46,7 @@ struct qr_index {
   uint64_t* spack_big = nullptr;   // BiRank16 n >= 2^35: 5-superblock groups over a CS-CTA cluster (sbcache.cu)
   uint64_t spack_big_slots = 0;    // groups per CTA
   uint32_t spack_big_cs = 0;       // cluster size (4, 8 or 16)
+  uint32_t spack_big_hi[3] = {};   // BiRank16: first group whose base s >> 24 is >= 1, 2, 3
 };
 
 struct qr_fm {

@@ -112,20 +112,24 @@ qr_status build_super_pack(qr_index* h, cudaStream_t st) {
 
 // ------------------------------------------------------------------ BiRank16 beyond 2^35 bits
 // The 2-CTA table above needs s < 2^24 (n < 2^35) and half of it must fit one CTA (n <= ~2^34.4).
-// For larger bit vectors (the paper's own 4 GiB, is n = 2^35) the superblock words go
-// to a wider cluster instead: groups of 5 superblocks per u64 — bits [0,32) s_{5g}, byte k-1 at
-// bit 32 + 8(k-1) = s_{5g+k} - s_{5g} (k = 1..4, <= 4 * 31) — group g at CTA g % CS, slot g / CS,
-// CS = 4, 8 or 16 CTAs of one cluster (<= 112 KB each: n up to 2^36 bits).
-__global__ void k_bi_pack_super5(const uint32_t* __restrict__ super, uint64_t n_super, uint64_t groups,
-                                 uint64_t slots, uint32_t cs_log, uint64_t* __restrict__ pack) {
+// For larger bit vectors (the paper's own 4 GiB, is n = 2^35) the same 6-superblock
+// groups go to a wider cluster (group g at CTA g % CS, slot g / CS; CS = 4, 8 or 16), with only
+// the low 24 bits of each group's base stored: bits 24-25 come from the first groups whose base
+// reaches 2^24, 2^25, 3 * 2^24 (s is non-decreasing), kernel parameters — n < 2^37 bits.
+__global__ void k_bi_pack_super6cs(const uint32_t* __restrict__ super, uint64_t n_super, uint64_t groups,
+                                   uint64_t slots, uint32_t cs_log, uint64_t* __restrict__ pack,
+                                   uint32_t* __restrict__ hi_first) {
   for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < groups; g += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t i0 = 5 * g;
+    const uint64_t i0 = 6 * g;
     const uint32_t s0 = super[i0];
-    uint64_t w = s0;
+    uint64_t w = s0 & 0xffffffu;
 #pragma unroll
-    for (int k = 1; k < 5; ++k)
-      if (i0 + k < n_super) w |= (uint64_t)(super[i0 + k] - s0) << (24 + 8 * k);
+    for (int k = 1; k < 6; ++k)
+      if (i0 + k < n_super) w |= (uint64_t)(super[i0 + k] - s0) << (16 + 8 * k);
     pack[(g & ((1ull << cs_log) - 1)) * slots + (g >> cs_log)] = w;
+    // s is non-decreasing: group g is the first of high part h when its predecessor's is lower
+    const uint32_t h = s0 >> 24, hp = g ? super[i0 - 6] >> 24 : 0u;
+    for (uint32_t k = hp + 1; k <= h && k <= 3; ++k) hi_first[k - 1] = (uint32_t)g;
   }
 }
 
@@ -182,27 +186,36 @@ qr_status build_super_pack_big(qr_index* h, cudaStream_t st) {
   }
   if (h->layout != QR_LAYOUT_BIRANK16) return QR_OK;
   if (h->n < (1ull << 35) && !g_rank_big_pack) return QR_OK;
-  const uint64_t groups = (h->n_super + 4) / 5;
+  if (h->n >= (1ull << 37)) return QR_OK;                            // s < 2^26: 2 high bits
+  // the 2-CTA encoding (6 superblocks per u64, 24-bit base) with the base's bits 24-25 recovered
+  // from three group boundaries (s is non-decreasing), split over the smallest cluster whose
+  // per-CTA part is <= 184 KB — the 2-CTA table's own size at 2^34, where the kernel reaches the
+  // gather ceiling; larger parts leave the L1 too little room for the misses in flight (a 216 KB
+  // part: 35.4 vs 42.5 Gq/s at 108 KB, profiles/r01_big_cs_probe.jsonl)
+  const uint64_t groups = (h->n_super + 5) / 6;
   const uint64_t cap = (uint64_t)max_dyn_smem(h->device);
+  constexpr uint64_t PART_MAX = 184 * 1024;
   uint32_t cs = 0;
-  // the smallest cluster whose per-CTA part is <= 112 KB: a larger part leaves the L1 too little
-  // room for the line misses in flight (n = 2^35: 35.4 Gq/s at 4 CTAs x 216 KB, 42.5 at 8 x 108 KB,
-  // 38.6 at 16 x 54 KB; profiles/r01_big_cs_probe.jsonl)
-  constexpr uint64_t PART_MAX = 112 * 1024;
   for (uint32_t c = 4; c <= 16; c *= 2) {
     const uint64_t slots = (((groups + c - 1) / c) + 1) & ~1ull;      // even: 16-B copies
     const bool fits = slots * 8 + 1024 <= cap;
     if (g_rank_big_cs ? (c == (uint32_t)g_rank_big_cs && fits) : (fits && slots * 8 <= PART_MAX)) { cs = c; break; }
   }
-  if (!cs) return QR_OK;                                              // n > ~2^36: global kernels
+  if (!cs) return QR_OK;
   const uint32_t cs_log = cs == 4 ? 2 : cs == 8 ? 3 : 4;
   const uint64_t slots = (((groups + cs - 1) / cs) + 1) & ~1ull;
-  cudaError_t e = cudaMalloc((void**)&h->spack_big, cs * slots * 8);
+  cudaError_t e = cudaMalloc((void**)&h->spack_big, cs * slots * 8 + 16);
   if (e) { h->spack_big = nullptr; return cuda_fail(e, "alloc large superblock table"); }
+  uint32_t* hi_first = reinterpret_cast<uint32_t*>(h->spack_big + cs * slots);
   cudaMemsetAsync(h->spack_big, 0, cs * slots * 8, st);
-  k_bi_pack_super5<<<grid_stride_blocks(groups, 256, h->sm_count, 8), 256, 0, st>>>(h->super, h->n_super, groups, slots,
-                                                                                    cs_log, h->spack_big);
-  if ((e = cudaGetLastError())) { cudaFree(h->spack_big); h->spack_big = nullptr; return cuda_fail(e, "pack superblocks"); }
+  cudaMemsetAsync(hi_first, 0xff, 16, st);                             // "never": UINT32_MAX
+  k_bi_pack_super6cs<<<grid_stride_blocks(groups, 256, h->sm_count, 8), 256, 0, st>>>(h->super, h->n_super, groups,
+                                                                                      slots, cs_log, h->spack_big,
+                                                                                      hi_first);
+  if ((e = cudaGetLastError()) || (e = cudaMemcpyAsync(h->spack_big_hi, hi_first, 12, cudaMemcpyDeviceToHost, st)) ||
+      (e = cudaStreamSynchronize(st))) {
+    cudaFree(h->spack_big); h->spack_big = nullptr; return cuda_fail(e, "pack superblocks");
+  }
   h->spack_big_slots = slots;
   h->spack_big_cs = cs;
   return QR_OK;
@@ -339,7 +352,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
 // sharing k_bi_rank2c's through a table policy spilled 40 B per thread here and cost 8-9%.
 template <int K, int THREADS, bool HAS_C>
 __global__ void __launch_bounds__(THREADS, 1)
-    k_bi_rank2v(const uint4* __restrict__ lines, const uint64_t* __restrict__ pack, uint64_t slots, uint32_t cs_log,
+    k_bi_rank2v(const uint4* __restrict__ lines, const uint64_t* __restrict__ pack, uint64_t slots, uint32_t cs_log, uint32_t hi1, uint32_t hi2,
+                uint32_t hi3,
                 const uint64_t* __restrict__ q, const uint8_t* __restrict__ cs, uint64_t* __restrict__ out, uint64_t m,
                 uint64_t last_line, unsigned long long* ctr) {
   extern __shared__ uint64_t sc_smem[];
@@ -377,9 +391,11 @@ __global__ void __launch_bounds__(THREADS, 1)
       if (half == 0 || pp[k] >= 256) ld_sector_na(lines + 4 * jj[k] + 2 * half, w[k][0], w[k][1], w[k][2], w[k][3]);
       s[k] = 0;
       if (half) {
-        const uint32_t sb = (uint32_t)(jj[k] >> BI_SB_LOG), g = sb / 5u, kk = sb - 5u * g;
+        const uint32_t sb = (uint32_t)(jj[k] >> BI_SB_LOG), g = sb / 6u, kk = sb - 6u * g;
         const uint64_t v = ld_dsmem_u64(map_to_rank(local, g & csm) + (g >> cs_log) * 8u);
-        s[k] = kk ? (uint32_t)v + ((uint32_t)(v >> (24u + 8u * kk)) & 0xffu) : (uint32_t)v;
+        const uint32_t base = ((uint32_t)v & 0xffffffu) |
+                              (((uint32_t)(g >= hi1) + (uint32_t)(g >= hi2) + (uint32_t)(g >= hi3)) << 24);
+        s[k] = kk ? base + ((uint32_t)(v >> (16u + 8u * kk)) & 0xffu) : base;
       }
     }
     const uint64_t stride = sc.stride;
@@ -1388,8 +1404,12 @@ cudaError_t launch_big_pack_rank(const qr_index* h, const uint64_t* q, const uin
   const uint4* L = h->lines;
   const uint64_t* P = h->spack_big;
   const uint64_t slots = h->spack_big_slots, last = h->n_lines - 1;
-  if (c) return launch_cs_clusters(k_bi_rank2v<4, 1024, true>, cs, smem, h, st, L, P, slots, cs_log_of(cs), q, c, out, m, last);
-  return launch_cs_clusters(k_bi_rank2v<4, 1024, false>, cs, smem, h, st, L, P, slots, cs_log_of(cs), q, c, out, m, last);
+  const uint32_t* hb = h->spack_big_hi;
+  if (c)
+    return launch_cs_clusters(k_bi_rank2v<4, 1024, true>, cs, smem, h, st, L, P, slots, cs_log_of(cs), hb[0], hb[1], hb[2],
+                              q, c, out, m, last);
+  return launch_cs_clusters(k_bi_rank2v<4, 1024, false>, cs, smem, h, st, L, P, slots, cs_log_of(cs), hb[0], hb[1], hb[2],
+                            q, c, out, m, last);
 }
 
 // QuadRank16 rank (what 0) / rank_4 (what 1) over the CS-CTA table

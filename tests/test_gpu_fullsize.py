@@ -246,3 +246,38 @@ def test_quadrank_2_34_chars_cluster_table(cuda):
         qs, cs = gen.queries(41, n, RUN, i0=int(off), with_c=True)
         assert np.array_equal(to_host(out[off:off + RUN]), ora.rank(qs, cs)), f"offset {off}"
         assert np.array_equal(to_host(o4[off:off + RUN]), ora.rank_all4(qs)), f"offset {off}"
+
+
+@pytest.mark.parametrize("p", [1.0, 0.9])
+def test_birank_large_table_high_bits(cuda, p):
+    """Superblock words of 2^24 and more (R >= 2^35 ones): the large-n cluster table stores 24-bit
+    group bases and recovers bits 24-25 from group boundaries.  n = 2^35 + 2^33 + 12345 bits of
+    density 1.0 (rank(q) = q, closed form) and 0.9 (oracle on sampled runs); both cross 2^24."""
+    torch = _torch()
+    n, m = (1 << 35) + (1 << 33) + 12345, 1 << 24
+    bits = torch.empty((n + 63) // 64, dtype=torch.uint64, device=cuda)
+    if p == 1.0:
+        bits.view(torch.int64).fill_(-1)
+    else:
+        gen.bits_dev(44, n, p, bits)
+    h = qr.qr_birank_build(bits, n)
+    del bits
+    q = torch.empty(m, dtype=torch.uint64, device=cuda)
+    gen.queries_dev(45, n, m, q)
+    out = torch.empty_like(q)
+    qr.qr_rank(h, q, None, out)
+    torch.cuda.synchronize()
+    if p == 1.0:
+        assert torch.equal(out, q)
+        return
+    ora = oracle.BitsOracle(gen.bits(44, n, p), n)
+    for off in sample_offsets(m, 44)[:16]:
+        qs = gen.queries(45, n, RUN, i0=int(off))
+        assert np.array_equal(to_host(out[off:off + RUN]), ora.rank(qs)), f"offset {off}"
+    tail = np.arange(n - 200000, n + 1, dtype=np.uint64)
+    tq = np.concatenate([tail, gen.queries(46, n, (1 << 22))])
+    dq = to_dev(tq, cuda)
+    ot = torch.empty_like(dq)
+    qr.qr_rank(h, dq, None, ot)
+    torch.cuda.synchronize()
+    assert np.array_equal(to_host(ot), ora.rank(tq))
