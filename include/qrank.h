@@ -269,10 +269,11 @@ const char* qr_last_error(void);
  *                      the banks), for batches whose 16 B/query of I/O is >= 2x the bytes all
  *                      the copies read; 0: lines from L2.
  *   "rank_big_pack"    1: also build the large-n superblock table for handles built afterwards
- *                      (normally only when the 2-CTA table cannot be used: BiRank16 n >= 2^35,
- *                      5 superblocks per u64 with a 32-bit base; QuadRank16 n > ~2^32.6 chars,
- *                      the 8-superblock groups; split over a 4/8/16-CTA cluster, <= 112 KB per
- *                      CTA) — for tests.
+ *                      (normally only when the 2-CTA table cannot be used: BiRank16 2^35 <= n <
+ *                      2^37, the 6-superblock groups with 24-bit bases + three high-bit group
+ *                      boundaries, <= 184 KB per CTA; QuadRank16 ~2^32.6 < n < 2^35 chars, the
+ *                      8-superblock groups, <= 112 KB per CTA; split over a 4/8/16-CTA
+ *                      cluster) — for tests.
  *   "rank_big_cs"      0 (default): the smallest cluster size meeting that bound; 4, 8, 16: force.
  *   "rank_smem"        the 2-CTA cluster shared-memory kernels: 0 never, 1 (default) by
  *                      structure size for batches >= 2^22, 2 whenever the table exists.
