@@ -272,7 +272,7 @@ const char* qr_last_error(void);
  *                      (normally only when the 2-CTA table cannot be used: BiRank16 2^35 <= n <
  *                      2^37, the 6-superblock groups with 24-bit bases + three high-bit group
  *                      boundaries, <= 184 KB per CTA; QuadRank16 ~2^32.6 < n < 2^35 chars, the
- *                      8-superblock groups, <= 112 KB per CTA; split over a 4/8/16-CTA
+ *                      8-superblock groups, <= 184 KB per CTA; split over a 4/8/16-CTA
  *                      cluster) — for tests.
  *   "rank_big_cs"      0 (default): the smallest cluster size meeting that bound; 4, 8, 16: force.
  *   "rank_smem"        the 2-CTA cluster shared-memory kernels: 0 never, 1 (default) by

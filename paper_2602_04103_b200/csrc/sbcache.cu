@@ -159,12 +159,13 @@ qr_status build_super_pack_big(qr_index* h, cudaStream_t st) {
   if (h->n_super == 0) return QR_OK;
   if (h->layout == QR_LAYOUT_QUADRANK16) {
     // 8-superblock groups of 32 B (22-bit base: n < 2^35 chars), for n whose 2-CTA table does
-    // not fit one CTA per half (n > ~2^32.6), or forced (tests)
+    // not fit one CTA per half (n > ~2^32.6), or forced (tests); parts <= 184 KB as for BiRank16
+    // (2^34 chars: 8 x 150 KB, 40.0 Gq/s vs 37.0 at 16 x 75 KB, profiles/r01_big_qd_probe_184k.jsonl)
     if (h->n >= (1ull << 35)) return QR_OK;
     const uint64_t groups = (h->n_super + 7) / 8;
     const uint64_t half = (groups + 1) / 2;
     if (!g_rank_big_pack && half * 32 + 1024 <= (uint64_t)max_dyn_smem(h->device)) return QR_OK;
-    constexpr uint64_t PART_MAX = 112 * 1024;
+    constexpr uint64_t PART_MAX = 184 * 1024;
     uint32_t cs = 0;
     for (uint32_t c = 4; c <= 16; c *= 2) {
       const uint64_t slots = (groups + c - 1) / c;
