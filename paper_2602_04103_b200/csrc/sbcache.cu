@@ -164,7 +164,9 @@ qr_status build_super_pack_big(qr_index* h, cudaStream_t st) {
     if (h->n >= (1ull << 35)) return QR_OK;
     const uint64_t groups = (h->n_super + 7) / 8;
     const uint64_t half = (groups + 1) / 2;
-    if (!g_rank_big_pack && half * 32 + 1024 <= (uint64_t)max_dyn_smem(h->device)) return QR_OK;
+    // also where the 2-CTA table would hold more than 184 KB per CTA: near its capacity it
+    // loses to this one (n = 1.45 x 2^32: 36.6 vs 42.5 Gq/s, profiles/r01_boundary_probe.jsonl)
+    if (!g_rank_big_pack && half * 32 <= 184 * 1024) return QR_OK;
     constexpr uint64_t PART_MAX = 184 * 1024;
     uint32_t cs = 0;
     for (uint32_t c = 4; c <= 16; c *= 2) {
@@ -186,8 +188,13 @@ qr_status build_super_pack_big(qr_index* h, cudaStream_t st) {
     return QR_OK;
   }
   if (h->layout != QR_LAYOUT_BIRANK16) return QR_OK;
-  if (h->n < (1ull << 35) && !g_rank_big_pack) return QR_OK;
   if (h->n >= (1ull << 37)) return QR_OK;                            // s < 2^26: 2 high bits
+  {
+    // n >= 2^35 (no 2-CTA table), or a 2-CTA table of more than 184 KB per CTA (n > ~2^34.06:
+    // 1.23 x 2^34 runs 34.2 Gq/s with it vs 44.1 with this one, profiles/r01_boundary_probe.jsonl)
+    const uint64_t g6 = (h->n_super + 5) / 6, half6 = (((g6 + 1) / 2 + 1) & ~1ull) * 8;
+    if (h->n < (1ull << 35) && half6 <= 184 * 1024 && !g_rank_big_pack) return QR_OK;
+  }
   // the 2-CTA encoding (6 superblocks per u64, 24-bit base) with the base's bits 24-25 recovered
   // from three group boundaries (s is non-decreasing), split over the smallest cluster whose
   // per-CTA part is <= 184 KB — the 2-CTA table's own size at 2^34, where the kernel reaches the
