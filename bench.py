@@ -620,7 +620,7 @@ def main():
                                                          bwt_layout=qr.QR_LAYOUT_QUADRANK16X2)
         rows["c4_quadfm_approx2"] = bench_approx(ctx, N4, 10**6, L4, SEED[4], K, W, kmax=2)
         rows["c5_reads_150bp_both_strands_approx1"] = bench_reads_approx(ctx, N5, 10**6, 150, 55, K, W, 1)
-        rows["c5_reads_150bp_both_strands_approx2"] = bench_reads_approx(ctx, N5, 10**5, 150, 55, K, W, 2)
+        rows["c5_reads_150bp_both_strands_approx2"] = bench_reads_approx(ctx, N5, 3 * 10**5, 150, 55, K, W, 2)
         rows["layout_variants"] = bench_variants(ctx, K, W)
         rows["latency_mode"] = bench_latency(ctx, K, W)
         rows["c1_small"] = bench_small(ctx, K, W)
