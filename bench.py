@@ -301,12 +301,15 @@ def bench_quadrank(ctx, steps, warmup):
     del out
     out4 = torch.empty((m, 4), dtype=torch.uint64, device=ctx.dev)
     ms4 = ctx.timed(lambda: qr.qr_rank_all4(h, q, out4, m, ctx.stream), steps, warmup)
+    # rank_4's own ceiling: the same loads with its 32-B output stream (qr_gather_ceiling mode 4)
+    cms4 = ctx.timed(lambda: qr.qr_gather_ceiling(h, q, out4, 4, m, ctx.stream), steps, warmup)
     del q, c, out4
     h.free()
     torch.cuda.empty_cache()
     return {"rank": {"ms": ms, "gq_s": ctx.world * m / ms / 1e6},
             "ceiling_mode0": {"ms": cms, "gq_s": ctx.world * m / cms / 1e6},
-            "rank_all4": {"ms": ms4, "gq_s": ctx.world * m / ms4 / 1e6}}
+            "rank_all4": {"ms": ms4, "gq_s": ctx.world * m / ms4 / 1e6},
+            "ceiling_rank4_shape": {"ms": cms4, "gq_s": ctx.world * m / cms4 / 1e6}}
 
 
 def bench_fm(ctx, n, kind, m_total, length, seed, steps, warmup, rank_queries=0, bwt_layout=None):

@@ -203,7 +203,8 @@ qr_status qr_fm_count_work(const qr_fm* fm, const uint8_t* patterns, const uint3
  * 64 B); mode 1: the full 64-B line always; mode 2: mode 0 plus qr_rank's superblock-word
  * read (BiRank; on QuadRank mode 2 = mode 0); mode 3: the cluster shared-memory rank kernel's
  * own launch shape and loads without the superblock read (BiRank16 with a superblock cache,
- * qr_super_cache_bytes > 0; else QR_EINVAL).  Device pointers only. */
+ * qr_super_cache_bytes > 0; else QR_EINVAL); mode 4: mode 0's loads with rank_4's output shape,
+ * 32 B written per query (QuadRank16 only; out holds 4m u64).  Device pointers only. */
 qr_status qr_gather_ceiling(const qr_index* h, const uint64_t* q, uint64_t* out, uint64_t m, int mode, void* stream);
 
 /* ------------------------------------------------------------------ handles */

@@ -315,7 +315,7 @@ def qr_fm_count_work(fm: Fm, patterns, lengths, fixed_len: int, out, m: int, wor
 def qr_gather_ceiling(h: Index, q, out, mode: int = 0, m: int | None = None, stream=None):
     m = (q.numel() if hasattr(q, "numel") else q.size) if m is None else m
     _need(q, 8, m, "qr_gather_ceiling q")
-    _need(out, 8, m, "qr_gather_ceiling out")
+    _need(out, 8, 4 * m if mode == 4 else m, "qr_gather_ceiling out")
     _check(lib().qr_gather_ceiling(h.ptr, _ptr(q), _ptr(out), m, mode, _stream(stream)), "qr_gather_ceiling")
     return out
 

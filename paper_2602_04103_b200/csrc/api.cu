@@ -561,7 +561,9 @@ QR_EXPORT qr_status qr_rank_all4(const qr_index* h, const uint64_t* q, uint64_t*
 QR_EXPORT qr_status qr_gather_ceiling(const qr_index* h, const uint64_t* q, uint64_t* out, uint64_t m, int mode,
                                       void* stream) {
   if (!h || (m && (!q || !out))) return fail(QR_EINVAL, "qr_gather_ceiling: null pointer");
-  if (mode < 0 || mode > 3) return fail(QR_EINVAL, "qr_gather_ceiling: mode must be 0..3");
+  if (mode < 0 || mode > 4) return fail(QR_EINVAL, "qr_gather_ceiling: mode must be 0..4");
+  if (mode == 4 && (h->layout != QR_LAYOUT_QUADRANK16))
+    return fail(QR_EINVAL, "qr_gather_ceiling: mode 4 (rank_4 output shape) needs a QuadRank16 handle");
   if (mode == 3 && (h->sigma != 2 || !h->spack))
     return fail(QR_EINVAL, "qr_gather_ceiling: mode 3 needs a BiRank16 handle with a superblock cache");
   DeviceGuard dg(h->device);

@@ -460,6 +460,12 @@ __global__ void __launch_bounds__(256) k_qd_gather2(const uint4* __restrict__ li
 #pragma unroll
     for (int k = 0; k < K; ++k) {
       const uint64_t idx = i0 + (uint64_t)k * npair;
+      if (MODE == 4) {          // rank_4's output shape: each lane of the pair stores 16 B (32 B per query)
+        const uint64_t a = w[k][0] ^ w[k][1], b = w[k][2] ^ w[k][3];
+        if (idx < m) asm volatile("st.global.L1::no_allocate.v2.u64 [%0], {%1,%2};" ::"l"(out + 4 * idx + 2 * half),
+                                  "l"(a), "l"(b) : "memory");
+        continue;
+      }
       uint64_t v = w[k][0] ^ w[k][1] ^ w[k][2] ^ w[k][3];
       v ^= __shfl_xor_sync(0xffffffffu, v, 1);
       if (half == 0 && idx < m) st_stream_u64(out + idx, v);
@@ -532,10 +538,12 @@ static cudaError_t qd_gather_k(const qr_index* h, const uint64_t* q, uint64_t* o
     const int dev = h->device, sms = h->sm_count;
 #define QR_QG2(SQ, MO) launch_ordered(k_qd_gather2<K, SQ, MO, false>, k_qd_gather2<K, SQ, MO, true>, dyn, dev, sms, g, st, \
                                       L, q, out, m, last)
+    if (mode == 4) return small ? QR_QG2(true, 4) : QR_QG2(false, 4);
     if (small) return mode ? QR_QG2(true, 1) : QR_QG2(true, 0);
     return mode ? QR_QG2(false, 1) : QR_QG2(false, 0);
 #undef QR_QG2
   }
+  if (mode == 4) return cudaErrorNotSupported;   // the rank_4-shaped ceiling exists for lane pairs only
   if (small) {
     if (mode) k_qd_gather<K, true, 1><<<g, 256, 0, st>>>(h->lines, q, out, m, last);
     else      k_qd_gather<K, true, 0><<<g, 256, 0, st>>>(h->lines, q, out, m, last);

@@ -448,3 +448,28 @@ def test_concurrent_host_threads(cuda):
     for t in ts:
         t.join()
     assert not errors, errors
+
+
+def test_gather_ceiling_rank4_shape(cuda):
+    """qr_gather_ceiling mode 4 (QuadRank16): rank_4's loads and its 32-B output per query — lane 0
+    of a pair stores the XOR pairs of sector 0, lane 1 those of sector 1 when the query reads it."""
+    torch = _torch()
+    n = 5 * S4 + 321
+    t = gen.dna(17, n)
+    h = qr.qr_quadrank_build(t, n)
+    lines, _ = qr.qr_export_layout(h)
+    u64 = lines.view(np.uint64).reshape(-1, 8)
+    q = gen.queries(18, n, 60000)
+    dq = to_dev(q, cuda)
+    out = torch.zeros((q.size, 4), dtype=torch.uint64, device=cuda)
+    qr.qr_gather_ceiling(h, dq, out, 4)
+    torch.cuda.synchronize()
+    j = (q // B4).astype(np.int64)
+    right = (32 + q - j.astype(np.uint64) * B4) >= 128
+    exp = np.stack([u64[j, 0] ^ u64[j, 1], u64[j, 2] ^ u64[j, 3],
+                    np.where(right, u64[j, 4] ^ u64[j, 5], 0).astype(np.uint64),
+                    np.where(right, u64[j, 6] ^ u64[j, 7], 0).astype(np.uint64)], axis=1)
+    assert np.array_equal(to_host(out), exp)
+    with pytest.raises(qr.QrError):                       # QuadRank16 only
+        hb = qr.qr_birank_build(gen.bits(3, 5000), 5000)
+        qr.qr_gather_ceiling(hb, dq[:10], torch.zeros((10, 4), dtype=torch.uint64, device=cuda), 4)
