@@ -84,6 +84,19 @@ def broadcast_index(h, n: int, layout: int, dist, device, src: int = 0):
     return qr_import_layout(lines, sup if sb else None, n, layout, device=device.index if hasattr(device, "index") else 0)
 
 
+def parse_cpulist(text: str) -> set:
+    """CPU ids of a Linux cpulist string ("0-7,16-23,40")."""
+    cpus = set()
+    for part in text.strip().split(","):
+        part = part.strip()
+        if "-" in part:
+            a, b = part.split("-")
+            cpus.update(range(int(a), int(b) + 1))
+        elif part:
+            cpus.add(int(part))
+    return cpus
+
+
 def gpu_local_cpus(device: int = 0) -> dict:
     """CPUs and NUMA node local to a GPU's PCI device (sysfs), intersected with the CPUs this
     process may run on.  Pinned host buffers allocated while running there land on the GPU's
@@ -96,15 +109,10 @@ def gpu_local_cpus(device: int = 0) -> dict:
     cpus, node = set(), -1
     try:
         with open(f"{base}/local_cpulist") as f:
-            for part in f.read().strip().split(","):
-                if "-" in part:
-                    a, b = part.split("-")
-                    cpus.update(range(int(a), int(b) + 1))
-                elif part:
-                    cpus.add(int(part))
+            cpus = parse_cpulist(f.read())
         with open(f"{base}/numa_node") as f:
             node = int(f.read().strip())
-    except OSError:
+    except (OSError, ValueError):
         pass
     import os
 

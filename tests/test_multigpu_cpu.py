@@ -72,3 +72,11 @@ def test_two_rank_gloo_shard_invariance():
     assert all(r[5] == 11.0 for r in res)                       # max over ranks
     assert all(r[6] == total for r in res)
     assert res[0][7] == res[1][7]
+
+
+def test_parse_cpulist():
+    from paper_2602_04103_b200.multigpu import parse_cpulist
+
+    assert parse_cpulist("0-3,8,10-11\n") == {0, 1, 2, 3, 8, 10, 11}
+    assert parse_cpulist("5") == {5}
+    assert parse_cpulist("") == set()
