@@ -683,3 +683,24 @@ def test_fm_count_approx_both_strands(cuda, n, kind, bwt_layout, kmax, fm_dyn_re
     qr.qr_sync()
     assert np.array_equal(hf, oracle.scan_count_hdk(sym, reads, roffs, np.full(m, L, np.uint32), kmax))
     assert np.array_equal(hr, oracle.scan_count_hdk(sym, rr, roffs, np.full(m, L, np.uint32), kmax))
+
+
+def test_fm_empty_batches(cuda):
+    """m = 0 is a no-op (QR_OK, nothing written) for every FM entry point, device and host."""
+    torch = _torch()
+    w = gen.dna(77, 3000)
+    fm = qr.qr_fm_build(w, 3000)
+    d = torch.full((4,), 7, dtype=torch.int32, device=cuda)
+    r = torch.full((4,), 7, dtype=torch.int32, device=cuda)
+    p = torch.zeros(64, dtype=torch.uint8, device=cuda)
+    qr.qr_fm_count(fm, p, None, 8, d, 0)
+    qr.qr_fm_count_both(fm, p, None, 8, d, r, 0)
+    for k in range(4):
+        qr.qr_fm_count_approx(fm, p, None, 8, k, d, 0)
+        qr.qr_fm_count_approx_both(fm, p, None, 8, k, d, r, 0)
+    torch.cuda.synchronize()
+    assert int(d.sum()) == 28 and int(r.sum()) == 28
+    h = np.full(4, 7, np.uint32)
+    qr.qr_fm_count(fm, np.zeros(64, np.uint8), np.zeros(4, np.uint32), 0, h, 0)
+    qr.qr_sync()
+    assert int(h.sum()) == 28
