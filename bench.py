@@ -174,7 +174,12 @@ class Ctx:
         return self.max_over_ranks(ms)
 
 
-from paper_2602_04103_b200.multigpu import on_gpu_local_cpus, shard  # noqa: E402  (contiguous shard of a global index range)
+def shard(total, world, rank):
+    """contiguous shard of a global index range (paper_2602_04103_b200.multigpu.shard), imported
+    lazily: the product package loads libqrank.so on import, which the reference arm must not."""
+    from paper_2602_04103_b200.multigpu import shard as _shard
+
+    return _shard(total, world, rank)
 
 
 # ------------------------------------------------------------------ rows
@@ -220,6 +225,8 @@ def bench_birank(ctx, p: float, steps, warmup, with_ceiling: bool, clocks=None, 
         # the full per-GPU batch from pinned host memory at N = 1; at N > 1 each rank stages
         # M2 / N queries so that the box pins ~16 GB in total, not 16 GB per GPU
         me = M2 if ctx.world == 1 else max(10**8, M2 // ctx.world)
+        from paper_2602_04103_b200.multigpu import on_gpu_local_cpus
+
         with on_gpu_local_cpus(ctx.dev.index or 0):     # pinned pages on the GPU's NUMA node
             qh = torch.empty(me, dtype=torch.uint64).pin_memory()
             oh = torch.empty(me, dtype=torch.uint64).pin_memory()
@@ -569,8 +576,20 @@ def run_reference(args):
             "cpu_baseline": {"value": round(v, 6), "unit": "Gqueries/s", "cores": oracle.threads(), "kind": "oracle",
                              "sample": f"{q.size} of the configs[1] queries per step (host-regenerated), text 2^34 bits; "
                                        f"prefix-array precompute {prep:.1f}s untimed"},
-            "e2e": {"value": round(v, 6), "unit": "Gqueries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+            "e2e": {"value": round(v, 6), "unit": "Gqueries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "repo_so_loaded": repo_so_loaded()}
     print(json.dumps(line), flush=True)
+
+
+def repo_so_loaded():
+    """The repo's own shared libraries mapped into this process (the reference arm must show only
+    oracle/ and gen/, never the product's libqrank.so)."""
+    try:
+        with open("/proc/self/maps") as f:
+            paths = {l.split()[-1] for l in f if l.rstrip().endswith(".so") and ROOT in l}
+        return sorted(os.path.relpath(p, ROOT) for p in paths)
+    except OSError:
+        return None
 
 
 def workload_config(n_gpus):

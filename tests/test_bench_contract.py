@@ -30,6 +30,8 @@ def test_reference_arm_json_line():
     assert cb["kind"] == "oracle" and cb["value"] == d["value"] and cb["sample"]
     assert cb["cores"] == len(os.sched_getaffinity(0))   # all host cores, whatever OMP_NUM_THREADS says
     assert d["e2e"] == {"value": d["value"], "unit": d["unit"], "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
+    # the oracle arm maps only the oracle and the generators, never the product library
+    assert d["repo_so_loaded"] and all(p.startswith(("oracle/", "gen/")) for p in d["repo_so_loaded"]), d["repo_so_loaded"]
 
 
 def test_reference_arm_other_ranks_silent():

@@ -270,6 +270,89 @@ def test_fm_work_instrumentation_consistent():
     assert np.array_equal(cnt[0::2] >= 1, np.ones(100, bool))    # exact substrings occur
 
 
+def _suffixes(sym):
+    """Every suffix of T$ as a tuple, '$' = -1 (smaller than every symbol)."""
+    return [tuple(int(x) for x in sym[i:]) + (-1,) for i in range(len(sym) + 1)]
+
+
+def _brute_interval(suf, Q):
+    """[lo, hi) of Q in the sorted suffixes of T$, from the suffix strings themselves
+    (no BWT, no LF mapping): lo = #suffixes whose first |Q| symbols compare below Q
+    ('$' = -1, smaller than every symbol), hi = lo + #suffixes that start with Q
+    (App. D: a BWT interval is the block of rows prefixed by Q)."""
+    L = len(Q)
+    Qt = tuple(int(x) for x in Q)
+    lo = cnt = 0
+    for s_i in suf:
+        head = s_i[:L]
+        if head < Qt:
+            lo += 1
+        elif head == Qt:
+            cnt += 1
+    return lo, lo + cnt
+
+
+def _brute_work(sym, suf, P, skip, block):
+    """(post-seed backward steps, distinct `block`-row lines touched) for one pattern,
+    derived from the definition of backward search: the step that
+    consumes P[j] runs iff the interval of P[j+1:] is non-empty (counted by a direct scan
+    of the text), it ranks at that interval's lo and hi, and the first `skip` steps of a
+    pattern of >= skip symbols are seeded by the k-mer table and not counted."""
+    L = len(P)
+    sk = skip if L >= skip else 0
+    steps = lines = 0
+    for t, j in enumerate(range(L - 1, -1, -1)):
+        Q = P[j + 1:]
+        occ = len(sym) + 1 if len(Q) == 0 else sum(
+            1 for a in range(len(sym) - len(Q) + 1) if np.array_equal(sym[a:a + len(Q)], Q))
+        if occ == 0:
+            break
+        if t >= sk:
+            lo, hi = _brute_interval(suf, Q)
+            assert hi - lo == occ                     # the two brute-force views agree
+            steps += 1
+            lines += 1 if lo // block == hi // block else 2
+    return steps, lines
+
+
+@pytest.mark.parametrize("block", [224, 192, 64, 7])
+def test_fm_work_vs_bruteforce_intervals(block):
+    """Pin for or_fm_work (SURVEY.md §8(c) instrumented mode, the FM algorithmic-bytes
+    denominator): per pattern, recompute the executed post-seed steps and the distinct lines
+    from brute-force suffix intervals, never from the oracle's own loop.  Covers patterns
+    shorter than the skip, intervals that empty mid-pattern, exact substrings (never empty),
+    repetitive texts (wide intervals that straddle lines) and skip = 0."""
+    rng = np.random.default_rng(block)
+    for t in range(6):
+        n = int(rng.integers(40, 300))
+        if t % 3 == 0:
+            sym = rng.integers(0, 4, n).astype(np.uint8)
+        elif t % 3 == 1:
+            sym = np.tile(rng.integers(0, 4, 3), n)[:n].astype(np.uint8)
+        else:
+            sym = np.where(rng.random(n) < 0.9, 0, rng.integers(0, 4, n)).astype(np.uint8)
+        f = oracle.FmOracle(sym)
+        suf = _suffixes(sym)
+        pats = [rng.integers(0, 4, int(rng.integers(0, 12))).astype(np.uint8) for _ in range(12)]
+        pats += [sym[a:a + int(rng.integers(1, 20))].copy() for a in rng.integers(0, n, 8)]
+        # exact substring with one late substitution: the interval empties mid-pattern
+        for a in rng.integers(0, max(1, n - 16), 4):
+            p = sym[a:a + 16].copy()
+            if p.size:
+                p[1] = (p[1] + 1) % 4
+            pats.append(p)
+        for skip in (0, 3, 8):
+            exp_s = exp_l = 0
+            for p in pats:
+                s_, l_ = _brute_work(sym, suf, p, skip, block)
+                exp_s += s_
+                exp_l += l_
+                cat1, off1, len1 = oracle.pack_patterns([p])
+                assert f.work(cat1, off1, len1, skip=skip, block=block) == (s_, l_), (list(p), skip)
+            cat, off, lens = oracle.pack_patterns(pats)
+            assert f.work(cat, off, lens, skip=skip, block=block) == (exp_s, exp_l)
+
+
 def test_hd1_scan_vs_bruteforce_and_variant_sum():
     """<=1-substitution counts: Python brute force on tiny texts, and the identity
     count_hd1(P) = sum over P and its 3L single-substitution variants of the exact count."""
