@@ -228,10 +228,12 @@ qr_status qr_export_layout(const qr_index* h, void* host_lines, void* host_super
 
 /* Re-create a handle from a layout saved with qr_export_layout (checkpoint / resume without
  * rebuilding; builds are deterministic): lines and super are host or device buffers of
- * the sizes qr_info reports for (n, layout); super may be NULL for layouts without an L1 array.
- * The contents are trusted (no validation pass). */
-qr_status qr_import_layout(const void* lines, const void* super, uint64_t n, int layout, int device, void* stream,
-                           qr_index** out);
+ * line_bytes and super_bytes bytes, which must equal the sizes qr_info reports for (n, layout)
+ * (else QR_EINVAL: a truncated file or a mismatched n is rejected before any copy); super may be
+ * NULL (super_bytes 0) for layouts without an L1 array.  The contents are trusted (no
+ * validation pass over the words). */
+qr_status qr_import_layout(const void* lines, uint64_t line_bytes, const void* super, uint64_t super_bytes, uint64_t n,
+                           int layout, int device, void* stream, qr_index** out);
 
 /* n, N = n+1 BWT rows, spos, C[0..4] (C[4] = n+1), and the QuadRank handle over the BWT
  * (owned by fm; valid until qr_fm_free). */

@@ -79,7 +79,7 @@ def lib():
             "qr_build": ([V, U64, I32, I32, V, PP], I32),
             "qr_layout": ([V, C.POINTER(C.c_int)], I32),
             "qr_rank_chain": ([V, V, V, V, U64, U64, V], I32),
-            "qr_import_layout": ([V, V, U64, I32, I32, V, PP], I32),
+            "qr_import_layout": ([V, U64, V, U64, U64, I32, I32, V, PP], I32),
             "qr_fm_build_ex": ([V, U64, V, I32, I32, V, PP], I32),
             "qr_fm_kmer_width": ([V, C.POINTER(C.c_int)], I32),
             "qr_fm_build_opts": ([V, U64, V, I32, I32, I32, V, PP], I32),
@@ -123,12 +123,29 @@ def _nbytes_item(a):
     return None
 
 
+def _contig(a, name: str):
+    """Reject strided views (torch non-contiguous, stride-0 expansions; numpy non-C-contiguous or
+    negative strides): the library reads and writes dense arrays from the data pointer."""
+    if a is None or isinstance(a, int):
+        return
+    if hasattr(a, "is_contiguous"):
+        if not a.is_contiguous():
+            raise QrError(QR_EINVAL, name, "tensor is not contiguous")
+        if a.numel() > 1 and any(st == 0 for st, sz in zip(a.stride(), a.shape) if sz > 1):
+            raise QrError(QR_EINVAL, name, "tensor has a zero stride")
+    elif hasattr(a, "flags"):
+        if not a.flags["C_CONTIGUOUS"] or any(st < 0 for st in a.strides):
+            raise QrError(QR_EINVAL, name, "array is not C-contiguous")
+
+
 def _need(a, itemsize: int, count: int, name: str):
-    """Reject arrays whose element size or length cannot hold `count` items (marshalling check:
-    a wrong dtype would otherwise be read or written out of bounds by the kernels)."""
+    """Reject arrays whose element size or length cannot hold `count` items, or that are not
+    dense (marshalling check: a wrong dtype or a strided view would otherwise be read or written
+    out of bounds by the kernels)."""
     info = _nbytes_item(a)
     if info is None:
         return
+    _contig(a, name)
     es, n = info
     if es * n < itemsize * count or (es != itemsize and itemsize in (1, 4, 8) and es not in (itemsize,)):
         raise QrError(QR_EINVAL, name, f"needs {count} items of {itemsize} B, got {n} of {es} B")
@@ -203,18 +220,22 @@ class Fm:
 
 # ----------------------------------------------------------------- C-ABI mirror (same names)
 def qr_birank_build(bits, n: int, device: int = 0, stream=None) -> Index:
+    _need(bits, 8, (n + 63) // 64, "qr_birank_build bits")
     out = C.c_void_p()
     _check(lib().qr_birank_build(_ptr(bits), n, device, _stream(stream), C.byref(out)), "qr_birank_build")
     return Index(out.value)
 
 
 def qr_build(text, n: int, layout: int, device: int = 0, stream=None) -> Index:
+    sigma2 = layout in (QR_LAYOUT_BIRANK16, QR_LAYOUT_BIRANK64X2, QR_LAYOUT_BIRANK16X2, QR_LAYOUT_BIRANK32X2)
+    _need(text, 8, (n + 63) // 64 if sigma2 else (n + 31) // 32, "qr_build text")
     out = C.c_void_p()
     _check(lib().qr_build(_ptr(text), n, layout, device, _stream(stream), C.byref(out)), "qr_build")
     return Index(out.value)
 
 
 def qr_quadrank_build(text2b, n: int, device: int = 0, stream=None) -> Index:
+    _need(text2b, 8, (n + 31) // 32, "qr_quadrank_build text2b")
     out = C.c_void_p()
     _check(lib().qr_quadrank_build(_ptr(text2b), n, device, _stream(stream), C.byref(out)), "qr_quadrank_build")
     return Index(out.value)
@@ -252,6 +273,8 @@ def qr_fm_build(text2b, n: int, sa=None, device: int = 0, stream=None, kmer_k: i
                 bwt_layout: int | None = None) -> Fm:
     """qr_fm_build (kmer_k None: the library's default width for n), qr_fm_build_ex (explicit width) or
     qr_fm_build_opts (explicit BWT rank layout, QR_LAYOUT_QUADRANK16 or QR_LAYOUT_QUADRANK16X2)."""
+    _need(text2b, 8, (n + 31) // 32, "qr_fm_build text2b")
+    _need(sa, 4, n + 1, "qr_fm_build sa")
     out = C.c_void_p()
     if bwt_layout is not None:
         k = kmer_k if kmer_k is not None else -1          # -1: the library's default width for n
@@ -271,6 +294,7 @@ def _need_fm(where: str, patterns, lengths, fixed_len: int, m: int, *outs):
         _need(o, 4, m, f"{where} out")
     if lengths is not None:
         _need(lengths, 4, m, f"{where} lengths")
+        _contig(patterns, f"{where} patterns")
     else:
         _need(patterns, 1, m * fixed_len, f"{where} patterns")
 
@@ -329,10 +353,23 @@ def qr_export_layout(h: Index):
     return lines, sup.view(np.uint32)
 
 
+def _byte_size(a) -> int:
+    if a is None:
+        return 0
+    es, n = _nbytes_item(a)
+    return es * n
+
+
 def qr_import_layout(lines, sup, n: int, layout: int, device: int = 0, stream=None) -> Index:
+    """lines / sup: contiguous torch tensors or numpy arrays (host or device) holding exactly the
+    layout's bytes; their sizes are passed to the library, which rejects a mismatch."""
+    _contig(lines, "qr_import_layout lines")
+    if sup is not None and _byte_size(sup) == 0:
+        sup = None
+    _contig(sup, "qr_import_layout super")
     out = C.c_void_p()
-    sp = _ptr(sup) if sup is not None and getattr(sup, "size", 1) else None
-    _check(lib().qr_import_layout(_ptr(lines), sp, n, layout, device, _stream(stream), C.byref(out)), "qr_import_layout")
+    _check(lib().qr_import_layout(_ptr(lines), _byte_size(lines), _ptr(sup), _byte_size(sup), n, layout, device,
+                                  _stream(stream), C.byref(out)), "qr_import_layout")
     return Index(out.value)
 
 

@@ -7,6 +7,7 @@
 #include <stdio.h>
 #include <string.h>
 
+#include <map>
 #include <mutex>
 #include <new>
 #include <vector>
@@ -25,7 +26,8 @@ int g_rank_s_lane = 1;
 int g_fm_dyn = 1;               // FM count: 1 = persistent grid + warp chunks from a global counter, 0 = static grid stride
 int g_fm_seed = 0;              // FM seed pre-pass (dynamic order only): 0 auto (L2-resident BWT), 1 never, 2 always
 int g_fm_smem = 1;              // FM superblock words from shared memory: 0 off, 1 auto, 2 packed table whenever it fits
-int g_fm_lean = 0;              // FM step flavour: 0 auto (by L2 residency), 1 de-duplicating, 2 lean
+int g_fm_refill = 8;            // L2-resident count kernel: refill a warp's lanes once this many are idle
+int g_fm_lean = 0;              // FM step flavour: 0 auto (by L2 residency), 1 de-duplicating, 2 lean, 3 one line per iteration
 int g_index64 = 0;              // 1: force the 64-bit line-index path (tests the n >= 2^36/2^37 code on small n)
 int g_rank_smem = 1;            // superblock words from cluster shared memory: 0 never, 1 large batches, 2 always
 int g_rank_dyn = 1;             // cluster rank kernels: 1 = dynamic (atomic chunk) work order, 0 = static grid stride
@@ -39,6 +41,22 @@ int g_rank_big_cs = 0;          // cluster size of that table: 0 smallest that f
 int g_rank_pair = 2;            // kernel shape: 2 by structure size (default), 1 lane pairs (one L2 request per query), 0 one lane per query
 uint64_t g_stage_chunk = 1ull << 23;   // queries per chunk on the staged host path (sweep: profiles/r01_e2e_sweep)
 int g_stage_slots = 3;                 // device buffers / internal streams of the staged path
+
+cudaError_t smem_limit_raise(const void* kern, size_t bytes, int device) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, size_t> limit;
+  if (bytes <= 48 * 1024) return cudaSuccess;          // the default limit
+  std::lock_guard<std::mutex> g(mu);
+  size_t& lim = limit[std::make_pair(kern, device)];
+  if (bytes <= lim) return cudaSuccess;
+  int prev = -1;
+  cudaGetDevice(&prev);
+  if (prev != device) cudaSetDevice(device);
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (prev >= 0 && prev != device) cudaSetDevice(prev);
+  if (e == cudaSuccess) lim = bytes;
+  return e;
+}
 
 static thread_local char t_err[512] = "";
 
@@ -380,8 +398,11 @@ QR_EXPORT qr_status qr_set_tuning(const char* key, int64_t value) {
   } else if (!strcmp(key, "fm_smem")) {
     if (value < 0 || value > 2) return fail(QR_EINVAL, "fm_smem must be 0 (off), 1 (auto) or 2 (packed)");
     g_fm_smem = (int)value;
+  } else if (!strcmp(key, "fm_refill")) {
+    if (value < 1 || value > 32) return fail(QR_EINVAL, "fm_refill must be 1..32");
+    g_fm_refill = (int)value;
   } else if (!strcmp(key, "fm_step")) {
-    if (value < 0 || value > 2) return fail(QR_EINVAL, "fm_step must be 0 (auto), 1 or 2");
+    if (value < 0 || value > 3) return fail(QR_EINVAL, "fm_step must be 0 (auto), 1, 2 or 3");
     g_fm_lean = (int)value;
   } else if (!strcmp(key, "index64")) {
     if (value != 0 && value != 1) return fail(QR_EINVAL, "index64 must be 0 or 1");
@@ -760,8 +781,8 @@ QR_EXPORT qr_status qr_export_layout(const qr_index* h, void* host_lines, void* 
   return QR_OK;
 }
 
-QR_EXPORT qr_status qr_import_layout(const void* lines, const void* super, uint64_t n, int layout, int device,
-                                     void* stream, qr_index** out) {
+QR_EXPORT qr_status qr_import_layout(const void* lines, uint64_t line_bytes, const void* super, uint64_t super_bytes,
+                                     uint64_t n, int layout, int device, void* stream, qr_index** out) {
   if (!out || !lines) return fail(QR_EINVAL, "qr_import_layout: null pointer");
   *out = nullptr;
   if (layout < QR_LAYOUT_BIRANK16 || layout > QR_LAYOUT_BIRANK32X2) return fail(QR_EINVAL, "qr_import_layout: bad layout");
@@ -773,6 +794,13 @@ QR_EXPORT qr_status qr_import_layout(const void* lines, const void* super, uint6
   qr_status s = alloc_index(sigma, n, device, &h, layout);
   if (s != QR_OK) return s;
   if (super_bytes_of(h) && !super) { qr_free(h); return fail(QR_EINVAL, "qr_import_layout: layout needs a superblock array"); }
+  if (line_bytes != h->n_lines * 64 || super_bytes != super_bytes_of(h)) {
+    const uint64_t el = h->n_lines * 64, es = super_bytes_of(h);
+    qr_free(h);
+    return fail(QR_EINVAL, "qr_import_layout: buffer sizes (%llu, %llu) B differ from the layout's (%llu, %llu) B for n = %llu",
+                (unsigned long long)line_bytes, (unsigned long long)super_bytes, (unsigned long long)el,
+                (unsigned long long)es, (unsigned long long)n);
+  }
   cudaStream_t st = (cudaStream_t)stream;
   cudaError_t e = cudaMemcpyAsync(h->lines, lines, h->n_lines * 64, cudaMemcpyDefault, st);
   if (!e && super_bytes_of(h)) e = cudaMemcpyAsync(h->super, super, super_bytes_of(h), cudaMemcpyDefault, st);

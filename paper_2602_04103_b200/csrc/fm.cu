@@ -483,11 +483,25 @@ struct PatWindow {
     base = P - mis;
     wk = -1;
   }
+  // The reload is a predicated load every lane issues (no branch), so a warp whose lanes cross
+  // their 8-byte windows at different steps does not split (ncu: the branchy reload ran with ~2
+  // of 32 lanes active in every loop iteration of the count kernel).
+  // at() for lanes that may hold no task (act == false): no load is issued for them
+  __device__ __forceinline__ uint32_t at_if(bool act, int64_t k) {
+    const int64_t a = k + mis;
+    const int64_t w = a >> 3;
+    const bool need = act && w != wk;
+    ldg_u64_keep(need, reinterpret_cast<const unsigned long long*>(base) + w, word);
+    wk = need ? w : wk;
+    return (uint32_t)(word >> (8 * ((uint32_t)a & 7u))) & 3u;
+  }
   __device__ __forceinline__ uint32_t at(int64_t k) {
     const int64_t a = k + mis;
     const int64_t w = a >> 3;
-    if (w != wk) { word = __ldg(reinterpret_cast<const unsigned long long*>(base) + w); wk = w; }
-    return (uint32_t)(word >> (8 * (a & 7))) & 3u;
+    const bool need = w != wk;
+    ldg_u64_keep(need, reinterpret_cast<const unsigned long long*>(base) + w, word);
+    wk = w;
+    return (uint32_t)(word >> (8 * ((uint32_t)a & 7u))) & 3u;
   }
 };
 
@@ -534,6 +548,95 @@ __device__ __forceinline__ void fm_step_lean(const FmParams& F, uint4 C4, uint32
   const uint32_t Cc = pick4(C4, c);
   lo = Cc + rl;
   hi = Cc + rh;
+}
+
+// ---- the "one line per iteration" step (knob fm_step = 3; default on L2-resident BWTs) -------
+// A backward step ranks c at lo and at hi.  After the k-mer seed the interval
+// is narrow, so lo and hi nearly always fall in one line ("cache lines are
+// automatically reused"); then one line gather, one delta, one superblock word and one C[c]
+// serve both ranks, and Occ(c, hi) differs from Occ(c, lo) only by the masked popcount of that
+// line's own planes.  When they do not share a line, the step takes two loop iterations: this
+// one ranks at lo (`pend` set, hi kept), the next ranks at hi.  Every iteration therefore runs
+// the same instructions — one line, up to two masked counts — and no lane of a warp waits on a
+// divergent second-rank path.  Returns true when the step is complete.
+__device__ __forceinline__ uint64_t half_mask(uint32_t xx, int t, bool right) {
+  // chars [xx, 128) of a half (left of the anchor) or [0, xx) (right of it), word t (64 chars)
+  const uint64_t pm = prefix_mask((int)xx, t);
+  return right ? pm : ~pm;
+}
+
+template <int SMS>
+__device__ __forceinline__ bool fm_step_pend(const FmParams& F, uint4 C4, uint32_t c, uint32_t& lo, uint32_t& hi,
+                                             uint32_t& pend, uint32_t& lines) {
+  const uint32_t x = pend ? hi : lo;
+  const uint32_t j = (x >> 5) / 7u;                    // floor(x / 224); lo, hi <= N: j <= last_line
+  const uint32_t jy = (hi >> 5) / 7u;
+  const uint32_t p = x + 32u - j * (uint32_t)QD_B;
+  const uint32_t py = hi + 32u - j * (uint32_t)QD_B;   // meaningful when jy == j
+  const bool rx = p >= 128u;
+  // hi is ranked in this iteration when it lies in the same half line (same 32-B sector, same
+  // delta); a pair split by the anchor or by a line boundary takes a second iteration
+  const bool two = !pend && jy == j && ((py >= 128u) == rx);
+  lines = pend ? 0u : (jy == j ? 1u : 2u);             // distinct lines of the step, counted once
+  const uint64_t* L = reinterpret_cast<const uint64_t*>(F.lines) + 8 * (uint64_t)j;
+  uint64_t a0, a1, a2, a3;
+  ld_sector(L + (rx ? 4 : 0), a0, a1, a2, a3);
+  const uint64_t dr = ldg_u64_if(rx, L + (c >> 1));   // right of the anchor: the delta word of sector 0
+  const uint32_t s = fm_super<SMS>(F, j >> QD_SB_LOG, c);
+  const uint64_t cl = 0ull - (uint64_t)(c & 1u), ch = 0ull - (uint64_t)(c >> 1);
+  const uint64_t ma0 = (a0 ^ cl) & (a1 ^ ch), ma1 = (a2 ^ cl) & (a3 ^ ch);   // c at each char of the half
+  // count masks: left of the anchor chars [xx, 128) = ~0 << d_t per word; right chars [0, xx) = its complement
+  const uint64_t inv = rx ? ~0ull : 0ull;
+  const uint32_t xx = p & 127u, yy = py & 127u;
+  const uint32_t d0 = min(xx, 64u), d1 = xx - d0, e0 = min(yy, 64u), e1 = yy - e0;
+  const uint32_t cx = __popcll(ma0 & (ones_shl(d0) ^ inv)) + __popcll(ma1 & (ones_shl(d1) ^ inv));
+  const uint32_t cy = __popcll(ma0 & (ones_shl(e0) ^ inv)) + __popcll(ma1 & (ones_shl(e1) ^ inv));
+  const uint64_t dw = rx ? dr : ((c & 2u) ? a1 : a0);
+  const uint32_t base = (s << QD_SHIFT) + (uint32_t)((dw >> (16 * (c & 1u))) & 0xffffull);
+  const uint32_t dol = c == 0 ? 1u : 0u;               // '$' stored as A at row spos
+  const uint32_t vx = (rx ? base + cx : base - cx) - (dol & (x > (uint32_t)F.spos ? 1u : 0u));
+  const uint32_t vy = (rx ? base + cy : base - cy) - (dol & (hi > (uint32_t)F.spos ? 1u : 0u));
+  const uint32_t Cc = pick4(C4, c);
+  const uint32_t nlo = Cc + vx, nhi = Cc + vy;
+  const bool done = pend || two;
+  lo = pend ? lo : nlo;
+  hi = pend ? nlo : (two ? nhi : hi);
+  pend = done ? 0u : 1u;
+  return done;
+}
+
+// The same over a QuadRank16x2 BWT: lo and hi share the iteration when they fall in one 32-B
+// sector (one gather, one delta, one superblock word); otherwise two iterations.
+template <int SMS>
+__device__ __forceinline__ bool fm_step_pend_x2(const FmParams& F, uint4 C4, uint32_t c, uint32_t& lo, uint32_t& hi,
+                                                uint32_t& pend, uint32_t& lines) {
+  const uint32_t x = pend ? hi : lo;
+  uint32_t j, h, p, jy, hy, py;
+  x2_locate(x, (uint32_t)F.last_line, j, h, p);
+  x2_locate(hi, (uint32_t)F.last_line, jy, hy, py);
+  const bool two = !pend && jy == j && hy == h;
+  lines = pend ? 0u : (jy == j ? 1u : 2u);
+  uint64_t w0, w1, w2, w3;
+  ld_sector(F.lines + 4 * (uint64_t)j + 2 * h, w0, w1, w2, w3);
+  const uint32_t s = fm_super<SMS>(F, j >> QD_SB_LOG, c);
+  const uint64_t nl = (c & 1u) ? 0ull : ~0ull, nh = (c & 2u) ? 0ull : ~0ull;   // planes (variants.cu)
+  const uint64_t m0 = (w1 ^ nl) & (w2 ^ nh);
+  const uint32_t m1 = ((uint32_t)w3 ^ (uint32_t)nl) & ((uint32_t)(w3 >> 32) ^ (uint32_t)nh);
+  const uint4 mx = reinterpret_cast<const uint4*>(g_x2_masks)[p];
+  const uint4 my = reinterpret_cast<const uint4*>(g_x2_masks)[two ? py : p];
+  const uint32_t cx = __popcll(m0 & (((uint64_t)mx.y << 32) | mx.x)) + __popc(m1 & mx.z);
+  const uint32_t cy = __popcll(m0 & (((uint64_t)my.y << 32) | my.x)) + __popc(m1 & my.z);
+  const uint32_t base = (s << QD_SHIFT) + (uint32_t)((w0 >> (16 * c)) & 0xffffull);
+  const uint32_t dol = c == 0 ? 1u : 0u;
+  const uint32_t vx = (p >= 48 ? base + cx : base - cx) - (dol & (x > (uint32_t)F.spos ? 1u : 0u));
+  const uint32_t vy = (py >= 48 ? base + cy : base - cy) - (dol & (hi > (uint32_t)F.spos ? 1u : 0u));
+  const uint32_t Cc = pick4(C4, c);
+  const uint32_t nlo = Cc + vx, nhi = Cc + vy;
+  const bool done = pend || two;
+  lo = pend ? lo : nlo;
+  hi = pend ? nlo : (two ? nhi : hi);
+  pend = done ? 0u : 1u;
+  return done;
 }
 
 // 8-mer table key of the pattern's last 8 symbols (P[len-8..len), 2 bits each, the last symbol
@@ -641,7 +744,7 @@ constexpr uint32_t FM_CHUNK = 64;
 #define QR_FM_MINB 4
 #endif
 
-template <bool FIXED, bool WORK, int STRANDS, bool LEAN, int SMS, bool DYN, int BW = 0>
+template <bool FIXED, bool WORK, int STRANDS, int STEP, int SMS, bool DYN, int BW = 0>
 __global__ void __launch_bounds__(256, QR_FM_MINB) k_fm_count(FmParams F, const uint8_t* __restrict__ pat,
                                                      const uint64_t* __restrict__ offs, const uint32_t* __restrict__ lens,
                                                      uint32_t fixed_len, uint32_t* __restrict__ out,
@@ -677,12 +780,23 @@ __global__ void __launch_bounds__(256, QR_FM_MINB) k_fm_count(FmParams F, const 
     // instead of following it (the first step's symbol is otherwise a dependent miss)
     if (DYN && seeds && k >= 0) (void)P.at(rc ? (int64_t)len - 1 - k : k);
   };
+  uint32_t pend = 0, csym = 0;                           // STEP 3: hi's rank deferred to the next iteration
   auto step = [&]() {                                    // one backward step (LF mapping)
+    if (STEP == 3) {
+      // k stays put while hi's rank is pending, so the symbol is simply re-read (no divergence)
+      csym = rc ? 3u - P.at((int64_t)len - 1 - k) : P.at(k);
+      uint32_t nl;
+      const bool done = BW == 1 ? fm_step_pend_x2<SMS>(F, C4, csym, lo, hi, pend, nl)
+                                : fm_step_pend<SMS>(F, C4, csym, lo, hi, pend, nl);
+      if (done) --k;
+      if (WORK) { n_steps += pend ? 0 : 1; n_lines += nl; }
+      return;
+    }
     const uint32_t c = rc ? 3u - P.at((int64_t)len - 1 - k) : P.at(k);
     uint32_t nl;
-    if (BW == 1)   fm_step_x2<SMS>(F, c, lo, hi, nl, &C4);
-    else if (LEAN) fm_step_lean<SMS>(F, C4, c, lo, hi, nl);
-    else           fm_step<SMS, 0>(F, c, lo, hi, nl);
+    if (BW == 1)        fm_step_x2<SMS>(F, c, lo, hi, nl, &C4);
+    else if (STEP == 2) fm_step_lean<SMS>(F, C4, c, lo, hi, nl);
+    else                fm_step<SMS, 0>(F, c, lo, hi, nl);
     --k;
     if (WORK) { n_steps += 1; n_lines += nl; }
   };
@@ -694,8 +808,8 @@ __global__ void __launch_bounds__(256, QR_FM_MINB) k_fm_count(FmParams F, const 
   if (!DYN) {
     if (ti < ntask) seed();
     while (ti < ntask) {
-      if (k >= 0 && lo < hi) step();
-      if (k < 0 || lo >= hi) {                           // finished: write, claim the next task
+      if (pend || (k >= 0 && lo < hi)) step();
+      if (!pend && (k < 0 || lo >= hi)) {                // finished: write, claim the next task
         finish();
         ti += stride;
         if (ti < ntask) seed();
@@ -707,8 +821,8 @@ __global__ void __launch_bounds__(256, QR_FM_MINB) k_fm_count(FmParams F, const 
     bool exhausted = false, has = false;
     while (true) {
       if (has) {
-        if (k >= 0 && lo < hi) step();
-        if (k < 0 || lo >= hi) { finish(); has = false; }
+        if (pend || (k >= 0 && lo < hi)) step();
+        if (!pend && (k < 0 || lo >= hi)) { finish(); has = false; }
       }
       const uint32_t needm = __ballot_sync(0xffffffffu, !has);
       if (needm && !exhausted) {
@@ -734,6 +848,104 @@ __global__ void __launch_bounds__(256, QR_FM_MINB) k_fm_count(FmParams F, const 
         }
       }
       if (exhausted && __ballot_sync(0xffffffffu, has) == 0) break;
+    }
+  }
+  if (WORK && n_steps) {
+    atomicAdd(work, (unsigned long long)n_steps);
+    atomicAdd(work + 1, (unsigned long long)n_lines);
+  }
+}
+
+// ---- count kernel for L2-resident BWTs (default there; knob fm_step = 3 forces it) ---------
+// Instruction-bound regime (configs[3]: the 18-21 MB BWT sits in L2, ncu issue-active ~70-75%),
+// so every issue slot counts:
+//  * one line per loop iteration (fm_step_pend / fm_step_pend_x2): lo and hi of a step share the
+//    line, its delta, superblock word and C[c] whenever they share a half line;
+//  * the step runs unconditionally in every lane — lanes without a live task compute on their
+//    last (valid) interval and discard the result — so no lane of a warp diverges around it
+//    (ncu of the guarded loop: its body ran 1.32x per iteration because lanes entering with a
+//    pending rank took a separate path);
+//  * lanes are refilled from the warp's task chunk only once at least `refill_min` of them are
+//    idle: the refill (seed load, pattern pointer) ran in ~93% of iterations with ~3 of 32 lanes
+//    active, ~80 issue slots each time;
+//  * seeds come from the k_fm_seed pre-pass (one 8-byte load per task).
+template <bool FIXED, bool WORK, int STRANDS, int SMS, int BW>
+__global__ void __launch_bounds__(256, QR_FM_MINB) k_fm_count_l2(FmParams F, const uint8_t* __restrict__ pat,
+                                                              const uint64_t* __restrict__ offs,
+                                                              const uint32_t* __restrict__ lens, uint32_t fixed_len,
+                                                              uint32_t* __restrict__ out, uint32_t* __restrict__ out_rc,
+                                                              uint64_t m, unsigned long long* __restrict__ work,
+                                                              unsigned long long* __restrict__ ctr,
+                                                              const uint2* __restrict__ seeds, uint32_t refill_min) {
+  if (BW == 1) x2_masks_init();
+  fm_preload_super<SMS>(F);
+  const uint64_t ntask = m * STRANDS;
+  const uint4 C4 = __ldg(reinterpret_cast<const uint4*>(F.Ct));
+  const uint32_t lane = threadIdx.x & 31u;
+  uint64_t ti = 0;
+  uint32_t lo = 0, hi = 0, len = 0, rc = 0, pend = 0;
+  int64_t k = -1;
+  bool has = false;
+  PatWindow P;
+  P.reset(pat);
+  uint64_t n_steps = 0, n_lines = 0;
+  uint64_t cb = 0, ce = 0;                               // the warp's chunk [cb, ce) (warp-uniform)
+  bool exhausted = false;
+  while (true) {
+    const uint32_t needm = __ballot_sync(0xffffffffu, !has);
+    const uint32_t cnt = __popc(needm);
+    if (cnt && !exhausted && (cnt >= refill_min || cnt == 32u)) {
+      const uint32_t r = __popc(needm & ((1u << lane) - 1u));
+      const uint64_t avail = ce - cb;
+      uint64_t nb = 0, ne = 0;
+      if (cnt > avail) {                                 // top up from a fresh chunk
+        if (lane == 0) nb = atomicAdd(ctr, (unsigned long long)FM_CHUNK);
+        nb = __shfl_sync(0xffffffffu, nb, 0);
+        ne = nb + FM_CHUNK < ntask ? nb + FM_CHUNK : ntask;
+        if (nb >= ntask) { exhausted = true; nb = ne = ntask; }
+      }
+      if (!has) {
+        const uint64_t t = r < avail ? cb + r : nb + (r - avail);
+        if (r < avail || t < ne) {
+          ti = t;
+          const uint64_t pi = STRANDS == 2 ? ti >> 1 : ti;
+          rc = STRANDS == 2 ? (uint32_t)(ti & 1) : 0u;
+          len = FIXED ? fixed_len : lens[pi];
+          P.reset(pat + (FIXED ? pi * (uint64_t)fixed_len : offs[pi]));
+          const uint2 iv = __ldg(seeds + ti);
+          lo = iv.x;
+          hi = iv.y;
+          k = (int64_t)len - 1 - ((F.K && len >= (uint32_t)F.K) ? F.K : 0);
+          pend = 0;
+          has = true;
+        }
+      }
+      if (cnt > avail) {
+        const uint64_t take = cnt - avail;
+        cb = nb + take < ne ? nb + take : ne;
+        ce = ne;
+      } else {
+        cb += cnt;
+      }
+    }
+    if (exhausted && __ballot_sync(0xffffffffu, has) == 0) break;
+    // one line of one backward step, in every lane (results kept only where act)
+    const bool act = has && (pend || (k >= 0 && lo < hi));
+    const int64_t idx = rc ? (int64_t)len - 1 - k : k;
+    const uint32_t c = P.at_if(act, idx) ^ (rc ? 3u : 0u);
+    uint32_t nlo = lo, nhi = hi, npend = pend, nl;
+    const bool done = BW == 1 ? fm_step_pend_x2<SMS>(F, C4, c, nlo, nhi, npend, nl)
+                              : fm_step_pend<SMS>(F, C4, c, nlo, nhi, npend, nl);
+    if (WORK && act) { n_steps += pend ? 0u : 1u; n_lines += nl; }
+    lo = act ? nlo : lo;
+    hi = act ? nhi : hi;
+    pend = act ? npend : pend;
+    k -= (act && done) ? 1 : 0;
+    if (has && !pend && (k < 0 || lo >= hi)) {           // finished: write the count
+      const uint32_t res = lo < hi ? hi - lo : 0u;
+      if (STRANDS == 2 && rc) out_rc[ti >> 1] = res;
+      else out[STRANDS == 2 ? ti >> 1 : ti] = res;
+      has = false;
     }
   }
   if (WORK && n_steps) {
@@ -1081,6 +1293,7 @@ static FmParams params_of(const qr_fm* fm) {
 
 extern int g_fm_blocks_per_sm;
 extern int g_fm_lean;
+extern int g_fm_refill;
 
 int l2_bytes(int device);
 
@@ -1091,10 +1304,13 @@ int l2_bytes(int device);
 static bool bwt_l2_resident(const qr_fm* fm) {
   return fm->bwt->n_lines * 64 <= (uint64_t)l2_bytes(fm->bwt->device) / 2;
 }
-static bool use_lean(const qr_fm* fm) {
-  if (g_fm_lean == 1) return false;
-  if (g_fm_lean == 2) return true;
-  return bwt_l2_resident(fm);
+// 1: de-duplicating step, 2: lean step, 3: one line per iteration (fm_step_pend; with the dynamic
+// order and seeds: k_fm_count_l2).  Auto: 3 on L2-resident BWTs (configs[3]: 7.07 -> 8.68 G
+// patterns/s over QuadRank16, 8.45 -> 9.12 over QuadRank16x2), 1 on HBM-resident ones (request-
+// bound there: configs[4] 0.97 vs 0.86 with 3; profiles/r02_fm_step_probe.jsonl).
+static int fm_step_of(const qr_fm* fm) {
+  if (g_fm_lean >= 1 && g_fm_lean <= 3) return g_fm_lean;
+  return bwt_l2_resident(fm) ? 3 : 1;
 }
 
 extern int g_fm_smem;
@@ -1117,17 +1333,37 @@ static int fm_smem_mode(const qr_fm* fm, size_t* bytes) {
   return 0;
 }
 
-template <bool FIXED, bool WORK, int STRANDS, bool LEAN, int SMS>
+static int cur_device() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return d;
+}
+
+template <bool FIXED, bool WORK, int STRANDS, int STEP, int SMS>
 static void launch_fm1(unsigned g, size_t smem, cudaStream_t st, const FmParams& F, const uint8_t* pat,
                        const uint64_t* offs, const uint32_t* lens, uint32_t fixed_len, uint32_t* out, uint32_t* out_rc,
                        uint64_t m, unsigned long long* w, unsigned long long* ctr, int sms, uint2* seeds) {
-  if (ctr) {
-    // QuadRank16x2 BWT: one step flavour (the sector-shared step), LEAN ignored
-    auto kern = F.bw ? k_fm_count<FIXED, WORK, STRANDS, false, SMS, true, 1> : k_fm_count<FIXED, WORK, STRANDS, LEAN, SMS, true, 0>;
+  if (ctr && seeds && STEP == 3) {
+    auto kern = F.bw ? k_fm_count_l2<FIXED, WORK, STRANDS, SMS, 1> : k_fm_count_l2<FIXED, WORK, STRANDS, SMS, 0>;
+    k_fm_seed<FIXED, STRANDS><<<grid_stride_blocks(m * STRANDS, 256, sms, 16), 256, 0, st>>>(F, pat, offs, lens,
+                                                                                           fixed_len, m, seeds);
+    smem_limit_raise((const void*)kern, smem, cur_device());
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem) != cudaSuccess || per_sm <= 0) {
+      cudaGetLastError();
+      per_sm = 1;
+    }
+    const uint64_t need = (m * STRANDS + 255) / 256;
+    unsigned gp = (unsigned)((uint64_t)per_sm * sms < need ? (uint64_t)per_sm * sms : (need ? need : 1));
+    kern<<<gp, 256, smem, st>>>(F, pat, offs, lens, fixed_len, out, out_rc, m, w, ctr, seeds, (uint32_t)g_fm_refill);
+  } else if (ctr) {
+    // QuadRank16x2 BWT: the sector-shared step, or the one-sector-per-iteration step (STEP 3)
+    auto kern = F.bw ? k_fm_count<FIXED, WORK, STRANDS, STEP == 3 ? 3 : 0, SMS, true, 1>
+                     : k_fm_count<FIXED, WORK, STRANDS, STEP, SMS, true, 0>;
     if (seeds)
       k_fm_seed<FIXED, STRANDS><<<grid_stride_blocks(m * STRANDS, 256, sms, 16), 256, 0, st>>>(F, pat, offs, lens,
                                                                                              fixed_len, m, seeds);
-    if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    smem_limit_raise((const void*)kern, smem, cur_device());
     int per_sm = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem) != cudaSuccess || per_sm <= 0) {
       cudaGetLastError();
@@ -1137,19 +1373,20 @@ static void launch_fm1(unsigned g, size_t smem, cudaStream_t st, const FmParams&
     unsigned gp = (unsigned)((uint64_t)per_sm * sms < need ? (uint64_t)per_sm * sms : (need ? need : 1));
     kern<<<gp, 256, smem, st>>>(F, pat, offs, lens, fixed_len, out, out_rc, m, w, ctr, seeds);
   } else {
-    auto kern = F.bw ? k_fm_count<FIXED, WORK, STRANDS, false, SMS, false, 1> : k_fm_count<FIXED, WORK, STRANDS, LEAN, SMS, false, 0>;
-    if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    auto kern = F.bw ? k_fm_count<FIXED, WORK, STRANDS, STEP == 3 ? 3 : 0, SMS, false, 1>
+                     : k_fm_count<FIXED, WORK, STRANDS, STEP, SMS, false, 0>;
+    smem_limit_raise((const void*)kern, smem, cur_device());
     kern<<<g, 256, smem, st>>>(F, pat, offs, lens, fixed_len, out, out_rc, m, w, nullptr, nullptr);
   }
 }
 
-template <bool FIXED, bool WORK, int STRANDS, bool LEAN>
+template <bool FIXED, bool WORK, int STRANDS, int STEP>
 static void launch_fm2(int sms_mode, unsigned g, size_t smem, cudaStream_t st, const FmParams& F, const uint8_t* pat,
                        const uint64_t* offs, const uint32_t* lens, uint32_t fixed_len, uint32_t* out, uint32_t* out_rc,
                        uint64_t m, unsigned long long* w, unsigned long long* ctr, int sms, uint2* seeds) {
-  if (sms_mode == 1)      launch_fm1<FIXED, WORK, STRANDS, LEAN, 1>(g, smem, st, F, pat, offs, lens, fixed_len, out, out_rc, m, w, ctr, sms, seeds);
-  else if (sms_mode == 2) launch_fm1<FIXED, WORK, STRANDS, LEAN, 2>(g, smem, st, F, pat, offs, lens, fixed_len, out, out_rc, m, w, ctr, sms, seeds);
-  else                    launch_fm1<FIXED, WORK, STRANDS, LEAN, 0>(g, 0, st, F, pat, offs, lens, fixed_len, out, out_rc, m, w, ctr, sms, seeds);
+  if (sms_mode == 1)      launch_fm1<FIXED, WORK, STRANDS, STEP, 1>(g, smem, st, F, pat, offs, lens, fixed_len, out, out_rc, m, w, ctr, sms, seeds);
+  else if (sms_mode == 2) launch_fm1<FIXED, WORK, STRANDS, STEP, 2>(g, smem, st, F, pat, offs, lens, fixed_len, out, out_rc, m, w, ctr, sms, seeds);
+  else                    launch_fm1<FIXED, WORK, STRANDS, STEP, 0>(g, 0, st, F, pat, offs, lens, fixed_len, out, out_rc, m, w, ctr, sms, seeds);
 }
 
 extern int g_fm_dyn;
@@ -1178,7 +1415,7 @@ static void keep_pool_memory(int device, cudaStream_t st) {
 }
 
 template <bool FIXED, bool WORK>
-static cudaError_t launch_fm(const qr_fm* fm, bool lean, unsigned g, cudaStream_t st, const FmParams& F,
+static cudaError_t launch_fm(const qr_fm* fm, int step, unsigned g, cudaStream_t st, const FmParams& F,
                              const uint8_t* pat, const uint64_t* offs, const uint32_t* lens, uint32_t fixed_len,
                              uint32_t* out, uint32_t* out_rc, uint64_t m, unsigned long long* w) {
   size_t smem = 0;
@@ -1198,13 +1435,15 @@ static cudaError_t launch_fm(const qr_fm* fm, bool lean, unsigned g, cudaStream_
     if ((e = lease.acquire(fm->bwt->device, st, &ctr))) { if (seeds) cudaFreeAsync(seeds, st); return e; }
   }
   const int sms = fm->bwt->sm_count;
-  if (lean) {
-    if (out_rc) launch_fm2<FIXED, WORK, 2, true>(sm, g, smem, st, F, pat, offs, lens, fixed_len, out, out_rc, m, w, ctr, sms, seeds);
-    else        launch_fm2<FIXED, WORK, 1, true>(sm, g, smem, st, F, pat, offs, lens, fixed_len, out, out_rc, m, w, ctr, sms, seeds);
-  } else {
-    if (out_rc) launch_fm2<FIXED, WORK, 2, false>(sm, g, smem, st, F, pat, offs, lens, fixed_len, out, out_rc, m, w, ctr, sms, seeds);
-    else        launch_fm2<FIXED, WORK, 1, false>(sm, g, smem, st, F, pat, offs, lens, fixed_len, out, out_rc, m, w, ctr, sms, seeds);
-  }
+#define QR_FM_GO(S)                                                                                              \
+  do {                                                                                                           \
+    if (out_rc) launch_fm2<FIXED, WORK, 2, S>(sm, g, smem, st, F, pat, offs, lens, fixed_len, out, out_rc, m, w, ctr, sms, seeds); \
+    else        launch_fm2<FIXED, WORK, 1, S>(sm, g, smem, st, F, pat, offs, lens, fixed_len, out, out_rc, m, w, ctr, sms, seeds); \
+  } while (0)
+  if (step == 3) QR_FM_GO(3);
+  else if (step == 2) QR_FM_GO(2);
+  else QR_FM_GO(1);
+#undef QR_FM_GO
   e = cudaGetLastError();
   if (ctr) {
     cudaError_t e2 = lease.release(st);
@@ -1260,8 +1499,8 @@ qr_status fm_count_device(const qr_fm* fm, const uint8_t* pat, const uint32_t* l
   cudaError_t e;
   if (!lengths) {
     if (approx) e = launch_approx<true>(fm, g, st, F, pat, nullptr, nullptr, fixed_len, out, out_rc, m, approx);
-    else if (work) e = launch_fm<true, true>(fm, use_lean(fm), g, st, F, pat, nullptr, nullptr, fixed_len, out, out_rc, m, w);
-    else      e = launch_fm<true, false>(fm, use_lean(fm), g, st, F, pat, nullptr, nullptr, fixed_len, out, out_rc, m, w);
+    else if (work) e = launch_fm<true, true>(fm, fm_step_of(fm), g, st, F, pat, nullptr, nullptr, fixed_len, out, out_rc, m, w);
+    else      e = launch_fm<true, false>(fm, fm_step_of(fm), g, st, F, pat, nullptr, nullptr, fixed_len, out, out_rc, m, w);
     if (e) return cuda_fail(e, "k_fm_count");
     return QR_OK;
   }
@@ -1276,8 +1515,8 @@ qr_status fm_count_device(const qr_fm* fm, const uint8_t* pat, const uint32_t* l
     cudaFreeAsync(offs, st); cudaFreeAsync(tmp, st); return cuda_fail(e, "scan");
   }
   if (approx) e = launch_approx<false>(fm, g, st, F, pat, offs, lengths, 0, out, out_rc, m, approx);
-  else if (work) e = launch_fm<false, true>(fm, use_lean(fm), g, st, F, pat, offs, lengths, 0, out, out_rc, m, w);
-  else      e = launch_fm<false, false>(fm, use_lean(fm), g, st, F, pat, offs, lengths, 0, out, out_rc, m, w);
+  else if (work) e = launch_fm<false, true>(fm, fm_step_of(fm), g, st, F, pat, offs, lengths, 0, out, out_rc, m, w);
+  else      e = launch_fm<false, false>(fm, fm_step_of(fm), g, st, F, pat, offs, lengths, 0, out, out_rc, m, w);
   cudaFreeAsync(offs, st);
   cudaFreeAsync(tmp, st);
   if (e) return cuda_fail(e, "k_fm_count");

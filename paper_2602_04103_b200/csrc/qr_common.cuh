@@ -70,6 +70,10 @@ int pointer_space(const void* p, int device);
 
 // SM count of a device (cached)
 int sm_count(int device);
+// Raise a kernel's dynamic shared-memory limit on `device` to at least `bytes` (process-wide,
+// mutex-guarded, never lowers it: a later launch with a smaller size must not undercut a
+// concurrent or cached launch that needs more).  Returns the attribute call's error, if any.
+cudaError_t smem_limit_raise(const void* kern, size_t bytes, int device);
 
 // internal builders used by fm.cu
 qr_status quadrank_build_device(const uint64_t* d_text2b, uint64_t n, int device, cudaStream_t st, qr_index** out);
@@ -153,6 +157,27 @@ __device__ __forceinline__ void ld_sector_na(const void* p, uint64_t& w0, uint64
 // Same, allocating in L1 (FM: lo and hi of a step, and consecutive steps, often share a line).
 __device__ __forceinline__ void ld_sector(const void* p, uint64_t& w0, uint64_t& w1, uint64_t& w2, uint64_t& w3) {
   asm volatile("ld.global.L2::64B.v4.u64 {%0,%1,%2,%3}, [%4];" : "=l"(w0), "=l"(w1), "=l"(w2), "=l"(w3) : "l"(p));
+}
+// Predicated 8-byte read-only load (no branch: lanes with pred == 0 issue nothing and get 0).
+__device__ __forceinline__ uint64_t ldg_u64_if(bool pred, const void* p) {
+  uint64_t v;
+  asm volatile(
+      "{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\tmov.u64 %0, 0;\n\t@q ld.global.nc.u64 %0, [%1];\n\t}"
+      : "=l"(v)
+      : "l"(p), "r"((uint32_t)pred));
+  return v;
+}
+// Predicated 8-byte read-only load into v (v keeps its value where pred == 0; no branch).
+__device__ __forceinline__ void ldg_u64_keep(bool pred, const void* p, uint64_t& v) {
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q ld.global.nc.u64 %0, [%1];\n\t}"
+               : "+l"(v)
+               : "l"(p), "r"((uint32_t)pred));
+}
+// ~0 << d with the PTX clamp (d = 64 gives 0; C's shift would be undefined there)
+__device__ __forceinline__ uint64_t ones_shl(uint32_t d) {
+  uint64_t v;
+  asm("shl.b64 %0, %1, %2;" : "=l"(v) : "l"(~0ull), "r"(d));
+  return v;
 }
 // Query-stream loads (coalesced, read once).  Coherent + volatile so that the software
 // prefetch of the next group's queries stays where it is written (issued while the current

@@ -1180,13 +1180,8 @@ template <typename Kern>
 static unsigned sc_grid(Kern kern, int threads, size_t smem, int device, int sms) {
   static std::mutex mu;
   static std::map<std::tuple<const void*, size_t, int>, unsigned> cache;
-  static std::map<std::pair<const void*, int>, size_t> limit;
+  smem_limit_raise((const void*)kern, smem, device);
   std::lock_guard<std::mutex> g(mu);
-  size_t& lim = limit[std::make_pair((const void*)kern, device)];
-  if (smem > lim) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    lim = smem;
-  }
   const auto key = std::make_tuple((const void*)kern, smem, device);
   auto it = cache.find(key);
   if (it != cache.end()) return it->second;
@@ -1300,17 +1295,6 @@ static uint64_t res_max_bytes(int device) {
   return cache[device] = r;
 }
 
-// raise a kernel's dynamic shared-memory limit to `bytes` (never lowers it; per kernel and device)
-static void res_smem_limit(const void* kern, size_t bytes, int device) {
-  static std::mutex mu;
-  static std::map<std::pair<const void*, int>, size_t> limit;
-  std::lock_guard<std::mutex> g(mu);
-  size_t& lim = limit[std::make_pair(kern, device)];
-  if (bytes > lim) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-    lim = bytes;
-  }
-}
 
 cudaError_t launch_lane_table_rank(const qr_index* h, const uint64_t* q, const uint8_t* c, uint64_t* out, uint64_t m,
                                    int what, cudaStream_t st) {
@@ -1331,7 +1315,7 @@ cudaError_t launch_lane_table_rank(const qr_index* h, const uint64_t* q, const u
       m * 16 >= 2 * res_bytes * (uint64_t)h->sm_count) {
     const unsigned grid = (unsigned)h->sm_count;                 // one 1024-thread CTA per SM
     auto go_res = [&](auto kern, const uint8_t* cc) -> cudaError_t {
-      res_smem_limit((const void*)kern, (size_t)res_bytes, h->device);
+      smem_limit_raise((const void*)kern, (size_t)res_bytes, h->device);
       kern<<<grid, 1024, (size_t)res_bytes, st>>>(h->lines, h->spack, words, half, q, cc, out, m, last, nullptr);
       return cudaGetLastError();
     };
@@ -1371,6 +1355,9 @@ static cudaError_t launch_cs_clusters(void (*kern)(KArgs...), uint32_t cs, size_
   cfg.attrs = &attr;
   cfg.numAttrs = 1;
   unsigned grid = 0;
+  // the limit is raised before EVERY launch (a smaller table of another handle may have been
+  // launched since this key was cached); it only ever grows, so concurrent launches stay valid
+  smem_limit_raise((const void*)kern, smem, h->device);
   {
     std::lock_guard<std::mutex> g(mu);
     const auto key = std::make_tuple((const void*)kern, h->device, cs, smem);
@@ -1378,7 +1365,6 @@ static cudaError_t launch_cs_clusters(void (*kern)(KArgs...), uint32_t cs, size_
     if (it != grids.end()) {
       grid = it->second;
     } else {
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       if (cs > 8) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
       cfg.gridDim = dim3((unsigned)h->sm_count / cs * cs);
       int clusters = 0;

@@ -65,6 +65,7 @@ def broadcast_index(h, n: int, layout: int, dist, device, src: int = 0):
     from . import _check, _ptr, lib, qr_import_layout
 
     rank = dist.get_rank()
+    device = torch.device("cuda", device_index(device))
     if rank == src:
         sizes = torch.tensor([h.line_bytes, h.super_bytes], dtype=torch.int64, device=device)
     else:
@@ -81,7 +82,20 @@ def broadcast_index(h, n: int, layout: int, dist, device, src: int = 0):
     torch.cuda.synchronize(device)
     if rank == src:
         return h
-    return qr_import_layout(lines, sup if sb else None, n, layout, device=device.index if hasattr(device, "index") else 0)
+    return qr_import_layout(lines, sup[:sb] if sb else None, n, layout, device=device_index(device))
+
+
+def device_index(device) -> int:
+    """CUDA ordinal of an int, a "cuda:k" string or a torch.device; "cuda" without an index is the
+    current device."""
+    import torch
+
+    if isinstance(device, int):
+        return device
+    d = torch.device(device)
+    if d.type != "cuda":
+        raise ValueError(f"not a CUDA device: {device}")
+    return d.index if d.index is not None else torch.cuda.current_device()
 
 
 def parse_cpulist(text: str) -> set:

@@ -25,6 +25,7 @@ def _torch():
 def fm_dyn_reset():
     yield
     qr.qr_set_tuning("fm_dyn", 1)
+    qr.qr_set_tuning("fm_step", DEFAULT_FM_STEP)
 
 
 def pack2(sym: np.ndarray) -> np.ndarray:
@@ -231,7 +232,7 @@ def test_fm_all_kmers_partition(cuda):
             assert int(to_host(d).astype(np.int64).sum()) == n - k + 1
 
 
-@pytest.mark.parametrize("step", [1, 2])
+@pytest.mark.parametrize("step", [1, 2, 3])
 @pytest.mark.parametrize("bps", [2, 16, 64])
 def test_fm_tuning_does_not_change_results(cuda, bps, step):
     torch = _torch()
@@ -416,7 +417,7 @@ def test_fm_kmer_width_does_not_change_counts(cuda, k):
         assert int((t[:, 1].astype(np.int64) - t[:, 0]).sum()) == n - k + 1
 
 
-@pytest.mark.parametrize("step", [1, 2])
+@pytest.mark.parametrize("step", [1, 2, 3])
 @pytest.mark.parametrize("fm_smem", [0, 1, 2])
 def test_fm_superblock_source_does_not_change_results(cuda, fm_smem, step):
     """The count kernel's superblock words from global memory (0), from the raw array copied to
@@ -503,9 +504,10 @@ def test_fm_default_kmer_width(cuda):
         fm.free()
 
 
+@pytest.mark.parametrize("step", [0, 3])
 @pytest.mark.parametrize("n,kind", [(1, 0), (7, 0), (100, 0), (1000, 0), (50000, 0), (25000, 1), (3_000_000, 0)])
 @pytest.mark.parametrize("dyn", [0, 1])
-def test_fm_over_quadrank16x2(cuda, n, kind, dyn, fm_dyn_reset):
+def test_fm_over_quadrank16x2(cuda, n, kind, dyn, step, fm_dyn_reset):
     """QuadFm over the sector-local QuadRank16x2 BWT (qr_fm_build_opts): the k-mer table, exact
     counts (variable lengths, one and both strands), <= 1-substitution counts and the work
     instrumentation must equal the oracle / the QuadRank16-backed index, static and dynamic order."""
@@ -518,6 +520,7 @@ def test_fm_over_quadrank16x2(cuda, n, kind, dyn, fm_dyn_reset):
     assert fm.kmer_k == fm16.kmer_k and fm.spos == ora.spos
     assert np.array_equal(qr.qr_fm_export_kmer(fm), qr.qr_fm_export_kmer(fm16))
     qr.qr_set_tuning("fm_dyn", dyn)
+    qr.qr_set_tuning("fm_step", step)
     pats = mixed_patterns(np.random.default_rng(n), sym, 1500)
     cat, off, lens = oracle.pack_patterns(pats)
     ref = ora.count(cat, off, lens)
@@ -548,8 +551,10 @@ def test_fm_over_quadrank16x2(cuda, n, kind, dyn, fm_dyn_reset):
         work = torch.zeros(2, dtype=torch.uint64, device=cuda)
         qr.qr_fm_count_work(fm, to_dev(fx, cuda), None, L, dw, m, work)
         torch.cuda.synchronize()
-        assert np.array_equal(to_host(dw).view(np.uint32),
-                              ora.count(fx, np.arange(m, dtype=np.uint64) * L, np.full(m, L, np.uint32)))
+        offs, lens_ = np.arange(m, dtype=np.uint64) * L, np.full(m, L, np.uint32)
+        assert np.array_equal(to_host(dw).view(np.uint32), ora.count(fx, offs, lens_))
+        # distinct 192-row lines (QuadRank16x2) per post-seed step, as the oracle counts them
+        assert [int(x) for x in to_host(work)] == list(ora.work(fx, offs, lens_, skip=fm.kmer_k, block=192))
 
 
 @pytest.mark.parametrize("kmax", [2, 3])

@@ -82,7 +82,7 @@ def test_random_fm(cuda, trial):
         pats.append(p)
     cat, off, lens = oracle.pack_patterns(pats)
     ref = oracle.scan_count(sym, cat, off, lens)
-    qr.qr_set_tuning("fm_step", int(rng.integers(0, 3)))
+    qr.qr_set_tuning("fm_step", int(rng.integers(0, 4)))
     qr.qr_set_tuning("fm_blocks_per_sm", int(rng.choice([1, 4, 64])))
     try:
         d = torch.empty(lens.size, dtype=torch.int32, device=cuda)

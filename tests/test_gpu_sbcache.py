@@ -479,6 +479,56 @@ def test_resident_structure_parity(cuda, smem_mode, resident, nb, n4):
         qr.qr_set_tuning("rank_resident", 1)
 
 
+def test_large_table_limit_large_small_large(cuda, smem_mode):
+    """Regression: the CS-CTA cluster launcher cached its grid per (kernel, table size)
+    and set the shared-memory limit only on a cache miss, so large -> small -> large handle order
+    launched the large table above a lowered limit (QR_ECUDA).  Tables of ~180 KB (2^35 bits) and
+    ~111 KB (1.23 x 2^34 bits, forced onto the large-n table) per CTA, queried in that order; every
+    result equals the global-memory kernel's."""
+    torch = _torch()
+    qr.qr_set_tuning("rank_big_pack", 1)
+    hs = {}
+    try:
+        for key, n in (("A", 1 << 35), ("B", int(1.23 * (1 << 34)))):
+            bits = torch.empty((n + 63) // 64, dtype=torch.uint64, device=cuda)
+            gen.bits_dev(72, n, 0.5, bits)
+            hs[key] = (qr.qr_birank_build(bits, n), n)
+            del bits
+    finally:
+        qr.qr_set_tuning("rank_big_pack", 0)
+    m = (1 << 22) + 5
+    for key in ("A", "B", "A"):
+        h, n = hs[key]
+        q = torch.empty(m, dtype=torch.uint64, device=cuda)
+        gen.queries_dev(73, n, m, q)
+        out = torch.empty_like(q)
+        qr.qr_set_tuning("rank_smem", 1)
+        qr.qr_rank(h, q, None, out)
+        qr.qr_set_tuning("rank_smem", 0)
+        ref = torch.empty_like(q)
+        qr.qr_rank(h, q, None, ref)
+        qr.qr_set_tuning("rank_smem", 1)
+        torch.cuda.synchronize()
+        assert torch.equal(out, ref), key
+
+
+def test_import_layout_rejects_wrong_sizes(cuda, smem_mode):
+    """qr_import_layout checks the buffers' byte counts against (n, layout) before copying."""
+    n = 5 * S + 3
+    w = gen.bits(94, n)
+    h = qr.qr_birank_build(w, n)
+    lines, sup = qr.qr_export_layout(h)
+    with pytest.raises(qr.QrError, match="differ"):
+        qr.qr_import_layout(lines[:-64], sup, n, qr.QR_LAYOUT_BIRANK16)
+    with pytest.raises(qr.QrError, match="differ"):
+        qr.qr_import_layout(lines, sup, n + S, qr.QR_LAYOUT_BIRANK16)
+    with pytest.raises(qr.QrError):
+        qr.qr_import_layout(lines, None, n, qr.QR_LAYOUT_BIRANK16)
+    h2 = qr.qr_import_layout(lines, sup, n, qr.QR_LAYOUT_BIRANK16)
+    q = gen.queries(95, n, 5000)
+    assert np.array_equal(_rank(h2, q, None, cuda, 0), oracle.BitsOracle(w, n).rank(q))
+
+
 @pytest.mark.parametrize("cs", [4, 8, 16])
 @pytest.mark.parametrize("n_sb,extra", [(1, 5), (37, 1234), (401, 77)])
 def test_large_table_cluster_kernel_parity(cuda, smem_mode, cs, n_sb, extra):

@@ -104,6 +104,49 @@ def test_binding_rejects_wrong_dtypes():
                             np.zeros(2, np.uint64))
 
 
+def test_binding_rejects_strided_and_short_buffers():
+    """Strided views (numpy slices, negative strides, torch transposes and stride-0 expansions) and
+    build inputs shorter than n symbols are refused before any pointer reaches the library."""
+    import numpy as np
+    import torch
+
+    h = object.__new__(qr.Index)
+    q = np.zeros(20, np.uint64)
+    with pytest.raises(qr.QrError, match="contiguous"):
+        qr.qr_rank(h, q[::2], None, np.zeros(10, np.uint64))
+    with pytest.raises(qr.QrError, match="contiguous"):
+        qr.qr_rank(h, q[:10], None, np.zeros(20, np.uint64)[::-2])
+    with pytest.raises(qr.QrError, match="contiguous"):
+        qr.qr_rank_all4(h, torch.zeros(10, dtype=torch.uint64), torch.zeros(4, 10, dtype=torch.uint64).t())
+    with pytest.raises(qr.QrError, match="zero stride|contiguous"):
+        qr.qr_rank(h, torch.zeros(1, dtype=torch.uint64).expand(10), None, torch.zeros(10, dtype=torch.uint64))
+    fm = object.__new__(qr.Fm)
+    with pytest.raises(qr.QrError, match="contiguous"):   # variable-length patterns, strided
+        qr.qr_fm_count(fm, np.zeros(64, np.uint8)[::2], np.full(2, 16, np.uint32), 0, np.zeros(2, np.uint32), 2)
+    with pytest.raises(qr.QrError):                        # 2^12 bits need 64 words
+        qr.qr_birank_build(np.zeros(63, np.uint64), 1 << 12)
+    with pytest.raises(qr.QrError):                        # 1000 chars need 32 words
+        qr.qr_quadrank_build(np.zeros(31, np.uint64), 1000)
+    with pytest.raises(qr.QrError):
+        qr.qr_build(np.zeros(31, np.uint64), 1000, qr.QR_LAYOUT_QUADRANK64)
+    with pytest.raises(qr.QrError):                        # SA of n + 1 rows
+        qr.qr_fm_build(np.zeros(32, np.uint64), 1000, sa=np.zeros(1000, np.uint32))
+    with pytest.raises(qr.QrError, match="contiguous"):
+        qr.qr_import_layout(np.zeros(256, np.uint8)[::2], None, 10, qr.QR_LAYOUT_BIRANK64X2)
+
+
+def test_device_index_normalisation():
+    import torch
+
+    from paper_2602_04103_b200.multigpu import device_index
+
+    assert device_index(3) == 3
+    assert device_index("cuda:2") == 2
+    assert device_index(torch.device("cuda", 5)) == 5
+    with pytest.raises(ValueError):
+        device_index("cpu")
+
+
 def test_tuning_knob_validation():
     """Every launch knob accepts its documented values and rejects the rest (QR_EINVAL, message
     set); the (K, CTA threads) pairs of the cluster kernels are checked against the instantiated
@@ -112,14 +155,14 @@ def test_tuning_knob_validation():
     ok = {
         "rank_smem": [0, 1, 2], "rank_dyn": [0, 1], "rank_smem_k": [0, 1, 2, 3, 4, 6, 8],
         "rank_smem_clusters": [0, 1, 74, 4096], "fm_dyn": [0, 1], "fm_seed": [0, 1, 2], "fm_smem": [0, 1, 2],
-        "fm_step": [0, 1, 2], "rank_pair": [0, 1, 2], "rank_s_lane": [0, 1], "index64": [0, 1],
+        "fm_step": [0, 1, 2, 3], "rank_pair": [0, 1, 2], "rank_s_lane": [0, 1], "index64": [0, 1],
         "rank_k": [1, 2, 4, 8], "rank_blocks_per_sm": [1, 64], "fm_blocks_per_sm": [1, 64],
         "stage_slots": [2, 4], "stage_chunk": [1024, 1 << 23], "rank_resident": [0, 1], "rank_big_pack": [0, 1],
         "rank_big_cs": [0, 4, 8, 16],
     }
     bad = {
         "rank_smem": [-1, 3], "rank_dyn": [2], "rank_smem_k": [5, 7, 16], "rank_smem_clusters": [-1, 4097],
-        "fm_dyn": [2], "fm_seed": [3], "fm_smem": [3], "fm_step": [3], "rank_pair": [3, -1], "rank_s_lane": [2],
+        "fm_dyn": [2], "fm_seed": [3], "fm_smem": [3], "fm_step": [4, -1], "rank_pair": [3, -1], "rank_s_lane": [2],
         "index64": [2], "rank_k": [0, 3], "rank_blocks_per_sm": [0, 65], "fm_blocks_per_sm": [0, 65],
         "stage_slots": [1, 5], "stage_chunk": [1023], "rank_resident": [2, -1], "rank_big_pack": [2],
         "rank_big_cs": [2, 32],
