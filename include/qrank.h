@@ -132,8 +132,9 @@ qr_status qr_fm_build(const uint64_t* text2b, uint64_t n, const uint32_t* sa_or_
 
 /* As qr_fm_build with a k-mer seed table of width kmer_k (0..14; 0 = no table, every search
  * starts from [0, n+1)).  qr_fm_build picks the paper's 8 for n < 2^20, 10 for
- * n < 2^24 and 12 above (on B200 the wider table replaces more backward steps
- * by one lookup).  The table holds 4^kmer_k intervals (8 B each: 512 KiB at 8, 8 MiB at 10,
+ * n < 2^24 and, above, 11 when the BWT's rank layout plus the 32 MiB 11-mer table fit in 60% of
+ * the device's L2 (seeds then come from L2), else 12 (on B200 the wider table
+ * replaces more backward steps by one lookup).  The table holds 4^kmer_k intervals (8 B each: 512 KiB at 8, 8 MiB at 10,
  * 128 MiB at 12, 2 GiB at 14).  Counts never depend on kmer_k.  QR_EINVAL outside 0..14. */
 qr_status qr_fm_build_ex(const uint64_t* text2b, uint64_t n, const uint32_t* sa_or_null, int kmer_k, int device,
                          void* stream, qr_fm** out);
@@ -195,6 +196,17 @@ qr_status qr_fm_count_approx_both(const qr_fm* fm, const uint8_t* patterns, cons
 qr_status qr_fm_count_work(const qr_fm* fm, const uint8_t* patterns, const uint32_t* lengths, uint32_t fixed_len,
                            uint32_t* out, uint64_t m, uint64_t* work, void* stream);
 
+/* Work accounting of every count flavour (device pointers only): the call qr_fm_count_approx
+ * (max_mismatches 0..3; 0 = exact) or, with out_rc non-NULL, qr_fm_count_approx_both makes,
+ * accumulating into work[0] the rank evaluations at an interval's two ends (exact backward
+ * steps after seeding, rank_4 pairs of the search tree) plus k-mer table
+ * lookups, and into work[1] the distinct 64-B lines (table entries) they gather — the
+ * denominator of the FM roofline fraction.  For max_mismatches = 0 and one
+ * strand this is qr_fm_count_work.  work: 2 u64 on the device, accumulated (not reset). */
+qr_status qr_fm_count_work_ex(const qr_fm* fm, const uint8_t* patterns, const uint32_t* lengths, uint32_t fixed_len,
+                              uint32_t max_mismatches, uint32_t* out_fwd, uint32_t* out_rc, uint64_t m,
+                              uint64_t* work, void* stream);
+
 /* ------------------------------------------------------------------ measurement */
 
 /* Gather ceiling ("null rank"): the same q stream, the same line-index
@@ -249,6 +261,15 @@ qr_status qr_fm_clone_to_device(const qr_fm* fm, int device, void* stream, qr_fm
 
 /* Synchronise `stream` and surface any asynchronous error. */
 qr_status qr_sync(void* stream);
+
+/* Output checksum for multi-GPU verification ("all_reduce of a u64 checksum"):
+ * *sum (one u64 on the device, accumulated, not reset) += sum over i < count of
+ * mix(index0 + i, word_i) mod 2^64, where word_i is element i of `data` (word_bytes 4 or 8) and
+ * mix a 64-bit hash of (global index, value).  The sum is additive over disjoint index ranges,
+ * so shards checksummed on different GPUs add up (one all_reduce) to the checksum of the whole
+ * batch on one GPU.  Not part of the method; measurement utility.  Device pointers only; QR_EINVAL
+ * for another word size. */
+qr_status qr_checksum(const void* data, uint64_t count, int word_bytes, uint64_t index0, uint64_t* sum, void* stream);
 
 void qr_free(qr_index* h);
 void qr_fm_free(qr_fm* fm);

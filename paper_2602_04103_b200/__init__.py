@@ -31,6 +31,7 @@ EXPORTS = (
     "qr_clone_to_device", "qr_fm_clone_to_device", "qr_sync", "qr_free", "qr_fm_free", "qr_last_error",
     "qr_version", "qr_set_tuning", "qr_build", "qr_layout", "qr_rank_chain", "qr_import_layout", "qr_fm_build_ex", "qr_fm_kmer_width",
     "qr_super_cache_bytes", "qr_super_cache_clusters", "qr_fm_build_opts", "qr_fm_count_approx_both",
+    "qr_fm_count_work_ex", "qr_checksum",
 )
 
 
@@ -61,6 +62,8 @@ def lib():
             "qr_fm_count": ([V, V, V, U32, V, U64, V], I32),
             "qr_fm_count_work": ([V, V, V, U32, V, U64, V, V], I32),
             "qr_fm_count_both": ([V, V, V, U32, V, V, U64, V], I32),
+            "qr_fm_count_work_ex": ([V, V, V, U32, U32, V, V, U64, V, V], I32),
+            "qr_checksum": ([V, U64, C.c_int, U64, V, V], I32),
             "qr_fm_count_approx": ([V, V, V, U32, U32, V, U64, V], I32),
             "qr_fm_count_approx_both": ([V, V, V, U32, U32, V, V, U64, V], I32),
             "qr_gather_ceiling": ([V, V, V, U64, I32, V], I32),
@@ -336,6 +339,20 @@ def qr_fm_count_work(fm: Fm, patterns, lengths, fixed_len: int, out, m: int, wor
     return out
 
 
+def qr_fm_count_work_ex(fm: Fm, patterns, lengths, fixed_len: int, max_mismatches: int, out, out_rc, m: int, work,
+                        stream=None):
+    """Work accounting of any count flavour (exact or <= 3 substitutions, one or both strands):
+    work[0] += rank evaluations at interval ends + table lookups, work[1] += lines gathered."""
+    if out_rc is None:
+        _need_fm("qr_fm_count_work_ex", patterns, lengths, fixed_len, m, out)
+    else:
+        _need_fm("qr_fm_count_work_ex", patterns, lengths, fixed_len, m, out, out_rc)
+    _need(work, 8, 2, "qr_fm_count_work_ex work")
+    _check(lib().qr_fm_count_work_ex(fm.ptr, _ptr(patterns), _ptr(lengths), fixed_len, max_mismatches, _ptr(out),
+                                     _ptr(out_rc), m, _ptr(work), _stream(stream)), "qr_fm_count_work_ex")
+    return out
+
+
 def qr_gather_ceiling(h: Index, q, out, mode: int = 0, m: int | None = None, stream=None):
     m = (q.numel() if hasattr(q, "numel") else q.size) if m is None else m
     _need(q, 8, m, "qr_gather_ceiling q")
@@ -422,6 +439,14 @@ def qr_super_cache_clusters(h: "Index") -> int:
     v = C.c_int(0)
     _check(lib().qr_super_cache_clusters(h.ptr, C.byref(v)), "qr_super_cache_clusters")
     return int(v.value)
+
+
+def qr_checksum(data, count: int, word_bytes: int, index0: int, acc, stream=None):
+    """acc (1 u64 on the device) += sum_i mix(index0 + i, data[i]) mod 2^64: additive over shards."""
+    _need(data, word_bytes, count, "qr_checksum data")
+    _need(acc, 8, 1, "qr_checksum acc")
+    _check(lib().qr_checksum(_ptr(data), count, word_bytes, index0, _ptr(acc), _stream(stream)), "qr_checksum")
+    return acc
 
 
 def qr_sync(stream=None):

@@ -27,6 +27,7 @@ int g_fm_dyn = 1;               // FM count: 1 = persistent grid + warp chunks f
 int g_fm_seed = 0;              // FM seed pre-pass (dynamic order only): 0 auto (L2-resident BWT), 1 never, 2 always
 int g_fm_smem = 1;              // FM superblock words from shared memory: 0 off, 1 auto, 2 packed table whenever it fits
 int g_fm_refill = 8;            // L2-resident count kernel: refill a warp's lanes once this many are idle
+int g_fm_packed = 1;            // L2-resident count kernel: packed post-seed symbols for short fixed-length batches
 int g_fm_lean = 0;              // FM step flavour: 0 auto (by L2 residency), 1 de-duplicating, 2 lean, 3 one line per iteration
 int g_index64 = 0;              // 1: force the 64-bit line-index path (tests the n >= 2^36/2^37 code on small n)
 int g_rank_smem = 1;            // superblock words from cluster shared memory: 0 never, 1 large batches, 2 always
@@ -152,7 +153,7 @@ uint64_t super_bytes_of(const qr_index* h) {
 }
 
 qr_status fm_build_device(const uint64_t* d_text, uint64_t n, const uint32_t* d_sa_given, int device, cudaStream_t st,
-                          qr_fm** out, int kmer_k, int bwt_layout);
+                          qr_fm** out, int kmer_k, int bwt_layout, int kmer_k_ax);
 __global__ void k_mask_tail_bits(uint64_t* words, uint64_t n);
 __global__ void k_mask_tail_chars(uint64_t* words, uint64_t n);
 cudaError_t launch_bi_gather(const qr_index* h, const uint64_t* q, uint64_t* out, uint64_t m, int mode, cudaStream_t st);
@@ -401,6 +402,9 @@ QR_EXPORT qr_status qr_set_tuning(const char* key, int64_t value) {
   } else if (!strcmp(key, "fm_refill")) {
     if (value < 1 || value > 32) return fail(QR_EINVAL, "fm_refill must be 1..32");
     g_fm_refill = (int)value;
+  } else if (!strcmp(key, "fm_packed")) {
+    if (value != 0 && value != 1) return fail(QR_EINVAL, "fm_packed must be 0 or 1");
+    g_fm_packed = (int)value;
   } else if (!strcmp(key, "fm_step")) {
     if (value < 0 || value > 3) return fail(QR_EINVAL, "fm_step must be 0 (auto), 1, 2 or 3");
     g_fm_lean = (int)value;
@@ -598,14 +602,23 @@ QR_EXPORT qr_status qr_gather_ceiling(const qr_index* h, const uint64_t* q, uint
 // more backward steps by one lookup and HBM holds them easily: 10 (8 MiB) from n = 2^20, 12
 // (128 MiB) from n = 2^24 — configs[3] 5.61 -> 6.57 G patterns/s, configs[4] 0.94 -> 0.99
 // (profiles/r01_fm_k_probe*.jsonl).  Counts never depend on it.
-int fm_default_kmer_k(uint64_t n) { return n < (1ull << 20) ? 8 : n < (1ull << 24) ? 10 : 12; }
+// From n = 2^24 the width is 11 when the BWT's rank layout and the 32 MiB 11-mer table fit in
+// 60% of the L2 together (the count kernel then seeds from L2, not HBM: configs[3] 9.14 -> 9.36
+// G patterns/s with packed seeds, profiles/r02_fm_step_probe.jsonl), else 12.
+int fm_default_kmer_k(uint64_t n, int layout, int device) {
+  if (n < (1ull << 20)) return 8;
+  if (n < (1ull << 24)) return 10;
+  const uint64_t line_chars = layout == QR_LAYOUT_QUADRANK16X2 ? 192 : 224;
+  const uint64_t bwt_bytes = ((n + 1) / line_chars + 1) * 64, t11 = (1ull << 22) * 8;
+  return bwt_bytes + t11 <= (uint64_t)l2_bytes(device) * 6 / 10 ? 11 : 12;
+}
 
 QR_EXPORT qr_status qr_fm_build_ex(const uint64_t* text2b, uint64_t n, const uint32_t* sa_or_null, int kmer_k,
                                    int device, void* stream, qr_fm** out);
 
 QR_EXPORT qr_status qr_fm_build(const uint64_t* text2b, uint64_t n, const uint32_t* sa_or_null, int device,
                                 void* stream, qr_fm** out) {
-  return qr_fm_build_ex(text2b, n, sa_or_null, fm_default_kmer_k(n), device, stream, out);
+  return qr_fm_build_opts(text2b, n, sa_or_null, -1, QR_LAYOUT_QUADRANK16, device, stream, out);
 }
 
 QR_EXPORT qr_status qr_fm_build_opts(const uint64_t* text2b, uint64_t n, const uint32_t* sa_or_null, int kmer_k,
@@ -618,7 +631,15 @@ QR_EXPORT qr_status qr_fm_build_ex(const uint64_t* text2b, uint64_t n, const uin
 
 QR_EXPORT qr_status qr_fm_build_opts(const uint64_t* text2b, uint64_t n, const uint32_t* sa_or_null, int kmer_k,
                                      int bwt_layout, int device, void* stream, qr_fm** out) {
-  if (kmer_k == -1) kmer_k = fm_default_kmer_k(n);
+  // The default width may pick 11 for the exact count (its table then sits in L2); the
+  // approximate-search kernels enumerate every K-mer within k substitutions of the seed, where a
+  // wider table saves more backtracking than HBM lookups cost: they get a 12-wide table of their
+  // own (configs[3] <= 1 substitution 0.50 -> 0.60 G patterns/s; profiles/r02_bench_full_*.jsonl).
+  int kmer_k_ax = kmer_k;
+  if (kmer_k == -1) {
+    kmer_k = fm_default_kmer_k(n, bwt_layout, device);
+    kmer_k_ax = kmer_k == 11 ? 12 : kmer_k;
+  }
   if (kmer_k < 0 || kmer_k > 14) return fail(QR_EINVAL, "qr_fm_build_ex: kmer_k must be 0..14");
   if (bwt_layout != QR_LAYOUT_QUADRANK16 && bwt_layout != QR_LAYOUT_QUADRANK16X2)
     return fail(QR_EINVAL, "qr_fm_build_opts: bwt_layout must be QR_LAYOUT_QUADRANK16 or QR_LAYOUT_QUADRANK16X2");
@@ -642,7 +663,7 @@ QR_EXPORT qr_status qr_fm_build_opts(const uint64_t* text2b, uint64_t n, const u
       free_staged(d, st); free_staged(dsa, st); return cuda_fail(e, "copy sa");
     }
   }
-  s = fm_build_device(d, n, dsa, device, st, out, kmer_k, bwt_layout);
+  s = fm_build_device(d, n, dsa, device, st, out, kmer_k, bwt_layout, kmer_k_ax);
   cudaError_t e = free_staged(d, st);
   free_staged(dsa, st);
   if (!e) e = cudaStreamSynchronize(st);
@@ -745,6 +766,14 @@ QR_EXPORT qr_status qr_fm_count_work(const qr_fm* fm, const uint8_t* patterns, c
                                      uint32_t fixed_len, uint32_t* out, uint64_t m, uint64_t* work, void* stream) {
   if (!work) return fail(QR_EINVAL, "qr_fm_count_work: null work");
   return fm_count_impl(fm, patterns, lengths, fixed_len, out, nullptr, m, work, stream);
+}
+
+QR_EXPORT qr_status qr_fm_count_work_ex(const qr_fm* fm, const uint8_t* patterns, const uint32_t* lengths,
+                                        uint32_t fixed_len, uint32_t max_mismatches, uint32_t* out_fwd,
+                                        uint32_t* out_rc, uint64_t m, uint64_t* work, void* stream) {
+  if (!work) return fail(QR_EINVAL, "qr_fm_count_work_ex: null work");
+  if (max_mismatches > 3) return fail(QR_EINVAL, "qr_fm_count_work_ex: max_mismatches must be 0..3");
+  return fm_count_impl(fm, patterns, lengths, fixed_len, out_fwd, out_rc, m, work, stream, (int)max_mismatches);
 }
 
 QR_EXPORT qr_status qr_info(const qr_index* h, uint64_t* n, int* sigma, uint64_t* line_bytes, uint64_t* super_bytes) {
@@ -861,12 +890,20 @@ QR_EXPORT qr_status qr_fm_clone_to_device(const qr_fm* fm, int device, void* str
   if (!c) return fail(QR_ENOMEM, "host allocation");
   c->bwt = nullptr;
   c->kmer = nullptr;
+  c->kmer_ax = nullptr;
   qr_status s = qr_clone_to_device(fm->bwt, device, stream, &c->bwt);
   if (s != QR_OK) { delete c; return s; }
   DeviceGuard dg(device);
   const size_t kb = (kmer_c_offset(fm->kmer_k) + 2) * sizeof(uint2);       // table + C[0..3] tail
   cudaError_t e = cudaMalloc((void**)&c->kmer, kb);
   if (!e) e = cudaMemcpyPeerAsync(c->kmer, device, fm->kmer, fm->bwt->device, kb, (cudaStream_t)stream);
+  if (fm->kmer_ax == fm->kmer) {
+    c->kmer_ax = c->kmer;
+  } else {
+    const size_t kx = kmer_entries(fm->kmer_k_ax) * sizeof(uint2);
+    if (!e) e = cudaMalloc((void**)&c->kmer_ax, kx);
+    if (!e) e = cudaMemcpyPeerAsync(c->kmer_ax, device, fm->kmer_ax, fm->bwt->device, kx, (cudaStream_t)stream);
+  }
   if (!e) e = cudaStreamSynchronize((cudaStream_t)stream);
   if (e) { qr_fm_free(c); return cuda_fail(e, "qr_fm_clone_to_device"); }
   *out = c;
@@ -893,6 +930,7 @@ QR_EXPORT void qr_fm_free(qr_fm* fm) {
   if (!fm) return;
   if (fm->bwt) {
     DeviceGuard dg(fm->bwt->device);
+    if (fm->kmer_ax && fm->kmer_ax != fm->kmer) cudaFree(fm->kmer_ax);
     if (fm->kmer) cudaFree(fm->kmer);
     qr_free(fm->bwt);
   }

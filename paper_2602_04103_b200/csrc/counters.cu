@@ -84,4 +84,39 @@ CounterLease::~CounterLease() {
   if (ring) static_cast<CtrRing*>(ring)->mu.unlock();
 }
 
+// ---- output checksum (qr_checksum) ----------------------------------------------------------
+__device__ __forceinline__ uint64_t cks_mix(uint64_t i, uint64_t v) {
+  uint64_t z = v ^ (i * 0x9E3779B97F4A7C15ull) ^ 0xD6E8FEB86659FD93ull;
+  z = (z ^ (z >> 32)) * 0xD6E8FEB86659FD93ull;
+  z = (z ^ (z >> 32)) * 0xD6E8FEB86659FD93ull;
+  return z ^ (z >> 32);
+}
+template <typename T>
+__global__ void k_checksum(const T* __restrict__ d, uint64_t n, uint64_t i0, unsigned long long* __restrict__ sum) {
+  uint64_t acc = 0;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    acc += cks_mix(i0 + i, (uint64_t)d[i]);
+  for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0 && acc) atomicAdd(sum, (unsigned long long)acc);
+}
+
 }  // namespace qr
+
+using namespace qr;
+#define QR_EXPORT extern "C" __attribute__((visibility("default")))
+
+QR_EXPORT qr_status qr_checksum(const void* data, uint64_t count, int word_bytes, uint64_t index0, uint64_t* sum,
+                                void* stream) {
+  if (!sum || (count && !data)) return fail(QR_EINVAL, "qr_checksum: null pointer");
+  if (word_bytes != 4 && word_bytes != 8) return fail(QR_EINVAL, "qr_checksum: word_bytes must be 4 or 8");
+  if (count == 0) return QR_OK;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const unsigned g = grid_stride_blocks(count, 256, sm_count(dev), 8);
+  cudaStream_t st = (cudaStream_t)stream;
+  unsigned long long* s = reinterpret_cast<unsigned long long*>(sum);
+  if (word_bytes == 8) k_checksum<uint64_t><<<g, 256, 0, st>>>((const uint64_t*)data, count, index0, s);
+  else k_checksum<uint32_t><<<g, 256, 0, st>>>((const uint32_t*)data, count, index0, s);
+  cudaError_t e = cudaGetLastError();
+  return e ? cuda_fail(e, "qr_checksum") : QR_OK;
+}

@@ -732,6 +732,55 @@ __global__ void __launch_bounds__(256) k_fm_seed(FmParams F, const uint8_t* __re
   }
 }
 
+// Seed pre-pass of k_fm_count_l2 for fixed-length batches whose post-seed part has <= 32
+// symbols (configs[3]: 32 - 12 = 20): besides the k-mer interval it packs the symbols the
+// backward search will consume, in consumption order, 2 bits each (bits [2t, 2t+2) = the t-th
+// step's symbol; reverse-complemented for STRANDS = 2 odd tasks).  The count kernel then takes
+// each step's symbol from a register shift instead of an 8-byte pattern window (address
+// arithmetic and a predicated load per step), and never reads the pattern bytes.
+// 2-bit fields of a 128-bit word in reverse order (field i -> field 63 - i)
+__device__ __forceinline__ unsigned __int128 rev2_128(unsigned __int128 a) {
+  const uint64_t lo = (uint64_t)a, hi = (uint64_t)(a >> 64);
+  auto rev2 = [](uint64_t x) {
+    x = __brevll(x);
+    return ((x >> 1) & 0x5555555555555555ull) | ((x & 0x5555555555555555ull) << 1);
+  };
+  return ((unsigned __int128)rev2(lo) << 64) | rev2(hi);
+}
+
+template <int STRANDS>
+__global__ void __launch_bounds__(256) k_fm_seed_packed(FmParams F, const uint8_t* __restrict__ pat, uint32_t len,
+                                                        uint64_t m, uint4* __restrict__ seeds) {
+  const uint64_t ntask = m * STRANDS;
+  const uint32_t kused = (F.K && len >= (uint32_t)F.K) ? (uint32_t)F.K : 0u;
+  const uint32_t nrem = len - kused;                       // <= 32 (checked by the launcher); len <= 46
+  const unsigned __int128 one = 1;
+  for (uint64_t ti = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; ti < ntask; ti += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t pi = STRANDS == 2 ? ti >> 1 : ti;
+    const uint32_t rc = STRANDS == 2 ? (uint32_t)(ti & 1) : 0u;
+    const uint8_t* p = pat + pi * (uint64_t)len;
+    // A = the pattern's symbols 2 bits each, P[i] at bits [2i, 2i+2), from the aligned 8-byte
+    // words covering [p, p + len) (<= 7 words: 53 bytes)
+    const uint32_t mis = (uint32_t)((uintptr_t)p & 7u);
+    const unsigned long long* w = reinterpret_cast<const unsigned long long*>(p - mis);
+    const uint32_t nw = (mis + len + 7) >> 3;
+    unsigned __int128 A = 0;
+    for (uint32_t i = 0; i < nw; ++i) A |= (unsigned __int128)compact8(__ldg(w + i) & 0x0303030303030303ull) << (16 * i);
+    A >>= 2 * mis;
+    const unsigned __int128 R = rev2_128(A);               // P[i] at bits [126 - 2i, 128 - 2i)
+    uint2 iv = make_uint2(0u, (uint32_t)F.N);
+    uint64_t sy;
+    if (rc) {   // RC(P)[j] = 3 - P[len-1-j]: key over its last K = sum_t (3 - P[t]) << 2t
+      if (kused) iv = __ldg(F.kmer + (uint32_t)((A ^ ((one << (2 * kused)) - 1)) & ((one << (2 * kused)) - 1)));
+      sy = (uint64_t)(((A >> (2 * kused)) ^ ((one << (2 * nrem)) - 1)) & ((one << (2 * nrem)) - 1));
+    } else {    // key = sum_t P[len-1-t] << 2t; symbols P[nrem-1], P[nrem-2], ..., P[0]
+      if (kused) iv = __ldg(F.kmer + (uint32_t)((R >> (128 - 2 * len)) & ((one << (2 * kused)) - 1)));
+      sy = nrem ? (uint64_t)((R >> (128 - 2 * nrem)) & ((one << (2 * nrem)) - 1)) : 0ull;
+    }
+    seeds[ti] = make_uint4(iv.x, iv.y, (uint32_t)sy, (uint32_t)(sy >> 32));
+  }
+}
+
 // Work order.  DYN = false: the lane's own grid-stride task sequence (ti, ti + stride, ...) over
 // a multi-wave grid.  DYN = true (default): a persistent grid whose warps take chunks of
 // FM_CHUNK tasks from a global counter (one atomicAdd per chunk); in every loop iteration the
@@ -869,14 +918,14 @@ __global__ void __launch_bounds__(256, QR_FM_MINB) k_fm_count(FmParams F, const 
 //    idle: the refill (seed load, pattern pointer) ran in ~93% of iterations with ~3 of 32 lanes
 //    active, ~80 issue slots each time;
 //  * seeds come from the k_fm_seed pre-pass (one 8-byte load per task).
-template <bool FIXED, bool WORK, int STRANDS, int SMS, int BW>
+template <bool FIXED, bool WORK, int STRANDS, int SMS, int BW, bool PACKED>
 __global__ void __launch_bounds__(256, QR_FM_MINB) k_fm_count_l2(FmParams F, const uint8_t* __restrict__ pat,
                                                               const uint64_t* __restrict__ offs,
                                                               const uint32_t* __restrict__ lens, uint32_t fixed_len,
                                                               uint32_t* __restrict__ out, uint32_t* __restrict__ out_rc,
                                                               uint64_t m, unsigned long long* __restrict__ work,
                                                               unsigned long long* __restrict__ ctr,
-                                                              const uint2* __restrict__ seeds, uint32_t refill_min) {
+                                                              const void* __restrict__ seeds_, uint32_t refill_min) {
   if (BW == 1) x2_masks_init();
   fm_preload_super<SMS>(F);
   const uint64_t ntask = m * STRANDS;
@@ -888,6 +937,7 @@ __global__ void __launch_bounds__(256, QR_FM_MINB) k_fm_count_l2(FmParams F, con
   bool has = false;
   PatWindow P;
   P.reset(pat);
+  uint64_t sy = 0;                                       // PACKED: the remaining symbols, next in bits 0-1
   uint64_t n_steps = 0, n_lines = 0;
   uint64_t cb = 0, ce = 0;                               // the warp's chunk [cb, ce) (warp-uniform)
   bool exhausted = false;
@@ -911,10 +961,17 @@ __global__ void __launch_bounds__(256, QR_FM_MINB) k_fm_count_l2(FmParams F, con
           const uint64_t pi = STRANDS == 2 ? ti >> 1 : ti;
           rc = STRANDS == 2 ? (uint32_t)(ti & 1) : 0u;
           len = FIXED ? fixed_len : lens[pi];
-          P.reset(pat + (FIXED ? pi * (uint64_t)fixed_len : offs[pi]));
-          const uint2 iv = __ldg(seeds + ti);
-          lo = iv.x;
-          hi = iv.y;
+          if (PACKED) {
+            const uint4 sv = __ldg(reinterpret_cast<const uint4*>(seeds_) + ti);
+            lo = sv.x;
+            hi = sv.y;
+            sy = ((uint64_t)sv.w << 32) | sv.z;
+          } else {
+            P.reset(pat + (FIXED ? pi * (uint64_t)fixed_len : offs[pi]));
+            const uint2 iv = __ldg(reinterpret_cast<const uint2*>(seeds_) + ti);
+            lo = iv.x;
+            hi = iv.y;
+          }
           k = (int64_t)len - 1 - ((F.K && len >= (uint32_t)F.K) ? F.K : 0);
           pend = 0;
           has = true;
@@ -931,8 +988,13 @@ __global__ void __launch_bounds__(256, QR_FM_MINB) k_fm_count_l2(FmParams F, con
     if (exhausted && __ballot_sync(0xffffffffu, has) == 0) break;
     // one line of one backward step, in every lane (results kept only where act)
     const bool act = has && (pend || (k >= 0 && lo < hi));
-    const int64_t idx = rc ? (int64_t)len - 1 - k : k;
-    const uint32_t c = P.at_if(act, idx) ^ (rc ? 3u : 0u);
+    uint32_t c;
+    if (PACKED) {
+      c = (uint32_t)sy & 3u;
+    } else {
+      const int64_t idx = rc ? (int64_t)len - 1 - k : k;
+      c = P.at_if(act, idx) ^ (rc ? 3u : 0u);
+    }
     uint32_t nlo = lo, nhi = hi, npend = pend, nl;
     const bool done = BW == 1 ? fm_step_pend_x2<SMS>(F, C4, c, nlo, nhi, npend, nl)
                               : fm_step_pend<SMS>(F, C4, c, nlo, nhi, npend, nl);
@@ -941,6 +1003,7 @@ __global__ void __launch_bounds__(256, QR_FM_MINB) k_fm_count_l2(FmParams F, con
     hi = act ? nhi : hi;
     pend = act ? npend : pend;
     k -= (act && done) ? 1 : 0;
+    if (PACKED) sy = (act && done) ? sy >> 2 : sy;
     if (has && !pend && (k < 0 || lo >= hi)) {           // finished: write the count
       const uint32_t res = lo < hi ? hi - lo : 0u;
       if (STRANDS == 2 && rc) out_rc[ti >> 1] = res;
@@ -1029,15 +1092,30 @@ __device__ __forceinline__ void fm_occ4(const FmParams& F, uint32_t x, uint32_t 
 // exact backward search of P[0..k] from [lo, hi); returns the final interval size
 // the same for three intervals continuing over the same symbols P[k], P[k-1], ...: their steps
 // are independent, so each position issues the loads of all live intervals before consuming any
-template <int BW, class W>
+// Work accounting of the approximate-search kernels (WORK = true, qr_fm_count_work_ex): ws counts
+// rank evaluations at an interval's two ends (exact steps, rank_4 pairs) plus k-mer table
+// lookups, wl the distinct lines (table entries) they gather.
+struct FmWork {
+  uint64_t ws = 0, wl = 0;
+};
+template <int BW>
+__device__ __forceinline__ uint32_t fm_line_of(const FmParams& F, uint32_t x) {
+  uint32_t j = BW == 1 ? (x >> 6) / 3u : (x >> 5) / 7u;
+  return j > (uint32_t)F.last_line ? (uint32_t)F.last_line : j;
+}
+
+template <int BW, bool WORK = false, class W>
 __device__ __forceinline__ uint32_t fm_continue3(const FmParams& F, W& P, int64_t k, uint32_t (&lo)[3],
-                                                 uint32_t (&hi)[3]) {
+                                                 uint32_t (&hi)[3], FmWork& wk) {
   uint32_t nl;
   for (; k >= 0 && (lo[0] < hi[0] || lo[1] < hi[1] || lo[2] < hi[2]); --k) {
     const uint32_t c = P.at(k);
 #pragma unroll
     for (int r = 0; r < 3; ++r)
-      if (lo[r] < hi[r]) fm_step<0, BW, true>(F, c, lo[r], hi[r], nl);
+      if (lo[r] < hi[r]) {
+        fm_step<0, BW, true>(F, c, lo[r], hi[r], nl);
+        if (WORK) { wk.ws += 1; wk.wl += nl; }
+      }
   }
   uint32_t t = 0;
 #pragma unroll
@@ -1045,11 +1123,23 @@ __device__ __forceinline__ uint32_t fm_continue3(const FmParams& F, W& P, int64_
   return t;
 }
 
-template <int BW, class W>
-__device__ __forceinline__ uint32_t fm_continue(const FmParams& F, W& P, int64_t k, uint32_t lo, uint32_t hi) {
+template <int BW, bool WORK = false, class W>
+__device__ __forceinline__ uint32_t fm_continue(const FmParams& F, W& P, int64_t k, uint32_t lo, uint32_t hi,
+                                                FmWork& wk) {
   uint32_t nl;
-  for (; k >= 0 && lo < hi; --k) fm_step<0, BW, true>(F, P.at(k), lo, hi, nl);
+  for (; k >= 0 && lo < hi; --k) {
+    fm_step<0, BW, true>(F, P.at(k), lo, hi, nl);
+    if (WORK) { wk.ws += 1; wk.wl += nl; }
+  }
   return lo < hi ? hi - lo : 0u;
+}
+// rank_4 at both ends of an interval (the four children of a search-tree node)
+template <int BW, bool WORK>
+__device__ __forceinline__ void fm_occ4_pair(const FmParams& F, uint32_t lo, uint32_t hi, uint32_t (&ol)[4],
+                                             uint32_t (&oh)[4], FmWork& wk) {
+  if (BW == 1) { fm_occ4_x2(F, lo, ol); fm_occ4_x2(F, hi, oh); }
+  else         { fm_occ4(F, lo, ol); fm_occ4(F, hi, oh); }
+  if (WORK) { wk.ws += 1; wk.wl += fm_line_of<BW>(F, lo) == fm_line_of<BW>(F, hi) ? 1u : 2u; }
 }
 
 // Next pattern index of a lane.  Static: grid stride.  Dynamic (ctr != null): the lanes that reach
@@ -1079,12 +1169,14 @@ __device__ __forceinline__ uint64_t approx_next(unsigned long long* ctr, uint64_
 #define QR_APPROX1_MINB 4
 #endif
 
-template <bool FIXED, int BW, int STRANDS>
+template <bool FIXED, int BW, int STRANDS, bool WORK = false>
 __global__ void __launch_bounds__(256, QR_APPROX1_MINB) k_fm_approx1(FmParams F, const uint8_t* __restrict__ pat,
                                                     const uint64_t* __restrict__ offs,
                                                     const uint32_t* __restrict__ lens, uint32_t fixed_len,
                                                     uint32_t* __restrict__ out, uint32_t* __restrict__ out_rc,
-                                                    uint64_t m, unsigned long long* __restrict__ ctr) {
+                                                    uint64_t m, unsigned long long* __restrict__ ctr,
+                                                    unsigned long long* __restrict__ work) {
+  FmWork wk;
   if (BW == 1) x2_masks_init();
   else qd_masks_init();
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
@@ -1109,10 +1201,12 @@ __global__ void __launch_bounds__(256, QR_APPROX1_MINB) k_fm_approx1(FmParams F,
         uint2 iv[3];                                       // the three variants' lookups issued together
 #pragma unroll
         for (uint32_t r = 1; r < 4; ++r) iv[r - 1] = __ldg(F.kmer + (key0 ^ ((f ^ ((f + r) & 3u)) << (2 * t))));
+        if (WORK) { wk.ws += 3; wk.wl += 3; }
         uint32_t vl[3] = {iv[0].x, iv[1].x, iv[2].x}, vh[3] = {iv[0].y, iv[1].y, iv[2].y};
-        total += fm_continue3<BW>(F, P, (int64_t)len - 1 - F.K, vl, vh);
+        total += fm_continue3<BW, WORK>(F, P, (int64_t)len - 1 - F.K, vl, vh, wk);
       }
       const uint2 iv0 = __ldg(F.kmer + key0);
+      if (WORK) { wk.ws += 1; wk.wl += 1; }
       lo = iv0.x; hi = iv0.y;
       j = (int64_t)len - 1 - F.K;
     } else {
@@ -1121,8 +1215,7 @@ __global__ void __launch_bounds__(256, QR_APPROX1_MINB) k_fm_approx1(FmParams F,
     }
     for (; j >= 0 && lo < hi; --j) {                     // exact path; branch on the mismatch at j
       uint32_t ol[4], oh[4];
-      if (BW == 1) { fm_occ4_x2(F, lo, ol); fm_occ4_x2(F, hi, oh); }
-      else         { fm_occ4(F, lo, ol); fm_occ4(F, hi, oh); }
+      fm_occ4_pair<BW, WORK>(F, lo, hi, ol, oh, wk);
       const uint32_t cj = P.at(j);
       uint32_t bl[3], bh[3];                              // the three substituted symbols' intervals
 #pragma unroll
@@ -1131,13 +1224,17 @@ __global__ void __launch_bounds__(256, QR_APPROX1_MINB) k_fm_approx1(FmParams F,
         bl[r] = Cs[c] + ol[c];
         bh[r] = Cs[c] + oh[c];
       }
-      total += fm_continue3<BW>(F, P, j - 1, bl, bh);
+      total += fm_continue3<BW, WORK>(F, P, j - 1, bl, bh, wk);
       lo = Cs[cj] + ol[cj];
       hi = Cs[cj] + oh[cj];
     }
     if (lo < hi) total += hi - lo;
     if (STRANDS == 2 && rc) out_rc[pi] = (uint32_t)total;
     else out[pi] = (uint32_t)total;
+  }
+  if (WORK && wk.ws) {
+    atomicAdd(work, (unsigned long long)wk.ws);
+    atomicAdd(work + 1, (unsigned long long)wk.wl);
   }
 }
 
@@ -1156,9 +1253,9 @@ __global__ void __launch_bounds__(256, QR_APPROX1_MINB) k_fm_approx1(FmParams F,
 // by node; every K-mer within distance KMAX of the pattern's last K symbols is looked up in the
 // k-mer table instead (1 + 3K + 9 C(K,2) [+ 27 C(K,3)] lookups), and the search continues from
 // each non-empty interval with the substitutions it has left.
-template <int BW, int KMAX, class W>
+template <int BW, int KMAX, bool WORK, class W>
 __device__ __forceinline__ uint64_t fm_backtrack(const FmParams& F, W& P, const uint32_t (&Cs)[4],
-                                                 uint32_t lo, uint32_t hi, uint32_t pos, int f0) {
+                                                 uint32_t lo, uint32_t hi, uint32_t pos, int f0, FmWork& wk) {
   constexpr uint32_t UNX = 8;   // not 4: a frame whose branches are all tried has fd = 4
   uint32_t flo[KMAX + 1], fhi[KMAX + 1], fpos[KMAX + 1], fd[KMAX + 1];   // fd: next branch symbol, UNX = unexpanded
   uint32_t clo[KMAX][4], chi[KMAX][4];                                   // children of frames 0 .. KMAX-1
@@ -1170,13 +1267,12 @@ __device__ __forceinline__ uint64_t fm_backtrack(const FmParams& F, W& P, const 
       if (flo[f] >= fhi[f]) { --f; continue; }
       if (fpos[f] == 0) { total += fhi[f] - flo[f]; --f; continue; }
       if (f == KMAX) {                                   // no substitution left: exact search
-        total += fm_continue<BW>(F, P, (int64_t)fpos[f] - 1, flo[f], fhi[f]);
+        total += fm_continue<BW, WORK>(F, P, (int64_t)fpos[f] - 1, flo[f], fhi[f], wk);
         --f;
         continue;
       }
       uint32_t ol[4], oh[4];
-      if (BW == 1) { fm_occ4_x2(F, flo[f], ol); fm_occ4_x2(F, fhi[f], oh); }
-      else         { fm_occ4(F, flo[f], ol); fm_occ4(F, fhi[f], oh); }
+      fm_occ4_pair<BW, WORK>(F, flo[f], fhi[f], ol, oh, wk);
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         clo[f][c] = Cs[c] + ol[c];
@@ -1204,12 +1300,14 @@ __device__ __forceinline__ uint32_t kmer_subst(uint32_t key, int t, uint32_t r) 
   return key ^ ((o ^ ((o + r) & 3u)) << (2 * t));
 }
 
-template <bool FIXED, int BW, int KMAX, int STRANDS>
+template <bool FIXED, int BW, int KMAX, int STRANDS, bool WORK = false>
 __global__ void QR_APPROX_LB k_fm_approxk(FmParams F, const uint8_t* __restrict__ pat,
                                                     const uint64_t* __restrict__ offs,
                                                     const uint32_t* __restrict__ lens, uint32_t fixed_len,
                                                     uint32_t* __restrict__ out, uint32_t* __restrict__ out_rc,
-                                                    uint64_t m, unsigned long long* __restrict__ ctr) {
+                                                    uint64_t m, unsigned long long* __restrict__ ctr,
+                                                    unsigned long long* __restrict__ work) {
+  FmWork wk;
   if (BW == 1) x2_masks_init();
   else qd_masks_init();
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
@@ -1231,7 +1329,8 @@ __global__ void QR_APPROX_LB k_fm_approxk(FmParams F, const uint8_t* __restrict_
       const uint32_t pos = len - (uint32_t)K;
       auto seed = [&](uint32_t key, int mm) {
         const uint2 iv = __ldg(F.kmer + key);
-        if (iv.x < iv.y) total += fm_backtrack<BW, KMAX>(F, P, Cs, iv.x, iv.y, pos, mm);
+        if (WORK) { wk.ws += 1; wk.wl += 1; }
+        if (iv.x < iv.y) total += fm_backtrack<BW, KMAX, WORK>(F, P, Cs, iv.x, iv.y, pos, mm, wk);
       };
       // the seeds with all KMAX substitutions inside the K-mer have none left: their three
       // variants at the last substituted position are looked up together and continue as one
@@ -1240,8 +1339,9 @@ __global__ void QR_APPROX_LB k_fm_approxk(FmParams F, const uint8_t* __restrict_
         uint2 iv[3];
 #pragma unroll
         for (uint32_t r = 1; r < 4; ++r) iv[r - 1] = __ldg(F.kmer + kmer_subst(key, t, r));
+        if (WORK) { wk.ws += 3; wk.wl += 3; }
         uint32_t vl[3] = {iv[0].x, iv[1].x, iv[2].x}, vh[3] = {iv[0].y, iv[1].y, iv[2].y};
-        total += fm_continue3<BW>(F, P, (int64_t)pos - 1, vl, vh);
+        total += fm_continue3<BW, WORK>(F, P, (int64_t)pos - 1, vl, vh, wk);
       };
       seed(key0, 0);
       for (int t1 = 0; t1 < K; ++t1)
@@ -1261,10 +1361,14 @@ __global__ void QR_APPROX_LB k_fm_approxk(FmParams F, const uint8_t* __restrict_
           }
         }
     } else {
-      total = fm_backtrack<BW, KMAX>(F, P, Cs, 0u, (uint32_t)F.N, len, 0);
+      total = fm_backtrack<BW, KMAX, WORK>(F, P, Cs, 0u, (uint32_t)F.N, len, 0, wk);
     }
     if (STRANDS == 2 && rc) out_rc[pi] = (uint32_t)total;
     else out[pi] = (uint32_t)total;
+  }
+  if (WORK && wk.ws) {
+    atomicAdd(work, (unsigned long long)wk.ws);
+    atomicAdd(work + 1, (unsigned long long)wk.wl);
   }
 }
 
@@ -1291,9 +1395,17 @@ static FmParams params_of(const qr_fm* fm) {
   return F;
 }
 
+// the approximate-search kernels' table (C[0..3] stays at the main table's tail, F.Ct)
+static FmParams params_ax(FmParams F, const qr_fm* fm) {
+  F.kmer = fm->kmer_ax;
+  F.K = fm->kmer_k_ax;
+  return F;
+}
+
 extern int g_fm_blocks_per_sm;
 extern int g_fm_lean;
 extern int g_fm_refill;
+extern int g_fm_packed;
 
 int l2_bytes(int device);
 
@@ -1333,6 +1445,13 @@ static int fm_smem_mode(const qr_fm* fm, size_t* bytes) {
   return 0;
 }
 
+// fixed-length batches whose post-seed symbols fit one u64 (2 bits each) take packed seeds
+static bool fm_packable(const FmParams& F, uint32_t fixed_len) {
+  if (g_fm_packed == 0) return false;
+  const uint32_t kused = (F.K && fixed_len >= (uint32_t)F.K) ? (uint32_t)F.K : 0u;
+  return fixed_len - kused <= 32u && fixed_len <= 46u;     // the seed kernel's 128-bit window
+}
+
 static int cur_device() {
   int d = 0;
   cudaGetDevice(&d);
@@ -1344,9 +1463,15 @@ static void launch_fm1(unsigned g, size_t smem, cudaStream_t st, const FmParams&
                        const uint64_t* offs, const uint32_t* lens, uint32_t fixed_len, uint32_t* out, uint32_t* out_rc,
                        uint64_t m, unsigned long long* w, unsigned long long* ctr, int sms, uint2* seeds) {
   if (ctr && seeds && STEP == 3) {
-    auto kern = F.bw ? k_fm_count_l2<FIXED, WORK, STRANDS, SMS, 1> : k_fm_count_l2<FIXED, WORK, STRANDS, SMS, 0>;
-    k_fm_seed<FIXED, STRANDS><<<grid_stride_blocks(m * STRANDS, 256, sms, 16), 256, 0, st>>>(F, pat, offs, lens,
-                                                                                           fixed_len, m, seeds);
+    const bool packed = FIXED && fm_packable(F, fixed_len);
+    auto kern = packed ? (F.bw ? k_fm_count_l2<FIXED, WORK, STRANDS, SMS, 1, true> : k_fm_count_l2<FIXED, WORK, STRANDS, SMS, 0, true>)
+                       : (F.bw ? k_fm_count_l2<FIXED, WORK, STRANDS, SMS, 1, false> : k_fm_count_l2<FIXED, WORK, STRANDS, SMS, 0, false>);
+    if (packed)
+      k_fm_seed_packed<STRANDS><<<grid_stride_blocks(m * STRANDS, 256, sms, 16), 256, 0, st>>>(F, pat, fixed_len, m,
+                                                                                               (uint4*)seeds);
+    else
+      k_fm_seed<FIXED, STRANDS><<<grid_stride_blocks(m * STRANDS, 256, sms, 16), 256, 0, st>>>(F, pat, offs, lens,
+                                                                                             fixed_len, m, seeds);
     smem_limit_raise((const void*)kern, smem, cur_device());
     int per_sm = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem) != cudaSuccess || per_sm <= 0) {
@@ -1430,7 +1555,8 @@ static cudaError_t launch_fm(const qr_fm* fm, int step, unsigned g, cudaStream_t
     const bool pre = g_fm_seed == 2 || (g_fm_seed == 0 && bwt_l2_resident(fm));
     if (pre) {
       keep_pool_memory(fm->bwt->device, st);
-      if ((e = cudaMallocAsync((void**)&seeds, m * (out_rc ? 2 : 1) * sizeof(uint2), st))) return e;
+      // 16 B per task: room for the packed seeds (k_fm_seed_packed) when the batch qualifies
+      if ((e = cudaMallocAsync((void**)&seeds, m * (out_rc ? 2 : 1) * sizeof(uint4), st))) return e;
     }
     if ((e = lease.acquire(fm->bwt->device, st, &ctr))) { if (seeds) cudaFreeAsync(seeds, st); return e; }
   }
@@ -1453,15 +1579,15 @@ static cudaError_t launch_fm(const qr_fm* fm, int step, unsigned g, cudaStream_t
   return e;
 }
 
-template <bool FIXED, int STRANDS>
+template <bool FIXED, int STRANDS, bool WORK>
 static cudaError_t launch_approx_s(const qr_fm* fm, unsigned g, cudaStream_t st, const FmParams& F, const uint8_t* pat,
                                    const uint64_t* offs, const uint32_t* lens, uint32_t fixed_len, uint32_t* out,
-                                   uint32_t* out_rc, uint64_t m, int kmax) {
-  auto kern = kmax == 1 ? (F.bw ? k_fm_approx1<FIXED, 1, STRANDS> : k_fm_approx1<FIXED, 0, STRANDS>)
-            : kmax == 2 ? (F.bw ? k_fm_approxk<FIXED, 1, 2, STRANDS> : k_fm_approxk<FIXED, 0, 2, STRANDS>)
-                        : (F.bw ? k_fm_approxk<FIXED, 1, 3, STRANDS> : k_fm_approxk<FIXED, 0, 3, STRANDS>);
+                                   uint32_t* out_rc, uint64_t m, int kmax, unsigned long long* work) {
+  auto kern = kmax == 1 ? (F.bw ? k_fm_approx1<FIXED, 1, STRANDS, WORK> : k_fm_approx1<FIXED, 0, STRANDS, WORK>)
+            : kmax == 2 ? (F.bw ? k_fm_approxk<FIXED, 1, 2, STRANDS, WORK> : k_fm_approxk<FIXED, 0, 2, STRANDS, WORK>)
+                        : (F.bw ? k_fm_approxk<FIXED, 1, 3, STRANDS, WORK> : k_fm_approxk<FIXED, 0, 3, STRANDS, WORK>);
   if (!g_fm_dyn) {
-    kern<<<g, 256, 0, st>>>(F, pat, offs, lens, fixed_len, out, out_rc, m, nullptr);
+    kern<<<g, 256, 0, st>>>(F, pat, offs, lens, fixed_len, out, out_rc, m, nullptr, work);
     return cudaGetLastError();
   }
   int per_sm = 0;
@@ -1474,7 +1600,7 @@ static cudaError_t launch_approx_s(const qr_fm* fm, unsigned g, cudaStream_t st,
   unsigned long long* ctr = nullptr;
   cudaError_t e = lease.acquire(fm->bwt->device, st, &ctr);
   if (e) return e;
-  kern<<<res < g ? res : g, 256, 0, st>>>(F, pat, offs, lens, fixed_len, out, out_rc, m, ctr);
+  kern<<<res < g ? res : g, 256, 0, st>>>(F, pat, offs, lens, fixed_len, out, out_rc, m, ctr, work);
   e = cudaGetLastError();
   cudaError_t e2 = lease.release(st);
   return e ? e : e2;
@@ -1483,9 +1609,13 @@ static cudaError_t launch_approx_s(const qr_fm* fm, unsigned g, cudaStream_t st,
 template <bool FIXED>
 static cudaError_t launch_approx(const qr_fm* fm, unsigned g, cudaStream_t st, const FmParams& F, const uint8_t* pat,
                                  const uint64_t* offs, const uint32_t* lens, uint32_t fixed_len, uint32_t* out,
-                                 uint32_t* out_rc, uint64_t m, int kmax) {
-  if (out_rc) return launch_approx_s<FIXED, 2>(fm, g, st, F, pat, offs, lens, fixed_len, out, out_rc, m, kmax);
-  return launch_approx_s<FIXED, 1>(fm, g, st, F, pat, offs, lens, fixed_len, out, nullptr, m, kmax);
+                                 uint32_t* out_rc, uint64_t m, int kmax, unsigned long long* work) {
+  if (work) {
+    if (out_rc) return launch_approx_s<FIXED, 2, true>(fm, g, st, F, pat, offs, lens, fixed_len, out, out_rc, m, kmax, work);
+    return launch_approx_s<FIXED, 1, true>(fm, g, st, F, pat, offs, lens, fixed_len, out, nullptr, m, kmax, work);
+  }
+  if (out_rc) return launch_approx_s<FIXED, 2, false>(fm, g, st, F, pat, offs, lens, fixed_len, out, out_rc, m, kmax, nullptr);
+  return launch_approx_s<FIXED, 1, false>(fm, g, st, F, pat, offs, lens, fixed_len, out, nullptr, m, kmax, nullptr);
 }
 
 qr_status fm_count_device(const qr_fm* fm, const uint8_t* pat, const uint32_t* lengths, uint32_t fixed_len,
@@ -1498,7 +1628,7 @@ qr_status fm_count_device(const qr_fm* fm, const uint8_t* pat, const uint32_t* l
   unsigned long long* w = reinterpret_cast<unsigned long long*>(work);
   cudaError_t e;
   if (!lengths) {
-    if (approx) e = launch_approx<true>(fm, g, st, F, pat, nullptr, nullptr, fixed_len, out, out_rc, m, approx);
+    if (approx) e = launch_approx<true>(fm, g, st, params_ax(F, fm), pat, nullptr, nullptr, fixed_len, out, out_rc, m, approx, w);
     else if (work) e = launch_fm<true, true>(fm, fm_step_of(fm), g, st, F, pat, nullptr, nullptr, fixed_len, out, out_rc, m, w);
     else      e = launch_fm<true, false>(fm, fm_step_of(fm), g, st, F, pat, nullptr, nullptr, fixed_len, out, out_rc, m, w);
     if (e) return cuda_fail(e, "k_fm_count");
@@ -1514,7 +1644,7 @@ qr_status fm_count_device(const qr_fm* fm, const uint8_t* pat, const uint32_t* l
   if ((e = cub::DeviceScan::ExclusiveSum(tmp, tb, offs, offs, (int64_t)m, st))) {
     cudaFreeAsync(offs, st); cudaFreeAsync(tmp, st); return cuda_fail(e, "scan");
   }
-  if (approx) e = launch_approx<false>(fm, g, st, F, pat, offs, lengths, 0, out, out_rc, m, approx);
+  if (approx) e = launch_approx<false>(fm, g, st, params_ax(F, fm), pat, offs, lengths, 0, out, out_rc, m, approx, w);
   else if (work) e = launch_fm<false, true>(fm, fm_step_of(fm), g, st, F, pat, offs, lengths, 0, out, out_rc, m, w);
   else      e = launch_fm<false, false>(fm, fm_step_of(fm), g, st, F, pat, offs, lengths, 0, out, out_rc, m, w);
   cudaFreeAsync(offs, st);
@@ -1525,7 +1655,7 @@ qr_status fm_count_device(const qr_fm* fm, const uint8_t* pat, const uint32_t* l
 
 // d_text: device copy, >= ceil(n/32) words, zero padded.  d_sa: optional device SA (N u32).
 qr_status fm_build_device(const uint64_t* d_text, uint64_t n, const uint32_t* d_sa_given, int device, cudaStream_t st,
-                          qr_fm** out, int kmer_k, int bwt_layout) {
+                          qr_fm** out, int kmer_k, int bwt_layout, int kmer_k_ax) {
   const uint64_t N = n + 1;
   const int sms = sm_count(device);
   cudaError_t e;
@@ -1588,6 +1718,21 @@ qr_status fm_build_device(const uint64_t* d_text, uint64_t n, const uint32_t* d_
     else      k_kmer_table<0><<<(unsigned)((ne + 255) / 256), 256, 0, st>>>(F, fm->kmer);
   }
   if ((e = cudaGetLastError())) return bail(cuda_fail(e, "k_kmer_table"));
+  fm->kmer_ax = fm->kmer;
+  fm->kmer_k_ax = kmer_k;
+  if (kmer_k_ax != kmer_k && kmer_k_ax > 0) {               // the approximate-search table
+    const uint64_t nx = kmer_entries(kmer_k_ax);
+    if ((e = cudaMalloc((void**)&fm->kmer_ax, nx * sizeof(uint2)))) {
+      fm->kmer_ax = fm->kmer;
+      return bail(cuda_fail(e, "alloc kmer (approximate search)"));
+    }
+    fm->kmer_k_ax = kmer_k_ax;
+    FmParams Fx = F;
+    Fx.K = kmer_k_ax;
+    if (F.bw) k_kmer_table<1><<<(unsigned)((nx + 255) / 256), 256, 0, st>>>(Fx, fm->kmer_ax);
+    else      k_kmer_table<0><<<(unsigned)((nx + 255) / 256), 256, 0, st>>>(Fx, fm->kmer_ax);
+    if ((e = cudaGetLastError())) return bail(cuda_fail(e, "k_kmer_table (approximate search)"));
+  }
   if ((e = cudaStreamSynchronize(st))) { release(); qr_fm_free(fm); return cuda_fail(e, "fm build"); }
   release();
   *out = fm;

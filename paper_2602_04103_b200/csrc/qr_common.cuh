@@ -57,6 +57,8 @@ struct qr_fm {
   uint64_t C[5];        // C[c] = 1 + #{t_i < c}; C[4] = N
   uint2* kmer;          // 4^K [lo, hi) intervals after K backward steps, then C[0..3] (2 uint2)
   int kmer_k;           // K: table of K-mers (PAPER.md:918 uses 8; 0 = no table)
+  uint2* kmer_ax;       // the approximate-search kernels' table (== kmer unless a wider one pays there)
+  int kmer_k_ax;
 };
 
 namespace qr {

@@ -232,9 +232,9 @@ def test_fm_all_kmers_partition(cuda):
             assert int(to_host(d).astype(np.int64).sum()) == n - k + 1
 
 
-@pytest.mark.parametrize("step", [1, 2, 3])
+@pytest.mark.parametrize("step,packed,refill", [(1, 1, 8), (2, 1, 8), (3, 1, 8), (3, 0, 8), (3, 1, 1), (3, 1, 32)])
 @pytest.mark.parametrize("bps", [2, 16, 64])
-def test_fm_tuning_does_not_change_results(cuda, bps, step):
+def test_fm_tuning_does_not_change_results(cuda, bps, step, packed, refill):
     torch = _torch()
     n = 90000
     w = gen.dna(31, n, 1)
@@ -249,6 +249,8 @@ def test_fm_tuning_does_not_change_results(cuda, bps, step):
     ref_fixed = ora.count(fixed, np.arange(m, dtype=np.uint64) * L, np.full(m, L, np.uint32))
     qr.qr_set_tuning("fm_blocks_per_sm", bps)
     qr.qr_set_tuning("fm_step", step)
+    qr.qr_set_tuning("fm_packed", packed)
+    qr.qr_set_tuning("fm_refill", refill)
     try:
         d = torch.empty(lens.size, dtype=torch.int32, device=cuda)
         qr.qr_fm_count(fm, to_dev(cat, cuda), to_dev(lens, cuda), 0, d, lens.size)
@@ -263,6 +265,8 @@ def test_fm_tuning_does_not_change_results(cuda, bps, step):
     finally:
         qr.qr_set_tuning("fm_blocks_per_sm", 64)
         qr.qr_set_tuning("fm_step", DEFAULT_FM_STEP)
+        qr.qr_set_tuning("fm_packed", 1)
+        qr.qr_set_tuning("fm_refill", 8)
     rc = np.concatenate([(3 - fixed[i * L:(i + 1) * L][::-1]).astype(np.uint8) for i in range(m)])
     assert np.array_equal(to_host(db).view(np.uint32), ref_fixed)
     assert np.array_equal(to_host(dr).view(np.uint32),
@@ -494,9 +498,11 @@ def test_fm_work_order_covers_every_task(cuda, dyn, seed, m):
 
 
 def test_fm_default_kmer_width(cuda):
-    """qr_fm_build's width: the paper's 8 below n = 2^20, 10 below 2^24, 12 above."""
+    """qr_fm_build's width: the paper's 8 below n = 2^20, 10 below 2^24, above 11 while the BWT
+    layout + the 32 MiB 11-mer table fit in 60% of the L2 (126 MB on B200), else 12."""
     torch = _torch()
-    for n, k in ((1000, 8), ((1 << 20) - 1, 8), (1 << 20, 10), ((1 << 24) - 1, 10), (1 << 24, 12)):
+    for n, k in ((1000, 8), ((1 << 20) - 1, 8), (1 << 20, 10), ((1 << 24) - 1, 10), (1 << 24, 11), (1 << 26, 11),
+                 (1 << 28, 12)):
         t = torch.empty((n + 31) // 32 + 1, dtype=torch.uint64, device=cuda)
         gen.dna_dev(50, n, 0, t)
         fm = qr.qr_fm_build(t, n)
@@ -709,3 +715,136 @@ def test_fm_empty_batches(cuda):
     qr.qr_fm_count(fm, np.zeros(64, np.uint8), np.zeros(4, np.uint32), 0, h, 0)
     qr.qr_sync()
     assert int(h.sum()) == 28
+
+
+_ORA_CACHE = {}
+
+
+@pytest.mark.parametrize("L", [12, 13, 43, 44, 45])
+@pytest.mark.parametrize("strands", [1, 2])
+def test_fm_packed_seed_boundaries(cuda, L, strands):
+    """L2-resident count kernel with packed post-seed symbols (k_fm_seed_packed): a 2^24-symbol text
+    takes K = 12, so L = 44 leaves exactly 32 symbols (the largest packed case), 45 falls back to
+    the pattern window, 12 and 13 leave none and one.  Both strands, exact substrings and iid
+    patterns, against the oracle's backward search."""
+    torch = _torch()
+    n = (1 << 24) + 77
+    w = gen.dna(91, n, 0)
+    sym = gen.unpack_dna(w, n)
+    fm = qr.qr_fm_build(w, n, kmer_k=12)
+    assert fm.kmer_k == 12
+    m = 6000
+    fx = gen.patterns(92 + L, 0, m, L, w, n)
+    offs, lens = np.arange(m, dtype=np.uint64) * L, np.full(m, L, np.uint32)
+    d = torch.empty(m, dtype=torch.int32, device=cuda)
+    dr = torch.empty(m, dtype=torch.int32, device=cuda)
+    if strands == 1:
+        qr.qr_fm_count(fm, to_dev(fx, cuda), None, L, d, m)
+    else:
+        qr.qr_fm_count_both(fm, to_dev(fx, cuda), None, L, d, dr, m)
+    torch.cuda.synchronize()
+    if n not in _ORA_CACHE:                               # one oracle SA for all parametrisations
+        _ORA_CACHE[n] = oracle.FmOracle(sym)
+    ora = _ORA_CACHE[n]
+    sel = np.arange(0, m, 3)                              # the oracle on every third pattern
+    cat = np.concatenate([fx[i * L:(i + 1) * L] for i in sel])
+    so, sl = np.arange(sel.size, dtype=np.uint64) * L, np.full(sel.size, L, np.uint32)
+    assert np.array_equal(to_host(d).view(np.uint32)[sel], ora.count(cat, so, sl))
+    if strands == 2:
+        rc = np.concatenate([revcomp(fx[i * L:(i + 1) * L]) for i in sel])
+        assert np.array_equal(to_host(dr).view(np.uint32)[sel], ora.count(rc, so, sl))
+
+
+@pytest.mark.parametrize("bwt_layout", [None, qr.QR_LAYOUT_QUADRANK16X2])
+def test_fm_count_work_ex_accounting(cuda, bwt_layout):
+    """qr_fm_count_work_ex (measurement counters of every count flavour): counts equal the plain
+    calls'; exact one strand equals qr_fm_count_work and the oracle's post-seed steps / lines;
+    both strands = forward + the reverse complements counted alone; approximate search counts at
+    least the exact path's work and more lines than rank pairs; the counters do not depend on the
+    work order (static / dynamic)."""
+    torch = _torch()
+    n = 60000
+    w = gen.dna(401, n, 1)
+    sym = gen.unpack_dna(w, n)
+    fm = qr.qr_fm_build(w, n, bwt_layout=bwt_layout)
+    ora = oracle.FmOracle(sym)
+    L, m = 40, 3000
+    fx = gen.patterns(402, 1, m, L, w, n)
+    rcx = np.concatenate([revcomp(fx[i * L:(i + 1) * L]) for i in range(m)])
+    offs, lens = np.arange(m, dtype=np.uint64) * L, np.full(m, L, np.uint32)
+    block = 192 if bwt_layout else 224
+
+    def work_of(pats, kmax, both, dyn=1):
+        qr.qr_set_tuning("fm_dyn", dyn)
+        o = torch.empty(m, dtype=torch.int32, device=cuda)
+        orc = torch.empty(m, dtype=torch.int32, device=cuda) if both else None
+        wk = torch.zeros(2, dtype=torch.uint64, device=cuda)
+        qr.qr_fm_count_work_ex(fm, to_dev(pats, cuda), None, L, kmax, o, orc, m, wk)
+        torch.cuda.synchronize()
+        qr.qr_set_tuning("fm_dyn", 1)
+        return [int(x) for x in to_host(wk)], to_host(o).view(np.uint32), None if orc is None else to_host(orc).view(np.uint32)
+
+    (s1, l1), c1, _ = work_of(fx, 0, False)
+    assert np.array_equal(c1, ora.count(fx, offs, lens))
+    assert (s1, l1) == ora.work(fx, offs, lens, skip=fm.kmer_k, block=block)
+    (sr, lr), cr, _ = work_of(rcx, 0, False)
+    (sb, lb), cbf, cbr = work_of(fx, 0, True)
+    assert (sb, lb) == (s1 + sr, l1 + lr)
+    assert np.array_equal(cbf, c1) and np.array_equal(cbr, cr)
+    for kmax in (1, 2):
+        (sa, la), ca, car = work_of(fx, kmax, True)
+        (sd, ld), _, _ = work_of(fx, kmax, True, dyn=0)
+        assert (sa, la) == (sd, ld)
+        assert sa >= s1 + sr and la >= sa
+        assert np.array_equal(ca, oracle.scan_count_hdk(sym, fx, offs, lens, kmax))
+        assert np.array_equal(car, oracle.scan_count_hdk(sym, rcx, offs, lens, kmax))
+
+
+def test_checksum_is_additive_over_shards(cuda):
+    """qr_checksum (multi-GPU output verification): the checksum of a whole batch equals the sum
+    mod 2^64 of its shards' checksums with global index offsets, for u64 and u32 outputs, and
+    differs when one word or the index offset changes."""
+    torch = _torch()
+    rng = np.random.default_rng(3)
+    for wb, dt in ((8, np.uint64), (4, np.uint32)):
+        a = rng.integers(0, 2**63, 100003).astype(dt)
+        d = to_dev(a, cuda)
+
+        def cks(lo, hi, i0):
+            acc = torch.zeros(1, dtype=torch.uint64, device=cuda)
+            qr.qr_checksum(d[lo:hi], hi - lo, wb, i0, acc)
+            torch.cuda.synchronize()
+            return int(acc.view(torch.int64).item()) & (2**64 - 1)
+        whole = cks(0, a.size, 0)
+        parts = (cks(0, 777, 0) + cks(777, 50000, 777) + cks(50000, a.size, 50000)) & (2**64 - 1)
+        assert whole == parts
+        assert cks(0, a.size, 1) != whole
+        b = a.copy()
+        b[12345] ^= 1
+        acc = torch.zeros(1, dtype=torch.uint64, device=cuda)
+        qr.qr_checksum(to_dev(b, cuda), b.size, wb, 0, acc)
+        torch.cuda.synchronize()
+        assert int(acc.view(torch.int64).item()) & (2**64 - 1) != whole
+
+
+def test_fm_default_width_dual_tables(cuda):
+    """From n = 2^24 on a B200 the default build keeps an 11-mer table for the exact count and a
+    12-mer table for the approximate-search kernels; every count equals the oracle's and the
+    single-table handles' (explicit widths 11 and 12), and a clone keeps both tables."""
+    torch = _torch()
+    n = (1 << 24) + 5
+    w = gen.dna(411, n, 0)
+    sym = gen.unpack_dna(w, n)
+    fm = qr.qr_fm_build(w, n)
+    assert fm.kmer_k == 11
+    L, m = 32, 300
+    fx = gen.patterns(412, 0, m, L, w, n)
+    offs, lens = np.arange(m, dtype=np.uint64) * L, np.full(m, L, np.uint32)
+    handles = [fm, qr.qr_fm_build(w, n, kmer_k=11), qr.qr_fm_build(w, n, kmer_k=12), qr.qr_fm_clone_to_device(fm, 0)]
+    for kmax in (0, 1, 2):
+        ref = oracle.scan_count_hdk(sym, fx, offs, lens, kmax)
+        for h in handles:
+            d = torch.empty(m, dtype=torch.int32, device=cuda)
+            qr.qr_fm_count_approx(h, to_dev(fx, cuda), None, L, kmax, d, m)
+            torch.cuda.synchronize()
+            assert np.array_equal(to_host(d).view(np.uint32), ref), (kmax, h.kmer_k)

@@ -1,5 +1,6 @@
 """configs[3] QuadFm count, one launch per (BWT layout, fm_step flavour) after one warm-up call —
-the command the ncu captures of the count and seed kernels run (FM_STEPS='16:2,16:3,x2:0,x2:3')."""
+the command the ncu captures of the count and seed kernels run (FM_STEPS='16:2,16:3,x2:0,x2:3';
+an item may add the k-mer width and the packed-seed knob: '16:3:11:0')."""
 import os
 import sys
 
@@ -21,10 +22,16 @@ o = torch.empty(m, dtype=torch.int32, device=dev)
 plan = os.environ.get("FM_STEPS", "16:2,16:3,x2:0,x2:3").split(",")
 fms = {}
 for item in plan:
-    lay, step = item.split(":")
-    if lay not in fms:
-        fms[lay] = qr.qr_fm_build(t, n, bwt_layout=qr.QR_LAYOUT_QUADRANK16 if lay == "16" else qr.QR_LAYOUT_QUADRANK16X2)
-    qr.qr_set_tuning("fm_step", int(step))
-    qr.qr_fm_count(fms[lay], pats, None, L, o, m, st)
+    f = item.split(":")
+    lay, step = f[0], int(f[1])
+    kk = int(f[2]) if len(f) > 2 else None
+    packed = int(f[3]) if len(f) > 3 else 1
+    key = (lay, kk)
+    if key not in fms:
+        fms[key] = qr.qr_fm_build(t, n, bwt_layout=qr.QR_LAYOUT_QUADRANK16 if lay == "16" else qr.QR_LAYOUT_QUADRANK16X2,
+                                  kmer_k=kk)
+    qr.qr_set_tuning("fm_step", step)
+    qr.qr_set_tuning("fm_packed", packed)
+    qr.qr_fm_count(fms[key], pats, None, L, o, m, st)
     torch.cuda.synchronize()
 print("ok")

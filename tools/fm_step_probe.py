@@ -41,7 +41,7 @@ for name, n, kind, m, L, seed in cfgs:
     out = torch.empty(m, dtype=torch.int32, device=dev)
     ref = None
     for lay, lname in ((None, "qr16"), (qr.QR_LAYOUT_QUADRANK16X2, "qr16x2")):
-        fm = qr.qr_fm_build(txt, n, bwt_layout=lay)
+        fm = qr.qr_fm_build(txt, n, bwt_layout=lay, kmer_k=int(os.environ["FM_K"]) if "FM_K" in os.environ else None)
         N = n + 1
         mq = 1 << 26
         q = torch.empty(mq, dtype=torch.uint64, device=dev)
@@ -55,14 +55,17 @@ for name, n, kind, m, L, seed in cfgs:
         gen.queries_dev(seed + 101, N, mq, q, c4)
         ms = t(lambda: qr.qr_rank(fm.bwt, q, c4, o, mq, st))
         rank_gq = mq / ms / 1e6
-        print(json.dumps(dict(cfg=name, layout=lname, bwt_bytes=fm.bwt.line_bytes, ceiling_gq_s=ceil,
+        print(json.dumps(dict(cfg=name, layout=lname, kmer_k=fm.kmer_k, bwt_bytes=fm.bwt.line_bytes, ceiling_gq_s=ceil,
                               rank_gq_s=rank_gq)), flush=True)
         del q, o, c4
         steps = (1, 2, 3) if lay is None else (0, 3)
         refills = [int(x) for x in os.environ.get("FM_REFILL", "8").split(",")]
-        for step, refill in [(s_, r_) for s_ in steps for r_ in (refills if s_ == 3 else [8])]:
+        packs = [int(x) for x in os.environ.get("FM_PACKED", "1").split(",")]
+        for step, refill, packed in [(s_, r_, p_) for s_ in steps for r_ in (refills if s_ == 3 else [8])
+                                     for p_ in (packs if s_ == 3 else [1])]:
             qr.qr_set_tuning("fm_step", step)
             qr.qr_set_tuning("fm_refill", refill)
+            qr.qr_set_tuning("fm_packed", packed)
             work = torch.zeros(2, dtype=torch.uint64, device=dev)
             qr.qr_fm_count_work(fm, pats, None, L, out, m, work, st)
             torch.cuda.synchronize()
@@ -72,7 +75,7 @@ for name, n, kind, m, L, seed in cfgs:
             ok = int(out.to(torch.int64).sum()) == ref and h == ref
             steps_, lines = (int(x) for x in work.cpu())
             lps = lines / ms / 1e6
-            print(json.dumps(dict(cfg=name, layout=lname, step=step, refill=refill, ms=round(ms, 4), gpat_s=round(m / ms / 1e6, 4),
+            print(json.dumps(dict(cfg=name, layout=lname, step=step, refill=refill, packed=packed, ms=round(ms, 4), gpat_s=round(m / ms / 1e6, 4),
                                   lines_per_pattern=lines / m, steps_per_pattern=steps_ / m, glines_s=round(lps, 3),
                                   frac_of_ceiling=round(lps / max(ceil.values()), 4), checksum_ok=ok)), flush=True)
         qr.qr_set_tuning("fm_step", 0)
