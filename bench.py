@@ -181,21 +181,15 @@ class Ctx:
         return int(t.item())
 
     def sum_u64_over_ranks(self, x: int) -> int:
-        """sum mod 2^64 of one u64 per rank (as two 32-bit halves, exact in int64)."""
-        if not self.dist:
-            return x & (2**64 - 1)
-        t = self.torch.tensor([x & 0xFFFFFFFF, x >> 32], dtype=self.torch.int64, device=self._cd())
-        self.dist.all_reduce(t)
-        lo, hi = (int(v) for v in t.cpu())
-        return (lo + (hi << 32)) & (2**64 - 1)
+        """sum mod 2^64 of one u64 per rank (multigpu.reduce_sum_u64)."""
+        from paper_2602_04103_b200.multigpu import reduce_sum_u64
+
+        return reduce_sum_u64(x, self.dist, self._cd())
 
     def gather_u64(self, x: int) -> list:
-        if not self.dist:
-            return [x]
-        t = self.torch.tensor([x & 0xFFFFFFFF, x >> 32], dtype=self.torch.int64, device=self._cd())
-        outs = [self.torch.zeros_like(t) for _ in range(self.world)]
-        self.dist.all_gather(outs, t)
-        return [int(o[0]) + (int(o[1]) << 32) for o in outs]
+        from paper_2602_04103_b200.multigpu import gather_u64
+
+        return gather_u64(x, self.dist, self._cd())
 
     def timed(self, fn, steps: int, warmup: int) -> float:
         """ms per step: W warm-up calls, then EXACTLY K calls bracketed by barrier + synchronize,
@@ -813,6 +807,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--rows", default="all", choices=["all", "headline"])
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--only", default="", help="comma-separated row names (development runs; default: every row)")
     ap.add_argument("--replicate", default="build", choices=["build", "broadcast"],
                     help="multi-GPU: every rank builds from the seeded text, or rank 0 builds and broadcasts")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
@@ -824,6 +819,9 @@ def main():
     import paper_2602_04103_b200 as qr
 
     ctx = Ctx(args)
+    for kv in filter(None, os.environ.get("QR_TUNING", "").split(",")):   # development runs only
+        k, v = kv.split("=")
+        qr.qr_set_tuning(k, int(v))
     K, W = args.steps, max(3, args.warmup)
     peak, peak_src = peaks()
     clocks = Clocks(ctx.gpu)
@@ -834,29 +832,38 @@ def main():
     rows = {}
     if args.rows == "all":
         X2 = qr.QR_LAYOUT_QUADRANK16X2
-        rows["c2_p0.01"] = safe(bench_birank, ctx, 0.01, K, W, with_ceiling=False)
-        rows["birank16_2^35_paper_size"] = safe(bench_birank_size, ctx, 35, K, W)
-        rows["c3_quadrank"] = safe(bench_quadrank, ctx, K, W, peak)
-        rows["c4_quadfm"] = safe(bench_fm, ctx, N4, 0, M4, L4, SEED[4], K, W)
-        rows["c4_quadfm_bwt16x2"] = safe(bench_fm, ctx, N4, 0, M4, L4, SEED[4], K, W, bwt_layout=X2)
-        rows["c5_quadfm"] = safe(bench_fm, ctx, N5, 1, M5, L5, SEED[5], K, W, rank_queries=R5)
-        rows["c5_quadfm_bwt16x2"] = safe(bench_fm, ctx, N5, 1, M5, L5, SEED[5], K, W, bwt_layout=X2)
-        # the paper's FM workload shape: 150-bp reads at 1% substitutions from either
-        # strand, each counted forward and reverse-complemented in one launch, over the configs[4] text
-        rows["c5_reads_150bp_both_strands"] = safe(bench_fm, ctx, N5, 1, 10**7, 150, 55, K, W, strands=2, ptype=2)
-        # ... and at the paper's own genome size (3.1 Gbp block-repeat stand-in for CHM13v2; n+1 < 2^32)
-        rows["genome_scale_reads_3.1Gbp"] = safe(bench_fm, ctx, 3_100_000_000, 1, 10**7, 150, 56, K, W, strands=2,
-                                                 ptype=2)
-        rows["c4_quadfm_approx1"] = safe(bench_fm, ctx, N4, 0, 10**6, L4, SEED[4], K, W, kmax=1)
-        rows["c4_quadfm_approx1_bwt16x2"] = safe(bench_fm, ctx, N4, 0, 10**6, L4, SEED[4], K, W, kmax=1, bwt_layout=X2)
-        rows["c4_quadfm_approx2"] = safe(bench_fm, ctx, N4, 0, 10**6, L4, SEED[4], K, W, kmax=2)
-        rows["c5_reads_150bp_both_strands_approx1"] = safe(bench_fm, ctx, N5, 1, 10**6, 150, 55, K, W, strands=2,
-                                                           kmax=1, ptype=2)
-        rows["c5_reads_150bp_both_strands_approx2"] = safe(bench_fm, ctx, N5, 1, 3 * 10**5, 150, 55, K, W, strands=2,
-                                                           kmax=2, ptype=2)
-        rows["layout_variants"] = safe(bench_variants, ctx, K, W)
-        rows["latency_mode"] = safe(bench_latency, ctx, K, W)
-        rows["c1_small"] = safe(bench_small, ctx, K, W)
+        spec = [
+            ("c2_p0.01", lambda: bench_birank(ctx, 0.01, K, W, with_ceiling=False)),
+            ("birank16_2^35_paper_size", lambda: bench_birank_size(ctx, 35, K, W)),
+            ("c3_quadrank", lambda: bench_quadrank(ctx, K, W, peak)),
+            ("c4_quadfm", lambda: bench_fm(ctx, N4, 0, M4, L4, SEED[4], K, W)),
+            ("c4_quadfm_bwt16x2", lambda: bench_fm(ctx, N4, 0, M4, L4, SEED[4], K, W, bwt_layout=X2)),
+            ("c5_quadfm", lambda: bench_fm(ctx, N5, 1, M5, L5, SEED[5], K, W, rank_queries=R5)),
+            ("c5_quadfm_bwt16x2", lambda: bench_fm(ctx, N5, 1, M5, L5, SEED[5], K, W, bwt_layout=X2)),
+            # the paper's FM workload shape: 150-bp reads at 1% substitutions from either
+            # strand, each counted forward and reverse-complemented in one launch, over the configs[4] text
+            ("c5_reads_150bp_both_strands", lambda: bench_fm(ctx, N5, 1, 10**7, 150, 55, K, W, strands=2, ptype=2)),
+            # ... and at the paper's own genome size (3.1 Gbp block-repeat stand-in for CHM13v2; n+1 < 2^32)
+            ("genome_scale_reads_3.1Gbp", lambda: bench_fm(ctx, 3_100_000_000, 1, 10**7, 150, 56, K, W, strands=2,
+                                                           ptype=2)),
+            ("c4_quadfm_approx1", lambda: bench_fm(ctx, N4, 0, 10**6, L4, SEED[4], K, W, kmax=1)),
+            ("c4_quadfm_approx1_bwt16x2", lambda: bench_fm(ctx, N4, 0, 10**6, L4, SEED[4], K, W, kmax=1,
+                                                           bwt_layout=X2)),
+            ("c4_quadfm_approx2", lambda: bench_fm(ctx, N4, 0, 10**6, L4, SEED[4], K, W, kmax=2)),
+            ("c4_quadfm_approx2_bwt16x2", lambda: bench_fm(ctx, N4, 0, 10**6, L4, SEED[4], K, W, kmax=2,
+                                                           bwt_layout=X2)),
+            ("c5_reads_150bp_both_strands_approx1", lambda: bench_fm(ctx, N5, 1, 10**6, 150, 55, K, W, strands=2,
+                                                                     kmax=1, ptype=2)),
+            ("c5_reads_150bp_both_strands_approx2", lambda: bench_fm(ctx, N5, 1, 3 * 10**5, 150, 55, K, W, strands=2,
+                                                                     kmax=2, ptype=2)),
+            ("layout_variants", lambda: bench_variants(ctx, K, W)),
+            ("latency_mode", lambda: bench_latency(ctx, K, W)),
+            ("c1_small", lambda: bench_small(ctx, K, W)),
+        ]
+        only = set(args.only.split(",")) if args.only else None
+        for name, fn in spec:
+            if only is None or name in only:
+                rows[name] = safe(fn)
     wall_gpu = time.perf_counter() - wall0
     ms = c2["ms"]
     value = c2["gq_s"]

@@ -47,6 +47,10 @@ typedef int32_t qr_status;
                         /* PAPER.md:514-515), or n+1 >= 2^32 for QuadFm (u32 counts)          */
 #define QR_ENOMEM    3  /* device or host allocation failed                                   */
 #define QR_ECUDA     4  /* a CUDA runtime call or kernel launch failed                        */
+#define QR_ERANGE    5  /* opt-in range check (qr_set_tuning("check_range", 1)): some q > n     */
+                        /* (PAPER.md:57 defines rank for 0 <= q <= n); the call still ran —     */
+                        /* memory-safe, those outputs unspecified — and qr_last_error() says   */
+                        /* how many queries were out of range                                  */
 
 typedef struct qr_index qr_index;   /* a rank layout (QR_LAYOUT_*)                             */
 

@@ -19,10 +19,10 @@ import os
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "lib", "libqrank.so")
 
-QR_OK, QR_EINVAL, QR_ECAPACITY, QR_ENOMEM, QR_ECUDA = 0, 1, 2, 3, 4
+QR_OK, QR_EINVAL, QR_ECAPACITY, QR_ENOMEM, QR_ECUDA, QR_ERANGE = 0, 1, 2, 3, 4, 5
 QR_LAYOUT_BIRANK16, QR_LAYOUT_BIRANK64X2, QR_LAYOUT_QUADRANK16, QR_LAYOUT_QUADRANK64, QR_LAYOUT_BIRANK16X2 = 1, 2, 3, 4, 5
 QR_LAYOUT_QUADRANK16X2, QR_LAYOUT_BIRANK32X2 = 6, 7
-_STATUS = {1: "QR_EINVAL", 2: "QR_ECAPACITY", 3: "QR_ENOMEM", 4: "QR_ECUDA"}
+_STATUS = {1: "QR_EINVAL", 2: "QR_ECAPACITY", 3: "QR_ENOMEM", 4: "QR_ECUDA", 5: "QR_ERANGE"}
 
 # every symbol include/qrank.h declares (tests check the .so exports all of them)
 EXPORTS = (

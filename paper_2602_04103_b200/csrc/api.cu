@@ -28,6 +28,7 @@ int g_fm_seed = 0;              // FM seed pre-pass (dynamic order only): 0 auto
 int g_fm_smem = 1;              // FM superblock words from shared memory: 0 off, 1 auto, 2 packed table whenever it fits
 int g_fm_refill = 8;            // L2-resident count kernel: refill a warp's lanes once this many are idle
 int g_fm_packed = 1;            // L2-resident count kernel: packed post-seed symbols for short fixed-length batches
+int g_check_range = 0;          // 1: qr_rank / qr_rank_all4 count q > n and return QR_ERANGE (synchronous)
 int g_fm_lean = 0;              // FM step flavour: 0 auto (by L2 residency), 1 de-duplicating, 2 lean, 3 one line per iteration
 int g_index64 = 0;              // 1: force the 64-bit line-index path (tests the n >= 2^36/2^37 code on small n)
 int g_rank_smem = 1;            // superblock words from cluster shared memory: 0 never, 1 large batches, 2 always
@@ -405,6 +406,9 @@ QR_EXPORT qr_status qr_set_tuning(const char* key, int64_t value) {
   } else if (!strcmp(key, "fm_packed")) {
     if (value != 0 && value != 1) return fail(QR_EINVAL, "fm_packed must be 0 or 1");
     g_fm_packed = (int)value;
+  } else if (!strcmp(key, "check_range")) {
+    if (value != 0 && value != 1) return fail(QR_EINVAL, "check_range must be 0 or 1");
+    g_check_range = (int)value;
   } else if (!strcmp(key, "fm_step")) {
     if (value < 0 || value > 3) return fail(QR_EINVAL, "fm_step must be 0 (auto), 1, 2 or 3");
     g_fm_lean = (int)value;
@@ -522,6 +526,34 @@ QR_EXPORT qr_status qr_layout(const qr_index* h, int* layout) {
   return QR_OK;
 }
 
+// The opt-in range check (knob check_range, QR_ERANGE): every chunk's queries are counted on
+// the device (q > n) on the stream that ranks them; the call then synchronises and reports.
+struct RangeCheck {
+  unsigned long long* d = nullptr;
+  bool on = false;
+  qr_status begin(cudaStream_t st) {
+    on = g_check_range != 0;
+    if (!on) return QR_OK;
+    cudaError_t e = cudaMallocAsync((void**)&d, 8, st);
+    if (!e) e = cudaMemsetAsync(d, 0, 8, st);
+    return e ? cuda_fail(e, "range check alloc") : QR_OK;
+  }
+  cudaError_t count(const uint64_t* dq, uint64_t cnt, uint64_t n, int device, cudaStream_t s) {
+    return on ? launch_count_gt(dq, cnt, n, d, device, s) : cudaSuccess;
+  }
+  qr_status end(qr_status s, cudaStream_t st, const char* who) {
+    if (!on) return s;
+    unsigned long long h = 0;
+    cudaError_t e = cudaMemcpyAsync(&h, d, 8, cudaMemcpyDeviceToHost, st);
+    if (!e) e = cudaStreamSynchronize(st);
+    cudaFreeAsync(d, st);
+    if (s != QR_OK) return s;
+    if (e) return cuda_fail(e, "range check");
+    if (h) return fail(QR_ERANGE, "%s: %llu of the queries are > n (PAPER.md:57: 0 <= q <= n)", who, h);
+    return QR_OK;
+  }
+};
+
 QR_EXPORT qr_status qr_rank(const qr_index* h, const uint64_t* q, const uint8_t* c, uint64_t* out, uint64_t m,
                             void* stream) {
   if (!h) return fail(QR_EINVAL, "qr_rank: null handle");
@@ -536,16 +568,22 @@ QR_EXPORT qr_status qr_rank(const qr_index* h, const uint64_t* q, const uint8_t*
   };
   int sp = classify({q, c, out}, h->device);
   if (sp < 0) return fail(QR_EINVAL, "qr_rank: q, c, out must all be device pointers on device %d or all host", h->device);
+  RangeCheck rc;
+  qr_status s0 = rc.begin(st);
+  if (s0 != QR_OK) return s0;
   if (sp == 1) {
-    cudaError_t e = launch(q, c, out, m, st);
-    return e ? cuda_fail(e, "qr_rank launch") : QR_OK;
+    cudaError_t e = rc.count(q, m, h->n, h->device, st);
+    if (!e) e = launch(q, c, out, m, st);
+    return rc.end(e ? cuda_fail(e, "qr_rank launch") : QR_OK, st, "qr_rank");
   }
   std::vector<StageArray> arr = {{q, nullptr, 8}, {nullptr, out, 8}};
   if (c) arr.push_back({c, nullptr, 1});
-  return run_staged(h->device, st, m, arr, [&](const std::vector<void*>& d, uint64_t cnt, cudaStream_t s) -> qr_status {
-    cudaError_t e = launch((const uint64_t*)d[0], c ? (const uint8_t*)d[2] : nullptr, (uint64_t*)d[1], cnt, s);
+  qr_status s1 = run_staged(h->device, st, m, arr, [&](const std::vector<void*>& d, uint64_t cnt, cudaStream_t s) -> qr_status {
+    cudaError_t e = rc.count((const uint64_t*)d[0], cnt, h->n, h->device, s);
+    if (!e) e = launch((const uint64_t*)d[0], c ? (const uint8_t*)d[2] : nullptr, (uint64_t*)d[1], cnt, s);
     return e ? cuda_fail(e, "qr_rank launch") : QR_OK;
   });
+  return rc.end(s1, st, "qr_rank");
 }
 
 QR_EXPORT qr_status qr_rank_chain(const qr_index* h, const uint64_t* q, const uint8_t* c, uint64_t* out, uint64_t m,
@@ -572,15 +610,21 @@ QR_EXPORT qr_status qr_rank_all4(const qr_index* h, const uint64_t* q, uint64_t*
   auto launch4 = [&](const uint64_t* dq, uint64_t* d4, uint64_t cnt, cudaStream_t s) -> cudaError_t {
     return is_variant(h) ? launch_variant(h, dq, nullptr, d4, cnt, 1, s) : launch_quadrank_all4(h, dq, d4, cnt, s);
   };
+  RangeCheck rc;
+  qr_status s0 = rc.begin(st);
+  if (s0 != QR_OK) return s0;
   if (sp == 1) {
-    cudaError_t e = launch4(q, out4, m, st);
-    return e ? cuda_fail(e, "qr_rank_all4 launch") : QR_OK;
+    cudaError_t e = rc.count(q, m, h->n, h->device, st);
+    if (!e) e = launch4(q, out4, m, st);
+    return rc.end(e ? cuda_fail(e, "qr_rank_all4 launch") : QR_OK, st, "qr_rank_all4");
   }
   std::vector<StageArray> arr = {{q, nullptr, 8}, {nullptr, out4, 32}};
-  return run_staged(h->device, st, m, arr, [&](const std::vector<void*>& d, uint64_t cnt, cudaStream_t s) -> qr_status {
-    cudaError_t e = launch4((const uint64_t*)d[0], (uint64_t*)d[1], cnt, s);
+  qr_status s1 = run_staged(h->device, st, m, arr, [&](const std::vector<void*>& d, uint64_t cnt, cudaStream_t s) -> qr_status {
+    cudaError_t e = rc.count((const uint64_t*)d[0], cnt, h->n, h->device, s);
+    if (!e) e = launch4((const uint64_t*)d[0], (uint64_t*)d[1], cnt, s);
     return e ? cuda_fail(e, "qr_rank_all4 launch") : QR_OK;
   });
+  return rc.end(s1, st, "qr_rank_all4");
 }
 
 QR_EXPORT qr_status qr_gather_ceiling(const qr_index* h, const uint64_t* q, uint64_t* out, uint64_t m, int mode,

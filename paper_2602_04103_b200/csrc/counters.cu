@@ -100,6 +100,21 @@ __global__ void k_checksum(const T* __restrict__ d, uint64_t n, uint64_t i0, uns
   if ((threadIdx.x & 31) == 0 && acc) atomicAdd(sum, (unsigned long long)acc);
 }
 
+// ---- opt-in range check (QR_ERANGE) ----------------------------------------------------------
+__global__ void k_count_gt(const uint64_t* __restrict__ q, uint64_t m, uint64_t n, unsigned long long* __restrict__ cnt) {
+  uint32_t c = 0;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m; i += (uint64_t)gridDim.x * blockDim.x)
+    c += q[i] > n ? 1u : 0u;
+  c = __reduce_add_sync(0xffffffffu, c);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(cnt, (unsigned long long)c);
+}
+cudaError_t launch_count_gt(const uint64_t* q, uint64_t m, uint64_t n, unsigned long long* cnt, int device,
+                            cudaStream_t st) {
+  if (m == 0) return cudaSuccess;
+  k_count_gt<<<grid_stride_blocks(m, 256, sm_count(device), 8), 256, 0, st>>>(q, m, n, cnt);
+  return cudaGetLastError();
+}
+
 }  // namespace qr
 
 using namespace qr;

@@ -1058,14 +1058,21 @@ __device__ __forceinline__ void fm_occ4(const FmParams& F, uint32_t x, uint32_t 
   j = j > (uint32_t)F.last_line ? (uint32_t)F.last_line : j;
   const uint32_t p = 32u + x - j * (uint32_t)QD_B;
   const uint4* L = F.lines + 4 * (uint64_t)j;
-  uint64_t a[4], b[4] = {0, 0, 0, 0};
-  ld_sector(L, a[0], a[1], a[2], a[3]);
-  if (p >= 128) ld_sector(L + 2, b[0], b[1], b[2], b[3]);
-  const uint4 sv = __ldg(reinterpret_cast<const uint4*>(F.super) + (j >> QD_SB_LOG));
   const bool right = p >= 128;
+  // the counted half's sector, and (right of the anchor) the 16 B of sector 0 holding the deltas:
+  // 6 live u64 instead of both sectors' 8 (the backtracking kernels are register-bound)
+  uint64_t w[4];
+  ld_sector(L + (right ? 2 : 0), w[0], w[1], w[2], w[3]);
+  uint64_t a[2];
+  if (right) {
+    const ulonglong2 dv = __ldg(reinterpret_cast<const ulonglong2*>(L));
+    a[0] = dv.x; a[1] = dv.y;
+  } else {
+    a[0] = w[0]; a[1] = w[1];
+  }
+  const uint4 sv = __ldg(reinterpret_cast<const uint4*>(F.super) + (j >> QD_SB_LOG));
   const int xx = (int)(p & 127u);
   const uint64_t inv = right ? 0ull : ~0ull;
-  const uint64_t* w = right ? b : a;
   uint32_t nl = 0, nh = 0, nt = 0;
   uint64_t mk[2];
   qd_masks((uint32_t)xx, mk[0], mk[1]);
@@ -1253,43 +1260,60 @@ __global__ void __launch_bounds__(256, QR_APPROX1_MINB) k_fm_approx1(FmParams F,
 // by node; every K-mer within distance KMAX of the pattern's last K symbols is looked up in the
 // k-mer table instead (1 + 3K + 9 C(K,2) [+ 27 C(K,3)] lookups), and the search continues from
 // each non-empty interval with the substitutions it has left.
+// The search frames live in shared memory, word-major with a stride of the CTA size (256), so a
+// warp's accesses to one field are 32 consecutive words (no bank conflict): indexed by the frame
+// number at run time they would otherwise sit in the local-memory stack (112 B per thread at
+// k = 2) and compete with the BWT gathers for the L1, and hold ~14 registers.
+template <int KMAX>
+struct FmFrames {
+  static constexpr int WORDS = 4 * (KMAX + 1) + 8 * KMAX;   // lo, hi, pos, next branch per frame; children
+  uint32_t* b;
+  __device__ __forceinline__ explicit FmFrames(uint32_t* smem) : b(smem + threadIdx.x) {}
+  __device__ __forceinline__ uint32_t& lo(int f) { return b[(0 * (KMAX + 1) + f) * 256]; }
+  __device__ __forceinline__ uint32_t& hi(int f) { return b[(1 * (KMAX + 1) + f) * 256]; }
+  __device__ __forceinline__ uint32_t& pos(int f) { return b[(2 * (KMAX + 1) + f) * 256]; }
+  __device__ __forceinline__ uint32_t& nd(int f) { return b[(3 * (KMAX + 1) + f) * 256]; }
+  __device__ __forceinline__ uint32_t& clo(int f, int c) { return b[(4 * (KMAX + 1) + 4 * f + c) * 256]; }
+  __device__ __forceinline__ uint32_t& chi(int f, int c) { return b[(4 * (KMAX + 1) + 4 * KMAX + 4 * f + c) * 256]; }
+};
+
 template <int BW, int KMAX, bool WORK, class W>
 __device__ __forceinline__ uint64_t fm_backtrack(const FmParams& F, W& P, const uint32_t (&Cs)[4],
-                                                 uint32_t lo, uint32_t hi, uint32_t pos, int f0, FmWork& wk) {
-  constexpr uint32_t UNX = 8;   // not 4: a frame whose branches are all tried has fd = 4
-  uint32_t flo[KMAX + 1], fhi[KMAX + 1], fpos[KMAX + 1], fd[KMAX + 1];   // fd: next branch symbol, UNX = unexpanded
-  uint32_t clo[KMAX][4], chi[KMAX][4];                                   // children of frames 0 .. KMAX-1
+                                                 uint32_t lo, uint32_t hi, uint32_t pos, int f0, FmWork& wk,
+                                                 FmFrames<KMAX>& fr) {
+  constexpr uint32_t UNX = 8;   // not 4: a frame whose branches are all tried has nd = 4
   uint64_t total = 0;
   int f = f0;
-  flo[f] = lo; fhi[f] = hi; fpos[f] = pos; fd[f] = UNX;
+  fr.lo(f) = lo; fr.hi(f) = hi; fr.pos(f) = pos; fr.nd(f) = UNX;
   while (f >= f0) {
-    if (fd[f] == UNX) {
-      if (flo[f] >= fhi[f]) { --f; continue; }
-      if (fpos[f] == 0) { total += fhi[f] - flo[f]; --f; continue; }
+    const uint32_t flo = fr.lo(f), fhi = fr.hi(f), fpos = fr.pos(f);
+    uint32_t d = fr.nd(f);
+    if (d == UNX) {
+      if (flo >= fhi) { --f; continue; }
+      if (fpos == 0) { total += fhi - flo; --f; continue; }
       if (f == KMAX) {                                   // no substitution left: exact search
-        total += fm_continue<BW, WORK>(F, P, (int64_t)fpos[f] - 1, flo[f], fhi[f], wk);
+        total += fm_continue<BW, WORK>(F, P, (int64_t)fpos - 1, flo, fhi, wk);
         --f;
         continue;
       }
       uint32_t ol[4], oh[4];
-      fm_occ4_pair<BW, WORK>(F, flo[f], fhi[f], ol, oh, wk);
+      fm_occ4_pair<BW, WORK>(F, flo, fhi, ol, oh, wk);
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
-        clo[f][c] = Cs[c] + ol[c];
-        chi[f][c] = Cs[c] + oh[c];
+        fr.clo(f, c) = Cs[c] + ol[c];
+        fr.chi(f, c) = Cs[c] + oh[c];
       }
-      fd[f] = 0;
+      d = 0;
     }
-    const uint32_t pc = P.at((int64_t)fpos[f] - 1);
-    uint32_t d = fd[f];
-    while (d < 4 && (d == pc || clo[f][d] >= chi[f][d])) ++d;
+    const uint32_t pc = P.at((int64_t)fpos - 1);
+    while (d < 4 && (d == pc || fr.clo(f, d) >= fr.chi(f, d))) ++d;
     if (d < 4) {                                         // descend into the substitution d
-      fd[f] = d + 1;
-      flo[f + 1] = clo[f][d]; fhi[f + 1] = chi[f][d]; fpos[f + 1] = fpos[f] - 1; fd[f + 1] = UNX;
+      fr.nd(f) = d + 1;
+      fr.lo(f + 1) = fr.clo(f, d); fr.hi(f + 1) = fr.chi(f, d); fr.pos(f + 1) = fpos - 1; fr.nd(f + 1) = UNX;
       ++f;
       continue;
     }
-    flo[f] = clo[f][pc]; fhi[f] = chi[f][pc]; fpos[f] -= 1; fd[f] = UNX;   // step on the pattern's symbol
+    fr.lo(f) = fr.clo(f, pc); fr.hi(f) = fr.chi(f, pc); fr.pos(f) = fpos - 1; fr.nd(f) = UNX;   // step on the pattern's symbol
   }
   return total;
 }
@@ -1310,6 +1334,8 @@ __global__ void QR_APPROX_LB k_fm_approxk(FmParams F, const uint8_t* __restrict_
   FmWork wk;
   if (BW == 1) x2_masks_init();
   else qd_masks_init();
+  extern __shared__ uint32_t fm_frames_smem[];
+  FmFrames<KMAX> fr(fm_frames_smem);
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   const uint4 C4 = __ldg(reinterpret_cast<const uint4*>(F.Ct));
   const uint32_t Cs[4] = {C4.x, C4.y, C4.z, C4.w};
@@ -1330,7 +1356,7 @@ __global__ void QR_APPROX_LB k_fm_approxk(FmParams F, const uint8_t* __restrict_
       auto seed = [&](uint32_t key, int mm) {
         const uint2 iv = __ldg(F.kmer + key);
         if (WORK) { wk.ws += 1; wk.wl += 1; }
-        if (iv.x < iv.y) total += fm_backtrack<BW, KMAX, WORK>(F, P, Cs, iv.x, iv.y, pos, mm, wk);
+        if (iv.x < iv.y) total += fm_backtrack<BW, KMAX, WORK>(F, P, Cs, iv.x, iv.y, pos, mm, wk, fr);
       };
       // the seeds with all KMAX substitutions inside the K-mer have none left: their three
       // variants at the last substituted position are looked up together and continue as one
@@ -1361,7 +1387,7 @@ __global__ void QR_APPROX_LB k_fm_approxk(FmParams F, const uint8_t* __restrict_
           }
         }
     } else {
-      total = fm_backtrack<BW, KMAX, WORK>(F, P, Cs, 0u, (uint32_t)F.N, len, 0, wk);
+      total = fm_backtrack<BW, KMAX, WORK>(F, P, Cs, 0u, (uint32_t)F.N, len, 0, wk, fr);
     }
     if (STRANDS == 2 && rc) out_rc[pi] = (uint32_t)total;
     else out[pi] = (uint32_t)total;
@@ -1586,12 +1612,15 @@ static cudaError_t launch_approx_s(const qr_fm* fm, unsigned g, cudaStream_t st,
   auto kern = kmax == 1 ? (F.bw ? k_fm_approx1<FIXED, 1, STRANDS, WORK> : k_fm_approx1<FIXED, 0, STRANDS, WORK>)
             : kmax == 2 ? (F.bw ? k_fm_approxk<FIXED, 1, 2, STRANDS, WORK> : k_fm_approxk<FIXED, 0, 2, STRANDS, WORK>)
                         : (F.bw ? k_fm_approxk<FIXED, 1, 3, STRANDS, WORK> : k_fm_approxk<FIXED, 0, 3, STRANDS, WORK>);
+  // k >= 2: the backtracking frames in shared memory (FmFrames), 256 threads x WORDS u32
+  const size_t smem = kmax == 2 ? FmFrames<2>::WORDS * 256 * 4 : kmax == 3 ? FmFrames<3>::WORDS * 256 * 4 : 0;
+  smem_limit_raise((const void*)kern, smem, cur_device());
   if (!g_fm_dyn) {
-    kern<<<g, 256, 0, st>>>(F, pat, offs, lens, fixed_len, out, out_rc, m, nullptr, work);
+    kern<<<g, 256, smem, st>>>(F, pat, offs, lens, fixed_len, out, out_rc, m, nullptr, work);
     return cudaGetLastError();
   }
   int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0) != cudaSuccess || per_sm <= 0) {
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem) != cudaSuccess || per_sm <= 0) {
     cudaGetLastError();
     per_sm = 1;
   }
@@ -1600,7 +1629,7 @@ static cudaError_t launch_approx_s(const qr_fm* fm, unsigned g, cudaStream_t st,
   unsigned long long* ctr = nullptr;
   cudaError_t e = lease.acquire(fm->bwt->device, st, &ctr);
   if (e) return e;
-  kern<<<res < g ? res : g, 256, 0, st>>>(F, pat, offs, lens, fixed_len, out, out_rc, m, ctr, work);
+  kern<<<res < g ? res : g, 256, smem, st>>>(F, pat, offs, lens, fixed_len, out, out_rc, m, ctr, work);
   e = cudaGetLastError();
   cudaError_t e2 = lease.release(st);
   return e ? e : e2;

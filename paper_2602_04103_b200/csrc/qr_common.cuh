@@ -72,6 +72,9 @@ int pointer_space(const void* p, int device);
 
 // SM count of a device (cached)
 int sm_count(int device);
+// number of q[i] > n into *cnt (device u64, accumulated): the opt-in range check (QR_ERANGE)
+cudaError_t launch_count_gt(const uint64_t* q, uint64_t m, uint64_t n, unsigned long long* cnt, int device,
+                            cudaStream_t st);
 // Raise a kernel's dynamic shared-memory limit on `device` to at least `bytes` (process-wide,
 // mutex-guarded, never lowers it: a later launch with a smaller size must not undercut a
 // concurrent or cached launch that needs more).  Returns the attribute call's error, if any.

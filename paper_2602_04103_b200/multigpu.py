@@ -44,6 +44,33 @@ def reduce_sum(x: int, dist=None, device=None) -> int:
     return int(t.item())
 
 
+def reduce_sum_u64(x: int, dist=None, device=None) -> int:
+    """sum mod 2^64 of one u64 per rank (an output checksum): all_reduce of the
+    two 32-bit halves in int64, which cannot overflow for up to 2^31 ranks, then recombined."""
+    x &= (1 << 64) - 1
+    if dist is None or not dist.is_initialized() or dist.get_world_size() == 1:
+        return x
+    import torch
+
+    t = torch.tensor([x & 0xFFFFFFFF, x >> 32], dtype=torch.int64, device=device)
+    dist.all_reduce(t)
+    lo, hi = (int(v) for v in t.cpu())
+    return (lo + (hi << 32)) & ((1 << 64) - 1)
+
+
+def gather_u64(x: int, dist=None, device=None) -> list:
+    """every rank's u64 (e.g. its shard checksum), in rank order, on every rank."""
+    x &= (1 << 64) - 1
+    if dist is None or not dist.is_initialized() or dist.get_world_size() == 1:
+        return [x]
+    import torch
+
+    t = torch.tensor([x & 0xFFFFFFFF, x >> 32], dtype=torch.int64, device=device)
+    outs = [torch.zeros_like(t) for _ in range(dist.get_world_size())]
+    dist.all_gather(outs, t)
+    return [int(o[0]) + (int(o[1]) << 32) for o in outs]
+
+
 def throughput(units_all_ranks: int, max_ms: float) -> float:
     """whole-job units per second: all ranks' units over the slowest rank's time."""
     return units_all_ranks / (max_ms * 1e-3)

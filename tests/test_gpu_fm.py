@@ -362,33 +362,6 @@ def test_fm_count_approx_one_mismatch(cuda, n, kind, dyn, fm_dyn_reset):
         qr.qr_fm_count_approx(fm, fx, None, L, 4, h, m)
 
 
-def test_cli_fm_count(cuda, tmp_path):
-    """End-to-end CLI on real-format files: FASTA genome, FASTQ reads, both strands."""
-    from paper_2602_04103_b200 import cli, io
-
-    n = 20000
-    sym = gen.unpack_dna(gen.dna(91, n), n)
-    fa = tmp_path / "g.fa"
-    fa.write_text(">g\n" + "\n".join(io.decode(sym[i:i + 70]) for i in range(0, n, 70)) + "\n")
-    rng = np.random.default_rng(3)
-    reads = [sym[a:a + 30].copy() for a in rng.integers(0, n - 30, 20)] + [rng.integers(0, 4, 25).astype(np.uint8)]
-    fq = tmp_path / "r.fq"
-    fq.write_text("".join(f"@r{i}\n{io.decode(r)}\n+\n{'I' * len(r)}\n" for i, r in enumerate(reads)))
-    out = tmp_path / "c.tsv"
-    assert cli.main(["fm-count", "--fasta", str(fa), "--fastq", str(fq), "--both-strands", "--out", str(out)]) == 0
-    rows = [tuple(int(x) for x in line.split("\t")) for line in out.read_text().splitlines()]
-    cat, off, lens = oracle.pack_patterns(reads)
-    rcat, roff, rlens = oracle.pack_patterns([revcomp(r) for r in reads])
-    assert [r[1] for r in rows] == list(oracle.scan_count(sym, cat, off, lens))
-    assert [r[2] for r in rows] == list(oracle.scan_count(sym, rcat, roff, rlens))
-    # both strands within 2 substitutions (one launch, qr_fm_count_approx_both)
-    assert cli.main(["fm-count", "--fasta", str(fa), "--fastq", str(fq), "--both-strands", "--max-mismatches", "2",
-                     "--out", str(out)]) == 0
-    rows = [tuple(int(x) for x in line.split("\t")) for line in out.read_text().splitlines()]
-    assert [r[1] for r in rows] == list(oracle.scan_count_hdk(sym, cat, off, lens, 2))
-    assert [r[2] for r in rows] == list(oracle.scan_count_hdk(sym, rcat, roff, rlens, 2))
-
-
 @pytest.mark.parametrize("k", [0, 1, 5, 8, 10, 12, 13, 14])
 def test_fm_kmer_width_does_not_change_counts(cuda, k):
     """Seeded vs unseeded counts are identical for every table width, incl. no table,
@@ -848,3 +821,32 @@ def test_fm_default_width_dual_tables(cuda):
             qr.qr_fm_count_approx(h, to_dev(fx, cuda), None, L, kmax, d, m)
             torch.cuda.synchronize()
             assert np.array_equal(to_host(d).view(np.uint32), ref), (kmax, h.kmer_k)
+
+
+@pytest.mark.parametrize("bwt_layout", [None, qr.QR_LAYOUT_QUADRANK16X2])
+@pytest.mark.parametrize("dyn", [0, 1])
+@pytest.mark.parametrize("n,kind", [(1, 0), (57, 0), (5000, 0), (60000, 1), (300000, 0)])
+def test_fm_approx_all_k_both_strands(cuda, bwt_layout, dyn, n, kind):
+    """Approximate search for k = 1, 2, 3 on both strands in one launch, variable lengths (empty,
+    shorter than the table width, longer), static and dynamic order, against the oracle's direct
+    scan (the k >= 2 kernel keeps its backtracking frames in shared memory, FmFrames)."""
+    torch = _torch()
+    w = gen.dna(900 + n, n, kind)
+    sym = gen.unpack_dna(w, n)
+    fm = qr.qr_fm_build(w, n, bwt_layout=bwt_layout)
+    rng = np.random.default_rng(n)
+    pats = mixed_patterns(rng, sym, 160)
+    cat, off, lens = oracle.pack_patterns(pats)
+    rc = [revcomp(p) for p in pats]
+    rcat, roff, rlens = oracle.pack_patterns(rc)
+    qr.qr_set_tuning("fm_dyn", dyn)
+    try:
+        for kmax in (1, 2, 3):
+            df = torch.empty(lens.size, dtype=torch.int32, device=cuda)
+            dr = torch.empty(lens.size, dtype=torch.int32, device=cuda)
+            qr.qr_fm_count_approx_both(fm, to_dev(cat, cuda), to_dev(lens, cuda), 0, kmax, df, dr, lens.size)
+            torch.cuda.synchronize()
+            assert np.array_equal(to_host(df).view(np.uint32), oracle.scan_count_hdk(sym, cat, off, lens, kmax)), kmax
+            assert np.array_equal(to_host(dr).view(np.uint32), oracle.scan_count_hdk(sym, rcat, roff, rlens, kmax)), kmax
+    finally:
+        qr.qr_set_tuning("fm_dyn", 1)

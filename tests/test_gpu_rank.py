@@ -473,3 +473,55 @@ def test_gather_ceiling_rank4_shape(cuda):
     with pytest.raises(qr.QrError):                       # QuadRank16 only
         hb = qr.qr_birank_build(gen.bits(3, 5000), 5000)
         qr.qr_gather_ceiling(hb, dq[:10], torch.zeros((10, 4), dtype=torch.uint64, device=cuda), 4)
+
+
+@pytest.mark.parametrize("space", ["device", "host"])
+def test_opt_in_range_check(cuda, space):
+    """check_range = 1 (reading R12: rank is defined for 0 <= q <= n): qr_rank and
+    qr_rank_all4 count the queries with q > n, still answer the valid ones exactly, and return
+    QR_ERANGE naming the count; q = n is in range; off (default) the same call returns QR_OK."""
+    torch = _torch()
+    n = 3 * S + 17
+    w = gen.bits(7, n)
+    h = qr.qr_birank_build(w, n)
+    n4 = 2 * S4 + 5
+    t = gen.dna(8, n4)
+    h4 = qr.qr_quadrank_build(t, n4)
+    q = gen.queries(10, n, 100000)
+    q[[5, 77, 99999]] = [n + 1, 2 * n, 1 << 50]
+    q[6] = n
+    bad = np.flatnonzero(q > n)
+    good = np.setdiff1d(np.arange(q.size), bad)
+    q4 = gen.queries(11, n4, 50000)
+    q4[[0, 1]] = [n4 + 1, n4 + 224]
+    c4 = np.zeros(q4.size, np.uint8)
+    dev = space == "device"
+    qq, q44 = (to_dev(q, cuda), to_dev(q4, cuda)) if dev else (q, q4)
+    out = torch.empty(q.size, dtype=torch.uint64, device=cuda) if dev else np.zeros(q.size, np.uint64)
+    o4 = torch.empty((q4.size, 4), dtype=torch.uint64, device=cuda) if dev else np.zeros((q4.size, 4), np.uint64)
+    cc = to_dev(c4, cuda) if dev else c4
+    o1 = torch.empty(q4.size, dtype=torch.uint64, device=cuda) if dev else np.zeros(q4.size, np.uint64)
+    qr.qr_set_tuning("check_range", 1)
+    try:
+        with pytest.raises(qr.QrError) as e:
+            qr.qr_rank(h, qq, None, out)
+        assert e.value.status == qr.QR_ERANGE and "3 of the queries" in str(e.value)
+        with pytest.raises(qr.QrError) as e:
+            qr.qr_rank_all4(h4, q44, o4)
+        assert e.value.status == qr.QR_ERANGE and "2 of the queries" in str(e.value)
+        with pytest.raises(qr.QrError) as e:
+            qr.qr_rank(h4, q44, cc, o1)
+        assert e.value.status == qr.QR_ERANGE
+        qok = q[good].copy()
+        ook = np.zeros(qok.size, np.uint64)
+        qr.qr_rank(h, qok, None, ook)                          # all in range (incl. q = n): QR_OK
+    finally:
+        qr.qr_set_tuning("check_range", 0)
+    torch.cuda.synchronize()
+    res = to_host(out) if dev else out
+    assert np.array_equal(res[good], oracle.BitsOracle(w, n).rank(q[good]))
+    assert np.array_equal(ook, oracle.BitsOracle(w, n).rank(qok))
+    r4 = to_host(o4) if dev else o4
+    assert np.array_equal(r4[2:], oracle.DnaOracle(t, n4).rank_all4(q4[2:]))
+    qr.qr_rank(h, qq, None, out)                               # default: no check, QR_OK
+    qr.qr_sync()

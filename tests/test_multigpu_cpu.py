@@ -34,7 +34,11 @@ def _worker(rank, world, port, q):
         mx = mg.reduce_max(t_ms, dist)
         tot = mg.reduce_sum(m, dist)
         chk = mg.reduce_sum(int(np.bitwise_xor.reduce(out) & 0x7FFFFFFF), dist)
-        q.put((rank, i0, m, qs.tobytes(), out.tobytes(), mx, tot, chk))
+        # u64 checksums near 2^64 wrap exactly; every rank sees every rank's value in order
+        big = (1 << 64) - 1 - rank
+        c64 = mg.reduce_sum_u64(big, dist)
+        allv = mg.gather_u64(big * 3 + rank, dist)
+        q.put((rank, i0, m, qs.tobytes(), out.tobytes(), mx, tot, chk, c64, allv))
     finally:
         dist.destroy_process_group()
 
@@ -72,6 +76,10 @@ def test_two_rank_gloo_shard_invariance():
     assert all(r[5] == 11.0 for r in res)                       # max over ranks
     assert all(r[6] == total for r in res)
     assert res[0][7] == res[1][7]
+    M = (1 << 64) - 1
+    assert all(r[8] == (2 * M - 1) % (1 << 64) for r in res)
+    assert all(r[9] == [((M - k) * 3 + k) % (1 << 64) for k in range(2)] for r in res)
+    assert mg.reduce_sum_u64(M + 5) == 4 and mg.gather_u64(7) == [7]      # one rank: identity (mod 2^64)
 
 
 def test_parse_cpulist():
