@@ -47,10 +47,17 @@ int g_stage_slots = 3;                 // device buffers / internal streams of t
 cudaError_t smem_limit_raise(const void* kern, size_t bytes, int device) {
   static std::mutex mu;
   static std::map<std::pair<const void*, int>, size_t> limit;
-  if (bytes <= 48 * 1024) return cudaSuccess;          // the default limit
+  if (bytes == 0) return cudaSuccess;
   std::lock_guard<std::mutex> g(mu);
   size_t& lim = limit[std::make_pair(kern, device)];
   if (bytes <= lim) return cudaSuccess;
+  // without the opt-in, dynamic + static shared memory must stay within 48 KB
+  cudaFuncAttributes fa;
+  if (cudaFuncGetAttributes(&fa, kern) == cudaSuccess && bytes + fa.sharedSizeBytes <= 48 * 1024) {
+    lim = bytes;
+    return cudaSuccess;
+  }
+  cudaGetLastError();
   int prev = -1;
   cudaGetDevice(&prev);
   if (prev != device) cudaSetDevice(device);

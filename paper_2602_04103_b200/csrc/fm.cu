@@ -16,6 +16,8 @@
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 
+#include <type_traits>
+
 #include "qr_common.cuh"
 
 namespace qr {
@@ -933,7 +935,8 @@ __global__ void __launch_bounds__(256, QR_FM_MINB) k_fm_count_l2(FmParams F, con
   const uint32_t lane = threadIdx.x & 31u;
   uint64_t ti = 0;
   uint32_t lo = 0, hi = 0, len = 0, rc = 0, pend = 0;
-  int64_t k = -1;
+  // packed seeds: patterns of <= 46 symbols, so the step counter fits 32 bits (no 64-bit compares)
+  typename std::conditional<PACKED, int32_t, int64_t>::type k = -1;
   bool has = false;
   PatWindow P;
   P.reset(pat);
@@ -972,7 +975,7 @@ __global__ void __launch_bounds__(256, QR_FM_MINB) k_fm_count_l2(FmParams F, con
             lo = iv.x;
             hi = iv.y;
           }
-          k = (int64_t)len - 1 - ((F.K && len >= (uint32_t)F.K) ? F.K : 0);
+          k = (decltype(k))len - 1 - ((F.K && len >= (uint32_t)F.K) ? F.K : 0);
           pend = 0;
           has = true;
         }
