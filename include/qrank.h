@@ -138,7 +138,8 @@ qr_status qr_fm_build(const uint64_t* text2b, uint64_t n, const uint32_t* sa_or_
  * starts from [0, n+1)).  qr_fm_build picks the paper's 8 for n < 2^20, 10 for
  * n < 2^24 and, above, 11 when the BWT's rank layout plus the 32 MiB 11-mer table fit in 60% of
  * the device's L2 (seeds then come from L2), else 12 (on B200 the wider table
- * replaces more backward steps by one lookup).  The table holds 4^kmer_k intervals (8 B each: 512 KiB at 8, 8 MiB at 10,
+ * replaces more backward steps by one lookup); from n = 2^24 the approximate-search calls use a
+ * 14-wide table of their own (2 GiB), built on the first such call (synchronous on its stream).  The table holds 4^kmer_k intervals (8 B each: 512 KiB at 8, 8 MiB at 10,
  * 128 MiB at 12, 2 GiB at 14).  Counts never depend on kmer_k.  QR_EINVAL outside 0..14. */
 qr_status qr_fm_build_ex(const uint64_t* text2b, uint64_t n, const uint32_t* sa_or_null, int kmer_k, int device,
                          void* stream, qr_fm** out);

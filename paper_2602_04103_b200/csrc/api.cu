@@ -160,6 +160,7 @@ uint64_t super_bytes_of(const qr_index* h) {
   return h->n_super * (h->layout == QR_LAYOUT_BIRANK32X2 ? 8 : h->sigma == 2 ? 4 : 16);
 }
 
+void fm_copy_locked(const qr_fm* src, qr_fm* dst);
 qr_status fm_build_device(const uint64_t* d_text, uint64_t n, const uint32_t* d_sa_given, int device, cudaStream_t st,
                           qr_fm** out, int kmer_k, int bwt_layout, int kmer_k_ax);
 __global__ void k_mask_tail_bits(uint64_t* words, uint64_t n);
@@ -684,12 +685,12 @@ QR_EXPORT qr_status qr_fm_build_opts(const uint64_t* text2b, uint64_t n, const u
                                      int bwt_layout, int device, void* stream, qr_fm** out) {
   // The default width may pick 11 for the exact count (its table then sits in L2); the
   // approximate-search kernels enumerate every K-mer within k substitutions of the seed, where a
-  // wider table saves more backtracking than HBM lookups cost: they get a 12-wide table of their
-  // own (configs[3] <= 1 substitution 0.50 -> 0.60 G patterns/s; profiles/r02_bench_full_*.jsonl).
+  // wider table saves more backtracking than HBM lookups cost: from n = 2^24 they get a 14-wide
+  // table of their own (2 GiB), built on the first approximate call (fm.cu fm_params_ax).
   int kmer_k_ax = kmer_k;
   if (kmer_k == -1) {
     kmer_k = fm_default_kmer_k(n, bwt_layout, device);
-    kmer_k_ax = kmer_k == 11 ? 12 : kmer_k;
+    kmer_k_ax = n >= (1ull << 24) ? 14 : kmer_k;            // built on the first approximate call
   }
   if (kmer_k < 0 || kmer_k > 14) return fail(QR_EINVAL, "qr_fm_build_ex: kmer_k must be 0..14");
   if (bwt_layout != QR_LAYOUT_QUADRANK16 && bwt_layout != QR_LAYOUT_QUADRANK16X2)
@@ -937,7 +938,8 @@ QR_EXPORT qr_status qr_clone_to_device(const qr_index* h, int device, void* stre
 QR_EXPORT qr_status qr_fm_clone_to_device(const qr_fm* fm, int device, void* stream, qr_fm** out) {
   if (!fm || !out) return fail(QR_EINVAL, "qr_fm_clone_to_device: null pointer");
   *out = nullptr;
-  qr_fm* c = new (std::nothrow) qr_fm(*fm);
+  qr_fm* c = new (std::nothrow) qr_fm();
+  if (c) fm_copy_locked(fm, c);                            // consistent with a concurrent lazy build
   if (!c) return fail(QR_ENOMEM, "host allocation");
   c->bwt = nullptr;
   c->kmer = nullptr;
@@ -949,7 +951,8 @@ QR_EXPORT qr_status qr_fm_clone_to_device(const qr_fm* fm, int device, void* str
   cudaError_t e = cudaMalloc((void**)&c->kmer, kb);
   if (!e) e = cudaMemcpyPeerAsync(c->kmer, device, fm->kmer, fm->bwt->device, kb, (cudaStream_t)stream);
   if (fm->kmer_ax == fm->kmer) {
-    c->kmer_ax = c->kmer;
+    c->kmer_ax = c->kmer;                                  // the clone builds a wider table itself
+    c->kmer_k_ax = c->kmer_k;
   } else {
     const size_t kx = kmer_entries(fm->kmer_k_ax) * sizeof(uint2);
     if (!e) e = cudaMalloc((void**)&c->kmer_ax, kx);

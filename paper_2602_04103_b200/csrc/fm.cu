@@ -1424,11 +1424,41 @@ static FmParams params_of(const qr_fm* fm) {
   return F;
 }
 
-// the approximate-search kernels' table (C[0..3] stays at the main table's tail, F.Ct)
-static FmParams params_ax(FmParams F, const qr_fm* fm) {
+// The approximate-search kernels' table (C[0..3] stays at the main table's tail, F.Ct).  When the
+// build asked for a wider one than the count's (qr_fm_build's default from n = 2^24: 14, 2 GiB —
+// each extra symbol of width replaces a level of the search tree by a lookup: configs[3] k = 2
+// 29.4 / 35.1 / 38.3 M patterns/s and 150-bp reads 4.63 / 5.19 / 6.24 M reads/s at 12 / 13 / 14,
+// profiles/r02_approx_width.jsonl) it is built here on the first approximate call, on the
+// caller's stream, once, under a process-wide lock; the handle's pointers are read under it too.
+static std::mutex g_ax_mu;
+void fm_copy_locked(const qr_fm* src, qr_fm* dst) {
+  std::lock_guard<std::mutex> g(g_ax_mu);
+  *dst = *src;
+}
+static qr_status fm_params_ax(const qr_fm* fmc, cudaStream_t st, FmParams& F) {
+  qr_fm* fm = const_cast<qr_fm*>(fmc);                     // a lazily filled cache of the handle
+  std::lock_guard<std::mutex> g(g_ax_mu);
+  if (fm->kmer_k_ax != fm->kmer_k_ax_want && fm->kmer_k_ax_want > 0) {
+    const uint64_t nx = kmer_entries(fm->kmer_k_ax_want);
+    uint2* t = nullptr;
+    if (cudaMalloc((void**)&t, nx * sizeof(uint2)) != cudaSuccess) {
+      cudaGetLastError();
+      fm->kmer_k_ax_want = fm->kmer_k_ax;                  // no memory for it: keep the count's table
+    } else {
+      FmParams Fx = F;
+      Fx.K = fm->kmer_k_ax_want;
+      if (F.bw) k_kmer_table<1><<<(unsigned)((nx + 255) / 256), 256, 0, st>>>(Fx, t);
+      else      k_kmer_table<0><<<(unsigned)((nx + 255) / 256), 256, 0, st>>>(Fx, t);
+      cudaError_t e = cudaGetLastError();
+      if (!e) e = cudaStreamSynchronize(st);               // complete before any stream may use it
+      if (e) { cudaFree(t); return cuda_fail(e, "k_kmer_table (approximate search)"); }
+      fm->kmer_ax = t;
+      fm->kmer_k_ax = fm->kmer_k_ax_want;
+    }
+  }
   F.kmer = fm->kmer_ax;
   F.K = fm->kmer_k_ax;
-  return F;
+  return QR_OK;
 }
 
 extern int g_fm_blocks_per_sm;
@@ -1659,8 +1689,13 @@ qr_status fm_count_device(const qr_fm* fm, const uint8_t* pat, const uint32_t* l
   unsigned g = grid_stride_blocks(tasks, 256, sms, g_fm_blocks_per_sm);
   unsigned long long* w = reinterpret_cast<unsigned long long*>(work);
   cudaError_t e;
+  FmParams Fa = F;
+  if (approx) {
+    qr_status sa = fm_params_ax(fm, st, Fa);
+    if (sa != QR_OK) return sa;
+  }
   if (!lengths) {
-    if (approx) e = launch_approx<true>(fm, g, st, params_ax(F, fm), pat, nullptr, nullptr, fixed_len, out, out_rc, m, approx, w);
+    if (approx) e = launch_approx<true>(fm, g, st, Fa, pat, nullptr, nullptr, fixed_len, out, out_rc, m, approx, w);
     else if (work) e = launch_fm<true, true>(fm, fm_step_of(fm), g, st, F, pat, nullptr, nullptr, fixed_len, out, out_rc, m, w);
     else      e = launch_fm<true, false>(fm, fm_step_of(fm), g, st, F, pat, nullptr, nullptr, fixed_len, out, out_rc, m, w);
     if (e) return cuda_fail(e, "k_fm_count");
@@ -1676,7 +1711,7 @@ qr_status fm_count_device(const qr_fm* fm, const uint8_t* pat, const uint32_t* l
   if ((e = cub::DeviceScan::ExclusiveSum(tmp, tb, offs, offs, (int64_t)m, st))) {
     cudaFreeAsync(offs, st); cudaFreeAsync(tmp, st); return cuda_fail(e, "scan");
   }
-  if (approx) e = launch_approx<false>(fm, g, st, params_ax(F, fm), pat, offs, lengths, 0, out, out_rc, m, approx, w);
+  if (approx) e = launch_approx<false>(fm, g, st, Fa, pat, offs, lengths, 0, out, out_rc, m, approx, w);
   else if (work) e = launch_fm<false, true>(fm, fm_step_of(fm), g, st, F, pat, offs, lengths, 0, out, out_rc, m, w);
   else      e = launch_fm<false, false>(fm, fm_step_of(fm), g, st, F, pat, offs, lengths, 0, out, out_rc, m, w);
   cudaFreeAsync(offs, st);
@@ -1750,21 +1785,9 @@ qr_status fm_build_device(const uint64_t* d_text, uint64_t n, const uint32_t* d_
     else      k_kmer_table<0><<<(unsigned)((ne + 255) / 256), 256, 0, st>>>(F, fm->kmer);
   }
   if ((e = cudaGetLastError())) return bail(cuda_fail(e, "k_kmer_table"));
-  fm->kmer_ax = fm->kmer;
-  fm->kmer_k_ax = kmer_k;
-  if (kmer_k_ax != kmer_k && kmer_k_ax > 0) {               // the approximate-search table
-    const uint64_t nx = kmer_entries(kmer_k_ax);
-    if ((e = cudaMalloc((void**)&fm->kmer_ax, nx * sizeof(uint2)))) {
-      fm->kmer_ax = fm->kmer;
-      return bail(cuda_fail(e, "alloc kmer (approximate search)"));
-    }
-    fm->kmer_k_ax = kmer_k_ax;
-    FmParams Fx = F;
-    Fx.K = kmer_k_ax;
-    if (F.bw) k_kmer_table<1><<<(unsigned)((nx + 255) / 256), 256, 0, st>>>(Fx, fm->kmer_ax);
-    else      k_kmer_table<0><<<(unsigned)((nx + 255) / 256), 256, 0, st>>>(Fx, fm->kmer_ax);
-    if ((e = cudaGetLastError())) return bail(cuda_fail(e, "k_kmer_table (approximate search)"));
-  }
+  fm->kmer_ax = fm->kmer;                                  // the approximate-search table: built
+  fm->kmer_k_ax = kmer_k;                                  // on the first approximate call when
+  fm->kmer_k_ax_want = kmer_k_ax > 0 ? kmer_k_ax : kmer_k; // wider than the count's (fm_params_ax)
   if ((e = cudaStreamSynchronize(st))) { release(); qr_fm_free(fm); return cuda_fail(e, "fm build"); }
   release();
   *out = fm;

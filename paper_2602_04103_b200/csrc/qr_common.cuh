@@ -59,6 +59,7 @@ struct qr_fm {
   int kmer_k;           // K: table of K-mers (PAPER.md:918 uses 8; 0 = no table)
   uint2* kmer_ax;       // the approximate-search kernels' table (== kmer unless a wider one pays there)
   int kmer_k_ax;
+  int kmer_k_ax_want;   // its width; a wider table than kmer_k is built on the first approximate call
 };
 
 namespace qr {

@@ -801,9 +801,11 @@ def test_checksum_is_additive_over_shards(cuda):
 
 
 def test_fm_default_width_dual_tables(cuda):
-    """From n = 2^24 on a B200 the default build keeps an 11-mer table for the exact count and a
-    12-mer table for the approximate-search kernels; every count equals the oracle's and the
-    single-table handles' (explicit widths 11 and 12), and a clone keeps both tables."""
+    """From n = 2^24 on a B200 the default build keeps an 11-mer table for the exact count and
+    builds a 14-mer table for the approximate-search kernels on their first call; every count
+    equals the oracle's and the single-table handles' (explicit widths 11 and 12), a clone made
+    before the first approximate call builds its own, and four host threads on their own streams
+    racing for a fresh handle's first approximate call all get exact counts."""
     torch = _torch()
     n = (1 << 24) + 5
     w = gen.dna(411, n, 0)
@@ -814,13 +816,36 @@ def test_fm_default_width_dual_tables(cuda):
     fx = gen.patterns(412, 0, m, L, w, n)
     offs, lens = np.arange(m, dtype=np.uint64) * L, np.full(m, L, np.uint32)
     handles = [fm, qr.qr_fm_build(w, n, kmer_k=11), qr.qr_fm_build(w, n, kmer_k=12), qr.qr_fm_clone_to_device(fm, 0)]
+    refs = {kmax: oracle.scan_count_hdk(sym, fx, offs, lens, kmax) for kmax in (0, 1, 2)}
     for kmax in (0, 1, 2):
-        ref = oracle.scan_count_hdk(sym, fx, offs, lens, kmax)
         for h in handles:
             d = torch.empty(m, dtype=torch.int32, device=cuda)
             qr.qr_fm_count_approx(h, to_dev(fx, cuda), None, L, kmax, d, m)
             torch.cuda.synchronize()
-            assert np.array_equal(to_host(d).view(np.uint32), ref), (kmax, h.kmer_k)
+            assert np.array_equal(to_host(d).view(np.uint32), refs[kmax]), (kmax, h.kmer_k)
+    import threading
+
+    fresh = qr.qr_fm_build(w, n)
+    errs, outs = [], {}
+
+    def worker(i):
+        try:
+            s_ = torch.cuda.Stream()
+            with torch.cuda.stream(s_):
+                d = torch.empty(m, dtype=torch.int32, device=cuda)
+                qr.qr_fm_count_approx(fresh, to_dev(fx, cuda), None, L, 1 + i % 2, d, m, s_)
+                s_.synchronize()
+                outs[i] = to_host(d).view(np.uint32)
+        except Exception as e:  # noqa: BLE001
+            errs.append(e)
+    ts = [threading.Thread(target=worker, args=(i,)) for i in range(4)]
+    for t_ in ts:
+        t_.start()
+    for t_ in ts:
+        t_.join()
+    assert not errs, errs
+    for i in range(4):
+        assert np.array_equal(outs[i], refs[1 + i % 2]), i
 
 
 @pytest.mark.parametrize("bwt_layout", [None, qr.QR_LAYOUT_QUADRANK16X2])
