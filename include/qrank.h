@@ -134,6 +134,12 @@ qr_status qr_rank_chain(const qr_index* h, const uint64_t* q, const uint8_t* c, 
 qr_status qr_fm_build(const uint64_t* text2b, uint64_t n, const uint32_t* sa_or_null, int device, void* stream,
                       qr_fm** out);
 
+/* As qr_fm_build from one byte per symbol (0..3 = A, C, G, T), the input form SURVEY §8(b)
+ * proposes: text: n bytes (host or device), packed to 2 bits per symbol on the GPU.  A byte > 3
+ * is QR_EINVAL (nothing is built).  Requires 1 <= n and n + 1 < 2^32. */
+qr_status qr_fm_build_u8(const uint8_t* text, uint64_t n, const uint32_t* sa_or_null, int device, void* stream,
+                         qr_fm** out);
+
 /* As qr_fm_build with a k-mer seed table of width kmer_k (0..14; 0 = no table, every search
  * starts from [0, n+1)).  qr_fm_build picks the paper's 8 for n < 2^20, 10 for
  * n < 2^24 and, above, 11 when the BWT's rank layout plus the 32 MiB 11-mer table fit in 60% of

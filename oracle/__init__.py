@@ -44,6 +44,7 @@ def lib():
             "or_fm_work": [u8p, u64p, u64p, C.c_uint64, u8p, u64p, u32p, C.c_uint64, C.c_uint32, C.c_uint64, u64p, u64p],
             "or_sa_count": [u8p, C.c_uint64, u32p, u8p, u64p, u32p, C.c_uint64, u32p],
             "or_scan_count": [u8p, C.c_uint64, u8p, u64p, u32p, C.c_uint64, u32p],
+            "or_scan_count_bucketed": [u8p, C.c_uint64, u8p, u64p, u32p, C.c_uint64, u32p],
             "or_scan_count_hd1": [u8p, C.c_uint64, u8p, u64p, u32p, C.c_uint64, u32p],
             "or_scan_count_hdk": [u8p, C.c_uint64, u8p, u64p, u32p, C.c_uint64, C.c_uint32, u32p],
             "or_threads": [],
@@ -189,6 +190,19 @@ def scan_count(sym: np.ndarray, cat, off, lens) -> np.ndarray:
     lens = np.ascontiguousarray(lens, dtype=np.uint32)
     out = np.empty(lens.size, dtype=np.uint32)
     lib().or_scan_count(_p(sym, u8p), sym.size, _p(cat, u8p), _p(off, u64p), _p(lens, u32p), lens.size, _p(out, u32p))
+    return out
+
+
+def scan_count_bucketed(sym: np.ndarray, cat, off, lens) -> np.ndarray:
+    """Occurrences by a direct scan of every text position, patterns of >= 8 symbols grouped by
+    their first 8 (the same counts as scan_count; for large batches on large texts)."""
+    sym = np.ascontiguousarray(sym, dtype=np.uint8)
+    cat = np.ascontiguousarray(cat, dtype=np.uint8)
+    off = np.ascontiguousarray(off, dtype=np.uint64)
+    lens = np.ascontiguousarray(lens, dtype=np.uint32)
+    out = np.empty(lens.size, dtype=np.uint32)
+    lib().or_scan_count_bucketed(_p(sym, u8p), sym.size, _p(cat, u8p), _p(off, u64p), _p(lens, u32p), lens.size,
+                                 _p(out, u32p))
     return out
 
 

@@ -16,6 +16,8 @@
  *                 plain BWT (App. D)
  *   count_hdk  := number of text positions within Hamming distance k of the pattern
  *                 (NEXT §8(f)3), by a direct scan of every position
+ *   or_scan_count / or_scan_count_bucketed := the FM count by a direct scan of every text
+ *                 position (the bucketed form only skips positions whose first 8 symbols differ)
  *
  * Conventions (DESIGN.md "Readings" 1, 11, 15): bits are LE in u64 words
  * (t_i = bit i%64 of word i/64); DNA is 2-bit LE (char i = bits 2(i%32)..+1 of
@@ -274,6 +276,63 @@ EXPORT void or_scan_count(const uint8_t* s, uint64_t n, const uint8_t* pat, cons
       }
     out[k] = (uint32_t)cnt;
   }
+}
+
+/* The same count as or_scan_count — the number of (overlapping) text positions where the whole
+ * pattern matches — for large batches on large texts: the patterns of >= 8
+ * symbols are grouped by their first 8 symbols, and each text position is compared in full only
+ * with the patterns whose first 8 symbols equal the text's there (a pattern whose first 8
+ * symbols differ cannot occur at that position); shorter patterns take or_scan_count.  Loop order
+ * and filtering only: every count is still a direct comparison at every position.  Pinned against
+ * or_scan_count and Python brute force (tests/test_oracle.py). */
+EXPORT void or_scan_count_bucketed(const uint8_t* s, uint64_t n, const uint8_t* pat, const uint64_t* off,
+                                   const uint32_t* len, uint64_t m, uint32_t* out) {
+  const uint32_t NB = 1u << 16;                      /* 8 symbols, 2 bits each */
+  uint32_t* head = (uint32_t*)calloc(NB + 1, sizeof(uint32_t));
+  uint32_t* list = (uint32_t*)malloc((m ? m : 1) * sizeof(uint32_t));
+  uint64_t* cnt = (uint64_t*)calloc(m ? m : 1, sizeof(uint64_t));
+  uint64_t k;
+  for (k = 0; k < m; ++k) {                          /* counting sort of the long patterns by key */
+    if (len[k] < 8) continue;
+    uint32_t key = 0;
+    for (int j = 0; j < 8; ++j) key = (key << 2) | (pat[off[k] + j] & 3u);
+    head[key + 1]++;
+  }
+  for (uint32_t b = 0; b < NB; ++b) head[b + 1] += head[b];
+  uint32_t* fill = (uint32_t*)malloc(NB * sizeof(uint32_t));
+  memcpy(fill, head, NB * sizeof(uint32_t));
+  for (k = 0; k < m; ++k) {
+    if (len[k] < 8) continue;
+    uint32_t key = 0;
+    for (int j = 0; j < 8; ++j) key = (key << 2) | (pat[off[k] + j] & 3u);
+    list[fill[key]++] = (uint32_t)k;
+  }
+  free(fill);
+  if (n >= 8) {
+#pragma omp parallel
+    {
+      uint64_t* loc = (uint64_t*)calloc(m ? m : 1, sizeof(uint64_t));
+#pragma omp for schedule(static)
+      for (int64_t i = 0; i <= (int64_t)n - 8; ++i) {
+        uint32_t key = 0;
+        for (int j = 0; j < 8; ++j) key = (key << 2) | s[i + j];
+        for (uint32_t t = head[key]; t < head[key + 1]; ++t) {
+          const uint32_t q = list[t];
+          const uint32_t L = len[q];
+          if ((uint64_t)i + L > n) continue;
+          if (memcmp(s + i, pat + off[q], L) == 0) loc[q]++;
+        }
+      }
+#pragma omp critical
+      for (uint64_t q = 0; q < m; ++q) cnt[q] += loc[q];
+      free(loc);
+    }
+  }
+  for (k = 0; k < m; ++k) {
+    if (len[k] >= 8) { out[k] = (uint32_t)cnt[k]; continue; }
+    or_scan_count(s, n, pat, off + k, len + k, 1, out + k);   /* short patterns: the plain scan */
+  }
+  free(head); free(list); free(cnt);
 }
 
 /* Approximate occurrences (NEXT §8(f)3; the paper's motivation for rank_4):

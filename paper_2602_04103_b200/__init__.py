@@ -31,7 +31,7 @@ EXPORTS = (
     "qr_clone_to_device", "qr_fm_clone_to_device", "qr_sync", "qr_free", "qr_fm_free", "qr_last_error",
     "qr_version", "qr_set_tuning", "qr_build", "qr_layout", "qr_rank_chain", "qr_import_layout", "qr_fm_build_ex", "qr_fm_kmer_width",
     "qr_super_cache_bytes", "qr_super_cache_clusters", "qr_fm_build_opts", "qr_fm_count_approx_both",
-    "qr_fm_count_work_ex", "qr_checksum",
+    "qr_fm_count_work_ex", "qr_checksum", "qr_fm_build_u8",
 )
 
 
@@ -64,6 +64,7 @@ def lib():
             "qr_fm_count_both": ([V, V, V, U32, V, V, U64, V], I32),
             "qr_fm_count_work_ex": ([V, V, V, U32, U32, V, V, U64, V, V], I32),
             "qr_checksum": ([V, U64, C.c_int, U64, V, V], I32),
+            "qr_fm_build_u8": ([V, U64, V, I32, V, PP], I32),
             "qr_fm_count_approx": ([V, V, V, U32, U32, V, U64, V], I32),
             "qr_fm_count_approx_both": ([V, V, V, U32, U32, V, V, U64, V], I32),
             "qr_gather_ceiling": ([V, V, V, U64, I32, V], I32),
@@ -289,6 +290,15 @@ def qr_fm_build(text2b, n: int, sa=None, device: int = 0, stream=None, kmer_k: i
     else:
         _check(lib().qr_fm_build_ex(_ptr(text2b), n, _ptr(sa), kmer_k, device, _stream(stream), C.byref(out)),
                "qr_fm_build_ex")
+    return Fm(out.value)
+
+
+def qr_fm_build_u8(text, n: int, sa=None, device: int = 0, stream=None) -> Fm:
+    """QuadFm index from one byte per symbol (0..3), packed on the GPU (SURVEY §8(b) input form)."""
+    _need(text, 1, n, "qr_fm_build_u8 text")
+    _need(sa, 4, n + 1, "qr_fm_build_u8 sa")
+    out = C.c_void_p()
+    _check(lib().qr_fm_build_u8(_ptr(text), n, _ptr(sa), device, _stream(stream), C.byref(out)), "qr_fm_build_u8")
     return Fm(out.value)
 
 

@@ -681,6 +681,60 @@ QR_EXPORT qr_status qr_fm_build_ex(const uint64_t* text2b, uint64_t n, const uin
   return qr_fm_build_opts(text2b, n, sa_or_null, kmer_k, QR_LAYOUT_QUADRANK16, device, stream, out);
 }
 
+// one byte per symbol -> 2-bit LE words (char i = bits 2(i%32).. of word i/32); a byte > 3 sets *bad
+__global__ void k_pack2(const uint8_t* __restrict__ t, uint64_t n, uint64_t* __restrict__ w, unsigned* __restrict__ bad) {
+  const uint64_t nw = (n + 31) >> 5;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nw; i += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t v = 0;
+    unsigned b = 0;
+    const uint64_t base = i << 5;
+    const uint32_t cnt = n - base < 32 ? (uint32_t)(n - base) : 32u;
+    for (uint32_t k = 0; k < cnt; ++k) {
+      const uint32_t c = t[base + k];
+      b |= c > 3u;
+      v |= (uint64_t)(c & 3u) << (2 * k);
+    }
+    w[i] = v;
+    if (b) atomicOr(bad, 1u);
+  }
+}
+
+QR_EXPORT qr_status qr_fm_build_u8(const uint8_t* text, uint64_t n, const uint32_t* sa_or_null, int device,
+                                   void* stream, qr_fm** out) {
+  if (!out || !text) return fail(QR_EINVAL, "qr_fm_build_u8: null pointer");
+  *out = nullptr;
+  if (n == 0) return fail(QR_EINVAL, "qr_fm_build_u8: empty text");
+  if (n + 1 >= (1ull << 32)) return fail(QR_ECAPACITY, "qr_fm_build_u8: n+1 >= 2^32 (u32 counts)");
+  DeviceGuard dg(device);
+  if (!dg.ok) return fail(QR_EINVAL, "qr_fm_build_u8: bad device %d", device);
+  cudaStream_t st = (cudaStream_t)stream;
+  const uint64_t words = (n + 31) >> 5;
+  uint8_t* dt = nullptr;
+  uint64_t* dw = nullptr;
+  unsigned* dbad = nullptr;
+  const bool dev_in = pointer_space(text, device) == 1;
+  cudaError_t e = cudaSuccess;
+  if (!dev_in) {
+    if (!(e = cudaMalloc((void**)&dt, n))) e = cudaMemcpyAsync(dt, text, n, cudaMemcpyDefault, st);
+  }
+  if (!e) e = cudaMalloc((void**)&dw, (words + 1) * 8);
+  if (!e) e = cudaMalloc((void**)&dbad, sizeof(unsigned));
+  if (!e) e = cudaMemsetAsync(dbad, 0, sizeof(unsigned), st);
+  if (!e) e = cudaMemsetAsync(dw + words, 0, 8, st);
+  if (!e) {
+    k_pack2<<<grid_stride_blocks(words, 256, sm_count(device), 8), 256, 0, st>>>(dev_in ? text : dt, n, dw, dbad);
+    e = cudaGetLastError();
+  }
+  unsigned hbad = 0;
+  if (!e) e = cudaMemcpyAsync(&hbad, dbad, sizeof(unsigned), cudaMemcpyDeviceToHost, st);
+  if (!e) e = cudaStreamSynchronize(st);
+  qr_status s = e ? cuda_fail(e, "qr_fm_build_u8") : hbad ? fail(QR_EINVAL, "qr_fm_build_u8: a symbol byte is > 3") : QR_OK;
+  if (s == QR_OK) s = qr_fm_build_opts(dw, n, sa_or_null, -1, QR_LAYOUT_QUADRANK16, device, stream, out);
+  cudaStreamSynchronize(st);
+  cudaFree(dt); cudaFree(dw); cudaFree(dbad);
+  return s;
+}
+
 QR_EXPORT qr_status qr_fm_build_opts(const uint64_t* text2b, uint64_t n, const uint32_t* sa_or_null, int kmer_k,
                                      int bwt_layout, int device, void* stream, qr_fm** out) {
   // The default width may pick 11 for the exact count (its table then sits in L2); the

@@ -875,3 +875,30 @@ def test_fm_approx_all_k_both_strands(cuda, bwt_layout, dyn, n, kind):
             assert np.array_equal(to_host(dr).view(np.uint32), oracle.scan_count_hdk(sym, rcat, roff, rlens, kmax)), kmax
     finally:
         qr.qr_set_tuning("fm_dyn", 1)
+
+
+@pytest.mark.parametrize("space", ["host", "device"])
+def test_fm_build_from_bytes(cuda, space):
+    """qr_fm_build_u8 (one byte per symbol, SURVEY §8(b)'s input form, packed on the GPU) builds
+    the same index as qr_fm_build from 2-bit words: same spos, C, k-mer table and counts (vs the
+    oracle); a byte > 3 is QR_EINVAL."""
+    torch = _torch()
+    n = 70001
+    w = gen.dna(431, n, 1)
+    sym = gen.unpack_dna(w, n)
+    src = sym if space == "host" else to_dev(sym, cuda)
+    fb = qr.qr_fm_build_u8(src, n)
+    fw = qr.qr_fm_build(w, n)
+    assert (fb.spos, fb.C, fb.kmer_k) == (fw.spos, fw.C, fw.kmer_k)
+    assert np.array_equal(qr.qr_fm_export_kmer(fb), qr.qr_fm_export_kmer(fw))
+    pats = mixed_patterns(np.random.default_rng(3), sym, 500)
+    cat, off, lens = oracle.pack_patterns(pats)
+    d = torch.empty(lens.size, dtype=torch.int32, device=cuda)
+    qr.qr_fm_count(fb, to_dev(cat, cuda), to_dev(lens, cuda), 0, d, lens.size)
+    torch.cuda.synchronize()
+    assert np.array_equal(to_host(d).view(np.uint32), oracle.FmOracle(sym).count(cat, off, lens))
+    bad = sym.copy()
+    bad[n // 2] = 4
+    with pytest.raises(qr.QrError) as e:
+        qr.qr_fm_build_u8(bad if space == "host" else to_dev(bad, cuda), n)
+    assert e.value.status == qr.QR_EINVAL

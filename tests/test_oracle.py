@@ -413,3 +413,27 @@ def test_hdk_scan_pins():
                     vc, vo, vl = oracle.pack_patterns(near)
                     assert int(f.count(vc, vo, vl).astype(np.int64).sum()) == g
             assert all(by_k[k][i] <= by_k[k + 1][i] for k in range(3))
+
+
+def test_scan_count_bucketed_equals_direct_scan():
+    """or_scan_count_bucketed (the configs[4] full-size check's counter) against the plain direct
+    scan and Python brute force: random and repetitive texts, patterns of 0..40 symbols (both sides
+    of the 8-symbol bucket key), exact substrings, substituted ones, longer than the text."""
+    rng = np.random.default_rng(77)
+    for t in range(8):
+        n = int(rng.integers(1, 3000))
+        sym = (rng.integers(0, 4, n) if t % 2 else np.tile(rng.integers(0, 4, 5), n)[:n]).astype(np.uint8)
+        pats = [rng.integers(0, 4, int(rng.integers(0, 12))).astype(np.uint8) for _ in range(30)]
+        for a in rng.integers(0, n, 30):
+            p = sym[a:a + int(rng.integers(1, 41))].copy()
+            if p.size > 3 and rng.random() < 0.4:
+                p[int(rng.integers(0, p.size))] ^= 1
+            pats.append(p)
+        pats.append(np.concatenate([sym, sym[:9]]))
+        cat, off, lens = oracle.pack_patterns(pats)
+        got = oracle.scan_count_bucketed(sym, cat, off, lens)
+        assert np.array_equal(got, oracle.scan_count(sym, cat, off, lens))
+        if n <= 600:
+            brute = [n + 1 if len(p) == 0 else sum(1 for i in range(n - len(p) + 1) if np.array_equal(sym[i:i + len(p)], p))
+                     for p in pats]
+            assert [int(x) for x in got] == brute
