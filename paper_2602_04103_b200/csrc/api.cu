@@ -26,7 +26,7 @@ int g_rank_s_lane = 1;
 int g_fm_dyn = 1;               // FM count: 1 = persistent grid + warp chunks from a global counter, 0 = static grid stride
 int g_fm_seed = 0;              // FM seed pre-pass (dynamic order only): 0 auto (L2-resident BWT), 1 never, 2 always
 int g_fm_smem = 1;              // FM superblock words from shared memory: 0 off, 1 auto, 2 packed table whenever it fits
-int g_fm_refill = 8;            // L2-resident count kernel: refill a warp's lanes once this many are idle
+int g_fm_refill = 0;            // L2-resident count kernel: refill a warp's lanes once this many are idle (0 auto)
 int g_fm_packed = 1;            // L2-resident count kernel: packed post-seed symbols for short fixed-length batches
 int g_check_range = 0;          // 1: qr_rank / qr_rank_all4 count q > n and return QR_ERANGE (synchronous)
 int g_fm_lean = 0;              // FM step flavour: 0 auto (by L2 residency), 1 de-duplicating, 2 lean, 3 one line per iteration
@@ -409,7 +409,7 @@ QR_EXPORT qr_status qr_set_tuning(const char* key, int64_t value) {
     if (value < 0 || value > 2) return fail(QR_EINVAL, "fm_smem must be 0 (off), 1 (auto) or 2 (packed)");
     g_fm_smem = (int)value;
   } else if (!strcmp(key, "fm_refill")) {
-    if (value < 1 || value > 32) return fail(QR_EINVAL, "fm_refill must be 1..32");
+    if (value < 0 || value > 32) return fail(QR_EINVAL, "fm_refill must be 0 (auto) or 1..32");
     g_fm_refill = (int)value;
   } else if (!strcmp(key, "fm_packed")) {
     if (value != 0 && value != 1) return fail(QR_EINVAL, "fm_packed must be 0 or 1");

@@ -920,8 +920,12 @@ __global__ void __launch_bounds__(256, QR_FM_MINB) k_fm_count(FmParams F, const 
 //    idle: the refill (seed load, pattern pointer) ran in ~93% of iterations with ~3 of 32 lanes
 //    active, ~80 issue slots each time;
 //  * seeds come from the k_fm_seed pre-pass (one 8-byte load per task).
+// 5 resident CTAs (47 / 44 registers, no spills): configs[3] 9.48 -> 9.58 G patterns/s; 6 spills
+#ifndef QR_FM_L2_MINB
+#define QR_FM_L2_MINB 5
+#endif
 template <bool FIXED, bool WORK, int STRANDS, int SMS, int BW, bool PACKED>
-__global__ void __launch_bounds__(256, QR_FM_MINB) k_fm_count_l2(FmParams F, const uint8_t* __restrict__ pat,
+__global__ void __launch_bounds__(256, QR_FM_L2_MINB) k_fm_count_l2(FmParams F, const uint8_t* __restrict__ pat,
                                                               const uint64_t* __restrict__ offs,
                                                               const uint32_t* __restrict__ lens, uint32_t fixed_len,
                                                               uint32_t* __restrict__ out, uint32_t* __restrict__ out_rc,
@@ -1479,9 +1483,12 @@ static bool bwt_l2_resident(const qr_fm* fm) {
 // order and seeds: k_fm_count_l2).  Auto: 3 on L2-resident BWTs (configs[3]: 7.07 -> 8.68 G
 // patterns/s over QuadRank16, 8.45 -> 9.12 over QuadRank16x2), 1 on HBM-resident ones (request-
 // bound there: configs[4] 0.97 vs 0.86 with 3; profiles/r02_fm_step_probe.jsonl).
-static int fm_step_of(const qr_fm* fm) {
+// On an HBM-resident BWT both strands at once (the paper's read workload) take the lean step
+// with the seed pre-pass: 150-bp reads 0.533 -> 0.588 G reads/s, while one strand keeps the
+// de-duplicating step without it (configs[4] 0.96 vs 0.89 / 0.95; profiles/r02_fm_hbm_strands.log).
+static int fm_step_of(const qr_fm* fm, bool both) {
   if (g_fm_lean >= 1 && g_fm_lean <= 3) return g_fm_lean;
-  return bwt_l2_resident(fm) ? 3 : 1;
+  return bwt_l2_resident(fm) ? 3 : both ? 2 : 1;
 }
 
 extern int g_fm_smem;
@@ -1539,7 +1546,10 @@ static void launch_fm1(unsigned g, size_t smem, cudaStream_t st, const FmParams&
     }
     const uint64_t need = (m * STRANDS + 255) / 256;
     unsigned gp = (unsigned)((uint64_t)per_sm * sms < need ? (uint64_t)per_sm * sms : (need ? need : 1));
-    kern<<<gp, 256, smem, st>>>(F, pat, offs, lens, fixed_len, out, out_rc, m, w, ctr, seeds, (uint32_t)g_fm_refill);
+    // refill threshold: 8 idle lanes over QuadRank16, 4 over QuadRank16x2 (its shorter step makes
+    // idle lanes cost less than refills): configs[3] 9.48 / 9.97 G patterns/s, knob fm_refill
+    const uint32_t refill = g_fm_refill ? (uint32_t)g_fm_refill : (F.bw ? 4u : 8u);
+    kern<<<gp, 256, smem, st>>>(F, pat, offs, lens, fixed_len, out, out_rc, m, w, ctr, seeds, refill);
   } else if (ctr) {
     // QuadRank16x2 BWT: the sector-shared step, or the one-sector-per-iteration step (STEP 3)
     auto kern = F.bw ? k_fm_count<FIXED, WORK, STRANDS, STEP == 3 ? 3 : 0, SMS, true, 1>
@@ -1610,8 +1620,9 @@ static cudaError_t launch_fm(const qr_fm* fm, int step, unsigned g, cudaStream_t
   cudaError_t e;
   if (g_fm_dyn) {
     // seed pre-pass: pays when the search is instruction-bound (L2-resident BWT: configs[3] 6.57
-    // -> 7.21 G patterns/s) and costs when it is latency-bound (HBM: configs[4] 0.99 -> 0.86)
-    const bool pre = g_fm_seed == 2 || (g_fm_seed == 0 && bwt_l2_resident(fm));
+    // -> 7.21 G patterns/s) and for both strands at once (two seeds per pattern read), costs for
+    // one strand when latency-bound (HBM: configs[4] 0.99 -> 0.86 in round 1, 0.96 -> 0.95 now)
+    const bool pre = g_fm_seed == 2 || (g_fm_seed == 0 && (bwt_l2_resident(fm) || out_rc));
     if (pre) {
       keep_pool_memory(fm->bwt->device, st);
       // 16 B per task: room for the packed seeds (k_fm_seed_packed) when the batch qualifies
@@ -1696,8 +1707,8 @@ qr_status fm_count_device(const qr_fm* fm, const uint8_t* pat, const uint32_t* l
   }
   if (!lengths) {
     if (approx) e = launch_approx<true>(fm, g, st, Fa, pat, nullptr, nullptr, fixed_len, out, out_rc, m, approx, w);
-    else if (work) e = launch_fm<true, true>(fm, fm_step_of(fm), g, st, F, pat, nullptr, nullptr, fixed_len, out, out_rc, m, w);
-    else      e = launch_fm<true, false>(fm, fm_step_of(fm), g, st, F, pat, nullptr, nullptr, fixed_len, out, out_rc, m, w);
+    else if (work) e = launch_fm<true, true>(fm, fm_step_of(fm, out_rc != nullptr), g, st, F, pat, nullptr, nullptr, fixed_len, out, out_rc, m, w);
+    else      e = launch_fm<true, false>(fm, fm_step_of(fm, out_rc != nullptr), g, st, F, pat, nullptr, nullptr, fixed_len, out, out_rc, m, w);
     if (e) return cuda_fail(e, "k_fm_count");
     return QR_OK;
   }
@@ -1712,8 +1723,8 @@ qr_status fm_count_device(const qr_fm* fm, const uint8_t* pat, const uint32_t* l
     cudaFreeAsync(offs, st); cudaFreeAsync(tmp, st); return cuda_fail(e, "scan");
   }
   if (approx) e = launch_approx<false>(fm, g, st, Fa, pat, offs, lengths, 0, out, out_rc, m, approx, w);
-  else if (work) e = launch_fm<false, true>(fm, fm_step_of(fm), g, st, F, pat, offs, lengths, 0, out, out_rc, m, w);
-  else      e = launch_fm<false, false>(fm, fm_step_of(fm), g, st, F, pat, offs, lengths, 0, out, out_rc, m, w);
+  else if (work) e = launch_fm<false, true>(fm, fm_step_of(fm, out_rc != nullptr), g, st, F, pat, offs, lengths, 0, out, out_rc, m, w);
+  else      e = launch_fm<false, false>(fm, fm_step_of(fm, out_rc != nullptr), g, st, F, pat, offs, lengths, 0, out, out_rc, m, w);
   cudaFreeAsync(offs, st);
   cudaFreeAsync(tmp, st);
   if (e) return cuda_fail(e, "k_fm_count");

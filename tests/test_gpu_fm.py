@@ -266,7 +266,7 @@ def test_fm_tuning_does_not_change_results(cuda, bps, step, packed, refill):
         qr.qr_set_tuning("fm_blocks_per_sm", 64)
         qr.qr_set_tuning("fm_step", DEFAULT_FM_STEP)
         qr.qr_set_tuning("fm_packed", 1)
-        qr.qr_set_tuning("fm_refill", 8)
+        qr.qr_set_tuning("fm_refill", 0)
     rc = np.concatenate([(3 - fixed[i * L:(i + 1) * L][::-1]).astype(np.uint8) for i in range(m)])
     assert np.array_equal(to_host(db).view(np.uint32), ref_fixed)
     assert np.array_equal(to_host(dr).view(np.uint32),

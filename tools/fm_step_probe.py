@@ -59,7 +59,7 @@ for name, n, kind, m, L, seed in cfgs:
                               rank_gq_s=rank_gq)), flush=True)
         del q, o, c4
         steps = (1, 2, 3) if lay is None else (0, 3)
-        refills = [int(x) for x in os.environ.get("FM_REFILL", "8").split(",")]
+        refills = [int(x) for x in os.environ.get("FM_REFILL", "0").split(",")]
         packs = [int(x) for x in os.environ.get("FM_PACKED", "1").split(",")]
         for step, refill, packed in [(s_, r_, p_) for s_ in steps for r_ in (refills if s_ == 3 else [8])
                                      for p_ in (packs if s_ == 3 else [1])]:
