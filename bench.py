@@ -132,6 +132,10 @@ class Clocks:
         return out
 
 
+class RowSkipped(Exception):
+    pass
+
+
 class Ctx:
     def __init__(self, args):
         import torch
@@ -191,9 +195,21 @@ class Ctx:
 
         return gather_u64(x, self.dist, self._cd())
 
+    def agree(self, ok: bool) -> bool:
+        """True iff every rank is ok (one all_reduce MIN): a row that failed on one rank before its
+        timed region (e.g. out of memory while building) is skipped by every rank, instead of
+        leaving the others waiting in a collective."""
+        if not self.dist:
+            return ok
+        t = self.torch.tensor([1 if ok else 0], dtype=self.torch.int64, device=self._cd())
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MIN)
+        return bool(t.item())
+
     def timed(self, fn, steps: int, warmup: int) -> float:
         """ms per step: W warm-up calls, then EXACTLY K calls bracketed by barrier + synchronize,
         CUDA events on the launching stream, max over ranks.  The wall window is kept for clocks."""
+        if self.dist and not self.agree(True):
+            raise RowSkipped("another rank failed before this timed region")
         torch = self.torch
         for _ in range(warmup):
             fn()
@@ -787,15 +803,21 @@ def finalize(obj, clocks: Clocks):
     return obj
 
 
-def safe(fn, *a, **kw):
-    """A row that fails (e.g. out of memory on a smaller GPU) is reported, not fatal."""
+def safe(ctx, fn):
+    """A row that fails (e.g. out of memory on a smaller GPU) is reported, not fatal; under
+    torchrun the failing rank tells the others at their next timed region (Ctx.agree)."""
     import torch
 
     try:
         torch.cuda.empty_cache()
-        return fn(*a, **kw)
+        return fn()
+    except RowSkipped as e:
+        torch.cuda.empty_cache()
+        return {"skipped": str(e)}
     except Exception as e:
         torch.cuda.empty_cache()
+        if ctx.dist:
+            ctx.agree(False)
         return {"skipped": f"{type(e).__name__}: {str(e)[:200]}"}
 
 
@@ -863,7 +885,7 @@ def main():
         only = set(args.only.split(",")) if args.only else None
         for name, fn in spec:
             if only is None or name in only:
-                rows[name] = safe(fn)
+                rows[name] = safe(ctx, fn)
     wall_gpu = time.perf_counter() - wall0
     ms = c2["ms"]
     value = c2["gq_s"]
