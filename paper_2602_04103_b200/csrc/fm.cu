@@ -459,6 +459,71 @@ __device__ __forceinline__ void fm_step(const FmParams& F, uint32_t c, uint32_t&
   else         fm_step16<SMS, MT>(F, c, lo, hi, lines);
 }
 
+// The exact step of the approximate-search continuations: when lo and hi fall in one half line
+// (QuadRank16) or one sector (QuadRank16x2) — nearly always, the intervals there being narrow —
+// both ranks come from one gather, one delta, one superblock word and one C[c], Occ(c, hi)
+// differing from Occ(c, lo) only in the count mask; otherwise the general step.
+template <int BW>
+__device__ __forceinline__ void fm_step_cont(const FmParams& F, uint32_t c, uint32_t& lo, uint32_t& hi,
+                                             uint32_t& lines) {
+  if (BW == 0) {
+    const uint32_t j = (lo >> 5) / 7u, jh = (hi >> 5) / 7u;          // lo, hi <= N: j <= last_line
+    const uint32_t pl = lo + 32u - j * (uint32_t)QD_B, ph = hi + 32u - j * (uint32_t)QD_B;
+    const bool rx = pl >= 128u;
+    if (jh == j && (ph >= 128u) == rx) {
+      const uint64_t* L = reinterpret_cast<const uint64_t*>(F.lines) + 8 * (uint64_t)j;
+      uint64_t a0, a1, a2, a3;
+      ld_sector(L + (rx ? 4 : 0), a0, a1, a2, a3);
+      const uint64_t dr = ldg_u64_if(rx, L + (c >> 1));
+      const uint32_t sv = __ldg(F.super + 4 * (j >> QD_SB_LOG) + c);
+      const uint64_t cl = 0ull - (uint64_t)(c & 1u), ch = 0ull - (uint64_t)(c >> 1);
+      const uint64_t ma0 = (a0 ^ cl) & (a1 ^ ch), ma1 = (a2 ^ cl) & (a3 ^ ch);
+      const uint64_t inv = rx ? ~0ull : 0ull;
+      const uint32_t xx = pl & 127u, yy = ph & 127u;
+      const uint32_t d0 = min(xx, 64u), d1 = xx - d0, e0 = min(yy, 64u), e1 = yy - e0;
+      const uint32_t cx = __popcll(ma0 & (ones_shl(d0) ^ inv)) + __popcll(ma1 & (ones_shl(d1) ^ inv));
+      const uint32_t cy = __popcll(ma0 & (ones_shl(e0) ^ inv)) + __popcll(ma1 & (ones_shl(e1) ^ inv));
+      const uint64_t dw = rx ? dr : ((c & 2u) ? a1 : a0);
+      const uint32_t base = (sv << QD_SHIFT) + (uint32_t)((dw >> (16 * (c & 1u))) & 0xffffull);
+      const uint32_t dol = c == 0 ? 1u : 0u;
+      const uint32_t vx = (rx ? base + cx : base - cx) - (dol & (lo > (uint32_t)F.spos ? 1u : 0u));
+      const uint32_t vy = (rx ? base + cy : base - cy) - (dol & (hi > (uint32_t)F.spos ? 1u : 0u));
+      const uint32_t Cc = __ldg(F.Ct + c);
+      lo = Cc + vx;
+      hi = Cc + vy;
+      lines = 1;
+      return;
+    }
+    fm_step16<0, true>(F, c, lo, hi, lines);
+  } else {
+    uint32_t j, h, p, jh, hh, ph;
+    x2_locate(lo, (uint32_t)F.last_line, j, h, p);
+    x2_locate(hi, (uint32_t)F.last_line, jh, hh, ph);
+    if (jh == j && hh == h) {
+      uint64_t w0, w1, w2, w3;
+      ld_sector(F.lines + 4 * (uint64_t)j + 2 * h, w0, w1, w2, w3);
+      const uint32_t sv = __ldg(F.super + 4 * (j >> QD_SB_LOG) + c);
+      const uint64_t nl = (c & 1u) ? 0ull : ~0ull, nh = (c & 2u) ? 0ull : ~0ull;
+      const uint64_t m0 = (w1 ^ nl) & (w2 ^ nh);
+      const uint32_t m1 = ((uint32_t)w3 ^ (uint32_t)nl) & ((uint32_t)(w3 >> 32) ^ (uint32_t)nh);
+      const uint4 mx = reinterpret_cast<const uint4*>(g_x2_masks)[p];
+      const uint4 my = reinterpret_cast<const uint4*>(g_x2_masks)[ph];
+      const uint32_t cx = __popcll(m0 & (((uint64_t)mx.y << 32) | mx.x)) + __popc(m1 & mx.z);
+      const uint32_t cy = __popcll(m0 & (((uint64_t)my.y << 32) | my.x)) + __popc(m1 & my.z);
+      const uint32_t base = (sv << QD_SHIFT) + (uint32_t)((w0 >> (16 * c)) & 0xffffull);
+      const uint32_t dol = c == 0 ? 1u : 0u;
+      const uint32_t vx = (p >= 48 ? base + cx : base - cx) - (dol & (lo > (uint32_t)F.spos ? 1u : 0u));
+      const uint32_t vy = (ph >= 48 ? base + cy : base - cy) - (dol & (hi > (uint32_t)F.spos ? 1u : 0u));
+      const uint32_t Cc = __ldg(F.Ct + c);
+      lo = Cc + vx;
+      hi = Cc + vy;
+      lines = 1;
+      return;
+    }
+    fm_step_x2<0>(F, c, lo, hi, lines);
+  }
+}
+
 template <int BW>
 __global__ void k_kmer_table(FmParams F, uint2* __restrict__ table) {
   if (BW == 1) x2_masks_init();
@@ -1127,7 +1192,7 @@ __device__ __forceinline__ uint32_t fm_continue3(const FmParams& F, W& P, int64_
 #pragma unroll
     for (int r = 0; r < 3; ++r)
       if (lo[r] < hi[r]) {
-        fm_step<0, BW, true>(F, c, lo[r], hi[r], nl);
+        fm_step_cont<BW>(F, c, lo[r], hi[r], nl);
         if (WORK) { wk.ws += 1; wk.wl += nl; }
       }
   }
@@ -1142,7 +1207,7 @@ __device__ __forceinline__ uint32_t fm_continue(const FmParams& F, W& P, int64_t
                                                 FmWork& wk) {
   uint32_t nl;
   for (; k >= 0 && lo < hi; --k) {
-    fm_step<0, BW, true>(F, P.at(k), lo, hi, nl);
+    fm_step_cont<BW>(F, P.at(k), lo, hi, nl);
     if (WORK) { wk.ws += 1; wk.wl += nl; }
   }
   return lo < hi ? hi - lo : 0u;
