@@ -418,7 +418,7 @@ QR_EXPORT qr_status qr_set_tuning(const char* key, int64_t value) {
     if (value != 0 && value != 1) return fail(QR_EINVAL, "check_range must be 0 or 1");
     g_check_range = (int)value;
   } else if (!strcmp(key, "fm_step")) {
-    if (value < 0 || value > 3) return fail(QR_EINVAL, "fm_step must be 0 (auto), 1, 2 or 3");
+    if (value < 0 || value > 4) return fail(QR_EINVAL, "fm_step must be 0 (auto), 1, 2, 3 or 4");
     g_fm_lean = (int)value;
   } else if (!strcmp(key, "index64")) {
     if (value != 0 && value != 1) return fail(QR_EINVAL, "index64 must be 0 or 1");

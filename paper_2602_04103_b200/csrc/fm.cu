@@ -494,7 +494,7 @@ __device__ __forceinline__ void fm_step_cont(const FmParams& F, uint32_t c, uint
       lines = 1;
       return;
     }
-    fm_step16<0, true>(F, c, lo, hi, lines);
+    fm_step16<0, false>(F, c, lo, hi, lines);             // arithmetic masks: no shared table needed
   } else {
     uint32_t j, h, p, jh, hh, ph;
     x2_locate(lo, (uint32_t)F.last_line, j, h, p);
@@ -912,6 +912,7 @@ __global__ void __launch_bounds__(256, QR_FM_MINB) k_fm_count(FmParams F, const 
     uint32_t nl;
     if (BW == 1)        fm_step_x2<SMS>(F, c, lo, hi, nl, &C4);
     else if (STEP == 2) fm_step_lean<SMS>(F, C4, c, lo, hi, nl);
+    else if (STEP == 4) fm_step_cont<0>(F, c, lo, hi, nl);
     else                fm_step<SMS, 0>(F, c, lo, hi, nl);
     --k;
     if (WORK) { n_steps += 1; n_lines += nl; }
@@ -1552,7 +1553,7 @@ static bool bwt_l2_resident(const qr_fm* fm) {
 // with the seed pre-pass: 150-bp reads 0.533 -> 0.588 G reads/s, while one strand keeps the
 // de-duplicating step without it (configs[4] 0.96 vs 0.89 / 0.95; profiles/r02_fm_hbm_strands.log).
 static int fm_step_of(const qr_fm* fm, bool both) {
-  if (g_fm_lean >= 1 && g_fm_lean <= 3) return g_fm_lean;
+  if (g_fm_lean >= 1 && g_fm_lean <= 4) return g_fm_lean;
   return bwt_l2_resident(fm) ? 3 : both ? 2 : 1;
 }
 
@@ -1703,6 +1704,7 @@ static cudaError_t launch_fm(const qr_fm* fm, int step, unsigned g, cudaStream_t
   } while (0)
   if (step == 3) QR_FM_GO(3);
   else if (step == 2) QR_FM_GO(2);
+  else if (step == 4) QR_FM_GO(4);
   else QR_FM_GO(1);
 #undef QR_FM_GO
   e = cudaGetLastError();

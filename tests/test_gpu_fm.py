@@ -232,7 +232,7 @@ def test_fm_all_kmers_partition(cuda):
             assert int(to_host(d).astype(np.int64).sum()) == n - k + 1
 
 
-@pytest.mark.parametrize("step,packed,refill", [(1, 1, 8), (2, 1, 8), (3, 1, 8), (3, 0, 8), (3, 1, 1), (3, 1, 32)])
+@pytest.mark.parametrize("step,packed,refill", [(1, 1, 8), (2, 1, 8), (3, 1, 8), (3, 0, 8), (3, 1, 1), (3, 1, 32), (4, 1, 0)])
 @pytest.mark.parametrize("bps", [2, 16, 64])
 def test_fm_tuning_does_not_change_results(cuda, bps, step, packed, refill):
     torch = _torch()
@@ -394,7 +394,7 @@ def test_fm_kmer_width_does_not_change_counts(cuda, k):
         assert int((t[:, 1].astype(np.int64) - t[:, 0]).sum()) == n - k + 1
 
 
-@pytest.mark.parametrize("step", [1, 2, 3])
+@pytest.mark.parametrize("step", [1, 2, 3, 4])
 @pytest.mark.parametrize("fm_smem", [0, 1, 2])
 def test_fm_superblock_source_does_not_change_results(cuda, fm_smem, step):
     """The count kernel's superblock words from global memory (0), from the raw array copied to
