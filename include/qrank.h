@@ -50,7 +50,8 @@ typedef int32_t qr_status;
 #define QR_ERANGE    5  /* opt-in range check (qr_set_tuning("check_range", 1)): some q > n     */
                         /* (PAPER.md:57 defines rank for 0 <= q <= n); the call still ran —     */
                         /* memory-safe, those outputs unspecified — and qr_last_error() says   */
-                        /* how many queries were out of range                                  */
+                        /* how many queries were out of range.  The checked call synchronises  */
+                        /* its stream, so it cannot be captured in a CUDA graph.               */
 
 typedef struct qr_index qr_index;   /* a rank layout (QR_LAYOUT_*)                             */
 

@@ -1508,7 +1508,11 @@ void fm_copy_locked(const qr_fm* src, qr_fm* dst) {
 static qr_status fm_params_ax(const qr_fm* fmc, cudaStream_t st, FmParams& F) {
   qr_fm* fm = const_cast<qr_fm*>(fmc);                     // a lazily filled cache of the handle
   std::lock_guard<std::mutex> g(g_ax_mu);
-  if (fm->kmer_k_ax != fm->kmer_k_ax_want && fm->kmer_k_ax_want > 0) {
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(st, &cap) != cudaSuccess) { cudaGetLastError(); cap = cudaStreamCaptureStatusNone; }
+  // inside a CUDA-graph capture the build (allocation + synchronisation) cannot run: the captured
+  // call uses the table the handle has now (results are width-independent)
+  if (cap == cudaStreamCaptureStatusNone && fm->kmer_k_ax != fm->kmer_k_ax_want && fm->kmer_k_ax_want > 0) {
     const uint64_t nx = kmer_entries(fm->kmer_k_ax_want);
     uint2* t = nullptr;
     if (cudaMalloc((void**)&t, nx * sizeof(uint2)) != cudaSuccess) {

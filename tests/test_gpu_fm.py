@@ -846,6 +846,19 @@ def test_fm_default_width_dual_tables(cuda):
     assert not errs, errs
     for i in range(4):
         assert np.array_equal(outs[i], refs[1 + i % 2]), i
+    # a CUDA-graph capture of the first approximate call on a fresh handle: the wider table cannot
+    # be built inside the capture, the captured call uses the count's table and is exact
+    fresh2 = qr.qr_fm_build(w, n)
+    dp = to_dev(fx, cuda)
+    dg = torch.empty(m, dtype=torch.int32, device=cuda)
+    s2 = torch.cuda.Stream()
+    s2.wait_stream(torch.cuda.current_stream())
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s2):
+        qr.qr_fm_count_approx(fresh2, dp, None, L, 2, dg, m, stream=torch.cuda.current_stream())
+    g.replay()
+    torch.cuda.synchronize()
+    assert np.array_equal(to_host(dg).view(np.uint32), refs[2])
 
 
 @pytest.mark.parametrize("bwt_layout", [None, qr.QR_LAYOUT_QUADRANK16X2])
