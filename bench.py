@@ -672,6 +672,22 @@ def _time_oracle(fn, target_s: float) -> tuple[float, int]:
     return time.perf_counter() - t0, reps
 
 
+def host_info() -> dict:
+    """CPU model, logical CPUs and RAM of the host the oracle runs on."""
+    info = {"nproc": os.cpu_count(), "cpus_allowed": len(os.sched_getaffinity(0))}
+    try:
+        with open("/proc/cpuinfo") as f:
+            info["cpu_model"] = next(l.split(":", 1)[1].strip() for l in f if l.startswith("model name"))
+    except (OSError, StopIteration):
+        pass
+    try:
+        with open("/proc/meminfo") as f:
+            info["ram_gb"] = round(int(next(l.split()[1] for l in f if l.startswith("MemTotal"))) / 2**20, 1)
+    except (OSError, StopIteration):
+        pass
+    return info
+
+
 def cpu_baselines(prep: OraclePrep, target_s: float = 10.0) -> dict:
     import numpy as np
 
@@ -680,7 +696,7 @@ def cpu_baselines(prep: OraclePrep, target_s: float = 10.0) -> dict:
 
     oracle.set_threads(len(os.sched_getaffinity(0)))   # torchrun sets OMP_NUM_THREADS=1 per rank
     cores = oracle.threads()
-    out = {}
+    out = {"host": host_info()}
     ora, prep_s = prep.get("c2")
     if ora is not None:
         q = gen.queries(SEED[2], N2, 1 << 27)
@@ -748,7 +764,7 @@ def run_reference(args):
                              "sample": f"{q.size} of the configs[1] queries per step (host-regenerated), text 2^34 bits; "
                                        f"prefix-array precompute {prep:.1f}s untimed"},
             "e2e": {"value": round(v, 6), "unit": "Gqueries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-            "repo_so_loaded": repo_so_loaded()}
+            "cpu_host": host_info(), "repo_so_loaded": repo_so_loaded()}
     print(json.dumps(line), flush=True)
 
 
@@ -916,7 +932,8 @@ def main():
                      "alg_bytes_per_query": round(alg_bytes_q, 3), "peak_source": peak_src,
                      "gather_ceiling_gq_s": round(ceil0, 4), "frac_of_gather_ceiling": round(value / ceil0, 4)},
         "cpu_baseline": cpu.get("c2_rank"),
-        "cpu_baseline_rows": {k: v for k, v in cpu.items() if k != "c2_rank"},
+        "cpu_baseline_rows": {k: v for k, v in cpu.items() if k not in ("c2_rank", "host")},
+        "cpu_host": cpu.get("host"),
         "e2e": finalize(c2.get("e2e"), clocks),
         "gpu_launches": c2["launches"],
         "clocks": head_clk,
