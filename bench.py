@@ -890,6 +890,10 @@ def main():
             ("c4_quadfm_approx2", lambda: bench_fm(ctx, N4, 0, 10**6, L4, SEED[4], K, W, kmax=2)),
             ("c4_quadfm_approx2_bwt16x2", lambda: bench_fm(ctx, N4, 0, 10**6, L4, SEED[4], K, W, kmax=2,
                                                            bwt_layout=X2)),
+            # k = 3, the largest substitution count the API takes
+            ("c4_quadfm_approx3", lambda: bench_fm(ctx, N4, 0, 2 * 10**5, L4, SEED[4], K, W, kmax=3)),
+            ("c4_quadfm_approx3_bwt16x2", lambda: bench_fm(ctx, N4, 0, 2 * 10**5, L4, SEED[4], K, W, kmax=3,
+                                                           bwt_layout=X2)),
             ("c5_reads_150bp_both_strands_approx1", lambda: bench_fm(ctx, N5, 1, 10**6, 150, 55, K, W, strands=2,
                                                                      kmax=1, ptype=2)),
             ("c5_reads_150bp_both_strands_approx2", lambda: bench_fm(ctx, N5, 1, 3 * 10**5, 150, 55, K, W, strands=2,

@@ -1237,14 +1237,16 @@ __device__ __forceinline__ uint64_t approx_next(unsigned long long* ctr, uint64_
   return b + __popc(am & ((1u << lane) - 1u));
 }
 
-#ifdef QR_APPROX_MINB
-#define QR_APPROX_LB __launch_bounds__(256, QR_APPROX_MINB)
-#else
-#define QR_APPROX_LB __launch_bounds__(256)
+// k = 2, 3 (k_fm_approxk) run 4 CTAs per SM too (64 registers, ~100-160 B of spills): since the
+// frames moved to shared memory, the extra warps beat the spills — k = 2 +4.5% (BWT16) / +5%
+// (150-bp reads), k = 3 +1-2%, BWT16x2 unchanged (profiles/r02_approx_minb.log); round 1's
+// register-resident frames measured -3% / -7% with the same bound
+#ifndef QR_APPROX_MINB
+#define QR_APPROX_MINB 4
 #endif
+#define QR_APPROX_LB __launch_bounds__(256, QR_APPROX_MINB)
 // k = 1 runs 4 CTAs per SM (64 registers): +10% on the HBM-resident 150-bp reads, where the
-// search waits on DRAM (profiles/r01_reads_approx_minblocks.jsonl); k = 2, 3 keep the compiler's
-// choice (4 CTAs: -3% / -7%)
+// search waits on DRAM (profiles/r01_reads_approx_minblocks.jsonl)
 #ifndef QR_APPROX1_MINB
 #define QR_APPROX1_MINB 4
 #endif
