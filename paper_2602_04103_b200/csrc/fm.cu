@@ -1282,12 +1282,12 @@ __global__ void __launch_bounds__(256, QR_APPROX1_MINB) k_fm_approx1(FmParams F,
         const uint32_t f = (key0 >> (2 * t)) & 3u;
         uint2 iv[3];                                       // the three variants' lookups issued together
 #pragma unroll
-        for (uint32_t r = 1; r < 4; ++r) iv[r - 1] = __ldg(F.kmer + (key0 ^ ((f ^ ((f + r) & 3u)) << (2 * t))));
+        for (uint32_t r = 1; r < 4; ++r) iv[r - 1] = ld_kmer(F.kmer + (key0 ^ ((f ^ ((f + r) & 3u)) << (2 * t))));
         if (WORK) { wk.ws += 3; wk.wl += 3; }
         uint32_t vl[3] = {iv[0].x, iv[1].x, iv[2].x}, vh[3] = {iv[0].y, iv[1].y, iv[2].y};
         total += fm_continue3<BW, WORK>(F, P, (int64_t)len - 1 - F.K, vl, vh, wk);
       }
-      const uint2 iv0 = __ldg(F.kmer + key0);
+      const uint2 iv0 = ld_kmer(F.kmer + key0);
       if (WORK) { wk.ws += 1; wk.wl += 1; }
       lo = iv0.x; hi = iv0.y;
       j = (int64_t)len - 1 - F.K;
@@ -1429,7 +1429,7 @@ __global__ void QR_APPROX_LB k_fm_approxk(FmParams F, const uint8_t* __restrict_
       const uint32_t key0 = rc ? kmer_key_rc(K, P.P, p, len) : kmer_key(K, P.P, p, len);
       const uint32_t pos = len - (uint32_t)K;
       auto seed = [&](uint32_t key, int mm) {
-        const uint2 iv = __ldg(F.kmer + key);
+        const uint2 iv = ld_kmer(F.kmer + key);
         if (WORK) { wk.ws += 1; wk.wl += 1; }
         if (iv.x < iv.y) total += fm_backtrack<BW, KMAX, WORK>(F, P, Cs, iv.x, iv.y, pos, mm, wk, fr);
       };
@@ -1439,7 +1439,7 @@ __global__ void QR_APPROX_LB k_fm_approxk(FmParams F, const uint8_t* __restrict_
       auto last_level = [&](uint32_t key, int t) {
         uint2 iv[3];
 #pragma unroll
-        for (uint32_t r = 1; r < 4; ++r) iv[r - 1] = __ldg(F.kmer + kmer_subst(key, t, r));
+        for (uint32_t r = 1; r < 4; ++r) iv[r - 1] = ld_kmer(F.kmer + kmer_subst(key, t, r));
         if (WORK) { wk.ws += 3; wk.wl += 3; }
         uint32_t vl[3] = {iv[0].x, iv[1].x, iv[2].x}, vh[3] = {iv[0].y, iv[1].y, iv[2].y};
         total += fm_continue3<BW, WORK>(F, P, (int64_t)pos - 1, vl, vh, wk);

@@ -164,6 +164,17 @@ __device__ __forceinline__ void ld_sector_na(const void* p, uint64_t& w0, uint64
 __device__ __forceinline__ void ld_sector(const void* p, uint64_t& w0, uint64_t& w1, uint64_t& w2, uint64_t& w3) {
   asm volatile("ld.global.L2::64B.v4.u64 {%0,%1,%2,%3}, [%4];" : "=l"(w0), "=l"(w1), "=l"(w2), "=l"(w3) : "l"(p));
 }
+// One k-mer table entry of the approximate search (8 B at a random index of a table of up to
+// 2 GiB), read-only, not allocated in L1, L2 fill limited to its 64-B line: __ldg's default 128-B
+// fill read 4 DRAM sectors per lookup (ncu: 3.6e9 sectors for 8.6e8 lookups + 2.9e8 BWT steps at
+// k = 2); +11% / +12% / +20% patterns/s at k = 1 / 2 / 3 (profiles/r02_kmer_ld.log).  The exact
+// count's seed lookups keep __ldg: its table is L2-resident and the hinted load measured -6% there.
+// (An L2::evict_first policy on top, to shield the BWT's lines, measured no better.)
+__device__ __forceinline__ uint2 ld_kmer(const uint2* p) {
+  uint2 v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::64B.v2.u32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p));
+  return v;
+}
 // Predicated 8-byte read-only load (no branch: lanes with pred == 0 issue nothing and get 0).
 __device__ __forceinline__ uint64_t ldg_u64_if(bool pred, const void* p) {
   uint64_t v;
