@@ -28,6 +28,7 @@ int g_fm_seed = 0;              // FM seed pre-pass (dynamic order only): 0 auto
 int g_fm_smem = 1;              // FM superblock words from shared memory: 0 off, 1 auto, 2 packed table whenever it fits
 int g_fm_refill = 0;            // L2-resident count kernel: refill a warp's lanes once this many are idle (0 auto)
 int g_fm_packed = 1;            // L2-resident count kernel: packed post-seed symbols for short fixed-length batches
+int g_fm_kbits = 0;             // approximate search: presence bitmap of the k-mer table, 0 auto (sparse table), 1 never, 2 always
 int g_check_range = 0;          // 1: qr_rank / qr_rank_all4 count q > n and return QR_ERANGE (synchronous)
 int g_fm_lean = 0;              // FM step flavour: 0 auto (by L2 residency), 1 de-duplicating, 2 lean, 3 one line per iteration
 int g_index64 = 0;              // 1: force the 64-bit line-index path (tests the n >= 2^36/2^37 code on small n)
@@ -414,6 +415,9 @@ QR_EXPORT qr_status qr_set_tuning(const char* key, int64_t value) {
   } else if (!strcmp(key, "fm_packed")) {
     if (value != 0 && value != 1) return fail(QR_EINVAL, "fm_packed must be 0 or 1");
     g_fm_packed = (int)value;
+  } else if (!strcmp(key, "fm_kbits")) {
+    if (value < 0 || value > 2) return fail(QR_EINVAL, "fm_kbits must be 0 (auto), 1 (never) or 2 (always)");
+    g_fm_kbits = (int)value;
   } else if (!strcmp(key, "check_range")) {
     if (value != 0 && value != 1) return fail(QR_EINVAL, "check_range must be 0 or 1");
     g_check_range = (int)value;
@@ -998,6 +1002,8 @@ QR_EXPORT qr_status qr_fm_clone_to_device(const qr_fm* fm, int device, void* str
   c->bwt = nullptr;
   c->kmer = nullptr;
   c->kmer_ax = nullptr;
+  c->kmer_bits = nullptr;                                  // rebuilt by the clone's first approximate call
+  c->kmer_bits_k = 0;
   qr_status s = qr_clone_to_device(fm->bwt, device, stream, &c->bwt);
   if (s != QR_OK) { delete c; return s; }
   DeviceGuard dg(device);
@@ -1039,6 +1045,7 @@ QR_EXPORT void qr_fm_free(qr_fm* fm) {
   if (fm->bwt) {
     DeviceGuard dg(fm->bwt->device);
     if (fm->kmer_ax && fm->kmer_ax != fm->kmer) cudaFree(fm->kmer_ax);
+    if (fm->kmer_bits) cudaFree(fm->kmer_bits);
     if (fm->kmer) cudaFree(fm->kmer);
     qr_free(fm->bwt);
   }

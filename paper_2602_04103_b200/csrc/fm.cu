@@ -11,6 +11,7 @@
 // a lane refills itself from its grid-stride pattern sequence as soon as its pattern finishes,
 // so lanes never wait for the slowest pattern of a static batch (the GPU analogue of the
 // paper's swap-pop active list).
+#include <algorithm>
 #include <mutex>
 
 #include <cub/device/device_radix_sort.cuh>
@@ -36,6 +37,7 @@ struct FmParams {
   const uint64_t* spack;  // packed superblock table (sbcache.cu encoding, 2 parts), or null
   uint32_t spack_half;    // groups per part
   uint32_t n_super;
+  const uint32_t* kbits;  // approximate search: presence bitmap of the table (4^K bits), or null
 };
 
 // Superblock word s_{sb,c}.  SMS 0: global memory (an L2 request per read);
@@ -1222,6 +1224,73 @@ __device__ __forceinline__ void fm_occ4_pair(const FmParams& F, uint32_t lo, uin
   if (WORK) { wk.ws += 1; wk.wl += fm_line_of<BW>(F, lo) == fm_line_of<BW>(F, hi) ? 1u : 2u; }
 }
 
+// Table entry of the approximate search.  Over a text with fewer distinct K-mers than 4^K / 2
+// most of the substituted K-mers a search looks up are absent (configs[3], n = 2^26, K = 14: 78%);
+// a presence bitmap of the table (4^K bits: 32 MiB at K = 14, L2-resident next to the BWT)
+// answers those from the L2 instead of reading the 2-GiB table from HBM.
+__device__ __forceinline__ uint2 ax_lookup(const FmParams& F, uint32_t key) {
+  if (F.kbits && !((__ldg(F.kbits + (key >> 5)) >> (key & 31u)) & 1u)) return make_uint2(0u, 0u);
+  return ld_kmer(F.kmer + key);
+}
+
+// key with the symbol at key position t replaced by (old + r) mod 4, r in 1..3
+__device__ __forceinline__ uint32_t kmer_subst(uint32_t key, int t, uint32_t r) {
+  const uint32_t o = (key >> (2 * t)) & 3u;
+  return key ^ ((o ^ ((o + r) & 3u)) << (2 * t));
+}
+
+// Presence of the three substitutions at key position t (bit r - 1: symbol (old + r) mod 4).
+__device__ __forceinline__ uint32_t ax_present3(const FmParams& F, uint32_t key, int t) {
+  uint32_t m = 0;
+#pragma unroll
+  for (uint32_t r = 1; r < 4; ++r) {
+    const uint32_t k = kmer_subst(key, t, r);
+    m |= ((__ldg(F.kbits + (k >> 5)) >> (k & 31u)) & 1u) << (r - 1);
+  }
+  return m;
+}
+
+// The last substitution level of a seeded search: every K-mer one substitution away from key at
+// a position t in [t0, K) (3 (K - t0) variants) is looked up and continued as an exact search
+// from pattern position pos - 1, the three variants of a position together (fm_continue3).  With
+// the presence bitmap all 3 (K - t0) probes are issued first (independent L2 loads) and only the
+// positions with a present variant are looked up and continued.
+template <int BW, bool WORK, class W>
+__device__ __forceinline__ uint64_t ax_last_levels(const FmParams& F, W& P, uint32_t key, int t0, uint32_t pos,
+                                                   FmWork& wk) {
+  const int nb = 3 * (F.K - t0);                          // <= 42 (K <= 14)
+  uint64_t pm = nb > 0 ? ~0ull >> (64 - nb) : 0ull;
+  if (F.kbits) {
+    pm = 0;
+    for (int t = t0; t < F.K; ++t) pm |= (uint64_t)ax_present3(F, key, t) << (3 * (t - t0));
+  }
+  if (WORK && nb > 0) { wk.ws += (uint32_t)nb; wk.wl += (uint32_t)nb; }   // one table lookup per variant
+  uint64_t total = 0;
+  while (pm) {
+    const int sh = 3 * ((__ffsll((long long)pm) - 1) / 3);
+    const uint32_t g = (uint32_t)(pm >> sh) & 7u;
+    pm &= ~(7ull << sh);
+    const int t = t0 + sh / 3;
+    uint2 iv[3];
+#pragma unroll
+    for (uint32_t r = 1; r < 4; ++r)
+      iv[r - 1] = (g >> (r - 1)) & 1u ? ld_kmer(F.kmer + kmer_subst(key, t, r)) : make_uint2(0u, 0u);
+    uint32_t vl[3] = {iv[0].x, iv[1].x, iv[2].x}, vh[3] = {iv[0].y, iv[1].y, iv[2].y};
+    total += fm_continue3<BW, WORK>(F, P, (int64_t)pos - 1, vl, vh, wk);
+  }
+  return total;
+}
+
+// bits[w] bit i = (table[32 w + i] is non-empty); every lane of a warp runs the same iterations
+__global__ void k_kmer_bits(const uint2* __restrict__ table, uint64_t entries, uint32_t* __restrict__ bits) {
+  const uint64_t ent32 = (entries + 31) & ~31ull;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < ent32; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint2 v = i < entries ? table[i] : make_uint2(0u, 0u);
+    const uint32_t b = __ballot_sync(0xffffffffu, v.x < v.y);
+    if ((threadIdx.x & 31u) == 0) bits[i >> 5] = b;
+  }
+}
+
 // Next pattern index of a lane.  Static: grid stride.  Dynamic (ctr != null): the lanes that reach
 // this point together (__activemask) take consecutive indices with one atomicAdd by the first of
 // them, so a lane that finishes its pattern starts another at once instead of idling until the
@@ -1237,14 +1306,18 @@ __device__ __forceinline__ uint64_t approx_next(unsigned long long* ctr, uint64_
   return b + __popc(am & ((1u << lane) - 1u));
 }
 
-// k = 2, 3 (k_fm_approxk) run 4 CTAs per SM too (64 registers, ~100-160 B of spills): since the
-// frames moved to shared memory, the extra warps beat the spills — k = 2 +4.5% (BWT16) / +5%
-// (150-bp reads), k = 3 +1-2%, BWT16x2 unchanged (profiles/r02_approx_minb.log); round 1's
-// register-resident frames measured -3% / -7% with the same bound
+// k = 2 (k_fm_approxk) runs 4 CTAs per SM too (64 registers, ~100 B of spills): since the frames
+// moved to shared memory, the extra warps beat the spills — +4.5% (BWT16) / +5% (150-bp reads),
+// BWT16x2 unchanged (profiles/r02_approx_minb.log; round 1's register-resident frames measured
+// -3% with the same bound).  k = 3 runs 3 (80 registers): since the presence bitmap batches its
+// last-level probes, +10% over 4 CTAs on BWT16, +1% on BWT16x2 (profiles/r02_approx_kbits.log).
 #ifndef QR_APPROX_MINB
 #define QR_APPROX_MINB 4
 #endif
-#define QR_APPROX_LB __launch_bounds__(256, QR_APPROX_MINB)
+#ifndef QR_APPROX3_MINB
+#define QR_APPROX3_MINB 3
+#endif
+#define QR_APPROX_LB __launch_bounds__(256, KMAX == 3 ? QR_APPROX3_MINB : QR_APPROX_MINB)
 // k = 1 runs 4 CTAs per SM (64 registers): +10% on the HBM-resident 150-bp reads, where the
 // search waits on DRAM (profiles/r01_reads_approx_minblocks.jsonl)
 #ifndef QR_APPROX1_MINB
@@ -1278,16 +1351,9 @@ __global__ void __launch_bounds__(256, QR_APPROX1_MINB) k_fm_approx1(FmParams F,
     int64_t j;
     if (F.K && len >= (uint32_t)F.K) {
       const uint32_t key0 = rc ? kmer_key_rc(F.K, P.P, p, len) : kmer_key(F.K, P.P, p, len);
-      for (int t = 0; t < F.K; ++t) {                     // one substitution among the last K symbols
-        const uint32_t f = (key0 >> (2 * t)) & 3u;
-        uint2 iv[3];                                       // the three variants' lookups issued together
-#pragma unroll
-        for (uint32_t r = 1; r < 4; ++r) iv[r - 1] = ld_kmer(F.kmer + (key0 ^ ((f ^ ((f + r) & 3u)) << (2 * t))));
-        if (WORK) { wk.ws += 3; wk.wl += 3; }
-        uint32_t vl[3] = {iv[0].x, iv[1].x, iv[2].x}, vh[3] = {iv[0].y, iv[1].y, iv[2].y};
-        total += fm_continue3<BW, WORK>(F, P, (int64_t)len - 1 - F.K, vl, vh, wk);
-      }
-      const uint2 iv0 = ld_kmer(F.kmer + key0);
+      // one substitution among the last K symbols
+      total += ax_last_levels<BW, WORK>(F, P, key0, 0, len - (uint32_t)F.K, wk);
+      const uint2 iv0 = ax_lookup(F, key0);
       if (WORK) { wk.ws += 1; wk.wl += 1; }
       lo = iv0.x; hi = iv0.y;
       j = (int64_t)len - 1 - F.K;
@@ -1393,11 +1459,6 @@ __device__ __forceinline__ uint64_t fm_backtrack(const FmParams& F, W& P, const 
   return total;
 }
 
-// key with the symbol at key position t replaced by (old + r) mod 4, r in 1..3
-__device__ __forceinline__ uint32_t kmer_subst(uint32_t key, int t, uint32_t r) {
-  const uint32_t o = (key >> (2 * t)) & 3u;
-  return key ^ ((o ^ ((o + r) & 3u)) << (2 * t));
-}
 
 template <bool FIXED, int BW, int KMAX, int STRANDS, bool WORK = false>
 __global__ void QR_APPROX_LB k_fm_approxk(FmParams F, const uint8_t* __restrict__ pat,
@@ -1429,36 +1490,26 @@ __global__ void QR_APPROX_LB k_fm_approxk(FmParams F, const uint8_t* __restrict_
       const uint32_t key0 = rc ? kmer_key_rc(K, P.P, p, len) : kmer_key(K, P.P, p, len);
       const uint32_t pos = len - (uint32_t)K;
       auto seed = [&](uint32_t key, int mm) {
-        const uint2 iv = ld_kmer(F.kmer + key);
+        const uint2 iv = ax_lookup(F, key);
         if (WORK) { wk.ws += 1; wk.wl += 1; }
         if (iv.x < iv.y) total += fm_backtrack<BW, KMAX, WORK>(F, P, Cs, iv.x, iv.y, pos, mm, wk, fr);
       };
-      // the seeds with all KMAX substitutions inside the K-mer have none left: their three
-      // variants at the last substituted position are looked up together and continue as one
-      // interleaved exact search (fm_continue3)
-      auto last_level = [&](uint32_t key, int t) {
-        uint2 iv[3];
-#pragma unroll
-        for (uint32_t r = 1; r < 4; ++r) iv[r - 1] = ld_kmer(F.kmer + kmer_subst(key, t, r));
-        if (WORK) { wk.ws += 3; wk.wl += 3; }
-        uint32_t vl[3] = {iv[0].x, iv[1].x, iv[2].x}, vh[3] = {iv[0].y, iv[1].y, iv[2].y};
-        total += fm_continue3<BW, WORK>(F, P, (int64_t)pos - 1, vl, vh, wk);
-      };
+      // the seeds with all KMAX substitutions inside the K-mer have none left: the variants at the
+      // last substituted position are looked up and continue as exact searches (ax_last_levels)
       seed(key0, 0);
       for (int t1 = 0; t1 < K; ++t1)
         for (uint32_t r1 = 1; r1 < 4; ++r1) {
           const uint32_t k1 = kmer_subst(key0, t1, r1);
           seed(k1, 1);
-          for (int t2 = t1 + 1; t2 < K; ++t2) {
-            if (KMAX == 2) {
-              last_level(k1, t2);
-            } else {
+          if (KMAX == 2) {
+            total += ax_last_levels<BW, WORK>(F, P, k1, t1 + 1, pos, wk);
+          } else {
+            for (int t2 = t1 + 1; t2 < K; ++t2)
               for (uint32_t r2 = 1; r2 < 4; ++r2) {
                 const uint32_t k2 = kmer_subst(k1, t2, r2);
                 seed(k2, 2);
-                for (int t3 = t2 + 1; t3 < K; ++t3) last_level(k2, t3);
+                total += ax_last_levels<BW, WORK>(F, P, k2, t2 + 1, pos, wk);
               }
-            }
           }
         }
     } else {
@@ -1493,6 +1544,7 @@ static FmParams params_of(const qr_fm* fm) {
   F.bw = fm->bwt->layout == QR_LAYOUT_QUADRANK16X2 ? 1 : 0;
   F.spack_half = (uint32_t)fm->bwt->spack_half;
   F.n_super = (uint32_t)fm->bwt->n_super;
+  F.kbits = nullptr;
   return F;
 }
 
@@ -1507,6 +1559,7 @@ void fm_copy_locked(const qr_fm* src, qr_fm* dst) {
   std::lock_guard<std::mutex> g(g_ax_mu);
   *dst = *src;
 }
+extern int g_fm_kbits;
 static qr_status fm_params_ax(const qr_fm* fmc, cudaStream_t st, FmParams& F) {
   qr_fm* fm = const_cast<qr_fm*>(fmc);                     // a lazily filled cache of the handle
   std::lock_guard<std::mutex> g(g_ax_mu);
@@ -1534,6 +1587,25 @@ static qr_status fm_params_ax(const qr_fm* fmc, cudaStream_t st, FmParams& F) {
   }
   F.kmer = fm->kmer_ax;
   F.K = fm->kmer_k_ax;
+  // the presence bitmap (ax_lookup): auto = when the table is sparse, N < 4^K / 2
+  const bool bits = F.K > 0 && (g_fm_kbits == 2 || (g_fm_kbits == 0 && 2 * fm->N < kmer_entries(F.K)));
+  if (bits && cap == cudaStreamCaptureStatusNone && fm->kmer_bits_k != F.K) {
+    if (fm->kmer_bits) { cudaFree(fm->kmer_bits); fm->kmer_bits = nullptr; fm->kmer_bits_k = 0; }
+    const uint64_t nx = kmer_entries(F.K);
+    uint32_t* b = nullptr;
+    if (cudaMalloc((void**)&b, ((nx + 31) / 32) * sizeof(uint32_t)) != cudaSuccess) {
+      cudaGetLastError();                                  // no memory for it: look every K-mer up
+    } else {
+      const unsigned grid = (unsigned)std::min<uint64_t>((nx + 255) / 256, 148ull * 64);
+      k_kmer_bits<<<grid, 256, 0, st>>>(F.kmer, nx, b);
+      cudaError_t e = cudaGetLastError();
+      if (!e) e = cudaStreamSynchronize(st);
+      if (e) { cudaFree(b); return cuda_fail(e, "k_kmer_bits (approximate search)"); }
+      fm->kmer_bits = b;
+      fm->kmer_bits_k = F.K;
+    }
+  }
+  F.kbits = bits && fm->kmer_bits_k == F.K ? fm->kmer_bits : nullptr;
   return QR_OK;
 }
 

@@ -60,6 +60,8 @@ struct qr_fm {
   uint2* kmer_ax;       // the approximate-search kernels' table (== kmer unless a wider one pays there)
   int kmer_k_ax;
   int kmer_k_ax_want;   // its width; a wider table than kmer_k is built on the first approximate call
+  uint32_t* kmer_bits;  // presence bitmap of kmer_ax (bit key = its interval is non-empty), or null
+  int kmer_bits_k;      // the width it was built for (0: none)
 };
 
 namespace qr {

@@ -890,6 +890,38 @@ def test_fm_approx_all_k_both_strands(cuda, bwt_layout, dyn, n, kind):
         qr.qr_set_tuning("fm_dyn", 1)
 
 
+@pytest.mark.parametrize("n,kind,kmer_k", [(5000, 0, None), (300000, 1, 8), (300000, 0, 12)])
+def test_fm_approx_presence_bitmap(cuda, n, kind, kmer_k):
+    """The approximate search's k-mer presence bitmap (fm_kbits: 0 auto = sparse tables only,
+    1 never, 2 always) changes no count: k = 1, 2, 3 on both strands against the oracle with the
+    bitmap off, forced on (also over a dense table, n = 300000 at K = 8) and auto, switched back
+    and forth on one handle (built on first use, kept for later calls)."""
+    torch = _torch()
+    w = gen.dna(1300 + n, n, kind)
+    sym = gen.unpack_dna(w, n)
+    fm = qr.qr_fm_build(w, n, kmer_k=kmer_k) if kmer_k else qr.qr_fm_build(w, n)
+    rng = np.random.default_rng(n + 7)
+    pats = mixed_patterns(rng, sym, 120)
+    cat, off, lens = oracle.pack_patterns(pats)
+    rc = [revcomp(p) for p in pats]
+    rcat, roff, rlens = oracle.pack_patterns(rc)
+    refs = {k: (oracle.scan_count_hdk(sym, cat, off, lens, k), oracle.scan_count_hdk(sym, rcat, roff, rlens, k))
+            for k in (1, 2, 3)}
+    dp, dl = to_dev(cat, cuda), to_dev(lens, cuda)
+    try:
+        for knob in (1, 2, 0, 1, 2):
+            qr.qr_set_tuning("fm_kbits", knob)
+            for kmax in (1, 2, 3):
+                df = torch.empty(lens.size, dtype=torch.int32, device=cuda)
+                dr = torch.empty(lens.size, dtype=torch.int32, device=cuda)
+                qr.qr_fm_count_approx_both(fm, dp, dl, 0, kmax, df, dr, lens.size)
+                torch.cuda.synchronize()
+                assert np.array_equal(to_host(df).view(np.uint32), refs[kmax][0]), (knob, kmax)
+                assert np.array_equal(to_host(dr).view(np.uint32), refs[kmax][1]), (knob, kmax)
+    finally:
+        qr.qr_set_tuning("fm_kbits", 0)
+
+
 @pytest.mark.parametrize("space", ["host", "device"])
 def test_fm_build_from_bytes(cuda, space):
     """qr_fm_build_u8 (one byte per symbol, SURVEY §8(b)'s input form, packed on the GPU) builds

@@ -155,14 +155,14 @@ def test_tuning_knob_validation():
     ok = {
         "rank_smem": [0, 1, 2], "rank_dyn": [0, 1], "rank_smem_k": [0, 1, 2, 3, 4, 6, 8],
         "rank_smem_clusters": [0, 1, 74, 4096], "fm_dyn": [0, 1], "fm_seed": [0, 1, 2], "fm_smem": [0, 1, 2],
-        "fm_step": [0, 1, 2, 3, 4], "fm_packed": [0, 1], "check_range": [0, 1], "fm_refill": [0, 1, 8, 32], "rank_pair": [0, 1, 2], "rank_s_lane": [0, 1], "index64": [0, 1],
+        "fm_step": [0, 1, 2, 3, 4], "fm_packed": [0, 1], "fm_kbits": [0, 1, 2], "check_range": [0, 1], "fm_refill": [0, 1, 8, 32], "rank_pair": [0, 1, 2], "rank_s_lane": [0, 1], "index64": [0, 1],
         "rank_k": [1, 2, 4, 8], "rank_blocks_per_sm": [1, 64], "fm_blocks_per_sm": [1, 64],
         "stage_slots": [2, 4], "stage_chunk": [1024, 1 << 23], "rank_resident": [0, 1], "rank_big_pack": [0, 1],
         "rank_big_cs": [0, 4, 8, 16],
     }
     bad = {
         "rank_smem": [-1, 3], "rank_dyn": [2], "rank_smem_k": [5, 7, 16], "rank_smem_clusters": [-1, 4097],
-        "fm_dyn": [2], "fm_seed": [3], "fm_smem": [3], "fm_step": [5, -1], "fm_packed": [2], "check_range": [2, -1], "fm_refill": [-1, 33], "rank_pair": [3, -1], "rank_s_lane": [2],
+        "fm_dyn": [2], "fm_seed": [3], "fm_smem": [3], "fm_step": [5, -1], "fm_packed": [2], "fm_kbits": [3, -1], "check_range": [2, -1], "fm_refill": [-1, 33], "rank_pair": [3, -1], "rank_s_lane": [2],
         "index64": [2], "rank_k": [0, 3], "rank_blocks_per_sm": [0, 65], "fm_blocks_per_sm": [0, 65],
         "stage_slots": [1, 5], "stage_chunk": [1023], "rank_resident": [2, -1], "rank_big_pack": [2],
         "rank_big_cs": [2, 32],
@@ -182,7 +182,7 @@ def test_tuning_knob_validation():
             assert L.qr_set_tuning(b"rank_smem_threads", t) == st, (k, t)
     finally:
         for key, v in (("rank_smem", 1), ("rank_dyn", 1), ("rank_smem_k", 0), ("rank_smem_clusters", 0), ("fm_dyn", 1),
-                       ("fm_seed", 0), ("fm_smem", 1), ("fm_step", 0), ("fm_packed", 1), ("check_range", 0), ("fm_refill", 0), ("rank_pair", 2), ("rank_s_lane", 1),
+                       ("fm_seed", 0), ("fm_smem", 1), ("fm_step", 0), ("fm_packed", 1), ("fm_kbits", 0), ("check_range", 0), ("fm_refill", 0), ("rank_pair", 2), ("rank_s_lane", 1),
                        ("index64", 0), ("rank_k", 2), ("rank_blocks_per_sm", 64), ("fm_blocks_per_sm", 64),
                        ("stage_slots", 3), ("stage_chunk", 1 << 23), ("rank_resident", 1), ("rank_big_pack", 0),
                        ("rank_big_cs", 0)):
