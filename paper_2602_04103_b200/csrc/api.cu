@@ -33,8 +33,6 @@ int g_check_range = 0;          // 1: qr_rank / qr_rank_all4 count q > n and ret
 int g_fm_lean = 0;              // FM step flavour: 0 auto (by L2 residency), 1 de-duplicating, 2 lean, 3 one line per iteration
 int g_index64 = 0;              // 1: force the 64-bit line-index path (tests the n >= 2^36/2^37 code on small n)
 int g_rank_smem = 1;            // superblock words from cluster shared memory: 0 never, 1 large batches, 2 always
-extern int g_rank_bucket, g_rank_bucket_shift, g_rank_bucket_dshift;   // bucket.cu
-extern uint64_t g_rank_bucket_chunk;
 int g_rank_dyn = 1;             // cluster rank kernels: 1 = dynamic (atomic chunk) work order, 0 = static grid stride
 int g_rank_smem_clusters = 0;   // cluster rank kernels: 0 = as many 2-CTA clusters as fit (occupancy API), else this many
 int g_rank_smem_threads = 0;    // cluster rank kernels: CTA size (0 auto: 1024, 768 for K = 6, 512 for K = 8)
@@ -399,18 +397,6 @@ QR_EXPORT qr_status qr_set_tuning(const char* key, int64_t value) {
   } else if (!strcmp(key, "rank_big_cs")) {
     if (value != 0 && value != 4 && value != 8 && value != 16) return fail(QR_EINVAL, "rank_big_cs must be 0, 4, 8 or 16");
     g_rank_big_cs = (int)value;
-  } else if (!strcmp(key, "rank_bucket")) {
-    if (value < 0 || value > 2) return fail(QR_EINVAL, "rank_bucket must be 0 (never), 1 (auto) or 2 (always)");
-    g_rank_bucket = (int)value;
-  } else if (!strcmp(key, "rank_bucket_shift")) {
-    if (value < 0 || value > 22) return fail(QR_EINVAL, "rank_bucket_shift must be 0 (auto) or 1..22");
-    g_rank_bucket_shift = (int)value;
-  } else if (!strcmp(key, "rank_bucket_dshift")) {
-    if (value < 0 || value > 28) return fail(QR_EINVAL, "rank_bucket_dshift must be 0 (auto) or 1..28");
-    g_rank_bucket_dshift = (int)value;
-  } else if (!strcmp(key, "rank_bucket_chunk")) {
-    if (value < 1 || value > (1ll << 31)) return fail(QR_EINVAL, "rank_bucket_chunk must be 1..2^31");
-    g_rank_bucket_chunk = (uint64_t)value;
   } else if (!strcmp(key, "rank_dyn")) {
     if (value != 0 && value != 1) return fail(QR_EINVAL, "rank_dyn must be 0 or 1");
     g_rank_dyn = (int)value;

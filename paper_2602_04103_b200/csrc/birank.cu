@@ -354,11 +354,6 @@ static cudaError_t bi_rank_k(const qr_index* h, const uint64_t* q, const uint8_t
 cudaError_t launch_birank_rank(const qr_index* h, const uint64_t* q, const uint8_t* c, uint64_t* out, uint64_t m,
                                cudaStream_t st) {
   if (m == 0) return cudaSuccess;
-  // large batches over structures >> L2: queries regrouped by line region (bucket.cu)
-  if (bucket_eligible(h, m)) {
-    const cudaError_t e = launch_bucket_rank(h, q, c, out, m, st);
-    if (e != cudaErrorNotSupported) return e;
-  }
   // n >= 2^35 (or forced for tests): superblock words from a CS-CTA cluster table (sbcache.cu)
   if (h->spack_big && g_rank_smem != 0 && m >= (1ull << 22) && !g_index64) return launch_big_pack_rank(h, q, c, out, m, st);
   const int shape = rank_shape(h, m);

@@ -104,9 +104,6 @@ cudaError_t launch_variant(const qr_index* h, const uint64_t* q, const uint8_t* 
                            cudaStream_t st);
 
 // kernel launchers (device pointers; validated by api.cu)
-bool bucket_eligible(const qr_index* h, uint64_t m);
-cudaError_t launch_bucket_rank(const qr_index* h, const uint64_t* q, const uint8_t* c, uint64_t* out, uint64_t m,
-                               cudaStream_t st);
 cudaError_t launch_birank_rank(const qr_index* h, const uint64_t* q, const uint8_t* c, uint64_t* out, uint64_t m,
                                cudaStream_t st);
 cudaError_t launch_quadrank_rank(const qr_index* h, const uint64_t* q, const uint8_t* c, uint64_t* out, uint64_t m,
