@@ -1551,6 +1551,277 @@ __global__ void QR_APPROX_LB k_fm_approxk(FmParams F, const uint8_t* __restrict_
   }
 }
 
+// ---- approximate counting with <= 1 substitution, breadth first (default for k = 1) ---------
+// The same decomposition as k_fm_approx1 (count_{<=1} = exact + every single-substitution branch,
+// PAPER.md:139-140), run level by level so that every lane of a warp does the same kind of work:
+//   k_ax1_seed  one thread per task: the exact seed interval of the last K symbols and the 3K
+//               one-substitution K-mers present in the table (presence bitmap, or all of them),
+//               written as lookup items (task, key) to a queue of exact size;
+//   k_ax1_path  the exact path below the seed with rank_4 at both ends (one step per lane and
+//               iteration, lanes refilled from the task range): the three substituted children
+//               of every step go to a second queue as interval items (task, pos, lo, hi);
+//   k_ax1_cont  (once per queue) plain exact searches of the items, one step per lane and
+//               iteration, refilled from the queue; each adds its count to the task's output.
+// In the recursive kernel a lane walks its pattern's exact path and, at every step, the
+// continuations of its three branches, so the lanes of a warp sit in different loops (ncu: ~11
+// of 32 lanes per instruction) and each lane's dependent gathers serialise behind the others'.
+// Interval items that do not fit the second queue (sized for ~4 per task) are continued by the
+// emitting lane itself.
+struct Ax1Ctl {                 // device counters of one chunk (zeroed before the chunk)
+  unsigned long long zq_n, aq_n, ctr_path, ctr_z, ctr_a;
+};
+
+template <bool FIXED, int STRANDS>
+__device__ __forceinline__ const uint8_t* ax_pattern(const uint8_t* pat, const uint64_t* offs, const uint32_t* lens,
+                                                     uint32_t fixed_len, uint64_t ti, uint32_t& len, uint32_t& rc) {
+  const uint64_t pi = STRANDS == 2 ? ti >> 1 : ti;
+  rc = STRANDS == 2 ? (uint32_t)(ti & 1) : 0u;
+  len = FIXED ? fixed_len : lens[pi];
+  return pat + (FIXED ? pi * (uint64_t)fixed_len : offs[pi]);
+}
+template <int STRANDS>
+__device__ __forceinline__ uint32_t* ax_out(uint32_t* out, uint32_t* out_rc, uint64_t ti) {
+  return (STRANDS == 2 && (ti & 1)) ? out_rc + (ti >> 1) : out + (STRANDS == 2 ? ti >> 1 : ti);
+}
+
+template <bool FIXED, int STRANDS, bool WORK>
+__global__ void __launch_bounds__(256) k_ax1_seed(FmParams F, const uint8_t* __restrict__ pat,
+                                                  const uint64_t* __restrict__ offs, const uint32_t* __restrict__ lens,
+                                                  uint32_t fixed_len, uint32_t* __restrict__ out,
+                                                  uint32_t* __restrict__ out_rc, uint64_t t0, uint64_t t1,
+                                                  uint2* __restrict__ seeds, uint2* __restrict__ zq, Ax1Ctl* ctl,
+                                                  unsigned long long* __restrict__ work) {
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint64_t warps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  uint64_t ws = 0;
+  for (uint64_t w0 = t0 + (((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) & ~31ull); w0 < t1; w0 += warps * 32) {
+    const uint64_t ti = w0 + lane;
+    const bool valid = ti < t1;
+    uint64_t pm = 0;
+    uint32_t key0 = 0, direct = 0;
+    if (valid) {
+      uint32_t len, rc;
+      const uint8_t* p = ax_pattern<FIXED, STRANDS>(pat, offs, lens, fixed_len, ti, len, rc);
+      uint2 iv0 = make_uint2(0u, (uint32_t)F.N);
+      if (F.K && len >= (uint32_t)F.K) {
+        PatWindow P;
+        P.reset(p);
+        key0 = rc ? kmer_key_rc(F.K, P, p, len) : kmer_key(F.K, P, p, len);
+        iv0 = ax_lookup(F, key0);
+        const int nb = 3 * F.K;
+        if (F.kbits) {
+          for (int t = 0; t < F.K; ++t) pm |= (uint64_t)ax_present3(F, key0, t) << (3 * t);
+        } else {
+          pm = ~0ull >> (64 - nb);
+        }
+        if (WORK) ws += (uint64_t)nb + 1;
+        if (len == (uint32_t)F.K) {                       // nothing left to continue: add directly
+          for (; pm; pm &= pm - 1) {
+            const int b = __ffsll((long long)pm) - 1;
+            const uint2 iv = ld_kmer(F.kmer + kmer_subst(key0, b / 3, (uint32_t)(b % 3) + 1));
+            direct += iv.x < iv.y ? iv.y - iv.x : 0u;
+          }
+        }
+      }
+      seeds[ti - t0] = iv0;
+      *ax_out<STRANDS>(out, out_rc, ti) = direct;
+    }
+    // reserve the warp's lookup items with one atomic, then write them
+    const uint32_t n = (uint32_t)__popcll(pm);
+    uint32_t incl = n;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= (uint32_t)o) incl += v;
+    }
+    const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
+    unsigned long long base = 0;
+    if (lane == 31 && tot) base = atomicAdd(&ctl->zq_n, (unsigned long long)tot);
+    base = __shfl_sync(0xffffffffu, base, 31) + (incl - n);
+    for (; pm; pm &= pm - 1) {
+      const int b = __ffsll((long long)pm) - 1;
+      zq[base++] = make_uint2((uint32_t)ti, kmer_subst(key0, b / 3, (uint32_t)(b % 3) + 1));
+    }
+  }
+  if (WORK && ws) { atomicAdd(work, (unsigned long long)ws); atomicAdd(work + 1, (unsigned long long)ws); }
+}
+
+// Warp-uniform refill of the lanes without a task from a range of indices [0, total) taken in
+// chunks of FM_CHUNK from a global counter (as in k_fm_count).  Returns false once the range is
+// exhausted and no lane holds a task.
+struct AxRefill {
+  uint64_t cb = 0, ce = 0;
+  bool exhausted = false;
+  template <class Seed>
+  __device__ __forceinline__ bool run(bool& has, uint64_t total, unsigned long long* ctr, Seed&& seed) {
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint32_t needm = __ballot_sync(0xffffffffu, !has);
+    if (needm && !exhausted) {
+      const uint32_t cnt = __popc(needm), r = __popc(needm & ((1u << lane) - 1u));
+      const uint64_t avail = ce - cb;
+      uint64_t nb = 0, ne = 0;
+      if (cnt > avail) {
+        if (lane == 0) nb = atomicAdd(ctr, (unsigned long long)FM_CHUNK);
+        nb = __shfl_sync(0xffffffffu, nb, 0);
+        ne = nb + FM_CHUNK < total ? nb + FM_CHUNK : total;
+        if (nb >= total) { exhausted = true; nb = ne = total; }
+      }
+      if (!has) {
+        const uint64_t t = r < avail ? cb + r : nb + (r - avail);
+        if (r < avail || t < ne) { seed(t); has = true; }
+      }
+      if (cnt > avail) {
+        const uint64_t take = cnt - avail;
+        cb = nb + take < ne ? nb + take : ne;
+        ce = ne;
+      } else {
+        cb += cnt;
+      }
+    }
+    return !(exhausted && __ballot_sync(0xffffffffu, has) == 0);
+  }
+};
+
+template <bool FIXED, int BW, int STRANDS, bool WORK>
+__global__ void __launch_bounds__(256, QR_APPROX1_MINB) k_ax1_path(FmParams F, const uint8_t* __restrict__ pat,
+                                                    const uint64_t* __restrict__ offs,
+                                                    const uint32_t* __restrict__ lens, uint32_t fixed_len,
+                                                    uint32_t* __restrict__ out, uint32_t* __restrict__ out_rc,
+                                                    uint64_t t0, uint64_t t1, const uint2* __restrict__ seeds,
+                                                    uint4* __restrict__ aq, uint64_t aq_cap, Ax1Ctl* ctl,
+                                                    unsigned long long* __restrict__ work) {
+  FmWork wk;
+  if (BW == 1) x2_masks_init();
+  else qd_masks_init();
+  const uint4 C4 = __ldg(reinterpret_cast<const uint4*>(F.Ct));
+  const uint32_t Cs[4] = {C4.x, C4.y, C4.z, C4.w};
+  const uint32_t lane = threadIdx.x & 31u;
+  StrandWindow<STRANDS> P;
+  uint64_t ti = 0;
+  uint32_t lo = 0, hi = 0, total = 0;
+  int32_t j = -1;
+  bool has = false;
+  AxRefill rf;
+  auto seed = [&](uint64_t t) {
+    ti = t0 + t;
+    uint32_t len, rc;
+    const uint8_t* p = ax_pattern<FIXED, STRANDS>(pat, offs, lens, fixed_len, ti, len, rc);
+    P.reset(p, len, rc);
+    const uint2 iv = seeds[t];
+    lo = iv.x; hi = iv.y;
+    j = (int32_t)len - 1 - ((F.K && len >= (uint32_t)F.K) ? F.K : 0);
+    total = 0;
+  };
+  while (rf.run(has, t1 - t0, &ctl->ctr_path, seed)) {
+    uint32_t cl[3] = {0u, 0u, 0u}, ch[3] = {0u, 0u, 0u}, n = 0;
+    int32_t jc = 0;
+    if (has) {
+      if (j >= 0 && lo < hi) {
+        uint32_t ol[4], oh[4];
+        fm_occ4_pair<BW, WORK>(F, lo, hi, ol, oh, wk);
+        const uint32_t cj = P.at(j);
+#pragma unroll
+        for (uint32_t r = 0; r < 3; ++r) {
+          const uint32_t c = (cj + 1 + r) & 3u;
+          const uint32_t bl = Cs[c] + ol[c], bh = Cs[c] + oh[c];
+          if (bl < bh) {
+            if (j == 0) total += bh - bl;                 // substitution at P[0]: a leaf
+            else { cl[n] = bl; ch[n] = bh; ++n; }
+          }
+        }
+        jc = j;
+        lo = Cs[cj] + ol[cj];
+        hi = Cs[cj] + oh[cj];
+        --j;
+      }
+    }
+    // the warp's new interval items (0..3 per lane): one atomic per warp that has any
+    if (__ballot_sync(0xffffffffu, n != 0)) {
+      const uint32_t lt = (1u << lane) - 1u;
+      const uint32_t b0 = __ballot_sync(0xffffffffu, n & 1u), b1 = __ballot_sync(0xffffffffu, (n >> 1) & 1u);
+      const uint32_t tot = __popc(b0) + 2u * __popc(b1);
+      unsigned long long base = 0;
+      if (lane == 0) base = atomicAdd(&ctl->aq_n, (unsigned long long)tot);
+      base = __shfl_sync(0xffffffffu, base, 0) + __popc(b0 & lt) + 2u * __popc(b1 & lt);
+      for (uint32_t r = 0; r < n; ++r) {
+        if (base + r < aq_cap) aq[base + r] = make_uint4((uint32_t)ti, (uint32_t)jc, cl[r], ch[r]);
+        else total += fm_continue<BW, WORK>(F, P, (int64_t)jc - 1, cl[r], ch[r], wk);   // queue full
+      }
+    }
+    if (has && !(j >= 0 && lo < hi)) {                   // finished: exact count + leaves
+      if (lo < hi) total += hi - lo;
+      uint32_t* o = ax_out<STRANDS>(out, out_rc, ti);
+      *o += total;
+      has = false;
+    }
+  }
+  if (WORK && wk.ws) {
+    atomicAdd(work, (unsigned long long)wk.ws);
+    atomicAdd(work + 1, (unsigned long long)wk.wl);
+  }
+}
+
+// LOOKUP: items are (task, key) of k_ax1_seed, the interval read from the table at refill
+// (resolving them in k_ax1_seed instead measured 1.35x slower on configs[3]: its lanes then walk
+// 3K dependent lookups, and the queue doubles); else (task, pos, lo, hi) of k_ax1_path.  Exact
+// backward search of P[pos-1 .. 0] from the interval, one step per lane and iteration.
+template <bool FIXED, int BW, int STRANDS, bool WORK, bool LOOKUP>
+__global__ void __launch_bounds__(256, QR_APPROX1_MINB) k_ax1_cont(FmParams F, const uint8_t* __restrict__ pat,
+                                                    const uint64_t* __restrict__ offs,
+                                                    const uint32_t* __restrict__ lens, uint32_t fixed_len,
+                                                    uint32_t* __restrict__ out, uint32_t* __restrict__ out_rc,
+                                                    const void* __restrict__ items, uint64_t cap, Ax1Ctl* ctl,
+                                                    unsigned long long* __restrict__ work) {
+  FmWork wk;
+  if (BW == 1) x2_masks_init();
+  const unsigned long long nq = LOOKUP ? ctl->zq_n : ctl->aq_n;
+  const uint64_t total_items = nq < cap ? nq : cap;
+  StrandWindow<STRANDS> P;
+  uint64_t ti = 0;
+  uint32_t lo = 0, hi = 0;
+  int32_t j = -1;
+  bool has = false;
+  AxRefill rf;
+  auto seed = [&](uint64_t t) {
+    uint32_t len, rc;
+    if (LOOKUP) {
+      const uint2 it = reinterpret_cast<const uint2*>(items)[t];
+      ti = it.x;
+      const uint8_t* p = ax_pattern<FIXED, STRANDS>(pat, offs, lens, fixed_len, ti, len, rc);
+      P.reset(p, len, rc);
+      const uint2 iv = ld_kmer(F.kmer + it.y);
+      lo = iv.x; hi = iv.y;
+      j = (int32_t)len - 1 - F.K;
+    } else {
+      const uint4 it = reinterpret_cast<const uint4*>(items)[t];
+      ti = it.x;
+      const uint8_t* p = ax_pattern<FIXED, STRANDS>(pat, offs, lens, fixed_len, ti, len, rc);
+      P.reset(p, len, rc);
+      lo = it.z; hi = it.w;
+      j = (int32_t)it.y - 1;
+    }
+  };
+  unsigned long long* ctr = LOOKUP ? &ctl->ctr_z : &ctl->ctr_a;
+  while (rf.run(has, total_items, ctr, seed)) {
+    if (has) {
+      if (j >= 0 && lo < hi) {
+        uint32_t nl;
+        fm_step_cont<BW>(F, P.at(j), lo, hi, nl);
+        if (WORK) { wk.ws += 1; wk.wl += nl; }
+        --j;
+      }
+      if (!(j >= 0 && lo < hi)) {
+        if (lo < hi) atomicAdd(ax_out<STRANDS>(out, out_rc, ti), hi - lo);
+        has = false;
+      }
+    }
+  }
+  if (WORK && wk.ws) {
+    atomicAdd(work, (unsigned long long)wk.ws);
+    atomicAdd(work + 1, (unsigned long long)wk.wl);
+  }
+}
+
 __global__ void k_u32_to_u64(const uint32_t* __restrict__ a, uint64_t* __restrict__ b, uint64_t m) {
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m; i += (uint64_t)gridDim.x * blockDim.x)
     b[i] = a[i];
@@ -1587,6 +1858,7 @@ void fm_copy_locked(const qr_fm* src, qr_fm* dst) {
   *dst = *src;
 }
 extern int g_fm_kbits;
+extern int g_fm_ax_bfs;
 static qr_status fm_params_ax(const qr_fm* fmc, cudaStream_t st, FmParams& F) {
   qr_fm* fm = const_cast<qr_fm*>(fmc);                     // a lazily filled cache of the handle
   std::lock_guard<std::mutex> g(g_ax_mu);
@@ -1821,10 +2093,65 @@ static cudaError_t launch_fm(const qr_fm* fm, int step, unsigned g, cudaStream_t
   return e;
 }
 
+template <typename Kern>
+static unsigned resident_grid(Kern k, int sms, size_t smem = 0) {
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, 256, smem) != cudaSuccess || per_sm <= 0) {
+    cudaGetLastError();
+    per_sm = 1;
+  }
+  return (unsigned)per_sm * (unsigned)sms;
+}
+
+// k = 1 breadth first (k_ax1_*), tasks in chunks so that the lookup queue (exactly 3K per task
+// at most) and the interval queue (~4 per task) stay within the pool's kept 2 GiB.
+uint64_t g_ax1_aq_per_task = 4;   // interval-queue items per task (tests: 0 sends every item inline)
+template <bool FIXED, int STRANDS, bool WORK>
+static cudaError_t launch_ax1_bfs(const qr_fm* fm, cudaStream_t st, const FmParams& F, const uint8_t* pat,
+                                  const uint64_t* offs, const uint32_t* lens, uint32_t fixed_len, uint32_t* out,
+                                  uint32_t* out_rc, uint64_t m, unsigned long long* work) {
+  const uint64_t ntask = m * STRANDS;
+  const uint64_t per_task_z = 3ull * (uint64_t)(F.K > 0 ? F.K : 0);
+  const uint64_t chunk = ntask < (1ull << 22) ? ntask : (1ull << 22);
+  const uint64_t aq_cap = chunk * g_ax1_aq_per_task;
+  const size_t aq_off = (256 + chunk * 8 + chunk * per_task_z * 8 + 255) & ~(size_t)255;   // uint4 items: 16-B aligned
+  const size_t bytes = aq_off + aq_cap * 16 + 16;
+  keep_pool_memory(fm->bwt->device, st);
+  unsigned char* buf = nullptr;
+  cudaError_t e = cudaMallocAsync((void**)&buf, bytes, st);
+  if (e) return e;
+  Ax1Ctl* ctl = reinterpret_cast<Ax1Ctl*>(buf);
+  uint2* seeds = reinterpret_cast<uint2*>(buf + 256);
+  uint2* zq = seeds + chunk;
+  uint4* aq = reinterpret_cast<uint4*>(buf + aq_off);
+  const int sms = fm->bwt->sm_count;
+  auto kp = F.bw ? k_ax1_path<FIXED, 1, STRANDS, WORK> : k_ax1_path<FIXED, 0, STRANDS, WORK>;
+  auto kz = F.bw ? k_ax1_cont<FIXED, 1, STRANDS, WORK, true> : k_ax1_cont<FIXED, 0, STRANDS, WORK, true>;
+  auto ka = F.bw ? k_ax1_cont<FIXED, 1, STRANDS, WORK, false> : k_ax1_cont<FIXED, 0, STRANDS, WORK, false>;
+  const unsigned gp = resident_grid(kp, sms), gz = resident_grid(kz, sms), ga = resident_grid(ka, sms);
+  for (uint64_t t0 = 0; t0 < ntask && !e; t0 += chunk) {
+    const uint64_t t1 = t0 + chunk < ntask ? t0 + chunk : ntask;
+    if ((e = cudaMemsetAsync(ctl, 0, sizeof(Ax1Ctl), st))) break;
+    k_ax1_seed<FIXED, STRANDS, WORK><<<grid_stride_blocks(t1 - t0, 256, sms, 8), 256, 0, st>>>(
+        F, pat, offs, lens, fixed_len, out, out_rc, t0, t1, seeds, zq, ctl, work);
+    kp<<<gp, 256, 0, st>>>(F, pat, offs, lens, fixed_len, out, out_rc, t0, t1, seeds, aq, aq_cap, ctl, work);
+    kz<<<gz, 256, 0, st>>>(F, pat, offs, lens, fixed_len, out, out_rc, zq, (t1 - t0) * per_task_z, ctl, work);
+    ka<<<ga, 256, 0, st>>>(F, pat, offs, lens, fixed_len, out, out_rc, aq, aq_cap, ctl, work);
+    e = cudaGetLastError();
+  }
+  cudaError_t e2 = cudaFreeAsync(buf, st);
+  return e ? e : e2;
+}
+
 template <bool FIXED, int STRANDS, bool WORK>
 static cudaError_t launch_approx_s(const qr_fm* fm, unsigned g, cudaStream_t st, const FmParams& F, const uint8_t* pat,
                                    const uint64_t* offs, const uint32_t* lens, uint32_t fixed_len, uint32_t* out,
                                    uint32_t* out_rc, uint64_t m, int kmax, unsigned long long* work) {
+  // breadth first (auto): 1.89x on the 150-bp reads (HBM-resident BWT), +2.4% on configs[3]; the
+  // recursive kernel stays on an L2-resident QuadRank16x2 BWT (1.68 vs 1.50 G patterns/s there)
+  const bool bfs = g_fm_ax_bfs == 2 || (g_fm_ax_bfs == 1 && !(F.bw == 1 && bwt_l2_resident(fm)));
+  if (kmax == 1 && bfs && g_fm_dyn && m * STRANDS < (1ull << 32))
+    return launch_ax1_bfs<FIXED, STRANDS, WORK>(fm, st, F, pat, offs, lens, fixed_len, out, out_rc, m, work);
   auto kern = kmax == 1 ? (F.bw ? k_fm_approx1<FIXED, 1, STRANDS, WORK> : k_fm_approx1<FIXED, 0, STRANDS, WORK>)
             : kmax == 2 ? (F.bw ? k_fm_approxk<FIXED, 1, 2, STRANDS, WORK> : k_fm_approxk<FIXED, 0, 2, STRANDS, WORK>)
                         : (F.bw ? k_fm_approxk<FIXED, 1, 3, STRANDS, WORK> : k_fm_approxk<FIXED, 0, 3, STRANDS, WORK>);
