@@ -15,7 +15,8 @@ CFLAGS  := -O2 -fPIC -fopenmp -std=c11 -Wall -Wno-unused-function
 PKG     := paper_2602_04103_b200
 QR_SRC  := $(wildcard $(PKG)/csrc/*.cu)
 QR_HDR  := $(wildcard $(PKG)/csrc/*.cuh) include/qrank.h
-QR_OBJ  := $(patsubst $(PKG)/csrc/%.cu,build/qr_%.o,$(QR_SRC))
+BUILD   ?= build
+QR_OBJ  := $(patsubst $(PKG)/csrc/%.cu,$(BUILD)/qr_%.o,$(QR_SRC))
 
 all: gen/libqrgen_host.so gen/libqrgen_dev.so oracle/liboracle.so $(if $(QR_SRC),$(PKG)/lib/libqrank.so examples/qrank_demo)
 
@@ -28,9 +29,9 @@ gen/libqrgen_dev.so: gen/qrgen_dev.cu gen/qrgen.h
 oracle/liboracle.so: oracle/oracle.c
 	$(HOSTCC) $(CFLAGS) -shared -o $@ oracle/oracle.c
 
-build/qr_%.o: $(PKG)/csrc/%.cu $(QR_HDR)
-	@mkdir -p build
-	$(NVCC) $(NVFLAGS) -c -o $@ $< 2> build/qr_$*.ptxas.txt || (cat build/qr_$*.ptxas.txt; false)
+$(BUILD)/qr_%.o: $(PKG)/csrc/%.cu $(QR_HDR)
+	@mkdir -p $(BUILD)
+	$(NVCC) $(NVFLAGS) -c -o $@ $< 2> $(BUILD)/qr_$*.ptxas.txt || (cat $(BUILD)/qr_$*.ptxas.txt; false)
 
 $(PKG)/lib/libqrank.so: $(QR_OBJ)
 	@mkdir -p $(PKG)/lib

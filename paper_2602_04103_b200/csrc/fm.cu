@@ -1567,6 +1567,9 @@ __global__ void QR_APPROX_LB k_fm_approxk(FmParams F, const uint8_t* __restrict_
 // of 32 lanes per instruction) and each lane's dependent gathers serialise behind the others'.
 // Interval items that do not fit the second queue (sized for ~4 per task) are continued by the
 // emitting lane itself.
+__device__ __forceinline__ uint32_t sel4(const uint32_t (&a)[4], uint32_t c) {
+  return (c & 2u) ? ((c & 1u) ? a[3] : a[2]) : ((c & 1u) ? a[1] : a[0]);
+}
 struct Ax1Ctl {                 // device counters of one chunk (zeroed before the chunk)
   unsigned long long zq_n, aq_n, ctr_path, ctr_z, ctr_a;
 };
@@ -1682,8 +1685,13 @@ struct AxRefill {
   }
 };
 
+// 3 CTAs per SM (80 registers, no spills): +5.6% on configs[3], +1.6% on the 150-bp reads over 4
+// (64 registers, ~190 B of spills; profiles/r02_approx1_bfs_minb.txt)
+#ifndef QR_AX1_PATH_MINB
+#define QR_AX1_PATH_MINB 3
+#endif
 template <bool FIXED, int BW, int STRANDS, bool WORK>
-__global__ void __launch_bounds__(256, QR_APPROX1_MINB) k_ax1_path(FmParams F, const uint8_t* __restrict__ pat,
+__global__ void __launch_bounds__(256, QR_AX1_PATH_MINB) k_ax1_path(FmParams F, const uint8_t* __restrict__ pat,
                                                     const uint64_t* __restrict__ offs,
                                                     const uint32_t* __restrict__ lens, uint32_t fixed_len,
                                                     uint32_t* __restrict__ out, uint32_t* __restrict__ out_rc,
@@ -1713,7 +1721,8 @@ __global__ void __launch_bounds__(256, QR_APPROX1_MINB) k_ax1_path(FmParams F, c
     total = 0;
   };
   while (rf.run(has, t1 - t0, &ctl->ctr_path, seed)) {
-    uint32_t cl[3] = {0u, 0u, 0u}, ch[3] = {0u, 0u, 0u}, n = 0;
+    // children in registers (static indices and selects: dynamically indexed arrays go to the stack)
+    uint32_t bl[4] = {0u, 0u, 0u, 0u}, bh[4] = {0u, 0u, 0u, 0u}, em = 0;   // em: children to queue
     int32_t jc = 0;
     if (has) {
       if (j >= 0 && lo < hi) {
@@ -1721,21 +1730,22 @@ __global__ void __launch_bounds__(256, QR_APPROX1_MINB) k_ax1_path(FmParams F, c
         fm_occ4_pair<BW, WORK>(F, lo, hi, ol, oh, wk);
         const uint32_t cj = P.at(j);
 #pragma unroll
-        for (uint32_t r = 0; r < 3; ++r) {
-          const uint32_t c = (cj + 1 + r) & 3u;
-          const uint32_t bl = Cs[c] + ol[c], bh = Cs[c] + oh[c];
-          if (bl < bh) {
-            if (j == 0) total += bh - bl;                 // substitution at P[0]: a leaf
-            else { cl[n] = bl; ch[n] = bh; ++n; }
+        for (int c = 0; c < 4; ++c) {
+          bl[c] = Cs[c] + ol[c];
+          bh[c] = Cs[c] + oh[c];
+          if ((uint32_t)c != cj && bl[c] < bh[c]) {
+            if (j == 0) total += bh[c] - bl[c];           // substitution at P[0]: a leaf
+            else em |= 1u << c;
           }
         }
         jc = j;
-        lo = Cs[cj] + ol[cj];
-        hi = Cs[cj] + oh[cj];
+        lo = sel4(bl, cj);
+        hi = sel4(bh, cj);
         --j;
       }
     }
     // the warp's new interval items (0..3 per lane): one atomic per warp that has any
+    const uint32_t n = __popc(em);
     if (__ballot_sync(0xffffffffu, n != 0)) {
       const uint32_t lt = (1u << lane) - 1u;
       const uint32_t b0 = __ballot_sync(0xffffffffu, n & 1u), b1 = __ballot_sync(0xffffffffu, (n >> 1) & 1u);
@@ -1743,10 +1753,13 @@ __global__ void __launch_bounds__(256, QR_APPROX1_MINB) k_ax1_path(FmParams F, c
       unsigned long long base = 0;
       if (lane == 0) base = atomicAdd(&ctl->aq_n, (unsigned long long)tot);
       base = __shfl_sync(0xffffffffu, base, 0) + __popc(b0 & lt) + 2u * __popc(b1 & lt);
-      for (uint32_t r = 0; r < n; ++r) {
-        if (base + r < aq_cap) aq[base + r] = make_uint4((uint32_t)ti, (uint32_t)jc, cl[r], ch[r]);
-        else total += fm_continue<BW, WORK>(F, P, (int64_t)jc - 1, cl[r], ch[r], wk);   // queue full
-      }
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        if ((em >> c) & 1u) {
+          const uint64_t at = base + __popc(em & ((1u << c) - 1u));
+          if (at < aq_cap) aq[at] = make_uint4((uint32_t)ti, (uint32_t)jc, bl[c], bh[c]);
+          else total += fm_continue<BW, WORK>(F, P, (int64_t)jc - 1, bl[c], bh[c], wk);   // queue full
+        }
     }
     if (has && !(j >= 0 && lo < hi)) {                   // finished: exact count + leaves
       if (lo < hi) total += hi - lo;
