@@ -1551,27 +1551,30 @@ __global__ void QR_APPROX_LB k_fm_approxk(FmParams F, const uint8_t* __restrict_
   }
 }
 
-// ---- approximate counting with <= 1 substitution, breadth first (default for k = 1) ---------
-// The same decomposition as k_fm_approx1 (count_{<=1} = exact + every single-substitution branch,
-// PAPER.md:139-140), run level by level so that every lane of a warp does the same kind of work:
-//   k_ax1_seed  one thread per task: the exact seed interval of the last K symbols and the 3K
-//               one-substitution K-mers present in the table (presence bitmap, or all of them),
-//               written as lookup items (task, key) to a queue of exact size;
-//   k_ax1_path  the exact path below the seed with rank_4 at both ends (one step per lane and
-//               iteration, lanes refilled from the task range): the three substituted children
-//               of every step go to a second queue as interval items (task, pos, lo, hi);
-//   k_ax1_cont  (once per queue) plain exact searches of the items, one step per lane and
-//               iteration, refilled from the queue; each adds its count to the task's output.
-// In the recursive kernel a lane walks its pattern's exact path and, at every step, the
-// continuations of its three branches, so the lanes of a warp sit in different loops (ncu: ~11
+// ---- approximate counting with <= k substitutions (k = 1, 2), breadth first ------------------
+// The same decomposition as the recursive kernels (a leaf of the substitution tree is a distinct
+// string; PAPER.md:139-140 — rank_4 at both ends of a node gives its four children), run level
+// by level (mm = substitutions left) so that every lane of a warp does the same kind of work:
+//   k_ax_seed   one thread per task: the exact seed interval of the last K symbols, and the
+//               K-mers within distance k of them that the table holds (presence bitmap, or all),
+//               written as lookup items (task, key) to one queue per level (exact sizes);
+//   k_ax_path   items with mm >= 1: their exact path with rank_4 at both ends (one step per lane
+//               and iteration, lanes refilled from the item range); the three substituted
+//               children of every step go to the queue of level mm - 1 as interval items
+//               (task, pos, lo, hi);
+//   k_ax_cont   items with mm = 0: plain exact searches, one step per lane and iteration.
+// Each item adds its count to its task's output (the level-k path, one item per task, first).
+// In the recursive kernels a lane walks its pattern's tree — the exact path and, at every step,
+// the continuations of its branches — so the lanes of a warp sit in different loops (ncu: ~11
 // of 32 lanes per instruction) and each lane's dependent gathers serialise behind the others'.
-// Interval items that do not fit the second queue (sized for ~4 per task) are continued by the
-// emitting lane itself.
+// Interval items that do not fit their queue (sized for ~4 per task) are searched by the
+// emitting lane itself (exact continuation, or the recursive one-substitution walk).
 __device__ __forceinline__ uint32_t sel4(const uint32_t (&a)[4], uint32_t c) {
   return (c & 2u) ? ((c & 1u) ? a[3] : a[2]) : ((c & 1u) ? a[1] : a[0]);
 }
-struct Ax1Ctl {                 // device counters of one chunk (zeroed before the chunk)
-  unsigned long long zq_n, aq_n, ctr_path, ctr_z, ctr_a;
+struct AxCtl {                  // device counters of one chunk (zeroed before the chunk)
+  unsigned long long n[4];      // queue sizes: Z1 (lookup, mm 1), Z0 (lookup, mm 0), Q1, Q0 (intervals)
+  unsigned long long ctr[8];    // work-order counters of the chunk's launches
 };
 
 template <bool FIXED, int STRANDS>
@@ -1586,21 +1589,56 @@ template <int STRANDS>
 __device__ __forceinline__ uint32_t* ax_out(uint32_t* out, uint32_t* out_rc, uint64_t ti) {
   return (STRANDS == 2 && (ti & 1)) ? out_rc + (ti >> 1) : out + (STRANDS == 2 ? ti >> 1 : ti);
 }
+// this lane's first slot of n items in a queue, one atomic per warp (all 32 lanes call it)
+__device__ __forceinline__ unsigned long long warp_reserve(unsigned long long* cnt, uint32_t n) {
+  const uint32_t lane = threadIdx.x & 31u;
+  uint32_t incl = n;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= (uint32_t)o) incl += v;
+  }
+  const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
+  unsigned long long base = 0;
+  if (lane == 31 && tot) base = atomicAdd(cnt, (unsigned long long)tot);
+  return __shfl_sync(0xffffffffu, base, 31) + (incl - n);
+}
+// presence of the 3 (K - t0) one-substitution variants of key at positions t0..K-1 (bit 3(t-t0)+r-1)
+__device__ __forceinline__ uint64_t ax_present_from(const FmParams& F, uint32_t key, int t0) {
+  const int nb = 3 * (F.K - t0);
+  if (nb <= 0) return 0ull;
+  if (!F.kbits) return ~0ull >> (64 - nb);
+  uint64_t pm = 0;
+  for (int t = t0; t < F.K; ++t) pm |= (uint64_t)ax_present3(F, key, t) << (3 * (t - t0));
+  return pm;
+}
+__device__ __forceinline__ uint32_t ax_variant(uint32_t key, int t0, int b) {
+  return kmer_subst(key, t0 + b / 3, (uint32_t)(b % 3) + 1);
+}
+// sizes of the listed variants' intervals (a K-mer that is the whole pattern: nothing to continue)
+__device__ __forceinline__ uint32_t ax_sizes(const FmParams& F, uint32_t key, int t0, uint64_t pm) {
+  uint32_t s = 0;
+  for (; pm; pm &= pm - 1) {
+    const uint2 iv = ld_kmer(F.kmer + ax_variant(key, t0, __ffsll((long long)pm) - 1));
+    s += iv.x < iv.y ? iv.y - iv.x : 0u;
+  }
+  return s;
+}
 
-template <bool FIXED, int STRANDS, bool WORK>
-__global__ void __launch_bounds__(256) k_ax1_seed(FmParams F, const uint8_t* __restrict__ pat,
-                                                  const uint64_t* __restrict__ offs, const uint32_t* __restrict__ lens,
-                                                  uint32_t fixed_len, uint32_t* __restrict__ out,
-                                                  uint32_t* __restrict__ out_rc, uint64_t t0, uint64_t t1,
-                                                  uint2* __restrict__ seeds, uint2* __restrict__ zq, Ax1Ctl* ctl,
-                                                  unsigned long long* __restrict__ work) {
+template <bool FIXED, int STRANDS, int KMAX, bool WORK>
+__global__ void __launch_bounds__(256) k_ax_seed(FmParams F, const uint8_t* __restrict__ pat,
+                                                 const uint64_t* __restrict__ offs, const uint32_t* __restrict__ lens,
+                                                 uint32_t fixed_len, uint32_t* __restrict__ out,
+                                                 uint32_t* __restrict__ out_rc, uint64_t t0, uint64_t t1,
+                                                 uint2* __restrict__ seeds, uint2* __restrict__ z1,
+                                                 uint2* __restrict__ z0, AxCtl* ctl, unsigned long long* __restrict__ work) {
   const uint32_t lane = threadIdx.x & 31u;
   const uint64_t warps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
   uint64_t ws = 0;
   for (uint64_t w0 = t0 + (((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) & ~31ull); w0 < t1; w0 += warps * 32) {
     const uint64_t ti = w0 + lane;
     const bool valid = ti < t1;
-    uint64_t pm = 0;
+    bool seeded = false, whole = false;
     uint32_t key0 = 0, direct = 0;
     if (valid) {
       uint32_t len, rc;
@@ -1611,40 +1649,31 @@ __global__ void __launch_bounds__(256) k_ax1_seed(FmParams F, const uint8_t* __r
         P.reset(p);
         key0 = rc ? kmer_key_rc(F.K, P, p, len) : kmer_key(F.K, P, p, len);
         iv0 = ax_lookup(F, key0);
-        const int nb = 3 * F.K;
-        if (F.kbits) {
-          for (int t = 0; t < F.K; ++t) pm |= (uint64_t)ax_present3(F, key0, t) << (3 * t);
-        } else {
-          pm = ~0ull >> (64 - nb);
-        }
-        if (WORK) ws += (uint64_t)nb + 1;
-        if (len == (uint32_t)F.K) {                       // nothing left to continue: add directly
-          for (; pm; pm &= pm - 1) {
-            const int b = __ffsll((long long)pm) - 1;
-            const uint2 iv = ld_kmer(F.kmer + kmer_subst(key0, b / 3, (uint32_t)(b % 3) + 1));
-            direct += iv.x < iv.y ? iv.y - iv.x : 0u;
-          }
-        }
+        seeded = true;
+        whole = len == (uint32_t)F.K;                     // the variants are leaves
+        if (WORK) ws += 1 + 3ull * F.K + (KMAX == 2 ? 9ull * F.K * (F.K - 1) / 2 : 0ull);
       }
       seeds[ti - t0] = iv0;
-      *ax_out<STRANDS>(out, out_rc, ti) = direct;
     }
-    // reserve the warp's lookup items with one atomic, then write them
-    const uint32_t n = (uint32_t)__popcll(pm);
-    uint32_t incl = n;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= (uint32_t)o) incl += v;
+    // one substitution inside the K-mer: level 0 (k = 1) or 1 (k = 2)
+    uint64_t pm = seeded ? ax_present_from(F, key0, 0) : 0ull;
+    if (whole) { direct += ax_sizes(F, key0, 0, pm); pm = 0; }
+    {
+      uint2* q = KMAX == 2 ? z1 : z0;
+      unsigned long long at = warp_reserve(&ctl->n[KMAX == 2 ? 0 : 1], (uint32_t)__popcll(pm));
+      for (; pm; pm &= pm - 1) q[at++] = make_uint2((uint32_t)ti, ax_variant(key0, 0, __ffsll((long long)pm) - 1));
     }
-    const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
-    unsigned long long base = 0;
-    if (lane == 31 && tot) base = atomicAdd(&ctl->zq_n, (unsigned long long)tot);
-    base = __shfl_sync(0xffffffffu, base, 31) + (incl - n);
-    for (; pm; pm &= pm - 1) {
-      const int b = __ffsll((long long)pm) - 1;
-      zq[base++] = make_uint2((uint32_t)ti, kmer_subst(key0, b / 3, (uint32_t)(b % 3) + 1));
+    if (KMAX == 2) {                                      // two substitutions inside the K-mer: level 0
+      for (int t1 = 0; t1 < F.K; ++t1)
+        for (uint32_t r1 = 1; r1 < 4; ++r1) {
+          const uint32_t k1 = kmer_subst(key0, t1, r1);
+          uint64_t pm2 = seeded ? ax_present_from(F, k1, t1 + 1) : 0ull;
+          if (whole) { direct += ax_sizes(F, k1, t1 + 1, pm2); pm2 = 0; }
+          unsigned long long at = warp_reserve(&ctl->n[1], (uint32_t)__popcll(pm2));
+          for (; pm2; pm2 &= pm2 - 1) z0[at++] = make_uint2((uint32_t)ti, ax_variant(k1, t1 + 1, __ffsll((long long)pm2) - 1));
+        }
     }
+    if (valid) *ax_out<STRANDS>(out, out_rc, ti) = direct;
   }
   if (WORK && ws) { atomicAdd(work, (unsigned long long)ws); atomicAdd(work + 1, (unsigned long long)ws); }
 }
@@ -1685,25 +1714,61 @@ struct AxRefill {
   }
 };
 
+// The recursive one-substitution walk of an interval (the queue-overflow path of level-1 items).
+template <int BW, bool WORK, class W>
+__device__ __noinline__ uint32_t ax1_inline(const FmParams& F, W& P, int64_t j, uint32_t lo, uint32_t hi,
+                                            FmWork& wk) {
+  const uint4 C4 = __ldg(reinterpret_cast<const uint4*>(F.Ct));
+  const uint32_t Cs[4] = {C4.x, C4.y, C4.z, C4.w};
+  uint32_t total = 0;
+  for (; j >= 0 && lo < hi; --j) {
+    uint32_t ol[4], oh[4];
+    fm_occ4_pair<BW, WORK>(F, lo, hi, ol, oh, wk);
+    const uint32_t cj = P.at(j);
+    uint32_t bl[4], bh[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      bl[c] = Cs[c] + ol[c];
+      bh[c] = Cs[c] + oh[c];
+    }
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+      if ((uint32_t)c != cj && bl[c] < bh[c])
+        total += j == 0 ? bh[c] - bl[c] : fm_continue<BW, WORK>(F, P, j - 1, bl[c], bh[c], wk);
+    lo = sel4(bl, cj);
+    hi = sel4(bh, cj);
+  }
+  return total + (lo < hi ? hi - lo : 0u);
+}
+
 // 3 CTAs per SM (80 registers, no spills): +5.6% on configs[3], +1.6% on the 150-bp reads over 4
 // (64 registers, ~190 B of spills; profiles/r02_approx1_bfs_minb.txt)
 #ifndef QR_AX1_PATH_MINB
 #define QR_AX1_PATH_MINB 3
 #endif
-template <bool FIXED, int BW, int STRANDS, bool WORK>
-__global__ void __launch_bounds__(256, QR_AX1_PATH_MINB) k_ax1_path(FmParams F, const uint8_t* __restrict__ pat,
+// SRC 0: the chunk's tasks from their seed intervals (level k, the only item of its task: the
+// output is updated in place); 1: lookup items (task, key); 2: interval items (task, pos, lo, hi).
+template <bool FIXED, int BW, int STRANDS, bool WORK, int SRC, int CHILD>   // CHILD: the children's mm
+__global__ void __launch_bounds__(256, QR_AX1_PATH_MINB) k_ax_path(FmParams F, const uint8_t* __restrict__ pat,
                                                     const uint64_t* __restrict__ offs,
                                                     const uint32_t* __restrict__ lens, uint32_t fixed_len,
                                                     uint32_t* __restrict__ out, uint32_t* __restrict__ out_rc,
                                                     uint64_t t0, uint64_t t1, const uint2* __restrict__ seeds,
-                                                    uint4* __restrict__ aq, uint64_t aq_cap, Ax1Ctl* ctl,
-                                                    unsigned long long* __restrict__ work) {
+                                                    const void* __restrict__ items, const unsigned long long* n_items,
+                                                    uint64_t items_cap, uint4* __restrict__ oq,
+                                                    unsigned long long* oq_n, uint64_t oq_cap,
+                                                    unsigned long long* ctr, unsigned long long* __restrict__ work) {
   FmWork wk;
   if (BW == 1) x2_masks_init();
   else qd_masks_init();
   const uint4 C4 = __ldg(reinterpret_cast<const uint4*>(F.Ct));
   const uint32_t Cs[4] = {C4.x, C4.y, C4.z, C4.w};
   const uint32_t lane = threadIdx.x & 31u;
+  uint64_t total_items = t1 - t0;
+  if (SRC != 0) {
+    const unsigned long long nq = *n_items;
+    total_items = nq < items_cap ? nq : items_cap;
+  }
   StrandWindow<STRANDS> P;
   uint64_t ti = 0;
   uint32_t lo = 0, hi = 0, total = 0;
@@ -1711,16 +1776,33 @@ __global__ void __launch_bounds__(256, QR_AX1_PATH_MINB) k_ax1_path(FmParams F, 
   bool has = false;
   AxRefill rf;
   auto seed = [&](uint64_t t) {
-    ti = t0 + t;
     uint32_t len, rc;
-    const uint8_t* p = ax_pattern<FIXED, STRANDS>(pat, offs, lens, fixed_len, ti, len, rc);
-    P.reset(p, len, rc);
-    const uint2 iv = seeds[t];
-    lo = iv.x; hi = iv.y;
-    j = (int32_t)len - 1 - ((F.K && len >= (uint32_t)F.K) ? F.K : 0);
+    if (SRC == 0) {
+      ti = t0 + t;
+      const uint8_t* p = ax_pattern<FIXED, STRANDS>(pat, offs, lens, fixed_len, ti, len, rc);
+      P.reset(p, len, rc);
+      const uint2 iv = seeds[t];
+      lo = iv.x; hi = iv.y;
+      j = (int32_t)len - 1 - ((F.K && len >= (uint32_t)F.K) ? F.K : 0);
+    } else if (SRC == 1) {
+      const uint2 it = reinterpret_cast<const uint2*>(items)[t];
+      ti = it.x;
+      const uint8_t* p = ax_pattern<FIXED, STRANDS>(pat, offs, lens, fixed_len, ti, len, rc);
+      P.reset(p, len, rc);
+      const uint2 iv = ld_kmer(F.kmer + it.y);
+      lo = iv.x; hi = iv.y;
+      j = (int32_t)len - 1 - F.K;
+    } else {
+      const uint4 it = reinterpret_cast<const uint4*>(items)[t];
+      ti = it.x;
+      const uint8_t* p = ax_pattern<FIXED, STRANDS>(pat, offs, lens, fixed_len, ti, len, rc);
+      P.reset(p, len, rc);
+      lo = it.z; hi = it.w;
+      j = (int32_t)it.y - 1;
+    }
     total = 0;
   };
-  while (rf.run(has, t1 - t0, &ctl->ctr_path, seed)) {
+  while (rf.run(has, total_items, ctr, seed)) {
     // children in registers (static indices and selects: dynamically indexed arrays go to the stack)
     uint32_t bl[4] = {0u, 0u, 0u, 0u}, bh[4] = {0u, 0u, 0u, 0u}, em = 0;   // em: children to queue
     int32_t jc = 0;
@@ -1751,20 +1833,22 @@ __global__ void __launch_bounds__(256, QR_AX1_PATH_MINB) k_ax1_path(FmParams F, 
       const uint32_t b0 = __ballot_sync(0xffffffffu, n & 1u), b1 = __ballot_sync(0xffffffffu, (n >> 1) & 1u);
       const uint32_t tot = __popc(b0) + 2u * __popc(b1);
       unsigned long long base = 0;
-      if (lane == 0) base = atomicAdd(&ctl->aq_n, (unsigned long long)tot);
+      if (lane == 0) base = atomicAdd(oq_n, (unsigned long long)tot);
       base = __shfl_sync(0xffffffffu, base, 0) + __popc(b0 & lt) + 2u * __popc(b1 & lt);
 #pragma unroll
       for (int c = 0; c < 4; ++c)
         if ((em >> c) & 1u) {
           const uint64_t at = base + __popc(em & ((1u << c) - 1u));
-          if (at < aq_cap) aq[at] = make_uint4((uint32_t)ti, (uint32_t)jc, bl[c], bh[c]);
-          else total += fm_continue<BW, WORK>(F, P, (int64_t)jc - 1, bl[c], bh[c], wk);   // queue full
+          if (at < oq_cap) oq[at] = make_uint4((uint32_t)ti, (uint32_t)jc, bl[c], bh[c]);
+          else if (CHILD == 0) total += fm_continue<BW, WORK>(F, P, (int64_t)jc - 1, bl[c], bh[c], wk);
+          else total += ax1_inline<BW, WORK>(F, P, (int64_t)jc - 1, bl[c], bh[c], wk);
         }
     }
-    if (has && !(j >= 0 && lo < hi)) {                   // finished: exact count + leaves
+    if (has && !(j >= 0 && lo < hi)) {                   // finished: the item's exact count + leaves
       if (lo < hi) total += hi - lo;
       uint32_t* o = ax_out<STRANDS>(out, out_rc, ti);
-      *o += total;
+      if (SRC == 0) *o += total;
+      else if (total) atomicAdd(o, total);
       has = false;
     }
   }
@@ -1774,20 +1858,21 @@ __global__ void __launch_bounds__(256, QR_AX1_PATH_MINB) k_ax1_path(FmParams F, 
   }
 }
 
-// LOOKUP: items are (task, key) of k_ax1_seed, the interval read from the table at refill
-// (resolving them in k_ax1_seed instead measured 1.35x slower on configs[3]: its lanes then walk
-// 3K dependent lookups, and the queue doubles); else (task, pos, lo, hi) of k_ax1_path.  Exact
-// backward search of P[pos-1 .. 0] from the interval, one step per lane and iteration.
+// Items with no substitution left: exact backward search of P[pos-1 .. 0].  LOOKUP: items
+// (task, key) of k_ax_seed, the interval read from the table at refill (resolving them in
+// k_ax_seed instead measured 1.35x slower on configs[3] at k = 1: its lanes then walk 3K
+// dependent lookups, and the queue doubles); else (task, pos, lo, hi) of k_ax_path.
 template <bool FIXED, int BW, int STRANDS, bool WORK, bool LOOKUP>
-__global__ void __launch_bounds__(256, QR_APPROX1_MINB) k_ax1_cont(FmParams F, const uint8_t* __restrict__ pat,
+__global__ void __launch_bounds__(256, QR_APPROX1_MINB) k_ax_cont(FmParams F, const uint8_t* __restrict__ pat,
                                                     const uint64_t* __restrict__ offs,
                                                     const uint32_t* __restrict__ lens, uint32_t fixed_len,
                                                     uint32_t* __restrict__ out, uint32_t* __restrict__ out_rc,
-                                                    const void* __restrict__ items, uint64_t cap, Ax1Ctl* ctl,
+                                                    const void* __restrict__ items, const unsigned long long* n_items,
+                                                    uint64_t cap, unsigned long long* ctr,
                                                     unsigned long long* __restrict__ work) {
   FmWork wk;
   if (BW == 1) x2_masks_init();
-  const unsigned long long nq = LOOKUP ? ctl->zq_n : ctl->aq_n;
+  const unsigned long long nq = *n_items;
   const uint64_t total_items = nq < cap ? nq : cap;
   StrandWindow<STRANDS> P;
   uint64_t ti = 0;
@@ -1814,7 +1899,6 @@ __global__ void __launch_bounds__(256, QR_APPROX1_MINB) k_ax1_cont(FmParams F, c
       j = (int32_t)it.y - 1;
     }
   };
-  unsigned long long* ctr = LOOKUP ? &ctl->ctr_z : &ctl->ctr_a;
   while (rf.run(has, total_items, ctr, seed)) {
     if (has) {
       if (j >= 0 && lo < hi) {
@@ -1872,6 +1956,7 @@ void fm_copy_locked(const qr_fm* src, qr_fm* dst) {
 }
 extern int g_fm_kbits;
 extern int g_fm_ax_bfs;
+int g_fm_ax_bfs2 = 1;   // k = 2 breadth first too (knob fm_ax_bfs2)
 static qr_status fm_params_ax(const qr_fm* fmc, cudaStream_t st, FmParams& F) {
   qr_fm* fm = const_cast<qr_fm*>(fmc);                     // a lazily filled cache of the handle
   std::lock_guard<std::mutex> g(g_ax_mu);
@@ -2116,40 +2201,63 @@ static unsigned resident_grid(Kern k, int sms, size_t smem = 0) {
   return (unsigned)per_sm * (unsigned)sms;
 }
 
-// k = 1 breadth first (k_ax1_*), tasks in chunks so that the lookup queue (exactly 3K per task
-// at most) and the interval queue (~4 per task) stay within the pool's kept 2 GiB.
-uint64_t g_ax1_aq_per_task = 4;   // interval-queue items per task (tests: 0 sends every item inline)
-template <bool FIXED, int STRANDS, bool WORK>
-static cudaError_t launch_ax1_bfs(const qr_fm* fm, cudaStream_t st, const FmParams& F, const uint8_t* pat,
-                                  const uint64_t* offs, const uint32_t* lens, uint32_t fixed_len, uint32_t* out,
-                                  uint32_t* out_rc, uint64_t m, unsigned long long* work) {
+// k = 1, 2 breadth first (k_ax_*), tasks in chunks so that the queues — the lookup items of the
+// seed variants (exactly 3K, and 9 C(K,2) at k = 2, per task at most) and the interval items of
+// the paths (~4 per task and level) — stay within the ~1.5 GB the pool keeps.
+uint64_t g_ax1_aq_per_task = 4;   // interval items per task and level (tests: 0 sends every one inline)
+template <bool FIXED, int STRANDS, bool WORK, int KMAX>
+static cudaError_t launch_ax_bfs(const qr_fm* fm, cudaStream_t st, const FmParams& F, const uint8_t* pat,
+                                 const uint64_t* offs, const uint32_t* lens, uint32_t fixed_len, uint32_t* out,
+                                 uint32_t* out_rc, uint64_t m, unsigned long long* work) {
   const uint64_t ntask = m * STRANDS;
-  const uint64_t per_task_z = 3ull * (uint64_t)(F.K > 0 ? F.K : 0);
-  const uint64_t chunk = ntask < (1ull << 22) ? ntask : (1ull << 22);
-  const uint64_t aq_cap = chunk * g_ax1_aq_per_task;
-  const size_t aq_off = (256 + chunk * 8 + chunk * per_task_z * 8 + 255) & ~(size_t)255;   // uint4 items: 16-B aligned
-  const size_t bytes = aq_off + aq_cap * 16 + 16;
+  const uint64_t K = F.K > 0 ? (uint64_t)F.K : 0;
+  const uint64_t z1_pt = KMAX == 2 ? 3 * K : 0, z0_pt = KMAX == 2 ? 9 * K * (K ? K - 1 : 0) / 2 : 3 * K;
+  const uint64_t q_pt = g_ax1_aq_per_task, nq = KMAX == 2 ? 2 : 1;
+  const uint64_t per_task = 8 + (z1_pt + z0_pt) * 8 + nq * q_pt * 16;
+  uint64_t chunk = (3ull << 29) / per_task;
+  chunk = chunk < 4096 ? 4096 : chunk;
+  chunk = ntask < chunk ? ntask : chunk;
+  const uint64_t q_cap = chunk * q_pt;
+  const size_t off_z1 = 256 + chunk * 8, off_z0 = off_z1 + chunk * z1_pt * 8;
+  const size_t off_q1 = (off_z0 + chunk * z0_pt * 8 + 255) & ~(size_t)255, off_q0 = off_q1 + (KMAX == 2 ? q_cap * 16 : 0);
+  const size_t bytes = off_q0 + q_cap * 16 + 16;
   keep_pool_memory(fm->bwt->device, st);
   unsigned char* buf = nullptr;
   cudaError_t e = cudaMallocAsync((void**)&buf, bytes, st);
   if (e) return e;
-  Ax1Ctl* ctl = reinterpret_cast<Ax1Ctl*>(buf);
+  AxCtl* ctl = reinterpret_cast<AxCtl*>(buf);
   uint2* seeds = reinterpret_cast<uint2*>(buf + 256);
-  uint2* zq = seeds + chunk;
-  uint4* aq = reinterpret_cast<uint4*>(buf + aq_off);
+  uint2* z1 = reinterpret_cast<uint2*>(buf + off_z1);
+  uint2* z0 = reinterpret_cast<uint2*>(buf + off_z0);
+  uint4* q1 = reinterpret_cast<uint4*>(buf + off_q1);
+  uint4* q0 = reinterpret_cast<uint4*>(buf + off_q0);
   const int sms = fm->bwt->sm_count;
-  auto kp = F.bw ? k_ax1_path<FIXED, 1, STRANDS, WORK> : k_ax1_path<FIXED, 0, STRANDS, WORK>;
-  auto kz = F.bw ? k_ax1_cont<FIXED, 1, STRANDS, WORK, true> : k_ax1_cont<FIXED, 0, STRANDS, WORK, true>;
-  auto ka = F.bw ? k_ax1_cont<FIXED, 1, STRANDS, WORK, false> : k_ax1_cont<FIXED, 0, STRANDS, WORK, false>;
-  const unsigned gp = resident_grid(kp, sms), gz = resident_grid(kz, sms), ga = resident_grid(ka, sms);
+#define QR_AX_K(KERN, ...) (F.bw ? KERN<FIXED, 1, STRANDS, WORK, __VA_ARGS__> : KERN<FIXED, 0, STRANDS, WORK, __VA_ARGS__>)
+  auto kp0 = QR_AX_K(k_ax_path, 0, KMAX - 1);
+  auto kp1 = QR_AX_K(k_ax_path, 1, 0);
+  auto kp2 = QR_AX_K(k_ax_path, 2, 0);
+  auto kcz = QR_AX_K(k_ax_cont, true);
+  auto kcq = QR_AX_K(k_ax_cont, false);
+#undef QR_AX_K
+  const unsigned gp = resident_grid(kp0, sms), gc = resident_grid(kcz, sms);
   for (uint64_t t0 = 0; t0 < ntask && !e; t0 += chunk) {
-    const uint64_t t1 = t0 + chunk < ntask ? t0 + chunk : ntask;
-    if ((e = cudaMemsetAsync(ctl, 0, sizeof(Ax1Ctl), st))) break;
-    k_ax1_seed<FIXED, STRANDS, WORK><<<grid_stride_blocks(t1 - t0, 256, sms, 8), 256, 0, st>>>(
-        F, pat, offs, lens, fixed_len, out, out_rc, t0, t1, seeds, zq, ctl, work);
-    kp<<<gp, 256, 0, st>>>(F, pat, offs, lens, fixed_len, out, out_rc, t0, t1, seeds, aq, aq_cap, ctl, work);
-    kz<<<gz, 256, 0, st>>>(F, pat, offs, lens, fixed_len, out, out_rc, zq, (t1 - t0) * per_task_z, ctl, work);
-    ka<<<ga, 256, 0, st>>>(F, pat, offs, lens, fixed_len, out, out_rc, aq, aq_cap, ctl, work);
+    const uint64_t t1 = t0 + chunk < ntask ? t0 + chunk : ntask, nt = t1 - t0;
+    if ((e = cudaMemsetAsync(ctl, 0, sizeof(AxCtl), st))) break;
+    k_ax_seed<FIXED, STRANDS, KMAX, WORK><<<grid_stride_blocks(nt, 256, sms, 8), 256, 0, st>>>(
+        F, pat, offs, lens, fixed_len, out, out_rc, t0, t1, seeds, z1, z0, ctl, work);
+    if (KMAX == 2) {
+      kp0<<<gp, 256, 0, st>>>(F, pat, offs, lens, fixed_len, out, out_rc, t0, t1, seeds, nullptr, nullptr, 0, q1,
+                              &ctl->n[2], q_cap, &ctl->ctr[0], work);
+      kp1<<<gp, 256, 0, st>>>(F, pat, offs, lens, fixed_len, out, out_rc, t0, t1, nullptr, z1, &ctl->n[0],
+                              nt * z1_pt, q0, &ctl->n[3], q_cap, &ctl->ctr[1], work);
+      kp2<<<gp, 256, 0, st>>>(F, pat, offs, lens, fixed_len, out, out_rc, t0, t1, nullptr, q1, &ctl->n[2], q_cap,
+                              q0, &ctl->n[3], q_cap, &ctl->ctr[2], work);
+    } else {
+      kp0<<<gp, 256, 0, st>>>(F, pat, offs, lens, fixed_len, out, out_rc, t0, t1, seeds, nullptr, nullptr, 0, q0,
+                              &ctl->n[3], q_cap, &ctl->ctr[0], work);
+    }
+    kcz<<<gc, 256, 0, st>>>(F, pat, offs, lens, fixed_len, out, out_rc, z0, &ctl->n[1], nt * z0_pt, &ctl->ctr[3], work);
+    kcq<<<gc, 256, 0, st>>>(F, pat, offs, lens, fixed_len, out, out_rc, q0, &ctl->n[3], q_cap, &ctl->ctr[4], work);
     e = cudaGetLastError();
   }
   cudaError_t e2 = cudaFreeAsync(buf, st);
@@ -2160,11 +2268,17 @@ template <bool FIXED, int STRANDS, bool WORK>
 static cudaError_t launch_approx_s(const qr_fm* fm, unsigned g, cudaStream_t st, const FmParams& F, const uint8_t* pat,
                                    const uint64_t* offs, const uint32_t* lens, uint32_t fixed_len, uint32_t* out,
                                    uint32_t* out_rc, uint64_t m, int kmax, unsigned long long* work) {
-  // breadth first (auto): 1.89x on the 150-bp reads (HBM-resident BWT), +2.4% on configs[3]; the
-  // recursive kernel stays on an L2-resident QuadRank16x2 BWT (1.68 vs 1.50 G patterns/s there)
-  const bool bfs = g_fm_ax_bfs == 2 || (g_fm_ax_bfs == 1 && !(F.bw == 1 && bwt_l2_resident(fm)));
-  if (kmax == 1 && bfs && g_fm_dyn && m * STRANDS < (1ull << 32))
-    return launch_ax1_bfs<FIXED, STRANDS, WORK>(fm, st, F, pat, offs, lens, fixed_len, out, out_rc, m, work);
+  // breadth first (auto, profiles/r02_approx_bfs_k2_ab.txt): k = 1 everywhere but on an
+  // L2-resident QuadRank16x2 BWT (150-bp reads 52.8 -> 103 M reads/s, configs[3] 1.31 -> 1.48 G;
+  // QuadRank16x2 configs[3] 1.68 recursive vs 1.50); k = 2 on L2-resident BWTs (configs[3] 69.9
+  // -> 88.3 M, QuadRank16x2 91.0 -> 93.2 M; the reads, HBM-resident, 6.98 recursive vs 6.11)
+  const bool l2 = bwt_l2_resident(fm);
+  const bool bfs = g_fm_ax_bfs == 2 ||
+                   (g_fm_ax_bfs == 1 && (kmax == 1 ? !(F.bw == 1 && l2) : (kmax == 2 && l2 && g_fm_ax_bfs2)));
+  if (bfs && g_fm_dyn && m * STRANDS < (1ull << 32)) {
+    if (kmax == 1) return launch_ax_bfs<FIXED, STRANDS, WORK, 1>(fm, st, F, pat, offs, lens, fixed_len, out, out_rc, m, work);
+    if (kmax == 2) return launch_ax_bfs<FIXED, STRANDS, WORK, 2>(fm, st, F, pat, offs, lens, fixed_len, out, out_rc, m, work);
+  }
   auto kern = kmax == 1 ? (F.bw ? k_fm_approx1<FIXED, 1, STRANDS, WORK> : k_fm_approx1<FIXED, 0, STRANDS, WORK>)
             : kmax == 2 ? (F.bw ? k_fm_approxk<FIXED, 1, 2, STRANDS, WORK> : k_fm_approxk<FIXED, 0, 2, STRANDS, WORK>)
                         : (F.bw ? k_fm_approxk<FIXED, 1, 3, STRANDS, WORK> : k_fm_approxk<FIXED, 0, 3, STRANDS, WORK>);

@@ -952,9 +952,10 @@ def test_fm_build_from_bytes(cuda, space):
 @pytest.mark.parametrize("bwt_layout", [None, qr.QR_LAYOUT_QUADRANK16X2])
 @pytest.mark.parametrize("queue", [0, 1, 4])
 @pytest.mark.parametrize("bfs,kbits", [(0, 0), (2, 1), (2, 2)])
-def test_fm_approx1_breadth_first_queues(cuda, bwt_layout, queue, bfs, kbits, fm_dyn_reset):
-    """k = 1 breadth first (seed items, the exact path's branch items, their continuations) with
-    the interval queue sized 0 (every branch continued inline by its lane), 1 or 4 items per task,
+@pytest.mark.parametrize("kmax", [1, 2])
+def test_fm_approx_breadth_first_queues(cuda, bwt_layout, queue, bfs, kbits, kmax, fm_dyn_reset):
+    """k = 1, 2 breadth first (seed items, the paths' branch items, their continuations) with
+    the interval queues sized 0 (every branch searched inline by its lane), 1 or 4 items per task,
     with and without the presence bitmap, against the recursive kernel's oracle — the direct
     Hamming scan — on both strands, ragged lengths (shorter than, equal to and longer than the
     seed width)."""
@@ -973,16 +974,17 @@ def test_fm_approx1_breadth_first_queues(cuda, bwt_layout, queue, bfs, kbits, fm
             k = int(rng.integers(0, L)); p[k] = (p[k] + 1 + rng.integers(0, 3)) % 4
         pats.append(p)
     cat, off, lens = oracle.pack_patterns(pats)
-    ref = oracle.scan_count_hd1(sym, cat, off, lens)
+    hd = oracle.scan_count_hd1 if kmax == 1 else (lambda *a: oracle.scan_count_hdk(*a, 2))
+    ref = hd(sym, cat, off, lens)
     ccat, coff, clens = oracle.pack_patterns([revcomp(p) for p in pats])
-    ref_rc = oracle.scan_count_hd1(sym, ccat, coff, clens)
+    ref_rc = hd(sym, ccat, coff, clens)
     try:
         qr.qr_set_tuning("fm_ax_bfs", bfs)
         qr.qr_set_tuning("fm_ax_queue", queue)
         qr.qr_set_tuning("fm_kbits", kbits)
         df = torch.empty(lens.size, dtype=torch.int32, device=cuda)
         dr = torch.empty(lens.size, dtype=torch.int32, device=cuda)
-        qr.qr_fm_count_approx_both(fm, to_dev(cat, cuda), to_dev(lens, cuda), 0, 1, df, dr, lens.size)
+        qr.qr_fm_count_approx_both(fm, to_dev(cat, cuda), to_dev(lens, cuda), 0, kmax, df, dr, lens.size)
         torch.cuda.synchronize()
     finally:
         qr.qr_set_tuning("fm_ax_bfs", 1)
