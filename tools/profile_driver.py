@@ -2,7 +2,8 @@
 ncu --set full captures (kernel order: bi_rank2c (BiRank16 rank, cluster shared-memory superblocks),
 BiRank16x2 / QuadRank16x2 rank (cluster kernels) after the QuadRank64 rank,
 bi_gather2 x3 (ceiling modes 0-2), bi_rank2c<VAR=3> (ceiling mode 3), qd_rank2c, qd_all4_2c, b64_rank,
-q64_rank, fm_count (c4, lean), fm_count (c5, de-duplicating), fm_count both strands, fm_approx1, fm_approxk k=2)."""
+q64_rank, fm_count (c4, lean), fm_count (c5, de-duplicating), fm_count both strands, the breadth-first
+<= 1 substitution on both strands of 10^6 reads, configs[3] <= 1 and <= 2 substitutions (breadth first)."""
 import os
 import sys
 
@@ -81,6 +82,9 @@ gen.patterns_dev(55, 2, mr, 150, t, n, reads)
 of = torch.empty(mr, dtype=torch.int32, device=dev)
 orc = torch.empty(mr, dtype=torch.int32, device=dev)
 qr.qr_fm_count_both(fm, reads, None, 150, of, orc, mr, st)
+torch.cuda.synchronize()
+ma = 10**6                                   # <= 1 substitution on both strands (breadth first)
+qr.qr_fm_count_approx_both(fm, reads[: ma * 150], None, 150, 1, of[:ma], orc[:ma], ma, st)
 torch.cuda.synchronize()
 fm.free()
 n = 1 << 26
