@@ -1573,8 +1573,9 @@ __device__ __forceinline__ uint32_t sel4(const uint32_t (&a)[4], uint32_t c) {
   return (c & 2u) ? ((c & 1u) ? a[3] : a[2]) : ((c & 1u) ? a[1] : a[0]);
 }
 struct AxCtl {                  // device counters of one chunk (zeroed before the chunk)
-  unsigned long long n[4];      // queue sizes: Z1 (lookup, mm 1), Z0 (lookup, mm 0), Q1, Q0 (intervals)
-  unsigned long long ctr[8];    // work-order counters of the chunk's launches
+  unsigned long long z[3];      // lookup-queue sizes by level (mm = substitutions left)
+  unsigned long long q[3];      // interval-queue sizes by level
+  unsigned long long ctr[10];   // work-order counters of the chunk's launches
 };
 
 template <bool FIXED, int STRANDS>
@@ -1625,15 +1626,18 @@ __device__ __forceinline__ uint32_t ax_sizes(const FmParams& F, uint32_t key, in
   return s;
 }
 
+// The n-substitution variants inside the K-mer go to level KMAX - n (n = 1..KMAX).
 template <bool FIXED, int STRANDS, int KMAX, bool WORK>
 __global__ void __launch_bounds__(256) k_ax_seed(FmParams F, const uint8_t* __restrict__ pat,
                                                  const uint64_t* __restrict__ offs, const uint32_t* __restrict__ lens,
                                                  uint32_t fixed_len, uint32_t* __restrict__ out,
                                                  uint32_t* __restrict__ out_rc, uint64_t t0, uint64_t t1,
-                                                 uint2* __restrict__ seeds, uint2* __restrict__ z1,
-                                                 uint2* __restrict__ z0, AxCtl* ctl, unsigned long long* __restrict__ work) {
+                                                 uint2* __restrict__ seeds, uint2* __restrict__ z0,
+                                                 uint2* __restrict__ z1, uint2* __restrict__ z2, AxCtl* ctl,
+                                                 unsigned long long* __restrict__ work) {
   const uint32_t lane = threadIdx.x & 31u;
   const uint64_t warps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  uint2* const zq[3] = {z0, z1, z2};
   uint64_t ws = 0;
   for (uint64_t w0 = t0 + (((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) & ~31ull); w0 < t1; w0 += warps * 32) {
     const uint64_t ti = w0 + lane;
@@ -1651,29 +1655,93 @@ __global__ void __launch_bounds__(256) k_ax_seed(FmParams F, const uint8_t* __re
         iv0 = ax_lookup(F, key0);
         seeded = true;
         whole = len == (uint32_t)F.K;                     // the variants are leaves
-        if (WORK) ws += 1 + 3ull * F.K + (KMAX == 2 ? 9ull * F.K * (F.K - 1) / 2 : 0ull);
+        if (WORK) {
+          const uint64_t K = (uint64_t)F.K;
+          ws += 1 + 3 * K + (KMAX >= 2 ? 9 * K * (K - 1) / 2 : 0) + (KMAX >= 3 ? 27 * K * (K - 1) * (K - 2) / 6 : 0);
+        }
       }
       seeds[ti - t0] = iv0;
     }
-    // one substitution inside the K-mer: level 0 (k = 1) or 1 (k = 2)
-    uint64_t pm = seeded ? ax_present_from(F, key0, 0) : 0ull;
-    if (whole) { direct += ax_sizes(F, key0, 0, pm); pm = 0; }
-    {
-      uint2* q = KMAX == 2 ? z1 : z0;
-      unsigned long long at = warp_reserve(&ctl->n[KMAX == 2 ? 0 : 1], (uint32_t)__popcll(pm));
-      for (; pm; pm &= pm - 1) q[at++] = make_uint2((uint32_t)ti, ax_variant(key0, 0, __ffsll((long long)pm) - 1));
-    }
-    if (KMAX == 2) {                                      // two substitutions inside the K-mer: level 0
-      for (int t1 = 0; t1 < F.K; ++t1)
+    // variants at positions t0.. of `key` (one more substitution than key has) to level lvl
+    auto emit = [&](uint32_t key, int tfrom, int lvl) {
+      uint64_t pm = seeded ? ax_present_from(F, key, tfrom) : 0ull;
+      if (whole) { direct += ax_sizes(F, key, tfrom, pm); pm = 0; }
+      unsigned long long at = warp_reserve(&ctl->z[lvl], (uint32_t)__popcll(pm));
+      for (; pm; pm &= pm - 1) zq[lvl][at++] = make_uint2((uint32_t)ti, ax_variant(key, tfrom, __ffsll((long long)pm) - 1));
+    };
+    emit(key0, 0, KMAX - 1);                              // one substitution
+    if (KMAX >= 2) {
+      for (int a1 = 0; a1 < F.K; ++a1)
         for (uint32_t r1 = 1; r1 < 4; ++r1) {
-          const uint32_t k1 = kmer_subst(key0, t1, r1);
-          uint64_t pm2 = seeded ? ax_present_from(F, k1, t1 + 1) : 0ull;
-          if (whole) { direct += ax_sizes(F, k1, t1 + 1, pm2); pm2 = 0; }
-          unsigned long long at = warp_reserve(&ctl->n[1], (uint32_t)__popcll(pm2));
-          for (; pm2; pm2 &= pm2 - 1) z0[at++] = make_uint2((uint32_t)ti, ax_variant(k1, t1 + 1, __ffsll((long long)pm2) - 1));
+          const uint32_t k1 = kmer_subst(key0, a1, r1);
+          emit(k1, a1 + 1, KMAX - 2);                     // two substitutions
+          if (KMAX >= 3)
+            for (int a2 = a1 + 1; a2 < F.K; ++a2)
+              for (uint32_t r2 = 1; r2 < 4; ++r2) emit(kmer_subst(k1, a2, r2), a2 + 1, KMAX - 3);   // three
         }
     }
     if (valid) *ax_out<STRANDS>(out, out_rc, ti) = direct;
+  }
+  if (WORK && ws) { atomicAdd(work, (unsigned long long)ws); atomicAdd(work + 1, (unsigned long long)ws); }
+}
+
+// k = 3: the 9828 (K = 14) variant probes of a task are spread over K threads (task, first
+// substituted position a1), so that a chunk of ~18K tasks still fills the GPU; loop bounds are
+// warp-uniform (inactive positions emit nothing) so every lane reaches each warp_reserve.
+template <int STRANDS>
+__global__ void k_ax_zero(uint32_t* __restrict__ out, uint32_t* __restrict__ out_rc, uint64_t t0, uint64_t t1) {
+  for (uint64_t ti = t0 + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; ti < t1; ti += (uint64_t)gridDim.x * blockDim.x)
+    *ax_out<STRANDS>(out, out_rc, ti) = 0u;
+}
+template <bool FIXED, int STRANDS, bool WORK>
+__global__ void __launch_bounds__(256) k_ax_seed3(FmParams F, const uint8_t* __restrict__ pat,
+                                                  const uint64_t* __restrict__ offs, const uint32_t* __restrict__ lens,
+                                                  uint32_t fixed_len, uint32_t* __restrict__ out,
+                                                  uint32_t* __restrict__ out_rc, uint64_t t0, uint64_t t1,
+                                                  uint2* __restrict__ seeds, uint2* __restrict__ z0,
+                                                  uint2* __restrict__ z1, uint2* __restrict__ z2, AxCtl* ctl,
+                                                  unsigned long long* __restrict__ work) {
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint64_t K = (uint64_t)F.K, units = (t1 - t0) * K;
+  const uint64_t nthr = (uint64_t)gridDim.x * blockDim.x;
+  uint2* const zq[3] = {z0, z1, z2};
+  uint64_t ws = 0;
+  for (uint64_t w0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) & ~31ull; w0 < units; w0 += nthr) {
+    const uint64_t u = w0 + lane;
+    const bool valid = u < units;
+    const uint64_t ti = t0 + (valid ? u / K : 0);
+    const int a1 = valid ? (int)(u % K) : 0;
+    bool seeded = false, whole = false;
+    uint32_t key0 = 0, direct = 0;
+    if (valid) {
+      uint32_t len, rc;
+      const uint8_t* p = ax_pattern<FIXED, STRANDS>(pat, offs, lens, fixed_len, ti, len, rc);
+      if (len >= (uint32_t)K) {
+        PatWindow P;
+        P.reset(p);
+        key0 = rc ? kmer_key_rc(F.K, P, p, len) : kmer_key(F.K, P, p, len);
+        seeded = true;
+        whole = len == (uint32_t)K;
+      }
+      if (a1 == 0) {
+        seeds[ti - t0] = seeded ? ax_lookup(F, key0) : make_uint2(0u, (uint32_t)F.N);
+        if (WORK && seeded) ws += 1 + 3 * K + 9 * K * (K - 1) / 2 + 27 * K * (K - 1) * (K - 2) / 6;
+      }
+    }
+    auto emit = [&](bool act, uint32_t key, int tfrom, int lvl) {
+      uint64_t pm = (act && seeded) ? ax_present_from(F, key, tfrom) : 0ull;
+      if (whole) { direct += ax_sizes(F, key, tfrom, pm); pm = 0; }
+      unsigned long long at = warp_reserve(&ctl->z[lvl], (uint32_t)__popcll(pm));
+      for (; pm; pm &= pm - 1) zq[lvl][at++] = make_uint2((uint32_t)ti, ax_variant(key, tfrom, __ffsll((long long)pm) - 1));
+    };
+    emit(a1 == 0, key0, 0, 2);                            // one substitution (the task's a1 = 0 thread)
+    for (uint32_t r1 = 1; r1 < 4; ++r1) {
+      const uint32_t k1 = kmer_subst(key0, a1, r1);
+      emit(true, k1, a1 + 1, 1);                          // two: the first at a1
+      for (int a2 = 1; a2 < F.K; ++a2)
+        for (uint32_t r2 = 1; r2 < 4; ++r2) emit(a2 > a1, kmer_subst(k1, a2, r2), a2 + 1, 0);   // three
+    }
+    if (valid && direct) atomicAdd(ax_out<STRANDS>(out, out_rc, ti), direct);
   }
   if (WORK && ws) { atomicAdd(work, (unsigned long long)ws); atomicAdd(work + 1, (unsigned long long)ws); }
 }
@@ -1841,7 +1909,8 @@ __global__ void __launch_bounds__(256, QR_AX1_PATH_MINB) k_ax_path(FmParams F, c
           const uint64_t at = base + __popc(em & ((1u << c) - 1u));
           if (at < oq_cap) oq[at] = make_uint4((uint32_t)ti, (uint32_t)jc, bl[c], bh[c]);
           else if (CHILD == 0) total += fm_continue<BW, WORK>(F, P, (int64_t)jc - 1, bl[c], bh[c], wk);
-          else total += ax1_inline<BW, WORK>(F, P, (int64_t)jc - 1, bl[c], bh[c], wk);
+          else if (CHILD == 1) total += ax1_inline<BW, WORK>(F, P, (int64_t)jc - 1, bl[c], bh[c], wk);
+          // CHILD 2 (k = 3): the queue holds 3 (len - K) items per task, every child fits
         }
     }
     if (has && !(j >= 0 && lo < hi)) {                   // finished: the item's exact count + leaves
@@ -1957,6 +2026,9 @@ void fm_copy_locked(const qr_fm* src, qr_fm* dst) {
 extern int g_fm_kbits;
 extern int g_fm_ax_bfs;
 int g_fm_ax_bfs2 = 1;   // k = 2 breadth first too (knob fm_ax_bfs2)
+int g_fm_ax_bfs3 = 1;   // k = 3 breadth first in auto mode (L2-resident BWT, fixed-length batches; knob
+                        // fm_ax_bfs3): configs[3] 4.49 -> 6.90 M patterns/s, QuadRank16x2 5.25 -> 5.56 M
+                        // (profiles/r02_approx_bfs_k3_ab.txt; with one seed thread per task 3.61: too few threads)
 static qr_status fm_params_ax(const qr_fm* fmc, cudaStream_t st, FmParams& F) {
   qr_fm* fm = const_cast<qr_fm*>(fmc);                     // a lazily filled cache of the handle
   std::lock_guard<std::mutex> g(g_ax_mu);
@@ -2201,9 +2273,11 @@ static unsigned resident_grid(Kern k, int sms, size_t smem = 0) {
   return (unsigned)per_sm * (unsigned)sms;
 }
 
-// k = 1, 2 breadth first (k_ax_*), tasks in chunks so that the queues — the lookup items of the
-// seed variants (exactly 3K, and 9 C(K,2) at k = 2, per task at most) and the interval items of
-// the paths (~4 per task and level) — stay within the ~1.5 GB the pool keeps.
+// k = 1..3 breadth first (k_ax_*), tasks in chunks so that the queues stay within ~1.5 GB of the
+// stream-ordered pool: the lookup items of the seed variants (exactly 3K, 9 C(K,2), 27 C(K,3) per
+// task at most), the level-(k-1) interval items of the seed paths (k = 3: exactly 3 (len - K) per
+// task, fixed-length batches only) and ~4 interval items per task for the levels below, whose
+// overflow the emitting lane searches itself.
 uint64_t g_ax1_aq_per_task = 4;   // interval items per task and level (tests: 0 sends every one inline)
 template <bool FIXED, int STRANDS, bool WORK, int KMAX>
 static cudaError_t launch_ax_bfs(const qr_fm* fm, cudaStream_t st, const FmParams& F, const uint8_t* pat,
@@ -2211,53 +2285,72 @@ static cudaError_t launch_ax_bfs(const qr_fm* fm, cudaStream_t st, const FmParam
                                  uint32_t* out_rc, uint64_t m, unsigned long long* work) {
   const uint64_t ntask = m * STRANDS;
   const uint64_t K = F.K > 0 ? (uint64_t)F.K : 0;
-  const uint64_t z1_pt = KMAX == 2 ? 3 * K : 0, z0_pt = KMAX == 2 ? 9 * K * (K ? K - 1 : 0) / 2 : 3 * K;
-  const uint64_t q_pt = g_ax1_aq_per_task, nq = KMAX == 2 ? 2 : 1;
-  const uint64_t per_task = 8 + (z1_pt + z0_pt) * 8 + nq * q_pt * 16;
+  const uint64_t nsub[4] = {1, 3 * K, 9 * K * (K ? K - 1 : 0) / 2, 27 * K * (K > 1 ? K - 1 : 0) * (K > 2 ? K - 2 : 0) / 6};
+  uint64_t z_pt[3] = {0, 0, 0}, q_pt[3] = {0, 0, 0};
+  for (int lvl = 0; lvl < KMAX; ++lvl) {
+    z_pt[lvl] = nsub[KMAX - lvl];                         // level lvl holds the (KMAX - lvl)-substitution K-mers
+    q_pt[lvl] = g_ax1_aq_per_task;
+  }
+  if (KMAX == 3) q_pt[2] = 3ull * (fixed_len > K ? fixed_len - K : 0);   // exact: no inline k = 2 walk
+  uint64_t per_task = 8;
+  for (int lvl = 0; lvl < KMAX; ++lvl) per_task += z_pt[lvl] * 8 + q_pt[lvl] * 16;
   uint64_t chunk = (3ull << 29) / per_task;
-  chunk = chunk < 4096 ? 4096 : chunk;
+  chunk = chunk < 1024 ? 1024 : chunk;
   chunk = ntask < chunk ? ntask : chunk;
-  const uint64_t q_cap = chunk * q_pt;
-  const size_t off_z1 = 256 + chunk * 8, off_z0 = off_z1 + chunk * z1_pt * 8;
-  const size_t off_q1 = (off_z0 + chunk * z0_pt * 8 + 255) & ~(size_t)255, off_q0 = off_q1 + (KMAX == 2 ? q_cap * 16 : 0);
-  const size_t bytes = off_q0 + q_cap * 16 + 16;
+  size_t off = 256 + chunk * 8;
+  size_t z_off[3] = {0, 0, 0}, q_off[3] = {0, 0, 0};
+  for (int lvl = 0; lvl < KMAX; ++lvl) { z_off[lvl] = off; off += chunk * z_pt[lvl] * 8; }
+  off = (off + 255) & ~(size_t)255;                       // uint4 items: 16-B aligned
+  for (int lvl = 0; lvl < KMAX; ++lvl) { q_off[lvl] = off; off += chunk * q_pt[lvl] * 16; }
   keep_pool_memory(fm->bwt->device, st);
   unsigned char* buf = nullptr;
-  cudaError_t e = cudaMallocAsync((void**)&buf, bytes, st);
+  cudaError_t e = cudaMallocAsync((void**)&buf, off + 16, st);
   if (e) return e;
   AxCtl* ctl = reinterpret_cast<AxCtl*>(buf);
   uint2* seeds = reinterpret_cast<uint2*>(buf + 256);
-  uint2* z1 = reinterpret_cast<uint2*>(buf + off_z1);
-  uint2* z0 = reinterpret_cast<uint2*>(buf + off_z0);
-  uint4* q1 = reinterpret_cast<uint4*>(buf + off_q1);
-  uint4* q0 = reinterpret_cast<uint4*>(buf + off_q0);
+  uint2* z[3];
+  uint4* q[3];
+  for (int lvl = 0; lvl < 3; ++lvl) {
+    z[lvl] = reinterpret_cast<uint2*>(buf + z_off[lvl]);
+    q[lvl] = reinterpret_cast<uint4*>(buf + q_off[lvl]);
+  }
   const int sms = fm->bwt->sm_count;
 #define QR_AX_K(KERN, ...) (F.bw ? KERN<FIXED, 1, STRANDS, WORK, __VA_ARGS__> : KERN<FIXED, 0, STRANDS, WORK, __VA_ARGS__>)
-  auto kp0 = QR_AX_K(k_ax_path, 0, KMAX - 1);
-  auto kp1 = QR_AX_K(k_ax_path, 1, 0);
-  auto kp2 = QR_AX_K(k_ax_path, 2, 0);
+  auto kp_seed = QR_AX_K(k_ax_path, 0, (KMAX > 1 ? KMAX - 1 : 0));
+  auto kp_z1 = QR_AX_K(k_ax_path, 1, 0);
+  auto kp_q1 = QR_AX_K(k_ax_path, 2, 0);
+  auto kp_z2 = QR_AX_K(k_ax_path, 1, 1);
+  auto kp_q2 = QR_AX_K(k_ax_path, 2, 1);
   auto kcz = QR_AX_K(k_ax_cont, true);
   auto kcq = QR_AX_K(k_ax_cont, false);
 #undef QR_AX_K
-  const unsigned gp = resident_grid(kp0, sms), gc = resident_grid(kcz, sms);
+  const unsigned gp = resident_grid(kp_seed, sms), gc = resident_grid(kcz, sms);
   for (uint64_t t0 = 0; t0 < ntask && !e; t0 += chunk) {
     const uint64_t t1 = t0 + chunk < ntask ? t0 + chunk : ntask, nt = t1 - t0;
     if ((e = cudaMemsetAsync(ctl, 0, sizeof(AxCtl), st))) break;
-    k_ax_seed<FIXED, STRANDS, KMAX, WORK><<<grid_stride_blocks(nt, 256, sms, 8), 256, 0, st>>>(
-        F, pat, offs, lens, fixed_len, out, out_rc, t0, t1, seeds, z1, z0, ctl, work);
-    if (KMAX == 2) {
-      kp0<<<gp, 256, 0, st>>>(F, pat, offs, lens, fixed_len, out, out_rc, t0, t1, seeds, nullptr, nullptr, 0, q1,
-                              &ctl->n[2], q_cap, &ctl->ctr[0], work);
-      kp1<<<gp, 256, 0, st>>>(F, pat, offs, lens, fixed_len, out, out_rc, t0, t1, nullptr, z1, &ctl->n[0],
-                              nt * z1_pt, q0, &ctl->n[3], q_cap, &ctl->ctr[1], work);
-      kp2<<<gp, 256, 0, st>>>(F, pat, offs, lens, fixed_len, out, out_rc, t0, t1, nullptr, q1, &ctl->n[2], q_cap,
-                              q0, &ctl->n[3], q_cap, &ctl->ctr[2], work);
+    if (KMAX == 3) {
+      k_ax_zero<STRANDS><<<grid_stride_blocks(nt, 256, sms, 8), 256, 0, st>>>(out, out_rc, t0, t1);
+      k_ax_seed3<FIXED, STRANDS, WORK><<<grid_stride_blocks(nt * K, 256, sms, 8), 256, 0, st>>>(
+          F, pat, offs, lens, fixed_len, out, out_rc, t0, t1, seeds, z[0], z[1], z[2], ctl, work);
     } else {
-      kp0<<<gp, 256, 0, st>>>(F, pat, offs, lens, fixed_len, out, out_rc, t0, t1, seeds, nullptr, nullptr, 0, q0,
-                              &ctl->n[3], q_cap, &ctl->ctr[0], work);
+      k_ax_seed<FIXED, STRANDS, KMAX, WORK><<<grid_stride_blocks(nt, 256, sms, 8), 256, 0, st>>>(
+          F, pat, offs, lens, fixed_len, out, out_rc, t0, t1, seeds, z[0], z[1], z[2], ctl, work);
     }
-    kcz<<<gc, 256, 0, st>>>(F, pat, offs, lens, fixed_len, out, out_rc, z0, &ctl->n[1], nt * z0_pt, &ctl->ctr[3], work);
-    kcq<<<gc, 256, 0, st>>>(F, pat, offs, lens, fixed_len, out, out_rc, q0, &ctl->n[3], q_cap, &ctl->ctr[4], work);
+    // the seed paths (level KMAX), then each level's lookup and interval items down to level 1
+    kp_seed<<<gp, 256, 0, st>>>(F, pat, offs, lens, fixed_len, out, out_rc, t0, t1, seeds, nullptr, nullptr, 0,
+                                q[KMAX - 1], &ctl->q[KMAX - 1], nt * q_pt[KMAX - 1], &ctl->ctr[0], work);
+    for (int lvl = KMAX - 1; lvl >= 1; --lvl) {
+      auto kz = lvl == 2 ? kp_z2 : kp_z1;
+      auto kq = lvl == 2 ? kp_q2 : kp_q1;
+      kz<<<gp, 256, 0, st>>>(F, pat, offs, lens, fixed_len, out, out_rc, t0, t1, nullptr, z[lvl], &ctl->z[lvl],
+                             nt * z_pt[lvl], q[lvl - 1], &ctl->q[lvl - 1], nt * q_pt[lvl - 1], &ctl->ctr[2 * lvl],
+                             work);
+      kq<<<gp, 256, 0, st>>>(F, pat, offs, lens, fixed_len, out, out_rc, t0, t1, nullptr, q[lvl], &ctl->q[lvl],
+                             nt * q_pt[lvl], q[lvl - 1], &ctl->q[lvl - 1], nt * q_pt[lvl - 1],
+                             &ctl->ctr[2 * lvl + 1], work);
+    }
+    kcz<<<gc, 256, 0, st>>>(F, pat, offs, lens, fixed_len, out, out_rc, z[0], &ctl->z[0], nt * z_pt[0], &ctl->ctr[7], work);
+    kcq<<<gc, 256, 0, st>>>(F, pat, offs, lens, fixed_len, out, out_rc, q[0], &ctl->q[0], nt * q_pt[0], &ctl->ctr[8], work);
     e = cudaGetLastError();
   }
   cudaError_t e2 = cudaFreeAsync(buf, st);
@@ -2268,16 +2361,19 @@ template <bool FIXED, int STRANDS, bool WORK>
 static cudaError_t launch_approx_s(const qr_fm* fm, unsigned g, cudaStream_t st, const FmParams& F, const uint8_t* pat,
                                    const uint64_t* offs, const uint32_t* lens, uint32_t fixed_len, uint32_t* out,
                                    uint32_t* out_rc, uint64_t m, int kmax, unsigned long long* work) {
-  // breadth first (auto, profiles/r02_approx_bfs_k2_ab.txt): k = 1 everywhere but on an
-  // L2-resident QuadRank16x2 BWT (150-bp reads 52.8 -> 103 M reads/s, configs[3] 1.31 -> 1.48 G;
-  // QuadRank16x2 configs[3] 1.68 recursive vs 1.50); k = 2 on L2-resident BWTs (configs[3] 69.9
-  // -> 88.3 M, QuadRank16x2 91.0 -> 93.2 M; the reads, HBM-resident, 6.98 recursive vs 6.11)
+  // breadth first (auto, profiles/r02_approx_bfs_k2_ab.txt, r02_approx_bfs_k3_ab.txt): k = 1
+  // everywhere but on an L2-resident QuadRank16x2 BWT (150-bp reads 52.8 -> 103 M reads/s,
+  // configs[3] 1.31 -> 1.48 G; QuadRank16x2 configs[3] 1.68 recursive vs 1.50); k = 2, 3 on
+  // L2-resident BWTs (configs[3] k = 2 69.9 -> 88.3 M, k = 3 4.49 -> 6.90 M; QuadRank16x2 91.0 ->
+  // 93.2 M, 5.25 -> 5.56 M; the reads, HBM-resident, k = 2 6.98 recursive vs 6.11)
   const bool l2 = bwt_l2_resident(fm);
   const bool bfs = g_fm_ax_bfs == 2 ||
-                   (g_fm_ax_bfs == 1 && (kmax == 1 ? !(F.bw == 1 && l2) : (kmax == 2 && l2 && g_fm_ax_bfs2)));
+                   (g_fm_ax_bfs == 1 && (kmax == 1 ? !(F.bw == 1 && l2) : l2 && (kmax == 2 ? g_fm_ax_bfs2 : g_fm_ax_bfs3)));
   if (bfs && g_fm_dyn && m * STRANDS < (1ull << 32)) {
     if (kmax == 1) return launch_ax_bfs<FIXED, STRANDS, WORK, 1>(fm, st, F, pat, offs, lens, fixed_len, out, out_rc, m, work);
     if (kmax == 2) return launch_ax_bfs<FIXED, STRANDS, WORK, 2>(fm, st, F, pat, offs, lens, fixed_len, out, out_rc, m, work);
+    if (kmax == 3 && FIXED && F.K > 0 && (g_fm_ax_bfs == 2 || g_fm_ax_bfs3))
+      return launch_ax_bfs<FIXED, STRANDS, WORK, 3>(fm, st, F, pat, offs, lens, fixed_len, out, out_rc, m, work);
   }
   auto kern = kmax == 1 ? (F.bw ? k_fm_approx1<FIXED, 1, STRANDS, WORK> : k_fm_approx1<FIXED, 0, STRANDS, WORK>)
             : kmax == 2 ? (F.bw ? k_fm_approxk<FIXED, 1, 2, STRANDS, WORK> : k_fm_approxk<FIXED, 0, 2, STRANDS, WORK>)

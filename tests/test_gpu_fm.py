@@ -992,3 +992,40 @@ def test_fm_approx_breadth_first_queues(cuda, bwt_layout, queue, bfs, kbits, kma
         qr.qr_set_tuning("fm_kbits", 0)
     assert np.array_equal(to_host(df).view(np.uint32), ref)
     assert np.array_equal(to_host(dr).view(np.uint32), ref_rc)
+
+
+@pytest.mark.parametrize("bwt_layout", [None, qr.QR_LAYOUT_QUADRANK16X2])
+@pytest.mark.parametrize("L", [10, 24, 33])
+@pytest.mark.parametrize("queue", [0, 4])
+def test_fm_approx3_breadth_first_fixed_length(cuda, bwt_layout, L, queue, fm_dyn_reset):
+    """k = 3 breadth first (fixed-length batches: the level-2 queue holds 3 (L - K) items per
+    task) against the recursive kernel and the oracle's Hamming scan, both strands; L = 10 is the
+    table width (every variant a leaf), with the level-1 and level-0 queues sized 0 and 4."""
+    torch = _torch()
+    n = 200_003
+    w = gen.dna(403, n, 0)
+    sym = gen.unpack_dna(w, n)
+    fm = qr.qr_fm_build(w, n, kmer_k=10, bwt_layout=bwt_layout)
+    m = 600
+    pats = gen.patterns(11, 1, m, L, w, n)              # substrings with 0-2 substitutions
+    offs = np.arange(m, dtype=np.uint64) * L
+    lens = np.full(m, L, np.uint32)
+    ref = oracle.scan_count_hdk(sym, pats, offs, lens, 3)
+    rc = np.concatenate([revcomp(pats[i * L:(i + 1) * L]) for i in range(m)])
+    ref_rc = oracle.scan_count_hdk(sym, rc, offs, lens, 3)
+    got = {}
+    try:
+        qr.qr_set_tuning("fm_ax_queue", queue)
+        for bfs in (0, 2):
+            qr.qr_set_tuning("fm_ax_bfs", bfs)
+            df = torch.empty(m, dtype=torch.int32, device=cuda)
+            dr = torch.empty(m, dtype=torch.int32, device=cuda)
+            qr.qr_fm_count_approx_both(fm, to_dev(pats, cuda), None, L, 3, df, dr, m)
+            torch.cuda.synchronize()
+            got[bfs] = (to_host(df).view(np.uint32), to_host(dr).view(np.uint32))
+    finally:
+        qr.qr_set_tuning("fm_ax_bfs", 1)
+        qr.qr_set_tuning("fm_ax_queue", 4)
+    for bfs in (0, 2):
+        assert np.array_equal(got[bfs][0], ref), bfs
+        assert np.array_equal(got[bfs][1], ref_rc), bfs
