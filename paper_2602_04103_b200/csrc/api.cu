@@ -29,7 +29,7 @@ int g_fm_smem = 1;              // FM superblock words from shared memory: 0 off
 int g_fm_refill = 0;            // L2-resident count kernel: refill a warp's lanes once this many are idle (0 auto)
 int g_fm_packed = 1;            // L2-resident count kernel: packed post-seed symbols for short fixed-length batches
 extern uint64_t g_ax1_aq_per_task;   // fm.cu
-extern int g_fm_ax_bfs2, g_fm_ax_bfs3;   // fm.cu
+extern int g_fm_ax_bfs2, g_fm_ax_bfs3, g_ax_seed_split;   // fm.cu
 int g_fm_ax_bfs = 1;            // approximate search k = 1: breadth-first kernels (k_ax1_*): 0 never, 1 auto, 2 always
 int g_fm_kbits = 0;             // approximate search: presence bitmap of the k-mer table, 0 auto (sparse table), 1 never, 2 always
 int g_check_range = 0;          // 1: qr_rank / qr_rank_all4 count q > n and return QR_ERANGE (synchronous)
@@ -427,6 +427,9 @@ QR_EXPORT qr_status qr_set_tuning(const char* key, int64_t value) {
   } else if (!strcmp(key, "fm_ax_bfs3")) {
     if (value != 0 && value != 1) return fail(QR_EINVAL, "fm_ax_bfs3 must be 0 or 1");
     g_fm_ax_bfs3 = (int)value;
+  } else if (!strcmp(key, "fm_ax_seed_split")) {
+    if (value != 0 && value != 1) return fail(QR_EINVAL, "fm_ax_seed_split must be 0 or 1");
+    g_ax_seed_split = (int)value;
   } else if (!strcmp(key, "fm_ax_queue")) {
     if (value < 0 || value > 64) return fail(QR_EINVAL, "fm_ax_queue must be 0..64 (interval items per task)");
     g_ax1_aq_per_task = (uint64_t)value;

@@ -1693,7 +1693,7 @@ __global__ void k_ax_zero(uint32_t* __restrict__ out, uint32_t* __restrict__ out
   for (uint64_t ti = t0 + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; ti < t1; ti += (uint64_t)gridDim.x * blockDim.x)
     *ax_out<STRANDS>(out, out_rc, ti) = 0u;
 }
-template <bool FIXED, int STRANDS, bool WORK>
+template <bool FIXED, int STRANDS, int KMAX, bool WORK>
 __global__ void __launch_bounds__(256) k_ax_seed3(FmParams F, const uint8_t* __restrict__ pat,
                                                   const uint64_t* __restrict__ offs, const uint32_t* __restrict__ lens,
                                                   uint32_t fixed_len, uint32_t* __restrict__ out,
@@ -1725,7 +1725,7 @@ __global__ void __launch_bounds__(256) k_ax_seed3(FmParams F, const uint8_t* __r
       }
       if (a1 == 0) {
         seeds[ti - t0] = seeded ? ax_lookup(F, key0) : make_uint2(0u, (uint32_t)F.N);
-        if (WORK && seeded) ws += 1 + 3 * K + 9 * K * (K - 1) / 2 + 27 * K * (K - 1) * (K - 2) / 6;
+        if (WORK && seeded) ws += 1 + 3 * K + 9 * K * (K - 1) / 2 + (KMAX == 3 ? 27 * K * (K - 1) * (K - 2) / 6 : 0);
       }
     }
     auto emit = [&](bool act, uint32_t key, int tfrom, int lvl) {
@@ -1734,12 +1734,13 @@ __global__ void __launch_bounds__(256) k_ax_seed3(FmParams F, const uint8_t* __r
       unsigned long long at = warp_reserve(&ctl->z[lvl], (uint32_t)__popcll(pm));
       for (; pm; pm &= pm - 1) zq[lvl][at++] = make_uint2((uint32_t)ti, ax_variant(key, tfrom, __ffsll((long long)pm) - 1));
     };
-    emit(a1 == 0, key0, 0, 2);                            // one substitution (the task's a1 = 0 thread)
+    emit(a1 == 0, key0, 0, KMAX - 1);                     // one substitution (the task's a1 = 0 thread)
     for (uint32_t r1 = 1; r1 < 4; ++r1) {
       const uint32_t k1 = kmer_subst(key0, a1, r1);
-      emit(true, k1, a1 + 1, 1);                          // two: the first at a1
-      for (int a2 = 1; a2 < F.K; ++a2)
-        for (uint32_t r2 = 1; r2 < 4; ++r2) emit(a2 > a1, kmer_subst(k1, a2, r2), a2 + 1, 0);   // three
+      emit(true, k1, a1 + 1, KMAX - 2);                   // two: the first at a1
+      if (KMAX == 3)
+        for (int a2 = 1; a2 < F.K; ++a2)
+          for (uint32_t r2 = 1; r2 < 4; ++r2) emit(a2 > a1, kmer_subst(k1, a2, r2), a2 + 1, 0);   // three
     }
     if (valid && direct) atomicAdd(ax_out<STRANDS>(out, out_rc, ti), direct);
   }
@@ -2278,6 +2279,7 @@ static unsigned resident_grid(Kern k, int sms, size_t smem = 0) {
 // task at most), the level-(k-1) interval items of the seed paths (k = 3: exactly 3 (len - K) per
 // task, fixed-length batches only) and ~4 interval items per task for the levels below, whose
 // overflow the emitting lane searches itself.
+int g_ax_seed_split = 1;          // k = 2: seed variants over (task, a1) threads (knob fm_ax_seed_split)
 uint64_t g_ax1_aq_per_task = 4;   // interval items per task and level (tests: 0 sends every one inline)
 template <bool FIXED, int STRANDS, bool WORK, int KMAX>
 static cudaError_t launch_ax_bfs(const qr_fm* fm, cudaStream_t st, const FmParams& F, const uint8_t* pat,
@@ -2328,9 +2330,9 @@ static cudaError_t launch_ax_bfs(const qr_fm* fm, cudaStream_t st, const FmParam
   for (uint64_t t0 = 0; t0 < ntask && !e; t0 += chunk) {
     const uint64_t t1 = t0 + chunk < ntask ? t0 + chunk : ntask, nt = t1 - t0;
     if ((e = cudaMemsetAsync(ctl, 0, sizeof(AxCtl), st))) break;
-    if (KMAX == 3) {
+    if (KMAX == 3 || (KMAX == 2 && g_ax_seed_split && K > 0)) {
       k_ax_zero<STRANDS><<<grid_stride_blocks(nt, 256, sms, 8), 256, 0, st>>>(out, out_rc, t0, t1);
-      k_ax_seed3<FIXED, STRANDS, WORK><<<grid_stride_blocks(nt * K, 256, sms, 8), 256, 0, st>>>(
+      k_ax_seed3<FIXED, STRANDS, (KMAX == 3 ? 3 : 2), WORK><<<grid_stride_blocks(nt * K, 256, sms, 8), 256, 0, st>>>(
           F, pat, offs, lens, fixed_len, out, out_rc, t0, t1, seeds, z[0], z[1], z[2], ctl, work);
     } else {
       k_ax_seed<FIXED, STRANDS, KMAX, WORK><<<grid_stride_blocks(nt, 256, sms, 8), 256, 0, st>>>(
