@@ -1932,8 +1932,11 @@ __global__ void __launch_bounds__(256, QR_AX1_PATH_MINB) k_ax_path(FmParams F, c
 // (task, key) of k_ax_seed, the interval read from the table at refill (resolving them in
 // k_ax_seed instead measured 1.35x slower on configs[3] at k = 1: its lanes then walk 3K
 // dependent lookups, and the queue doubles); else (task, pos, lo, hi) of k_ax_path.
+#ifndef QR_AX_CONT_MINB
+#define QR_AX_CONT_MINB QR_APPROX1_MINB
+#endif
 template <bool FIXED, int BW, int STRANDS, bool WORK, bool LOOKUP>
-__global__ void __launch_bounds__(256, QR_APPROX1_MINB) k_ax_cont(FmParams F, const uint8_t* __restrict__ pat,
+__global__ void __launch_bounds__(256, QR_AX_CONT_MINB) k_ax_cont(FmParams F, const uint8_t* __restrict__ pat,
                                                     const uint64_t* __restrict__ offs,
                                                     const uint32_t* __restrict__ lens, uint32_t fixed_len,
                                                     uint32_t* __restrict__ out, uint32_t* __restrict__ out_rc,

@@ -734,7 +734,8 @@ def test_fm_count_work_ex_accounting(cuda, bwt_layout):
     calls'; exact one strand equals qr_fm_count_work and the oracle's post-seed steps / lines;
     both strands = forward + the reverse complements counted alone; approximate search counts at
     least the exact path's work and more lines than rank pairs; the counters do not depend on the
-    work order (static / dynamic)."""
+    work order (static / dynamic) — nor on the search order (breadth first, k = 1-3, or the
+    recursive kernels)."""
     torch = _torch()
     n = 60000
     w = gen.dna(401, n, 1)
@@ -764,9 +765,9 @@ def test_fm_count_work_ex_accounting(cuda, bwt_layout):
     (sb, lb), cbf, cbr = work_of(fx, 0, True)
     assert (sb, lb) == (s1 + sr, l1 + lr)
     assert np.array_equal(cbf, c1) and np.array_equal(cbr, cr)
-    for kmax in (1, 2):
-        (sa, la), ca, car = work_of(fx, kmax, True)
-        (sd, ld), _, _ = work_of(fx, kmax, True, dyn=0)
+    for kmax in (1, 2, 3):
+        (sa, la), ca, car = work_of(fx, kmax, True)        # breadth first (dynamic order) ...
+        (sd, ld), _, _ = work_of(fx, kmax, True, dyn=0)    # ... and the recursive kernels count alike
         assert (sa, la) == (sd, ld)
         assert sa >= s1 + sr and la >= sa
         assert np.array_equal(ca, oracle.scan_count_hdk(sym, fx, offs, lens, kmax))
